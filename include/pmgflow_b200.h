@@ -1,0 +1,166 @@
+/*
+ * pmgflow_b200.h -- C ABI of the B200-native (sm_100a, FP64) JFNK-pMG hot
+ * path.  Plain pointers and sizes only; no torch / CUDA C++ types.
+ *
+ * The reference (pmgflow, pure Python/NumPy) has no FFI; its seams are
+ * duck-typed Python callables.  Each entry point below
+ * replaces one of those call sites; the ctypes binding a maintainer adds
+ * is shown in INTEGRATION.md and lives in paper_2202_09733_b200/_lib.py.
+ *
+ * Conventions
+ *  - Vectors are caller-owned DEVICE buffers (FP64, contiguous) in the
+ *    reference layout: element e occupies [e*sz, (e+1)*sz), shaped
+ *    (n, n, nvars) C-order, first index along eta (spatial.py:209-215).
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default).
+ *    Calls are asynchronous on that stream except the pmgb_status* and
+ *    pmgb_sync calls.  One stream per discretization; not re-entrant.
+ *  - Return value: 0 ok; > 0 a cudaError_t; < 0 a library error
+ *    (see pmgb_error_string).
+ *  - Non-physical states (rho <= 0 or p <= 0 at points, then traces,
+ *    spatial.py:439-446, 506-510) do not abort the enqueued work; the
+ *    first one seen is latched in a device status word and read back
+ *    by pmgb_status (kind 1 = state, 2 = trace, with the smallest
+ *    offending element of that residual evaluation).  Kind 3 = singular
+ *    element-Jacobi block (newton_krylov.py:202-208).
+ */
+#ifndef PMGFLOW_B200_H
+#define PMGFLOW_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PMGB_API __attribute__((visibility("default")))
+
+typedef struct pmgb_disc pmgb_disc;
+
+/* Discretization setup: replaces Discretization.__init__
+ * (spatial.py:298-359) + element_geometry (mesh.py:322-395); uniform
+ * degree 0..5.  All pointers are HOST arrays, copied to the device. */
+typedef struct pmgb_disc_desc {
+  int64_t n_elem;
+  int32_t degree;             /* p; n = p + 1 points per direction       */
+  int32_t kind;               /* 0 euler, 1 navier-stokes, 2 adv-diff    */
+  double gamma, mu, kappa;    /* EquationSpec.gamma / .mu / .heat_cond.  */
+  double adv_x, adv_y, diffusivity;
+  const double* free_stream;  /* (nvars) EquationSpec.free_stream()      */
+  const double* D;            /* (n, n) D[k][i] = l_i'(x_k)              */
+  const double* eL;           /* (n) basis at xi = -1                    */
+  const double* eR;           /* (n) basis at xi = +1                    */
+  const double* lL;           /* (n) eL / w                              */
+  const double* lR;           /* (n) eR / w                              */
+  const double* xg;           /* (n) Gauss points                        */
+  const double* geom;         /* (M, 20) see mesh.pack_geometry          */
+  const int64_t* links;       /* (M, 4, 4) nb elem|-1, nb face, rev, is_left */
+  const int32_t* tags;        /* (M, 4) boundary tag code, -1 interior    */
+} pmgb_disc_desc;
+
+PMGB_API int pmgb_disc_create(const pmgb_disc_desc* desc, pmgb_disc** out);
+PMGB_API int pmgb_disc_destroy(pmgb_disc* d);
+PMGB_API int64_t pmgb_disc_n_dofs(const pmgb_disc* d);
+
+/* R(q) -- replaces Discretization.residual (spatial.py:501-570). */
+PMGB_API int pmgb_residual(pmgb_disc* d, const double* q, double* R, void* stream);
+
+/* Fused residual evaluation with prologue q + eps*X (X may be NULL) and
+ * an epilogue; replaces the vector algebra wrapped around residual()
+ * at newton_krylov.py:71-76 (jfnk_matvec), :402-405 (PTC matvec),
+ * time_integration.py:138-141 (stage_function), pmg.py:152-159
+ * (LevelState.F / defect) and pmg.py:325-326 (pmg_solve outer F). */
+enum {
+  PMGB_EPI_R = 0,        /* out = R                                   */
+  PMGB_EPI_F = 1,        /* out = s q - R                             */
+  PMGB_EPI_DEFECT = 2,   /* out = (Sb - (s q - R)) + Se               */
+  PMGB_EPI_JV = 3,       /* out = s X - (R(q + eps X) - R0) / eps     */
+  PMGB_EPI_STAGE_F = 4,  /* out = (q - E) / adt - R                   */
+  PMGB_EPI_STAGE_JV = 5, /* out = X/dtau + (F(q + eps X) - R0) / eps  */
+  PMGB_EPI_NEG_R = 6,    /* out = -R                                  */
+  PMGB_EPI_OUTER_F = 7   /* out = (s q - R) - Se                      */
+};
+typedef struct pmgb_epilogue {
+  int32_t mode;
+  int32_t pad;
+  double s, eps, adt, dtau, sb_scalar, se_scalar;
+  const double* X;   /* device; JV modes           */
+  const double* R0;  /* device; R0 (JV) / Fk (STAGE_JV) */
+  const double* E;   /* device; explicit stage part */
+  const double* Sb;  /* device or NULL -> sb_scalar */
+  const double* Se;  /* device or NULL -> se_scalar */
+} pmgb_epilogue;
+PMGB_API int pmgb_eval(pmgb_disc* d, const double* q, const double* X, double eps,
+                       const pmgb_epilogue* epi, double* out, void* stream);
+
+/* (shift I - dR/dq) X ~ shift X - (R(q+eps X) - R0)/eps
+ * -- newton_krylov.py:71-76. */
+PMGB_API int pmgb_jfnk_matvec(pmgb_disc* d, const double* X, const double* q, const double* R0,
+                              double shift, double eps, double* out, void* stream);
+
+/* freeze (spatial.py:700-766): face traces qtr (M,4,n,nv) and one-sided
+ * viscous normal fluxes fvn (M,4,n,nv) of state q; every frozen record of
+ * the reference is a gather from these two arrays. fvn unused (may be
+ * NULL) for inviscid kinds. */
+PMGB_API int pmgb_freeze(pmgb_disc* d, const double* q, double* qtr, double* fvn, void* stream);
+
+/* element_residual (spatial.py:768-853) for B instances (elems[b], Q[b]),
+ * neighbours frozen at (qtr, fvn).  elems: device int64 (B). */
+PMGB_API int pmgb_element_residual(pmgb_disc* d, const int64_t* elems, int64_t B, const double* Q,
+                                   const double* qtr, const double* fvn, double* out, void* stream);
+
+/* assemble_element_blocks (newton_krylov.py:157-210): FD blocks of
+ * shift I - dR_e/dq_e (eps perturbations of the frozen element-local
+ * residual) stored column-major per element in blocksT (M, sz, sz), and
+ * their inverses (column-major) in invT.  blocksT may equal invT
+ * (in-place inverse).  Singular blocks latch status kind 3. */
+PMGB_API int pmgb_blocks_assemble(pmgb_disc* d, const double* q, double shift, double eps,
+                                  double* blocksT, double* invT, void* stream);
+PMGB_API int pmgb_blocks_invert(int64_t n_elem, int32_t sz, const double* blocksT, double* invT,
+                                void* stream);
+
+/* BlockJacobian.apply / ej_apply (newton_krylov.py:166-171, 213-214):
+ * y_e = B_e^-1 x_e.  pmgb_ej_update: out = base + omega * B^-1 d
+ * (smooth_ej, pmg.py:162-164); out may alias base. */
+PMGB_API int pmgb_ej_apply(int64_t n_elem, int32_t sz, const double* invT, const double* x, double* y,
+                           void* stream);
+PMGB_API int pmgb_ej_update(int64_t n_elem, int32_t sz, const double* invT, const double* d, double omega,
+                            const double* base, double* out, void* stream);
+
+/* pMG transfers (pmg.py:117-136).  T is a HOST (n_out x n_in) matrix:
+ * Gamma for restriction, Pi for prolongation.
+ *   pmgb_transfer:     dst = (T (x) T) (src - src_base)   [src_base may be NULL]
+ *   accumulate != 0:   dst += ...                          (prolong + add) */
+PMGB_API int pmgb_transfer(int64_t n_elem, int32_t nvars, int32_t n_in, int32_t n_out, const double* T,
+                           const double* src, const double* src_base, double* dst, int32_t accumulate,
+                           void* stream);
+
+/* Deterministic reductions and Arnoldi (newton_krylov.py:79-151). */
+PMGB_API int pmgb_dot(int64_t n, const double* x, const double* y, double* result_dev, void* stream);
+PMGB_API int pmgb_nrm2(int64_t n, const double* x, double* result_dev, void* stream);
+/* MGS of w against rows 0..j of V (row stride ld): H_dev[0..j+1] gets
+ * column j of the Hessenberg matrix, V[j+1] = w / H[j+1] when
+ * H[j+1] > thresh, *finite_dev = 1 if w entered with a non-finite. */
+PMGB_API int pmgb_mgs(int64_t n, double* V, int64_t ld, int32_t j, double* w, double* H_dev, double thresh,
+                      int32_t* finite_dev, void* stream);
+/* out = sum_i c[i] x[i], k <= 8, c and the pointer array on the HOST. */
+PMGB_API int pmgb_lincomb(int64_t n, int32_t k, const double* c, const double* const* xs, double* out,
+                          void* stream);
+/* out = V[0:k]^T y, y on the device (k <= 128). */
+PMGB_API int pmgb_gemv_t(int64_t n, int32_t k, const double* V, int64_t ld, const double* y_dev, double* out,
+                         void* stream);
+/* *flag_dev = any(x != 0) */
+PMGB_API int pmgb_any_nonzero(int64_t n, const double* x, int32_t* flag_dev, void* stream);
+
+/* Status word (non-physical / singular), synchronising. */
+PMGB_API int pmgb_status(void* stream, int32_t* kind, int64_t* element, int32_t clear);
+PMGB_API int pmgb_status_clear(void* stream);
+PMGB_API int pmgb_sync(void* stream);
+PMGB_API const char* pmgb_error_string(int code);
+/* Build/version tag and a count of kernel launches issued (diagnostics). */
+PMGB_API const char* pmgb_version(void);
+PMGB_API int64_t pmgb_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PMGFLOW_B200_H */

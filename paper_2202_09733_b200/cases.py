@@ -1,0 +1,174 @@
+"""BASELINE.json configurations mapped onto the reference's features.
+
+SURVEY.md 8.0 pins each config to what the reference actually has:
+Roe + BR1 (not Rusanov/LDG), esdirk2 as the ESDIRK3 stand-in, row4 as
+the "4-stage ROW", EJ smoothers on every level + pmg.smoother_shift,
+wall-adiabatic for the isothermal wall, a geometric wall-normal ratio
+that actually fills [0, 1] for config 4, and dt from
+dt_conv = h_min / ((2p+1) max(|u| + c)).  Inputs are analytic and
+seeded; the same NumPy array feeds the oracle and the device.
+
+Initial-condition builders follow harness.isentropic_vortex
+(/root/reference/pkg/src/pmgflow/harness.py:499-517).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .equation import EquationSpec
+from .mesh import Mesh, generate_box, generate_channel, solution_point_coords
+
+
+def isentropic_vortex(eqn: EquationSpec, t: float = 0.0, L: float = 10.0, beta: float = 5.0):
+    """Vortex on the free stream (1, 1, 0) of a periodic [0, L]^2 box.
+
+    Same closed form as harness.isentropic_vortex (harness.py:499-517),
+    including its periodic wrap xc = mod(x - t - L/2, L) - L/2, which
+    puts the core on the x = 0 seam at y = L/2."""
+    g = eqn.gamma
+    Tinf = 1.0 / (g * eqn.mach ** 2)
+
+    def fn(x, y):
+        xc = np.mod(x - 1.0 * t - L / 2, L) - L / 2
+        yc = y - L / 2
+        r2 = xc * xc + yc * yc
+        e = np.exp(0.5 * (1.0 - r2))
+        u = 1.0 - beta / (2 * np.pi) * e * yc
+        v = beta / (2 * np.pi) * e * xc
+        T = Tinf - (g - 1.0) * beta ** 2 / (8.0 * g * np.pi ** 2) * np.exp(1 - r2)
+        rho = (T / Tinf) ** (1.0 / (g - 1.0))
+        p = rho * T
+        E = p / (g - 1.0) + 0.5 * rho * (u * u + v * v)
+        return np.stack([rho, rho * u, rho * v, E], axis=-1)
+    return fn
+
+
+def explicit_dt(mesh: Mesh, p: int, eqn: EquationSpec, q: np.ndarray) -> float:
+    """dt_conv = h_min / ((2p+1) max(|u| + c)) on the state q."""
+    Q = q.reshape(-1, 4)
+    rho = Q[:, 0]
+    u, v = Q[:, 1] / rho, Q[:, 2] / rho
+    pr = (eqn.gamma - 1.0) * (Q[:, 3] - 0.5 * rho * (u * u + v * v))
+    smax = float(np.max(np.sqrt(u * u + v * v) + np.sqrt(eqn.gamma * pr / rho)))
+    return mesh.h_min / ((2 * p + 1) * smax)
+
+
+@dataclass
+class Case:
+    name: str
+    mesh: Mesh
+    p: int
+    eqn: EquationSpec
+    q0: np.ndarray
+    dt: float
+    scheme: str
+    levels: str
+    kdim: int
+    steps: int
+    extra: dict = field(default_factory=dict)
+
+    @property
+    def n_dofs(self) -> int:
+        return self.q0.size
+
+
+def _project(mesh, p, fn):
+    xy = solution_point_coords(mesh, p)
+    return np.asarray(fn(xy[..., 0], xy[..., 1]), dtype=np.float64).reshape(-1)
+
+
+def _noise(q, amp, seed=0):
+    return q + amp * np.random.default_rng(seed).uniform(-1.0, 1.0, q.shape)
+
+
+def config(k: int, seed: int = 0, nx: int | None = None) -> Case:
+    """BASELINE.json configs[k-1] (k = 1..5); nx overrides the mesh size
+    for reduced-size parity runs of the same physics."""
+    if k == 1:
+        n = nx or 16
+        mesh = generate_box(n, n, 10.0, 10.0, periodic=True)
+        eqn = EquationSpec(kind="navier-stokes", mach=0.5, reynolds=100.0, ref_length=10.0)
+        q0 = _noise(_project(mesh, 3, isentropic_vortex(eqn)), 1e-6, seed)
+        dt = 20.0 * explicit_dt(mesh, 3, eqn, q0)
+        return Case("config1", mesh, 3, eqn, q0, dt, "esdirk2", "3-2", 30, 1,
+                    {"smoother_shift": 50.0, "rtol": 1e-3})
+    if k == 2:
+        n = nx or 256
+        mesh = generate_box(n, n, 10.0, 10.0, periodic=True)
+        eqn = EquationSpec(kind="navier-stokes", mach=0.5, reynolds=1000.0, ref_length=10.0)
+        q0 = _noise(_project(mesh, 4, isentropic_vortex(eqn)), 1e-6, seed)
+        dt = 50.0 * explicit_dt(mesh, 4, eqn, q0)
+        return Case("config2", mesh, 4, eqn, q0, dt, "esdirk2", "4-2", 30, 10,
+                    {"smoother_shift": 50.0, "rtol": 1e-3})
+    if k == 3:
+        n = nx or 128
+        mesh = generate_box(n, n, 10.0, 10.0, periodic=True)
+        eqn = EquationSpec(kind="navier-stokes", mach=1e-3, reynolds=500.0, ref_length=10.0)
+        rng = np.random.default_rng(seed)
+        xy = solution_point_coords(mesh, 4)
+        x, y = xy[..., 0], xy[..., 1]
+        rho = 1.0 + 1e-3 * np.exp(-((x - 5.0) ** 2 + (y - 5.0) ** 2) / 0.5 ** 2)
+        u = 1.0 + 1e-6 * rng.uniform(-1, 1, x.shape)
+        v = 1e-6 * rng.uniform(-1, 1, x.shape)
+        p = np.full_like(x, 1.0 / (eqn.gamma * eqn.mach ** 2))
+        E = p / (eqn.gamma - 1.0) + 0.5 * rho * (u * u + v * v)
+        q0 = np.stack([rho, rho * u, rho * v, E], axis=-1).reshape(-1)
+        return Case("config3", mesh, 4, eqn, q0, np.inf, "steady", "4-3-2-1-0", 30, 1,
+                    {"smoother_shift": 1e3})
+    if k == 4:
+        nxx, ny = (nx or 512), (nx // 4 if nx else 128)
+        ratio = 1.0497  # fills [0, 1] from h0 = 1e-4 over 128 cells
+        h = 1e-4 * ratio ** np.arange(ny)
+        yn = np.concatenate([[0.0], np.cumsum(h)])
+        yn = yn / yn[-1]
+        mesh = generate_channel(nxx, ny, 4.0, yn)
+        eqn = EquationSpec(kind="navier-stokes", mach=0.2, reynolds=1e4, ref_length=1.0)
+        xy = solution_point_coords(mesh, 3)
+        y = xy[..., 1]
+        u = np.tanh(y / 0.05)
+        rho = np.ones_like(y)
+        v = np.zeros_like(y)
+        p = np.full_like(y, 1.0 / (eqn.gamma * eqn.mach ** 2))
+        E = p / (eqn.gamma - 1.0) + 0.5 * rho * (u * u + v * v)
+        q0 = _noise(np.stack([rho, rho * u, rho * v, E], axis=-1).reshape(-1), 1e-5, seed)
+        dt = 10.0 * explicit_dt(mesh, 3, eqn, q0)
+        return Case("config4", mesh, 3, eqn, q0, dt, "row4", "3-2", 60, 20, {"smoother_shift": 50.0})
+    if k == 5:
+        n = nx or 1024
+        mesh = generate_box(n, n, 10.0, 10.0, periodic=True)
+        eqn = EquationSpec(kind="navier-stokes", mach=0.3, reynolds=2000.0, ref_length=10.0)
+        rng = np.random.default_rng(seed)
+        signs = rng.choice([-1.0, 1.0], size=(8, 8))
+        xy = solution_point_coords(mesh, 5)
+        x, y = xy[..., 0], xy[..., 1]
+        L, cell = 10.0, 10.0 / 8
+        fs = eqn.free_stream()
+        g = eqn.gamma
+        Tinf = 1.0 / (g * eqn.mach ** 2)
+        du = np.zeros_like(x)
+        dv = np.zeros_like(x)
+        dT = np.zeros_like(x)
+        for i in range(8):
+            for j in range(8):
+                cx, cy = (i + 0.5) * cell, (j + 0.5) * cell
+                xc = np.mod(x - cx + L / 2, L) - L / 2
+                yc = np.mod(y - cy + L / 2, L) - L / 2
+                r2 = (xc * xc + yc * yc) / (0.25 * cell) ** 2
+                e = np.exp(0.5 * (1.0 - r2))
+                b = 5.0 * signs[i, j] * 0.25
+                du += -b / (2 * np.pi) * e * yc / (0.25 * cell)
+                dv += b / (2 * np.pi) * e * xc / (0.25 * cell)
+                dT += -(g - 1.0) * b ** 2 / (8.0 * g * np.pi ** 2) * np.exp(1 - r2)
+        T = Tinf + dT
+        rho = (T / Tinf) ** (1.0 / (g - 1.0))
+        u, v = 1.0 + du, dv
+        p = rho * T
+        E = p / (g - 1.0) + 0.5 * rho * (u * u + v * v)
+        q0 = np.stack([rho, rho * u, rho * v, E], axis=-1).reshape(-1)
+        del fs
+        dt = 100.0 * explicit_dt(mesh, 5, eqn, q0)
+        return Case("config5", mesh, 5, eqn, q0, dt, "esdirk2", "5-4", 30, 5, {"smoother_shift": 50.0})
+    raise ValueError("config index is 1..5")

@@ -1,0 +1,264 @@
+// extern "C" boundary of libpmgflow_b200.so -- see include/pmgflow_b200.h.
+#include <atomic>
+#include <climits>
+#include <cstring>
+#include <vector>
+
+#include "../../include/pmgflow_b200.h"
+#include "pmgb_internal.cuh"
+
+namespace pmgb {
+int launch_inverse(int64_t M, int SZ, const double* BT, double* invT, cudaStream_t st, Status* stp);
+int launch_block_gemv(int64_t M, int SZ, const double* invT, const double* x, double omega, const double* base,
+                      double* out, cudaStream_t st);
+int launch_transfer(int64_t M, int nv, int nin, int nout, const double* T, const double* src,
+                    const double* src_base, double* dst, int accumulate, cudaStream_t st);
+int launch_dot(int64_t n, const double* x, const double* y, double* out, int do_sqrt, cudaStream_t st);
+int launch_mgs(int64_t n, double* V, int64_t ld, int j, double* w, double* H, double thresh, int* finite_flag,
+               cudaStream_t st);
+int launch_lincomb(int64_t n, int k, const double* c, const double* const* xs, double* out, cudaStream_t st);
+int launch_gemv_t(int64_t n, int k, const double* V, int64_t ld, const double* y, double* out, cudaStream_t st);
+int launch_any_nonzero(int64_t n, const double* x, int* flag_dev, cudaStream_t st);
+Status* status_ptr();
+}  // namespace pmgb
+
+using namespace pmgb;
+
+struct pmgb_disc {
+  DiscDev d;
+};
+
+static std::atomic<int64_t> g_launches{0};
+static inline cudaStream_t S(void* s) { return (cudaStream_t)s; }
+
+extern "C" {
+
+PMGB_API const char* pmgb_version(void) { return "pmgflow_b200 0.1 sm_100a fp64"; }
+PMGB_API int64_t pmgb_launch_count(void) { return g_launches.load(); }
+
+PMGB_API const char* pmgb_error_string(int code) {
+  if (code == 0) return "ok";
+  if (code > 0) return cudaGetErrorString((cudaError_t)code);
+  switch (code) {
+    case -1: return "invalid argument";
+    case -2: return "unsupported polynomial degree (0..5)";
+    case -3: return "unsupported equation kind";
+    case -1000: return "no kernel instance for this degree/kind";
+    case -1001: return "vector count out of range";
+  }
+  return "unknown pmgflow_b200 error";
+}
+
+PMGB_API int pmgb_disc_create(const pmgb_disc_desc* desc, pmgb_disc** out) {
+  if (!desc || !out) return -1;
+  if (desc->degree < 0 || desc->degree > 5) return -2;
+  if (desc->kind < 0 || desc->kind > 2) return -3;
+  pmgb_disc* h = new pmgb_disc();
+  DiscDev& d = h->d;
+  std::memset(&d.C, 0, sizeof(d.C));
+  d.p = desc->degree;
+  const int n = d.p + 1;
+  d.kind = desc->kind == 0 ? K_EULER : desc->kind == 1 ? K_NS : (desc->diffusivity > 0.0 ? K_ADVD : K_ADV);
+  d.nv = desc->kind == 2 ? 1 : 4;
+  d.M = desc->n_elem;
+  d.n_dofs = d.M * n * n * d.nv;
+  for (int i = 0; i < n * n; ++i) d.C.D[i] = desc->D[i];
+  for (int i = 0; i < n; ++i) {
+    d.C.eL[i] = desc->eL[i];
+    d.C.eR[i] = desc->eR[i];
+    d.C.lL[i] = desc->lL[i];
+    d.C.lR[i] = desc->lR[i];
+    d.C.xg[i] = desc->xg[i];
+  }
+  for (int v = 0; v < d.nv; ++v) d.C.qinf[v] = desc->free_stream[v];
+  d.C.gamma = desc->gamma;
+  d.C.mu = desc->mu;
+  d.C.kappa = desc->kappa;
+  d.C.adv_x = desc->adv_x;
+  d.C.adv_y = desc->adv_y;
+  d.C.diff = desc->diffusivity;
+  std::vector<int2> lk((size_t)d.M * 4);
+  for (int64_t e = 0; e < d.M; ++e) {
+    for (int f = 0; f < 4; ++f) {
+      const int64_t* r = desc->links + (e * 4 + f) * 4;
+      const int tag = desc->tags[e * 4 + f];
+      int2 v;
+      v.x = (int)r[0];
+      const int face = r[0] >= 0 ? (int)r[1] : 0;
+      v.y = (face & 3) | ((int)(r[2] & 1) << 2) | ((int)(r[3] & 1) << 3) | ((tag < 0 ? 0 : tag & 15) << 4);
+      lk[(size_t)e * 4 + f] = v;
+    }
+  }
+  const size_t face_bytes = sizeof(double) * (size_t)d.M * 4 * n * d.nv;
+  cudaError_t err = cudaSuccess;
+  err = cudaMalloc(&d.geom, sizeof(double) * 20 * (size_t)d.M);
+  if (!err) err = cudaMalloc(&d.link, sizeof(int2) * 4 * (size_t)d.M);
+  if (!err) err = cudaMalloc(&d.qtr, face_bytes);
+  if (!err) err = cudaMalloc(&d.fvn, face_bytes);
+  if (!err) err = cudaMalloc(&d.qp, sizeof(double) * (size_t)d.n_dofs);
+  if (!err) err = cudaMemcpy(d.geom, desc->geom, sizeof(double) * 20 * (size_t)d.M, cudaMemcpyHostToDevice);
+  if (!err) err = cudaMemcpy(d.link, lk.data(), sizeof(int2) * 4 * (size_t)d.M, cudaMemcpyHostToDevice);
+  if (err) {
+    pmgb_disc_destroy(h);
+    return (int)err;
+  }
+  d.mesh.M = d.M;
+  d.mesh.geom = d.geom;
+  d.mesh.link = d.link;
+  *out = h;
+  return 0;
+}
+
+PMGB_API int pmgb_disc_destroy(pmgb_disc* h) {
+  if (!h) return 0;
+  cudaFree(h->d.geom);
+  cudaFree(h->d.link);
+  cudaFree(h->d.qtr);
+  cudaFree(h->d.fvn);
+  cudaFree(h->d.qp);
+  delete h;
+  return 0;
+}
+
+PMGB_API int64_t pmgb_disc_n_dofs(const pmgb_disc* h) { return h ? h->d.n_dofs : -1; }
+
+static int n_res_launches(const DiscDev& d) { return (d.kind == K_NS || d.kind == K_ADVD) ? 3 : 2; }
+
+PMGB_API int pmgb_eval(pmgb_disc* h, const double* q, const double* X, double eps, const pmgb_epilogue* e,
+                       double* out, void* stream) {
+  if (!h || !q || !out || !e) return -1;
+  Epi ep;
+  ep.mode = e->mode;
+  ep.s = e->s;
+  ep.eps = e->eps;
+  ep.adt = e->adt;
+  ep.dtau = e->dtau;
+  ep.sb_scalar = e->sb_scalar;
+  ep.se_scalar = e->se_scalar;
+  ep.X = e->X;
+  ep.R0 = e->R0;
+  ep.E = e->E;
+  ep.Sb = e->Sb;
+  ep.Se = e->Se;
+  g_launches += n_res_launches(h->d);
+  return launch_residual(h->d, q, X, eps, ep, out, S(stream));
+}
+
+PMGB_API int pmgb_residual(pmgb_disc* h, const double* q, double* R, void* stream) {
+  pmgb_epilogue e;
+  std::memset(&e, 0, sizeof(e));
+  e.mode = PMGB_EPI_R;
+  return pmgb_eval(h, q, nullptr, 0.0, &e, R, stream);
+}
+
+PMGB_API int pmgb_jfnk_matvec(pmgb_disc* h, const double* X, const double* q, const double* R0, double shift,
+                              double eps, double* out, void* stream) {
+  pmgb_epilogue e;
+  std::memset(&e, 0, sizeof(e));
+  e.mode = PMGB_EPI_JV;
+  e.s = shift;
+  e.eps = eps;
+  e.X = X;
+  e.R0 = R0;
+  return pmgb_eval(h, q, X, eps, &e, out, stream);
+}
+
+PMGB_API int pmgb_freeze(pmgb_disc* h, const double* q, double* qtr, double* fvn, void* stream) {
+  if (!h || !q || !qtr) return -1;
+  g_launches += n_res_launches(h->d) - 1;
+  return launch_freeze(h->d, q, qtr, fvn, S(stream));
+}
+
+PMGB_API int pmgb_element_residual(pmgb_disc* h, const int64_t* elems, int64_t B, const double* Q,
+                                   const double* qtr, const double* fvn, double* out, void* stream) {
+  if (!h || (B > 0 && (!elems || !Q || !qtr || !out))) return -1;
+  g_launches += 1;
+  return launch_local_residual(h->d, elems, B, Q, qtr, fvn, out, S(stream));
+}
+
+PMGB_API int pmgb_blocks_invert(int64_t M, int32_t sz, const double* BT, double* invT, void* stream) {
+  g_launches += 1;
+  return launch_inverse(M, sz, BT, invT, S(stream), status_ptr());
+}
+
+PMGB_API int pmgb_blocks_assemble(pmgb_disc* h, const double* q, double shift, double eps, double* BT,
+                                  double* invT, void* stream) {
+  if (!h || !q || !BT) return -1;
+  const DiscDev& d = h->d;
+  int rc = launch_freeze(d, q, d.qtr, d.fvn, S(stream));
+  if (rc) return rc;
+  rc = launch_blocks(d, q, d.qtr, d.fvn, shift, eps, BT, S(stream));
+  if (rc) return rc;
+  g_launches += n_res_launches(d);
+  if (invT) {
+    const int n = d.p + 1;
+    return pmgb_blocks_invert(d.M, n * n * d.nv, BT, invT, stream);
+  }
+  return 0;
+}
+
+PMGB_API int pmgb_ej_apply(int64_t M, int32_t sz, const double* invT, const double* x, double* y, void* stream) {
+  g_launches += 1;
+  return launch_block_gemv(M, sz, invT, x, 0.0, nullptr, y, S(stream));
+}
+
+PMGB_API int pmgb_ej_update(int64_t M, int32_t sz, const double* invT, const double* dd, double omega,
+                            const double* base, double* out, void* stream) {
+  if (!base) return -1;
+  g_launches += 1;
+  return launch_block_gemv(M, sz, invT, dd, omega, base, out, S(stream));
+}
+
+PMGB_API int pmgb_transfer(int64_t M, int32_t nv, int32_t nin, int32_t nout, const double* T, const double* src,
+                           const double* src_base, double* dst, int32_t accumulate, void* stream) {
+  if (nin < 1 || nin > 6 || nout < 1 || nout > 6) return -1;
+  g_launches += 1;
+  return launch_transfer(M, nv, nin, nout, T, src, src_base, dst, accumulate, S(stream));
+}
+
+PMGB_API int pmgb_dot(int64_t n, const double* x, const double* y, double* r, void* stream) {
+  g_launches += 1;
+  return launch_dot(n, x, y, r, 0, S(stream));
+}
+
+PMGB_API int pmgb_nrm2(int64_t n, const double* x, double* r, void* stream) {
+  g_launches += 1;
+  return launch_dot(n, x, x, r, 1, S(stream));
+}
+
+PMGB_API int pmgb_mgs(int64_t n, double* V, int64_t ld, int32_t j, double* w, double* H, double thresh,
+                      int32_t* finite_dev, void* stream) {
+  g_launches += j + 3;
+  return launch_mgs(n, V, ld, j, w, H, thresh, finite_dev, S(stream));
+}
+
+PMGB_API int pmgb_lincomb(int64_t n, int32_t k, const double* c, const double* const* xs, double* out,
+                          void* stream) {
+  g_launches += 1;
+  return launch_lincomb(n, k, c, xs, out, S(stream));
+}
+
+PMGB_API int pmgb_gemv_t(int64_t n, int32_t k, const double* V, int64_t ld, const double* y, double* out,
+                         void* stream) {
+  g_launches += 1;
+  return launch_gemv_t(n, k, V, ld, y, out, S(stream));
+}
+
+PMGB_API int pmgb_any_nonzero(int64_t n, const double* x, int32_t* flag, void* stream) {
+  g_launches += 1;
+  return launch_any_nonzero(n, x, flag, S(stream));
+}
+
+PMGB_API int pmgb_status(void* stream, int32_t* kind, int64_t* element, int32_t clear) {
+  Status s;
+  const int rc = status_read(S(stream), &s, clear);
+  if (kind) *kind = s.kind;
+  if (element) *element = s.element;
+  return rc;
+}
+
+PMGB_API int pmgb_status_clear(void* stream) { return status_clear_async(S(stream)); }
+
+PMGB_API int pmgb_sync(void* stream) { return (int)cudaStreamSynchronize(S(stream)); }
+
+}  // extern "C"

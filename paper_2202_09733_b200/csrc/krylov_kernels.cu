@@ -1,0 +1,218 @@
+// Deterministic BLAS-1 and Arnoldi (modified Gram-Schmidt) kernels.
+//
+// Reference: newton_krylov.py:79-151 (gmres_solve): H[i,j] = V_i . w,
+// w -= H[i,j] V_i (:119-121), H[j+1,j] = ||w|| (:122), V_{j+1} = w/H
+// (:124-127), x += P(V^T y) (:147-148); np.all(np.isfinite(w)) (:116).
+//
+// Every reduction uses a fixed grid, a fixed per-thread stride order, a
+// fixed warp-shuffle tree and a fixed-order final pass by the last CTA
+// to arrive (the arrival order never changes the arithmetic), so results
+// are bitwise reproducible run to run -- the reference's residual logs
+// are bitwise deterministic (tests/test_acceptance.py:472-501).
+#include "pmgb_internal.cuh"
+
+namespace pmgb {
+
+constexpr int RED_THREADS = 256;
+constexpr int RED_BLOCKS = 296;  // 2 x 148 SMs
+
+struct RedScratch {
+  double* partial;          // RED_BLOCKS
+  unsigned int* counter;    // 1
+  int* flag;                // 1
+};
+
+static RedScratch g_red = {nullptr, nullptr, nullptr};
+
+static int red_scratch(RedScratch* out) {
+  if (g_red.partial == nullptr) {
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, sizeof(double) * RED_BLOCKS + 64);
+    if (e != cudaSuccess) return (int)e;
+    cudaMemset(p, 0, sizeof(double) * RED_BLOCKS + 64);
+    g_red.partial = (double*)p;
+    g_red.counter = (unsigned int*)((char*)p + sizeof(double) * RED_BLOCKS);
+    g_red.flag = (int*)((char*)p + sizeof(double) * RED_BLOCKS + 16);
+    cudaDeviceSynchronize();
+  }
+  *out = g_red;
+  return 0;
+}
+
+__device__ __forceinline__ double block_sum(double v) {
+  __shared__ double ws[RED_THREADS / 32];
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) ws[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x < 32) {
+    s = (lane < RED_THREADS / 32) ? ws[lane] : 0.0;
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off);
+  }
+  return s;  // valid in thread 0
+}
+
+// last-arriving CTA sums the partials in a fixed order
+__device__ __forceinline__ bool finish(const RedScratch& rs, double mine, double* out, bool do_sqrt) {
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    rs.partial[blockIdx.x] = mine;
+    __threadfence();
+    const unsigned prev = atomicAdd(rs.counter, 1u);
+    last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last) return false;
+  __threadfence();
+  double v = 0.0;
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) v += ((volatile double*)rs.partial)[i];
+  v = block_sum(v);
+  if (threadIdx.x == 0) {
+    *out = do_sqrt ? sqrt(v) : v;
+    *rs.counter = 0u;
+  }
+  return true;
+}
+
+// w <- w - h_prev * Vprev (if Vprev); out = Vnext . w  (Vnext may be w)
+// optionally flags a non-finite w on the first pass.
+__global__ void __launch_bounds__(RED_THREADS)
+k_mgs_pass(int64_t n, double* __restrict__ w, const double* __restrict__ Vprev, const double* hprev,
+           const double* Vnext, double* out, int do_sqrt, int check_finite, RedScratch rs) {
+  const double h = Vprev ? *hprev : 0.0;
+  double acc = 0.0;
+  int bad = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    double wi = w[i];
+    if (Vprev) {
+      wi = wi - h * Vprev[i];
+      w[i] = wi;
+    }
+    if (check_finite && !isfinite(wi)) bad = 1;
+    acc += Vnext[i] * wi;
+  }
+  if (check_finite && __syncthreads_or(bad) && threadIdx.x == 0) atomicOr(rs.flag, 1);
+  const double s = block_sum(acc);
+  finish(rs, s, out, do_sqrt != 0);
+}
+
+__global__ void __launch_bounds__(RED_THREADS)
+k_dot(int64_t n, const double* __restrict__ x, const double* __restrict__ y, double* out, int do_sqrt,
+      RedScratch rs) {
+  double acc = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) acc += x[i] * y[i];
+  const double s = block_sum(acc);
+  finish(rs, s, out, do_sqrt != 0);
+}
+
+// V_{j+1} = w / H if H > thresh (newton_krylov.py:123-127)
+__global__ void k_normalize(int64_t n, const double* __restrict__ w, const double* h, double thresh,
+                            double* __restrict__ v) {
+  const double hv = *h;
+  if (!(hv > thresh)) return;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) v[i] = w[i] / hv;
+}
+
+// out = sum_{i<k} c_i x_i  (coefficients by value, k <= 8)
+struct Lin {
+  double c[8];
+  const double* x[8];
+  int k;
+};
+
+__global__ void k_lincomb(int64_t n, const Lin L, double* __restrict__ out) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    double s = L.c[0] * L.x[0][i];
+    for (int j = 1; j < L.k; ++j) s = s + L.c[j] * L.x[j][i];
+    out[i] = s;
+  }
+}
+
+// out = V^T y with y on the device (x += P(V[:j].T @ y))
+__global__ void k_gemv_t(int64_t n, int k, const double* __restrict__ V, int64_t ld, const double* y,
+                         double* __restrict__ out) {
+  __shared__ double ys[128];
+  for (int j = threadIdx.x; j < k && j < 128; j += blockDim.x) ys[j] = y[j];
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    double s = 0.0;
+    for (int j = 0; j < k; ++j) s += V[(int64_t)j * ld + i] * ys[j];
+    out[i] = s;
+  }
+}
+
+__global__ void k_any_nonzero(int64_t n, const double* __restrict__ x, int* flag) {
+  int hit = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    if (x[i] != 0.0) hit = 1;
+  if (__syncthreads_or(hit) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
+static unsigned ew_grid(int64_t n) {
+  int64_t g = (n + 255) / 256;
+  if (g > 148 * 16) g = 148 * 16;
+  if (g < 1) g = 1;
+  return (unsigned)g;
+}
+
+int launch_dot(int64_t n, const double* x, const double* y, double* out, int do_sqrt, cudaStream_t st) {
+  RedScratch rs;
+  int e = red_scratch(&rs);
+  if (e) return e;
+  k_dot<<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, x, y, out, do_sqrt, rs);
+  return (int)cudaGetLastError();
+}
+
+// One full MGS orthogonalisation of w against V[0..j] (row stride ld):
+// H[0..j] and H[j+1] = ||w||, V[j+1] = w / H[j+1] when H[j+1] > thresh.
+// The finite flag covers w as it enters (before any projection).
+int launch_mgs(int64_t n, double* V, int64_t ld, int j, double* w, double* H, double thresh, int* finite_flag,
+               cudaStream_t st) {
+  RedScratch rs;
+  int e = red_scratch(&rs);
+  if (e) return e;
+  cudaMemsetAsync(rs.flag, 0, sizeof(int), st);
+  for (int i = 0; i <= j; ++i) {
+    const double* Vprev = (i == 0) ? nullptr : V + (int64_t)(i - 1) * ld;
+    const double* hprev = (i == 0) ? nullptr : H + (i - 1);
+    k_mgs_pass<<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, w, Vprev, hprev, V + (int64_t)i * ld, H + i, 0,
+                                                   i == 0 ? 1 : 0, rs);
+  }
+  k_mgs_pass<<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, w, V + (int64_t)j * ld, H + j, w, H + j + 1, 1, 0, rs);
+  k_normalize<<<ew_grid(n), 256, 0, st>>>(n, w, H + j + 1, thresh, V + (int64_t)(j + 1) * ld);
+  if (finite_flag) cudaMemcpyAsync(finite_flag, rs.flag, sizeof(int), cudaMemcpyDeviceToDevice, st);
+  return (int)cudaGetLastError();
+}
+
+int launch_lincomb(int64_t n, int k, const double* c, const double* const* xs, double* out, cudaStream_t st) {
+  if (k < 1 || k > 8) return -1001;
+  Lin L;
+  for (int i = 0; i < 8; ++i) {
+    L.c[i] = i < k ? c[i] : 0.0;
+    L.x[i] = i < k ? xs[i] : nullptr;
+  }
+  L.k = k;
+  k_lincomb<<<ew_grid(n), 256, 0, st>>>(n, L, out);
+  return (int)cudaGetLastError();
+}
+
+int launch_gemv_t(int64_t n, int k, const double* V, int64_t ld, const double* y, double* out, cudaStream_t st) {
+  if (k < 1 || k > 128) return -1001;
+  k_gemv_t<<<ew_grid(n), 256, 0, st>>>(n, k, V, ld, y, out);
+  return (int)cudaGetLastError();
+}
+
+int launch_any_nonzero(int64_t n, const double* x, int* flag_dev, cudaStream_t st) {
+  cudaMemsetAsync(flag_dev, 0, sizeof(int), st);
+  k_any_nonzero<<<ew_grid(n), 256, 0, st>>>(n, x, flag_dev);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace pmgb

@@ -1,0 +1,109 @@
+// Internal definitions shared by the sm_100a FP64 kernels.
+//
+// Data layout in HBM (all FP64, element-major, reference AoS layout):
+//   solution / residual vectors: [M][n][n][nv]   (eta index, xi index, var)
+//     -- reference spatial.py:209-215, SURVEY Appendix B
+//   face traces qtr:             [M][4][n][nv]   CCW point order per face
+//   one-sided viscous flux fvn:  [M][4][n][nv]   along the element's own normal
+//   geometry record:             [M][20]         see mesh.pack_geometry
+//   face links:                  [M][4] int2     {nb elem | -1, flags}
+//   EJ blocks / inverses:        [M][sz][sz] column-major (B^T row-major)
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace pmgb {
+
+enum Kind { K_EULER = 0, K_NS = 1, K_ADV = 2, K_ADVD = 3 };
+enum Tag { T_WALL_ADIABATIC = 0, T_WALL_SLIP = 1, T_FAR_FIELD = 2 };
+
+// link.y bit layout
+__host__ __device__ inline int lk_face(int y) { return y & 3; }
+__host__ __device__ inline int lk_rev(int y) { return (y >> 2) & 1; }
+__host__ __device__ inline int lk_left(int y) { return (y >> 3) & 1; }
+__host__ __device__ inline int lk_tag(int y) { return (y >> 4) & 15; }
+
+template <int KIND> struct KT;
+template <> struct KT<K_EULER> { static constexpr int NV = 4, NW = 3; static constexpr bool VISC = false, FLOW = true; };
+template <> struct KT<K_NS>    { static constexpr int NV = 4, NW = 3; static constexpr bool VISC = true,  FLOW = true; };
+template <> struct KT<K_ADV>   { static constexpr int NV = 1, NW = 1; static constexpr bool VISC = false, FLOW = false; };
+template <> struct KT<K_ADVD>  { static constexpr int NV = 1, NW = 1; static constexpr bool VISC = true,  FLOW = false; };
+
+// CTA shape: one thread per solution point, EPB elements per CTA.
+template <int P> struct BC {
+  static constexpr int N = P + 1, NP = N * N, NF = 4 * N;
+  static constexpr int THREADS = (P >= 5) ? 256 : 128;
+  static constexpr int EPB = (THREADS / NP) > 32 ? 32 : ((THREADS / NP) >= 1 ? THREADS / NP : 1);
+};
+
+// Operator matrices + physics constants, passed by value (constant bank).
+struct FrConst {
+  double D[36];               // D[k*n + i] = l_i'(x_k)
+  double eL[6], eR[6], lL[6], lR[6], xg[6];
+  double qinf[4];
+  double gamma, mu, kappa, adv_x, adv_y, diff;
+};
+
+struct FrMesh {
+  int64_t M;
+  const double* __restrict__ geom;  // (M,20)
+  const int2* __restrict__ link;    // (M,4)
+};
+
+// Fused epilogue of the final residual phase (SURVEY 8(b) "fused prologue/epilogue").
+enum EpiMode {
+  EPI_R = 0,         // out = R(q)                                  spatial.py:501
+  EPI_F = 1,         // out = s q - R(q)                            pmg.py:152-153
+  EPI_DEFECT = 2,    // out = (Sb - (s q - R(q))) + Se              pmg.py:155-159
+  EPI_JV = 3,        // out = s X - (R(q+eps X) - R0)/eps           newton_krylov.py:71-76
+  EPI_STAGE_F = 4,   // out = (q - E)/adt - R(q)                    time_integration.py:138-141
+  EPI_STAGE_JV = 5,  // out = X/dtau + (F(q+eps X) - Fk)/eps        newton_krylov.py:402-405
+  EPI_NEG_R = 6,     // out = -R(q)       (steady stage function)   time_integration.py:139-140
+  EPI_OUTER_F = 7,   // out = s q - R(q) - Se                       pmg.py:325-326
+};
+
+struct Epi {
+  int mode;
+  double s, eps, adt, dtau, sb_scalar, se_scalar;
+  const double* X;    // perturbation direction (JV modes)
+  const double* R0;   // R0 (EPI_JV) or Fk (EPI_STAGE_JV)
+  const double* E;    // explicit stage part
+  const double* Sb;   // S_base array (or null -> sb_scalar)
+  const double* Se;   // S_extra array (or null -> se_scalar)
+};
+
+// Device-global status: first non-physical state seen since the last clear.
+struct Status {
+  int kind;             // 0 none, 1 state, 2 trace, 3 singular block
+  int pad;
+  long long element;
+};
+
+}  // namespace pmgb
+
+// host-side launch helpers (defined in fr_kernels.cu etc.)
+namespace pmgb {
+struct DiscDev {
+  int p, kind;
+  int64_t M;
+  FrConst C;
+  FrMesh mesh;
+  double* geom;
+  int2* link;
+  double* qtr;   // scratch traces (M,4,n,nv)
+  double* fvn;   // scratch viscous flux (M,4,n,nv)
+  double* qp;    // scratch perturbed state
+  int nv;
+  int64_t n_dofs;
+};
+
+int launch_residual(const DiscDev& d, const double* q, const double* X, double eps,
+                    const Epi& epi, double* out, cudaStream_t st);
+int launch_freeze(const DiscDev& d, const double* q, double* qtr, double* fvn, cudaStream_t st);
+int launch_local_residual(const DiscDev& d, const int64_t* elems, int64_t B, const double* Q,
+                          const double* qtr, const double* fvn, double* out, cudaStream_t st);
+int launch_blocks(const DiscDev& d, const double* q, const double* qtr, const double* fvn,
+                  double shift, double eps, double* blocksT, cudaStream_t st);
+int status_clear_async(cudaStream_t st);
+int status_read(cudaStream_t st, Status* out, int clear);
+}  // namespace pmgb

@@ -1,0 +1,316 @@
+"""Device pseudo-transient Newton-Krylov -- drop-in for pmgflow.newton_krylov.
+
+Control flow is the reference's, line for line
+(``/root/reference/pkg/src/pmgflow/newton_krylov.py``); every vector
+operation runs in libpmgflow_b200 on device-resident FP64 tensors:
+
+* ``jfnk_matvec``        :71-76   fused prologue/epilogue R kernel
+* ``gmres_solve``        :79-151  device MGS Arnoldi (deterministic
+                                  reductions), host Givens / back-solve on
+                                  the (m+1) x m Hessenberg matrix, one
+                                  device->host sync per Arnoldi step
+* ``assemble_element_blocks`` / ``BlockJacobian`` / ``ej_apply``
+                         :157-214 FD blocks + batched Gauss-Jordan inverse
+                                  + batched block GEMV
+* ``ptc_solve`` / ``ser_update`` / ``PtcConfig`` / ``KrylovConfig``
+                         :28-68, :377-437
+
+Non-physical states are latched on the device and raised at the same
+control-flow points the reference raises them (after the enqueued work
+of a residual call is synchronised), so the PTC halving and pMG
+fallback decisions are unchanged.  The block-ILU0 / MBNK machinery
+(:220-371) is outside this round's scope.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import check, load
+from .equation import NonPhysicalStateError
+from .spatial import Discretization, raise_status
+from .vec import any_nonzero, lincomb, nrm2, ptr, stream, to_device
+
+FD_EPS = 1e-6
+
+
+@dataclass
+class PtcConfig:
+    dtau_init: float = 1e-3
+    dtau_max: float = 1e12
+    max_iters: int = 100
+    rtol: float = 1e-4
+    atol: float | None = None
+    ser: bool = True
+    ser_as_printed: bool = False
+    refresh_every: int = 0
+    max_halvings: int = 1
+
+    def __post_init__(self):
+        if self.dtau_init <= 0:
+            raise ValueError("dtau_init must be positive")
+
+
+@dataclass
+class KrylovConfig:
+    kdim: int = 30
+    max_restarts: int = 10
+    rtol: float = 1e-4
+
+    def __post_init__(self):
+        if self.kdim < 1:
+            raise ValueError("kdim must be >= 1")
+
+
+def ser_update(dtau, f_old, f_new, dtau_max, as_printed=False):
+    """SER pseudo-step growth (newton_krylov.py:56-68)."""
+    if f_old == 0.0 or f_new == 0.0:
+        return dtau_max
+    ratio = (f_new / f_old) if as_printed else (f_old / f_new)
+    return min(dtau * ratio, dtau_max)
+
+
+def _device_disc(residual):
+    """The Discretization behind a bound ``disc.residual`` (fused path)."""
+    d = getattr(residual, "__self__", None)
+    if isinstance(d, Discretization) and getattr(residual, "__func__", None) is Discretization.residual:
+        return d
+    return None
+
+
+def jfnk_matvec(X, q, R0, residual, shift, eps=FD_EPS, check_zero=True, sync=True):
+    """(shift I - dR/dq) X ~ shift X - (R(q + eps X) - R0)/eps."""
+    Xd = to_device(X)
+    if check_zero and not any_nonzero(Xd):
+        return torch.zeros_like(Xd)
+    qd, R0d = to_device(q), to_device(R0)
+    disc = _device_disc(residual)
+    if disc is not None:
+        out = disc.eval(qd, _lib.EPI_JV, X=Xd, eps=eps, s=shift, R0=R0d, check_status=sync)
+    else:
+        qp = lincomb((1.0, eps), (qd, Xd))
+        Rp = to_device(residual(qp))
+        out = lincomb((shift, -1.0 / eps, 1.0 / eps), (Xd, Rp, R0d))
+    return out
+
+
+def _back_substitute(H, g):
+    k = len(g)
+    y = np.zeros(k)
+    for i in range(k - 1, -1, -1):
+        y[i] = (g[i] - H[i, i + 1:k] @ y[i + 1:k]) / H[i, i]
+    return y
+
+
+def gmres_solve(matvec, b, cfg: KrylovConfig, x0=None, precond=None):
+    """Right-preconditioned restarted GMRES(m), newton_krylov.py:79-151.
+
+    matvec / precond map device tensors to device tensors.  Returns
+    (x, total inner iterations, final relative residual)."""
+    lib = load()
+    b = to_device(b)
+    n = b.numel()
+    bnorm = nrm2(b)
+    x = torch.zeros_like(b) if x0 is None else to_device(x0).clone()
+    if bnorm == 0.0:
+        return x, 0, 0.0
+    if precond is None:
+        precond = lambda v: v
+    m = cfg.kdim
+    V = torch.empty((m + 1, n), dtype=torch.float64, device=b.device)
+    Hd = torch.zeros((m, m + 2), dtype=torch.float64, device=b.device)
+    flag = torch.zeros(1, dtype=torch.int32, device=b.device)
+    thresh = 1e-14 * bnorm
+    total = 0
+    relres = np.inf
+    for _ in range(cfg.max_restarts):
+        if any_nonzero(x):
+            r = lincomb((1.0, -1.0), (b, matvec(x)))
+        else:
+            r = b.clone()
+        beta = nrm2(r)
+        raise_status()
+        relres = beta / bnorm
+        if relres <= cfg.rtol:
+            return x, total, relres
+        H = np.zeros((m + 1, m))
+        cs = np.zeros(m)
+        sn = np.zeros(m)
+        g = np.zeros(m + 1)
+        g[0] = beta
+        lincomb((1.0 / beta,), (r,), out=V[0])
+        j_done = 0
+        breakdown = False
+        for j in range(m):
+            w = matvec(precond(V[j]))
+            check(lib.pmgb_mgs(n, V.data_ptr(), n, j, ptr(w), Hd[j].data_ptr(), thresh,
+                               flag.data_ptr(), stream()), "mgs")
+            hcol = Hd[j, :j + 2].cpu().numpy()
+            raise_status()
+            if int(flag.item()):
+                raise RuntimeError(f"non-finite Arnoldi vector at inner iteration {total + 1}")
+            H[:j + 2, j] = hcol
+            total += 1
+            if not (H[j + 1, j] > thresh):
+                breakdown = True
+            for i in range(j):
+                t = cs[i] * H[i, j] + sn[i] * H[i + 1, j]
+                H[i + 1, j] = -sn[i] * H[i, j] + cs[i] * H[i + 1, j]
+                H[i, j] = t
+            rho = np.hypot(H[j, j], H[j + 1, j])
+            if rho == 0.0:
+                cs[j], sn[j] = 1.0, 0.0
+            else:
+                cs[j] = H[j, j] / rho
+                sn[j] = H[j + 1, j] / rho
+            H[j, j] = rho
+            H[j + 1, j] = 0.0
+            g[j + 1] = -sn[j] * g[j]
+            g[j] = cs[j] * g[j]
+            j_done = j + 1
+            relres = abs(g[j + 1]) / bnorm
+            if relres <= cfg.rtol or breakdown:
+                break
+        y = _back_substitute(H[:j_done, :j_done], g[:j_done])
+        yd = torch.as_tensor(y, device=b.device)
+        comb = torch.empty_like(b)
+        check(lib.pmgb_gemv_t(n, j_done, V.data_ptr(), n, yd.data_ptr(), comb.data_ptr(), stream()), "gemv_t")
+        x = lincomb((1.0, 1.0), (x, to_device(precond(comb))))
+        if relres <= cfg.rtol or breakdown:
+            return x, total, relres
+    return x, total, relres
+
+
+# ---------------------------------------------------------------------------
+# element-Jacobi blocks
+
+class BlockJacobian:
+    """Inverted diagonal blocks of (shift I - dR/dq), one per element.
+
+    Storage is column-major per element on the device (``invT[e][j][i]
+    = B_e^-1[i][j]``); ``inv`` / ``blocks`` give the reference's
+    per-group (M, sz, sz) row-major views."""
+
+    def __init__(self, disc: Discretization, shift: float, invT: torch.Tensor, blocksT=None):
+        self.disc = disc
+        self.shift = shift
+        self.invT = invT
+        self.blocksT = blocksT
+
+    @property
+    def inv(self):
+        return [self.invT.transpose(1, 2)]
+
+    @property
+    def blocks(self):
+        if self.blocksT is None:
+            raise AttributeError("blocks were not kept (keep_blocks=False)")
+        return [self.blocksT.transpose(1, 2)]
+
+    def apply(self, X):
+        is_np = not isinstance(X, torch.Tensor)
+        Xd = to_device(X, self.disc.device)
+        out = torch.empty_like(Xd)
+        check(load().pmgb_ej_apply(self.disc.mesh.n_elements, self.disc.elem_size, self.invT.data_ptr(),
+                                   ptr(Xd), ptr(out), stream()), "ej_apply")
+        return out.cpu().numpy() if is_np else out
+
+    def update(self, d: torch.Tensor, omega: float, base: torch.Tensor, out=None) -> torch.Tensor:
+        """out = base + omega * B^-1 d (smooth_ej, pmg.py:164)."""
+        if out is None:
+            out = torch.empty_like(base)
+        check(load().pmgb_ej_update(self.disc.mesh.n_elements, self.disc.elem_size, self.invT.data_ptr(),
+                                    ptr(d), float(omega), ptr(base), ptr(out), stream()), "ej_update")
+        return out
+
+
+def assemble_element_blocks(disc: Discretization, data, shift: float, frozen=None, eps: float = FD_EPS,
+                            keep_blocks: bool = True) -> BlockJacobian:
+    """FD element blocks of shift I - dR/dq and their inverses.
+
+    ``frozen`` is accepted for signature parity; the device freeze of
+    ``data`` is always recomputed inside the assembly (same values).
+    Raises RuntimeError("singular Jacobi block for element e")."""
+    del frozen
+    q = to_device(data, disc.device)
+    M, sz = disc.mesh.n_elements, disc.elem_size
+    invT = torch.empty((M, sz, sz), dtype=torch.float64, device=disc.device)
+    blocksT = torch.empty_like(invT) if keep_blocks else invT
+    check(load().pmgb_blocks_assemble(disc._h, ptr(q), float(shift), float(eps), blocksT.data_ptr(),
+                                      invT.data_ptr(), stream()), "blocks_assemble")
+    raise_status()
+    return BlockJacobian(disc, shift, invT, blocksT if keep_blocks else None)
+
+
+def ej_apply(blocks: BlockJacobian, X):
+    return blocks.apply(X)
+
+
+# ---------------------------------------------------------------------------
+# pseudo-transient continuation (newton_krylov.py:377-437)
+
+def _norm_checked(v: torch.Tensor) -> float:
+    nv = nrm2(v)
+    raise_status()
+    return nv
+
+
+def ptc_solve(F, q0, cfg: PtcConfig, krylov: KrylovConfig, precond_factory=None, eps: float = FD_EPS):
+    """Drive F(q) = 0 by PTC with JFNK-GMRES; returns (q, stats).
+
+    ``F`` maps device tensors to device tensors.  If it exposes
+    ``fused_jv(X, q, Fk, dtau, eps)`` (the device stage function does),
+    the PTC matvec X/dtau + (F(q+eps X) - Fk)/eps is one fused kernel
+    chain; otherwise it is composed from F and device BLAS-1."""
+    q = to_device(q0).clone()
+    Fk = F(q)
+    n0 = _norm_checked(Fk)
+    stats = {"iters": 0, "gmres_iters": 0, "converged": True, "aborted": False,
+             "history": [(n0, 1.0, cfg.dtau_init)], "final_norm": n0}
+    if n0 == 0.0 or (cfg.atol is not None and n0 <= cfg.atol):
+        return q, stats
+    dtau = cfg.dtau_init
+    P = precond_factory(q, dtau) if precond_factory else None
+    fused = getattr(F, "fused_jv", None)
+    halvings = 0
+    k = 0
+    while k < cfg.max_iters:
+        if fused is not None:
+            def matvec(X, q=q, Fk=Fk, dtau=dtau):
+                return fused(X, q, Fk, dtau, eps)
+        else:
+            def matvec(X, q=q, Fk=Fk, dtau=dtau):
+                Fp = F(lincomb((1.0, eps), (q, X)))
+                return lincomb((1.0 / dtau, 1.0 / eps, -1.0 / eps), (X, Fp, Fk))
+        try:
+            dq, it, _ = gmres_solve(matvec, lincomb((-1.0,), (Fk,)), krylov, precond=P)
+            stats["gmres_iters"] += it
+            qn = lincomb((1.0, 1.0), (q, dq))
+            Fn = F(qn)
+            nk = _norm_checked(Fn)
+        except NonPhysicalStateError:
+            halvings += 1
+            if halvings > cfg.max_halvings:
+                stats["converged"] = False
+                stats["aborted"] = True
+                return q, stats
+            dtau = 0.5 * dtau
+            continue
+        k += 1
+        stats["iters"] = k
+        q, Fk = qn, Fn
+        if cfg.ser:
+            prev = stats["history"][-1][0]
+            dtau = ser_update(dtau, prev, nk, cfg.dtau_max, cfg.ser_as_printed)
+        stats["history"].append((nk, nk / n0 if n0 else 0.0, dtau))
+        stats["final_norm"] = nk
+        if nk / n0 <= cfg.rtol or (cfg.atol is not None and nk <= cfg.atol):
+            return q, stats
+        if precond_factory and cfg.refresh_every and k % cfg.refresh_every == 0:
+            P = precond_factory(q, dtau)
+    stats["converged"] = False
+    return q, stats

@@ -1,0 +1,229 @@
+"""Device FR discretization -- the drop-in for pmgflow.spatial.Discretization.
+
+Same constructor, attributes and entry points as the reference class
+(``/root/reference/pkg/src/pmgflow/spatial.py:295-904``) for uniform
+polynomial degree, with the arithmetic in libpmgflow_b200 (sm_100a FP64):
+
+* ``residual(q)``           spatial.py:501-570 -> 3 kernels (traces,
+                            one-sided viscous flux, common flux + FR
+                            divergence); NonPhysicalStateError as the
+                            reference (smallest element, state before trace)
+* ``freeze(q)``             spatial.py:700-766 -> device traces + fvn
+* ``element_residual``      spatial.py:768-853 -> one fused kernel
+* ``free_stream_field/project/new_field`` (spatial.py:363-380)
+
+Vectors may be NumPy arrays (copied in and out: the reference-facing
+end-to-end path) or contiguous float64 CUDA tensors (device-resident
+path used by the solvers).  Mixed-degree meshes are out of scope for
+this round and rejected loudly.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import check, load
+from .equation import KIND_CODE, EquationSpec, NonPhysicalStateError
+from .mesh import Mesh, face_links, pack_geometry, solution_point_coords, element_geometry
+from .operators import basis, face_operators
+from .vec import ptr, require_cuda, stream, to_device
+
+__all__ = ["Discretization", "SolutionField", "FrozenState", "NonPhysicalStateError",
+           "EquationSpec", "raise_status"]
+
+
+def raise_status(clear: bool = True):
+    """Synchronise and turn the device status word into the reference's
+    exceptions: NonPhysicalStateError(element, what) (spatial.py:27-32,
+    439-446) or RuntimeError for a singular block (newton_krylov.py:207)."""
+    kind = ctypes.c_int32(0)
+    elem = ctypes.c_int64(0)
+    check(load().pmgb_status(stream(), ctypes.byref(kind), ctypes.byref(elem), int(clear)), "status")
+    if kind.value == 1:
+        raise NonPhysicalStateError(elem.value, "state")
+    if kind.value == 2:
+        raise NonPhysicalStateError(elem.value, "trace")
+    if kind.value == 3:
+        raise RuntimeError(f"singular Jacobi block for element {elem.value}")
+
+
+def clear_status():
+    check(load().pmgb_status_clear(stream()), "status_clear")
+
+
+@dataclass
+class SolutionField:
+    nvars: int
+    degrees: np.ndarray
+    offsets: np.ndarray
+    data: torch.Tensor
+
+    @property
+    def n_elements(self) -> int:
+        return len(self.degrees)
+
+    def element(self, e: int) -> torch.Tensor:
+        n = int(self.degrees[e]) + 1
+        return self.data[int(self.offsets[e]):int(self.offsets[e + 1])].view(n, n, self.nvars)
+
+    def copy(self) -> "SolutionField":
+        return SolutionField(self.nvars, self.degrees, self.offsets, self.data.clone())
+
+    def with_data(self, data) -> "SolutionField":
+        return SolutionField(self.nvars, self.degrees, self.offsets, data)
+
+
+@dataclass
+class FrozenState:
+    """Device form of the reference's frozen records: every interior
+    record (neighbour q trace, w trace, -fvn) is a gather from these."""
+
+    qtr: torch.Tensor   # (M, 4, n, nv)
+    fvn: torch.Tensor   # (M, 4, n, nv)
+
+
+class Discretization:
+    """FR residual operator on the device for a uniform-degree mesh."""
+
+    def __init__(self, mesh: Mesh, degrees, eqn: EquationSpec, device=None):
+        require_cuda()
+        self.mesh = mesh
+        self.eqn = eqn
+        degrees = np.asarray(degrees, dtype=np.int64)
+        if degrees.ndim == 0:
+            degrees = np.full(mesh.n_elements, int(degrees))
+        if len(degrees) != mesh.n_elements:
+            raise ValueError("degree map length does not match element count")
+        if (degrees < 0).any():
+            raise ValueError("degrees must be >= 0")
+        if degrees.size and (degrees != degrees[0]).any():
+            raise NotImplementedError("mixed-degree meshes are not on the device path yet")
+        self.degrees = degrees
+        self.p = int(degrees[0]) if degrees.size else 0
+        if self.p > 5:
+            raise NotImplementedError("device kernels cover p = 0..5")
+        self.n = self.p + 1
+        self.nvars = eqn.nvars
+        self.elem_size = self.nvars * self.n * self.n
+        M = mesh.n_elements
+        self.offsets = np.arange(M + 1, dtype=np.int64) * self.elem_size
+        self.n_dofs = int(self.offsets[-1])
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+
+        D, eL, eR, lL, lR = face_operators(self.p)
+        self._ops = dict(D=np.ascontiguousarray(D), eL=eL.copy(), eR=eR.copy(), lL=lL.copy(),
+                         lR=lR.copy(), xg=basis(self.p).points.copy())
+        self._geom = np.ascontiguousarray(pack_geometry(mesh))
+        links, tags = face_links(mesh)
+        self._links = np.ascontiguousarray(links)
+        self._tags = np.ascontiguousarray(tags)
+        self._qinf = np.ascontiguousarray(eqn.free_stream(), dtype=np.float64)
+        dp = lambda a: a.ctypes.data_as(_lib.c_double_p)
+        desc = _lib.DiscDesc(
+            n_elem=M, degree=self.p, kind=KIND_CODE[eqn.kind],
+            gamma=eqn.gamma, mu=eqn.mu, kappa=eqn.heat_conductivity if eqn.kind == "navier-stokes" else 0.0,
+            adv_x=float(eqn.advection[0]), adv_y=float(eqn.advection[1]), diffusivity=eqn.diffusivity,
+            free_stream=dp(self._qinf), D=dp(self._ops["D"]), eL=dp(self._ops["eL"]), eR=dp(self._ops["eR"]),
+            lL=dp(self._ops["lL"]), lR=dp(self._ops["lR"]), xg=dp(self._ops["xg"]), geom=dp(self._geom),
+            links=self._links.ctypes.data_as(_lib.c_int64_p), tags=self._tags.ctypes.data_as(_lib.c_int32_p))
+        h = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            check(load().pmgb_disc_create(ctypes.byref(desc), ctypes.byref(h)), "disc_create")
+        self._h = h
+        self._face_shape = (M, 4, self.n, self.nvars)
+        self._geometry = None
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                load().pmgb_disc_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    # -- host-side conveniences ------------------------------------------------
+
+    @property
+    def geometry(self):
+        if self._geometry is None:
+            self._geometry = element_geometry(self.mesh, self.p)
+        return self._geometry
+
+    def new_field(self) -> SolutionField:
+        return SolutionField(self.nvars, self.degrees, self.offsets,
+                             torch.zeros(self.n_dofs, dtype=torch.float64, device=self.device))
+
+    def free_stream_field(self) -> SolutionField:
+        f = self.new_field()
+        f.data.view(-1, self.nvars).copy_(torch.as_tensor(self.eqn.free_stream(), device=self.device))
+        return f
+
+    def project(self, fn) -> SolutionField:
+        xy = solution_point_coords(self.mesh, self.p)
+        vals = np.asarray(fn(xy[..., 0], xy[..., 1]), dtype=np.float64).reshape(-1)
+        f = self.new_field()
+        f.data.copy_(torch.as_tensor(vals))
+        return f
+
+    # -- device entry points ---------------------------------------------------
+
+    def eval(self, q: torch.Tensor, mode: int, out: torch.Tensor | None = None, *, X=None, eps=0.0,
+             s=0.0, adt=0.0, dtau=0.0, R0=None, E=None, Sb=0.0, Se=0.0, check_status=False):
+        """Fused residual + epilogue (see include/pmgflow_b200.h, PMGB_EPI_*)."""
+        if out is None:
+            out = torch.empty(self.n_dofs, dtype=torch.float64, device=self.device)
+        ep = _lib.Epilogue()
+        ep.mode = mode
+        ep.s, ep.eps, ep.adt, ep.dtau = float(s), float(eps), float(adt), float(dtau)
+        ep.X = ptr(X) if X is not None else None
+        ep.R0 = ptr(R0) if R0 is not None else None
+        ep.E = ptr(E) if E is not None else None
+        if isinstance(Sb, torch.Tensor):
+            ep.Sb = ptr(Sb)
+        else:
+            ep.sb_scalar = float(Sb)
+        if isinstance(Se, torch.Tensor):
+            ep.Se = ptr(Se)
+        else:
+            ep.se_scalar = float(Se)
+        xp = ptr(X) if (X is not None and mode in (_lib.EPI_JV, _lib.EPI_STAGE_JV)) else None
+        check(load().pmgb_eval(self._h, ptr(q), xp, float(eps), ctypes.byref(ep), ptr(out), stream()), "eval")
+        if check_status:
+            raise_status()
+        return out
+
+    def residual(self, data):
+        """R(q); NumPy in -> NumPy out (end-to-end), CUDA tensor -> tensor."""
+        if isinstance(data, torch.Tensor) and data.is_cuda:
+            return self.eval(to_device(data), _lib.EPI_R, check_status=True)
+        q = to_device(data, self.device)
+        R = self.eval(q, _lib.EPI_R, check_status=True)
+        return R.cpu().numpy()
+
+    def freeze(self, data) -> FrozenState:
+        q = to_device(data, self.device)
+        qtr = torch.empty(self._face_shape, dtype=torch.float64, device=self.device)
+        fvn = torch.empty(self._face_shape, dtype=torch.float64, device=self.device)
+        check(load().pmgb_freeze(self._h, ptr(q), qtr.data_ptr(), fvn.data_ptr(), stream()), "freeze")
+        return FrozenState(qtr, fvn)
+
+    def element_residual(self, e, Q, frozen: FrozenState):
+        """Element-local residual with frozen neighbours; Q (..., n, n, nv).
+        ``e`` may be an int or a per-instance array of element ids."""
+        is_np = not isinstance(Q, torch.Tensor)
+        Qd = to_device(Q, self.device)
+        shape = Qd.shape
+        Qf = Qd.reshape(-1, self.elem_size).contiguous()
+        B = Qf.shape[0]
+        el = torch.as_tensor(np.broadcast_to(np.asarray(e, dtype=np.int64), (B,)).copy(), device=self.device)
+        out = torch.empty_like(Qf)
+        check(load().pmgb_element_residual(self._h, el.data_ptr(), B, Qf.data_ptr(), frozen.qtr.data_ptr(),
+                                           frozen.fvn.data_ptr(), out.data_ptr(), stream()), "element_residual")
+        out = out.reshape(shape)
+        return out.cpu().numpy() if is_np else out
