@@ -11,6 +11,8 @@
 //
 // Thread mapping: one thread per solution point, EPB elements per CTA,
 // face work strided over the same CTA; operators staged in shared memory.
+// Shared arrays are SoA component planes (consecutive points of a plane
+// are consecutive doubles), so point-parallel accesses are conflict-free.
 // BR1 reaches two elements deep, so the global residual is split at the
 // two neighbour exchanges (traces, then one-sided viscous fluxes).
 #include <climits>
@@ -21,28 +23,43 @@
 namespace pmgb {
 
 // ---------------------------------------------------------------------------
-// shared-memory layout (in doubles) per CTA
+// shared-memory layout (in doubles) per CTA.  Planes: point planes hold
+// NPT = E*NP values (index el*NP + pt), face planes NFT = E*4N values
+// (index el*4N + f*N + k).
 
 template <int P, int KIND>
 struct SL {
   using B = BC<P>;
   using T = KT<KIND>;
   static constexpr int E = B::EPB, N = B::N, NP = B::NP, NV = T::NV, NW = T::NW;
-  static constexpr int OP = 0;                       // D(36) eL eR lL lR xg (6 each)
-  static constexpr int Q = OP + 72;                  // [E][NP][NV]
-  static constexpr int G = Q + E * NP * NV;          // [E][20]
-  static constexpr int W = G + E * 20;               // [E][NP][NW]
-  static constexpr int FC = W + E * NP * NW;         // [E][4][N][NV]  common face flux, CCW
-  static constexpr int WH = FC + E * 4 * N * NV;     // [E][4][N][NW]  BR1 common value, CCW
-  static constexpr int CG = WH + E * 4 * N * NW;     // [E][2][4][N][NW] gradient lifting terms (line idx)
-  static constexpr int GR = CG + E * 8 * N * NW;     // [E][NP][2][NW] gradients
-  static constexpr int FT = GR + E * NP * 2 * NW;    // [E][NP][NV]
-  static constexpr int GT = FT + E * NP * NV;        // [E][NP][NV]
-  static constexpr int CF = GT + E * NP * NV;        // [E][4][N][NV]  flux lifting terms (line idx)
-  static constexpr int TR = CF + E * 4 * N * NV;     // [E][4][N][NV]  own traces, CCW
-  static constexpr int R0 = TR + E * 4 * N * NV;     // [NP*NV] unperturbed local residual (blocks)
-  static constexpr int TOTAL = R0 + NP * NV;
-  static constexpr size_t BYTES = sizeof(double) * TOTAL;
+  static constexpr int NPT = E * NP, NFT = E * 4 * N;
+  static constexpr int OP = 0;                    // D(36) eL eR lL lR xg (6 each)
+  static constexpr int G = 72;                    // [E][20] geometry records
+  static constexpr int Q = G + E * 20;            // [NV] point planes
+  static constexpr int W = Q + NV * NPT;          // [NW] point planes   viscous variables
+  static constexpr int WH = W + NW * NPT;         // [NW] face planes    BR1 common value (CCW k)
+  static constexpr int CG = WH + NW * NFT;        // [2NW] face planes   gradient lifting (line j)
+  static constexpr int FC = CG + 2 * NW * NFT;    // [NV] face planes    common flux (CCW k)
+  static constexpr int FT = FC + NV * NFT;        // [NV] point planes   contravariant flux xi
+  static constexpr int GT = FT + NV * NPT;        // [NV] point planes   contravariant flux eta
+  static constexpr int CF = CG;                   // [NV] face planes    flux lifting (aliases CG: dead by then)
+  static constexpr int END_ASM = GT + NV * NPT;
+  static constexpr int GR = END_ASM;              // [2NW] point planes  gradients (local pipeline)
+  static constexpr int TR = GR + 2 * NW * NPT;    // [NV] face planes    own traces (local pipeline)
+  static constexpr int R0 = TR + NV * NFT;        // [NP*NV]             unperturbed local residual
+  static constexpr int END_LOCAL = R0 + NP * NV;
+  static constexpr int GR_FVN = FC;               // k_fvn keeps gradients where FC would be
+  static constexpr size_t BYTES_TRACE = sizeof(double) * (Q + NV * NPT);
+  static constexpr size_t BYTES_FVN = sizeof(double) * (GR_FVN + 2 * NW * NPT);
+  static constexpr size_t BYTES_ASM = sizeof(double) * END_ASM;
+  static constexpr size_t BYTES_LOCAL = sizeof(double) * END_LOCAL;
+  static_assert(2 * NW >= NV || true, "CF alias");
+};
+
+template <int P> struct MinBlocks {
+  static constexpr int ASM = (BC<P>::THREADS >= 256) ? 2 : 5;
+  static constexpr int FVN = (BC<P>::THREADS >= 256) ? 3 : 6;
+  static constexpr int TRACE = (BC<P>::THREADS >= 256) ? 4 : 8;
 };
 
 struct Ops {
@@ -74,6 +91,8 @@ __device__ __forceinline__ int fpt(int f, int k, int i) {
   return f == 0 ? i * N + k : f == 1 ? k * N + i : f == 2 ? i * N + (N - 1 - k) : (N - 1 - k) * N + i;
 }
 
+__device__ __forceinline__ double rcp(double x) { return __drcp_rn(x); }
+
 // ---------------------------------------------------------------------------
 // pointwise physics (spatial.py:94-203)
 
@@ -81,9 +100,10 @@ struct Phys {
   double gamma, mu, kappa, ax, ay, diff;
 };
 
-__device__ __forceinline__ void prim(const double* q, double g, double& r, double& u, double& v, double& p) {
+__device__ __forceinline__ void prim(const double* q, double g, double& r, double& ir, double& u, double& v,
+                                     double& p) {
   r = q[0];
-  const double ir = 1.0 / r;
+  ir = rcp(r);
   u = q[1] * ir;
   v = q[2] * ir;
   p = (g - 1.0) * (q[3] - 0.5 * r * (u * u + v * v));
@@ -92,37 +112,37 @@ __device__ __forceinline__ void prim(const double* q, double g, double& r, doubl
 // Roe flux along (nx, ny), no entropy fix (spatial.py:113-163)
 __device__ __forceinline__ void roe(const double* qL, const double* qR, double nx, double ny, double g,
                                     double* F) {
-  double rL, uL, vL, pL, rR, uR, vR, pR;
-  prim(qL, g, rL, uL, vL, pL);
-  prim(qR, g, rR, uR, vR, pR);
-  const double HL = (qL[3] + pL) / rL;
-  const double HR = (qR[3] + pR) / rR;
+  double rL, irL, uL, vL, pL, rR, irR, uR, vR, pR;
+  prim(qL, g, rL, irL, uL, vL, pL);
+  prim(qR, g, rR, irR, uR, vR, pR);
+  const double EpL = qL[3] + pL, EpR = qR[3] + pR;
+  const double HL = EpL * irL;
+  const double HR = EpR * irR;
   const double sL = sqrt(rL), sR = sqrt(rR);
-  const double w = sL / (sL + sR), w1 = 1.0 - w;
+  const double w = sL * rcp(sL + sR), w1 = 1.0 - w;
   const double u = w * uL + w1 * uR;
   const double v = w * vL + w1 * vR;
   const double H = w * HL + w1 * HR;
   const double ke = 0.5 * (u * u + v * v);
   const double c2 = (g - 1.0) * (H - ke);
   const double c = sqrt(c2);
+  const double ic2 = rcp(c2);
   const double rb = sL * sR;
   const double un = u * nx + v * ny;
   const double du = uR - uL, dv = vR - vL;
   const double dn = du * nx + dv * ny;
   const double dtg = -du * ny + dv * nx;
   const double dp = pR - pL;
-  const double i2 = 1.0 / (2.0 * c2);
-  const double k1 = fabs(un - c) * ((dp - rb * c * dn) * i2);
-  const double k2 = fabs(un) * ((rR - rL) - dp / c2);
+  const double k1 = fabs(un - c) * ((dp - rb * c * dn) * (0.5 * ic2));
+  const double k2 = fabs(un) * ((rR - rL) - dp * ic2);
   const double k3 = fabs(un) * (rb * dtg);
-  const double k4 = fabs(un + c) * ((dp + rb * c * dn) * i2);
+  const double k4 = fabs(un + c) * ((dp + rb * c * dn) * (0.5 * ic2));
   const double ut = -u * ny + v * nx;
   const double d0 = k1 + k2 + k4;
   const double d1 = k1 * (u - c * nx) + k2 * u - k3 * ny + k4 * (u + c * nx);
   const double d2 = k1 * (v - c * ny) + k2 * v + k3 * nx + k4 * (v + c * ny);
   const double d3 = k1 * (H - c * un) + k2 * ke + k3 * ut + k4 * (H + c * un);
   const double qnL = uL * nx + vL * ny, qnR = uR * nx + vR * ny;
-  const double EpL = qL[3] + pL, EpR = qR[3] + pR;
   F[0] = 0.5 * (qL[0] * qnL + qR[0] * qnR) - 0.5 * d0;
   F[1] = 0.5 * ((qL[1] * qnL + pL * nx) + (qR[1] * qnR + pR * nx)) - 0.5 * d1;
   F[2] = 0.5 * ((qL[2] * qnL + pL * ny) + (qR[2] * qnR + pR * ny)) - 0.5 * d2;
@@ -163,13 +183,12 @@ __device__ __forceinline__ void ghost(const double* q, int tag, double nx, doubl
   }
 }
 
-// viscous variables W (spatial.py:448-454)
+// viscous variables W = (u, v, T = p/rho) (spatial.py:448-454)
 template <int KIND>
 __device__ __forceinline__ void grad_vars(const double* q, double g, double* w) {
   if constexpr (KT<KIND>::FLOW) {
-    const double r = q[0], ir = 1.0 / r;
-    const double u = q[1] * ir, v = q[2] * ir;
-    const double p = (g - 1.0) * (q[3] - 0.5 * r * (u * u + v * v));
+    double r, ir, u, v, p;
+    prim(q, g, r, ir, u, v, p);
     w[0] = u;
     w[1] = v;
     w[2] = p * ir;
@@ -183,7 +202,7 @@ template <int KIND>
 __device__ __forceinline__ void visc_flux(const double* q, const double* gx, const double* gy, const Phys& ph,
                                           double* fx, double* fy) {
   if constexpr (KT<KIND>::FLOW) {
-    const double ir = 1.0 / q[0];
+    const double ir = rcp(q[0]);
     const double u = q[1] * ir, v = q[2] * ir;
     const double d = gx[0] + gy[1];
     const double txx = ph.mu * (2.0 * gx[0] - (2.0 / 3.0) * d);
@@ -203,28 +222,9 @@ __device__ __forceinline__ void visc_flux(const double* q, const double* gx, con
   }
 }
 
-template <int KIND>
-__device__ __forceinline__ void inv_flux(const double* q, const Phys& ph, double* fx, double* fy) {
-  if constexpr (KT<KIND>::FLOW) {
-    double r, u, v, p;
-    prim(q, ph.gamma, r, u, v, p);
-    fx[0] = q[1];
-    fx[1] = q[1] * u + p;
-    fx[2] = q[1] * v;
-    fx[3] = u * (q[3] + p);
-    fy[0] = q[2];
-    fy[1] = q[2] * u;
-    fy[2] = q[2] * v + p;
-    fy[3] = v * (q[3] + p);
-  } else {
-    fx[0] = ph.ax * q[0];
-    fy[0] = ph.ay * q[0];
-  }
-}
-
 __device__ __forceinline__ bool physical(const double* q, double g) {
-  double r, u, v, p;
-  prim(q, g, r, u, v, p);
+  double r, ir, u, v, p;
+  prim(q, g, r, ir, u, v, p);
   return (r > 0.0) && (p > 0.0);
 }
 
@@ -247,13 +247,16 @@ __device__ __forceinline__ Phys phys_of(const FrConst& C) {
 // ---------------------------------------------------------------------------
 // staging helpers
 
+// element-major AoS global (E elements from e0) -> SoA point planes
 template <int P, int NV>
 __device__ __forceinline__ void load_points(const double* __restrict__ src, int64_t e0, int64_t M, double* sQ) {
-  constexpr int NP = BC<P>::NP, E = BC<P>::EPB;
-  const int64_t nval = (int64_t)E * NP * NV;
+  constexpr int NP = BC<P>::NP, E = BC<P>::EPB, NPT = E * NP;
   const int64_t lim = (M - e0) * NP * NV;
   const double* base = src + e0 * NP * NV;
-  for (int i = threadIdx.x; i < nval; i += blockDim.x) sQ[i] = (i < lim) ? __ldg(base + i) : 1.0;
+  for (int i = threadIdx.x; i < NPT * NV; i += blockDim.x) {
+    const int v = i % NV, g = i / NV;
+    sQ[v * NPT + g] = (i < lim) ? __ldg(base + i) : 1.0;
+  }
 }
 
 template <int P>
@@ -264,24 +267,49 @@ __device__ __forceinline__ void load_geom(const double* __restrict__ geom, int64
   for (int i = threadIdx.x; i < E * 20; i += blockDim.x) sG[i] = (i < lim) ? __ldg(base + i) : 0.0;
 }
 
-// trace of smem point array X[NP][C] component c at face (f, k)
-template <int N, int C>
-__device__ __forceinline__ double line_sum(const Ops& op, const double* X, int f, int k, int c) {
+// trace of one point plane (already offset to the element) at face (f, k)
+template <int N>
+__device__ __forceinline__ double line_sum(const Ops& op, const double* plane_el, int f, int k) {
   const double* w = (f == 0 || f == 3) ? op.eL : op.eR;
   double s = 0.0;
 #pragma unroll
-  for (int i = 0; i < N; ++i) s += w[i] * X[fpt<N>(f, k, i) * C + c];
+  for (int i = 0; i < N; ++i) s += w[i] * plane_el[fpt<N>(f, k, i)];
   return s;
+}
+
+template <int NV>
+__device__ __forceinline__ void ld_face(const double* __restrict__ src, double* out) {
+  if constexpr (NV == 4) {
+    const double2 a = __ldg(reinterpret_cast<const double2*>(src));
+    const double2 b = __ldg(reinterpret_cast<const double2*>(src) + 1);
+    out[0] = a.x;
+    out[1] = a.y;
+    out[2] = b.x;
+    out[3] = b.y;
+  } else {
+    out[0] = __ldg(src);
+  }
+}
+
+template <int NV>
+__device__ __forceinline__ void st_face(double* dst, const double* v) {
+  if constexpr (NV == 4) {
+    reinterpret_cast<double2*>(dst)[0] = make_double2(v[0], v[1]);
+    reinterpret_cast<double2*>(dst)[1] = make_double2(v[2], v[3]);
+  } else {
+    dst[0] = v[0];
+  }
 }
 
 // ---------------------------------------------------------------------------
 // BR1 gradient pieces (spatial.py:594-603 via _divergence 407-430)
 
-// face thread: lifting terms for the x and y gradients at (f, k) -> line index j
+// face thread: lifting terms of the x and y gradients at (f, k) -> line j
 template <int P, int KIND>
 __device__ __forceinline__ void grad_corrections(const Ops& op, const double* sW, const double* sG_el,
-                                                 const double* sWH_el, double* sCG_el, int f, int k) {
+                                                 const double* sWH, double* sCG, int el, int f, int k) {
   constexpr int N = P + 1, NW = KT<KIND>::NW;
+  constexpr int NPT = SL<P, KIND>::NPT, NFT = SL<P, KIND>::NFT, NP = N * N;
   const Metric mt = metric(sG_el);
   const double nx = sG_el[8 + 2 * f], ny = sG_el[9 + 2 * f], js = sG_el[16 + f];
   const double sgn = (f == 1 || f == 2) ? 1.0 : -1.0;
@@ -298,86 +326,112 @@ __device__ __forceinline__ void grad_corrections(const Ops& op, const double* sW
     // y-gradient: Ft = -J01 W,           Gt =  J00 W
     const double fxx = xiline ? mt.J11(x) : -mt.J10(x);
     const double fyy = xiline ? -mt.J01(x) : mt.J00(x);
-    const double* Wp = sW + fpt<N>(f, k, i) * NW;
+    const int p = el * NP + fpt<N>(f, k, i);
 #pragma unroll
     for (int c = 0; c < NW; ++c) {
-      lx[c] += w[i] * (fxx * Wp[c]);
-      ly[c] += w[i] * (fyy * Wp[c]);
+      const double Wv = sW[c * NPT + p];
+      lx[c] += w[i] * (fxx * Wv);
+      ly[c] += w[i] * (fyy * Wv);
     }
   }
-  const double* wh = sWH_el + (f * N + k) * NW;
+  const int fi = el * 4 * N + f * N + k;
+  const int fj = el * 4 * N + f * N + j;
 #pragma unroll
   for (int c = 0; c < NW; ++c) {
-    sCG_el[((0 * 4 + f) * N + j) * NW + c] = sgn * js * (nx * wh[c]) - lx[c];
-    sCG_el[((1 * 4 + f) * N + j) * NW + c] = sgn * js * (ny * wh[c]) - ly[c];
+    const double wh = sWH[c * NFT + fi];
+    sCG[c * NFT + fj] = sgn * js * (nx * wh) - lx[c];
+    sCG[(NW + c) * NFT + fj] = sgn * js * (ny * wh) - ly[c];
   }
 }
 
 // point thread: corrected gradients at (a, b)
 template <int P, int KIND>
 __device__ __forceinline__ void gradient_at(const Ops& op, const double* sW, const double* sG_el,
-                                            const double* sCG_el, int a, int b, double* gx, double* gy) {
+                                            const double* sCG, int el, int a, int b, double* gx, double* gy) {
   constexpr int N = P + 1, NW = KT<KIND>::NW;
+  constexpr int NPT = SL<P, KIND>::NPT, NFT = SL<P, KIND>::NFT, NP = N * N;
   const Metric mt = metric(sG_el);
-  double sx[NW], sy[NW];
+  double sx[NW], sy[NW], dx[NW], dy[NW];
 #pragma unroll
-  for (int c = 0; c < NW; ++c) sx[c] = sy[c] = 0.0;
-  // d/dxi of Ft along row a, d/deta of Gt along column b
-  double dx[NW], dy[NW];
-#pragma unroll
-  for (int c = 0; c < NW; ++c) dx[c] = dy[c] = 0.0;
+  for (int c = 0; c < NW; ++c) sx[c] = sy[c] = dx[c] = dy[c] = 0.0;
+  const int base = el * NP;
 #pragma unroll
   for (int i = 0; i < N; ++i) {
     const double Db = op.D[b * N + i], Da = op.D[a * N + i];
     const double xi = op.xg[i];
-    const double* Wr = sW + (a * N + i) * NW;  // row a, column i
-    const double* Wc = sW + (i * N + b) * NW;  // row i, column b
-    const double j11 = mt.J11(xi), j01 = mt.J01(xi);   // xi_i dependence (row line)
-    const double j10 = mt.J10(xi), j00 = mt.J00(xi);   // eta_i dependence (column line)
+    const double j11 = mt.J11(xi), j01 = mt.J01(xi);  // row line: xi_i
+    const double j10 = mt.J10(xi), j00 = mt.J00(xi);  // column line: eta_i
 #pragma unroll
     for (int c = 0; c < NW; ++c) {
-      sx[c] += Db * (j11 * Wr[c]);
-      sy[c] += Db * (-j01 * Wr[c]);
-      dx[c] += Da * (-j10 * Wc[c]);
-      dy[c] += Da * (j00 * Wc[c]);
+      const double Wr = sW[c * NPT + base + a * N + i];
+      const double Wc = sW[c * NPT + base + i * N + b];
+      sx[c] += Db * (j11 * Wr);
+      sy[c] += Db * (-j01 * Wr);
+      dx[c] += Da * (-j10 * Wc);
+      dy[c] += Da * (j00 * Wc);
     }
   }
   const double xa = op.xg[a], xb = op.xg[b];
-  const double det = mt.J00(xa) * mt.J11(xb) - mt.J01(xb) * mt.J10(xa);
-  const double* cx = sCG_el;
-  const double* cy = sCG_el + 4 * N * NW;
+  const double idet = rcp(mt.J00(xa) * mt.J11(xb) - mt.J01(xb) * mt.J10(xa));
+  const int f0 = el * 4 * N;
+  const double lRb = op.lR[b], lLb = op.lL[b], lRa = op.lR[a], lLa = op.lL[a];
 #pragma unroll
   for (int c = 0; c < NW; ++c) {
+    const double* cx = sCG + c * NFT + f0;
+    const double* cy = sCG + (NW + c) * NFT + f0;
     double vx = sx[c] + dx[c];
-    vx = vx + op.lR[b] * cx[(1 * N + a) * NW + c];
-    vx = vx - op.lL[b] * cx[(3 * N + a) * NW + c];
-    vx = vx + op.lR[a] * cx[(2 * N + b) * NW + c];
-    vx = vx - op.lL[a] * cx[(0 * N + b) * NW + c];
+    vx = vx + lRb * cx[1 * N + a];
+    vx = vx - lLb * cx[3 * N + a];
+    vx = vx + lRa * cx[2 * N + b];
+    vx = vx - lLa * cx[0 * N + b];
     double vy = sy[c] + dy[c];
-    vy = vy + op.lR[b] * cy[(1 * N + a) * NW + c];
-    vy = vy - op.lL[b] * cy[(3 * N + a) * NW + c];
-    vy = vy + op.lR[a] * cy[(2 * N + b) * NW + c];
-    vy = vy - op.lL[a] * cy[(0 * N + b) * NW + c];
-    gx[c] = vx / det;
-    gy[c] = vy / det;
+    vy = vy + lRb * cy[1 * N + a];
+    vy = vy - lLb * cy[3 * N + a];
+    vy = vy + lRa * cy[2 * N + b];
+    vy = vy - lLa * cy[0 * N + b];
+    gx[c] = vx * idet;
+    gy[c] = vy * idet;
   }
 }
 
-// point thread: total flux (inviscid - viscous), transformed -> sFT/sGT
+// point thread: total flux (inviscid - viscous), transformed
 template <int P, int KIND>
 __device__ __forceinline__ void point_fluxes(const double* q, const double* gx, const double* gy,
                                              const Phys& ph, const Metric& mt, double xa, double xb,
                                              double* Ft, double* Gt) {
   constexpr int NV = KT<KIND>::NV;
   double fx[NV], fy[NV];
-  inv_flux<KIND>(q, ph, fx, fy);
-  if constexpr (KT<KIND>::VISC) {
-    double vx[NV], vy[NV];
-    visc_flux<KIND>(q, gx, gy, ph, vx, vy);
-#pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      fx[v] = fx[v] - vx[v];
-      fy[v] = fy[v] - vy[v];
+  if constexpr (KT<KIND>::FLOW) {
+    double r, ir, u, v, p;
+    prim(q, ph.gamma, r, ir, u, v, p);
+    fx[0] = q[1];
+    fx[1] = q[1] * u + p;
+    fx[2] = q[1] * v;
+    fx[3] = u * (q[3] + p);
+    fy[0] = q[2];
+    fy[1] = q[2] * u;
+    fy[2] = q[2] * v + p;
+    fy[3] = v * (q[3] + p);
+    if constexpr (KT<KIND>::VISC) {
+      const double d = gx[0] + gy[1];
+      const double txx = ph.mu * (2.0 * gx[0] - (2.0 / 3.0) * d);
+      const double tyy = ph.mu * (2.0 * gy[1] - (2.0 / 3.0) * d);
+      const double txy = ph.mu * (gy[0] + gx[1]);
+      fx[1] = fx[1] - txx;
+      fx[2] = fx[2] - txy;
+      fx[3] = fx[3] - (u * txx + v * txy + ph.kappa * gx[2]);
+      fy[1] = fy[1] - txy;
+      fy[2] = fy[2] - tyy;
+      fy[3] = fy[3] - (u * txy + v * tyy + ph.kappa * gy[2]);
+      fx[0] = fx[0] - 0.0;
+      fy[0] = fy[0] - 0.0;
+    }
+  } else {
+    fx[0] = ph.ax * q[0];
+    fy[0] = ph.ay * q[0];
+    if constexpr (KT<KIND>::VISC) {
+      fx[0] = fx[0] - ph.diff * gx[0];
+      fy[0] = fy[0] - ph.diff * gy[0];
     }
   }
   const double j00 = mt.J00(xa), j10 = mt.J10(xa), j01 = mt.J01(xb), j11 = mt.J11(xb);
@@ -388,67 +442,78 @@ __device__ __forceinline__ void point_fluxes(const double* q, const double* gx, 
   }
 }
 
-// face thread: FR lifting term of the flux divergence, line index j
+// face thread: FR lifting term of the flux divergence, line j
 template <int P, int KIND>
-__device__ __forceinline__ void flux_corrections(const Ops& op, const double* sFT_el, const double* sGT_el,
-                                                 const double* sG_el, const double* Fc, double* sCF_el,
-                                                 int f, int k) {
-  constexpr int N = P + 1, NV = KT<KIND>::NV;
+__device__ __forceinline__ void flux_corrections(const Ops& op, const double* sFT, const double* sGT,
+                                                 const double* sG_el, const double* Fc, double* sCF,
+                                                 int el, int f, int k) {
+  constexpr int N = P + 1, NV = KT<KIND>::NV, NP = N * N;
+  constexpr int NPT = SL<P, KIND>::NPT, NFT = SL<P, KIND>::NFT;
   const double js = sG_el[16 + f];
   const double sgn = (f == 1 || f == 2) ? 1.0 : -1.0;
   const int j = (f >= 2) ? N - 1 - k : k;
-  const double* X = (f == 1 || f == 3) ? sFT_el : sGT_el;
+  const double* X = (f == 1 || f == 3) ? sFT : sGT;
+  const int fj = el * 4 * N + f * N + j;
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
-    const double l = line_sum<N, NV>(op, X, f, k, v);
-    sCF_el[(f * N + j) * NV + v] = sgn * js * Fc[v] - l;
+    const double l = line_sum<N>(op, X + v * NPT + el * NP, f, k);
+    sCF[v * NFT + fj] = sgn * js * Fc[v] - l;
   }
 }
 
 // point thread: -div / det (spatial.py:407-430, 627)
 template <int P, int KIND>
-__device__ __forceinline__ void divergence_at(const Ops& op, const double* sFT_el, const double* sGT_el,
-                                              const double* sCF_el, const Metric& mt, int a, int b,
+__device__ __forceinline__ void divergence_at(const Ops& op, const double* sFT, const double* sGT,
+                                              const double* sCF, const Metric& mt, int el, int a, int b,
                                               double* R) {
-  constexpr int N = P + 1, NV = KT<KIND>::NV;
-  double s[NV];
+  constexpr int N = P + 1, NV = KT<KIND>::NV, NP = N * N;
+  constexpr int NPT = SL<P, KIND>::NPT, NFT = SL<P, KIND>::NFT;
+  double s[NV], t[NV];
 #pragma unroll
-  for (int v = 0; v < NV; ++v) s[v] = 0.0;
-  double t[NV];
-#pragma unroll
-  for (int v = 0; v < NV; ++v) t[v] = 0.0;
+  for (int v = 0; v < NV; ++v) s[v] = t[v] = 0.0;
+  const int base = el * NP;
 #pragma unroll
   for (int i = 0; i < N; ++i) {
     const double Db = op.D[b * N + i], Da = op.D[a * N + i];
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
-      s[v] += Db * sFT_el[(a * N + i) * NV + v];
-      t[v] += Da * sGT_el[(i * N + b) * NV + v];
+      s[v] += Db * sFT[v * NPT + base + a * N + i];
+      t[v] += Da * sGT[v * NPT + base + i * N + b];
     }
   }
   const double xa = op.xg[a], xb = op.xg[b];
-  const double det = mt.J00(xa) * mt.J11(xb) - mt.J01(xb) * mt.J10(xa);
+  const double idet = rcp(mt.J00(xa) * mt.J11(xb) - mt.J01(xb) * mt.J10(xa));
+  const int f0 = el * 4 * N;
+  const double lRb = op.lR[b], lLb = op.lL[b], lRa = op.lR[a], lLa = op.lL[a];
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
+    const double* cf = sCF + v * NFT + f0;
     double d = s[v] + t[v];
-    d = d + op.lR[b] * sCF_el[(1 * N + a) * NV + v];
-    d = d - op.lL[b] * sCF_el[(3 * N + a) * NV + v];
-    d = d + op.lR[a] * sCF_el[(2 * N + b) * NV + v];
-    d = d - op.lL[a] * sCF_el[(0 * N + b) * NV + v];
-    R[v] = -(d / det);
+    d = d + lRb * cf[1 * N + a];
+    d = d - lLb * cf[3 * N + a];
+    d = d + lRa * cf[2 * N + b];
+    d = d - lLa * cf[0 * N + b];
+    R[v] = -(d * idet);
   }
+}
+
+template <int NV, int NPT>
+__device__ __forceinline__ void gather_point(const double* sQ, int t, double* q) {
+#pragma unroll
+  for (int v = 0; v < NV; ++v) q[v] = sQ[v * NPT + t];
 }
 
 // ---------------------------------------------------------------------------
 // phase 1: traces (+ optional q + eps X prologue, + physicality flags)
 
 template <int P, int KIND>
-__global__ void __launch_bounds__(BC<P>::THREADS)
+__global__ void __launch_bounds__(BC<P>::THREADS, MinBlocks<P>::TRACE)
 k_trace(const FrConst C, const FrMesh m, const double* __restrict__ q, const double* __restrict__ X,
         double eps, double* __restrict__ qp, double* __restrict__ qtr, int* __restrict__ bad) {
   extern __shared__ double sm[];
   using L = SL<P, KIND>;
   constexpr int N = BC<P>::N, NP = BC<P>::NP, NF = BC<P>::NF, E = BC<P>::EPB, NV = KT<KIND>::NV;
+  constexpr int NPT = L::NPT;
   const Ops op = stage_ops(C, sm);
   double* sQ = sm + L::Q;
   const int64_t e0 = (int64_t)blockIdx.x * E;
@@ -457,17 +522,17 @@ k_trace(const FrConst C, const FrMesh m, const double* __restrict__ q, const dou
     load_points<P, NV>(q, e0, M, sQ);
   } else {
     // q + eps * X, rounded as the reference does (newton_krylov.py:76)
-    const int64_t nval = (int64_t)E * NP * NV, lim = (M - e0) * NP * NV;
+    const int64_t lim = (M - e0) * NP * NV;
     const double* qb = q + e0 * NP * NV;
     const double* xb = X + e0 * NP * NV;
     double* pb = qp + e0 * NP * NV;
-    for (int i = threadIdx.x; i < nval; i += blockDim.x) {
+    for (int i = threadIdx.x; i < NPT * NV; i += blockDim.x) {
       double v = 1.0;
       if (i < lim) {
         v = __dadd_rn(__ldg(qb + i), __dmul_rn(eps, __ldg(xb + i)));
         pb[i] = v;
       }
-      sQ[i] = v;
+      sQ[(i % NV) * NPT + i / NV] = v;
     }
   }
   __syncthreads();
@@ -475,9 +540,11 @@ k_trace(const FrConst C, const FrMesh m, const double* __restrict__ q, const dou
   if constexpr (KT<KIND>::FLOW) {
     if (bad != nullptr) {
       const int t = threadIdx.x;
-      if (t < E * NP) {
+      if (t < NPT) {
         const int64_t e = e0 + t / NP;
-        if (e < M && !physical(sQ + t * NV, g)) atomicMin(bad, (int)e);
+        double qq[NV];
+        gather_point<NV, NPT>(sQ, t, qq);
+        if (e < M && !physical(qq, g)) atomicMin(bad, (int)e);
       }
     }
   }
@@ -485,16 +552,13 @@ k_trace(const FrConst C, const FrMesh m, const double* __restrict__ q, const dou
     const int el = t / NF, r = t % NF, f = r / N, k = r % N;
     const int64_t e = e0 + el;
     if (e >= M) continue;
-    const double* Qe = sQ + el * NP * NV;
     double tr[NV];
 #pragma unroll
-    for (int v = 0; v < NV; ++v) tr[v] = line_sum<N, NV>(op, Qe, f, k, v);
+    for (int v = 0; v < NV; ++v) tr[v] = line_sum<N>(op, sQ + v * NPT + el * NP, f, k);
     if constexpr (KT<KIND>::FLOW) {
       if (bad != nullptr && !physical(tr, g)) atomicMin(bad + 1, (int)e);
     }
-    double* dst = qtr + ((e * 4 + f) * N + k) * NV;
-#pragma unroll
-    for (int v = 0; v < NV; ++v) dst[v] = tr[v];
+    st_face<NV>(qtr + ((e * 4 + f) * N + k) * NV, tr);
   }
 }
 
@@ -502,20 +566,20 @@ k_trace(const FrConst C, const FrMesh m, const double* __restrict__ q, const dou
 // phase 2: one-sided viscous normal flux on every face (spatial.py:536-557)
 
 template <int P, int KIND>
-__global__ void __launch_bounds__(BC<P>::THREADS)
+__global__ void __launch_bounds__(BC<P>::THREADS, MinBlocks<P>::FVN)
 k_fvn(const FrConst C, const FrMesh m, const double* __restrict__ q, const double* __restrict__ qtr,
       double* __restrict__ fvn) {
   extern __shared__ double sm[];
   using L = SL<P, KIND>;
   constexpr int N = BC<P>::N, NP = BC<P>::NP, NF = BC<P>::NF, E = BC<P>::EPB;
-  constexpr int NV = KT<KIND>::NV, NW = KT<KIND>::NW;
+  constexpr int NV = KT<KIND>::NV, NW = KT<KIND>::NW, NPT = L::NPT, NFT = L::NFT;
   const Ops op = stage_ops(C, sm);
   double* sQ = sm + L::Q;
   double* sG = sm + L::G;
   double* sW = sm + L::W;
   double* sWH = sm + L::WH;
   double* sCG = sm + L::CG;
-  double* sGR = sm + L::GR;
+  double* sGR = sm + L::GR_FVN;
   const int64_t e0 = (int64_t)blockIdx.x * E;
   const int64_t M = m.M;
   const Phys ph = phys_of(C);
@@ -523,21 +587,23 @@ k_fvn(const FrConst C, const FrMesh m, const double* __restrict__ q, const doubl
   load_geom<P>(m.geom, e0, M, sG);
   __syncthreads();
   const int t0 = threadIdx.x;
-  if (t0 < E * NP) grad_vars<KIND>(sQ + t0 * NV, ph.gamma, sW + t0 * NW);
+  if (t0 < NPT) {
+    double qq[NV], w[NW];
+    gather_point<NV, NPT>(sQ, t0, qq);
+    grad_vars<KIND>(qq, ph.gamma, w);
+#pragma unroll
+    for (int c = 0; c < NW; ++c) sW[c * NPT + t0] = w[c];
+  }
   for (int t = threadIdx.x; t < E * NF; t += blockDim.x) {
     const int el = t / NF, r = t % NF, f = r / N, k = r % N;
     const int64_t e = e0 + el;
     if (e >= M) continue;
     const int2 lk = m.link[e * 4 + f];
     double tr[NV], nb[NV];
-    const double* src = qtr + ((e * 4 + f) * N + k) * NV;
-#pragma unroll
-    for (int v = 0; v < NV; ++v) tr[v] = __ldg(src + v);
+    ld_face<NV>(qtr + ((e * 4 + f) * N + k) * NV, tr);
     if (lk.x >= 0) {
       const int kk = lk_rev(lk.y) ? N - 1 - k : k;
-      const double* ns = qtr + (((int64_t)lk.x * 4 + lk_face(lk.y)) * N + kk) * NV;
-#pragma unroll
-      for (int v = 0; v < NV; ++v) nb[v] = __ldg(ns + v);
+      ld_face<NV>(qtr + (((int64_t)lk.x * 4 + lk_face(lk.y)) * N + kk) * NV, nb);
     } else {
       const double* gq = sG + el * 20;
       ghost<KIND>(tr, lk_tag(lk.y), gq[8 + 2 * f], gq[9 + 2 * f], C.qinf, nb);
@@ -545,26 +611,24 @@ k_fvn(const FrConst C, const FrMesh m, const double* __restrict__ q, const doubl
     double wa[NW], wc[NW];
     grad_vars<KIND>(tr, ph.gamma, wa);
     grad_vars<KIND>(nb, ph.gamma, wc);
-    double* wh = sWH + ((el * 4 + f) * N + k) * NW;
 #pragma unroll
-    for (int c = 0; c < NW; ++c) wh[c] = 0.5 * (wa[c] + wc[c]);
+    for (int c = 0; c < NW; ++c) sWH[c * NFT + t] = 0.5 * (wa[c] + wc[c]);
   }
   __syncthreads();
   for (int t = threadIdx.x; t < E * NF; t += blockDim.x) {
     const int el = t / NF, r = t % NF, f = r / N, k = r % N;
     if (e0 + el >= M) continue;
-    grad_corrections<P, KIND>(op, sW + el * NP * NW, sG + el * 20, sWH + el * 4 * N * NW,
-                              sCG + el * 8 * N * NW, f, k);
+    grad_corrections<P, KIND>(op, sW, sG + el * 20, sWH, sCG, el, f, k);
   }
   __syncthreads();
-  if (t0 < E * NP) {
+  if (t0 < NPT) {
     const int el = t0 / NP, pt = t0 % NP;
     double gx[NW], gy[NW];
-    gradient_at<P, KIND>(op, sW + el * NP * NW, sG + el * 20, sCG + el * 8 * N * NW, pt / N, pt % N, gx, gy);
+    gradient_at<P, KIND>(op, sW, sG + el * 20, sCG, el, pt / N, pt % N, gx, gy);
 #pragma unroll
     for (int c = 0; c < NW; ++c) {
-      sGR[(t0 * 2 + 0) * NW + c] = gx[c];
-      sGR[(t0 * 2 + 1) * NW + c] = gy[c];
+      sGR[c * NPT + t0] = gx[c];
+      sGR[(NW + c) * NPT + t0] = gy[c];
     }
   }
   __syncthreads();
@@ -572,23 +636,21 @@ k_fvn(const FrConst C, const FrMesh m, const double* __restrict__ q, const doubl
     const int el = t / NF, r = t % NF, f = r / N, k = r % N;
     const int64_t e = e0 + el;
     if (e >= M) continue;
-    const double* GRe = sGR + el * NP * 2 * NW;
     double gx[NW], gy[NW];
 #pragma unroll
     for (int c = 0; c < NW; ++c) {
-      gx[c] = line_sum<N, 2 * NW>(op, GRe, f, k, c);
-      gy[c] = line_sum<N, 2 * NW>(op, GRe, f, k, NW + c);
+      gx[c] = line_sum<N>(op, sGR + c * NPT + el * NP, f, k);
+      gy[c] = line_sum<N>(op, sGR + (NW + c) * NPT + el * NP, f, k);
     }
     double tr[NV];
-    const double* src = qtr + ((e * 4 + f) * N + k) * NV;
-#pragma unroll
-    for (int v = 0; v < NV; ++v) tr[v] = __ldg(src + v);
+    ld_face<NV>(qtr + ((e * 4 + f) * N + k) * NV, tr);
     double fx[NV], fy[NV];
     visc_flux<KIND>(tr, gx, gy, ph, fx, fy);
     const double nx = sG[el * 20 + 8 + 2 * f], ny = sG[el * 20 + 9 + 2 * f];
-    double* dst = fvn + ((e * 4 + f) * N + k) * NV;
+    double o[NV];
 #pragma unroll
-    for (int v = 0; v < NV; ++v) dst[v] = fx[v] * nx + fy[v] * ny;
+    for (int v = 0; v < NV; ++v) o[v] = fx[v] * nx + fy[v] * ny;
+    st_face<NV>(fvn + ((e * 4 + f) * N + k) * NV, o);
   }
 }
 
@@ -638,13 +700,13 @@ __device__ __forceinline__ void commit_status(int* bad, Status* st) {
 }
 
 template <int P, int KIND>
-__global__ void __launch_bounds__(BC<P>::THREADS)
+__global__ void __launch_bounds__(BC<P>::THREADS, MinBlocks<P>::ASM)
 k_assemble(const FrConst C, const FrMesh m, const double* __restrict__ q, const double* __restrict__ qtr,
            const double* __restrict__ fvn, const Epi ep, double* __restrict__ out, int* bad, Status* st) {
   extern __shared__ double sm[];
   using L = SL<P, KIND>;
   constexpr int N = BC<P>::N, NP = BC<P>::NP, NF = BC<P>::NF, E = BC<P>::EPB;
-  constexpr int NV = KT<KIND>::NV, NW = KT<KIND>::NW;
+  constexpr int NV = KT<KIND>::NV, NW = KT<KIND>::NW, NPT = L::NPT, NFT = L::NFT;
   constexpr bool VISC = KT<KIND>::VISC;
   if (blockIdx.x == 0 && threadIdx.x == 0) commit_status(bad, st);
   const Ops op = stage_ops(C, sm);
@@ -665,7 +727,13 @@ k_assemble(const FrConst C, const FrMesh m, const double* __restrict__ q, const 
   __syncthreads();
   const int t0 = threadIdx.x;
   if constexpr (VISC) {
-    if (t0 < E * NP) grad_vars<KIND>(sQ + t0 * NV, ph.gamma, sW + t0 * NW);
+    if (t0 < NPT) {
+      double qq[NV], w[NW];
+      gather_point<NV, NPT>(sQ, t0, qq);
+      grad_vars<KIND>(qq, ph.gamma, w);
+#pragma unroll
+      for (int c = 0; c < NW; ++c) sW[c * NPT + t0] = w[c];
+    }
   }
   // common face fluxes: inviscid on the L side's normal (-F to R), viscous
   // 0.5 (fvn_own - fvn_nb), BR1 average (spatial.py:520-568)
@@ -678,14 +746,12 @@ k_assemble(const FrConst C, const FrMesh m, const double* __restrict__ q, const 
     const double nx = gq[8 + 2 * f], ny = gq[9 + 2 * f];
     double tr[NV], nb[NV], F[NV];
     const int64_t own = ((e * 4 + f) * N + k) * NV;
-#pragma unroll
-    for (int v = 0; v < NV; ++v) tr[v] = __ldg(qtr + own + v);
+    ld_face<NV>(qtr + own, tr);
     int64_t nbi = -1;
     if (lk.x >= 0) {
       const int kk = lk_rev(lk.y) ? N - 1 - k : k;
       nbi = (((int64_t)lk.x * 4 + lk_face(lk.y)) * N + kk) * NV;
-#pragma unroll
-      for (int v = 0; v < NV; ++v) nb[v] = __ldg(qtr + nbi + v);
+      ld_face<NV>(qtr + nbi, nb);
       if (lk_left(lk.y)) {
         num_flux<KIND>(tr, nb, nx, ny, ph, F);
       } else {
@@ -702,62 +768,69 @@ k_assemble(const FrConst C, const FrMesh m, const double* __restrict__ q, const 
       double wa[NW], wc[NW];
       grad_vars<KIND>(tr, ph.gamma, wa);
       grad_vars<KIND>(nb, ph.gamma, wc);
-      double* wh = sWH + ((el * 4 + f) * N + k) * NW;
 #pragma unroll
-      for (int c = 0; c < NW; ++c) wh[c] = 0.5 * (wa[c] + wc[c]);
+      for (int c = 0; c < NW; ++c) sWH[c * NFT + t] = 0.5 * (wa[c] + wc[c]);
       double Fv[NV];
-#pragma unroll
-      for (int v = 0; v < NV; ++v) Fv[v] = __ldg(fvn + own + v);
+      ld_face<NV>(fvn + own, Fv);
       if (nbi >= 0) {
+        double Fn[NV];
+        ld_face<NV>(fvn + nbi, Fn);
 #pragma unroll
-        for (int v = 0; v < NV; ++v) Fv[v] = 0.5 * (Fv[v] - __ldg(fvn + nbi + v));
+        for (int v = 0; v < NV; ++v) Fv[v] = 0.5 * (Fv[v] - Fn[v]);
       } else if (KT<KIND>::FLOW && lk_tag(lk.y) == T_WALL_ADIABATIC) {
         Fv[NV - 1] = 0.0;
       }
 #pragma unroll
       for (int v = 0; v < NV; ++v) F[v] = F[v] - Fv[v];
     }
-    double* fc = sFC + ((el * 4 + f) * N + k) * NV;
 #pragma unroll
-    for (int v = 0; v < NV; ++v) fc[v] = F[v];
+    for (int v = 0; v < NV; ++v) sFC[v * NFT + t] = F[v];
   }
   __syncthreads();
   if constexpr (VISC) {
     for (int t = threadIdx.x; t < E * NF; t += blockDim.x) {
       const int el = t / NF, r = t % NF, f = r / N, k = r % N;
       if (e0 + el >= M) continue;
-      grad_corrections<P, KIND>(op, sW + el * NP * NW, sG + el * 20, sWH + el * 4 * N * NW,
-                                sCG + el * 8 * N * NW, f, k);
+      grad_corrections<P, KIND>(op, sW, sG + el * 20, sWH, sCG, el, f, k);
     }
     __syncthreads();
   }
-  if (t0 < E * NP) {
+  if (t0 < NPT) {
     const int el = t0 / NP, pt = t0 % NP, a = pt / N, b = pt % N;
     double gx[NW], gy[NW];
-    if constexpr (VISC)
-      gradient_at<P, KIND>(op, sW + el * NP * NW, sG + el * 20, sCG + el * 8 * N * NW, a, b, gx, gy);
+    if constexpr (VISC) gradient_at<P, KIND>(op, sW, sG + el * 20, sCG, el, a, b, gx, gy);
     const Metric mt = metric(sG + el * 20);
-    point_fluxes<P, KIND>(sQ + t0 * NV, gx, gy, ph, mt, op.xg[a], op.xg[b], sFT + t0 * NV, sGT + t0 * NV);
+    double qq[NV], Ft[NV], Gt[NV];
+    gather_point<NV, NPT>(sQ, t0, qq);
+    point_fluxes<P, KIND>(qq, gx, gy, ph, mt, op.xg[a], op.xg[b], Ft, Gt);
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      sFT[v * NPT + t0] = Ft[v];
+      sGT[v * NPT + t0] = Gt[v];
+    }
   }
   __syncthreads();
   for (int t = threadIdx.x; t < E * NF; t += blockDim.x) {
     const int el = t / NF, r = t % NF, f = r / N, k = r % N;
     if (e0 + el >= M) continue;
-    flux_corrections<P, KIND>(op, sFT + el * NP * NV, sGT + el * NP * NV, sG + el * 20,
-                              sFC + ((el * 4 + f) * N + k) * NV, sCF + el * 4 * N * NV, f, k);
+    double Fc[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) Fc[v] = sFC[v * NFT + t];
+    flux_corrections<P, KIND>(op, sFT, sGT, sG + el * 20, Fc, sCF, el, f, k);
   }
   __syncthreads();
-  if (t0 < E * NP) {
+  if (t0 < NPT) {
     const int el = t0 / NP, pt = t0 % NP;
     const int64_t e = e0 + el;
     if (e < M) {
       const Metric mt = metric(sG + el * 20);
       double R[NV];
-      divergence_at<P, KIND>(op, sFT + el * NP * NV, sGT + el * NP * NV, sCF + el * 4 * N * NV, mt,
-                             pt / N, pt % N, R);
+      divergence_at<P, KIND>(op, sFT, sGT, sCF, mt, el, pt / N, pt % N, R);
       const int64_t base = (e * NP + pt) * NV;
+      double o[NV];
 #pragma unroll
-      for (int v = 0; v < NV; ++v) out[base + v] = epi_apply(ep, base + v, R[v], sQ[t0 * NV + v]);
+      for (int v = 0; v < NV; ++v) o[v] = epi_apply(ep, base + v, R[v], sQ[v * NPT + t0]);
+      st_face<NV>(out + base, o);
     }
   }
 }
@@ -765,12 +838,12 @@ k_assemble(const FrConst C, const FrMesh m, const double* __restrict__ q, const 
 // ---------------------------------------------------------------------------
 // element-local residual with frozen neighbour data (spatial.py:768-853)
 //
-// Slot s of the CTA holds one (element, state) instance in sQ[s]; the
+// Slot s of the CTA holds one (element, state) instance in the Q planes;
 // neighbours enter only through the frozen traces qtr and one-sided
 // viscous fluxes fvn of the linearisation state.  Fluxes are evaluated on
 // the element's own normal (the reference's local path).  Leaves the
-// local residual of point thread t in R (valid when t < E*NP and the
-// slot is live).
+// local residual of point thread t in R (valid when t < NPT and the slot
+// is live).
 
 template <int P, int KIND>
 __device__ __forceinline__ void local_pipeline(const FrConst& C, const FrMesh& m, const Ops& op, double* sm,
@@ -778,7 +851,7 @@ __device__ __forceinline__ void local_pipeline(const FrConst& C, const FrMesh& m
                                                const double* __restrict__ fvn, double* R) {
   using L = SL<P, KIND>;
   constexpr int N = BC<P>::N, NP = BC<P>::NP, NF = BC<P>::NF, E = BC<P>::EPB;
-  constexpr int NV = KT<KIND>::NV, NW = KT<KIND>::NW;
+  constexpr int NV = KT<KIND>::NV, NW = KT<KIND>::NW, NPT = L::NPT, NFT = L::NFT;
   constexpr bool VISC = KT<KIND>::VISC;
   double* sQ = sm + L::Q;
   double* sG = sm + L::G;
@@ -794,7 +867,13 @@ __device__ __forceinline__ void local_pipeline(const FrConst& C, const FrMesh& m
   const Phys ph = phys_of(C);
   const int t0 = threadIdx.x;
   if constexpr (VISC) {
-    if (t0 < E * NP) grad_vars<KIND>(sQ + t0 * NV, ph.gamma, sW + t0 * NW);
+    if (t0 < NPT) {
+      double qq[NV], w[NW];
+      gather_point<NV, NPT>(sQ, t0, qq);
+      grad_vars<KIND>(qq, ph.gamma, w);
+#pragma unroll
+      for (int c = 0; c < NW; ++c) sW[c * NPT + t0] = w[c];
+    }
   }
   for (int t = threadIdx.x; t < E * NF; t += blockDim.x) {
     const int el = t / NF, r = t % NF, f = r / N, k = r % N;
@@ -803,33 +882,27 @@ __device__ __forceinline__ void local_pipeline(const FrConst& C, const FrMesh& m
     const int2 lk = m.link[e * 4 + f];
     const double* gq = sG + el * 20;
     const double nx = gq[8 + 2 * f], ny = gq[9 + 2 * f];
-    const double* Qe = sQ + el * NP * NV;
     double tr[NV], nb[NV], F[NV];
 #pragma unroll
-    for (int v = 0; v < NV; ++v) tr[v] = line_sum<N, NV>(op, Qe, f, k, v);
+    for (int v = 0; v < NV; ++v) tr[v] = line_sum<N>(op, sQ + v * NPT + el * NP, f, k);
     if (lk.x >= 0) {
       const int kk = lk_rev(lk.y) ? N - 1 - k : k;
-      const double* ns = qtr + (((int64_t)lk.x * 4 + lk_face(lk.y)) * N + kk) * NV;
-#pragma unroll
-      for (int v = 0; v < NV; ++v) nb[v] = __ldg(ns + v);
+      ld_face<NV>(qtr + (((int64_t)lk.x * 4 + lk_face(lk.y)) * N + kk) * NV, nb);
     } else {
       ghost<KIND>(tr, lk_tag(lk.y), nx, ny, C.qinf, nb);
     }
     num_flux<KIND>(tr, nb, nx, ny, ph, F);
-    double* fc = sFC + ((el * 4 + f) * N + k) * NV;
-    double* st = sTR + ((el * 4 + f) * N + k) * NV;
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
-      fc[v] = F[v];
-      st[v] = tr[v];
+      sFC[v * NFT + t] = F[v];
+      sTR[v * NFT + t] = tr[v];
     }
     if constexpr (VISC) {
       double wa[NW], wc[NW];
       grad_vars<KIND>(tr, ph.gamma, wa);
       grad_vars<KIND>(nb, ph.gamma, wc);
-      double* wh = sWH + ((el * 4 + f) * N + k) * NW;
 #pragma unroll
-      for (int c = 0; c < NW; ++c) wh[c] = 0.5 * (wa[c] + wc[c]);
+      for (int c = 0; c < NW; ++c) sWH[c * NFT + t] = 0.5 * (wa[c] + wc[c]);
     }
   }
   __syncthreads();
@@ -837,40 +910,49 @@ __device__ __forceinline__ void local_pipeline(const FrConst& C, const FrMesh& m
     for (int t = threadIdx.x; t < E * NF; t += blockDim.x) {
       const int el = t / NF, r = t % NF, f = r / N, k = r % N;
       if (slot_elem[el] < 0) continue;
-      grad_corrections<P, KIND>(op, sW + el * NP * NW, sG + el * 20, sWH + el * 4 * N * NW,
-                                sCG + el * 8 * N * NW, f, k);
+      grad_corrections<P, KIND>(op, sW, sG + el * 20, sWH, sCG, el, f, k);
     }
     __syncthreads();
   }
-  if (t0 < E * NP) {
+  if (t0 < NPT) {
     const int el = t0 / NP, pt = t0 % NP, a = pt / N, b = pt % N;
     double gx[NW], gy[NW];
     if constexpr (VISC) {
-      gradient_at<P, KIND>(op, sW + el * NP * NW, sG + el * 20, sCG + el * 8 * N * NW, a, b, gx, gy);
+      gradient_at<P, KIND>(op, sW, sG + el * 20, sCG, el, a, b, gx, gy);
 #pragma unroll
       for (int c = 0; c < NW; ++c) {
-        sGR[(t0 * 2 + 0) * NW + c] = gx[c];
-        sGR[(t0 * 2 + 1) * NW + c] = gy[c];
+        sGR[c * NPT + t0] = gx[c];
+        sGR[(NW + c) * NPT + t0] = gy[c];
       }
     }
     const Metric mt = metric(sG + el * 20);
-    point_fluxes<P, KIND>(sQ + t0 * NV, gx, gy, ph, mt, op.xg[a], op.xg[b], sFT + t0 * NV, sGT + t0 * NV);
+    double qq[NV], Ft[NV], Gt[NV];
+    gather_point<NV, NPT>(sQ, t0, qq);
+    point_fluxes<P, KIND>(qq, gx, gy, ph, mt, op.xg[a], op.xg[b], Ft, Gt);
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      sFT[v * NPT + t0] = Ft[v];
+      sGT[v * NPT + t0] = Gt[v];
+    }
   }
   __syncthreads();
   for (int t = threadIdx.x; t < E * NF; t += blockDim.x) {
     const int el = t / NF, r = t % NF, f = r / N, k = r % N;
     const int64_t e = slot_elem[el];
     if (e < 0) continue;
-    double* fc = sFC + ((el * 4 + f) * N + k) * NV;
+    double Fc[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) Fc[v] = sFC[v * NFT + t];
     if constexpr (VISC) {
-      const double* GRe = sGR + el * NP * 2 * NW;
       double gx[NW], gy[NW];
 #pragma unroll
       for (int c = 0; c < NW; ++c) {
-        gx[c] = line_sum<N, 2 * NW>(op, GRe, f, k, c);
-        gy[c] = line_sum<N, 2 * NW>(op, GRe, f, k, NW + c);
+        gx[c] = line_sum<N>(op, sGR + c * NPT + el * NP, f, k);
+        gy[c] = line_sum<N>(op, sGR + (NW + c) * NPT + el * NP, f, k);
       }
-      const double* tr = sTR + ((el * 4 + f) * N + k) * NV;
+      double tr[NV];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) tr[v] = sTR[v * NFT + t];
       double fx[NV], fy[NV];
       visc_flux<KIND>(tr, gx, gy, ph, fx, fy);
       const double nx = sG[el * 20 + 8 + 2 * f], ny = sG[el * 20 + 9 + 2 * f];
@@ -880,32 +962,33 @@ __device__ __forceinline__ void local_pipeline(const FrConst& C, const FrMesh& m
       for (int v = 0; v < NV; ++v) Fv[v] = fx[v] * nx + fy[v] * ny;
       if (lk.x >= 0) {
         const int kk = lk_rev(lk.y) ? N - 1 - k : k;
-        const double* ns = fvn + (((int64_t)lk.x * 4 + lk_face(lk.y)) * N + kk) * NV;
+        double Fn[NV];
+        ld_face<NV>(fvn + (((int64_t)lk.x * 4 + lk_face(lk.y)) * N + kk) * NV, Fn);
 #pragma unroll
-        for (int v = 0; v < NV; ++v) Fv[v] = 0.5 * (Fv[v] + (-__ldg(ns + v)));
+        for (int v = 0; v < NV; ++v) Fv[v] = 0.5 * (Fv[v] + (-Fn[v]));
       } else if (KT<KIND>::FLOW && lk_tag(lk.y) == T_WALL_ADIABATIC) {
         Fv[NV - 1] = 0.0;
       }
 #pragma unroll
-      for (int v = 0; v < NV; ++v) fc[v] = fc[v] - Fv[v];
+      for (int v = 0; v < NV; ++v) Fc[v] = Fc[v] - Fv[v];
     }
-    flux_corrections<P, KIND>(op, sFT + el * NP * NV, sGT + el * NP * NV, sG + el * 20, fc,
-                              sCF + el * 4 * N * NV, f, k);
+    // CF aliases CG, whose last readers (gradient_at) finished before the
+    // previous barrier
+    flux_corrections<P, KIND>(op, sFT, sGT, sG + el * 20, Fc, sCF, el, f, k);
   }
   __syncthreads();
-  if (t0 < E * NP) {
+  if (t0 < NPT) {
     const int el = t0 / NP, pt = t0 % NP;
     if (slot_elem[el] >= 0) {
       const Metric mt = metric(sG + el * 20);
-      divergence_at<P, KIND>(op, sFT + el * NP * NV, sGT + el * NP * NV, sCF + el * 4 * N * NV, mt,
-                             pt / N, pt % N, R);
+      divergence_at<P, KIND>(op, sFT, sGT, sCF, mt, el, pt / N, pt % N, R);
     }
   }
 }
 
 // batched element-local residual: instance b = (elems[b], Q[b])
 template <int P, int KIND>
-__global__ void __launch_bounds__(BC<P>::THREADS)
+__global__ void __launch_bounds__(BC<P>::THREADS, MinBlocks<P>::ASM)
 k_local(const FrConst C, const FrMesh m, const int64_t* __restrict__ elems, int64_t B,
         const double* __restrict__ Q, const double* __restrict__ qtr, const double* __restrict__ fvn,
         double* __restrict__ out) {
@@ -937,12 +1020,12 @@ k_local(const FrConst C, const FrMesh m, const int64_t* __restrict__ elems, int6
 // slots; column c perturbs local DoF c-1 by +eps (newton_krylov.py:174-184).
 // Writes B^T (column-major block) so each column is a contiguous store.
 template <int P, int KIND>
-__global__ void __launch_bounds__(BC<P>::THREADS)
+__global__ void __launch_bounds__(BC<P>::THREADS, MinBlocks<P>::ASM)
 k_blocks(const FrConst C, const FrMesh m, const double* __restrict__ q, const double* __restrict__ qtr,
          const double* __restrict__ fvn, double shift, double eps, double* __restrict__ BT) {
   extern __shared__ double sm[];
   using L = SL<P, KIND>;
-  constexpr int NP = BC<P>::NP, E = BC<P>::EPB, NV = KT<KIND>::NV;
+  constexpr int NP = BC<P>::NP, E = BC<P>::EPB, NV = KT<KIND>::NV, NPT = L::NPT;
   constexpr int SZ = NP * NV;
   __shared__ int64_t slot[E];
   const Ops op = stage_ops(C, sm);
@@ -952,15 +1035,15 @@ k_blocks(const FrConst C, const FrMesh m, const double* __restrict__ q, const do
   const double* qe = q + e * SZ;
   const int t0 = threadIdx.x;
   double* BTe = BT + e * (int64_t)SZ * SZ;
+  for (int i = threadIdx.x; i < E * 20; i += blockDim.x) sm[L::G + i] = __ldg(m.geom + e * 20 + i % 20);
   for (int c0 = 0; c0 <= SZ; c0 += E) {
     __syncthreads();
     for (int s = threadIdx.x; s < E; s += blockDim.x) slot[s] = (c0 + s <= SZ) ? e : -1;
     for (int i = threadIdx.x; i < E * SZ; i += blockDim.x) {
       const int s = i / SZ, d = i % SZ, c = c0 + s;
       const double v = __ldg(qe + d);
-      sQ[i] = (c >= 1 && d == c - 1) ? v + eps : v;
+      sQ[(d % NV) * NPT + s * NP + d / NV] = (c >= 1 && d == c - 1) ? v + eps : v;
     }
-    for (int i = threadIdx.x; i < E * 20; i += blockDim.x) sm[L::G + i] = __ldg(m.geom + e * 20 + i % 20);
     __syncthreads();
     double R[NV];
     local_pipeline<P, KIND>(C, m, op, sm, slot, qtr, fvn, R);
@@ -970,7 +1053,7 @@ k_blocks(const FrConst C, const FrMesh m, const double* __restrict__ q, const do
       for (int v = 0; v < NV; ++v) sR0[pt * NV + v] = R[v];
     }
     __syncthreads();
-    if (t0 < E * NP && c >= 1 && c <= SZ) {
+    if (t0 < NPT && c >= 1 && c <= SZ) {
       double* col = BTe + (int64_t)(c - 1) * SZ;
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
@@ -996,9 +1079,9 @@ static int run_residual(const DiscDev& d, const double* q, const double* X, doub
   constexpr int E = BC<P>::EPB, TH = BC<P>::THREADS;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_trace<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES);
-    cudaFuncSetAttribute(k_fvn<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES);
-    cudaFuncSetAttribute(k_assemble<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES);
+    cudaFuncSetAttribute(k_trace<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES_TRACE);
+    cudaFuncSetAttribute(k_fvn<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES_FVN);
+    cudaFuncSetAttribute(k_assemble<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES_ASM);
     attr = true;
   }
   int* bad = nullptr;
@@ -1008,9 +1091,9 @@ static int run_residual(const DiscDev& d, const double* q, const double* X, doub
   const unsigned grid = (unsigned)((d.M + E - 1) / E);
   const double* qq = q;
   if (X != nullptr) qq = d.qp;
-  k_trace<P, KIND><<<grid, TH, L::BYTES, st>>>(d.C, d.mesh, q, X, eps, d.qp, d.qtr, bad);
-  if (KT<KIND>::VISC) k_fvn<P, KIND><<<grid, TH, L::BYTES, st>>>(d.C, d.mesh, qq, d.qtr, d.fvn);
-  k_assemble<P, KIND><<<grid, TH, L::BYTES, st>>>(d.C, d.mesh, qq, d.qtr, d.fvn, epi, out, bad, stp);
+  k_trace<P, KIND><<<grid, TH, L::BYTES_TRACE, st>>>(d.C, d.mesh, q, X, eps, d.qp, d.qtr, bad);
+  if (KT<KIND>::VISC) k_fvn<P, KIND><<<grid, TH, L::BYTES_FVN, st>>>(d.C, d.mesh, qq, d.qtr, d.fvn);
+  k_assemble<P, KIND><<<grid, TH, L::BYTES_ASM, st>>>(d.C, d.mesh, qq, d.qtr, d.fvn, epi, out, bad, stp);
   return (int)cudaGetLastError();
 }
 
@@ -1020,13 +1103,13 @@ static int run_freeze(const DiscDev& d, const double* q, double* qtr, double* fv
   constexpr int E = BC<P>::EPB, TH = BC<P>::THREADS;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_trace<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES);
-    cudaFuncSetAttribute(k_fvn<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES);
+    cudaFuncSetAttribute(k_trace<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES_TRACE);
+    cudaFuncSetAttribute(k_fvn<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES_FVN);
     attr = true;
   }
   const unsigned grid = (unsigned)((d.M + E - 1) / E);
-  k_trace<P, KIND><<<grid, TH, L::BYTES, st>>>(d.C, d.mesh, q, nullptr, 0.0, nullptr, qtr, nullptr);
-  if (KT<KIND>::VISC) k_fvn<P, KIND><<<grid, TH, L::BYTES, st>>>(d.C, d.mesh, q, qtr, fvn);
+  k_trace<P, KIND><<<grid, TH, L::BYTES_TRACE, st>>>(d.C, d.mesh, q, nullptr, 0.0, nullptr, qtr, nullptr);
+  if (KT<KIND>::VISC) k_fvn<P, KIND><<<grid, TH, L::BYTES_FVN, st>>>(d.C, d.mesh, q, qtr, fvn);
   return (int)cudaGetLastError();
 }
 
@@ -1037,12 +1120,12 @@ static int run_local(const DiscDev& d, const int64_t* elems, int64_t B, const do
   constexpr int E = BC<P>::EPB, TH = BC<P>::THREADS;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_local<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES);
+    cudaFuncSetAttribute(k_local<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES_LOCAL);
     attr = true;
   }
   if (B <= 0) return 0;
   const unsigned grid = (unsigned)((B + E - 1) / E);
-  k_local<P, KIND><<<grid, TH, L::BYTES, st>>>(d.C, d.mesh, elems, B, Q, qtr, fvn, out);
+  k_local<P, KIND><<<grid, TH, L::BYTES_LOCAL, st>>>(d.C, d.mesh, elems, B, Q, qtr, fvn, out);
   return (int)cudaGetLastError();
 }
 
@@ -1053,11 +1136,11 @@ static int run_blocks(const DiscDev& d, const double* q, const double* qtr, cons
   constexpr int TH = BC<P>::THREADS;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_blocks<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES);
+    cudaFuncSetAttribute(k_blocks<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES_LOCAL);
     attr = true;
   }
   if (d.M <= 0) return 0;
-  k_blocks<P, KIND><<<(unsigned)d.M, TH, L::BYTES, st>>>(d.C, d.mesh, q, qtr, fvn, shift, eps, BT);
+  k_blocks<P, KIND><<<(unsigned)d.M, TH, L::BYTES_LOCAL, st>>>(d.C, d.mesh, q, qtr, fvn, shift, eps, BT);
   return (int)cudaGetLastError();
 }
 

@@ -1,0 +1,239 @@
+"""Implicit ESDIRK / Rosenbrock steppers on device vectors.
+
+Drop-in for pmgflow.time_integration
+(``/root/reference/pkg/src/pmgflow/time_integration.py``): the same
+schemes (esdirk2, esdirk4, row2, row4 -- the published tableaux,
+:45-106), ``StageProblem`` / ``stage_function`` (:117-141),
+``esdirk_step`` (:144-168) and ``row_step`` (:171-197).  The stage
+algebra runs as fused device linear combinations and the stage function
+F(q) = (q - explicit)/(a_ii dt) - R(q) is one fused residual epilogue;
+``StageFunction.fused_jv`` gives ptc_solve the fused PTC matvec.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .vec import lincomb, to_device
+
+
+@dataclass(frozen=True)
+class StageScheme:
+    name: str
+    kind: str
+    order: int
+    a: np.ndarray
+    b: np.ndarray
+    c: np.ndarray
+    cmat: np.ndarray | None = None
+    gamma: float = 0.0
+
+    @property
+    def stages(self) -> int:
+        return len(self.b)
+
+    @property
+    def diagonal(self) -> float:
+        return self.gamma if self.kind == "row" else float(self.a[-1, -1])
+
+
+def _lower(rows, s):
+    a = np.zeros((s, s))
+    for i, r in enumerate(rows):
+        a[i, :len(r)] = r
+    return a
+
+
+def _esdirk2():
+    g = (2.0 - np.sqrt(2.0)) / 2.0
+    a = _lower([[0.0], [g, g], [(1 - g) / 2, (1 - g) / 2, g]], 3)
+    return StageScheme("esdirk2", "esdirk", 2, a, a[-1].copy(), a.sum(axis=1))
+
+
+def _esdirk4():
+    # Kennedy & Carpenter ESDIRK4(3)6L[2]SA, gamma = 1/4 (stiffly accurate)
+    g = 0.25
+    a = _lower([
+        [0.0],
+        [g, g],
+        [8611 / 62500, -1743 / 31250, g],
+        [5012029 / 34652500, -654441 / 2922500, 174375 / 388108, g],
+        [15267082809 / 155376265600, -71443401 / 120774400, 730878875 / 902184768, 2285395 / 8070912, g],
+        [82889 / 524892, 0.0, 15625 / 83664, 69875 / 102672, -2260 / 8211, g],
+    ], 6)
+    return StageScheme("esdirk4", "esdirk", 4, a, a[-1].copy(), a.sum(axis=1))
+
+
+def _row2():
+    g = 1.0 + 1.0 / np.sqrt(2.0)
+    a = _lower([[], [1.0 / g]], 2)
+    cm = _lower([[], [-2.0 / g]], 2)
+    m = np.array([3.0 / (2.0 * g), 1.0 / (2.0 * g)])
+    return StageScheme("row2", "row", 2, a, m, a.sum(axis=1), cm, g)
+
+
+def _row4():
+    # RODASP (six stages, stiffly accurate, gamma = 1/4), K-variable form
+    m4 = [1.221224509226641, 6.019134481288629, 12.53708332932087, -0.6878860361058950]
+    a = _lower([
+        [],
+        [1.544],
+        [0.9466785280815826, 0.2557011698983284],
+        [3.314825187068521, 2.896124015972201, 0.9986419139977817],
+        m4,
+        m4 + [1.0],
+    ], 6)
+    cm = _lower([
+        [],
+        [-5.6688],
+        [-2.430093356833875, -0.2063599157091915],
+        [-0.1073529058151375, -9.594562251023355, -20.47028614809616],
+        [7.496443313967647, -10.24680431464352, -33.99990352819905, 11.70890893206160],
+        [8.083246795921522, -7.981132988064893, -31.52159432874371, 16.31930543123136, -6.058818238834054],
+    ], 6)
+    m = np.array(m4 + [1.0, 1.0])
+    alpha = np.array([0.0, 0.386, 0.210, 0.630, 1.0, 1.0])
+    return StageScheme("row4", "row", 4, a, m, alpha, cm, 0.25)
+
+
+_SCHEMES = {"esdirk2": _esdirk2, "esdirk4": _esdirk4, "row2": _row2, "row4": _row4}
+
+
+def get_scheme(name: str) -> StageScheme:
+    try:
+        return _SCHEMES[name]()
+    except KeyError:
+        raise ValueError(f"unknown scheme {name!r}; available: {sorted(_SCHEMES)}") from None
+
+
+@dataclass
+class StageProblem:
+    residual: object
+    a_ii: float = 1.0
+    dt: float = np.inf
+    explicit: object = None
+    steady: bool = False
+
+    @property
+    def shift(self) -> float:
+        return 0.0 if self.steady else 1.0 / (self.a_ii * self.dt)
+
+
+def _disc_of(residual):
+    from .newton_krylov import _device_disc
+    return _device_disc(residual)
+
+
+class StageFunction:
+    """F(q) for a StageProblem; fused on the device when the problem's
+    residual is a device Discretization.residual."""
+
+    def __init__(self, prob: StageProblem, check_status: bool = False):
+        self.prob = prob
+        self.disc = _disc_of(prob.residual)
+        self.check_status = check_status
+        if not prob.steady and prob.explicit is not None:
+            self.E = to_device(prob.explicit)
+        else:
+            self.E = None
+        self.adt = prob.a_ii * prob.dt
+
+    def __call__(self, q):
+        q = to_device(q)
+        p = self.prob
+        if self.disc is not None:
+            if p.steady:
+                return self.disc.eval(q, _lib.EPI_NEG_R, check_status=self.check_status)
+            return self.disc.eval(q, _lib.EPI_STAGE_F, E=self.E, adt=self.adt, check_status=self.check_status)
+        R = to_device(p.residual(q))
+        if p.steady:
+            return lincomb((-1.0,), (R,))
+        return lincomb((1.0 / self.adt, -1.0 / self.adt, -1.0), (q, self.E, R))
+
+    def fused_jv(self, X, q, Fk, dtau, eps):
+        """X/dtau + (F(q + eps X) - Fk)/eps as one residual evaluation."""
+        if self.disc is None:
+            Fp = self(lincomb((1.0, eps), (q, X)))
+            return lincomb((1.0 / dtau, 1.0 / eps, -1.0 / eps), (X, Fp, Fk))
+        if self.prob.steady:
+            return self.disc.eval(q, _lib.EPI_STAGE_JV, X=X, eps=eps, E=q, adt=np.inf, dtau=dtau, R0=Fk)
+        return self.disc.eval(q, _lib.EPI_STAGE_JV, X=X, eps=eps, E=self.E, adt=self.adt, dtau=dtau, R0=Fk)
+
+
+def stage_function(q, prob: StageProblem):
+    return StageFunction(prob, check_status=True)(q)
+
+
+def _sum_terms(base, coeffs, vecs):
+    """base + sum c_j v_j in fused chunks of <= 8 vectors."""
+    out = base
+    terms = [(c, v) for c, v in zip(coeffs, vecs) if c != 0.0]
+    while terms:
+        chunk, terms = terms[:7], terms[7:]
+        out = lincomb([1.0] + [c for c, _ in chunk], [out] + [v for _, v in chunk])
+    return out if out is not base else base.clone()
+
+
+def esdirk_step(q, dt: float, scheme: StageScheme, residual, solve_stage):
+    """One ESDIRK step (time_integration.py:144-168)."""
+    if scheme.kind != "esdirk":
+        raise ValueError("scheme is not an ESDIRK tableau")
+    q = to_device(q)
+    s = scheme.stages
+    stage_R = [to_device(residual(q))]
+    stage_info = []
+    qi = q
+    for i in range(1, s):
+        explicit = _sum_terms(q, [dt * scheme.a[i, j] for j in range(i)], stage_R)
+        prob = StageProblem(residual, float(scheme.a[i, i]), dt, explicit)
+        qi, info = solve_stage(prob, qi)
+        stage_info.append(info)
+        if not info.get("converged", True):
+            raise RuntimeError(f"stage {i + 1} nonlinear solve did not converge: {info}")
+        stage_R.append(to_device(residual(qi)))
+    q_new = _sum_terms(q, [dt * scheme.b[j] for j in range(s)], stage_R)
+    return q_new, stage_info
+
+
+def row_step(q, dt: float, scheme: StageScheme, residual, solve_linear):
+    """One Rosenbrock step (time_integration.py:171-197)."""
+    if scheme.kind != "row":
+        raise ValueError("scheme is not a Rosenbrock tableau")
+    q = to_device(q)
+    s = scheme.stages
+    sigma = 1.0 / (scheme.gamma * dt)
+    K = []
+    stage_info = []
+    for i in range(s):
+        y = _sum_terms(q, [scheme.a[i, j] for j in range(i)], K) if i else q
+        rhs = to_device(residual(y))
+        if i:
+            rhs = _sum_terms(rhs, [scheme.cmat[i, j] / dt for j in range(i)], K)
+        Ki, info = solve_linear(rhs, sigma, i)
+        stage_info.append(info)
+        if not info.get("converged", True):
+            raise RuntimeError(f"stage {i + 1} linear solve did not converge: {info}")
+        K.append(to_device(Ki))
+    q_new = _sum_terms(q, list(scheme.b), K)
+    return q_new, stage_info
+
+
+def stability_function(scheme: StageScheme, z: complex) -> complex:
+    """Amplification factor on dq/dt = lambda q via the stage algebra."""
+    if scheme.kind == "esdirk":
+        qs = [1.0 + 0j]
+        for i in range(1, scheme.stages):
+            explicit = 1.0 + sum(scheme.a[i, j] * z * qs[j] for j in range(i))
+            qs.append(explicit / (1.0 - scheme.a[i, i] * z))
+        return 1.0 + sum(scheme.b[j] * z * qs[j] for j in range(scheme.stages))
+    denom = 1.0 / scheme.gamma - z
+    K = []
+    for i in range(scheme.stages):
+        y = 1.0 + sum(scheme.a[i, j] * K[j] for j in range(i))
+        rhs = z * y + sum(scheme.cmat[i, j] * K[j] for j in range(i))
+        K.append(rhs / denom)
+    return 1.0 + sum(scheme.b[j] * K[j] for j in range(scheme.stages))

@@ -18,7 +18,7 @@ for mode, name in ((_lib.EPI_R, "R"), (_lib.EPI_JV, "Jv")):
         d.eval(q, mode, out, X=X, eps=1e-6, s=1.0, R0=R)
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    reps = 50
+    reps = int(sys.argv[2]) if len(sys.argv) > 2 else 50
     ev0.record()
     for _ in range(reps):
         d.eval(q, mode, out, X=X, eps=1e-6, s=1.0, R0=R)
