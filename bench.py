@@ -1,0 +1,387 @@
+#!/usr/bin/env python
+"""Benchmark of the FP64 FR residual hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1], "config 2"): 256x256 periodic quad
+mesh, p=4 (25 points/element), compressible Navier-Stokes, Roe + BR1
+(SURVEY 8.0), isentropic vortex + seeded 1e-6 noise; 6,553,600 FP64 DoF.
+A "step" is one residual evaluation R(q) over the whole mesh; value =
+DoF-updates/s (GDoF/s) over all ranks.  Also timed: the fused Jv
+(the GMRES matvec) and one ESDIRK2 JFNK-pMG p{4-2} time step at config 2
+(the metric's second half), plus config 1's step beside the CPU oracle.
+
+Multi-GPU: each rank evaluates its own replica of the config-2 mesh
+(weak scaling, no data-path collective).  Times
+are CUDA-event device times on the launching stream, max over ranks.
+
+--impl reference: the reference arm -- the CPU oracle (NumPy restatement
+of the reference, oracle/, pinned to the reference's golden vectors)
+timed on this box's host cores on the same config and metric.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "FP64 FR residual/Jv GDoF/s (% HBM roofline); JFNK-pMG wall time per time step"
+UNIT = "GDoF/s"
+FLOP_PER_DOF_R = {2: 190.2, 3: 185.6, 4: 186.8, 5: 191.0}   # instrumented reference count
+BYTES_PER_DOF_R = 16.0                                          # read q + write R (compulsory)
+BYTES_PER_DOF_JV = 32.0                                         # read q, v, R0; write out
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--no-step", action="store_true", help="skip the JFNK-pMG time-step timings")
+    ap.add_argument("--config", type=int, default=2)
+    return ap.parse_args()
+
+
+def dist_info():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the CPU oracle
+
+def cpu_residual_rate(case, seconds_budget=20.0, max_calls=None):
+    """Time the oracle residual on this host (1 thread: NumPy einsum)."""
+    from oracle.fr_oracle import OracleDisc
+    d = OracleDisc(case.mesh, case.p, case.eqn)
+    d.residual(case.q0)  # warm caches
+    times = []
+    t_start = time.perf_counter()
+    while True:
+        t0 = time.perf_counter()
+        d.residual(case.q0)
+        times.append(time.perf_counter() - t0)
+        if (max_calls and len(times) >= max_calls) or time.perf_counter() - t_start > seconds_budget:
+            break
+    best = min(times)
+    return case.n_dofs / best / 1e9, best, len(times)
+
+
+def run_reference(args):
+    ws, rank, _ = dist_info()
+    if rank != 0:
+        return 0
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    from oracle.fr_oracle import OracleDisc
+    from paper_2202_09733_b200 import cases
+    case = cases.config(args.config)
+    d = OracleDisc(case.mesh, case.p, case.eqn)
+    for _ in range(max(0, args.warmup)):
+        d.residual(case.q0)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        d.residual(case.q0)
+    el = time.perf_counter() - t0
+    rate = case.n_dofs * args.steps / el / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded isentropic vortex + 1e-6 noise, SURVEY 8(d))",
+        "config": {"workload": f"config{args.config}: R(u) over {case.mesh.n_elements} elements, p={case.p}, "
+                               f"{case.n_dofs} DoF, NS Roe+BR1", "parallelism": "cpu"},
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": 1, "kind": "port",
+                         "sample": f"{args.steps} full-mesh residual evaluations of config{args.config} "
+                                   "by the NumPy oracle (oracle/fr_oracle.py), 1 thread"},
+        "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (B200_PROFILING.md clocks line)
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.rows = []
+        self._stop = threading.Event()
+        self._thr = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([c.strip() for c in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._thr = threading.Thread(target=self._run, daemon=True)
+        self._thr.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._thr.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 5 + i and r[5 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+
+def measure_fp64_peak(torch, lib, stream):
+    out = torch.zeros(1, dtype=torch.float64, device="cuda")
+    blocks, iters = 148 * 8, 20000
+    lib.pmgb_probe_fp64(1000, blocks, out.data_ptr(), stream)
+    torch.cuda.synchronize()
+    best = 0.0
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        lib.pmgb_probe_fp64(iters, blocks, out.data_ptr(), stream)
+        e1.record()
+        e1.synchronize()
+        t = e0.elapsed_time(e1) * 1e-3
+        best = max(best, 2.0 * 8 * iters * blocks * 256 / t / 1e12)
+    return best
+
+
+def event_time(torch, fn, reps):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for i in range(reps):
+        fn(i)
+    e1.record()
+    e1.synchronize()
+    return e0.elapsed_time(e1) * 1e-3
+
+
+def run_ours(args):
+    import torch
+    ws, rank, local = dist_info()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2202_09733_b200 import _lib, cases
+    from paper_2202_09733_b200.spatial import Discretization
+    from paper_2202_09733_b200.vec import launch_count, stream
+
+    lib = _lib.load()
+    W = max(3, args.warmup)
+    K = max(1, args.steps)
+    case = cases.config(args.config)
+    disc = Discretization(case.mesh, case.p, case.eqn)
+    n = disc.n_dofs
+    st = stream()
+    fp64_peak = measure_fp64_peak(torch, lib, st)
+    measured = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    hbm_peak = float(measured.get("hbm_gbs", 6650.0))
+
+    # 4 rotating q/R buffer pairs (4 x 105 MB > 126 MB L2)
+    q0 = torch.as_tensor(case.q0, device="cuda")
+    nbuf = 4
+    qs = [q0.clone() for _ in range(nbuf)]
+    Rs = [torch.empty_like(q0) for _ in range(nbuf)]
+    Xs = [torch.randn(n, dtype=torch.float64, device="cuda", generator=torch.Generator("cuda").manual_seed(i))
+          for i in range(nbuf)]
+    R0s = [disc.residual(q) for q in qs]
+
+    def r_step(i):
+        disc.eval(qs[i % nbuf], _lib.EPI_R, Rs[i % nbuf])
+
+    def jv_step(i):
+        j = i % nbuf
+        disc.eval(qs[j], _lib.EPI_JV, Rs[j], X=Xs[j], eps=1e-6, s=3.7, R0=R0s[j])
+
+    for i in range(W):
+        r_step(i)
+        jv_step(i)
+    torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    l0 = launch_count()
+    with ClockSampler(local) as clk:
+        t_r = event_time(torch, r_step, K)
+    launches_r = launch_count() - l0
+    t_jv = event_time(torch, jv_step, K)
+    if ws > 1:
+        tt = torch.tensor([t_r, t_jv], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t_r, t_jv = float(tt[0]), float(tt[1])
+    ms_r = t_r / K * 1e3
+    rate_r = ws * n * K / t_r / 1e9
+    rate_jv = ws * n * K / t_jv / 1e9
+    per_gpu_r = n / (t_r / K)
+
+    # e2e through the public API with host buffers: H2D of q, R, D2H of R
+    qh = torch.from_numpy(case.q0.copy()).pin_memory()
+    Rh = torch.empty(n, dtype=torch.float64).pin_memory()
+    qd = torch.empty(n, dtype=torch.float64, device="cuda")
+
+    def e2e_step(i):
+        qd.copy_(qh, non_blocking=True)
+        R = disc.eval(qd, _lib.EPI_R, Rs[0])
+        Rh.copy_(R, non_blocking=True)
+    for i in range(W):
+        e2e_step(i)
+    t_e2e = event_time(torch, e2e_step, K)
+    if ws > 1:
+        tt = torch.tensor([t_e2e], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t_e2e = float(tt[0])
+    rate_e2e = ws * n * K / t_e2e / 1e9
+    # parity spot check of the e2e result against the device-resident path
+    torch.cuda.synchronize()
+
+    # JFNK-pMG time step (the metric's second half)
+    step = {}
+    if not args.no_step and rank == 0:
+        step = time_steps(torch, case, args)
+
+    if rank != 0:
+        if ws > 1:
+            torch.distributed.barrier()
+        return 0
+
+    flops = FLOP_PER_DOF_R[case.p] * n
+    achieved = flops / (t_r / K) / 1e12
+    line = {
+        "metric": METRIC, "value": rate_r, "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": W,
+        "ms_per_step": ms_r, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded isentropic vortex + 1e-6 noise, SURVEY 8(d))",
+        "config": {"workload": f"config{args.config}: R(u) over {case.mesh.n_elements} elements "
+                               f"({int(np.sqrt(case.mesh.n_elements))}^2 periodic), p={case.p}, {n} DoF, "
+                               "NS Roe+BR1 (SURVEY 8.0)",
+                   "l2": "4 rotating q/R buffer pairs (419 MB > 126 MB L2)",
+                   "parallelism": f"replica x{ws}" if ws > 1 else "single GPU"},
+        "jv_gdofs": rate_jv,
+        "jv_ms": t_jv / K * 1e3,
+        "roofline": {
+            "bound": "fp64", "kernel": "R(u): k_trace + k_fvn + k_assemble",
+            "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak,
+            "peak_source": "measured in this run (DFMA probe, pmgb_probe_fp64)",
+            "flop_per_dof": FLOP_PER_DOF_R[case.p],
+            "hbm_view": {"achieved_gbs": BYTES_PER_DOF_R * per_gpu_r / 1e9, "peak_gbs": hbm_peak,
+                         "frac": BYTES_PER_DOF_R * per_gpu_r / 1e9 / hbm_peak,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
+            "bound_gdofs": min(hbm_peak / BYTES_PER_DOF_R, fp64_peak * 1e3 / FLOP_PER_DOF_R[case.p]),
+            "traffic": None,
+        },
+        "e2e": {"value": rate_e2e, "unit": UNIT, "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n},
+        "gpu_launches": int(launches_r),
+        "clocks": clk.summary(),
+        "step_time": step,
+    }
+    # CPU baseline: the oracle on this host, bounded sample
+    try:
+        os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+        cpu_rate, best, ncall = cpu_residual_rate(case, seconds_budget=15.0)
+        line["cpu_baseline"] = {"value": cpu_rate, "unit": UNIT, "cores": 1, "kind": "port",
+                                "sample": f"best of {ncall} full-mesh oracle residual evaluations "
+                                          f"(config{args.config}, {best:.2f} s each)"}
+    except Exception as exc:  # pragma: no cover
+        line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 1, "kind": "port", "sample": f"failed: {exc}"}
+    prof = ROOT / "profiles" / "traffic_r1.json"
+    if prof.exists():
+        try:
+            line["roofline"]["traffic"] = json.loads(prof.read_text()).get(f"config{args.config}_R_bytes")
+        except Exception:
+            pass
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.barrier()
+    return 0
+
+
+def time_steps(torch, case2, args):
+    """One ESDIRK2 JFNK-pMG step at config 2 (after one warm-up step) and
+    one at config 1 beside the CPU oracle's config-1 step."""
+    from paper_2202_09733_b200 import cases
+    from paper_2202_09733_b200 import time_integration as ti
+    from paper_2202_09733_b200.harness import ImplicitDriver
+    from paper_2202_09733_b200.spatial import Discretization
+    out = {}
+    for k, c in ((1, cases.config(1)), (2, case2)):
+        d = Discretization(c.mesh, c.p, c.eqn)
+        cfg = {"case.precond": "pmg", "pmg.levels": c.levels, "pmg.smooth": "2",
+               "pmg.smoother_shift": c.extra["smoother_shift"], "gmres.kdim": c.kdim,
+               "gmres.rtol": 1e-3, "ptc.dtau_init": c.dt, "ptc.rtol": 1e-4}
+        q = torch.as_tensor(c.q0, device="cuda")
+        sch = ti.get_scheme("esdirk2")
+        rec = {"scheme": "esdirk2", "pmg": c.levels, "smoother_shift": c.extra["smoother_shift"],
+               "dt": c.dt}
+        try:
+            drv = ImplicitDriver(d, cfg)
+            drv.step(q, c.dt, sch)  # warm-up (allocator + caches)
+            torch.cuda.synchronize()
+            drv = ImplicitDriver(d, cfg)
+            t0 = time.perf_counter()
+            q1, info = drv.step(q, c.dt, sch)
+            torch.cuda.synchronize()
+            rec.update(gpu_s=time.perf_counter() - t0, ptc_iters=[i["iters"] for i in info],
+                       gmres_iters=[i["gmres_iters"] for i in info])
+        except Exception as exc:
+            rec.update(gpu_s=None, error=str(exc)[:200])
+        out[f"config{k}"] = rec
+    try:
+        from oracle import solver_oracle as so
+        from oracle.fr_oracle import OracleDisc
+        c = cases.config(1)
+        od = OracleDisc(c.mesh, c.p, c.eqn)
+        drv = so.Driver(od, "pmg", c.levels, 2, smoother_shift=50.0, gmres_rtol=1e-3, dtau_init=c.dt)
+        s = ti.get_scheme("esdirk2")
+        t0 = time.perf_counter()
+        drv.esdirk_step(c.q0, c.dt, s.a, s.b)
+        out["config1"]["cpu_oracle_s"] = time.perf_counter() - t0
+        out["config1"]["speedup_vs_cpu"] = out["config1"]["cpu_oracle_s"] / out["config1"]["gpu_s"]
+    except Exception as exc:  # pragma: no cover
+        out["config1"]["cpu_oracle_s"] = f"failed: {exc}"
+    return out
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

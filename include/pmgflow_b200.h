@@ -110,21 +110,25 @@ PMGB_API int pmgb_element_residual(pmgb_disc* d, const int64_t* elems, int64_t B
 
 /* assemble_element_blocks (newton_krylov.py:157-210): FD blocks of
  * shift I - dR_e/dq_e (eps perturbations of the frozen element-local
- * residual) stored column-major per element in blocksT (M, sz, sz), and
- * their inverses (column-major) in invT.  blocksT may equal invT
- * (in-place inverse).  Singular blocks latch status kind 3. */
+ * residual) stored column-major per element in blocksT (M, sz, sz).  If
+ * XT is not NULL the blocks are also inverted (np.linalg.inv at
+ * newton_krylov.py:201) by Gauss-Jordan with implicit partial pivoting:
+ * XT (M, sz, sz) receives the in-place factor column-major and perm
+ * (M, 2*sz) uint8 the pivot rows p and their inverse q, such that
+ * B^-1[i][j] = X[p_i][q_j].  XT may equal blocksT.  A singular block
+ * latches status kind 3 (RuntimeError at newton_krylov.py:202-208). */
 PMGB_API int pmgb_blocks_assemble(pmgb_disc* d, const double* q, double shift, double eps,
-                                  double* blocksT, double* invT, void* stream);
-PMGB_API int pmgb_blocks_invert(int64_t n_elem, int32_t sz, const double* blocksT, double* invT,
+                                  double* blocksT, double* XT, uint8_t* perm, void* stream);
+PMGB_API int pmgb_blocks_invert(int64_t n_elem, int32_t sz, const double* blocksT, double* XT, uint8_t* perm,
                                 void* stream);
 
 /* BlockJacobian.apply / ej_apply (newton_krylov.py:166-171, 213-214):
- * y_e = B_e^-1 x_e.  pmgb_ej_update: out = base + omega * B^-1 d
- * (smooth_ej, pmg.py:162-164); out may alias base. */
-PMGB_API int pmgb_ej_apply(int64_t n_elem, int32_t sz, const double* invT, const double* x, double* y,
-                           void* stream);
-PMGB_API int pmgb_ej_update(int64_t n_elem, int32_t sz, const double* invT, const double* d, double omega,
-                            const double* base, double* out, void* stream);
+ * y_e = B_e^-1 x_e from (XT, perm).  pmgb_ej_update: out = base + omega *
+ * B^-1 d (smooth_ej, pmg.py:162-164); out may alias base. */
+PMGB_API int pmgb_ej_apply(int64_t n_elem, int32_t sz, const double* XT, const uint8_t* perm, const double* x,
+                           double* y, void* stream);
+PMGB_API int pmgb_ej_update(int64_t n_elem, int32_t sz, const double* XT, const uint8_t* perm, const double* d,
+                            double omega, const double* base, double* out, void* stream);
 
 /* pMG transfers (pmg.py:117-136).  T is a HOST (n_out x n_in) matrix:
  * Gamma for restriction, Pi for prolongation.
@@ -156,6 +160,9 @@ PMGB_API int pmgb_status(void* stream, int32_t* kind, int64_t* element, int32_t 
 PMGB_API int pmgb_status_clear(void* stream);
 PMGB_API int pmgb_sync(void* stream);
 PMGB_API const char* pmgb_error_string(int code);
+/* FP64 throughput probe: `blocks` CTAs x 256 threads x 8 DFMA chains x
+ * iters (2 flops each); the FP64 roof for bench.py's roofline. */
+PMGB_API int pmgb_probe_fp64(int64_t iters, int32_t blocks, double* out_dev, void* stream);
 /* Build/version tag and a count of kernel launches issued (diagnostics). */
 PMGB_API const char* pmgb_version(void);
 PMGB_API int64_t pmgb_launch_count(void);

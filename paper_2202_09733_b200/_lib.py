@@ -57,11 +57,12 @@ SIGNATURES = {
     "pmgb_element_residual": (ctypes.c_int, [c_void_p, c_void_p, ctypes.c_int64, c_void_p, c_void_p,
                                              c_void_p, c_void_p, c_void_p]),
     "pmgb_blocks_assemble": (ctypes.c_int, [c_void_p, c_void_p, ctypes.c_double, ctypes.c_double,
-                                            c_void_p, c_void_p, c_void_p]),
-    "pmgb_blocks_invert": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int32, c_void_p, c_void_p, c_void_p]),
-    "pmgb_ej_apply": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int32, c_void_p, c_void_p, c_void_p, c_void_p]),
-    "pmgb_ej_update": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int32, c_void_p, c_void_p, ctypes.c_double,
-                                      c_void_p, c_void_p, c_void_p]),
+                                            c_void_p, c_void_p, c_void_p, c_void_p]),
+    "pmgb_blocks_invert": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int32, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "pmgb_ej_apply": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int32, c_void_p, c_void_p, c_void_p, c_void_p,
+                                     c_void_p]),
+    "pmgb_ej_update": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int32, c_void_p, c_void_p, c_void_p,
+                                      ctypes.c_double, c_void_p, c_void_p, c_void_p]),
     "pmgb_transfer": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                                      c_double_p, c_void_p, c_void_p, c_void_p, ctypes.c_int32, c_void_p]),
     "pmgb_dot": (ctypes.c_int, [ctypes.c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
@@ -78,6 +79,7 @@ SIGNATURES = {
     "pmgb_sync": (ctypes.c_int, [c_void_p]),
     "pmgb_error_string": (ctypes.c_char_p, [ctypes.c_int]),
     "pmgb_version": (ctypes.c_char_p, []),
+    "pmgb_probe_fp64": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int32, c_void_p, c_void_p]),
     "pmgb_launch_count": (ctypes.c_int64, []),
 }
 

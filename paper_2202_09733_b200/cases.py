@@ -101,8 +101,12 @@ def config(k: int, seed: int = 0, nx: int | None = None) -> Case:
         eqn = EquationSpec(kind="navier-stokes", mach=0.5, reynolds=1000.0, ref_length=10.0)
         q0 = _noise(_project(mesh, 4, isentropic_vortex(eqn)), 1e-6, seed)
         dt = 50.0 * explicit_dt(mesh, 4, eqn, q0)
+        # smoother_shift: the EJ smoother only contracts once the shift
+        # exceeds ~half the viscous spectral radius (mu (p+1)^4 / h^2 ~ 4e3
+        # here); 50 (config 1's value) stalls GMRES on the device and in the
+        # oracle alike, 5000 converges (4 PTC / 75 GMRES per stage)
         return Case("config2", mesh, 4, eqn, q0, dt, "esdirk2", "4-2", 30, 10,
-                    {"smoother_shift": 50.0, "rtol": 1e-3})
+                    {"smoother_shift": 5000.0, "rtol": 1e-3})
     if k == 3:
         n = nx or 128
         mesh = generate_box(n, n, 10.0, 10.0, periodic=True)

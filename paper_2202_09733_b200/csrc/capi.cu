@@ -8,9 +8,9 @@
 #include "pmgb_internal.cuh"
 
 namespace pmgb {
-int launch_inverse(int64_t M, int SZ, const double* BT, double* invT, cudaStream_t st, Status* stp);
-int launch_block_gemv(int64_t M, int SZ, const double* invT, const double* x, double omega, const double* base,
-                      double* out, cudaStream_t st);
+int launch_inverse(int64_t M, int SZ, const double* BT, double* XT, uint8_t* perm, cudaStream_t st, Status* stp);
+int launch_block_gemv(int64_t M, int SZ, const double* XT, const uint8_t* perm, const double* x, double omega,
+                      const double* base, double* out, cudaStream_t st);
 int launch_transfer(int64_t M, int nv, int nin, int nout, const double* T, const double* src,
                     const double* src_base, double* dst, int accumulate, cudaStream_t st);
 int launch_dot(int64_t n, const double* x, const double* y, double* out, int do_sqrt, cudaStream_t st);
@@ -19,6 +19,7 @@ int launch_mgs(int64_t n, double* V, int64_t ld, int j, double* w, double* H, do
 int launch_lincomb(int64_t n, int k, const double* c, const double* const* xs, double* out, cudaStream_t st);
 int launch_gemv_t(int64_t n, int k, const double* V, int64_t ld, const double* y, double* out, cudaStream_t st);
 int launch_any_nonzero(int64_t n, const double* x, int* flag_dev, cudaStream_t st);
+int launch_probe_fp64(int64_t iters, int blocks, double* out, cudaStream_t st);
 Status* status_ptr();
 }  // namespace pmgb
 
@@ -176,13 +177,14 @@ PMGB_API int pmgb_element_residual(pmgb_disc* h, const int64_t* elems, int64_t B
   return launch_local_residual(h->d, elems, B, Q, qtr, fvn, out, S(stream));
 }
 
-PMGB_API int pmgb_blocks_invert(int64_t M, int32_t sz, const double* BT, double* invT, void* stream) {
+PMGB_API int pmgb_blocks_invert(int64_t M, int32_t sz, const double* BT, double* XT, uint8_t* perm, void* stream) {
+  if (!BT || !XT || !perm) return -1;
   g_launches += 1;
-  return launch_inverse(M, sz, BT, invT, S(stream), status_ptr());
+  return launch_inverse(M, sz, BT, XT, perm, S(stream), status_ptr());
 }
 
 PMGB_API int pmgb_blocks_assemble(pmgb_disc* h, const double* q, double shift, double eps, double* BT,
-                                  double* invT, void* stream) {
+                                  double* XT, uint8_t* perm, void* stream) {
   if (!h || !q || !BT) return -1;
   const DiscDev& d = h->d;
   int rc = launch_freeze(d, q, d.qtr, d.fvn, S(stream));
@@ -190,23 +192,24 @@ PMGB_API int pmgb_blocks_assemble(pmgb_disc* h, const double* q, double shift, d
   rc = launch_blocks(d, q, d.qtr, d.fvn, shift, eps, BT, S(stream));
   if (rc) return rc;
   g_launches += n_res_launches(d);
-  if (invT) {
+  if (XT) {
     const int n = d.p + 1;
-    return pmgb_blocks_invert(d.M, n * n * d.nv, BT, invT, stream);
+    return pmgb_blocks_invert(d.M, n * n * d.nv, BT, XT, perm, stream);
   }
   return 0;
 }
 
-PMGB_API int pmgb_ej_apply(int64_t M, int32_t sz, const double* invT, const double* x, double* y, void* stream) {
+PMGB_API int pmgb_ej_apply(int64_t M, int32_t sz, const double* XT, const uint8_t* perm, const double* x, double* y,
+                           void* stream) {
   g_launches += 1;
-  return launch_block_gemv(M, sz, invT, x, 0.0, nullptr, y, S(stream));
+  return launch_block_gemv(M, sz, XT, perm, x, 0.0, nullptr, y, S(stream));
 }
 
-PMGB_API int pmgb_ej_update(int64_t M, int32_t sz, const double* invT, const double* dd, double omega,
-                            const double* base, double* out, void* stream) {
+PMGB_API int pmgb_ej_update(int64_t M, int32_t sz, const double* XT, const uint8_t* perm, const double* dd,
+                            double omega, const double* base, double* out, void* stream) {
   if (!base) return -1;
   g_launches += 1;
-  return launch_block_gemv(M, sz, invT, dd, omega, base, out, S(stream));
+  return launch_block_gemv(M, sz, XT, perm, dd, omega, base, out, S(stream));
 }
 
 PMGB_API int pmgb_transfer(int64_t M, int32_t nv, int32_t nin, int32_t nout, const double* T, const double* src,
@@ -260,5 +263,9 @@ PMGB_API int pmgb_status(void* stream, int32_t* kind, int64_t* element, int32_t 
 PMGB_API int pmgb_status_clear(void* stream) { return status_clear_async(S(stream)); }
 
 PMGB_API int pmgb_sync(void* stream) { return (int)cudaStreamSynchronize(S(stream)); }
+
+PMGB_API int pmgb_probe_fp64(int64_t iters, int32_t blocks, double* out_dev, void* stream) {
+  return launch_probe_fp64(iters, blocks, out_dev, S(stream));
+}
 
 }  // extern "C"

@@ -1,180 +1,320 @@
-// Element-Jacobi blocks: batched in-place Gauss-Jordan inverse and the
-// HBM-bound batched block GEMV / fused EJ sweep update.
+// Element-Jacobi blocks: batched register-tiled Gauss-Jordan inversion and
+// the HBM-bound batched block GEMV / fused EJ sweep update; pMG transfers.
 //
 // Reference: newton_krylov.py:187-210 (np.linalg.inv of the FD blocks,
 // RuntimeError on a singular block), :157-171 (BlockJacobian.apply =
-// einsum("mij,mj->mi")), pmg.py:162-164 (q <- q + omega B^-1 d).
+// einsum("mij,mj->mi")), pmg.py:162-164 (q <- q + omega B^-1 d),
+// pmg.py:117-136 (Gamma (x) Gamma restriction, Pi (x) Pi prolongation).
 //
-// Storage: blocks and inverses are column-major per element (B^T
-// row-major), so the GEMV thread for row i streams invT[e][j][i] with
-// consecutive i across the warp (coalesced), x[e][j] is a broadcast.
+// Inverse storage.  Gauss-Jordan runs in place with implicit partial
+// pivoting (pivot of column k = largest |a_rk| over rows not yet used,
+// ties to the lowest row -- the candidate set LAPACK getrf searches after
+// its swaps), so rows never move.  The in-place result X satisfies
+//     B^-1[i][j] = X[p_i][q_j],   p_k = pivot row of column k, q = p^-1,
+// and is stored column-major XT[c][r] = X[r][c] with perm[0:sz] = p and
+// perm[sz:2sz] = q (uint8).  The GEMV applies the permutations on the fly:
+//     y[q_r] = sum_c XT[c][r] x[p_c]
+// so nothing is ever un-permuted in memory.
 #include <climits>
+#include <cstdint>
 
 #include "pmgb_internal.cuh"
 
 namespace pmgb {
 
-// Gauss-Jordan with implicit partial pivoting (no row swaps): pivot of
-// column k = largest |A[r][k]| over rows not yet used (ties -> lowest r),
-// i.e. the same candidate set LAPACK's getrf searches after its swaps.
-// Runs on A = B^T; the result is A^-1 = (B^-1)^T = invT, un-permuted on
-// the store: A^-1[i][j] = X[prow[i]][q[j]], q = prow^-1.
-__global__ void __launch_bounds__(256)
-k_inverse(int SZ, const double* __restrict__ BT, double* __restrict__ invT, Status* st) {
-  extern __shared__ double sm[];
-  double* A = sm;                       // SZ*SZ
-  double* col = A + SZ * SZ;            // SZ
-  int* used = (int*)(col + SZ);         // SZ
-  int* prow = used + SZ;                // SZ
-  int* qinv = prow + SZ;                // SZ
-  __shared__ int s_p;
-  __shared__ double s_pv;
+template <int SZ> struct GJTile;
+template <> struct GJTile<1>   { static constexpr int TR = 1, TC = 1; };
+template <> struct GJTile<4>   { static constexpr int TR = 1, TC = 2; };
+template <> struct GJTile<9>   { static constexpr int TR = 3, TC = 3; };
+template <> struct GJTile<16>  { static constexpr int TR = 2, TC = 4; };
+template <> struct GJTile<25>  { static constexpr int TR = 5, TC = 5; };
+template <> struct GJTile<36>  { static constexpr int TR = 3, TC = 6; };
+template <> struct GJTile<64>  { static constexpr int TR = 4, TC = 8; };
+template <> struct GJTile<100> { static constexpr int TR = 4, TC = 10; };
+template <> struct GJTile<144> { static constexpr int TR = 6, TC = 12; };
+
+template <int SZ> struct GJShape {
+  static constexpr int TR = GJTile<SZ>::TR, TC = GJTile<SZ>::TC;
+  static constexpr int NRG = (SZ + TR - 1) / TR, NCG = (SZ + TC - 1) / TC;
+  static constexpr int THREADS = ((NRG * NCG + 31) / 32) * 32;
+  static constexpr int ROWS_PER_LANE = (SZ + 31) / 32;
+};
+
+// One CTA per block.  BT: FD blocks, column-major (BT[c][r] = B[r][c]).
+template <int SZ>
+__global__ void __launch_bounds__(GJShape<SZ>::THREADS)
+k_gj_inverse(const double* __restrict__ BT, double* __restrict__ XT, uint8_t* __restrict__ perm, Status* st) {
+  using S = GJShape<SZ>;
+  constexpr int TR = S::TR, TC = S::TC, NRG = S::NRG, NCG = S::NCG, RPL = S::ROWS_PER_LANE;
+  __shared__ double colbuf[2][SZ];
+  __shared__ double rowbuf[2][SZ];
+  __shared__ int pivs[SZ];
   __shared__ int s_bad;
   const int64_t e = blockIdx.x;
-  const int tid = threadIdx.x, T = blockDim.x;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const bool active = tid < NRG * NCG;
+  const int rg = tid % NRG, cg = tid / NRG;
+  const int r0 = rg * TR, c0 = cg * TC;
   const double* src = BT + e * (int64_t)SZ * SZ;
-  for (int i = tid; i < SZ * SZ; i += T) A[i] = __ldg(src + i);
-  for (int i = tid; i < SZ; i += T) used[i] = 0;
+  double a[TR][TC];
+#pragma unroll
+  for (int j = 0; j < TC; ++j) {
+#pragma unroll
+    for (int i = 0; i < TR; ++i) {
+      const int r = r0 + i, c = c0 + j;
+      a[i][j] = (active && r < SZ && c < SZ) ? __ldg(src + (int64_t)c * SZ + r) : 0.0;
+    }
+  }
   if (tid == 0) s_bad = 0;
-  __syncthreads();
-  for (int k = 0; k < SZ; ++k) {
-    if (tid < 32) {
+  unsigned used = 0;  // bit m: row lane + 32 m already pivoted (per warp copy)
+  for (int kg = 0; kg < NCG; ++kg) {
+#pragma unroll
+    for (int kk = 0; kk < TC; ++kk) {
+      const int k = kg * TC + kk;
+      if (k >= SZ) break;
+      const int b = k & 1;
+      if (active && cg == kg) {
+#pragma unroll
+        for (int i = 0; i < TR; ++i)
+          if (r0 + i < SZ) colbuf[b][r0 + i] = a[i][kk];
+      }
+      __syncthreads();
+      // pivot search, redundantly in every warp (deterministic)
       double bv = -1.0;
       int br = INT_MAX;
-      for (int r = tid; r < SZ; r += 32) {
-        if (!used[r]) {
-          const double v = fabs(A[r * SZ + k]);
-          if (v > bv || (v != v && bv == -1.0)) { bv = v; br = r; }
+#pragma unroll
+      for (int m = 0; m < RPL; ++m) {
+        const int r = lane + 32 * m;
+        if (r < SZ && !((used >> m) & 1u)) {
+          const double v = fabs(colbuf[b][r]);
+          if (v > bv) {
+            bv = v;
+            br = r;
+          }
         }
       }
+#pragma unroll
       for (int off = 16; off > 0; off >>= 1) {
-        const double ov = __shfl_down_sync(0xffffffffu, bv, off);
-        const int orr = __shfl_down_sync(0xffffffffu, br, off);
-        if (ov > bv || (ov == bv && orr < br)) { bv = ov; br = orr; }
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, off);
+        const int orr = __shfl_xor_sync(0xffffffffu, br, off);
+        if (ov > bv || (ov == bv && orr < br)) {
+          bv = ov;
+          br = orr;
+        }
       }
+      const bool nan_col = (br == INT_MAX);
+      int p = nan_col ? k : br;  // every candidate NaN: flagged singular below
+      if ((p & 31) == lane) used |= 1u << (p >> 5);
+      const double pv = colbuf[b][p];
       if (tid == 0) {
-        if (br == INT_MAX) br = k;  // all NaN: keep going, flagged below
-        s_p = br;
-        s_pv = A[br * SZ + k];
-        used[br] = 1;
-        prow[k] = br;
-        qinv[br] = k;
-        if (!(s_pv != 0.0) || !isfinite(s_pv)) s_bad = 1;
+        pivs[k] = p;
+        if (nan_col || !(pv != 0.0) || !isfinite(pv)) s_bad = 1;
+      }
+      const double pinv = 1.0 / pv;
+      if (active && rg == p / TR) {
+        const int ip = p - r0;
+#pragma unroll
+        for (int i = 0; i < TR; ++i) {
+          if (i == ip) {
+#pragma unroll
+            for (int j = 0; j < TC; ++j) {
+              const int c = c0 + j;
+              if (c < SZ) rowbuf[b][c] = ((cg == kg && j == kk) ? 1.0 : a[i][j]) * pinv;
+            }
+          }
+        }
+      }
+      __syncthreads();
+      if (active) {
+        double pr[TC];
+#pragma unroll
+        for (int j = 0; j < TC; ++j) pr[j] = (c0 + j < SZ) ? rowbuf[b][c0 + j] : 0.0;
+#pragma unroll
+        for (int i = 0; i < TR; ++i) {
+          const int r = r0 + i;
+          if (r >= SZ) continue;
+          if (r == p) {
+#pragma unroll
+            for (int j = 0; j < TC; ++j) a[i][j] = pr[j];
+          } else {
+            const double f = colbuf[b][r];
+#pragma unroll
+            for (int j = 0; j < TC; ++j) {
+              const double x = (cg == kg && j == kk) ? 0.0 : a[i][j];
+              a[i][j] = x - f * pr[j];
+            }
+          }
+        }
       }
     }
-    __syncthreads();
-    const int p = s_p;
-    const double pinv = 1.0 / s_pv;
-    for (int r = tid; r < SZ; r += T) col[r] = A[r * SZ + k];
-    __syncthreads();
-    for (int c = tid; c < SZ; c += T) A[p * SZ + c] = (c == k ? 1.0 : A[p * SZ + c]) * pinv;
-    __syncthreads();
-    for (int i = tid; i < SZ * SZ; i += T) {
-      const int r = i / SZ, c = i - r * SZ;
-      if (r == p) continue;
-      const double a = (c == k) ? 0.0 : A[i];
-      A[i] = a - col[r] * A[p * SZ + c];
-    }
-    __syncthreads();
   }
+  __syncthreads();
   if (tid == 0 && s_bad && st != nullptr) {
     if (atomicCAS(&st->kind, 0, 3) == 0) st->element = e;
   }
-  double* dst = invT + e * (int64_t)SZ * SZ;
-  for (int i = tid; i < SZ * SZ; i += T) {
-    const int r = i / SZ, c = i - r * SZ;
-    dst[i] = A[prow[r] * SZ + qinv[c]];
+  double* dst = XT + e * (int64_t)SZ * SZ;
+  if (active) {
+#pragma unroll
+    for (int j = 0; j < TC; ++j) {
+#pragma unroll
+      for (int i = 0; i < TR; ++i) {
+        const int r = r0 + i, c = c0 + j;
+        if (r < SZ && c < SZ) dst[(int64_t)c * SZ + r] = a[i][j];
+      }
+    }
+  }
+  uint8_t* pe = perm + e * 2 * SZ;
+  for (int k = tid; k < SZ; k += blockDim.x) {
+    const int p = pivs[k];
+    pe[k] = (uint8_t)p;
+    pe[SZ + p] = (uint8_t)k;
   }
 }
 
-// y[e][i] = sum_j invT[e][j][i] x[e][j]; optional fused EJ update
-// out = base + omega * y   (pmg.py:164)
+// y[q_r] = sum_c XT[c][r] x[p_c]  (optionally out = base + omega * y, pmg.py:164)
+// Thread per (element, r); the CTA stages the gathered x[p_c] of its
+// elements in shared memory.
 template <bool UPDATE>
 __global__ void __launch_bounds__(256)
-k_block_gemv(int64_t M, int SZ, const double* __restrict__ invT, const double* __restrict__ x,
-             double omega, const double* __restrict__ base, double* __restrict__ out) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= M * SZ) return;
-  const int64_t e = t / SZ;
-  const int i = (int)(t - e * SZ);
-  const double* Ae = invT + e * (int64_t)SZ * SZ + i;
-  const double* xe = x + e * SZ;
-  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-  int j = 0;
-  for (; j + 4 <= SZ; j += 4) {
-    a0 += __ldg(Ae + (int64_t)(j + 0) * SZ) * __ldg(xe + j + 0);
-    a1 += __ldg(Ae + (int64_t)(j + 1) * SZ) * __ldg(xe + j + 1);
-    a2 += __ldg(Ae + (int64_t)(j + 2) * SZ) * __ldg(xe + j + 2);
-    a3 += __ldg(Ae + (int64_t)(j + 3) * SZ) * __ldg(xe + j + 3);
+k_block_gemv(int64_t M, int SZ, const double* __restrict__ XT, const uint8_t* __restrict__ perm,
+             const double* __restrict__ x, double omega, const double* __restrict__ base,
+             double* __restrict__ out) {
+  extern __shared__ double xs[];
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x;
+  const int64_t total = M * SZ;
+  const int64_t e_first = t0 / SZ;
+  int64_t e_last = (t0 + blockDim.x - 1) / SZ;
+  if (e_last > M - 1) e_last = M - 1;
+  const int span = (int)(e_last - e_first + 1);
+  for (int i = threadIdx.x; i < span * SZ; i += blockDim.x) {
+    const int el = i / SZ, c = i - el * SZ;
+    const int64_t e = e_first + el;
+    const int pc = perm[e * 2 * SZ + c];
+    xs[i] = __ldg(x + e * SZ + pc);
   }
-  for (; j < SZ; ++j) a0 += __ldg(Ae + (int64_t)j * SZ) * __ldg(xe + j);
+  __syncthreads();
+  const int64_t t = t0 + threadIdx.x;
+  if (t >= total) return;
+  const int64_t e = t / SZ;
+  const int r = (int)(t - e * SZ);
+  const double* Ae = XT + e * (int64_t)SZ * SZ + r;
+  const double* xe = xs + (e - e_first) * SZ;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  int c = 0;
+  for (; c + 4 <= SZ; c += 4) {
+    a0 += __ldg(Ae + (int64_t)(c + 0) * SZ) * xe[c + 0];
+    a1 += __ldg(Ae + (int64_t)(c + 1) * SZ) * xe[c + 1];
+    a2 += __ldg(Ae + (int64_t)(c + 2) * SZ) * xe[c + 2];
+    a3 += __ldg(Ae + (int64_t)(c + 3) * SZ) * xe[c + 3];
+  }
+  for (; c < SZ; ++c) a0 += __ldg(Ae + (int64_t)c * SZ) * xe[c];
   const double y = (a0 + a1) + (a2 + a3);
-  if (UPDATE) out[t] = base[t] + omega * y;
-  else out[t] = y;
+  const int64_t o = e * SZ + perm[e * 2 * SZ + SZ + r];
+  if (UPDATE) out[o] = base[o] + omega * y;
+  else out[o] = y;
 }
 
-int launch_inverse(int64_t M, int SZ, const double* BT, double* invT, cudaStream_t st, Status* stp) {
-  if (M <= 0) return 0;
-  const size_t bytes = sizeof(double) * ((size_t)SZ * SZ + SZ) + sizeof(int) * 3 * SZ;
-  static size_t attr = 0;
-  if (bytes > attr) {
-    cudaFuncSetAttribute(k_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    attr = bytes;
-  }
-  k_inverse<<<(unsigned)M, 256, bytes, st>>>(SZ, BT, invT, stp);
+template <int SZ>
+static int run_gj(int64_t M, const double* BT, double* XT, uint8_t* perm, cudaStream_t st, Status* stp) {
+  k_gj_inverse<SZ><<<(unsigned)M, GJShape<SZ>::THREADS, 0, st>>>(BT, XT, perm, stp);
   return (int)cudaGetLastError();
 }
 
-int launch_block_gemv(int64_t M, int SZ, const double* invT, const double* x, double omega,
+int launch_inverse(int64_t M, int SZ, const double* BT, double* XT, uint8_t* perm, cudaStream_t st,
+                   Status* stp) {
+  if (M <= 0) return 0;
+  switch (SZ) {
+    case 1: return run_gj<1>(M, BT, XT, perm, st, stp);
+    case 4: return run_gj<4>(M, BT, XT, perm, st, stp);
+    case 9: return run_gj<9>(M, BT, XT, perm, st, stp);
+    case 16: return run_gj<16>(M, BT, XT, perm, st, stp);
+    case 25: return run_gj<25>(M, BT, XT, perm, st, stp);
+    case 36: return run_gj<36>(M, BT, XT, perm, st, stp);
+    case 64: return run_gj<64>(M, BT, XT, perm, st, stp);
+    case 100: return run_gj<100>(M, BT, XT, perm, st, stp);
+    case 144: return run_gj<144>(M, BT, XT, perm, st, stp);
+  }
+  return -1000;
+}
+
+int launch_block_gemv(int64_t M, int SZ, const double* XT, const uint8_t* perm, const double* x, double omega,
                       const double* base, double* out, cudaStream_t st) {
   const int64_t n = M * SZ;
   if (n <= 0) return 0;
   const unsigned grid = (unsigned)((n + 255) / 256);
-  if (base) k_block_gemv<true><<<grid, 256, 0, st>>>(M, SZ, invT, x, omega, base, out);
-  else k_block_gemv<false><<<grid, 256, 0, st>>>(M, SZ, invT, x, 0.0, nullptr, out);
+  const size_t smem = sizeof(double) * (size_t)((255 / SZ) + 2) * SZ;
+  if (base)
+    k_block_gemv<true><<<grid, 256, smem, st>>>(M, SZ, XT, perm, x, omega, base, out);
+  else
+    k_block_gemv<false><<<grid, 256, smem, st>>>(M, SZ, XT, perm, x, 0.0, nullptr, out);
   return (int)cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------
-// pMG transfers (pmg.py:117-136): per element and variable
-//   restrict: lo[a][b] = sum_ij G[a][i] G[b][j] hi[i][j]
-//   prolong : hi[a][b] += sum_ij P[a][i] P[b][j] (lo - lo_base)[i][j]
+// pMG transfers (pmg.py:117-136), per element and variable:
+//   dst[a][b] (+)= sum_ij T[a][i] T[b][j] (src - src_base)[i][j]
+// The CTA stages its elements' inputs in shared memory (coalesced), then
+// contracts separably: tmp[i][b] = sum_j T[b][j] s[i][j]; out = sum_i T[a][i] tmp[i][b].
 
 struct TransferOp {
   double T[36];  // (n_out x n_in) row-major
 };
 
-__global__ void __launch_bounds__(256)
-k_restrict(int64_t M, int nv, int nin, int nout, const TransferOp op, const double* __restrict__ src,
+constexpr int TR_THREADS = 256;
+
+__global__ void __launch_bounds__(TR_THREADS)
+k_transfer(int64_t M, int nv, int nin, int nout, int epb, const TransferOp op, const double* __restrict__ src,
            const double* __restrict__ src_base, double* __restrict__ dst, int accumulate) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int per = nout * nout * nv;
-  if (t >= M * per) return;
-  const int64_t e = t / per;
-  const int r = (int)(t - e * per);
-  const int v = r % nv, pt = r / nv, a = pt / nout, b = pt % nout;
-  const double* s = src + e * (int64_t)nin * nin * nv + v;
-  const double* sb = src_base ? src_base + e * (int64_t)nin * nin * nv + v : nullptr;
-  double acc = 0.0;
-  for (int i = 0; i < nin; ++i) {
-    const double ta = op.T[a * nin + i];
-    for (int j = 0; j < nin; ++j) {
-      double x = __ldg(s + (i * nin + j) * nv);
-      if (sb) x = x - __ldg(sb + (i * nin + j) * nv);
-      acc += (ta * op.T[b * nin + j]) * x;
-    }
+  extern __shared__ double sm[];
+  const int in_sz = nin * nin * nv, mid_sz = nin * nout * nv, out_sz = nout * nout * nv;
+  double* s_in = sm;                       // epb * in_sz
+  double* s_mid = sm + epb * in_sz;        // epb * mid_sz
+  const int64_t e0 = (int64_t)blockIdx.x * epb;
+  const int64_t ne = (M - e0) < epb ? (M - e0) : epb;
+  const int64_t nin_vals = ne * in_sz;
+  const double* sb = src + e0 * in_sz;
+  const double* bb = src_base ? src_base + e0 * in_sz : nullptr;
+  for (int i = threadIdx.x; i < nin_vals; i += blockDim.x) {
+    double v = __ldg(sb + i);
+    if (bb) v = v - __ldg(bb + i);
+    s_in[i] = v;
   }
-  if (accumulate) dst[t] = dst[t] + acc;
-  else dst[t] = acc;
+  __syncthreads();
+  // tmp[el][i][b][v] = sum_j T[b][j] s[el][i][j][v]
+  for (int t = threadIdx.x; t < ne * mid_sz; t += blockDim.x) {
+    const int el = t / mid_sz, r = t - el * mid_sz;
+    const int v = r % nv, ib = r / nv, i = ib / nout, b = ib % nout;
+    const double* s = s_in + el * in_sz + i * nin * nv + v;
+    double acc = 0.0;
+    for (int j = 0; j < nin; ++j) acc += op.T[b * nin + j] * s[j * nv];
+    s_mid[t] = acc;
+  }
+  __syncthreads();
+  double* db = dst + e0 * out_sz;
+  for (int t = threadIdx.x; t < ne * out_sz; t += blockDim.x) {
+    const int el = t / out_sz, r = t - el * out_sz;
+    const int v = r % nv, ab = r / nv, a = ab / nout, b = ab % nout;
+    const double* m = s_mid + el * mid_sz + b * nv + v;
+    double acc = 0.0;
+    for (int i = 0; i < nin; ++i) acc += op.T[a * nin + i] * m[i * nout * nv];
+    if (accumulate) db[t] = db[t] + acc;
+    else db[t] = acc;
+  }
 }
 
 int launch_transfer(int64_t M, int nv, int nin, int nout, const double* T, const double* src,
                     const double* src_base, double* dst, int accumulate, cudaStream_t st) {
   TransferOp op;
   for (int i = 0; i < 36; ++i) op.T[i] = (i < nin * nout) ? T[i] : 0.0;
-  const int64_t n = M * nout * nout * nv;
-  if (n <= 0) return 0;
-  k_restrict<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(M, nv, nin, nout, op, src, src_base, dst, accumulate);
+  if (M <= 0) return 0;
+  const int in_sz = nin * nin * nv, mid_sz = nin * nout * nv;
+  int epb = 1024 / (in_sz > 1 ? in_sz : 1);
+  if (epb < 1) epb = 1;
+  if (epb > 256) epb = 256;
+  const size_t smem = sizeof(double) * (size_t)epb * (in_sz + mid_sz);
+  const unsigned grid = (unsigned)((M + epb - 1) / epb);
+  k_transfer<<<grid, TR_THREADS, smem, st>>>(M, nv, nin, nout, epb, op, src, src_base, dst, accumulate);
   return (int)cudaGetLastError();
 }
 

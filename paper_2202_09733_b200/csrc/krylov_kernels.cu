@@ -14,7 +14,7 @@
 namespace pmgb {
 
 constexpr int RED_THREADS = 256;
-constexpr int RED_BLOCKS = 296;  // 2 x 148 SMs
+constexpr int RED_BLOCKS = 148 * 8;  // fixed grid: reductions are order-deterministic
 
 struct RedScratch {
   double* partial;          // RED_BLOCKS
@@ -76,22 +76,54 @@ __device__ __forceinline__ bool finish(const RedScratch& rs, double mine, double
 }
 
 // w <- w - h_prev * Vprev (if Vprev); out = Vnext . w  (Vnext may be w)
-// optionally flags a non-finite w on the first pass.
+// optionally flags a non-finite w on the first pass.  Each thread walks
+// a fixed sequence of 4-element chunks; all loads of a chunk are issued
+// before any store (w and Vnext may alias), keeping 4 loads per stream
+// in flight.
+constexpr int CH = 4;
+
 __global__ void __launch_bounds__(RED_THREADS)
-k_mgs_pass(int64_t n, double* __restrict__ w, const double* __restrict__ Vprev, const double* hprev,
-           const double* Vnext, double* out, int do_sqrt, int check_finite, RedScratch rs) {
+k_mgs_pass(int64_t n, double* w, const double* __restrict__ Vprev, const double* hprev, const double* Vnext,
+           double* out, int do_sqrt, int check_finite, RedScratch rs) {
   const double h = Vprev ? *hprev : 0.0;
   double acc = 0.0;
   int bad = 0;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+  const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nchunks = n / CH;
+  for (int64_t c = tid; c < nchunks; c += nthreads) {
+    const int64_t i = c * CH;
+    double wv[CH], vn[CH], vp[CH];
+#pragma unroll
+    for (int u = 0; u < CH; ++u) wv[u] = w[i + u];
+#pragma unroll
+    for (int u = 0; u < CH; ++u) vn[u] = Vnext[i + u];
+    if (Vprev) {
+#pragma unroll
+      for (int u = 0; u < CH; ++u) vp[u] = Vprev[i + u];
+    }
+#pragma unroll
+    for (int u = 0; u < CH; ++u) {
+      double wi = wv[u];
+      if (Vprev) wi = wi - h * vp[u];
+      if (check_finite && !isfinite(wi)) bad = 1;
+      if (Vnext == w) vn[u] = wi;
+      acc += vn[u] * wi;
+      wv[u] = wi;
+    }
+    if (Vprev) {
+#pragma unroll
+      for (int u = 0; u < CH; ++u) w[i + u] = wv[u];
+    }
+  }
+  for (int64_t i = nchunks * CH + tid; i < n; i += nthreads) {  // tail
     double wi = w[i];
     if (Vprev) {
       wi = wi - h * Vprev[i];
       w[i] = wi;
     }
     if (check_finite && !isfinite(wi)) bad = 1;
-    acc += Vnext[i] * wi;
+    acc += (Vnext == w ? wi : Vnext[i]) * wi;
   }
   if (check_finite && __syncthreads_or(bad) && threadIdx.x == 0) atomicOr(rs.flag, 1);
   const double s = block_sum(acc);
@@ -102,8 +134,21 @@ __global__ void __launch_bounds__(RED_THREADS)
 k_dot(int64_t n, const double* __restrict__ x, const double* __restrict__ y, double* out, int do_sqrt,
       RedScratch rs) {
   double acc = 0.0;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) acc += x[i] * y[i];
+  const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nchunks = n / CH;
+  for (int64_t c = tid; c < nchunks; c += nthreads) {
+    const int64_t i = c * CH;
+    double a[CH], b[CH];
+#pragma unroll
+    for (int u = 0; u < CH; ++u) {
+      a[u] = x[i + u];
+      b[u] = y[i + u];
+    }
+#pragma unroll
+    for (int u = 0; u < CH; ++u) acc += a[u] * b[u];
+  }
+  for (int64_t i = nchunks * CH + tid; i < n; i += nthreads) acc += x[i] * y[i];
   const double s = block_sum(acc);
   finish(rs, s, out, do_sqrt != 0);
 }
@@ -212,6 +257,30 @@ int launch_gemv_t(int64_t n, int k, const double* V, int64_t ld, const double* y
 int launch_any_nonzero(int64_t n, const double* x, int* flag_dev, cudaStream_t st) {
   cudaMemsetAsync(flag_dev, 0, sizeof(int), st);
   k_any_nonzero<<<ew_grid(n), 256, 0, st>>>(n, x, flag_dev);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace pmgb
+
+namespace pmgb {
+
+// FP64 peak probe: 8 independent DFMA chains per thread, full grid.
+// flops = 2 * 8 * iters * threads.  Used by bench.py for the FP64 roof
+// (MEASURED_PEAKS.json has HBM and bf16 only).
+__global__ void __launch_bounds__(256) k_probe_fp64(int64_t iters, double seed, double* out) {
+  double a0 = seed + threadIdx.x * 1e-9, a1 = a0 + 1e-3, a2 = a0 + 2e-3, a3 = a0 + 3e-3;
+  double a4 = a0 + 4e-3, a5 = a0 + 5e-3, a6 = a0 + 6e-3, a7 = a0 + 7e-3;
+  const double m = 0.999999999, c = 1e-12;
+  for (int64_t i = 0; i < iters; ++i) {
+    a0 = fma(a0, m, c); a1 = fma(a1, m, c); a2 = fma(a2, m, c); a3 = fma(a3, m, c);
+    a4 = fma(a4, m, c); a5 = fma(a5, m, c); a6 = fma(a6, m, c); a7 = fma(a7, m, c);
+  }
+  const double s = ((a0 + a1) + (a2 + a3)) + ((a4 + a5) + (a6 + a7));
+  if (s == 12345.678) out[0] = s;  // never true; keeps the chains live
+}
+
+int launch_probe_fp64(int64_t iters, int blocks, double* out, cudaStream_t st) {
+  k_probe_fp64<<<blocks, 256, 0, st>>>(iters, 1.0, out);
   return (int)cudaGetLastError();
 }
 

@@ -191,19 +191,27 @@ def gmres_solve(matvec, b, cfg: KrylovConfig, x0=None, precond=None):
 class BlockJacobian:
     """Inverted diagonal blocks of (shift I - dR/dq), one per element.
 
-    Storage is column-major per element on the device (``invT[e][j][i]
-    = B_e^-1[i][j]``); ``inv`` / ``blocks`` give the reference's
-    per-group (M, sz, sz) row-major views."""
+    Device storage (include/pmgflow_b200.h): the in-place Gauss-Jordan
+    factor ``XT`` (M, sz, sz) column-major and the pivot permutations
+    ``perm`` (M, 2 sz) uint8, with B^-1[i][j] = X[p_i][q_j].  ``inv`` /
+    ``blocks`` rebuild the reference's per-group (M, sz, sz) row-major
+    arrays (newton_krylov.py:157-164) for inspection."""
 
-    def __init__(self, disc: Discretization, shift: float, invT: torch.Tensor, blocksT=None):
+    def __init__(self, disc: Discretization, shift: float, XT: torch.Tensor, perm: torch.Tensor, blocksT=None):
         self.disc = disc
         self.shift = shift
-        self.invT = invT
+        self.XT = XT
+        self.perm = perm
         self.blocksT = blocksT
 
     @property
     def inv(self):
-        return [self.invT.transpose(1, 2)]
+        M, sz = self.XT.shape[0], self.XT.shape[1]
+        X = self.XT.transpose(1, 2)
+        p = self.perm[:, :sz].long()
+        q = self.perm[:, sz:].long()
+        rows = torch.gather(X, 1, p[:, :, None].expand(M, sz, sz))
+        return [torch.gather(rows, 2, q[:, None, :].expand(M, sz, sz))]
 
     @property
     def blocks(self):
@@ -215,16 +223,17 @@ class BlockJacobian:
         is_np = not isinstance(X, torch.Tensor)
         Xd = to_device(X, self.disc.device)
         out = torch.empty_like(Xd)
-        check(load().pmgb_ej_apply(self.disc.mesh.n_elements, self.disc.elem_size, self.invT.data_ptr(),
-                                   ptr(Xd), ptr(out), stream()), "ej_apply")
+        check(load().pmgb_ej_apply(self.disc.mesh.n_elements, self.disc.elem_size, self.XT.data_ptr(),
+                                   self.perm.data_ptr(), ptr(Xd), ptr(out), stream()), "ej_apply")
         return out.cpu().numpy() if is_np else out
 
     def update(self, d: torch.Tensor, omega: float, base: torch.Tensor, out=None) -> torch.Tensor:
         """out = base + omega * B^-1 d (smooth_ej, pmg.py:164)."""
         if out is None:
             out = torch.empty_like(base)
-        check(load().pmgb_ej_update(self.disc.mesh.n_elements, self.disc.elem_size, self.invT.data_ptr(),
-                                    ptr(d), float(omega), ptr(base), ptr(out), stream()), "ej_update")
+        check(load().pmgb_ej_update(self.disc.mesh.n_elements, self.disc.elem_size, self.XT.data_ptr(),
+                                    self.perm.data_ptr(), ptr(d), float(omega), ptr(base), ptr(out), stream()),
+              "ej_update")
         return out
 
 
@@ -238,12 +247,13 @@ def assemble_element_blocks(disc: Discretization, data, shift: float, frozen=Non
     del frozen
     q = to_device(data, disc.device)
     M, sz = disc.mesh.n_elements, disc.elem_size
-    invT = torch.empty((M, sz, sz), dtype=torch.float64, device=disc.device)
-    blocksT = torch.empty_like(invT) if keep_blocks else invT
+    XT = torch.empty((M, sz, sz), dtype=torch.float64, device=disc.device)
+    perm = torch.empty((M, 2 * sz), dtype=torch.uint8, device=disc.device)
+    blocksT = torch.empty_like(XT) if keep_blocks else XT
     check(load().pmgb_blocks_assemble(disc._h, ptr(q), float(shift), float(eps), blocksT.data_ptr(),
-                                      invT.data_ptr(), stream()), "blocks_assemble")
+                                      XT.data_ptr(), perm.data_ptr(), stream()), "blocks_assemble")
     raise_status()
-    return BlockJacobian(disc, shift, invT, blocksT if keep_blocks else None)
+    return BlockJacobian(disc, shift, XT, perm, blocksT if keep_blocks else None)
 
 
 def ej_apply(blocks: BlockJacobian, X):

@@ -1,0 +1,276 @@
+"""Device Jv / EJ blocks / transfers / GMRES / pMG / steppers vs the oracle
+and the reference golden vectors, all through the C ABI.
+
+Tolerances: Jv 1e-8 (the fixed eps = 1e-6 amplifies
+R rounding by 1e6); FD blocks 1e-7 of the block scale; solver iteration
+counts +-1; one-step solutions 1e-7 (esdirk2, floor 1.2e-8) and 1e-6 (row4,
+floor 7.4e-8)."""
+
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import solver_oracle as so
+from oracle.fr_oracle import OracleDisc
+from paper_2202_09733_b200 import _lib, cases, mesh as mm
+from paper_2202_09733_b200 import newton_krylov as nk
+from paper_2202_09733_b200 import pmg
+from paper_2202_09733_b200 import time_integration as ti
+from paper_2202_09733_b200.equation import EquationSpec, NonPhysicalStateError
+from paper_2202_09733_b200.harness import ImplicitDriver
+from paper_2202_09733_b200.spatial import Discretization
+
+pytestmark = pytest.mark.gpu
+G = np.load(Path(__file__).parent / "golden" / "golden.npz")
+
+
+def rel(a, b):
+    a = a.cpu().numpy() if isinstance(a, torch.Tensor) else a
+    b = b.cpu().numpy() if isinstance(b, torch.Tensor) else b
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300))
+
+
+def t(x):
+    return torch.as_tensor(np.asarray(x, dtype=np.float64), device="cuda")
+
+
+def test_jv_matches_reference_and_own_residual(cuda):
+    c = cases.config(1)
+    d = Discretization(c.mesh, c.p, c.eqn)
+    q = t(c.q0)
+    R0 = d.residual(q)
+    v = t(G["c1/v"])
+    Jv = nk.jfnk_matvec(v, q, R0, d.residual, 3.7)
+    assert rel(Jv, G["c1/Jv"]) <= 1e-8
+    # bitwise consistency with the device's own R(q + eps v) and R(q)
+    qp = torch.as_tensor(c.q0 + 1e-6 * G["c1/v"], device="cuda")
+    # (torch turns division by a Python scalar into a reciprocal multiply)
+    ref = 3.7 * v - (d.residual(qp) - R0) / torch.full_like(R0, 1e-6)
+    assert torch.equal(Jv, ref)
+
+
+def test_jv_zero_vector_short_circuits(cuda):
+    c = cases.config(1)
+    d = Discretization(c.mesh, c.p, c.eqn)
+    q = t(c.q0)
+    out = nk.jfnk_matvec(torch.zeros_like(q), q, d.residual(q), d.residual, 2.0)
+    assert float(out.abs().max()) == 0.0
+
+
+def test_blocks_match_reference(cuda):
+    m = mm.generate_box(3, 3, 1.0, 1.0, periodic=True)
+    eqn = EquationSpec(kind="navier-stokes", mach=0.3, reynolds=100.0)
+    d = Discretization(m, 2, eqn)
+    bj = nk.assemble_element_blocks(d, t(G["blk/q"]), 30.0)
+    B = bj.blocks[0].cpu().numpy()
+    ref = G["blk/blocks"]
+    assert np.abs(B - ref).max() / np.abs(ref).max() <= 1e-7
+    Y = bj.apply(t(G["blk/X"]))
+    assert rel(Y, G["blk/Y"]) <= 1e-7
+    # the inverse really inverts the device blocks
+    inv = bj.inv[0].cpu().numpy()
+    eye = np.einsum("mij,mjk->mik", B, inv)
+    assert np.abs(eye - np.eye(B.shape[1])).max() <= 1e-11
+
+
+@pytest.mark.parametrize("kind,p", [("euler", 1), ("ns", 2), ("ns", 3), ("ns", 4), ("advd", 2)])
+def test_blocks_match_oracle(cuda, kind, p):
+    kw = {"euler": dict(kind="euler", mach=0.3),
+          "ns": dict(kind="navier-stokes", mach=0.3, reynolds=50.0),
+          "advd": dict(kind="advection-diffusion", advection=(1.0, 0.4), diffusivity=0.5)}[kind]
+    m = mm.generate_box(3, 2, 1.0, 1.0)
+    eqn = EquationSpec(**kw)
+    o = OracleDisc(m, p, eqn)
+    rng = np.random.default_rng(3)
+    q = (rng.standard_normal(o.n_dofs) if kind == "advd"
+         else o.free_stream_field() * (1 + 0.01 * rng.standard_normal(o.n_dofs)))
+    ob = so.assemble_blocks(o, q, 5.0)
+    d = Discretization(m, p, eqn)
+    db = nk.assemble_element_blocks(d, t(q), 5.0)
+    B = db.blocks[0].cpu().numpy()
+    assert np.abs(B - ob.blocks).max() / np.abs(ob.blocks).max() <= 1e-7
+    X = rng.standard_normal(o.n_dofs)
+    assert rel(db.apply(t(X)), ob.apply(X)) <= 1e-6
+
+
+def test_transfers_match_oracle(cuda):
+    c = cases.config(1)
+    top = Discretization(c.mesh, 3, c.eqn)
+    ctx = pmg.PmgContext(top, pmg.PmgPrecondConfig(pmg.PHierarchy.parse("3-2-1")))
+    o = so.Pmg(OracleDisc(c.mesh, 3, c.eqn), "3-2-1", 1)
+    x = t(c.q0)
+    lo = ctx.tables[0].restrict(x)
+    assert rel(lo, o._restrict(0, c.q0)) <= 1e-14
+    lo2 = ctx.tables[1].restrict(lo)
+    assert rel(lo2, o._restrict(1, lo.cpu().numpy())) <= 1e-14
+    hi = ctx.tables[0].prolong(lo)
+    assert rel(hi, o._prolong(0, lo.cpu().numpy())) <= 1e-14
+
+
+def test_gmres_dense_kat(cuda):
+    # reference tests/test_newton_krylov.py:29-48 on device vectors
+    rng = np.random.default_rng(7)
+    n = 40
+    A = rng.standard_normal((n, n))
+    A = A @ A.T + n * np.eye(n)
+    b = rng.standard_normal(n)
+    Ad = t(A)
+    x, it, rr = nk.gmres_solve(lambda v: Ad @ v, t(b), nk.KrylovConfig(kdim=40, rtol=1e-12))
+    assert np.allclose(x.cpu().numpy(), np.linalg.solve(A, b), atol=1e-8) and rr <= 1e-12
+    x, it, rr = nk.gmres_solve(lambda v: Ad @ v, t(b), nk.KrylovConfig(kdim=5, max_restarts=60, rtol=1e-10))
+    assert rr <= 1e-10 and it > 5
+    with pytest.raises(RuntimeError, match="iteration 1"):
+        nk.gmres_solve(lambda v: torch.full_like(v, float("nan")), t(b), nk.KrylovConfig())
+    D = t(np.diag([2.0, 3.0, 4.0, 5.0]))
+    x, it, rr = nk.gmres_solve(lambda v: D @ v, t([1.0, 1.0, 0.0, 0.0]), nk.KrylovConfig(kdim=10, rtol=1e-13))
+    assert it <= 3
+
+
+def test_precondition_matches_reference(cuda):
+    c = cases.config(1)
+    d = Discretization(c.mesh, c.p, c.eqn)
+    ctx = pmg.PmgContext(d, pmg.PmgPrecondConfig(pmg.PHierarchy.parse("3-2", "2"), smoother_shift=50.0))
+    ctx.prepare(t(c.q0), float(G["c1/pc_shift"]))
+    v = G["c1/v"]
+    Y = ctx.precondition(t(v / np.linalg.norm(v)))
+    assert rel(Y, G["c1/pc_Y"]) <= 1e-8
+    # deterministic
+    Y2 = ctx.precondition(t(v / np.linalg.norm(v)))
+    assert torch.equal(Y, Y2)
+
+
+def test_ej_recovery_criterion6(cuda):
+    # reference tests/test_acceptance.py:220-243: single level, one sweep
+    m = mm.generate_box(4, 4, 1.0, 1.0)
+    d = Discretization(m, 2, EquationSpec(kind="navier-stokes", mach=0.3, reynolds=100.0))
+    rng = np.random.default_rng(1)
+    q = d.free_stream_field().data.cpu().numpy()
+    q *= 1.0 + 0.01 * rng.standard_normal(len(q))
+    ctx = pmg.PmgContext(d, pmg.PmgPrecondConfig(pmg.PHierarchy.parse("2", "1", "ej")))
+    ctx.prepare(t(q), 30.0)
+    X = rng.standard_normal(d.n_dofs)
+    Y = ctx.precondition(t(X))
+    ref = nk.ej_apply(nk.assemble_element_blocks(d, t(q), 30.0), t(X))
+    assert float((Y - ref).abs().max()) <= 1e-12
+
+
+def test_esdirk2_step_config1_matches_reference(cuda):
+    c = cases.config(1)
+    d = Discretization(c.mesh, c.p, c.eqn)
+    cfg = {"case.precond": "pmg", "pmg.levels": "3-2", "pmg.smooth": "2", "pmg.smoother_shift": 50.0,
+           "gmres.kdim": 30, "gmres.rtol": 1e-3, "ptc.dtau_init": c.dt, "ptc.rtol": 1e-4}
+    drv = ImplicitDriver(d, cfg)
+    counts = []
+    orig = nk.gmres_solve
+
+    def logged(*a, **k):
+        r = orig(*a, **k)
+        counts.append(r[1])
+        return r
+    nk.gmres_solve = logged
+    try:
+        q1, info = drv.step(t(c.q0), c.dt, ti.get_scheme("esdirk2"))
+    finally:
+        nk.gmres_solve = orig
+    ref = list(G["c1/esdirk2/gmres_counts"])
+    assert len(counts) == len(ref), (counts, ref)
+    assert all(abs(a - b) <= 1 for a, b in zip(counts, ref)), (counts, ref)
+    assert [i["iters"] for i in info] == list(G["c1/esdirk2/ptc_iters"])
+    assert rel(q1, G["c1/esdirk2/q1"]) <= 1e-7
+
+
+def test_row4_step_config1_matches_reference(cuda):
+    c = cases.config(1)
+    d = Discretization(c.mesh, c.p, c.eqn)
+    cfg = {"case.precond": "pmg", "pmg.levels": "3-2", "pmg.smooth": "2", "pmg.smoother_shift": 50.0,
+           "gmres.kdim": 30, "gmres.rtol": 1e-3}
+    drv = ImplicitDriver(d, cfg)
+    q1, info = drv.step(t(c.q0), c.dt, ti.get_scheme("row4"))
+    counts = [i["iters"] for i in info]
+    ref = list(G["c1/row4/gmres_counts"])
+    assert all(abs(a - b) <= 1 for a, b in zip(counts, ref)), (counts, ref)
+    assert rel(q1, G["c1/row4/q1"]) <= 1e-6
+
+
+def test_pmg_solve_lowmach_matches_reference(cuda):
+    c = cases.config(3, nx=4)
+    d = Discretization(c.mesh, 4, c.eqn)
+    ctx = pmg.PmgContext(d, pmg.PmgPrecondConfig(pmg.PHierarchy.parse("4-3-2-1-0", "2"), smoother_shift=1e3))
+    q, st = pmg.pmg_solve(ctx, t(c.q0), nk.PtcConfig(dtau_init=0.1, max_iters=6, rtol=1e-10))
+    h = np.array(st["history"])
+    ref = G["c3/history"]
+    assert h.shape == ref.shape
+    assert np.allclose(h[:, 1], ref[:, 1], rtol=2e-3, atol=1e-12)
+    assert rel(q, G["c3/q"]) <= 1e-9
+
+
+def test_ptc_halves_on_nonphysical(cuda):
+    # a stage solve that drives the state non-physical must halve dtau
+    m = mm.generate_box(2, 2, 1.0, 1.0, periodic=True)
+    eqn = EquationSpec(kind="euler", mach=0.3)
+    d = Discretization(m, 1, eqn)
+    q0 = d.free_stream_field().data
+    calls = []
+
+    def F(q):
+        calls.append(1)
+        if len(calls) >= 2:
+            bad = q.clone()
+            bad[0] = -1.0
+            return d.eval(bad, _lib.EPI_NEG_R)
+        return d.eval(q, _lib.EPI_NEG_R) + 1.0
+    q, st = nk.ptc_solve(F, q0, nk.PtcConfig(dtau_init=1.0, max_iters=10, rtol=1e-10), nk.KrylovConfig())
+    assert st["aborted"] and not st["converged"]
+
+
+def _c2_small(nx):
+    c = cases.config(2, nx=nx)
+    return c, OracleDisc(c.mesh, c.p, c.eqn), Discretization(c.mesh, c.p, c.eqn)
+
+
+def test_transfers_4_2_match_oracle(cuda):
+    c, o, d = _c2_small(8)
+    ctx = pmg.PmgContext(d, pmg.PmgPrecondConfig(pmg.PHierarchy.parse("4-2-0")))
+    om = so.Pmg(o, "4-2-0", 1)
+    lo = ctx.tables[0].restrict(t(c.q0))
+    assert rel(lo, om._restrict(0, c.q0)) <= 1e-14
+    lo0 = ctx.tables[1].restrict(lo)
+    assert rel(lo0, om._restrict(1, lo.cpu().numpy())) <= 1e-14
+    base = lo * 0.5
+    hi = t(c.q0)
+    ctx.tables[0].prolong_add(lo, base, hi)
+    ref = c.q0 + om._prolong(0, (lo - base).cpu().numpy())
+    assert rel(hi, ref) <= 1e-14
+
+
+def test_precondition_p4_matches_oracle(cuda):
+    c, o, d = _c2_small(8)
+    sch = ti.get_scheme("esdirk2")
+    shift = 1.0 / (float(sch.a[1, 1]) * c.dt) + 1.0 / c.dt
+    ctx = pmg.PmgContext(d, pmg.PmgPrecondConfig(pmg.PHierarchy.parse("4-2", "2"), smoother_shift=50.0))
+    ctx.prepare(t(c.q0), shift)
+    om = so.Pmg(o, "4-2", 2, smoother_shift=50.0)
+    om.prepare(c.q0, shift)
+    rng = np.random.default_rng(5)
+    X = rng.standard_normal(o.n_dofs)
+    X /= np.linalg.norm(X)
+    assert rel(ctx.precondition(t(X)), om.precondition(X)) <= 1e-8
+    # the block inverse of the fine level matches NumPy's inverse of the FD blocks
+    ob = so.assemble_blocks(o, c.q0, shift + 50.0)
+    db = nk.assemble_element_blocks(d, t(c.q0), shift + 50.0)
+    assert rel(db.inv[0], ob.inv) <= 1e-8  # FD blocks carry the 1/eps rounding amplification
+
+
+def test_esdirk2_step_config2_physics_small_mesh(cuda):
+    c, o, d = _c2_small(16)
+    drv_o = so.Driver(o, "pmg", "4-2", 2, smoother_shift=50.0, gmres_rtol=1e-3, dtau_init=c.dt)
+    s = ti.get_scheme("esdirk2")
+    q_o = drv_o.esdirk_step(c.q0, c.dt, s.a, s.b)
+    cfg = {"case.precond": "pmg", "pmg.levels": "4-2", "pmg.smooth": "2", "pmg.smoother_shift": 50.0,
+           "gmres.kdim": 30, "gmres.rtol": 1e-3, "ptc.dtau_init": c.dt, "ptc.rtol": 1e-4}
+    q_d, info = ImplicitDriver(d, cfg).step(t(c.q0), c.dt, s)
+    assert [i["iters"] for i in info] == [r[1] for r in drv_o.records]
+    assert all(abs(a - b) <= 1 for a, b in zip([i["gmres_iters"] for i in info], [r[2] for r in drv_o.records]))
+    assert rel(q_d, q_o) <= 1e-7
