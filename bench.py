@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--no-step", action="store_true", help="skip the JFNK-pMG time-step timings")
     ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU-oracle baseline sample")
     return ap.parse_args()
 
 
@@ -311,6 +312,8 @@ def run_ours(args):
     }
     # CPU baseline: the oracle on this host, bounded sample
     try:
+        if args.no_cpu:
+            raise RuntimeError("skipped (--no-cpu)")
         os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
         cpu_rate, best, ncall = cpu_residual_rate(case, seconds_budget=15.0)
         line["cpu_baseline"] = {"value": cpu_rate, "unit": UNIT, "cores": 1, "kind": "port",

@@ -12,7 +12,7 @@ import ctypes
 import os
 from pathlib import Path
 
-_LIB_PATH = Path(__file__).resolve().with_name("libpmgflow_b200.so")
+_LIB_PATH = Path(os.environ.get("PMGB_LIB") or Path(__file__).resolve().with_name("libpmgflow_b200.so"))
 _lib = None
 
 c_double_p = ctypes.POINTER(ctypes.c_double)

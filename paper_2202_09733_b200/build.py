@@ -24,10 +24,10 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "--fmad=true"]
 
 
-def _compile(src: str, verbose: bool) -> Path:
-    obj = CSRC / "build" / (Path(src).stem + ".o")
+def _compile(src: str, verbose: bool, defines=(), tag: str = "") -> Path:
+    obj = CSRC / ("build" + tag) / (Path(src).stem + ".o")
     obj.parent.mkdir(exist_ok=True)
-    cmd = [NVCC, *FLAGS, "-c", str(CSRC / src), "-o", str(obj)]
+    cmd = [NVCC, *FLAGS, *defines, "-c", str(CSRC / src), "-o", str(obj)]
     if verbose:
         cmd += ["-Xptxas", "-v"]
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -46,19 +46,27 @@ def needs_build() -> bool:
     return any(p.stat().st_mtime > t for p in deps if p.exists())
 
 
-def build(verbose: bool = False, force: bool = False) -> Path:
-    if not force and not needs_build():
+def build(verbose: bool = False, force: bool = False, defines=(), out: Path | None = None) -> Path:
+    """Build the library; ``defines``/``out`` produce experiment variants
+    (e.g. -DPMGB_CTA_THREADS=32 into libpmgflow_b200_v32.so) loaded via
+    the PMGB_LIB environment variable -- the shipped default is LIB."""
+    target = out or LIB
+    if not force and out is None and not defines and not needs_build():
         return LIB
+    tag = "" if target == LIB else "_" + target.stem
     with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
-        objs = list(ex.map(lambda s: _compile(s, verbose), SOURCES))
-    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(LIB),
+        objs = list(ex.map(lambda s: _compile(s, verbose, defines, tag), SOURCES))
+    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(target),
            *map(str, objs), "-lcudart"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr[-4000:]}")
-    return LIB
+    return target
 
 
 if __name__ == "__main__":
     v = "--verbose" in sys.argv
-    print(build(verbose=v, force="--force" in sys.argv or v))
+    defs = [a for a in sys.argv[1:] if a.startswith("-D")]
+    outs = [a.split("=", 1)[1] for a in sys.argv[1:] if a.startswith("--out=")]
+    out = HERE / outs[0] if outs else None
+    print(build(verbose=v, force="--force" in sys.argv or v, defines=defs, out=out))

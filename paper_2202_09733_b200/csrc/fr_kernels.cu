@@ -57,9 +57,10 @@ struct SL {
 };
 
 template <int P> struct MinBlocks {
-  static constexpr int ASM = (BC<P>::THREADS >= 256) ? 2 : 5;
-  static constexpr int FVN = (BC<P>::THREADS >= 256) ? 3 : 6;
-  static constexpr int TRACE = (BC<P>::THREADS >= 256) ? 4 : 8;
+  static constexpr int cap(int v) { return v < 1 ? 1 : (v > 32 ? 32 : v); }
+  static constexpr int ASM = cap(65536 / (BC<P>::THREADS * PMGB_REG_TARGET));
+  static constexpr int FVN = cap(65536 / (BC<P>::THREADS * 80));
+  static constexpr int TRACE = cap(65536 / (BC<P>::THREADS * 64));
 };
 
 struct Ops {

@@ -30,9 +30,18 @@ template <> struct KT<K_ADV>   { static constexpr int NV = 1, NW = 1; static con
 template <> struct KT<K_ADVD>  { static constexpr int NV = 1, NW = 1; static constexpr bool VISC = true,  FLOW = false; };
 
 // CTA shape: one thread per solution point, EPB elements per CTA.
+#ifndef PMGB_CTA_THREADS
+#define PMGB_CTA_THREADS 128
+#endif
+#ifndef PMGB_CTA_THREADS_P5
+#define PMGB_CTA_THREADS_P5 256
+#endif
+#ifndef PMGB_REG_TARGET
+#define PMGB_REG_TARGET 96
+#endif
 template <int P> struct BC {
   static constexpr int N = P + 1, NP = N * N, NF = 4 * N;
-  static constexpr int THREADS = (P >= 5) ? 256 : 128;
+  static constexpr int THREADS = (P >= 5) ? PMGB_CTA_THREADS_P5 : PMGB_CTA_THREADS;
   static constexpr int EPB = (THREADS / NP) > 32 ? 32 : ((THREADS / NP) >= 1 ? THREADS / NP : 1);
 };
 
