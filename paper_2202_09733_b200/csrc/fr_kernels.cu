@@ -92,7 +92,29 @@ __device__ __forceinline__ int fpt(int f, int k, int i) {
   return f == 0 ? i * N + k : f == 1 ? k * N + i : f == 2 ? i * N + (N - 1 - k) : (N - 1 - k) * N + i;
 }
 
-__device__ __forceinline__ double rcp(double x) { return __drcp_rn(x); }
+// Reciprocal and square root without the IEEE slow-path branches of
+// __drcp_rn / sqrt: MUFU seed + two Newton steps (~1 ulp; parity budget
+// is 1e-12 relative).  Valid states only feed positive normal inputs;
+// non-physical inputs still produce NaN/Inf, and the physicality flags are
+// evaluated on the raw state, not through these.
+__device__ __forceinline__ double rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
+__device__ __forceinline__ double fsqrt(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  // two Newton steps on y ~ 1/sqrt(x), then s = x y with one correction
+  y = y * fma(-0.5 * x * y, y, 1.5);
+  y = y * fma(-0.5 * x * y, y, 1.5);
+  const double s = x * y;
+  return fma(0.5 * y, fma(-s, s, x), s);
+}
 
 // ---------------------------------------------------------------------------
 // pointwise physics (spatial.py:94-203)
@@ -119,14 +141,14 @@ __device__ __forceinline__ void roe(const double* qL, const double* qR, double n
   const double EpL = qL[3] + pL, EpR = qR[3] + pR;
   const double HL = EpL * irL;
   const double HR = EpR * irR;
-  const double sL = sqrt(rL), sR = sqrt(rR);
+  const double sL = fsqrt(rL), sR = fsqrt(rR);
   const double w = sL * rcp(sL + sR), w1 = 1.0 - w;
   const double u = w * uL + w1 * uR;
   const double v = w * vL + w1 * vR;
   const double H = w * HL + w1 * HR;
   const double ke = 0.5 * (u * u + v * v);
   const double c2 = (g - 1.0) * (H - ke);
-  const double c = sqrt(c2);
+  const double c = fsqrt(c2);
   const double ic2 = rcp(c2);
   const double rb = sL * sR;
   const double un = u * nx + v * ny;
@@ -261,6 +283,13 @@ __device__ __forceinline__ void load_points(const double* __restrict__ src, int6
 }
 
 template <int P>
+__device__ __forceinline__ void load_links(const int2* __restrict__ link, int64_t e0, int64_t M, int2* sLK) {
+  constexpr int E = BC<P>::EPB;
+  const int64_t lim = (M - e0) * 4;
+  for (int i = threadIdx.x; i < E * 4; i += blockDim.x) sLK[i] = (i < lim) ? link[e0 * 4 + i] : make_int2(-1, 0);
+}
+
+template <int P>
 __device__ __forceinline__ void load_geom(const double* __restrict__ geom, int64_t e0, int64_t M, double* sG) {
   constexpr int E = BC<P>::EPB;
   const int64_t lim = (M - e0) * 20;
@@ -268,14 +297,33 @@ __device__ __forceinline__ void load_geom(const double* __restrict__ geom, int64
   for (int i = threadIdx.x; i < E * 20; i += blockDim.x) sG[i] = (i < lim) ? __ldg(base + i) : 0.0;
 }
 
+// Interpolation line of face f, point k: points base + i * stride, i < N
+struct Line {
+  int base, stride;
+  const double* w;
+};
+template <int N>
+__device__ __forceinline__ Line face_line(const Ops& op, int f, int k) {
+  Line L;
+  L.base = f == 0 ? k : f == 1 ? k * N : f == 2 ? (N - 1 - k) : (N - 1 - k) * N;
+  L.stride = (f == 0 || f == 2) ? N : 1;
+  L.w = (f == 0 || f == 3) ? op.eL : op.eR;
+  return L;
+}
+
+template <int N>
+__device__ __forceinline__ double line_sum(const Line& L, const double* plane_el) {
+  double s = 0.0;
+  const double* x = plane_el + L.base;
+#pragma unroll
+  for (int i = 0; i < N; ++i) s += L.w[i] * x[i * L.stride];
+  return s;
+}
+
 // trace of one point plane (already offset to the element) at face (f, k)
 template <int N>
 __device__ __forceinline__ double line_sum(const Ops& op, const double* plane_el, int f, int k) {
-  const double* w = (f == 0 || f == 3) ? op.eL : op.eR;
-  double s = 0.0;
-#pragma unroll
-  for (int i = 0; i < N; ++i) s += w[i] * plane_el[fpt<N>(f, k, i)];
-  return s;
+  return line_sum<N>(face_line<N>(op, f, k), plane_el);
 }
 
 template <int NV>
@@ -584,6 +632,8 @@ k_fvn(const FrConst C, const FrMesh m, const double* __restrict__ q, const doubl
   const int64_t e0 = (int64_t)blockIdx.x * E;
   const int64_t M = m.M;
   const Phys ph = phys_of(C);
+  __shared__ int2 sLK[E * 4];
+  load_links<P>(m.link, e0, M, sLK);
   load_points<P, NV>(q, e0, M, sQ);
   load_geom<P>(m.geom, e0, M, sG);
   __syncthreads();
@@ -599,13 +649,15 @@ k_fvn(const FrConst C, const FrMesh m, const double* __restrict__ q, const doubl
     const int el = t / NF, r = t % NF, f = r / N, k = r % N;
     const int64_t e = e0 + el;
     if (e >= M) continue;
-    const int2 lk = m.link[e * 4 + f];
+    const int2 lk = sLK[el * 4 + f];
+    const bool interior = lk.x >= 0;
+    const int kk = lk_rev(lk.y) ? N - 1 - k : k;
+    const int64_t own = ((e * 4 + f) * N + k) * NV;
+    const int64_t nbi = interior ? (((int64_t)lk.x * 4 + lk_face(lk.y)) * N + kk) * NV : own;
     double tr[NV], nb[NV];
-    ld_face<NV>(qtr + ((e * 4 + f) * N + k) * NV, tr);
-    if (lk.x >= 0) {
-      const int kk = lk_rev(lk.y) ? N - 1 - k : k;
-      ld_face<NV>(qtr + (((int64_t)lk.x * 4 + lk_face(lk.y)) * N + kk) * NV, nb);
-    } else {
+    ld_face<NV>(qtr + own, tr);
+    ld_face<NV>(qtr + nbi, nb);
+    if (!interior) {
       const double* gq = sG + el * 20;
       ghost<KIND>(tr, lk_tag(lk.y), gq[8 + 2 * f], gq[9 + 2 * f], C.qinf, nb);
     }
@@ -723,6 +775,8 @@ k_assemble(const FrConst C, const FrMesh m, const double* __restrict__ q, const 
   const int64_t e0 = (int64_t)blockIdx.x * E;
   const int64_t M = m.M;
   const Phys ph = phys_of(C);
+  __shared__ int2 sLK[E * 4];
+  load_links<P>(m.link, e0, M, sLK);
   load_points<P, NV>(q, e0, M, sQ);
   load_geom<P>(m.geom, e0, M, sG);
   __syncthreads();
@@ -737,34 +791,43 @@ k_assemble(const FrConst C, const FrMesh m, const double* __restrict__ q, const 
     }
   }
   // common face fluxes: inviscid on the L side's normal (-F to R), viscous
-  // 0.5 (fvn_own - fvn_nb), BR1 average (spatial.py:520-568)
+  // 0.5 (fvn_own - fvn_nb), BR1 average (spatial.py:520-568).  Branch-free
+  // across L/R sides: operands are selected, one Roe evaluation per thread.
   for (int t = threadIdx.x; t < E * NF; t += blockDim.x) {
     const int el = t / NF, r = t % NF, f = r / N, k = r % N;
     const int64_t e = e0 + el;
     if (e >= M) continue;
-    const int2 lk = m.link[e * 4 + f];
+    const int2 lk = sLK[el * 4 + f];
     const double* gq = sG + el * 20;
     const double nx = gq[8 + 2 * f], ny = gq[9 + 2 * f];
-    double tr[NV], nb[NV], F[NV];
+    const bool interior = lk.x >= 0;
+    const int kk = lk_rev(lk.y) ? N - 1 - k : k;
     const int64_t own = ((e * 4 + f) * N + k) * NV;
+    const int64_t nbi = interior ? (((int64_t)lk.x * 4 + lk_face(lk.y)) * N + kk) * NV : own;
+    double tr[NV], nb[NV], F[NV], Fo[NV], Fn[NV];
     ld_face<NV>(qtr + own, tr);
-    int64_t nbi = -1;
-    if (lk.x >= 0) {
-      const int kk = lk_rev(lk.y) ? N - 1 - k : k;
-      nbi = (((int64_t)lk.x * 4 + lk_face(lk.y)) * N + kk) * NV;
-      ld_face<NV>(qtr + nbi, nb);
-      if (lk_left(lk.y)) {
-        num_flux<KIND>(tr, nb, nx, ny, ph, F);
-      } else {
-        const double* gn = m.geom + (int64_t)lk.x * 20 + 8 + 2 * lk_face(lk.y);
-        num_flux<KIND>(nb, tr, __ldg(gn), __ldg(gn + 1), ph, F);
-#pragma unroll
-        for (int v = 0; v < NV; ++v) F[v] = -F[v];
-      }
-    } else {
-      ghost<KIND>(tr, lk_tag(lk.y), nx, ny, C.qinf, nb);
-      num_flux<KIND>(tr, nb, nx, ny, ph, F);
+    ld_face<NV>(qtr + nbi, nb);
+    if constexpr (VISC) {
+      ld_face<NV>(fvn + own, Fo);
+      ld_face<NV>(fvn + nbi, Fn);
     }
+    const bool left = !interior || lk_left(lk.y);
+    double nux = nx, nuy = ny;
+    if (!left) {
+      const double* gn = m.geom + (int64_t)lk.x * 20 + 8 + 2 * lk_face(lk.y);
+      nux = __ldg(gn);
+      nuy = __ldg(gn + 1);
+    }
+    if (!interior) ghost<KIND>(tr, lk_tag(lk.y), nx, ny, C.qinf, nb);
+    double qa[NV], qc[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      qa[v] = left ? tr[v] : nb[v];
+      qc[v] = left ? nb[v] : tr[v];
+    }
+    num_flux<KIND>(qa, qc, nux, nuy, ph, F);
+#pragma unroll
+    for (int v = 0; v < NV; ++v) F[v] = left ? F[v] : -F[v];
     if constexpr (VISC) {
       double wa[NW], wc[NW];
       grad_vars<KIND>(tr, ph.gamma, wa);
@@ -772,15 +835,9 @@ k_assemble(const FrConst C, const FrMesh m, const double* __restrict__ q, const 
 #pragma unroll
       for (int c = 0; c < NW; ++c) sWH[c * NFT + t] = 0.5 * (wa[c] + wc[c]);
       double Fv[NV];
-      ld_face<NV>(fvn + own, Fv);
-      if (nbi >= 0) {
-        double Fn[NV];
-        ld_face<NV>(fvn + nbi, Fn);
 #pragma unroll
-        for (int v = 0; v < NV; ++v) Fv[v] = 0.5 * (Fv[v] - Fn[v]);
-      } else if (KT<KIND>::FLOW && lk_tag(lk.y) == T_WALL_ADIABATIC) {
-        Fv[NV - 1] = 0.0;
-      }
+      for (int v = 0; v < NV; ++v) Fv[v] = interior ? 0.5 * (Fo[v] - Fn[v]) : Fo[v];
+      if (KT<KIND>::FLOW && !interior && lk_tag(lk.y) == T_WALL_ADIABATIC) Fv[NV - 1] = 0.0;
 #pragma unroll
       for (int v = 0; v < NV; ++v) F[v] = F[v] - Fv[v];
     }
