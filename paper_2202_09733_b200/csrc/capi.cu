@@ -97,6 +97,7 @@ PMGB_API int pmgb_disc_create(const pmgb_disc_desc* desc, pmgb_disc** out) {
   if (!err) err = cudaMalloc(&d.qtr, face_bytes);
   if (!err) err = cudaMalloc(&d.fvn, face_bytes);
   if (!err) err = cudaMalloc(&d.qp, sizeof(double) * (size_t)d.n_dofs);
+  if (!err) err = cudaMalloc(&d.grad, sizeof(double) * (size_t)d.M * n * n * (d.nv == 4 ? 6 : 2));
   if (!err) err = cudaMemcpy(d.geom, desc->geom, sizeof(double) * 20 * (size_t)d.M, cudaMemcpyHostToDevice);
   if (!err) err = cudaMemcpy(d.link, lk.data(), sizeof(int2) * 4 * (size_t)d.M, cudaMemcpyHostToDevice);
   if (err) {
@@ -117,6 +118,7 @@ PMGB_API int pmgb_disc_destroy(pmgb_disc* h) {
   cudaFree(h->d.qtr);
   cudaFree(h->d.fvn);
   cudaFree(h->d.qp);
+  cudaFree(h->d.grad);
   delete h;
   return 0;
 }

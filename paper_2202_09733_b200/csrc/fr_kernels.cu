@@ -49,9 +49,14 @@ struct SL {
   static constexpr int R0 = TR + NV * NFT;        // [NP*NV]             unperturbed local residual
   static constexpr int END_LOCAL = R0 + NP * NV;
   static constexpr int GR_FVN = FC;               // k_fvn keeps gradients where FC would be
+  // compact layout of k_assemble (gradients come from k_fvn)
+  static constexpr int A_FC = Q + NV * NPT;
+  static constexpr int A_FT = A_FC + NV * NFT;
+  static constexpr int A_GT = A_FT + NV * NPT;
+  static constexpr int A_CF = A_GT + NV * NPT;
   static constexpr size_t BYTES_TRACE = sizeof(double) * (Q + NV * NPT);
   static constexpr size_t BYTES_FVN = sizeof(double) * (GR_FVN + 2 * NW * NPT);
-  static constexpr size_t BYTES_ASM = sizeof(double) * END_ASM;
+  static constexpr size_t BYTES_ASM = sizeof(double) * (A_CF + NV * NFT);
   static constexpr size_t BYTES_LOCAL = sizeof(double) * END_LOCAL;
   static_assert(2 * NW >= NV || true, "CF alias");
 };
@@ -270,15 +275,32 @@ __device__ __forceinline__ Phys phys_of(const FrConst& C) {
 // ---------------------------------------------------------------------------
 // staging helpers
 
-// element-major AoS global (E elements from e0) -> SoA point planes
+// element-major AoS global (E elements from e0) -> SoA point planes.
+// NV = 4: one thread per point, two 16-byte loads (rows are 32 B aligned).
 template <int P, int NV>
 __device__ __forceinline__ void load_points(const double* __restrict__ src, int64_t e0, int64_t M, double* sQ) {
   constexpr int NP = BC<P>::NP, E = BC<P>::EPB, NPT = E * NP;
-  const int64_t lim = (M - e0) * NP * NV;
-  const double* base = src + e0 * NP * NV;
-  for (int i = threadIdx.x; i < NPT * NV; i += blockDim.x) {
-    const int v = i % NV, g = i / NV;
-    sQ[v * NPT + g] = (i < lim) ? __ldg(base + i) : 1.0;
+  if constexpr (NV == 4) {
+    const int64_t lim = (M - e0) * NP;
+    const double2* base = reinterpret_cast<const double2*>(src + e0 * NP * 4);
+    for (int g = threadIdx.x; g < NPT; g += blockDim.x) {
+      double2 a = make_double2(1.0, 1.0), b = make_double2(1.0, 1.0);
+      if (g < lim) {
+        a = __ldg(base + 2 * g);
+        b = __ldg(base + 2 * g + 1);
+      }
+      sQ[g] = a.x;
+      sQ[NPT + g] = a.y;
+      sQ[2 * NPT + g] = b.x;
+      sQ[3 * NPT + g] = b.y;
+    }
+  } else {
+    const int64_t lim = (M - e0) * NP * NV;
+    const double* base = src + e0 * NP * NV;
+    for (int i = threadIdx.x; i < NPT * NV; i += blockDim.x) {
+      const int v = i % NV, g = i / NV;
+      sQ[v * NPT + g] = (i < lim) ? __ldg(base + i) : 1.0;
+    }
   }
 }
 
@@ -617,7 +639,7 @@ k_trace(const FrConst C, const FrMesh m, const double* __restrict__ q, const dou
 template <int P, int KIND>
 __global__ void __launch_bounds__(BC<P>::THREADS, MinBlocks<P>::FVN)
 k_fvn(const FrConst C, const FrMesh m, const double* __restrict__ q, const double* __restrict__ qtr,
-      double* __restrict__ fvn) {
+      double* __restrict__ fvn, double* __restrict__ grad) {
   extern __shared__ double sm[];
   using L = SL<P, KIND>;
   constexpr int N = BC<P>::N, NP = BC<P>::NP, NF = BC<P>::NF, E = BC<P>::EPB;
@@ -682,6 +704,14 @@ k_fvn(const FrConst C, const FrMesh m, const double* __restrict__ q, const doubl
     for (int c = 0; c < NW; ++c) {
       sGR[c * NPT + t0] = gx[c];
       sGR[(NW + c) * NPT + t0] = gy[c];
+    }
+    if (grad != nullptr && e0 + el < M) {
+      double* gd = grad + ((e0 + el) * NP + pt) * (2 * NW);
+#pragma unroll
+      for (int c = 0; c < NW; ++c) {
+        gd[c] = gx[c];
+        gd[NW + c] = gy[c];
+      }
     }
   }
   __syncthreads();
@@ -755,7 +785,8 @@ __device__ __forceinline__ void commit_status(int* bad, Status* st) {
 template <int P, int KIND>
 __global__ void __launch_bounds__(BC<P>::THREADS, MinBlocks<P>::ASM)
 k_assemble(const FrConst C, const FrMesh m, const double* __restrict__ q, const double* __restrict__ qtr,
-           const double* __restrict__ fvn, const Epi ep, double* __restrict__ out, int* bad, Status* st) {
+           const double* __restrict__ fvn, const double* __restrict__ grad, const Epi ep,
+           double* __restrict__ out, int* bad, Status* st) {
   extern __shared__ double sm[];
   using L = SL<P, KIND>;
   constexpr int N = BC<P>::N, NP = BC<P>::NP, NF = BC<P>::NF, E = BC<P>::EPB;
@@ -765,13 +796,10 @@ k_assemble(const FrConst C, const FrMesh m, const double* __restrict__ q, const 
   const Ops op = stage_ops(C, sm);
   double* sQ = sm + L::Q;
   double* sG = sm + L::G;
-  double* sW = sm + L::W;
-  double* sFC = sm + L::FC;
-  double* sWH = sm + L::WH;
-  double* sCG = sm + L::CG;
-  double* sFT = sm + L::FT;
-  double* sGT = sm + L::GT;
-  double* sCF = sm + L::CF;
+  double* sFC = sm + L::A_FC;
+  double* sFT = sm + L::A_FT;
+  double* sGT = sm + L::A_GT;
+  double* sCF = sm + L::A_CF;
   const int64_t e0 = (int64_t)blockIdx.x * E;
   const int64_t M = m.M;
   const Phys ph = phys_of(C);
@@ -781,15 +809,6 @@ k_assemble(const FrConst C, const FrMesh m, const double* __restrict__ q, const 
   load_geom<P>(m.geom, e0, M, sG);
   __syncthreads();
   const int t0 = threadIdx.x;
-  if constexpr (VISC) {
-    if (t0 < NPT) {
-      double qq[NV], w[NW];
-      gather_point<NV, NPT>(sQ, t0, qq);
-      grad_vars<KIND>(qq, ph.gamma, w);
-#pragma unroll
-      for (int c = 0; c < NW; ++c) sW[c * NPT + t0] = w[c];
-    }
-  }
   // common face fluxes: inviscid on the L side's normal (-F to R), viscous
   // 0.5 (fvn_own - fvn_nb), BR1 average (spatial.py:520-568).  Branch-free
   // across L/R sides: operands are selected, one Roe evaluation per thread.
@@ -829,11 +848,6 @@ k_assemble(const FrConst C, const FrMesh m, const double* __restrict__ q, const 
 #pragma unroll
     for (int v = 0; v < NV; ++v) F[v] = left ? F[v] : -F[v];
     if constexpr (VISC) {
-      double wa[NW], wc[NW];
-      grad_vars<KIND>(tr, ph.gamma, wa);
-      grad_vars<KIND>(nb, ph.gamma, wc);
-#pragma unroll
-      for (int c = 0; c < NW; ++c) sWH[c * NFT + t] = 0.5 * (wa[c] + wc[c]);
       double Fv[NV];
 #pragma unroll
       for (int v = 0; v < NV; ++v) Fv[v] = interior ? 0.5 * (Fo[v] - Fn[v]) : Fo[v];
@@ -844,19 +858,36 @@ k_assemble(const FrConst C, const FrMesh m, const double* __restrict__ q, const 
 #pragma unroll
     for (int v = 0; v < NV; ++v) sFC[v * NFT + t] = F[v];
   }
-  __syncthreads();
-  if constexpr (VISC) {
-    for (int t = threadIdx.x; t < E * NF; t += blockDim.x) {
-      const int el = t / NF, r = t % NF, f = r / N, k = r % N;
-      if (e0 + el >= M) continue;
-      grad_corrections<P, KIND>(op, sW, sG + el * 20, sWH, sCG, el, f, k);
-    }
-    __syncthreads();
-  }
+  // volume fluxes at the points: gradients come from k_fvn (same values
+  // it used for the one-sided viscous fluxes)
   if (t0 < NPT) {
     const int el = t0 / NP, pt = t0 % NP, a = pt / N, b = pt % N;
     double gx[NW], gy[NW];
-    if constexpr (VISC) gradient_at<P, KIND>(op, sW, sG + el * 20, sCG, el, a, b, gx, gy);
+    if constexpr (VISC) {
+      if (e0 + el < M) {
+        const double* gs = grad + ((e0 + el) * NP + pt) * (2 * NW);
+        if constexpr (NW == 3) {
+          const double2 g0 = __ldg(reinterpret_cast<const double2*>(gs));
+          const double2 g1 = __ldg(reinterpret_cast<const double2*>(gs) + 1);
+          const double2 g2 = __ldg(reinterpret_cast<const double2*>(gs) + 2);
+          gx[0] = g0.x;
+          gx[1] = g0.y;
+          gx[2] = g1.x;
+          gy[0] = g1.y;
+          gy[1] = g2.x;
+          gy[2] = g2.y;
+        } else {
+#pragma unroll
+          for (int c = 0; c < NW; ++c) {
+            gx[c] = __ldg(gs + c);
+            gy[c] = __ldg(gs + NW + c);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < NW; ++c) gx[c] = gy[c] = 0.0;
+      }
+    }
     const Metric mt = metric(sG + el * 20);
     double qq[NV], Ft[NV], Gt[NV];
     gather_point<NV, NPT>(sQ, t0, qq);
@@ -1150,8 +1181,8 @@ static int run_residual(const DiscDev& d, const double* q, const double* X, doub
   const double* qq = q;
   if (X != nullptr) qq = d.qp;
   k_trace<P, KIND><<<grid, TH, L::BYTES_TRACE, st>>>(d.C, d.mesh, q, X, eps, d.qp, d.qtr, bad);
-  if (KT<KIND>::VISC) k_fvn<P, KIND><<<grid, TH, L::BYTES_FVN, st>>>(d.C, d.mesh, qq, d.qtr, d.fvn);
-  k_assemble<P, KIND><<<grid, TH, L::BYTES_ASM, st>>>(d.C, d.mesh, qq, d.qtr, d.fvn, epi, out, bad, stp);
+  if (KT<KIND>::VISC) k_fvn<P, KIND><<<grid, TH, L::BYTES_FVN, st>>>(d.C, d.mesh, qq, d.qtr, d.fvn, d.grad);
+  k_assemble<P, KIND><<<grid, TH, L::BYTES_ASM, st>>>(d.C, d.mesh, qq, d.qtr, d.fvn, d.grad, epi, out, bad, stp);
   return (int)cudaGetLastError();
 }
 
@@ -1167,7 +1198,7 @@ static int run_freeze(const DiscDev& d, const double* q, double* qtr, double* fv
   }
   const unsigned grid = (unsigned)((d.M + E - 1) / E);
   k_trace<P, KIND><<<grid, TH, L::BYTES_TRACE, st>>>(d.C, d.mesh, q, nullptr, 0.0, nullptr, qtr, nullptr);
-  if (KT<KIND>::VISC) k_fvn<P, KIND><<<grid, TH, L::BYTES_FVN, st>>>(d.C, d.mesh, q, qtr, fvn);
+  if (KT<KIND>::VISC) k_fvn<P, KIND><<<grid, TH, L::BYTES_FVN, st>>>(d.C, d.mesh, q, qtr, fvn, nullptr);
   return (int)cudaGetLastError();
 }
 
