@@ -20,6 +20,13 @@
 
 #include "pmgb_internal.cuh"
 
+#ifndef PMGB_FVN_REGS
+#define PMGB_FVN_REGS 64
+#endif
+#ifndef PMGB_TRACE_REGS
+#define PMGB_TRACE_REGS 40
+#endif
+
 namespace pmgb {
 
 // ---------------------------------------------------------------------------
@@ -64,8 +71,8 @@ struct SL {
 template <int P> struct MinBlocks {
   static constexpr int cap(int v) { return v < 1 ? 1 : (v > 32 ? 32 : v); }
   static constexpr int ASM = cap(65536 / (BC<P>::THREADS * PMGB_REG_TARGET));
-  static constexpr int FVN = cap(65536 / (BC<P>::THREADS * 80));
-  static constexpr int TRACE = cap(65536 / (BC<P>::THREADS * 64));
+  static constexpr int FVN = cap(65536 / (BC<P>::THREADS * PMGB_FVN_REGS));
+  static constexpr int TRACE = cap(65536 / (BC<P>::THREADS * PMGB_TRACE_REGS));
 };
 
 struct Ops {

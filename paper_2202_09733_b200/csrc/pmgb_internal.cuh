@@ -37,7 +37,7 @@ template <> struct KT<K_ADVD>  { static constexpr int NV = 1, NW = 1; static con
 #define PMGB_CTA_THREADS_P5 256
 #endif
 #ifndef PMGB_REG_TARGET
-#define PMGB_REG_TARGET 96
+#define PMGB_REG_TARGET 80
 #endif
 template <int P> struct BC {
   static constexpr int N = P + 1, NP = N * N, NF = 4 * N;
