@@ -195,11 +195,10 @@ def event_time(torch, fn, reps):
 
 def run_ours(args):
     import torch
+    from paper_2202_09733_b200 import dist as pdist
     ws, rank, local = dist_info()
     torch.cuda.set_device(local)
-    if ws > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    pdist.init("nccl", torch.device("cuda", local))
     from paper_2202_09733_b200 import _lib, cases
     from paper_2202_09733_b200.spatial import Discretization
     from paper_2202_09733_b200.vec import launch_count, stream
@@ -235,20 +234,16 @@ def run_ours(args):
         r_step(i)
         jv_step(i)
     torch.cuda.synchronize()
-    if ws > 1:
-        torch.distributed.barrier()
+    pdist.barrier()
     l0 = launch_count()
     with ClockSampler(local) as clk:
         t_r = event_time(torch, r_step, K)
     launches_r = launch_count() - l0
     t_jv = event_time(torch, jv_step, K)
-    if ws > 1:
-        tt = torch.tensor([t_r, t_jv], device="cuda", dtype=torch.float64)
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        t_r, t_jv = float(tt[0]), float(tt[1])
+    t_r, t_jv = pdist.max_over_ranks([t_r, t_jv], "cuda")
     ms_r = t_r / K * 1e3
-    rate_r = ws * n * K / t_r / 1e9
-    rate_jv = ws * n * K / t_jv / 1e9
+    rate_r = pdist.job_rate(n * K, ws, t_r) / 1e9
+    rate_jv = pdist.job_rate(n * K, ws, t_jv) / 1e9
     per_gpu_r = n / (t_r / K)
 
     # e2e through the public API with host buffers: H2D of q, R, D2H of R
@@ -263,11 +258,8 @@ def run_ours(args):
     for i in range(W):
         e2e_step(i)
     t_e2e = event_time(torch, e2e_step, K)
-    if ws > 1:
-        tt = torch.tensor([t_e2e], device="cuda", dtype=torch.float64)
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        t_e2e = float(tt[0])
-    rate_e2e = ws * n * K / t_e2e / 1e9
+    t_e2e, = pdist.max_over_ranks([t_e2e], "cuda")
+    rate_e2e = pdist.job_rate(n * K, ws, t_e2e) / 1e9
     # parity spot check of the e2e result against the device-resident path
     torch.cuda.synchronize()
 
@@ -277,8 +269,7 @@ def run_ours(args):
         step = time_steps(torch, case, args)
 
     if rank != 0:
-        if ws > 1:
-            torch.distributed.barrier()
+        pdist.barrier()
         return 0
 
     flops = FLOP_PER_DOF_R[case.p] * n
@@ -328,8 +319,7 @@ def run_ours(args):
         except Exception:
             pass
     print(json.dumps(line), flush=True)
-    if ws > 1:
-        torch.distributed.barrier()
+    pdist.barrier()
     return 0
 
 
