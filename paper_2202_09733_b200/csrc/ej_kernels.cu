@@ -31,7 +31,7 @@ template <> struct GJTile<25>  { static constexpr int TR = 5, TC = 5; };
 template <> struct GJTile<36>  { static constexpr int TR = 3, TC = 6; };
 template <> struct GJTile<64>  { static constexpr int TR = 4, TC = 8; };
 template <> struct GJTile<100> { static constexpr int TR = 4, TC = 10; };
-template <> struct GJTile<144> { static constexpr int TR = 6, TC = 12; };
+template <> struct GJTile<144> { static constexpr int TR = 8, TC = 6; };
 
 template <int SZ> struct GJShape {
   static constexpr int TR = GJTile<SZ>::TR, TC = GJTile<SZ>::TC;
@@ -41,8 +41,14 @@ template <int SZ> struct GJShape {
 };
 
 // One CTA per block.  BT: FD blocks, column-major (BT[c][r] = B[r][c]).
+// Per pivot step: column-k owners publish the column, every warp finds the
+// pivot redundantly (lane l owns rows [l*RPL, l*RPL+RPL): one max-reduction
+// + a ballot, the lowest tied lane holds the lowest row), the pivot-row
+// owners publish the normalised row, and every thread updates its tile
+// with exactly one DFMA per entry (pivot row / pivot column zeroed first,
+// the pivot row's multiplier is 1).
 template <int SZ>
-__global__ void __launch_bounds__(GJShape<SZ>::THREADS)
+__global__ void __launch_bounds__(GJShape<SZ>::THREADS, (GJShape<SZ>::THREADS <= 256 ? 2 : 1))
 k_gj_inverse(const double* __restrict__ BT, double* __restrict__ XT, uint8_t* __restrict__ perm, Status* st) {
   using S = GJShape<SZ>;
   constexpr int TR = S::TR, TC = S::TC, NRG = S::NRG, NCG = S::NCG, RPL = S::ROWS_PER_LANE;
@@ -67,84 +73,92 @@ k_gj_inverse(const double* __restrict__ BT, double* __restrict__ XT, uint8_t* __
     }
   }
   if (tid == 0) s_bad = 0;
-  unsigned used = 0;  // bit m: row lane + 32 m already pivoted (per warp copy)
+  unsigned used = 0;  // bit m: row lane*RPL + m already pivoted (same in every warp)
   for (int kg = 0; kg < NCG; ++kg) {
 #pragma unroll
     for (int kk = 0; kk < TC; ++kk) {
       const int k = kg * TC + kk;
       if (k >= SZ) break;
-      const int b = k & 1;
-      if (active && cg == kg) {
+      double* cb = colbuf[k & 1];
+      double* rb = rowbuf[k & 1];
+      const bool colown = active && cg == kg;
+      if (colown) {
 #pragma unroll
         for (int i = 0; i < TR; ++i)
-          if (r0 + i < SZ) colbuf[b][r0 + i] = a[i][kk];
+          if (r0 + i < SZ) cb[r0 + i] = a[i][kk];
       }
       __syncthreads();
-      // pivot search, redundantly in every warp (deterministic)
-      double bv = -1.0;
-      int br = INT_MAX;
+      double best = -1.0;
+      int brow = -1;
 #pragma unroll
       for (int m = 0; m < RPL; ++m) {
-        const int r = lane + 32 * m;
+        const int r = lane * RPL + m;
         if (r < SZ && !((used >> m) & 1u)) {
-          const double v = fabs(colbuf[b][r]);
-          if (v > bv) {
-            bv = v;
-            br = r;
+          const double v = fabs(cb[r]);
+          if (v > best) {
+            best = v;
+            brow = r;
           }
         }
       }
+      double wmax = best;
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, bv, off);
-        const int orr = __shfl_xor_sync(0xffffffffu, br, off);
-        if (ov > bv || (ov == bv && orr < br)) {
-          bv = ov;
-          br = orr;
-        }
+        const double o = __shfl_xor_sync(0xffffffffu, wmax, off);
+        wmax = o > wmax ? o : wmax;
       }
-      const bool nan_col = (br == INT_MAX);
-      int p = nan_col ? k : br;  // every candidate NaN: flagged singular below
-      if ((p & 31) == lane) used |= 1u << (p >> 5);
-      const double pv = colbuf[b][p];
+      const unsigned ball = __ballot_sync(0xffffffffu, brow >= 0 && best == wmax);
+      const bool nan_col = (ball == 0u);
+      int p = __shfl_sync(0xffffffffu, brow, nan_col ? 0 : __ffs(ball) - 1);
+      if (nan_col) p = k;  // every candidate NaN: flagged singular below
+      if (lane == p / RPL) used |= 1u << (p - lane * RPL);
+      const double pv = cb[p];
       if (tid == 0) {
         pivs[k] = p;
         if (nan_col || !(pv != 0.0) || !isfinite(pv)) s_bad = 1;
       }
       const double pinv = 1.0 / pv;
-      if (active && rg == p / TR) {
-        const int ip = p - r0;
+      const bool rowown = active && rg == p / TR;
+      const int ip = p - r0;
+      if (rowown) {
 #pragma unroll
         for (int i = 0; i < TR; ++i) {
           if (i == ip) {
 #pragma unroll
             for (int j = 0; j < TC; ++j) {
               const int c = c0 + j;
-              if (c < SZ) rowbuf[b][c] = ((cg == kg && j == kk) ? 1.0 : a[i][j]) * pinv;
+              if (c < SZ) rb[c] = ((cg == kg && j == kk) ? 1.0 : a[i][j]) * pinv;
             }
           }
         }
       }
       __syncthreads();
       if (active) {
-        double pr[TC];
-#pragma unroll
-        for (int j = 0; j < TC; ++j) pr[j] = (c0 + j < SZ) ? rowbuf[b][c0 + j] : 0.0;
+        double g[TR];
 #pragma unroll
         for (int i = 0; i < TR; ++i) {
           const int r = r0 + i;
-          if (r >= SZ) continue;
-          if (r == p) {
+          g[i] = (r < SZ) ? ((r == p) ? 1.0 : -cb[r]) : 0.0;
+        }
+        if (colown) {
 #pragma unroll
-            for (int j = 0; j < TC; ++j) a[i][j] = pr[j];
-          } else {
-            const double f = colbuf[b][r];
+          for (int i = 0; i < TR; ++i) a[i][kk] = 0.0;
+        }
+        if (rowown) {
 #pragma unroll
-            for (int j = 0; j < TC; ++j) {
-              const double x = (cg == kg && j == kk) ? 0.0 : a[i][j];
-              a[i][j] = x - f * pr[j];
+          for (int i = 0; i < TR; ++i)
+            if (i == ip) {
+#pragma unroll
+              for (int j = 0; j < TC; ++j) a[i][j] = 0.0;
             }
-          }
+        }
+        double pr[TC];
+#pragma unroll
+        for (int j = 0; j < TC; ++j) pr[j] = (c0 + j < SZ) ? rb[c0 + j] : 0.0;
+#pragma unroll
+        for (int i = 0; i < TR; ++i) {
+#pragma unroll
+          for (int j = 0; j < TC; ++j) a[i][j] = fma(g[i], pr[j], a[i][j]);
         }
       }
     }

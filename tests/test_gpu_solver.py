@@ -75,7 +75,7 @@ def test_blocks_match_reference(cuda):
     assert np.abs(eye - np.eye(B.shape[1])).max() <= 1e-11
 
 
-@pytest.mark.parametrize("kind,p", [("euler", 1), ("ns", 2), ("ns", 3), ("ns", 4), ("advd", 2)])
+@pytest.mark.parametrize("kind,p", [("euler", 1), ("ns", 2), ("ns", 3), ("ns", 4), ("ns", 5), ("advd", 2), ("advd", 4)])
 def test_blocks_match_oracle(cuda, kind, p):
     kw = {"euler": dict(kind="euler", mach=0.3),
           "ns": dict(kind="navier-stokes", mach=0.3, reynolds=50.0),
