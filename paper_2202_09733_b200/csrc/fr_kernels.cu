@@ -661,12 +661,36 @@ k_fvn(const FrConst C, const FrMesh m, const double* __restrict__ q, const doubl
   const int64_t e0 = (int64_t)blockIdx.x * E;
   const int64_t M = m.M;
   const Phys ph = phys_of(C);
-  __shared__ int2 sLK[E * 4];
-  load_links<P>(m.link, e0, M, sLK);
+  // Prologue: q / geometry into shared memory and the face-trace gathers
+  // (own + neighbour) into registers, all before the first barrier.
+  constexpr bool ONE_FACE = (E * NF <= BC<P>::THREADS);
+  const int t0 = threadIdx.x;
   load_points<P, NV>(q, e0, M, sQ);
   load_geom<P>(m.geom, e0, M, sG);
+  double tr[NV], nb[NV];
+  int2 lk = make_int2(-1, 0);
+  bool face_live = false;
+  int fel = 0, ff = 0;
+  if constexpr (ONE_FACE) {
+    if (t0 < E * NF) {
+      fel = t0 / NF;
+      const int r = t0 % NF;
+      ff = r / N;
+      const int fk = r % N;
+      const int64_t e = e0 + fel;
+      face_live = e < M;
+      if (face_live) {
+        lk = m.link[e * 4 + ff];
+        const bool interior = lk.x >= 0;
+        const int kk = lk_rev(lk.y) ? N - 1 - fk : fk;
+        const int64_t own = ((e * 4 + ff) * N + fk) * NV;
+        const int64_t nbi = interior ? (((int64_t)lk.x * 4 + lk_face(lk.y)) * N + kk) * NV : own;
+        ld_face<NV>(qtr + own, tr);
+        ld_face<NV>(qtr + nbi, nb);
+      }
+    }
+  }
   __syncthreads();
-  const int t0 = threadIdx.x;
   if (t0 < NPT) {
     double qq[NV], w[NW];
     gather_point<NV, NPT>(sQ, t0, qq);
@@ -674,27 +698,34 @@ k_fvn(const FrConst C, const FrMesh m, const double* __restrict__ q, const doubl
 #pragma unroll
     for (int c = 0; c < NW; ++c) sW[c * NPT + t0] = w[c];
   }
-  for (int t = threadIdx.x; t < E * NF; t += blockDim.x) {
-    const int el = t / NF, r = t % NF, f = r / N, k = r % N;
-    const int64_t e = e0 + el;
-    if (e >= M) continue;
-    const int2 lk = sLK[el * 4 + f];
-    const bool interior = lk.x >= 0;
-    const int kk = lk_rev(lk.y) ? N - 1 - k : k;
-    const int64_t own = ((e * 4 + f) * N + k) * NV;
-    const int64_t nbi = interior ? (((int64_t)lk.x * 4 + lk_face(lk.y)) * N + kk) * NV : own;
-    double tr[NV], nb[NV];
-    ld_face<NV>(qtr + own, tr);
-    ld_face<NV>(qtr + nbi, nb);
-    if (!interior) {
+  auto face_avg = [&](int t, int el, int f, int2 lkk, double* tr_, double* nb_) {
+    if (lkk.x < 0) {
       const double* gq = sG + el * 20;
-      ghost<KIND>(tr, lk_tag(lk.y), gq[8 + 2 * f], gq[9 + 2 * f], C.qinf, nb);
+      ghost<KIND>(tr_, lk_tag(lkk.y), gq[8 + 2 * f], gq[9 + 2 * f], C.qinf, nb_);
     }
     double wa[NW], wc[NW];
-    grad_vars<KIND>(tr, ph.gamma, wa);
-    grad_vars<KIND>(nb, ph.gamma, wc);
+    grad_vars<KIND>(tr_, ph.gamma, wa);
+    grad_vars<KIND>(nb_, ph.gamma, wc);
 #pragma unroll
     for (int c = 0; c < NW; ++c) sWH[c * NFT + t] = 0.5 * (wa[c] + wc[c]);
+  };
+  if constexpr (ONE_FACE) {
+    if (face_live) face_avg(t0, fel, ff, lk, tr, nb);
+  } else {
+    for (int t = threadIdx.x; t < E * NF; t += blockDim.x) {
+      const int el = t / NF, r = t % NF, f = r / N, k = r % N;
+      const int64_t e = e0 + el;
+      if (e >= M) continue;
+      const int2 lkk = m.link[e * 4 + f];
+      const bool interior = lkk.x >= 0;
+      const int kk = lk_rev(lkk.y) ? N - 1 - k : k;
+      const int64_t own = ((e * 4 + f) * N + k) * NV;
+      const int64_t nbi = interior ? (((int64_t)lkk.x * 4 + lk_face(lkk.y)) * N + kk) * NV : own;
+      double tr2[NV], nb2[NV];
+      ld_face<NV>(qtr + own, tr2);
+      ld_face<NV>(qtr + nbi, nb2);
+      face_avg(t, el, f, lkk, tr2, nb2);
+    }
   }
   __syncthreads();
   for (int t = threadIdx.x; t < E * NF; t += blockDim.x) {
@@ -810,67 +841,51 @@ k_assemble(const FrConst C, const FrMesh m, const double* __restrict__ q, const 
   const int64_t e0 = (int64_t)blockIdx.x * E;
   const int64_t M = m.M;
   const Phys ph = phys_of(C);
-  __shared__ int2 sLK[E * 4];
-  load_links<P>(m.link, e0, M, sLK);
+  // Prologue: every global load of the kernel is issued before the first
+  // barrier -- q / geometry into shared memory, the face gathers (own and
+  // neighbour traces, one-sided viscous fluxes, the L side's normal) and
+  // the point gradients into registers -- so their latencies overlap.
+  static_assert(E * NF <= BC<P>::THREADS || P <= 2, "face prologue needs one face point per thread");
+  constexpr bool ONE_FACE = (E * NF <= BC<P>::THREADS);
+  const int t0 = threadIdx.x;
   load_points<P, NV>(q, e0, M, sQ);
   load_geom<P>(m.geom, e0, M, sG);
-  __syncthreads();
-  const int t0 = threadIdx.x;
-  // common face fluxes: inviscid on the L side's normal (-F to R), viscous
-  // 0.5 (fvn_own - fvn_nb), BR1 average (spatial.py:520-568).  Branch-free
-  // across L/R sides: operands are selected, one Roe evaluation per thread.
-  for (int t = threadIdx.x; t < E * NF; t += blockDim.x) {
-    const int el = t / NF, r = t % NF, f = r / N, k = r % N;
-    const int64_t e = e0 + el;
-    if (e >= M) continue;
-    const int2 lk = sLK[el * 4 + f];
-    const double* gq = sG + el * 20;
-    const double nx = gq[8 + 2 * f], ny = gq[9 + 2 * f];
-    const bool interior = lk.x >= 0;
-    const int kk = lk_rev(lk.y) ? N - 1 - k : k;
-    const int64_t own = ((e * 4 + f) * N + k) * NV;
-    const int64_t nbi = interior ? (((int64_t)lk.x * 4 + lk_face(lk.y)) * N + kk) * NV : own;
-    double tr[NV], nb[NV], F[NV], Fo[NV], Fn[NV];
-    ld_face<NV>(qtr + own, tr);
-    ld_face<NV>(qtr + nbi, nb);
-    if constexpr (VISC) {
-      ld_face<NV>(fvn + own, Fo);
-      ld_face<NV>(fvn + nbi, Fn);
+  double tr[NV], nb[NV], Fo[NV], Fn[NV], gx[NW], gy[NW];
+  double nux = 0.0, nuy = 0.0;
+  int2 lk = make_int2(-1, 0);
+  bool face_live = false;
+  int fel = 0, ff = 0, fk = 0;
+  if constexpr (ONE_FACE) {
+    if (t0 < E * NF) {
+      fel = t0 / NF;
+      const int r = t0 % NF;
+      ff = r / N;
+      fk = r % N;
+      const int64_t e = e0 + fel;
+      face_live = e < M;
+      if (face_live) {
+        lk = m.link[e * 4 + ff];
+        const bool interior = lk.x >= 0;
+        const int kk = lk_rev(lk.y) ? N - 1 - fk : fk;
+        const int64_t own = ((e * 4 + ff) * N + fk) * NV;
+        const int64_t nbi = interior ? (((int64_t)lk.x * 4 + lk_face(lk.y)) * N + kk) * NV : own;
+        ld_face<NV>(qtr + own, tr);
+        ld_face<NV>(qtr + nbi, nb);
+        if constexpr (VISC) {
+          ld_face<NV>(fvn + own, Fo);
+          ld_face<NV>(fvn + nbi, Fn);
+        }
+        if (interior && !lk_left(lk.y)) {
+          const double* gn = m.geom + (int64_t)lk.x * 20 + 8 + 2 * lk_face(lk.y);
+          nux = __ldg(gn);
+          nuy = __ldg(gn + 1);
+        }
+      }
     }
-    const bool left = !interior || lk_left(lk.y);
-    double nux = nx, nuy = ny;
-    if (!left) {
-      const double* gn = m.geom + (int64_t)lk.x * 20 + 8 + 2 * lk_face(lk.y);
-      nux = __ldg(gn);
-      nuy = __ldg(gn + 1);
-    }
-    if (!interior) ghost<KIND>(tr, lk_tag(lk.y), nx, ny, C.qinf, nb);
-    double qa[NV], qc[NV];
-#pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      qa[v] = left ? tr[v] : nb[v];
-      qc[v] = left ? nb[v] : tr[v];
-    }
-    num_flux<KIND>(qa, qc, nux, nuy, ph, F);
-#pragma unroll
-    for (int v = 0; v < NV; ++v) F[v] = left ? F[v] : -F[v];
-    if constexpr (VISC) {
-      double Fv[NV];
-#pragma unroll
-      for (int v = 0; v < NV; ++v) Fv[v] = interior ? 0.5 * (Fo[v] - Fn[v]) : Fo[v];
-      if (KT<KIND>::FLOW && !interior && lk_tag(lk.y) == T_WALL_ADIABATIC) Fv[NV - 1] = 0.0;
-#pragma unroll
-      for (int v = 0; v < NV; ++v) F[v] = F[v] - Fv[v];
-    }
-#pragma unroll
-    for (int v = 0; v < NV; ++v) sFC[v * NFT + t] = F[v];
   }
-  // volume fluxes at the points: gradients come from k_fvn (same values
-  // it used for the one-sided viscous fluxes)
-  if (t0 < NPT) {
-    const int el = t0 / NP, pt = t0 % NP, a = pt / N, b = pt % N;
-    double gx[NW], gy[NW];
-    if constexpr (VISC) {
+  if constexpr (VISC) {
+    if (t0 < NPT) {
+      const int el = t0 / NP, pt = t0 % NP;
       if (e0 + el < M) {
         const double* gs = grad + ((e0 + el) * NP + pt) * (2 * NW);
         if constexpr (NW == 3) {
@@ -895,6 +910,74 @@ k_assemble(const FrConst C, const FrMesh m, const double* __restrict__ q, const 
         for (int c = 0; c < NW; ++c) gx[c] = gy[c] = 0.0;
       }
     }
+  }
+  __syncthreads();
+  // common face fluxes: inviscid on the L side's normal (-F to R), viscous
+  // 0.5 (fvn_own - fvn_nb), BR1 average (spatial.py:520-568).  Branch-free
+  // across L/R sides: operands are selected, one Roe evaluation per thread.
+  auto face_flux = [&](int t, int el, int f, int k, int2 lkk, double* tr_, double* nb_, const double* Fo_,
+                       const double* Fn_, double nux_, double nuy_) {
+    const double* gq = sG + el * 20;
+    const double nx = gq[8 + 2 * f], ny = gq[9 + 2 * f];
+    const bool interior = lkk.x >= 0;
+    const bool left = !interior || lk_left(lkk.y);
+    if (left) {
+      nux_ = nx;
+      nuy_ = ny;
+    }
+    if (!interior) ghost<KIND>(tr_, lk_tag(lkk.y), nx, ny, C.qinf, nb_);
+    double qa[NV], qc[NV], F[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      qa[v] = left ? tr_[v] : nb_[v];
+      qc[v] = left ? nb_[v] : tr_[v];
+    }
+    num_flux<KIND>(qa, qc, nux_, nuy_, ph, F);
+#pragma unroll
+    for (int v = 0; v < NV; ++v) F[v] = left ? F[v] : -F[v];
+    if constexpr (VISC) {
+      double Fv[NV];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) Fv[v] = interior ? 0.5 * (Fo_[v] - Fn_[v]) : Fo_[v];
+      if (KT<KIND>::FLOW && !interior && lk_tag(lkk.y) == T_WALL_ADIABATIC) Fv[NV - 1] = 0.0;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) F[v] = F[v] - Fv[v];
+    }
+#pragma unroll
+    for (int v = 0; v < NV; ++v) sFC[v * NFT + t] = F[v];
+  };
+  if constexpr (ONE_FACE) {
+    if (face_live) face_flux(t0, fel, ff, fk, lk, tr, nb, Fo, Fn, nux, nuy);
+  } else {
+    for (int t = threadIdx.x; t < E * NF; t += blockDim.x) {
+      const int el = t / NF, r = t % NF, f = r / N, k = r % N;
+      const int64_t e = e0 + el;
+      if (e >= M) continue;
+      const int2 lkk = m.link[e * 4 + f];
+      const bool interior = lkk.x >= 0;
+      const int kk = lk_rev(lkk.y) ? N - 1 - k : k;
+      const int64_t own = ((e * 4 + f) * N + k) * NV;
+      const int64_t nbi = interior ? (((int64_t)lkk.x * 4 + lk_face(lkk.y)) * N + kk) * NV : own;
+      double tr2[NV], nb2[NV], Fo2[NV], Fn2[NV];
+      ld_face<NV>(qtr + own, tr2);
+      ld_face<NV>(qtr + nbi, nb2);
+      if constexpr (VISC) {
+        ld_face<NV>(fvn + own, Fo2);
+        ld_face<NV>(fvn + nbi, Fn2);
+      }
+      double nx2 = 0.0, ny2 = 0.0;
+      if (interior && !lk_left(lkk.y)) {
+        const double* gn = m.geom + (int64_t)lkk.x * 20 + 8 + 2 * lk_face(lkk.y);
+        nx2 = __ldg(gn);
+        ny2 = __ldg(gn + 1);
+      }
+      face_flux(t, el, f, k, lkk, tr2, nb2, Fo2, Fn2, nx2, ny2);
+    }
+  }
+  // volume fluxes at the points: gradients come from k_fvn (same values
+  // it used for the one-sided viscous fluxes)
+  if (t0 < NPT) {
+    const int el = t0 / NP, pt = t0 % NP, a = pt / N, b = pt % N;
     const Metric mt = metric(sG + el * 20);
     double qq[NV], Ft[NV], Gt[NV];
     gather_point<NV, NPT>(sQ, t0, qq);
