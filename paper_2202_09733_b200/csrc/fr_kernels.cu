@@ -270,6 +270,7 @@ struct Metric {
   __device__ __forceinline__ double J10(double eta) const { return b0 + b1 * eta; }  // y_xi
   __device__ __forceinline__ double J01(double xi) const { return c0 + c1 * xi; }    // x_eta
   __device__ __forceinline__ double J11(double xi) const { return d0 + d1 * xi; }    // y_eta
+  __device__ __forceinline__ bool affine() const { return a1 == 0.0 && b1 == 0.0 && c1 == 0.0 && d1 == 0.0; }
 };
 __device__ __forceinline__ Metric metric(const double* g) {
   return Metric{g[0], g[1], g[2], g[3], g[4], g[5], g[6], g[7]};
@@ -397,19 +398,31 @@ __device__ __forceinline__ void grad_corrections(const Ops& op, const double* sW
   double lx[NW], ly[NW];
 #pragma unroll
   for (int c = 0; c < NW; ++c) lx[c] = ly[c] = 0.0;
-#pragma unroll
-  for (int i = 0; i < N; ++i) {
-    const double x = op.xg[i];
-    // x-gradient: Ft = J11 W (xi lines), Gt = -J10 W (eta lines)
-    // y-gradient: Ft = -J01 W,           Gt =  J00 W
-    const double fxx = xiline ? mt.J11(x) : -mt.J10(x);
-    const double fyy = xiline ? -mt.J01(x) : mt.J00(x);
-    const int p = el * NP + fpt<N>(f, k, i);
+  const Line L = face_line<N>(op, f, k);
+  if (mt.affine()) {
+    const double fxx = xiline ? mt.d0 : -mt.b0;
+    const double fyy = xiline ? -mt.c0 : mt.a0;
 #pragma unroll
     for (int c = 0; c < NW; ++c) {
-      const double Wv = sW[c * NPT + p];
-      lx[c] += w[i] * (fxx * Wv);
-      ly[c] += w[i] * (fyy * Wv);
+      const double t = line_sum<N>(L, sW + c * NPT + el * NP);
+      lx[c] = fxx * t;
+      ly[c] = fyy * t;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const double x = op.xg[i];
+      // x-gradient: Ft = J11 W (xi lines), Gt = -J10 W (eta lines)
+      // y-gradient: Ft = -J01 W,           Gt =  J00 W
+      const double fxx = xiline ? mt.J11(x) : -mt.J10(x);
+      const double fyy = xiline ? -mt.J01(x) : mt.J00(x);
+      const int p = el * NP + L.base + i * L.stride;
+#pragma unroll
+      for (int c = 0; c < NW; ++c) {
+        const double Wv = sW[c * NPT + p];
+        lx[c] += w[i] * (fxx * Wv);
+        ly[c] += w[i] * (fyy * Wv);
+      }
     }
   }
   const int fi = el * 4 * N + f * N + k;
@@ -433,20 +446,43 @@ __device__ __forceinline__ void gradient_at(const Ops& op, const double* sW, con
 #pragma unroll
   for (int c = 0; c < NW; ++c) sx[c] = sy[c] = dx[c] = dy[c] = 0.0;
   const int base = el * NP;
+  if (mt.affine()) {
+    // parallelogram element: J constant, factor it out of the line sums
+    double Sr[NW], Sc[NW];
 #pragma unroll
-  for (int i = 0; i < N; ++i) {
-    const double Db = op.D[b * N + i], Da = op.D[a * N + i];
-    const double xi = op.xg[i];
-    const double j11 = mt.J11(xi), j01 = mt.J01(xi);  // row line: xi_i
-    const double j10 = mt.J10(xi), j00 = mt.J00(xi);  // column line: eta_i
+    for (int c = 0; c < NW; ++c) Sr[c] = Sc[c] = 0.0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const double Db = op.D[b * N + i], Da = op.D[a * N + i];
+#pragma unroll
+      for (int c = 0; c < NW; ++c) {
+        Sr[c] += Db * sW[c * NPT + base + a * N + i];
+        Sc[c] += Da * sW[c * NPT + base + i * N + b];
+      }
+    }
 #pragma unroll
     for (int c = 0; c < NW; ++c) {
-      const double Wr = sW[c * NPT + base + a * N + i];
-      const double Wc = sW[c * NPT + base + i * N + b];
-      sx[c] += Db * (j11 * Wr);
-      sy[c] += Db * (-j01 * Wr);
-      dx[c] += Da * (-j10 * Wc);
-      dy[c] += Da * (j00 * Wc);
+      sx[c] = mt.d0 * Sr[c];
+      sy[c] = -mt.c0 * Sr[c];
+      dx[c] = -mt.b0 * Sc[c];
+      dy[c] = mt.a0 * Sc[c];
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const double Db = op.D[b * N + i], Da = op.D[a * N + i];
+      const double xi = op.xg[i];
+      const double j11 = mt.J11(xi), j01 = mt.J01(xi);  // row line: xi_i
+      const double j10 = mt.J10(xi), j00 = mt.J00(xi);  // column line: eta_i
+#pragma unroll
+      for (int c = 0; c < NW; ++c) {
+        const double Wr = sW[c * NPT + base + a * N + i];
+        const double Wc = sW[c * NPT + base + i * N + b];
+        sx[c] += Db * (j11 * Wr);
+        sy[c] += Db * (-j01 * Wr);
+        dx[c] += Da * (-j10 * Wc);
+        dy[c] += Da * (j00 * Wc);
+      }
     }
   }
   const double xa = op.xg[a], xb = op.xg[b];
