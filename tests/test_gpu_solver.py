@@ -274,3 +274,20 @@ def test_esdirk2_step_config2_physics_small_mesh(cuda):
     assert [i["iters"] for i in info] == [r[1] for r in drv_o.records]
     assert all(abs(a - b) <= 1 for a, b in zip([i["gmres_iters"] for i in info], [r[2] for r in drv_o.records]))
     assert rel(q_d, q_o) <= 1e-7
+
+
+@pytest.mark.parametrize("nx", [16, 32])
+def test_row4_step_config4_channel_walls(cuda, nx):
+    # BASELINE config 4 physics on a reduced stretched channel: x-periodic,
+    # adiabatic wall at y=0, slip wall at y=1, ROW4 + GMRES(60) + pMG p{3-2}
+    c = cases.config(4, nx=nx)
+    o = OracleDisc(c.mesh, c.p, c.eqn)
+    d = Discretization(c.mesh, c.p, c.eqn)
+    drv_o = so.Driver(o, "pmg", "3-2", 2, smoother_shift=50.0, gmres_rtol=1e-3, kdim=60)
+    s = ti.get_scheme("row4")
+    q_o = drv_o.row_step(c.q0, c.dt, s.a, s.cmat, s.b, s.gamma)
+    cfg = {"case.precond": "pmg", "pmg.levels": "3-2", "pmg.smooth": "2", "pmg.smoother_shift": 50.0,
+           "gmres.kdim": 60, "gmres.rtol": 1e-3}
+    q_d, info = ImplicitDriver(d, cfg).step(t(c.q0), c.dt, s)
+    assert all(abs(a["iters"] - b[2]) <= 1 for a, b in zip(info, drv_o.records))
+    assert rel(q_d, q_o) <= 1e-7
