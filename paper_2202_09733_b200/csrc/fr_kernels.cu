@@ -84,8 +84,9 @@ struct Ops {
   const double* xg;
 };
 
+template <int TH>
 __device__ __forceinline__ Ops stage_ops(const FrConst& C, double* sm) {
-  for (int i = threadIdx.x; i < 66; i += blockDim.x) {
+  for (int i = threadIdx.x; i < 66; i += TH) {
     double v;
     if (i < 36) v = C.D[i];
     else if (i < 42) v = C.eL[i - 36];
@@ -291,7 +292,7 @@ __device__ __forceinline__ void load_points(const double* __restrict__ src, int6
   if constexpr (NV == 4) {
     const int64_t lim = (M - e0) * NP;
     const double2* base = reinterpret_cast<const double2*>(src + e0 * NP * 4);
-    for (int g = threadIdx.x; g < NPT; g += blockDim.x) {
+    for (int g = threadIdx.x; g < NPT; g += BC<P>::THREADS) {
       double2 a = make_double2(1.0, 1.0), b = make_double2(1.0, 1.0);
       if (g < lim) {
         a = __ldg(base + 2 * g);
@@ -305,7 +306,7 @@ __device__ __forceinline__ void load_points(const double* __restrict__ src, int6
   } else {
     const int64_t lim = (M - e0) * NP * NV;
     const double* base = src + e0 * NP * NV;
-    for (int i = threadIdx.x; i < NPT * NV; i += blockDim.x) {
+    for (int i = threadIdx.x; i < NPT * NV; i += BC<P>::THREADS) {
       const int v = i % NV, g = i / NV;
       sQ[v * NPT + g] = (i < lim) ? __ldg(base + i) : 1.0;
     }
@@ -316,7 +317,7 @@ template <int P>
 __device__ __forceinline__ void load_links(const int2* __restrict__ link, int64_t e0, int64_t M, int2* sLK) {
   constexpr int E = BC<P>::EPB;
   const int64_t lim = (M - e0) * 4;
-  for (int i = threadIdx.x; i < E * 4; i += blockDim.x) sLK[i] = (i < lim) ? link[e0 * 4 + i] : make_int2(-1, 0);
+  for (int i = threadIdx.x; i < E * 4; i += BC<P>::THREADS) sLK[i] = (i < lim) ? link[e0 * 4 + i] : make_int2(-1, 0);
 }
 
 template <int P>
@@ -324,7 +325,7 @@ __device__ __forceinline__ void load_geom(const double* __restrict__ geom, int64
   constexpr int E = BC<P>::EPB;
   const int64_t lim = (M - e0) * 20;
   const double* base = geom + e0 * 20;
-  for (int i = threadIdx.x; i < E * 20; i += blockDim.x) sG[i] = (i < lim) ? __ldg(base + i) : 0.0;
+  for (int i = threadIdx.x; i < E * 20; i += BC<P>::THREADS) sG[i] = (i < lim) ? __ldg(base + i) : 0.0;
 }
 
 // Interpolation line of face f, point k: points base + i * stride, i < N
@@ -628,7 +629,7 @@ k_trace(const FrConst C, const FrMesh m, const double* __restrict__ q, const dou
   using L = SL<P, KIND>;
   constexpr int N = BC<P>::N, NP = BC<P>::NP, NF = BC<P>::NF, E = BC<P>::EPB, NV = KT<KIND>::NV;
   constexpr int NPT = L::NPT;
-  const Ops op = stage_ops(C, sm);
+  const Ops op = stage_ops<BC<P>::THREADS>(C, sm);
   double* sQ = sm + L::Q;
   const int64_t e0 = (int64_t)blockIdx.x * E;
   const int64_t M = m.M;
@@ -640,7 +641,7 @@ k_trace(const FrConst C, const FrMesh m, const double* __restrict__ q, const dou
     const double* qb = q + e0 * NP * NV;
     const double* xb = X + e0 * NP * NV;
     double* pb = qp + e0 * NP * NV;
-    for (int i = threadIdx.x; i < NPT * NV; i += blockDim.x) {
+    for (int i = threadIdx.x; i < NPT * NV; i += BC<P>::THREADS) {
       double v = 1.0;
       if (i < lim) {
         v = __dadd_rn(__ldg(qb + i), __dmul_rn(eps, __ldg(xb + i)));
@@ -662,7 +663,7 @@ k_trace(const FrConst C, const FrMesh m, const double* __restrict__ q, const dou
       }
     }
   }
-  for (int t = threadIdx.x; t < E * NF; t += blockDim.x) {
+  for (int t = threadIdx.x; t < E * NF; t += BC<P>::THREADS) {
     const int el = t / NF, r = t % NF, f = r / N, k = r % N;
     const int64_t e = e0 + el;
     if (e >= M) continue;
@@ -687,7 +688,7 @@ k_fvn(const FrConst C, const FrMesh m, const double* __restrict__ q, const doubl
   using L = SL<P, KIND>;
   constexpr int N = BC<P>::N, NP = BC<P>::NP, NF = BC<P>::NF, E = BC<P>::EPB;
   constexpr int NV = KT<KIND>::NV, NW = KT<KIND>::NW, NPT = L::NPT, NFT = L::NFT;
-  const Ops op = stage_ops(C, sm);
+  const Ops op = stage_ops<BC<P>::THREADS>(C, sm);
   double* sQ = sm + L::Q;
   double* sG = sm + L::G;
   double* sW = sm + L::W;
@@ -748,7 +749,7 @@ k_fvn(const FrConst C, const FrMesh m, const double* __restrict__ q, const doubl
   if constexpr (ONE_FACE) {
     if (face_live) face_avg(t0, fel, ff, lk, tr, nb);
   } else {
-    for (int t = threadIdx.x; t < E * NF; t += blockDim.x) {
+    for (int t = threadIdx.x; t < E * NF; t += BC<P>::THREADS) {
       const int el = t / NF, r = t % NF, f = r / N, k = r % N;
       const int64_t e = e0 + el;
       if (e >= M) continue;
@@ -764,7 +765,7 @@ k_fvn(const FrConst C, const FrMesh m, const double* __restrict__ q, const doubl
     }
   }
   __syncthreads();
-  for (int t = threadIdx.x; t < E * NF; t += blockDim.x) {
+  for (int t = threadIdx.x; t < E * NF; t += BC<P>::THREADS) {
     const int el = t / NF, r = t % NF, f = r / N, k = r % N;
     if (e0 + el >= M) continue;
     grad_corrections<P, KIND>(op, sW, sG + el * 20, sWH, sCG, el, f, k);
@@ -789,7 +790,7 @@ k_fvn(const FrConst C, const FrMesh m, const double* __restrict__ q, const doubl
     }
   }
   __syncthreads();
-  for (int t = threadIdx.x; t < E * NF; t += blockDim.x) {
+  for (int t = threadIdx.x; t < E * NF; t += BC<P>::THREADS) {
     const int el = t / NF, r = t % NF, f = r / N, k = r % N;
     const int64_t e = e0 + el;
     if (e >= M) continue;
@@ -867,7 +868,7 @@ k_assemble(const FrConst C, const FrMesh m, const double* __restrict__ q, const 
   constexpr int NV = KT<KIND>::NV, NW = KT<KIND>::NW, NPT = L::NPT, NFT = L::NFT;
   constexpr bool VISC = KT<KIND>::VISC;
   if (blockIdx.x == 0 && threadIdx.x == 0) commit_status(bad, st);
-  const Ops op = stage_ops(C, sm);
+  const Ops op = stage_ops<BC<P>::THREADS>(C, sm);
   double* sQ = sm + L::Q;
   double* sG = sm + L::G;
   double* sFC = sm + L::A_FC;
@@ -985,7 +986,7 @@ k_assemble(const FrConst C, const FrMesh m, const double* __restrict__ q, const 
   if constexpr (ONE_FACE) {
     if (face_live) face_flux(t0, fel, ff, fk, lk, tr, nb, Fo, Fn, nux, nuy);
   } else {
-    for (int t = threadIdx.x; t < E * NF; t += blockDim.x) {
+    for (int t = threadIdx.x; t < E * NF; t += BC<P>::THREADS) {
       const int el = t / NF, r = t % NF, f = r / N, k = r % N;
       const int64_t e = e0 + el;
       if (e >= M) continue;
@@ -1025,7 +1026,7 @@ k_assemble(const FrConst C, const FrMesh m, const double* __restrict__ q, const 
     }
   }
   __syncthreads();
-  for (int t = threadIdx.x; t < E * NF; t += blockDim.x) {
+  for (int t = threadIdx.x; t < E * NF; t += BC<P>::THREADS) {
     const int el = t / NF, r = t % NF, f = r / N, k = r % N;
     if (e0 + el >= M) continue;
     double Fc[NV];
@@ -1090,7 +1091,7 @@ __device__ __forceinline__ void local_pipeline(const FrConst& C, const FrMesh& m
       for (int c = 0; c < NW; ++c) sW[c * NPT + t0] = w[c];
     }
   }
-  for (int t = threadIdx.x; t < E * NF; t += blockDim.x) {
+  for (int t = threadIdx.x; t < E * NF; t += BC<P>::THREADS) {
     const int el = t / NF, r = t % NF, f = r / N, k = r % N;
     const int64_t e = slot_elem[el];
     if (e < 0) continue;
@@ -1122,7 +1123,7 @@ __device__ __forceinline__ void local_pipeline(const FrConst& C, const FrMesh& m
   }
   __syncthreads();
   if constexpr (VISC) {
-    for (int t = threadIdx.x; t < E * NF; t += blockDim.x) {
+    for (int t = threadIdx.x; t < E * NF; t += BC<P>::THREADS) {
       const int el = t / NF, r = t % NF, f = r / N, k = r % N;
       if (slot_elem[el] < 0) continue;
       grad_corrections<P, KIND>(op, sW, sG + el * 20, sWH, sCG, el, f, k);
@@ -1151,7 +1152,7 @@ __device__ __forceinline__ void local_pipeline(const FrConst& C, const FrMesh& m
     }
   }
   __syncthreads();
-  for (int t = threadIdx.x; t < E * NF; t += blockDim.x) {
+  for (int t = threadIdx.x; t < E * NF; t += BC<P>::THREADS) {
     const int el = t / NF, r = t % NF, f = r / N, k = r % N;
     const int64_t e = slot_elem[el];
     if (e < 0) continue;
@@ -1211,12 +1212,12 @@ k_local(const FrConst C, const FrMesh m, const int64_t* __restrict__ elems, int6
   using L = SL<P, KIND>;
   constexpr int NP = BC<P>::NP, E = BC<P>::EPB, NV = KT<KIND>::NV;
   __shared__ int64_t slot[E];
-  const Ops op = stage_ops(C, sm);
+  const Ops op = stage_ops<BC<P>::THREADS>(C, sm);
   const int64_t b0 = (int64_t)blockIdx.x * E;
-  for (int s = threadIdx.x; s < E; s += blockDim.x) slot[s] = (b0 + s < B) ? elems[b0 + s] : -1;
+  for (int s = threadIdx.x; s < E; s += BC<P>::THREADS) slot[s] = (b0 + s < B) ? elems[b0 + s] : -1;
   load_points<P, NV>(Q, b0, B, sm + L::Q);
   __syncthreads();
-  for (int i = threadIdx.x; i < E * 20; i += blockDim.x) {
+  for (int i = threadIdx.x; i < E * 20; i += BC<P>::THREADS) {
     const int64_t e = slot[i / 20];
     sm[L::G + i] = (e >= 0) ? __ldg(m.geom + e * 20 + i % 20) : 0.0;
   }
@@ -1243,18 +1244,18 @@ k_blocks(const FrConst C, const FrMesh m, const double* __restrict__ q, const do
   constexpr int NP = BC<P>::NP, E = BC<P>::EPB, NV = KT<KIND>::NV, NPT = L::NPT;
   constexpr int SZ = NP * NV;
   __shared__ int64_t slot[E];
-  const Ops op = stage_ops(C, sm);
+  const Ops op = stage_ops<BC<P>::THREADS>(C, sm);
   const int64_t e = blockIdx.x;
   double* sQ = sm + L::Q;
   double* sR0 = sm + L::R0;
   const double* qe = q + e * SZ;
   const int t0 = threadIdx.x;
   double* BTe = BT + e * (int64_t)SZ * SZ;
-  for (int i = threadIdx.x; i < E * 20; i += blockDim.x) sm[L::G + i] = __ldg(m.geom + e * 20 + i % 20);
+  for (int i = threadIdx.x; i < E * 20; i += BC<P>::THREADS) sm[L::G + i] = __ldg(m.geom + e * 20 + i % 20);
   for (int c0 = 0; c0 <= SZ; c0 += E) {
     __syncthreads();
-    for (int s = threadIdx.x; s < E; s += blockDim.x) slot[s] = (c0 + s <= SZ) ? e : -1;
-    for (int i = threadIdx.x; i < E * SZ; i += blockDim.x) {
+    for (int s = threadIdx.x; s < E; s += BC<P>::THREADS) slot[s] = (c0 + s <= SZ) ? e : -1;
+    for (int i = threadIdx.x; i < E * SZ; i += BC<P>::THREADS) {
       const int s = i / SZ, d = i % SZ, c = c0 + s;
       const double v = __ldg(qe + d);
       sQ[(d % NV) * NPT + s * NP + d / NV] = (c >= 1 && d == c - 1) ? v + eps : v;
