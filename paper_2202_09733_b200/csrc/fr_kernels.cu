@@ -1051,6 +1051,161 @@ k_assemble(const FrConst C, const FrMesh m, const double* __restrict__ q, const 
   }
 }
 
+// cp.async (LDGSTS) helpers: 16-byte global->shared copies that do not
+// stage through registers, so the issuing thread keeps running.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  const int sz = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// Phase 3, one face point per thread (p >= 3, 4 conserved variables):
+// q and geometry go to shared memory by cp.async while the face threads
+// gather their traces / fluxes and evaluate the common face fluxes straight
+// from registers; the first barrier only guards the point stage.
+template <int P, int KIND>
+__global__ void __launch_bounds__(BC<P>::THREADS, MinBlocks<P>::ASM)
+k_assemble_async(const FrConst C, const FrMesh m, const double* __restrict__ q, const double* __restrict__ qtr,
+                 const double* __restrict__ fvn, const double* __restrict__ grad, const Epi ep,
+                 double* __restrict__ out, int* bad, Status* st) {
+  extern __shared__ __align__(16) double sm[];
+  using L = SL<P, KIND>;
+  constexpr int TH = BC<P>::THREADS;
+  constexpr int N = BC<P>::N, NP = BC<P>::NP, NF = BC<P>::NF, E = BC<P>::EPB;
+  constexpr int NV = KT<KIND>::NV, NW = KT<KIND>::NW, NPT = L::NPT, NFT = L::NFT;
+  constexpr bool VISC = KT<KIND>::VISC;
+  static_assert(NV == 4 && E * NF <= TH, "async assemble: flow kinds, one face point per thread");
+  if (blockIdx.x == 0 && threadIdx.x == 0) commit_status(bad, st);
+  double* sQA = sm + L::Q;  // AoS [E][NP][NV]
+  double* sG = sm + L::G;
+  double* sFC = sm + L::A_FC;
+  double* sFT = sm + L::A_FT;
+  double* sGT = sm + L::A_GT;
+  double* sCF = sm + L::A_CF;
+  const int64_t e0 = (int64_t)blockIdx.x * E;
+  const int64_t M = m.M;
+  const int ne = (int)((M - e0) < E ? (M - e0) : E);
+  const int t0 = threadIdx.x;
+  {
+    const double* qs = q + e0 * NP * NV;
+    for (int i = t0; i < E * NP * NV / 2; i += TH) cp_async16(sQA + 2 * i, qs + 2 * i, 2 * i < ne * NP * NV);
+    const double* gsrc = m.geom + e0 * 20;
+    for (int i = t0; i < E * 10; i += TH) cp_async16(sG + 2 * i, gsrc + 2 * i, 2 * i < ne * 20);
+    cp_async_commit();
+  }
+  const Ops op = stage_ops<TH>(C, sm);
+  const Phys ph = phys_of(C);
+  // point gradients into registers
+  double gx[NW], gy[NW];
+  if constexpr (VISC) {
+#pragma unroll
+    for (int c = 0; c < NW; ++c) gx[c] = gy[c] = 0.0;
+    if (t0 < NPT) {
+      const int el = t0 / NP, pt = t0 % NP;
+      if (el < ne) {
+        const double2* gs = reinterpret_cast<const double2*>(grad + ((e0 + el) * NP + pt) * (2 * NW));
+        const double2 g0 = __ldg(gs), g1 = __ldg(gs + 1), g2 = __ldg(gs + 2);
+        gx[0] = g0.x;
+        gx[1] = g0.y;
+        gx[2] = g1.x;
+        gy[0] = g1.y;
+        gy[1] = g2.x;
+        gy[2] = g2.y;
+      }
+    }
+  }
+  // face threads: gathers and common face flux, no shared memory needed
+  if (t0 < E * NF) {
+    const int fel = t0 / NF, r = t0 % NF, f = r / N, k = r % N;
+    if (fel < ne) {
+      const int64_t e = e0 + fel;
+      const int2 lk = m.link[e * 4 + f];
+      const bool interior = lk.x >= 0;
+      const int kk = lk_rev(lk.y) ? N - 1 - k : k;
+      const int64_t own = ((e * 4 + f) * N + k) * NV;
+      const int64_t nbi = interior ? (((int64_t)lk.x * 4 + lk_face(lk.y)) * N + kk) * NV : own;
+      double tr[NV], nb[NV], Fo[NV], Fn[NV], F[NV];
+      ld_face<NV>(qtr + own, tr);
+      ld_face<NV>(qtr + nbi, nb);
+      if constexpr (VISC) {
+        ld_face<NV>(fvn + own, Fo);
+        ld_face<NV>(fvn + nbi, Fn);
+      }
+      const double2 no = __ldg(reinterpret_cast<const double2*>(m.geom + e * 20 + 8 + 2 * f));
+      const bool left = !interior || lk_left(lk.y);
+      double nux = no.x, nuy = no.y;
+      if (!left) {
+        const double2 nn = __ldg(reinterpret_cast<const double2*>(m.geom + (int64_t)lk.x * 20 + 8 + 2 * lk_face(lk.y)));
+        nux = nn.x;
+        nuy = nn.y;
+      }
+      if (!interior) ghost<KIND>(tr, lk_tag(lk.y), no.x, no.y, C.qinf, nb);
+      double qa[NV], qc[NV];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        qa[v] = left ? tr[v] : nb[v];
+        qc[v] = left ? nb[v] : tr[v];
+      }
+      num_flux<KIND>(qa, qc, nux, nuy, ph, F);
+#pragma unroll
+      for (int v = 0; v < NV; ++v) F[v] = left ? F[v] : -F[v];
+      if constexpr (VISC) {
+        double Fv[NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) Fv[v] = interior ? 0.5 * (Fo[v] - Fn[v]) : Fo[v];
+        if (!interior && lk_tag(lk.y) == T_WALL_ADIABATIC) Fv[NV - 1] = 0.0;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) F[v] = F[v] - Fv[v];
+      }
+#pragma unroll
+      for (int v = 0; v < NV; ++v) sFC[v * NFT + t0] = F[v];
+    }
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  if (t0 < NPT) {
+    const int el = t0 / NP, pt = t0 % NP, a = pt / N, b = pt % N;
+    const Metric mt = metric(sG + el * 20);
+    const double2 q01 = reinterpret_cast<const double2*>(sQA)[2 * t0];
+    const double2 q23 = reinterpret_cast<const double2*>(sQA)[2 * t0 + 1];
+    const double qq[NV] = {q01.x, q01.y, q23.x, q23.y};
+    double Ft[NV], Gt[NV];
+    point_fluxes<P, KIND>(qq, gx, gy, ph, mt, op.xg[a], op.xg[b], Ft, Gt);
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      sFT[v * NPT + t0] = Ft[v];
+      sGT[v * NPT + t0] = Gt[v];
+    }
+  }
+  __syncthreads();
+  if (t0 < E * NF) {
+    const int el = t0 / NF, r = t0 % NF, f = r / N, k = r % N;
+    if (el < ne) {
+      double Fc[NV];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) Fc[v] = sFC[v * NFT + t0];
+      flux_corrections<P, KIND>(op, sFT, sGT, sG + el * 20, Fc, sCF, el, f, k);
+    }
+  }
+  __syncthreads();
+  if (t0 < NPT) {
+    const int el = t0 / NP, pt = t0 % NP;
+    if (el < ne) {
+      const int64_t e = e0 + el;
+      const Metric mt = metric(sG + el * 20);
+      double R[NV];
+      divergence_at<P, KIND>(op, sFT, sGT, sCF, mt, el, pt / N, pt % N, R);
+      const int64_t base = (e * NP + pt) * NV;
+      double o[NV];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) o[v] = epi_apply(ep, base + v, R[v], sQA[t0 * NV + v]);
+      st_face<NV>(out + base, o);
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // element-local residual with frozen neighbour data (spatial.py:768-853)
 //
@@ -1298,6 +1453,8 @@ static int run_residual(const DiscDev& d, const double* q, const double* X, doub
     cudaFuncSetAttribute(k_trace<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES_TRACE);
     cudaFuncSetAttribute(k_fvn<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES_FVN);
     cudaFuncSetAttribute(k_assemble<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES_ASM);
+    if constexpr (KT<KIND>::NV == 4 && E * BC<P>::NF <= TH)
+      cudaFuncSetAttribute(k_assemble_async<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES_ASM);
     attr = true;
   }
   int* bad = nullptr;
@@ -1309,7 +1466,11 @@ static int run_residual(const DiscDev& d, const double* q, const double* X, doub
   if (X != nullptr) qq = d.qp;
   k_trace<P, KIND><<<grid, TH, L::BYTES_TRACE, st>>>(d.C, d.mesh, q, X, eps, d.qp, d.qtr, bad);
   if (KT<KIND>::VISC) k_fvn<P, KIND><<<grid, TH, L::BYTES_FVN, st>>>(d.C, d.mesh, qq, d.qtr, d.fvn, d.grad);
-  k_assemble<P, KIND><<<grid, TH, L::BYTES_ASM, st>>>(d.C, d.mesh, qq, d.qtr, d.fvn, d.grad, epi, out, bad, stp);
+  if constexpr (KT<KIND>::NV == 4 && E * BC<P>::NF <= TH)
+    k_assemble_async<P, KIND><<<grid, TH, L::BYTES_ASM, st>>>(d.C, d.mesh, qq, d.qtr, d.fvn, d.grad, epi, out, bad,
+                                                              stp);
+  else
+    k_assemble<P, KIND><<<grid, TH, L::BYTES_ASM, st>>>(d.C, d.mesh, qq, d.qtr, d.fvn, d.grad, epi, out, bad, stp);
   return (int)cudaGetLastError();
 }
 
