@@ -844,6 +844,60 @@ __device__ __forceinline__ double epi_apply(const Epi& ep, int64_t i, double R, 
   return R;
 }
 
+// Epilogue with operands preloaded by the caller:
+//   JV: o1 = X, o2 = R0;  STAGE_F: o3 = E;  STAGE_JV: o1 = X, o2 = Fk, o3 = E;
+//   DEFECT: o1 = Sb, o2 = Se;  OUTER_F: o2 = Se
+__device__ __forceinline__ double epi_pre(const Epi& ep, double R, double qv, double o1, double o2, double o3) {
+  switch (ep.mode) {
+    case EPI_R:
+      return R;
+    case EPI_F:
+      return ep.s * qv - R;
+    case EPI_DEFECT:
+      return (o1 - (ep.s * qv - R)) + o2;
+    case EPI_JV:
+      return __dsub_rn(__dmul_rn(ep.s, o1), __ddiv_rn(__dsub_rn(R, o2), ep.eps));
+    case EPI_STAGE_F:
+      return __dsub_rn(__ddiv_rn(__dsub_rn(qv, o3), ep.adt), R);
+    case EPI_STAGE_JV: {
+      const double F = __dsub_rn(__ddiv_rn(__dsub_rn(qv, o3), ep.adt), R);
+      return __dadd_rn(__ddiv_rn(o1, ep.dtau), __ddiv_rn(__dsub_rn(F, o2), ep.eps));
+    }
+    case EPI_NEG_R:
+      return -R;
+    case EPI_OUTER_F:
+      return (ep.s * qv - R) - o2;
+  }
+  return R;
+}
+
+__device__ __forceinline__ void epi_load(const Epi& ep, int64_t i, double& o1, double& o2, double& o3) {
+  o1 = o2 = o3 = 0.0;
+  switch (ep.mode) {
+    case EPI_JV:
+      o1 = __ldg(ep.X + i);
+      o2 = __ldg(ep.R0 + i);
+      break;
+    case EPI_STAGE_F:
+      o3 = __ldg(ep.E + i);
+      break;
+    case EPI_STAGE_JV:
+      o1 = __ldg(ep.X + i);
+      o2 = __ldg(ep.R0 + i);
+      o3 = __ldg(ep.E + i);
+      break;
+    case EPI_DEFECT:
+      o1 = ep.Sb ? __ldg(ep.Sb + i) : ep.sb_scalar;
+      o2 = ep.Se ? __ldg(ep.Se + i) : ep.se_scalar;
+      break;
+    case EPI_OUTER_F:
+      o2 = ep.Se ? __ldg(ep.Se + i) : ep.se_scalar;
+      break;
+    default:
+      break;
+  }
+}
+
 __device__ __forceinline__ void commit_status(int* bad, Status* st) {
   if (bad == nullptr) return;
   const int bs = bad[0], bt = bad[1];
@@ -1180,28 +1234,74 @@ k_assemble_async(const FrConst C, const FrMesh m, const double* __restrict__ q, 
     }
   }
   __syncthreads();
-  if (t0 < E * NF) {
-    const int el = t0 / NF, r = t0 % NF, f = r / N, k = r % N;
-    if (el < ne) {
-      double Fc[NV];
+  // FR divergence by line threads (one per element, line, variable); the
+  // operator coefficients are compile-time indexed kernel parameters
+  // (constant bank), so the contractions read shared memory only for data.
+  //   rows  : s[a][b] = sum_i D[b][i] Ft[a][i] + lR[b] c1[a] - lL[b] c3[a]
+  //   cols  : R[a][b] = -(s[a][b] + sum_i D[a][i] Gt[i][b] + lR[a] c2[b] - lL[a] c0[b]) / det
+  // with c_f = +-js_f Fc_f - (trace of Ft / Gt on face f)  (spatial.py:407-430)
+  constexpr int NL = E * N * NV;
+  if (t0 < NL) {
+    const int el = t0 / (N * NV), r = t0 % (N * NV), a = r / NV, v = r % NV;
+    double* rowp = sFT + v * NPT + el * NP + a * N;
+    double x[N];
 #pragma unroll
-      for (int v = 0; v < NV; ++v) Fc[v] = sFC[v * NFT + t0];
-      flux_corrections<P, KIND>(op, sFT, sGT, sG + el * 20, Fc, sCF, el, f, k);
+    for (int i = 0; i < N; ++i) x[i] = rowp[i];
+    double t1 = 0.0, t3 = 0.0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      t1 += C.eR[i] * x[i];
+      t3 += C.eL[i] * x[i];
+    }
+    const double* gq = sG + el * 20;
+    const double c1 = gq[17] * sFC[v * NFT + el * 4 * N + 1 * N + a] - t1;
+    const double c3 = -gq[19] * sFC[v * NFT + el * 4 * N + 3 * N + (N - 1 - a)] - t3;
+#pragma unroll
+    for (int b = 0; b < N; ++b) {
+      double sb = 0.0;
+#pragma unroll
+      for (int i = 0; i < N; ++i) sb += C.D[b * N + i] * x[i];
+      rowp[b] = (sb + C.lR[b] * c1) - C.lL[b] * c3;  // in place: this thread owns row a
     }
   }
   __syncthreads();
-  if (t0 < NPT) {
-    const int el = t0 / NP, pt = t0 % NP;
+  if (t0 < NL) {
+    const int el = t0 / (N * NV), r = t0 % (N * NV), b = r / NV, v = r % NV;
     if (el < ne) {
-      const int64_t e = e0 + el;
-      const Metric mt = metric(sG + el * 20);
-      double R[NV];
-      divergence_at<P, KIND>(op, sFT, sGT, sCF, mt, el, pt / N, pt % N, R);
-      const int64_t base = (e * NP + pt) * NV;
-      double o[NV];
+      const double* colp = sGT + v * NPT + el * NP + b;
+      double y[N];
 #pragma unroll
-      for (int v = 0; v < NV; ++v) o[v] = epi_apply(ep, base + v, R[v], sQA[t0 * NV + v]);
-      st_face<NV>(out + base, o);
+      for (int i = 0; i < N; ++i) y[i] = colp[i * N];
+      double t2 = 0.0, t0f = 0.0;
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        t2 += C.eR[i] * y[i];
+        t0f += C.eL[i] * y[i];
+      }
+      const double* gq = sG + el * 20;
+      const Metric mt = metric(gq);
+      const double c2 = gq[18] * sFC[v * NFT + el * 4 * N + 2 * N + (N - 1 - b)] - t2;
+      const double c0 = -gq[16] * sFC[v * NFT + el * 4 * N + 0 * N + b] - t0f;
+      const double xb = C.xg[b];
+      const double j11 = mt.J11(xb), j01 = mt.J01(xb);
+      const int64_t e = e0 + el;
+      double o1[N], o2[N], o3[N];
+#pragma unroll
+      for (int a = 0; a < N; ++a) epi_load(ep, (e * NP + a * N + b) * NV + v, o1[a], o2[a], o3[a]);
+#pragma unroll
+      for (int a = 0; a < N; ++a) {
+        double ta = 0.0;
+#pragma unroll
+        for (int i = 0; i < N; ++i) ta += C.D[a * N + i] * y[i];
+        const double xa = C.xg[a];
+        const double idet = rcp(mt.J00(xa) * j11 - j01 * mt.J10(xa));
+        double d = sFT[v * NPT + el * NP + a * N + b] + ta;
+        d = (d + C.lR[a] * c2) - C.lL[a] * c0;
+        const double R = -(d * idet);
+        const int pt = a * N + b;
+        const int64_t gi = (e * NP + pt) * NV + v;
+        out[gi] = epi_pre(ep, R, sQA[(el * NP + pt) * NV + v], o1[a], o2[a], o3[a]);
+      }
     }
   }
 }
