@@ -765,27 +765,105 @@ k_fvn(const FrConst C, const FrMesh m, const double* __restrict__ q, const doubl
     }
   }
   __syncthreads();
-  for (int t = threadIdx.x; t < E * NF; t += BC<P>::THREADS) {
-    const int el = t / NF, r = t % NF, f = r / N, k = r % N;
-    if (e0 + el >= M) continue;
-    grad_corrections<P, KIND>(op, sW, sG + el * 20, sWH, sCG, el, f, k);
+  // BR1 gradients by line threads (element, line, viscous variable):
+  //  rows : x-part   sum_i D[b][i] J11(xi_i) W[a][i] + lR[b] cx1 - lL[b] cx3 (and y with -J01)
+  //  cols : eta-part sum_i D[a][i] (-J10 | J00)(eta_i) W[i][b] + lR[a] c2 - lL[a] c0, then / det
+  // c_f = +-js_f n_f What_f - (trace of the metric-weighted W on face f)  (spatial.py:594-603)
+  constexpr int TH = BC<P>::THREADS;
+  constexpr int NLG = E * N * NW;
+  double* sPX = sGR;             // [NW][NPT] x partials, then gx
+  double* sPY = sGR + NW * NPT;  // [NW][NPT] y partials, then gy
+  for (int t = t0; t < NLG; t += TH) {
+    const int el = t / (N * NW), r = t % (N * NW), a = r / NW, c = r % NW;
+    const double* gq = sG + el * 20;
+    const Metric mt = metric(gq);
+    const double* Wr = sW + c * NPT + el * NP + a * N;
+    double wx[N], wy[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const double x = Wr[i], xi = C.xg[i];
+      wx[i] = mt.J11(xi) * x;
+      wy[i] = -mt.J01(xi) * x;
+    }
+    double tx1 = 0.0, ty1 = 0.0, tx3 = 0.0, ty3 = 0.0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      tx1 += C.eR[i] * wx[i];
+      ty1 += C.eR[i] * wy[i];
+      tx3 += C.eL[i] * wx[i];
+      ty3 += C.eL[i] * wy[i];
+    }
+    const double wh1 = sWH[c * NFT + el * 4 * N + 1 * N + a];
+    const double wh3 = sWH[c * NFT + el * 4 * N + 3 * N + (N - 1 - a)];
+    const double cx1 = gq[17] * (gq[10] * wh1) - tx1;
+    const double cy1 = gq[17] * (gq[11] * wh1) - ty1;
+    const double cx3 = -gq[19] * (gq[14] * wh3) - tx3;
+    const double cy3 = -gq[19] * (gq[15] * wh3) - ty3;
+    double* px = sPX + c * NPT + el * NP + a * N;
+    double* py = sPY + c * NPT + el * NP + a * N;
+#pragma unroll
+    for (int b = 0; b < N; ++b) {
+      double sx = 0.0, sy = 0.0;
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        sx += C.D[b * N + i] * wx[i];
+        sy += C.D[b * N + i] * wy[i];
+      }
+      px[b] = (sx + C.lR[b] * cx1) - C.lL[b] * cx3;
+      py[b] = (sy + C.lR[b] * cy1) - C.lL[b] * cy3;
+    }
   }
   __syncthreads();
-  if (t0 < NPT) {
-    const int el = t0 / NP, pt = t0 % NP;
-    double gx[NW], gy[NW];
-    gradient_at<P, KIND>(op, sW, sG + el * 20, sCG, el, pt / N, pt % N, gx, gy);
+  for (int t = t0; t < NLG; t += TH) {
+    const int el = t / (N * NW), r = t % (N * NW), b = r / NW, c = r % NW;
+    const double* gq = sG + el * 20;
+    const Metric mt = metric(gq);
+    const double* Wc = sW + c * NPT + el * NP + b;
+    double vx[N], vy[N];
 #pragma unroll
-    for (int c = 0; c < NW; ++c) {
-      sGR[c * NPT + t0] = gx[c];
-      sGR[(NW + c) * NPT + t0] = gy[c];
+    for (int i = 0; i < N; ++i) {
+      const double y = Wc[i * N], eta = C.xg[i];
+      vx[i] = -mt.J10(eta) * y;
+      vy[i] = mt.J00(eta) * y;
     }
-    if (grad != nullptr && e0 + el < M) {
-      double* gd = grad + ((e0 + el) * NP + pt) * (2 * NW);
+    double tx2 = 0.0, ty2 = 0.0, tx0 = 0.0, ty0 = 0.0;
 #pragma unroll
-      for (int c = 0; c < NW; ++c) {
-        gd[c] = gx[c];
-        gd[NW + c] = gy[c];
+    for (int i = 0; i < N; ++i) {
+      tx2 += C.eR[i] * vx[i];
+      ty2 += C.eR[i] * vy[i];
+      tx0 += C.eL[i] * vx[i];
+      ty0 += C.eL[i] * vy[i];
+    }
+    const double wh2 = sWH[c * NFT + el * 4 * N + 2 * N + (N - 1 - b)];
+    const double wh0 = sWH[c * NFT + el * 4 * N + 0 * N + b];
+    const double cx2 = gq[18] * (gq[12] * wh2) - tx2;
+    const double cy2 = gq[18] * (gq[13] * wh2) - ty2;
+    const double cx0 = -gq[16] * (gq[8] * wh0) - tx0;
+    const double cy0 = -gq[16] * (gq[9] * wh0) - ty0;
+    const double xb = C.xg[b];
+    const double j11b = mt.J11(xb), j01b = mt.J01(xb);
+    const bool live = e0 + el < M;
+#pragma unroll
+    for (int a = 0; a < N; ++a) {
+      double dx = 0.0, dy = 0.0;
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        dx += C.D[a * N + i] * vx[i];
+        dy += C.D[a * N + i] * vy[i];
+      }
+      const double xa = C.xg[a];
+      const double idet = rcp(mt.J00(xa) * j11b - j01b * mt.J10(xa));
+      const int pt = a * N + b;
+      double* px = sPX + c * NPT + el * NP + pt;
+      double* py = sPY + c * NPT + el * NP + pt;
+      const double gxv = (((*px) + dx) + C.lR[a] * cx2 - C.lL[a] * cx0) * idet;
+      const double gyv = (((*py) + dy) + C.lR[a] * cy2 - C.lL[a] * cy0) * idet;
+      *px = gxv;
+      *py = gyv;
+      if (grad != nullptr && live) {
+        double* gd = grad + ((e0 + el) * NP + pt) * (2 * NW);
+        gd[c] = gxv;
+        gd[NW + c] = gyv;
       }
     }
   }
