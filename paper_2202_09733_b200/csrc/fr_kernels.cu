@@ -677,6 +677,82 @@ k_trace(const FrConst C, const FrMesh m, const double* __restrict__ q, const dou
   }
 }
 
+// Phase 1 by line threads (4 conserved variables): thread (element, line,
+// direction) reads one row (contiguous N x 4 doubles) or column of q --
+// forming q + eps X on the fly with the reference's rounding -- and writes
+// the two face traces at that line's ends.  Row threads also check the
+// points of their row and write the perturbed state.  No shared memory,
+// no barrier.
+template <int P, int KIND>
+__global__ void __launch_bounds__(128)
+k_trace_lines(const FrConst C, const FrMesh m, const double* __restrict__ q, const double* __restrict__ X,
+              double eps, double* __restrict__ qp, double* __restrict__ qtr, int* __restrict__ bad) {
+  constexpr int N = P + 1, NP = N * N, NV = 4;
+  const int64_t t = (int64_t)blockIdx.x * 128 + threadIdx.x;
+  if (t >= m.M * 2 * N) return;
+  const int64_t e = t / (2 * N);
+  const int r = (int)(t - e * 2 * N);
+  const bool row = r < N;
+  const int line = row ? r : r - N;
+  const int stride = row ? NV : N * NV;  // between consecutive points of the line
+  const int64_t base = e * NP * NV + (row ? (int64_t)line * N * NV : (int64_t)line * NV);
+  double v[N][NV];
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    const double2 a = __ldg(reinterpret_cast<const double2*>(q + base + i * stride));
+    const double2 b = __ldg(reinterpret_cast<const double2*>(q + base + i * stride) + 1);
+    v[i][0] = a.x;
+    v[i][1] = a.y;
+    v[i][2] = b.x;
+    v[i][3] = b.y;
+  }
+  if (X != nullptr) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const double2 a = __ldg(reinterpret_cast<const double2*>(X + base + i * stride));
+      const double2 b = __ldg(reinterpret_cast<const double2*>(X + base + i * stride) + 1);
+      v[i][0] = __dadd_rn(v[i][0], __dmul_rn(eps, a.x));
+      v[i][1] = __dadd_rn(v[i][1], __dmul_rn(eps, a.y));
+      v[i][2] = __dadd_rn(v[i][2], __dmul_rn(eps, b.x));
+      v[i][3] = __dadd_rn(v[i][3], __dmul_rn(eps, b.y));
+    }
+    if (row) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        double2* o = reinterpret_cast<double2*>(qp + base + i * stride);
+        o[0] = make_double2(v[i][0], v[i][1]);
+        o[1] = make_double2(v[i][2], v[i][3]);
+      }
+    }
+  }
+  const double g = C.gamma;
+  if (bad != nullptr && row) {
+    bool ok = true;
+#pragma unroll
+    for (int i = 0; i < N; ++i) ok = ok && physical(v[i], g);
+    if (!ok) atomicMin(bad, (int)e);
+  }
+  // rows: face 1 (xi=+1) point k=line, face 3 (xi=-1) point k=N-1-line
+  // cols: face 2 (eta=+1) point k=N-1-line, face 0 (eta=-1) point k=line
+  double tp[NV], tm[NV];
+#pragma unroll
+  for (int c = 0; c < NV; ++c) {
+    double sp = 0.0, sm = 0.0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      sp += C.eR[i] * v[i][c];
+      sm += C.eL[i] * v[i][c];
+    }
+    tp[c] = sp;
+    tm[c] = sm;
+  }
+  const int fp = row ? 1 : 2, fm = row ? 3 : 0;
+  const int kp = row ? line : N - 1 - line, km = row ? N - 1 - line : line;
+  if (bad != nullptr && !(physical(tp, g) && physical(tm, g))) atomicMin(bad + 1, (int)e);
+  st_face<NV>(qtr + ((e * 4 + fp) * N + kp) * NV, tp);
+  st_face<NV>(qtr + ((e * 4 + fm) * N + km) * NV, tm);
+}
+
 // ---------------------------------------------------------------------------
 // phase 2: one-sided viscous normal flux on every face (spatial.py:536-557)
 
@@ -1642,7 +1718,12 @@ static int run_residual(const DiscDev& d, const double* q, const double* X, doub
   const unsigned grid = (unsigned)((d.M + E - 1) / E);
   const double* qq = q;
   if (X != nullptr) qq = d.qp;
-  k_trace<P, KIND><<<grid, TH, L::BYTES_TRACE, st>>>(d.C, d.mesh, q, X, eps, d.qp, d.qtr, bad);
+  if constexpr (KT<KIND>::FLOW) {
+    const unsigned gl = (unsigned)((d.M * 2 * (P + 1) + 127) / 128);
+    k_trace_lines<P, KIND><<<gl, 128, 0, st>>>(d.C, d.mesh, q, X, eps, d.qp, d.qtr, bad);
+  } else {
+    k_trace<P, KIND><<<grid, TH, L::BYTES_TRACE, st>>>(d.C, d.mesh, q, X, eps, d.qp, d.qtr, bad);
+  }
   if (KT<KIND>::VISC) k_fvn<P, KIND><<<grid, TH, L::BYTES_FVN, st>>>(d.C, d.mesh, qq, d.qtr, d.fvn, d.grad);
   if constexpr (KT<KIND>::NV == 4 && E * BC<P>::NF <= TH)
     k_assemble_async<P, KIND><<<grid, TH, L::BYTES_ASM, st>>>(d.C, d.mesh, qq, d.qtr, d.fvn, d.grad, epi, out, bad,
@@ -1663,7 +1744,12 @@ static int run_freeze(const DiscDev& d, const double* q, double* qtr, double* fv
     attr = true;
   }
   const unsigned grid = (unsigned)((d.M + E - 1) / E);
-  k_trace<P, KIND><<<grid, TH, L::BYTES_TRACE, st>>>(d.C, d.mesh, q, nullptr, 0.0, nullptr, qtr, nullptr);
+  if constexpr (KT<KIND>::FLOW) {
+    const unsigned gl = (unsigned)((d.M * 2 * (P + 1) + 127) / 128);
+    k_trace_lines<P, KIND><<<gl, 128, 0, st>>>(d.C, d.mesh, q, nullptr, 0.0, nullptr, qtr, nullptr);
+  } else {
+    k_trace<P, KIND><<<grid, TH, L::BYTES_TRACE, st>>>(d.C, d.mesh, q, nullptr, 0.0, nullptr, qtr, nullptr);
+  }
   if (KT<KIND>::VISC) k_fvn<P, KIND><<<grid, TH, L::BYTES_FVN, st>>>(d.C, d.mesh, q, qtr, fvn, nullptr);
   return (int)cudaGetLastError();
 }
