@@ -44,6 +44,7 @@ PMGB_API const char* pmgb_error_string(int code) {
     case -1: return "invalid argument";
     case -2: return "unsupported polynomial degree (0..5)";
     case -3: return "unsupported equation kind";
+    case -4: return "mesh too large for one device context (face offsets exceed 2^31)";
     case -1000: return "no kernel instance for this degree/kind";
     case -1001: return "vector count out of range";
   }
@@ -54,6 +55,7 @@ PMGB_API int pmgb_disc_create(const pmgb_disc_desc* desc, pmgb_disc** out) {
   if (!desc || !out) return -1;
   if (desc->degree < 0 || desc->degree > 5) return -2;
   if (desc->kind < 0 || desc->kind > 2) return -3;
+  if (desc->n_elem * 4 * (desc->degree + 1) * 4 >= ((int64_t)1 << 31)) return -4;  // 32-bit face offsets
   pmgb_disc* h = new pmgb_disc();
   DiscDev& d = h->d;
   std::memset(&d.C, 0, sizeof(d.C));

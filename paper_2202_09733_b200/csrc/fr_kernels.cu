@@ -1324,39 +1324,30 @@ k_assemble_async(const FrConst C, const FrMesh m, const double* __restrict__ q, 
       }
     }
   }
-  // face threads: gathers and common face flux, no shared memory needed
+  // face threads: gathers and common face flux, no shared memory needed.
+  // 32-bit element-relative offsets (host guarantees M*4*N*NV < 2^31); the
+  // L/R operand order of the Roe flux is chosen by address, not by selects.
   if (t0 < E * NF) {
     const int fel = t0 / NF, r = t0 % NF, f = r / N, k = r % N;
     if (fel < ne) {
-      const int64_t e = e0 + fel;
+      const int e = (int)e0 + fel;
       const int2 lk = m.link[e * 4 + f];
       const bool interior = lk.x >= 0;
+      const bool left = !interior || lk_left(lk.y);
       const int kk = lk_rev(lk.y) ? N - 1 - k : k;
-      const int64_t own = ((e * 4 + f) * N + k) * NV;
-      const int64_t nbi = interior ? (((int64_t)lk.x * 4 + lk_face(lk.y)) * N + kk) * NV : own;
-      double tr[NV], nb[NV], Fo[NV], Fn[NV], F[NV];
-      ld_face<NV>(qtr + own, tr);
-      ld_face<NV>(qtr + nbi, nb);
+      const int own = ((e * 4 + f) * N + k) * NV;
+      const int nbi = interior ? ((lk.x * 4 + lk_face(lk.y)) * N + kk) * NV : own;
+      double qa[NV], qc[NV], Fo[NV], Fn[NV], F[NV];
+      ld_face<NV>(qtr + (left ? own : nbi), qa);
+      ld_face<NV>(qtr + (left ? nbi : own), qc);
       if constexpr (VISC) {
         ld_face<NV>(fvn + own, Fo);
         ld_face<NV>(fvn + nbi, Fn);
       }
-      const double2 no = __ldg(reinterpret_cast<const double2*>(m.geom + e * 20 + 8 + 2 * f));
-      const bool left = !interior || lk_left(lk.y);
-      double nux = no.x, nuy = no.y;
-      if (!left) {
-        const double2 nn = __ldg(reinterpret_cast<const double2*>(m.geom + (int64_t)lk.x * 20 + 8 + 2 * lk_face(lk.y)));
-        nux = nn.x;
-        nuy = nn.y;
-      }
-      if (!interior) ghost<KIND>(tr, lk_tag(lk.y), no.x, no.y, C.qinf, nb);
-      double qa[NV], qc[NV];
-#pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        qa[v] = left ? tr[v] : nb[v];
-        qc[v] = left ? nb[v] : tr[v];
-      }
-      num_flux<KIND>(qa, qc, nux, nuy, ph, F);
+      const int gface = left ? e * 20 + 8 + 2 * f : lk.x * 20 + 8 + 2 * lk_face(lk.y);
+      const double2 nu = __ldg(reinterpret_cast<const double2*>(m.geom + gface));
+      if (!interior) ghost<KIND>(qa, lk_tag(lk.y), nu.x, nu.y, C.qinf, qc);
+      num_flux<KIND>(qa, qc, nu.x, nu.y, ph, F);
 #pragma unroll
       for (int v = 0; v < NV; ++v) F[v] = left ? F[v] : -F[v];
       if constexpr (VISC) {
