@@ -944,25 +944,34 @@ k_fvn(const FrConst C, const FrMesh m, const double* __restrict__ q, const doubl
     }
   }
   __syncthreads();
-  for (int t = threadIdx.x; t < E * NF; t += BC<P>::THREADS) {
-    const int el = t / NF, r = t % NF, f = r / N, k = r % N;
-    const int64_t e = e0 + el;
-    if (e >= M) continue;
-    double gx[NW], gy[NW];
+  // one-sided viscous normal flux on every own face point (spatial.py:456-464)
+  auto face_fvn = [&](int el, int f, int k, const double* trv) {
+    const Line Lf = face_line<N>(op, f, k);
+    double gxv[NW], gyv[NW];
 #pragma unroll
     for (int c = 0; c < NW; ++c) {
-      gx[c] = line_sum<N>(op, sGR + c * NPT + el * NP, f, k);
-      gy[c] = line_sum<N>(op, sGR + (NW + c) * NPT + el * NP, f, k);
+      gxv[c] = line_sum<N>(Lf, sGR + c * NPT + el * NP);
+      gyv[c] = line_sum<N>(Lf, sGR + (NW + c) * NPT + el * NP);
     }
-    double tr[NV];
-    ld_face<NV>(qtr + ((e * 4 + f) * N + k) * NV, tr);
     double fx[NV], fy[NV];
-    visc_flux<KIND>(tr, gx, gy, ph, fx, fy);
+    visc_flux<KIND>(trv, gxv, gyv, ph, fx, fy);
     const double nx = sG[el * 20 + 8 + 2 * f], ny = sG[el * 20 + 9 + 2 * f];
     double o[NV];
 #pragma unroll
     for (int v = 0; v < NV; ++v) o[v] = fx[v] * nx + fy[v] * ny;
-    st_face<NV>(fvn + ((e * 4 + f) * N + k) * NV, o);
+    st_face<NV>(fvn + ((((int)e0 + el) * 4 + f) * N + k) * NV, o);
+  };
+  if constexpr (ONE_FACE) {
+    // own trace still in registers from the prologue gather
+    if (face_live) face_fvn(fel, ff, (t0 % NF) % N, tr);
+  } else {
+    for (int t = threadIdx.x; t < E * NF; t += BC<P>::THREADS) {
+      const int el = t / NF, r = t % NF, f = r / N, k = r % N;
+      if (e0 + el >= M) continue;
+      double trv[NV];
+      ld_face<NV>(qtr + ((((int)e0 + el) * 4 + f) * N + k) * NV, trv);
+      face_fvn(el, f, k, trv);
+    }
   }
 }
 
