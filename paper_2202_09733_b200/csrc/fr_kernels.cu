@@ -110,6 +110,12 @@ __device__ __forceinline__ int fpt(int f, int k, int i) {
 // is 1e-12 relative).  Valid states only feed positive normal inputs;
 // non-physical inputs still produce NaN/Inf, and the physicality flags are
 // evaluated on the raw state, not through these.
+// Programmatic dependent launch: a kernel launched with the PDL attribute
+// may start while its predecessor drains; it must wait before touching the
+// predecessor's outputs.  Both are no-ops for ordinary launches.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::); }
+
 __device__ __forceinline__ double rcp(double x) {
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
@@ -688,6 +694,7 @@ __global__ void __launch_bounds__(128)
 k_trace_lines(const FrConst C, const FrMesh m, const double* __restrict__ q, const double* __restrict__ X,
               double eps, double* __restrict__ qp, double* __restrict__ qtr, int* __restrict__ bad) {
   constexpr int N = P + 1, NP = N * N, NV = 4;
+  pdl_trigger();
   const int64_t t = (int64_t)blockIdx.x * 128 + threadIdx.x;
   if (t >= m.M * 2 * N) return;
   const int64_t e = t / (2 * N);
@@ -764,6 +771,7 @@ k_fvn(const FrConst C, const FrMesh m, const double* __restrict__ q, const doubl
   using L = SL<P, KIND>;
   constexpr int N = BC<P>::N, NP = BC<P>::NP, NF = BC<P>::NF, E = BC<P>::EPB;
   constexpr int NV = KT<KIND>::NV, NW = KT<KIND>::NW, NPT = L::NPT, NFT = L::NFT;
+  pdl_trigger();
   const Ops op = stage_ops<BC<P>::THREADS>(C, sm);
   double* sQ = sm + L::Q;
   double* sG = sm + L::G;
@@ -784,6 +792,7 @@ k_fvn(const FrConst C, const FrMesh m, const double* __restrict__ q, const doubl
   int2 lk = make_int2(-1, 0);
   bool face_live = false;
   int fel = 0, ff = 0;
+  pdl_wait();  // traces come from k_trace
   if constexpr (ONE_FACE) {
     if (t0 < E * NF) {
       fel = t0 / NF;
@@ -1294,7 +1303,6 @@ k_assemble_async(const FrConst C, const FrMesh m, const double* __restrict__ q, 
   constexpr int NV = KT<KIND>::NV, NW = KT<KIND>::NW, NPT = L::NPT, NFT = L::NFT;
   constexpr bool VISC = KT<KIND>::VISC;
   static_assert(NV == 4 && E * NF <= TH, "async assemble: flow kinds, one face point per thread");
-  if (blockIdx.x == 0 && threadIdx.x == 0) commit_status(bad, st);
   double* sQA = sm + L::Q;  // AoS [E][NP][NV]
   double* sG = sm + L::G;
   double* sFC = sm + L::A_FC;
@@ -1314,6 +1322,8 @@ k_assemble_async(const FrConst C, const FrMesh m, const double* __restrict__ q, 
   }
   const Ops op = stage_ops<TH>(C, sm);
   const Phys ph = phys_of(C);
+  pdl_wait();  // gradients / fvn from k_fvn, traces and status flags from k_trace
+  if (blockIdx.x == 0 && threadIdx.x == 0) commit_status(bad, st);
   // point gradients into registers
   double gx[NW], gy[NW];
   if constexpr (VISC) {
@@ -1697,6 +1707,23 @@ k_blocks(const FrConst C, const FrMesh m, const double* __restrict__ q, const do
 static __device__ int g_bad[2] = {INT_MAX, INT_MAX};
 static __device__ Status g_status = {0, 0, 0};
 
+// launch with programmatic stream serialization (PDL) enabled
+template <typename... KArgs, typename... Args>
+static void launch_pdl(void (*kernel)(KArgs...), unsigned grid, int threads, size_t smem, cudaStream_t st,
+                       Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 template <int P, int KIND>
 static int run_residual(const DiscDev& d, const double* q, const double* X, double eps, const Epi& epi,
                         double* out, cudaStream_t st) {
@@ -1724,10 +1751,11 @@ static int run_residual(const DiscDev& d, const double* q, const double* X, doub
   } else {
     k_trace<P, KIND><<<grid, TH, L::BYTES_TRACE, st>>>(d.C, d.mesh, q, X, eps, d.qp, d.qtr, bad);
   }
-  if (KT<KIND>::VISC) k_fvn<P, KIND><<<grid, TH, L::BYTES_FVN, st>>>(d.C, d.mesh, qq, d.qtr, d.fvn, d.grad);
+  if (KT<KIND>::VISC) launch_pdl(k_fvn<P, KIND>, grid, TH, L::BYTES_FVN, st, d.C, d.mesh, qq, (const double*)d.qtr,
+                                 d.fvn, d.grad);
   if constexpr (KT<KIND>::NV == 4 && E * BC<P>::NF <= TH)
-    k_assemble_async<P, KIND><<<grid, TH, L::BYTES_ASM, st>>>(d.C, d.mesh, qq, d.qtr, d.fvn, d.grad, epi, out, bad,
-                                                              stp);
+    launch_pdl(k_assemble_async<P, KIND>, grid, TH, L::BYTES_ASM, st, d.C, d.mesh, qq, (const double*)d.qtr,
+               (const double*)d.fvn, (const double*)d.grad, epi, out, bad, stp);
   else
     k_assemble<P, KIND><<<grid, TH, L::BYTES_ASM, st>>>(d.C, d.mesh, qq, d.qtr, d.fvn, d.grad, epi, out, bad, stp);
   return (int)cudaGetLastError();
