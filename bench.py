@@ -246,22 +246,23 @@ def run_ours(args):
     rate_jv = pdist.job_rate(n * K, ws, t_jv) / 1e9
     per_gpu_r = n / (t_r / K)
 
-    # e2e through the public API with host buffers: H2D of q, R, D2H of R
-    qh = torch.from_numpy(case.q0.copy()).pin_memory()
-    Rh = torch.empty(n, dtype=torch.float64).pin_memory()
-    qd = torch.empty(n, dtype=torch.float64, device="cuda")
-
-    def e2e_step(i):
-        qd.copy_(qh, non_blocking=True)
-        R = disc.eval(qd, _lib.EPI_R, Rs[0])
-        Rh.copy_(R, non_blocking=True)
-    for i in range(W):
-        e2e_step(i)
-    t_e2e = event_time(torch, e2e_step, K)
+    # e2e through the public API with host buffers: every step copies its q
+    # from pinned host memory, evaluates R and copies R back; the
+    # Discretization.residual_batch call overlaps step i's H2D, step i-1's
+    # compute and step i-2's D2H on two copy engines + the compute stream.
+    qh = [torch.from_numpy(case.q0.copy()).pin_memory() for _ in range(2)]
+    Rh = [torch.empty(n, dtype=torch.float64).pin_memory() for _ in range(2)]
+    disc.residual_batch([qh[i % 2] for i in range(W)], [Rh[i % 2] for i in range(W)])
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    disc.residual_batch([qh[i % 2] for i in range(K)], [Rh[i % 2] for i in range(K)])
+    e1.record()
+    e1.synchronize()
+    t_e2e = e0.elapsed_time(e1) * 1e-3
     t_e2e, = pdist.max_over_ranks([t_e2e], "cuda")
     rate_e2e = pdist.job_rate(n * K, ws, t_e2e) / 1e9
-    # parity spot check of the e2e result against the device-resident path
-    torch.cuda.synchronize()
+    e2e_ok = bool(np.array_equal(Rh[(K - 1) % 2].numpy(), disc.residual(qs[0]).cpu().numpy()))
 
     # JFNK-pMG time step (the metric's second half)
     step = {}
@@ -296,7 +297,9 @@ def run_ours(args):
             "bound_gdofs": min(hbm_peak / BYTES_PER_DOF_R, fp64_peak * 1e3 / FLOP_PER_DOF_R[case.p]),
             "traffic": None,
         },
-        "e2e": {"value": rate_e2e, "unit": UNIT, "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n},
+        "e2e": {"value": rate_e2e, "unit": UNIT, "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
+                "api": "Discretization.residual_batch (pinned host in/out, copies overlapped with compute)",
+                "matches_device_path": e2e_ok},
         "gpu_launches": int(launches_r),
         "clocks": clk.summary(),
         "step_time": step,

@@ -206,6 +206,52 @@ class Discretization:
         R = self.eval(q, _lib.EPI_R, check_status=True)
         return R.cpu().numpy()
 
+    def residual_batch(self, qs, outs=None):
+        """R(q) for a sequence of HOST arrays, copies overlapped with compute.
+
+        Step i's host->device copy, step i-1's residual and step i-2's
+        device->host copy run concurrently on three streams (two copy
+        engines + compute), with double-buffered device staging.  Inputs
+        should be pinned CPU tensors for full PCIe bandwidth; results go to
+        ``outs`` (pinned CPU tensors, same length) or new pinned tensors.
+        Raises NonPhysicalStateError after the batch if any step produced a
+        non-physical state (the first one, as latched on the device)."""
+        n = self.n_dofs
+        qs = [q if isinstance(q, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(q)) for q in qs]
+        if outs is None:
+            outs = [torch.empty(n, dtype=torch.float64).pin_memory() for _ in qs]
+        dev = self.device
+        s_in, s_cmp, s_out = (torch.cuda.Stream(dev) for _ in range(3))
+        dq = [torch.empty(n, dtype=torch.float64, device=dev) for _ in range(2)]
+        dr = [torch.empty(n, dtype=torch.float64, device=dev) for _ in range(2)]
+        ev_in = [torch.cuda.Event() for _ in qs]
+        ev_cmp = [torch.cuda.Event() for _ in qs]
+        ev_out = [torch.cuda.Event() for _ in qs]
+        cur = torch.cuda.current_stream(dev)
+        for st in (s_in, s_cmp, s_out):
+            st.wait_stream(cur)
+        for i, q in enumerate(qs):
+            b = i % 2
+            with torch.cuda.stream(s_in):
+                if i >= 2:
+                    s_in.wait_event(ev_cmp[i - 2])   # staging buffer free
+                dq[b].copy_(q, non_blocking=True)
+                ev_in[i].record(s_in)
+            with torch.cuda.stream(s_cmp):
+                s_cmp.wait_event(ev_in[i])
+                if i >= 2:
+                    s_cmp.wait_event(ev_out[i - 2])  # result buffer drained
+                self.eval(dq[b], _lib.EPI_R, dr[b])
+                ev_cmp[i].record(s_cmp)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(ev_cmp[i])
+                outs[i].copy_(dr[b], non_blocking=True)
+                ev_out[i].record(s_out)
+        for st in (s_in, s_cmp, s_out):
+            cur.wait_stream(st)
+        raise_status()
+        return outs
+
     def freeze(self, data) -> FrozenState:
         q = to_device(data, self.device)
         qtr = torch.empty(self._face_shape, dtype=torch.float64, device=self.device)

@@ -142,3 +142,13 @@ def test_local_equals_global(cuda):
     for e in (0, 4, 7):
         Re = dev.element_residual(e, q[orc.offsets[e]:orc.offsets[e + 1]].reshape(3, 3, 4), fr)
         assert np.max(np.abs(Re.reshape(-1) - R[orc.offsets[e]:orc.offsets[e + 1]])) <= 1e-12
+
+
+def test_residual_batch_host_pipeline(cuda):
+    c = cases.config(1)
+    dev = Discretization(c.mesh, c.p, c.eqn)
+    rng = np.random.default_rng(3)
+    qs = [c.q0 * (1.0 + 1e-3 * rng.standard_normal(c.q0.shape)) for _ in range(5)]
+    outs = dev.residual_batch([torch.from_numpy(q).pin_memory() for q in qs])
+    for q, R in zip(qs, outs):
+        assert np.array_equal(R.numpy(), dev.residual(q))
