@@ -858,8 +858,10 @@ k_fvn(const FrConst C, const FrMesh m, const double* __restrict__ q, const doubl
   constexpr int NLG = E * N * NW;
   double* sPX = sGR;             // [NW][NPT] x partials, then gx
   double* sPY = sGR + NW * NPT;  // [NW][NPT] y partials, then gy
+  // pass 1, rows: thread t = (c, el, a) with a fastest, so the row it reads
+  // and writes starts at N * t (stride N odd: no bank conflicts)
   for (int t = t0; t < NLG; t += TH) {
-    const int el = t / (N * NW), r = t % (N * NW), a = r / NW, c = r % NW;
+    const int c = t / (E * N), el = (t / N) % E, a = t % N;
     const double* gq = sG + el * 20;
     const Metric mt = metric(gq);
     const double* Wr = sW + c * NPT + el * NP + a * N;
@@ -899,8 +901,12 @@ k_fvn(const FrConst C, const FrMesh m, const double* __restrict__ q, const doubl
     }
   }
   __syncthreads();
+  // pass 2, columns: thread t = (b, el, c) finishes column b of both
+  // gradient components and forms their traces on faces 0 (eL) and 2 (eR)
+  // in sGF, summed in line_sum's order
+  double* sGF = sm + L::CG;  // [2NW] face planes: gradient traces (CCW k)
   for (int t = t0; t < NLG; t += TH) {
-    const int el = t / (N * NW), r = t % (N * NW), b = r / NW, c = r % NW;
+    const int b = t / (E * NW), el = (t / NW) % E, c = t % NW;
     const double* gq = sG + el * 20;
     const Metric mt = metric(gq);
     const double* Wc = sW + c * NPT + el * NP + b;
@@ -927,7 +933,7 @@ k_fvn(const FrConst C, const FrMesh m, const double* __restrict__ q, const doubl
     const double cy0 = -gq[16] * (gq[9] * wh0) - ty0;
     const double xb = C.xg[b];
     const double j11b = mt.J11(xb), j01b = mt.J01(xb);
-    const bool live = e0 + el < M;
+    double fx0 = 0.0, fy0 = 0.0, fx2 = 0.0, fy2 = 0.0;
 #pragma unroll
     for (int a = 0; a < N; ++a) {
       double dx = 0.0, dy = 0.0;
@@ -945,22 +951,56 @@ k_fvn(const FrConst C, const FrMesh m, const double* __restrict__ q, const doubl
       const double gyv = (((*py) + dy) + C.lR[a] * cy2 - C.lL[a] * cy0) * idet;
       *px = gxv;
       *py = gyv;
-      if (grad != nullptr && live) {
-        double* gd = grad + ((e0 + el) * NP + pt) * (2 * NW);
-        gd[c] = gxv;
-        gd[NW + c] = gyv;
-      }
+      fx0 += C.eL[a] * gxv;
+      fy0 += C.eL[a] * gyv;
+      fx2 += C.eR[a] * gxv;
+      fy2 += C.eR[a] * gyv;
+    }
+    const int s0 = el * 4 * N + 0 * N + b, s2 = el * 4 * N + 2 * N + (N - 1 - b);
+    sGF[c * NFT + s0] = fx0;
+    sGF[(NW + c) * NFT + s0] = fy0;
+    sGF[c * NFT + s2] = fx2;
+    sGF[(NW + c) * NFT + s2] = fy2;
+  }
+  __syncthreads();
+  // pass 3, rows of the final gradients: traces on faces 1 (eR) and 3 (eL)
+  for (int t = t0; t < NLG; t += TH) {
+    const int c = t / (E * N), el = (t / N) % E, a = t % N;
+    const double* gxr = sPX + c * NPT + el * NP + a * N;
+    const double* gyr = sPY + c * NPT + el * NP + a * N;
+    double fx1 = 0.0, fy1 = 0.0, fx3 = 0.0, fy3 = 0.0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const double x = gxr[i], y = gyr[i];
+      fx1 += C.eR[i] * x;
+      fy1 += C.eR[i] * y;
+      fx3 += C.eL[i] * x;
+      fy3 += C.eL[i] * y;
+    }
+    const int s1 = el * 4 * N + 1 * N + a, s3 = el * 4 * N + 3 * N + (N - 1 - a);
+    sGF[c * NFT + s1] = fx1;
+    sGF[(NW + c) * NFT + s1] = fy1;
+    sGF[c * NFT + s3] = fx3;
+    sGF[(NW + c) * NFT + s3] = fy3;
+  }
+  // point gradients to global, coalesced in the [M][NP][2NW] layout
+  if (grad != nullptr) {
+    const int nlive = (int)((M - e0) < E ? (M - e0) : E) * NP * 2 * NW;
+    double* gb = grad + e0 * NP * 2 * NW;
+    for (int i = t0; i < nlive; i += TH) {
+      const int pt = i / (2 * NW), comp = i % (2 * NW);
+      gb[i] = sGR[comp * NPT + pt];
     }
   }
   __syncthreads();
   // one-sided viscous normal flux on every own face point (spatial.py:456-464)
   auto face_fvn = [&](int el, int f, int k, const double* trv) {
-    const Line Lf = face_line<N>(op, f, k);
     double gxv[NW], gyv[NW];
+    const int slot = el * 4 * N + f * N + k;
 #pragma unroll
     for (int c = 0; c < NW; ++c) {
-      gxv[c] = line_sum<N>(Lf, sGR + c * NPT + el * NP);
-      gyv[c] = line_sum<N>(Lf, sGR + (NW + c) * NPT + el * NP);
+      gxv[c] = sGF[c * NFT + slot];
+      gyv[c] = sGF[(NW + c) * NFT + slot];
     }
     double fx[NV], fy[NV];
     visc_flux<KIND>(trv, gxv, gyv, ph, fx, fy);

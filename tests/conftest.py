@@ -2,6 +2,11 @@ import os
 import sys
 from pathlib import Path
 
+# The oracle's BLAS reductions must not depend on the host's core count:
+# discrete outcomes (PTC / GMRES iteration counts) are compared exactly.
+for _v in ("OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+    os.environ.setdefault(_v, "1")
+
 import pytest
 
 ROOT = Path(__file__).resolve().parents[1]
@@ -10,6 +15,11 @@ if str(ROOT) not in sys.path:
 
 
 def pytest_configure(config):
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(1, user_api="blas")
+    except ImportError:
+        pass
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a) and the built library")
     config.addinivalue_line("markers", "slow: long-running CPU check")
 
