@@ -55,7 +55,12 @@ struct SL {
   static constexpr int TR = GR + 2 * NW * NPT;    // [NV] face planes    own traces (local pipeline)
   static constexpr int R0 = TR + NV * NFT;        // [NP*NV]             unperturbed local residual
   static constexpr int END_LOCAL = R0 + NP * NV;
-  static constexpr int GR_FVN = FC;               // k_fvn keeps gradients where FC would be
+  // k_fvn: face planes padded to an element stride of 4N+1 (bank spread),
+  // then the gradient planes, 16-byte aligned for the block copy to global
+  static constexpr int NFS = 4 * N + 1, NFTP = E * NFS;
+  static constexpr int F_WH = W + NW * NPT;       // [NW] padded face planes  BR1 common value
+  static constexpr int F_GF = F_WH + NW * NFTP;   // [2NW] padded face planes gradient traces
+  static constexpr int GR_FVN = (F_GF + 2 * NW * NFTP + 1) & ~1;  // [2NW] point planes
   // compact layout of k_assemble (gradients come from k_fvn)
   static constexpr int A_FC = Q + NV * NPT;
   static constexpr int A_FT = A_FC + NV * NFT;
@@ -770,14 +775,13 @@ k_fvn(const FrConst C, const FrMesh m, const double* __restrict__ q, const doubl
   extern __shared__ double sm[];
   using L = SL<P, KIND>;
   constexpr int N = BC<P>::N, NP = BC<P>::NP, NF = BC<P>::NF, E = BC<P>::EPB;
-  constexpr int NV = KT<KIND>::NV, NW = KT<KIND>::NW, NPT = L::NPT, NFT = L::NFT;
+  constexpr int NV = KT<KIND>::NV, NW = KT<KIND>::NW, NPT = L::NPT, NFS = L::NFS, NFTP = L::NFTP;
   pdl_trigger();
   const Ops op = stage_ops<BC<P>::THREADS>(C, sm);
   double* sQ = sm + L::Q;
   double* sG = sm + L::G;
   double* sW = sm + L::W;
-  double* sWH = sm + L::WH;
-  double* sCG = sm + L::CG;
+  double* sWH = sm + L::F_WH;
   double* sGR = sm + L::GR_FVN;
   const int64_t e0 = (int64_t)blockIdx.x * E;
   const int64_t M = m.M;
@@ -829,7 +833,7 @@ k_fvn(const FrConst C, const FrMesh m, const double* __restrict__ q, const doubl
     grad_vars<KIND>(tr_, ph.gamma, wa);
     grad_vars<KIND>(nb_, ph.gamma, wc);
 #pragma unroll
-    for (int c = 0; c < NW; ++c) sWH[c * NFT + t] = 0.5 * (wa[c] + wc[c]);
+    for (int c = 0; c < NW; ++c) sWH[c * NFTP + el * NFS + (t - el * NF)] = 0.5 * (wa[c] + wc[c]);
   };
   if constexpr (ONE_FACE) {
     if (face_live) face_avg(t0, fel, ff, lk, tr, nb);
@@ -880,8 +884,8 @@ k_fvn(const FrConst C, const FrMesh m, const double* __restrict__ q, const doubl
       tx3 += C.eL[i] * wx[i];
       ty3 += C.eL[i] * wy[i];
     }
-    const double wh1 = sWH[c * NFT + el * 4 * N + 1 * N + a];
-    const double wh3 = sWH[c * NFT + el * 4 * N + 3 * N + (N - 1 - a)];
+    const double wh1 = sWH[c * NFTP + el * NFS + 1 * N + a];
+    const double wh3 = sWH[c * NFTP + el * NFS + 3 * N + (N - 1 - a)];
     const double cx1 = gq[17] * (gq[10] * wh1) - tx1;
     const double cy1 = gq[17] * (gq[11] * wh1) - ty1;
     const double cx3 = -gq[19] * (gq[14] * wh3) - tx3;
@@ -904,7 +908,7 @@ k_fvn(const FrConst C, const FrMesh m, const double* __restrict__ q, const doubl
   // pass 2, columns: thread t = (b, el, c) finishes column b of both
   // gradient components and forms their traces on faces 0 (eL) and 2 (eR)
   // in sGF, summed in line_sum's order
-  double* sGF = sm + L::CG;  // [2NW] face planes: gradient traces (CCW k)
+  double* sGF = sm + L::F_GF;  // [2NW] padded face planes: gradient traces (CCW k)
   for (int t = t0; t < NLG; t += TH) {
     const int b = t / (E * NW), el = (t / NW) % E, c = t % NW;
     const double* gq = sG + el * 20;
@@ -925,8 +929,8 @@ k_fvn(const FrConst C, const FrMesh m, const double* __restrict__ q, const doubl
       tx0 += C.eL[i] * vx[i];
       ty0 += C.eL[i] * vy[i];
     }
-    const double wh2 = sWH[c * NFT + el * 4 * N + 2 * N + (N - 1 - b)];
-    const double wh0 = sWH[c * NFT + el * 4 * N + 0 * N + b];
+    const double wh2 = sWH[c * NFTP + el * NFS + 2 * N + (N - 1 - b)];
+    const double wh0 = sWH[c * NFTP + el * NFS + 0 * N + b];
     const double cx2 = gq[18] * (gq[12] * wh2) - tx2;
     const double cy2 = gq[18] * (gq[13] * wh2) - ty2;
     const double cx0 = -gq[16] * (gq[8] * wh0) - tx0;
@@ -956,11 +960,11 @@ k_fvn(const FrConst C, const FrMesh m, const double* __restrict__ q, const doubl
       fx2 += C.eR[a] * gxv;
       fy2 += C.eR[a] * gyv;
     }
-    const int s0 = el * 4 * N + 0 * N + b, s2 = el * 4 * N + 2 * N + (N - 1 - b);
-    sGF[c * NFT + s0] = fx0;
-    sGF[(NW + c) * NFT + s0] = fy0;
-    sGF[c * NFT + s2] = fx2;
-    sGF[(NW + c) * NFT + s2] = fy2;
+    const int s0 = el * NFS + 0 * N + b, s2 = el * NFS + 2 * N + (N - 1 - b);
+    sGF[c * NFTP + s0] = fx0;
+    sGF[(NW + c) * NFTP + s0] = fy0;
+    sGF[c * NFTP + s2] = fx2;
+    sGF[(NW + c) * NFTP + s2] = fy2;
   }
   __syncthreads();
   // pass 3, rows of the final gradients: traces on faces 1 (eR) and 3 (eL)
@@ -977,30 +981,29 @@ k_fvn(const FrConst C, const FrMesh m, const double* __restrict__ q, const doubl
       fx3 += C.eL[i] * x;
       fy3 += C.eL[i] * y;
     }
-    const int s1 = el * 4 * N + 1 * N + a, s3 = el * 4 * N + 3 * N + (N - 1 - a);
-    sGF[c * NFT + s1] = fx1;
-    sGF[(NW + c) * NFT + s1] = fy1;
-    sGF[c * NFT + s3] = fx3;
-    sGF[(NW + c) * NFT + s3] = fy3;
+    const int s1 = el * NFS + 1 * N + a, s3 = el * NFS + 3 * N + (N - 1 - a);
+    sGF[c * NFTP + s1] = fx1;
+    sGF[(NW + c) * NFTP + s1] = fy1;
+    sGF[c * NFTP + s3] = fx3;
+    sGF[(NW + c) * NFTP + s3] = fy3;
   }
-  // point gradients to global, coalesced in the [M][NP][2NW] layout
+  // point gradients to global: the CTA's 2NW planes are one contiguous
+  // block of the [M/E][2NW][E*NP] scratch layout (allocation rounded up)
   if (grad != nullptr) {
-    const int nlive = (int)((M - e0) < E ? (M - e0) : E) * NP * 2 * NW;
-    double* gb = grad + e0 * NP * 2 * NW;
-    for (int i = t0; i < nlive; i += TH) {
-      const int pt = i / (2 * NW), comp = i % (2 * NW);
-      gb[i] = sGR[comp * NPT + pt];
-    }
+    constexpr int NB2 = NW * NPT;  // double2 per block
+    const double2* src = reinterpret_cast<const double2*>(sGR);
+    double2* dst = reinterpret_cast<double2*>(grad + (int64_t)blockIdx.x * (2 * NW * NPT));
+    for (int i = t0; i < NB2; i += TH) dst[i] = src[i];
   }
   __syncthreads();
   // one-sided viscous normal flux on every own face point (spatial.py:456-464)
   auto face_fvn = [&](int el, int f, int k, const double* trv) {
     double gxv[NW], gyv[NW];
-    const int slot = el * 4 * N + f * N + k;
+    const int slot = el * NFS + f * N + k;
 #pragma unroll
     for (int c = 0; c < NW; ++c) {
-      gxv[c] = sGF[c * NFT + slot];
-      gyv[c] = sGF[(NW + c) * NFT + slot];
+      gxv[c] = sGF[c * NFTP + slot];
+      gyv[c] = sGF[(NW + c) * NFTP + slot];
     }
     double fx[NV], fy[NV];
     visc_flux<KIND>(trv, gxv, gyv, ph, fx, fy);
@@ -1190,23 +1193,11 @@ k_assemble(const FrConst C, const FrMesh m, const double* __restrict__ q, const 
     if (t0 < NPT) {
       const int el = t0 / NP, pt = t0 % NP;
       if (e0 + el < M) {
-        const double* gs = grad + ((e0 + el) * NP + pt) * (2 * NW);
-        if constexpr (NW == 3) {
-          const double2 g0 = __ldg(reinterpret_cast<const double2*>(gs));
-          const double2 g1 = __ldg(reinterpret_cast<const double2*>(gs) + 1);
-          const double2 g2 = __ldg(reinterpret_cast<const double2*>(gs) + 2);
-          gx[0] = g0.x;
-          gx[1] = g0.y;
-          gx[2] = g1.x;
-          gy[0] = g1.y;
-          gy[1] = g2.x;
-          gy[2] = g2.y;
-        } else {
+        const double* gs = grad + (int64_t)blockIdx.x * (2 * NW * NPT) + t0;
 #pragma unroll
-          for (int c = 0; c < NW; ++c) {
-            gx[c] = __ldg(gs + c);
-            gy[c] = __ldg(gs + NW + c);
-          }
+        for (int c = 0; c < NW; ++c) {
+          gx[c] = __ldg(gs + c * NPT);
+          gy[c] = __ldg(gs + (NW + c) * NPT);
         }
       } else {
 #pragma unroll
@@ -1372,14 +1363,12 @@ k_assemble_async(const FrConst C, const FrMesh m, const double* __restrict__ q, 
     if (t0 < NPT) {
       const int el = t0 / NP, pt = t0 % NP;
       if (el < ne) {
-        const double2* gs = reinterpret_cast<const double2*>(grad + ((e0 + el) * NP + pt) * (2 * NW));
-        const double2 g0 = __ldg(gs), g1 = __ldg(gs + 1), g2 = __ldg(gs + 2);
-        gx[0] = g0.x;
-        gx[1] = g0.y;
-        gx[2] = g1.x;
-        gy[0] = g1.y;
-        gy[1] = g2.x;
-        gy[2] = g2.y;
+        const double* gs = grad + (int64_t)blockIdx.x * (2 * NW * NPT) + t0;
+#pragma unroll
+        for (int c = 0; c < NW; ++c) {
+          gx[c] = __ldg(gs + c * NPT);
+          gy[c] = __ldg(gs + (NW + c) * NPT);
+        }
       }
     }
   }

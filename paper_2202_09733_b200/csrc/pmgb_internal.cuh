@@ -101,7 +101,7 @@ struct DiscDev {
   int2* link;
   double* qtr;   // scratch traces (M,4,n,nv)
   double* fvn;   // scratch viscous flux (M,4,n,nv)
-  double* grad;  // scratch BR1 gradients at the points (M,n,n,2*nw)
+  double* grad;  // scratch BR1 gradients, per CTA block: [M/EPB][2*nw][EPB*n*n]
   double* qp;    // scratch perturbed state
   int nv;
   int64_t n_dofs;
