@@ -23,6 +23,9 @@
 #ifndef PMGB_FVN_REGS
 #define PMGB_FVN_REGS 64
 #endif
+#ifndef PMGB_FVN_REGS_P5
+#define PMGB_FVN_REGS_P5 80
+#endif
 #ifndef PMGB_TRACE_REGS
 #define PMGB_TRACE_REGS 40
 #endif
@@ -76,7 +79,7 @@ struct SL {
 template <int P> struct MinBlocks {
   static constexpr int cap(int v) { return v < 1 ? 1 : (v > 32 ? 32 : v); }
   static constexpr int ASM = cap(65536 / (BC<P>::THREADS * PMGB_REG_TARGET));
-  static constexpr int FVN = cap(65536 / (BC<P>::THREADS * PMGB_FVN_REGS));
+  static constexpr int FVN = cap(65536 / (BC<P>::THREADS * (P == 5 ? PMGB_FVN_REGS_P5 : PMGB_FVN_REGS)));
   static constexpr int TRACE = cap(65536 / (BC<P>::THREADS * PMGB_TRACE_REGS));
 };
 
