@@ -799,17 +799,21 @@ k_fvn(const FrConst C, const FrMesh m, const double* __restrict__ q, const doubl
   int2 lk = make_int2(-1, 0);
   bool face_live = false;
   int fel = 0, ff = 0;
-  pdl_wait();  // traces come from k_trace
+  // the link table is static mesh data: fetch it before the dependency wait
   if constexpr (ONE_FACE) {
     if (t0 < E * NF) {
       fel = t0 / NF;
-      const int r = t0 % NF;
-      ff = r / N;
-      const int fk = r % N;
+      ff = (t0 % NF) / N;
+      face_live = e0 + fel < M;
+      if (face_live) lk = m.link[(e0 + fel) * 4 + ff];
+    }
+  }
+  pdl_wait();  // traces come from k_trace
+  if constexpr (ONE_FACE) {
+    if (t0 < E * NF) {
+      const int fk = (t0 % NF) % N;
       const int64_t e = e0 + fel;
-      face_live = e < M;
       if (face_live) {
-        lk = m.link[e * 4 + ff];
         const bool interior = lk.x >= 0;
         const int kk = lk_rev(lk.y) ? N - 1 - fk : fk;
         const int64_t own = ((e * 4 + ff) * N + fk) * NV;
@@ -1354,6 +1358,18 @@ k_assemble_async(const FrConst C, const FrMesh m, const double* __restrict__ q, 
     for (int i = t0; i < E * 10; i += TH) cp_async16(sG + 2 * i, gsrc + 2 * i, 2 * i < ne * 20);
     cp_async_commit();
   }
+  // static mesh data of this thread's face point before the dependency wait
+  const bool face_thread = t0 < E * NF && t0 / NF < ne;
+  int2 lk = make_int2(-1, 0);
+  double2 nu = make_double2(0.0, 0.0);
+  if (face_thread) {
+    const int fel = t0 / NF, f = (t0 % NF) / N;
+    const int e = (int)e0 + fel;
+    lk = m.link[e * 4 + f];
+    const bool left = lk.x < 0 || lk_left(lk.y);
+    const int gface = left ? e * 20 + 8 + 2 * f : lk.x * 20 + 8 + 2 * lk_face(lk.y);
+    nu = __ldg(reinterpret_cast<const double2*>(m.geom + gface));
+  }
   const Ops op = stage_ops<TH>(C, sm);
   const Phys ph = phys_of(C);
   pdl_wait();  // gradients / fvn from k_fvn, traces and status flags from k_trace
@@ -1378,11 +1394,10 @@ k_assemble_async(const FrConst C, const FrMesh m, const double* __restrict__ q, 
   // face threads: gathers and common face flux, no shared memory needed.
   // 32-bit element-relative offsets (host guarantees M*4*N*NV < 2^31); the
   // L/R operand order of the Roe flux is chosen by address, not by selects.
-  if (t0 < E * NF) {
+  if (face_thread) {
     const int fel = t0 / NF, r = t0 % NF, f = r / N, k = r % N;
-    if (fel < ne) {
+    {
       const int e = (int)e0 + fel;
-      const int2 lk = m.link[e * 4 + f];
       const bool interior = lk.x >= 0;
       const bool left = !interior || lk_left(lk.y);
       const int kk = lk_rev(lk.y) ? N - 1 - k : k;
@@ -1395,8 +1410,6 @@ k_assemble_async(const FrConst C, const FrMesh m, const double* __restrict__ q, 
         ld_face<NV>(fvn + own, Fo);
         ld_face<NV>(fvn + nbi, Fn);
       }
-      const int gface = left ? e * 20 + 8 + 2 * f : lk.x * 20 + 8 + 2 * lk_face(lk.y);
-      const double2 nu = __ldg(reinterpret_cast<const double2*>(m.geom + gface));
       if (!interior) ghost<KIND>(qa, lk_tag(lk.y), nu.x, nu.y, C.qinf, qc);
       num_flux<KIND>(qa, qc, nu.x, nu.y, ph, F);
 #pragma unroll
