@@ -87,6 +87,21 @@ class FrozenState:
     fvn: torch.Tensor   # (M, 4, n, nv)
 
 
+def _mesh_tables(mesh: Mesh):
+    """Packed geometry records and face links depend on the mesh only (not
+    on the degree): computed once per mesh object and reused by every pMG
+    level and every Discretization built on it."""
+    cache = getattr(mesh, "_pmgb_tables", None)
+    if cache is None:
+        links, tags = face_links(mesh)
+        cache = (np.ascontiguousarray(pack_geometry(mesh)), links, tags)
+        try:
+            object.__setattr__(mesh, "_pmgb_tables", cache)
+        except (AttributeError, TypeError):
+            pass  # slotted / foreign mesh objects: no cache
+    return cache
+
+
 class Discretization:
     """FR residual operator on the device for a uniform-degree mesh."""
 
@@ -118,8 +133,8 @@ class Discretization:
         D, eL, eR, lL, lR = face_operators(self.p)
         self._ops = dict(D=np.ascontiguousarray(D), eL=eL.copy(), eR=eR.copy(), lL=lL.copy(),
                          lR=lR.copy(), xg=basis(self.p).points.copy())
-        self._geom = np.ascontiguousarray(pack_geometry(mesh))
-        links, tags = face_links(mesh)
+        geom, links, tags = _mesh_tables(mesh)
+        self._geom = geom
         self._links = np.ascontiguousarray(links)
         self._tags = np.ascontiguousarray(tags)
         self._qinf = np.ascontiguousarray(eqn.free_stream(), dtype=np.float64)
