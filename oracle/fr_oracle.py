@@ -292,6 +292,103 @@ class OracleDisc:
             Fv[..., 3] = np.where(wall, 0.0, Fv[..., 3])
         return self._assemble(e, Q, Fc - Fv, grads).reshape(-1)
 
+    # -- the same residual on all host cores (bench.py's reference arm) -------
+
+    def _gather_nb_chunk(self, s, face_data):
+        return face_data[self.nb[s][..., None], self.fnb[s][..., None], self.kk[s]]
+
+    def _first_bad(self, X):
+        if self.eqn.kind == "advection-diffusion":
+            return -1
+        rho, _, _, p = primitive(X, self.eqn.gamma)
+        bad = ~((rho > 0.0) & (p > 0.0))
+        rows = np.nonzero(bad.reshape(bad.shape[0], -1).any(axis=1))[0]
+        return int(rows[0]) if rows.size else -1
+
+    def residual_mt(self, q, threads=None, chunk=None):
+        """``residual`` evaluated phase by phase over element chunks on a
+        thread pool (NumPy releases the GIL inside its loops).  Every element
+        sees exactly the operations of ``residual`` -- the result is bitwise
+        identical (tests/test_oracle_golden.py) -- and a non-physical state
+        raises the same error (state checks before trace checks, lowest
+        element first)."""
+        import concurrent.futures as cf
+        import os
+        T = int(threads or len(os.sched_getaffinity(0)))
+        n, nv, eqn = self.n, self.nv, self.eqn
+        Q = np.asarray(q, dtype=float).reshape(-1, n, n, nv)
+        M = Q.shape[0]
+        C = int(chunk or max(64, -(-M // (4 * T))))
+        sl = [slice(a, min(a + C, M)) for a in range(0, M, C)]
+        pool = getattr(self, "_pool", None)
+        if pool is None or getattr(self, "_pool_threads", 0) != T:
+            pool = self._pool = cf.ThreadPoolExecutor(T)
+            self._pool_threads = T
+
+        def run(fn):
+            return list(pool.map(fn, sl))
+
+        tr = np.empty((M, 4, n, nv))
+
+        def p1(s):
+            bs = self._first_bad(Q[s])
+            tr[s] = self._traces(Q[s])
+            bt = self._first_bad(tr[s])
+            return (bs + s.start if bs >= 0 else -1, bt + s.start if bt >= 0 else -1)
+
+        flags = run(p1)
+        for k, what in ((0, "state"), (1, "trace")):
+            hits = [f[k] for f in flags if f[k] >= 0]
+            if hits:
+                raise NonPhysicalStateError(min(hits), what)
+        inter = self.interior[..., None, None]
+        left = (self.is_left | ~self.interior)[..., None, None]
+        nrm_nb = self.nrm[self.nb[..., None], self.fnb[..., None]]  # (M, 4, 1, 2)
+        nb_tr = np.empty_like(tr)
+        Fc = np.empty_like(tr)
+
+        def p2(s):
+            gh = self._ghosts(s, tr[s])
+            nbt = np.where(inter[s], self._gather_nb_chunk(s, tr), gh)
+            qa = np.where(left[s], tr[s], nbt)
+            qc = np.where(left[s], nbt, tr[s])
+            shp = tr[s].shape[:-1] + (2,)
+            nrm_own = np.broadcast_to(self.nrm[s][:, :, None, :], shp)
+            nrm = np.where(left[s], nrm_own, np.broadcast_to(nrm_nb[s], shp))
+            F = self._num_flux(qa, qc, nrm)
+            Fc[s] = np.where(left[s], F, -F)
+            nb_tr[s] = nbt
+
+        run(p2)
+        R = np.empty_like(Q)
+        if not eqn.viscous:
+            def pe(s):
+                R[s] = self._assemble(s, Q[s], Fc[s], None)
+            run(pe)
+            return R.reshape(-1)
+        nw = self._grad_vars(Q[:1]).shape[-1]
+        gx = np.empty((M, n, n, nw))
+        gy = np.empty((M, n, n, nw))
+        fvn = np.empty_like(tr)
+
+        def p3(s):
+            What = 0.5 * (self._grad_vars(tr[s]) + self._grad_vars(nb_tr[s]))
+            gxs, gys = self._gradient(s, self._grad_vars(Q[s]), What)
+            gx[s], gy[s] = gxs, gys
+            fvn[s] = self._fvn(s, tr[s], gxs, gys)
+
+        run(p3)
+
+        def p4(s):
+            Fv = np.where(inter[s], 0.5 * (fvn[s] - self._gather_nb_chunk(s, fvn)), fvn[s])
+            if eqn.kind == "navier-stokes":
+                wall = (self.tag[s] == WALL_ADIABATIC)[..., None]
+                Fv[..., 3] = np.where(wall, 0.0, Fv[..., 3])
+            R[s] = self._assemble(s, Q[s], Fc[s] - Fv, (gx[s], gy[s]))
+
+        run(p4)
+        return R.reshape(-1)
+
     # -- frozen neighbour data (spatial.py:700-766) --------------------------
 
     def freeze(self, q) -> Frozen:

@@ -142,3 +142,27 @@ def test_oracle_pmg_solve_matches_reference():
     # the FD blocks amplify rounding; histories agree to ~1e-3
     assert np.allclose(h[:, 1], ref[:, 1], rtol=2e-3, atol=1e-12)
     assert rel(q, G["c3/q"]) <= 1e-9
+
+
+@pytest.mark.parametrize("mesh", list(MESHES))
+@pytest.mark.parametrize("kind", list(KINDS))
+def test_oracle_threaded_residual_is_bitwise_identical(mesh, kind):
+    # bench.py's reference arm runs residual_mt on all host cores: it must be
+    # the same computation as residual, chunking included
+    d = OracleDisc(MESHES[mesh](), 3, EquationSpec(**KINDS[kind]))
+    q = G[f"res/{mesh}/{kind}/p3/q"]
+    assert np.array_equal(d.residual_mt(q, threads=3, chunk=5), d.residual(q))
+
+
+def test_oracle_threaded_residual_raises_like_residual():
+    from paper_2202_09733_b200.equation import NonPhysicalStateError
+    d = OracleDisc(MESHES["box4p"](), 2, EquationSpec(**KINDS["ns"]))
+    q = G["res/box4p/ns/p2/q"].copy().reshape(16, 3, 3, 4)
+    q[11, 1, 1, 0] = -1.0   # negative density at an interior point of element 11
+    q[6, 0, 0, 3] = 0.0     # negative pressure at a corner point of element 6
+    errs = []
+    for f in (d.residual, lambda x: d.residual_mt(x, threads=4, chunk=3)):
+        with pytest.raises(NonPhysicalStateError) as ei:
+            f(q.reshape(-1))
+        errs.append(str(ei.value))
+    assert errs[0] == errs[1]
