@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--no-step", action="store_true", help="skip the JFNK-pMG time-step timings")
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU-oracle baseline sample")
+    ap.add_argument("--no-configs", action="store_true", help="skip the configs 3-5 measurements")
     return ap.parse_args()
 
 
@@ -281,6 +282,9 @@ def run_ours(args):
     step = {}
     if not args.no_step and rank == 0:
         step = time_steps(torch, case, args)
+    others = {}
+    if not args.no_configs and rank == 0 and args.config == 2:
+        others = time_other_configs(torch, args)
 
     if rank != 0:
         pdist.barrier()
@@ -316,6 +320,7 @@ def run_ours(args):
         "gpu_launches": int(launches_r),
         "clocks": clk.summary(),
         "step_time": step,
+        "configs": others,
     }
     # CPU baseline: the oracle on this host, bounded sample
     try:
@@ -337,6 +342,74 @@ def run_ours(args):
     print(json.dumps(line), flush=True)
     pdist.barrier()
     return 0
+
+
+def time_other_configs(torch, args):
+    """BASELINE configs 3-5: R and Jv rates (rotating
+    buffers, >= 4x L2), config 3's nonlinear pMG solve per outer iteration
+    (one V-cycle each, levels 4-3-2-1-0), config 4's ROW4 step (walls,
+    GMRES(60), pMG 3-2), config 5 at capacity (151M DoF, R/Jv only:
+    its p=5 EJ blocks would need 174 GB)."""
+    from paper_2202_09733_b200 import _lib, cases, newton_krylov as nk, pmg
+    from paper_2202_09733_b200 import time_integration as ti
+    from paper_2202_09733_b200.harness import ImplicitDriver
+    from paper_2202_09733_b200.spatial import Discretization
+    out = {}
+    for k in (3, 4, 5):
+        rec = {}
+        try:
+            c = cases.config(k)
+            d = Discretization(c.mesh, c.p, c.eqn)
+            n = d.n_dofs
+            nb = max(2, int(np.ceil(4 * 126e6 / (32.0 * n))))
+            q0 = torch.as_tensor(c.q0, device="cuda")
+            qs = [q0.clone() for _ in range(nb)]
+            Rs = [torch.empty_like(q0) for _ in range(nb)]
+            X = torch.randn(n, dtype=torch.float64, device="cuda", generator=torch.Generator("cuda").manual_seed(7))
+            R0 = d.residual(q0)
+            reps = 10 if n > 1e8 else 40
+            r_step = lambda i: d.eval(qs[i % nb], _lib.EPI_R, Rs[i % nb])
+            jv_step = lambda i: d.eval(qs[i % nb], _lib.EPI_JV, Rs[i % nb], X=X, eps=1e-6, s=3.7, R0=R0)
+            for i in range(3):
+                r_step(i)
+                jv_step(i)
+            t_r = event_time(torch, r_step, reps)
+            t_jv = event_time(torch, jv_step, reps)
+            rec.update(n_dofs=n, p=c.p, r_gdofs=n * reps / t_r / 1e9, r_ms=t_r / reps * 1e3,
+                       jv_gdofs=n * reps / t_jv / 1e9, rotating_pairs=nb)
+            del qs, Rs
+            if k == 3:
+                hier = pmg.PHierarchy.parse(c.levels, "2")
+                ctx = pmg.PmgContext(d, pmg.PmgPrecondConfig(hier, smoother_shift=c.extra["smoother_shift"]))
+                pmg.pmg_solve(ctx, q0, nk.PtcConfig(dtau_init=0.1, max_iters=1, rtol=1e-14))
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                _, stt = pmg.pmg_solve(ctx, q0, nk.PtcConfig(dtau_init=0.1, max_iters=3, rtol=1e-14))
+                torch.cuda.synchronize()
+                el = time.perf_counter() - t0
+                rec.update(pmg_solve={"levels": c.levels, "outer_iters": stt["iters"], "s": el,
+                                      "ms_per_outer_iter_incl_prepare": el / max(1, stt["iters"]) * 1e3,
+                                      "rel_history": [h[1] for h in stt["history"]]})
+                del ctx
+            if k == 4:
+                cfg = {"case.precond": "pmg", "pmg.levels": c.levels, "pmg.smooth": "2",
+                       "pmg.smoother_shift": c.extra["smoother_shift"], "gmres.kdim": c.kdim, "gmres.rtol": 1e-3}
+                sch = ti.get_scheme("row4")
+                ImplicitDriver(d, cfg).step(q0, c.dt, sch)
+                drv = ImplicitDriver(d, cfg)
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                _, info = drv.step(q0, c.dt, sch)
+                torch.cuda.synchronize()
+                rec.update(row4_step={"s": time.perf_counter() - t0, "dt": c.dt,
+                                      "gmres_iters": [i["iters"] for i in info]})
+                del drv
+            del d, q0, X, R0
+        except Exception as exc:  # pragma: no cover
+            rec["error"] = str(exc)[:200]
+        torch.cuda.empty_cache()
+        out[f"config{k}"] = rec
+    return out
 
 
 def time_steps(torch, case2, args):
