@@ -99,10 +99,8 @@ PMGB_API int pmgb_disc_create(const pmgb_disc_desc* desc, pmgb_disc** out) {
   if (!err) err = cudaMalloc(&d.qtr, face_bytes);
   if (!err) err = cudaMalloc(&d.fvn, face_bytes);
   if (!err) err = cudaMalloc(&d.qp, sizeof(double) * (size_t)d.n_dofs);
-  // gradients are stored per CTA block of EPB <= 32 elements ([M/E][2NW][E*NP]);
-  // the grid covers at most M + EPB - 1 elements, so pad by 32
-  const size_t m_pad = (size_t)d.M + 32;
-  if (!err) err = cudaMalloc(&d.grad, sizeof(double) * m_pad * n * n * (d.nv == 4 ? 6 : 2));
+  // gradients: per CTA block, k_fvn's padded planes (fr_grad_scratch_doubles)
+  if (!err) err = cudaMalloc(&d.grad, sizeof(double) * fr_grad_scratch_doubles(d.p, d.kind, d.M));
   if (!err) err = cudaMemcpy(d.geom, desc->geom, sizeof(double) * 20 * (size_t)d.M, cudaMemcpyHostToDevice);
   if (!err) err = cudaMemcpy(d.link, lk.data(), sizeof(int2) * 4 * (size_t)d.M, cudaMemcpyHostToDevice);
   if (err) {

@@ -58,19 +58,39 @@ struct SL {
   static constexpr int TR = GR + 2 * NW * NPT;    // [NV] face planes    own traces (local pipeline)
   static constexpr int R0 = TR + NV * NFT;        // [NP*NV]             unperturbed local residual
   static constexpr int END_LOCAL = R0 + NP * NV;
-  // k_fvn: face planes padded to an element stride of 4N+1 (bank spread),
-  // then the gradient planes, 16-byte aligned for the block copy to global
+  // Padded point planes of k_fvn / k_assemble_async (bank spread): point
+  // (el, a, b) of a plane at el*ES + a*RS + b, planes PS apart.  The strides
+  // minimise modelled shared wavefronts over the point-, row- and
+  // column-thread patterns of both kernels (even N needs them most).
+  static constexpr int RS = N;
+  static constexpr int ES_T = P == 3 ? 17 : N * RS;
+  static constexpr int ES = ES_T > N * RS ? ES_T : N * RS;
+  // p=4 and p=5 measured fastest unpadded (the model's gains there are
+  // smaller than the extra index arithmetic and spills they cost)
+  static constexpr int PS_T = P == 1 ? 129 : P == 2 ? 132 : P == 3 ? 139 : 0;
+  static constexpr int PS = PS_T > E * ES ? PS_T : E * ES;
+  __host__ __device__ static constexpr int pix(int el, int a, int b) { return el * ES + a * RS + b; }
+  static constexpr bool PADDED = !(RS == N && ES == NP);
+  __host__ __device__ static constexpr int pix(int t) { return PADDED ? pix(t / NP, (t % NP) / N, t % N) : t; }
+  // k_fvn: padded point planes Q, W; face planes padded to an element
+  // stride of 4N+1; the gradient planes 16-byte aligned for the block copy
   static constexpr int NFS = 4 * N + 1, NFTP = E * NFS;
-  static constexpr int F_WH = W + NW * NPT;       // [NW] padded face planes  BR1 common value
+  static constexpr int F_Q = G + E * 20;          // [NV] padded point planes
+  static constexpr int F_W = F_Q + NV * PS;       // [NW] padded point planes   viscous variables
+  static constexpr int F_WH = F_W + NW * PS;      // [NW] padded face planes  BR1 common value
   static constexpr int F_GF = F_WH + NW * NFTP;   // [2NW] padded face planes gradient traces
-  static constexpr int GR_FVN = (F_GF + 2 * NW * NFTP + 1) & ~1;  // [2NW] point planes
+  static constexpr int GR_FVN = (F_GF + 2 * NW * NFTP + 1) & ~1;  // [2NW] padded point planes
+  // k_assemble_async: AoS q (cp.async), face fluxes, padded flux planes
+  static constexpr int P_FT = Q + NV * NPT + NV * NFT;  // after A_FC (AoS q, face fluxes)
+  static constexpr int P_GT = P_FT + NV * PS;
+  static constexpr size_t BYTES_ASYNC = sizeof(double) * (P_GT + NV * PS);
   // compact layout of k_assemble (gradients come from k_fvn)
   static constexpr int A_FC = Q + NV * NPT;
   static constexpr int A_FT = A_FC + NV * NFT;
   static constexpr int A_GT = A_FT + NV * NPT;
   static constexpr int A_CF = A_GT + NV * NPT;
   static constexpr size_t BYTES_TRACE = sizeof(double) * (Q + NV * NPT);
-  static constexpr size_t BYTES_FVN = sizeof(double) * (GR_FVN + 2 * NW * NPT);
+  static constexpr size_t BYTES_FVN = sizeof(double) * (GR_FVN + 2 * NW * PS);
   static constexpr size_t BYTES_ASM = sizeof(double) * (A_CF + NV * NFT);
   static constexpr size_t BYTES_LOCAL = sizeof(double) * END_LOCAL;
   static_assert(2 * NW >= NV || true, "CF alias");
@@ -323,6 +343,35 @@ __device__ __forceinline__ void load_points(const double* __restrict__ src, int6
     for (int i = threadIdx.x; i < NPT * NV; i += BC<P>::THREADS) {
       const int v = i % NV, g = i / NV;
       sQ[v * NPT + g] = (i < lim) ? __ldg(base + i) : 1.0;
+    }
+  }
+}
+
+// element-major AoS global -> padded SoA point planes (SL::pix layout)
+template <int P, int NV, class L>
+__device__ __forceinline__ void load_points_pad(const double* __restrict__ src, int64_t e0, int64_t M, double* sQ) {
+  constexpr int NP = BC<P>::NP, E = BC<P>::EPB, NPT = E * NP;
+  if constexpr (NV == 4) {
+    const int64_t lim = (M - e0) * NP;
+    const double2* base = reinterpret_cast<const double2*>(src + e0 * NP * 4);
+    for (int g = threadIdx.x; g < NPT; g += BC<P>::THREADS) {
+      double2 a = make_double2(1.0, 1.0), b = make_double2(1.0, 1.0);
+      if (g < lim) {
+        a = __ldg(base + 2 * g);
+        b = __ldg(base + 2 * g + 1);
+      }
+      const int d = L::pix(g);
+      sQ[d] = a.x;
+      sQ[L::PS + d] = a.y;
+      sQ[2 * L::PS + d] = b.x;
+      sQ[3 * L::PS + d] = b.y;
+    }
+  } else {
+    const int64_t lim = (M - e0) * NP * NV;
+    const double* base = src + e0 * NP * NV;
+    for (int i = threadIdx.x; i < NPT * NV; i += BC<P>::THREADS) {
+      const int v = i % NV, g = i / NV;
+      sQ[v * L::PS + L::pix(g)] = (i < lim) ? __ldg(base + i) : 1.0;
     }
   }
 }
@@ -779,11 +828,12 @@ k_fvn(const FrConst C, const FrMesh m, const double* __restrict__ q, const doubl
   using L = SL<P, KIND>;
   constexpr int N = BC<P>::N, NP = BC<P>::NP, NF = BC<P>::NF, E = BC<P>::EPB;
   constexpr int NV = KT<KIND>::NV, NW = KT<KIND>::NW, NPT = L::NPT, NFS = L::NFS, NFTP = L::NFTP;
+  constexpr int PS = L::PS, ES = L::ES, RS = L::RS;
   pdl_trigger();
   const Ops op = stage_ops<BC<P>::THREADS>(C, sm);
-  double* sQ = sm + L::Q;
+  double* sQ = sm + L::F_Q;
   double* sG = sm + L::G;
-  double* sW = sm + L::W;
+  double* sW = sm + L::F_W;
   double* sWH = sm + L::F_WH;
   double* sGR = sm + L::GR_FVN;
   const int64_t e0 = (int64_t)blockIdx.x * E;
@@ -793,7 +843,7 @@ k_fvn(const FrConst C, const FrMesh m, const double* __restrict__ q, const doubl
   // (own + neighbour) into registers, all before the first barrier.
   constexpr bool ONE_FACE = (E * NF <= BC<P>::THREADS);
   const int t0 = threadIdx.x;
-  load_points<P, NV>(q, e0, M, sQ);
+  load_points_pad<P, NV, L>(q, e0, M, sQ);
   load_geom<P>(m.geom, e0, M, sG);
   double tr[NV], nb[NV];
   int2 lk = make_int2(-1, 0);
@@ -826,10 +876,12 @@ k_fvn(const FrConst C, const FrMesh m, const double* __restrict__ q, const doubl
   __syncthreads();
   if (t0 < NPT) {
     double qq[NV], w[NW];
-    gather_point<NV, NPT>(sQ, t0, qq);
+    const int px0 = L::pix(t0);
+#pragma unroll
+    for (int v = 0; v < NV; ++v) qq[v] = sQ[v * PS + px0];
     grad_vars<KIND>(qq, ph.gamma, w);
 #pragma unroll
-    for (int c = 0; c < NW; ++c) sW[c * NPT + t0] = w[c];
+    for (int c = 0; c < NW; ++c) sW[c * PS + px0] = w[c];
   }
   auto face_avg = [&](int t, int el, int f, int2 lkk, double* tr_, double* nb_) {
     if (lkk.x < 0) {
@@ -867,15 +919,15 @@ k_fvn(const FrConst C, const FrMesh m, const double* __restrict__ q, const doubl
   // c_f = +-js_f n_f What_f - (trace of the metric-weighted W on face f)  (spatial.py:594-603)
   constexpr int TH = BC<P>::THREADS;
   constexpr int NLG = E * N * NW;
-  double* sPX = sGR;             // [NW][NPT] x partials, then gx
-  double* sPY = sGR + NW * NPT;  // [NW][NPT] y partials, then gy
+  double* sPX = sGR;            // [NW][PS] x partials, then gx
+  double* sPY = sGR + NW * PS;  // [NW][PS] y partials, then gy
   // pass 1, rows: thread t = (c, el, a) with a fastest, so the row it reads
   // and writes starts at N * t (stride N odd: no bank conflicts)
   for (int t = t0; t < NLG; t += TH) {
     const int c = t / (E * N), el = (t / N) % E, a = t % N;
     const double* gq = sG + el * 20;
     const Metric mt = metric(gq);
-    const double* Wr = sW + c * NPT + el * NP + a * N;
+    const double* Wr = sW + c * PS + el * ES + a * RS;
     double wx[N], wy[N];
 #pragma unroll
     for (int i = 0; i < N; ++i) {
@@ -897,8 +949,8 @@ k_fvn(const FrConst C, const FrMesh m, const double* __restrict__ q, const doubl
     const double cy1 = gq[17] * (gq[11] * wh1) - ty1;
     const double cx3 = -gq[19] * (gq[14] * wh3) - tx3;
     const double cy3 = -gq[19] * (gq[15] * wh3) - ty3;
-    double* px = sPX + c * NPT + el * NP + a * N;
-    double* py = sPY + c * NPT + el * NP + a * N;
+    double* px = sPX + c * PS + el * ES + a * RS;
+    double* py = sPY + c * PS + el * ES + a * RS;
 #pragma unroll
     for (int b = 0; b < N; ++b) {
       double sx = 0.0, sy = 0.0;
@@ -920,11 +972,11 @@ k_fvn(const FrConst C, const FrMesh m, const double* __restrict__ q, const doubl
     const int b = t / (E * NW), el = (t / NW) % E, c = t % NW;
     const double* gq = sG + el * 20;
     const Metric mt = metric(gq);
-    const double* Wc = sW + c * NPT + el * NP + b;
+    const double* Wc = sW + c * PS + el * ES + b;
     double vx[N], vy[N];
 #pragma unroll
     for (int i = 0; i < N; ++i) {
-      const double y = Wc[i * N], eta = C.xg[i];
+      const double y = Wc[i * RS], eta = C.xg[i];
       vx[i] = -mt.J10(eta) * y;
       vy[i] = mt.J00(eta) * y;
     }
@@ -955,9 +1007,8 @@ k_fvn(const FrConst C, const FrMesh m, const double* __restrict__ q, const doubl
       }
       const double xa = C.xg[a];
       const double idet = rcp(mt.J00(xa) * j11b - j01b * mt.J10(xa));
-      const int pt = a * N + b;
-      double* px = sPX + c * NPT + el * NP + pt;
-      double* py = sPY + c * NPT + el * NP + pt;
+      double* px = sPX + c * PS + el * ES + a * RS + b;
+      double* py = sPY + c * PS + el * ES + a * RS + b;
       const double gxv = (((*px) + dx) + C.lR[a] * cx2 - C.lL[a] * cx0) * idet;
       const double gyv = (((*py) + dy) + C.lR[a] * cy2 - C.lL[a] * cy0) * idet;
       *px = gxv;
@@ -977,8 +1028,8 @@ k_fvn(const FrConst C, const FrMesh m, const double* __restrict__ q, const doubl
   // pass 3, rows of the final gradients: traces on faces 1 (eR) and 3 (eL)
   for (int t = t0; t < NLG; t += TH) {
     const int c = t / (E * N), el = (t / N) % E, a = t % N;
-    const double* gxr = sPX + c * NPT + el * NP + a * N;
-    const double* gyr = sPY + c * NPT + el * NP + a * N;
+    const double* gxr = sPX + c * PS + el * ES + a * RS;
+    const double* gyr = sPY + c * PS + el * ES + a * RS;
     double fx1 = 0.0, fy1 = 0.0, fx3 = 0.0, fy3 = 0.0;
 #pragma unroll
     for (int i = 0; i < N; ++i) {
@@ -994,12 +1045,12 @@ k_fvn(const FrConst C, const FrMesh m, const double* __restrict__ q, const doubl
     sGF[c * NFTP + s3] = fx3;
     sGF[(NW + c) * NFTP + s3] = fy3;
   }
-  // point gradients to global: the CTA's 2NW planes are one contiguous
-  // block of the [M/E][2NW][E*NP] scratch layout (allocation rounded up)
+  // point gradients to global: the CTA's 2NW padded planes are one
+  // contiguous block of the [grid][2NW][PS] scratch (fr_grad_scratch_doubles)
   if (grad != nullptr) {
-    constexpr int NB2 = NW * NPT;  // double2 per block
+    constexpr int NB2 = NW * PS;  // double2 per block
     const double2* src = reinterpret_cast<const double2*>(sGR);
-    double2* dst = reinterpret_cast<double2*>(grad + (int64_t)blockIdx.x * (2 * NW * NPT));
+    double2* dst = reinterpret_cast<double2*>(grad + (int64_t)blockIdx.x * (2 * NW * PS));
     for (int i = t0; i < NB2; i += TH) dst[i] = src[i];
   }
   __syncthreads();
@@ -1200,11 +1251,12 @@ k_assemble(const FrConst C, const FrMesh m, const double* __restrict__ q, const 
     if (t0 < NPT) {
       const int el = t0 / NP, pt = t0 % NP;
       if (e0 + el < M) {
-        const double* gs = grad + (int64_t)blockIdx.x * (2 * NW * NPT) + t0;
+        // gradients in k_fvn's padded block layout
+        const double* gs = grad + (int64_t)blockIdx.x * (2 * NW * L::PS) + L::pix(t0);
 #pragma unroll
         for (int c = 0; c < NW; ++c) {
-          gx[c] = __ldg(gs + c * NPT);
-          gy[c] = __ldg(gs + (NW + c) * NPT);
+          gx[c] = __ldg(gs + c * L::PS);
+          gy[c] = __ldg(gs + (NW + c) * L::PS);
         }
       } else {
 #pragma unroll
@@ -1339,14 +1391,14 @@ k_assemble_async(const FrConst C, const FrMesh m, const double* __restrict__ q, 
   constexpr int TH = BC<P>::THREADS;
   constexpr int N = BC<P>::N, NP = BC<P>::NP, NF = BC<P>::NF, E = BC<P>::EPB;
   constexpr int NV = KT<KIND>::NV, NW = KT<KIND>::NW, NPT = L::NPT, NFT = L::NFT;
+  constexpr int PS = L::PS, ES = L::ES, RS = L::RS;
   constexpr bool VISC = KT<KIND>::VISC;
   static_assert(NV == 4 && E * NF <= TH, "async assemble: flow kinds, one face point per thread");
   double* sQA = sm + L::Q;  // AoS [E][NP][NV]
   double* sG = sm + L::G;
   double* sFC = sm + L::A_FC;
-  double* sFT = sm + L::A_FT;
-  double* sGT = sm + L::A_GT;
-  double* sCF = sm + L::A_CF;
+  double* sFT = sm + L::P_FT;  // [NV] padded point planes
+  double* sGT = sm + L::P_GT;
   const int64_t e0 = (int64_t)blockIdx.x * E;
   const int64_t M = m.M;
   const int ne = (int)((M - e0) < E ? (M - e0) : E);
@@ -1382,11 +1434,11 @@ k_assemble_async(const FrConst C, const FrMesh m, const double* __restrict__ q, 
     if (t0 < NPT) {
       const int el = t0 / NP, pt = t0 % NP;
       if (el < ne) {
-        const double* gs = grad + (int64_t)blockIdx.x * (2 * NW * NPT) + t0;
+        const double* gs = grad + (int64_t)blockIdx.x * (2 * NW * PS) + L::pix(t0);
 #pragma unroll
         for (int c = 0; c < NW; ++c) {
-          gx[c] = __ldg(gs + c * NPT);
-          gy[c] = __ldg(gs + (NW + c) * NPT);
+          gx[c] = __ldg(gs + c * PS);
+          gy[c] = __ldg(gs + (NW + c) * PS);
         }
       }
     }
@@ -1436,10 +1488,11 @@ k_assemble_async(const FrConst C, const FrMesh m, const double* __restrict__ q, 
     const double qq[NV] = {q01.x, q01.y, q23.x, q23.y};
     double Ft[NV], Gt[NV];
     point_fluxes<P, KIND>(qq, gx, gy, ph, mt, op.xg[a], op.xg[b], Ft, Gt);
+    const int px0 = L::pix(t0);
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
-      sFT[v * NPT + t0] = Ft[v];
-      sGT[v * NPT + t0] = Gt[v];
+      sFT[v * PS + px0] = Ft[v];
+      sGT[v * PS + px0] = Gt[v];
     }
   }
   __syncthreads();
@@ -1452,7 +1505,7 @@ k_assemble_async(const FrConst C, const FrMesh m, const double* __restrict__ q, 
   constexpr int NL = E * N * NV;
   if (t0 < NL) {
     const int el = t0 / (N * NV), r = t0 % (N * NV), a = r / NV, v = r % NV;
-    double* rowp = sFT + v * NPT + el * NP + a * N;
+    double* rowp = sFT + v * PS + el * ES + a * RS;
     double x[N];
 #pragma unroll
     for (int i = 0; i < N; ++i) x[i] = rowp[i];
@@ -1477,10 +1530,10 @@ k_assemble_async(const FrConst C, const FrMesh m, const double* __restrict__ q, 
   if (t0 < NL) {
     const int el = t0 / (N * NV), r = t0 % (N * NV), b = r / NV, v = r % NV;
     if (el < ne) {
-      const double* colp = sGT + v * NPT + el * NP + b;
+      const double* colp = sGT + v * PS + el * ES + b;
       double y[N];
 #pragma unroll
-      for (int i = 0; i < N; ++i) y[i] = colp[i * N];
+      for (int i = 0; i < N; ++i) y[i] = colp[i * RS];
       double t2 = 0.0, t0f = 0.0;
 #pragma unroll
       for (int i = 0; i < N; ++i) {
@@ -1504,7 +1557,7 @@ k_assemble_async(const FrConst C, const FrMesh m, const double* __restrict__ q, 
         for (int i = 0; i < N; ++i) ta += C.D[a * N + i] * y[i];
         const double xa = C.xg[a];
         const double idet = rcp(mt.J00(xa) * j11 - j01 * mt.J10(xa));
-        double d = sFT[v * NPT + el * NP + a * N + b] + ta;
+        double d = sFT[v * PS + el * ES + a * RS + b] + ta;
         d = (d + C.lR[a] * c2) - C.lL[a] * c0;
         const double R = -(d * idet);
         const int pt = a * N + b;
@@ -1780,7 +1833,7 @@ static int run_residual(const DiscDev& d, const double* q, const double* X, doub
     cudaFuncSetAttribute(k_fvn<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES_FVN);
     cudaFuncSetAttribute(k_assemble<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES_ASM);
     if constexpr (KT<KIND>::NV == 4 && E * BC<P>::NF <= TH)
-      cudaFuncSetAttribute(k_assemble_async<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES_ASM);
+      cudaFuncSetAttribute(k_assemble_async<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES_ASYNC);
     attr = true;
   }
   int* bad = nullptr;
@@ -1799,7 +1852,7 @@ static int run_residual(const DiscDev& d, const double* q, const double* X, doub
   if (KT<KIND>::VISC) launch_pdl(k_fvn<P, KIND>, grid, TH, L::BYTES_FVN, st, d.C, d.mesh, qq, (const double*)d.qtr,
                                  d.fvn, d.grad);
   if constexpr (KT<KIND>::NV == 4 && E * BC<P>::NF <= TH)
-    launch_pdl(k_assemble_async<P, KIND>, grid, TH, L::BYTES_ASM, st, d.C, d.mesh, qq, (const double*)d.qtr,
+    launch_pdl(k_assemble_async<P, KIND>, grid, TH, L::BYTES_ASYNC, st, d.C, d.mesh, qq, (const double*)d.qtr,
                (const double*)d.fvn, (const double*)d.grad, epi, out, bad, stp);
   else
     k_assemble<P, KIND><<<grid, TH, L::BYTES_ASM, st>>>(d.C, d.mesh, qq, d.qtr, d.fvn, d.grad, epi, out, bad, stp);
@@ -1886,6 +1939,25 @@ static int run_blocks(const DiscDev& d, const double* q, const double* qtr, cons
     case K_ADVD * 8 + 5: return FN<5, K_ADVD>(__VA_ARGS__);                 \
   }                                                                         \
   return -1000;
+
+template <int P, int KIND>
+static size_t grad_scratch_doubles_t(int64_t M) {
+  using L = SL<P, KIND>;
+  constexpr int E = BC<P>::EPB;
+  return (size_t)((M + E - 1) / E) * 2 * KT<KIND>::NW * L::PS;
+}
+
+size_t fr_grad_scratch_doubles(int p, int kind, int64_t M) {
+  switch (kind * 8 + p) {
+#define PMGB_GS(K, PP) case K * 8 + PP: return grad_scratch_doubles_t<PP, K>(M);
+    PMGB_GS(K_EULER, 0) PMGB_GS(K_EULER, 1) PMGB_GS(K_EULER, 2) PMGB_GS(K_EULER, 3) PMGB_GS(K_EULER, 4) PMGB_GS(K_EULER, 5)
+    PMGB_GS(K_NS, 0) PMGB_GS(K_NS, 1) PMGB_GS(K_NS, 2) PMGB_GS(K_NS, 3) PMGB_GS(K_NS, 4) PMGB_GS(K_NS, 5)
+    PMGB_GS(K_ADV, 0) PMGB_GS(K_ADV, 1) PMGB_GS(K_ADV, 2) PMGB_GS(K_ADV, 3) PMGB_GS(K_ADV, 4) PMGB_GS(K_ADV, 5)
+    PMGB_GS(K_ADVD, 0) PMGB_GS(K_ADVD, 1) PMGB_GS(K_ADVD, 2) PMGB_GS(K_ADVD, 3) PMGB_GS(K_ADVD, 4) PMGB_GS(K_ADVD, 5)
+#undef PMGB_GS
+  }
+  return 0;
+}
 
 int launch_residual(const DiscDev& d, const double* q, const double* X, double eps, const Epi& epi,
                     double* out, cudaStream_t st) {

@@ -101,7 +101,7 @@ struct DiscDev {
   int2* link;
   double* qtr;   // scratch traces (M,4,n,nv)
   double* fvn;   // scratch viscous flux (M,4,n,nv)
-  double* grad;  // scratch BR1 gradients, per CTA block: [M/EPB][2*nw][EPB*n*n]
+  double* grad;  // scratch BR1 gradients, per CTA block in k_fvn's padded planes: [grid][2*nw][PS]
   double* qp;    // scratch perturbed state
   int nv;
   int64_t n_dofs;
@@ -109,6 +109,7 @@ struct DiscDev {
 
 int launch_residual(const DiscDev& d, const double* q, const double* X, double eps,
                     const Epi& epi, double* out, cudaStream_t st);
+size_t fr_grad_scratch_doubles(int p, int kind, int64_t M);
 int launch_freeze(const DiscDev& d, const double* q, double* qtr, double* fvn, cudaStream_t st);
 int launch_local_residual(const DiscDev& d, const int64_t* elems, int64_t B, const double* Q,
                           const double* qtr, const double* fvn, double* out, cudaStream_t st);
