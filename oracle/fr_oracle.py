@@ -17,7 +17,7 @@ Reference citations (``/root/reference/pkg/src/pmgflow/spatial.py``):
   _divergence 407-430, _transformed 432-437, _check_physical 439-446,
   _grad_vars 448-454, _one_sided_fvn 456-464, residual 501-570,
   _br1_gradient 594-603, _assemble 605-629, freeze 700-766,
-  element_residual 768-853.
+  element_residual 768-853, neighbor_face_record 855-903.
 """
 
 from __future__ import annotations
@@ -406,14 +406,26 @@ class OracleDisc:
             fvn_nb = -self._gather_nb(fvn)
         return Frozen(q_nb, fvn_nb)
 
-    def element_residual(self, e: int, Q, frozen: Frozen):
+    def element_residual(self, e: int, Q, frozen: Frozen, override=None):
         """Element-local residual with frozen neighbours, own-side fluxes
-        throughout (spatial.py:768-853).  Q: (..., n, n, nv)."""
+        throughout (spatial.py:768-853).  Q: (..., n, n, nv).  ``override``
+        = (f, q_rec, fvn_rec) replaces face f's frozen record by batched
+        records from ``neighbor_record`` (the reference's face_override,
+        spatial.py:787-790)."""
         Q = np.asarray(Q, dtype=float)
         tr = self._traces(Q)
         inter = self.interior[e][:, None, None]
+        q_nb = frozen.q_nb[e]
+        fvn_nb = frozen.fvn_nb[e] if frozen.fvn_nb is not None else None
+        if override is not None:
+            f_ov, q_rec, fvn_rec = override
+            q_nb = np.broadcast_to(q_nb, tr.shape).copy()
+            q_nb[..., f_ov, :, :] = q_rec
+            if fvn_nb is not None:
+                fvn_nb = np.broadcast_to(fvn_nb, tr.shape).copy()
+                fvn_nb[..., f_ov, :, :] = fvn_rec
         gh = self._ghosts(e, tr)
-        q_out = np.where(inter, frozen.q_nb[e], gh)
+        q_out = np.where(inter, q_nb, gh)
         nrm = np.broadcast_to(self.nrm[e][:, None, :], tr.shape[:-1] + (2,))
         Fc = self._num_flux(tr, q_out, nrm)
         grads = None
@@ -421,12 +433,37 @@ class OracleDisc:
             What = 0.5 * (self._grad_vars(tr) + self._grad_vars(q_out))
             grads = self._gradient(e, self._grad_vars(Q), What)
             fvn = self._fvn(e, tr, *grads)
-            Fv = np.where(inter, 0.5 * (fvn + frozen.fvn_nb[e]), fvn)
+            Fv = np.where(inter, 0.5 * (fvn + fvn_nb), fvn)
             if self.eqn.kind == "navier-stokes":
                 wall = (self.tag[e] == WALL_ADIABATIC)[:, None]
                 Fv[..., 3] = np.where(wall, 0.0, Fv[..., 3])
             Fc = Fc - Fv
         return self._assemble(e, Q, Fc, grads)
+
+    def neighbor_record(self, e: int, f: int, Q_nb, frozen: Frozen):
+        """Face record of e's face f recomputed from a (batched) neighbour
+        state Q_nb with the neighbour's own other faces frozen
+        (spatial.py:855-903): the neighbour's trace and, when viscous, its
+        one-sided viscous flux, aligned to e's face points, in the Frozen
+        sign convention (fvn = -neighbour flux)."""
+        nb, fnb, rev = int(self.nb[e, f]), int(self.fnb[e, f]), bool(self.link[e, f, 2])
+        Q_nb = np.asarray(Q_nb, dtype=float)
+        tr = self._traces(Q_nb)
+        q_rec = tr[..., fnb, :, :]
+        if rev:
+            q_rec = q_rec[..., ::-1, :]
+        fvn_rec = None
+        if self.eqn.viscous:
+            inter = self.interior[nb][:, None, None]
+            gh = self._ghosts(nb, tr)
+            q_out = np.where(inter, frozen.q_nb[nb], gh)
+            What = 0.5 * (self._grad_vars(tr) + self._grad_vars(q_out))
+            gx, gy = self._gradient(nb, self._grad_vars(Q_nb), What)
+            fv = self._fvn(nb, tr, gx, gy)[..., fnb, :, :]
+            if rev:
+                fv = fv[..., ::-1, :]
+            fvn_rec = -fv
+        return q_rec, fvn_rec
 
     # -- field helpers -------------------------------------------------------
 

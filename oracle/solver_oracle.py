@@ -144,12 +144,136 @@ def assemble_blocks(disc: OracleDisc, q, shift, eps=FD_EPS):
 
 
 # ---------------------------------------------------------------------------
+# block-sparse Jacobian and block ILU0 (newton_krylov.py:215-371)
+
+def coupling_block(disc: OracleDisc, e, f, q, frozen, eps=FD_EPS):
+    """-dR_e/dq_nb across face f of element e, by batched differencing of
+    the neighbour state (newton_krylov.py:254-278)."""
+    sz = int(disc.offsets[1])
+    n, nv = disc.n, disc.nv
+    nb = int(disc.nb[e, f])
+    batch = np.repeat(q[nb * sz:(nb + 1) * sz][None, :], sz + 1, axis=0)
+    batch[np.arange(1, sz + 1), np.arange(sz)] += eps
+    q_rec, fvn_rec = disc.neighbor_record(e, f, batch.reshape(sz + 1, n, n, nv), frozen)
+    Qe = np.broadcast_to(q[e * sz:(e + 1) * sz].reshape(n, n, nv), (sz + 1, n, n, nv))
+    R = disc.element_residual(e, Qe, frozen, override=(f, q_rec, fvn_rec)).reshape(sz + 1, sz)
+    return -(R[1:] - R[0]).T / eps
+
+
+class SparseBlocks:
+    """Block-CSR over element adjacency, columns sorted per row
+    (SparseBlockMatrix, newton_krylov.py:218-251)."""
+
+    def __init__(self, indptr, indices, blocks, sz):
+        self.indptr, self.indices, self.blocks, self.sz = indptr, indices, blocks, sz
+        self.n = len(indptr) - 1
+
+    def entry(self, i, j):
+        for k in range(self.indptr[i], self.indptr[i + 1]):
+            if self.indices[k] == j:
+                return k
+        return -1
+
+    def matvec(self, X):
+        sz = self.sz
+        out = np.zeros_like(X)
+        for i in range(self.n):
+            acc = np.zeros(sz)
+            for k in range(self.indptr[i], self.indptr[i + 1]):
+                j = int(self.indices[k])
+                acc += self.blocks[k] @ X[j * sz:(j + 1) * sz]
+            out[i * sz:(i + 1) * sz] = acc
+        return out
+
+
+def sparse_pattern(disc: OracleDisc):
+    M = disc.mesh.n_elements
+    indptr, indices = [0], []
+    for i in range(M):
+        cols = {i} | {int(disc.nb[i, f]) for f in range(4) if disc.interior[i, f]}
+        indices.extend(sorted(cols))
+        indptr.append(len(indices))
+    return np.array(indptr), np.array(indices)
+
+
+def assemble_sparse(disc: OracleDisc, q, shift, frozen=None, eps=FD_EPS):
+    """A = shift I - dR/dq on the adjacency pattern: element blocks on the
+    diagonal, coupling blocks accumulated per interior face in the mesh's
+    face order (newton_krylov.py:281-311)."""
+    frozen = disc.freeze(q) if frozen is None else frozen
+    sz = int(disc.offsets[1])
+    indptr, indices = sparse_pattern(disc)
+    S = SparseBlocks(indptr, indices, [None] * len(indices), sz)
+    for e in range(disc.mesh.n_elements):
+        blk = element_block(disc, e, q, frozen, eps)
+        blk[np.arange(sz), np.arange(sz)] += shift
+        S.blocks[S.entry(e, e)] = blk
+    for eL, fL, eR, fR, _ in disc.mesh.interior_faces:
+        for e, f, nb in ((int(eL), int(fL), int(eR)), (int(eR), int(fR), int(eL))):
+            k = S.entry(e, nb)
+            blk = coupling_block(disc, e, f, q, frozen, eps)
+            S.blocks[k] = blk if S.blocks[k] is None else S.blocks[k] + blk
+    return S
+
+
+class Ilu0:
+    def __init__(self, F: SparseBlocks, diag_inv):
+        self.F, self.diag_inv = F, diag_inv
+
+    def apply(self, X):
+        """LU y = X by block forward / backward sweeps (newton_krylov.py:348-368)."""
+        F, sz = self.F, self.F.sz
+        y = np.zeros_like(X)
+        for i in range(F.n):
+            acc = X[i * sz:(i + 1) * sz].copy()
+            for k in range(F.indptr[i], F.indptr[i + 1]):
+                j = int(F.indices[k])
+                if j < i:
+                    acc -= F.blocks[k] @ y[j * sz:(j + 1) * sz]
+            y[i * sz:(i + 1) * sz] = acc
+        out = np.zeros_like(X)
+        for i in range(F.n - 1, -1, -1):
+            acc = y[i * sz:(i + 1) * sz].copy()
+            for k in range(F.indptr[i], F.indptr[i + 1]):
+                j = int(F.indices[k])
+                if j > i:
+                    acc -= F.blocks[k] @ out[j * sz:(j + 1) * sz]
+            out[i * sz:(i + 1) * sz] = self.diag_inv[i] @ acc
+        return out
+
+
+def ilu0_factor(A: SparseBlocks) -> Ilu0:
+    """Block ILU with zero fill on A's pattern (newton_krylov.py:319-345)."""
+    blocks = [b.copy() for b in A.blocks]
+    F = SparseBlocks(A.indptr, A.indices, blocks, A.sz)
+    diag_inv = [None] * F.n
+    for i in range(F.n):
+        row = list(range(F.indptr[i], F.indptr[i + 1]))
+        for k in row:
+            kk = int(F.indices[k])
+            if kk >= i:
+                continue
+            blocks[k] = blocks[k] @ diag_inv[kk]
+            krow = {int(F.indices[t]): t for t in range(F.indptr[kk], F.indptr[kk + 1])}
+            for k2 in row:
+                j = int(F.indices[k2])
+                if j > kk and j in krow:
+                    blocks[k2] = blocks[k2] - blocks[k] @ blocks[krow[j]]
+        try:
+            diag_inv[i] = np.linalg.inv(blocks[F.entry(i, i)])
+        except np.linalg.LinAlgError:
+            raise RuntimeError(f"singular ILU0 pivot block at element {i}")
+    return Ilu0(F, diag_inv)
+
+
+# ---------------------------------------------------------------------------
 # pMG
 
 class Level:
     def __init__(self, disc, nsweeps):
         self.disc, self.nsweeps = disc, nsweeps
         self.shift, self.q, self.S_base, self.S_extra, self.blocks = 0.0, None, 0.0, 0.0, None
+        self.smoother, self.frozen_q, self.sparse, self.ilu = "ej", None, None, None
 
     def F(self, q):
         return self.shift * q - self.disc.residual(q)
@@ -164,19 +288,33 @@ def _transfer(T, data, n_in, n_out, nv):
 
 
 class Pmg:
-    """PmgContext with EJ smoothers on every level (pmg.py:181-298)."""
+    """PmgContext (pmg.py:181-298): EJ and/or MBNK smoothers per level,
+    optional switch to MBNK after ``switch_after`` solver cycles."""
 
-    def __init__(self, disc: OracleDisc, levels, smooth=2, omega=1.0, smoother_shift=0.0, m_max=1):
+    def __init__(self, disc: OracleDisc, levels, smooth=2, omega=1.0, smoother_shift=0.0, m_max=1,
+                 smoother="ej", switch_after=None, mbnk_rtol=0.1, mbnk_maxiter=5):
         degs = [int(t) for t in str(levels).split("-")]
-        sm = [int(t) for t in str(smooth).split("-")]
-        sm = sm * len(degs) if len(sm) == 1 else sm
-        assert disc.p == degs[0]
+        L = len(degs)
+
+        def spread(text, cast):
+            toks = [cast(t) for t in str(text).split("-")]
+            return toks * L if len(toks) == 1 else toks
+        sm, kinds = spread(smooth, int), spread(smoother, str)
+        assert disc.p == degs[0] and len(sm) == L and len(kinds) == L
         self.omega, self.smoother_shift, self.m_max = omega, smoother_shift, m_max
+        self.switch_after, self.mbnk_rtol, self.mbnk_maxiter = switch_after, mbnk_rtol, mbnk_maxiter
         self.levels = [Level(disc if k == 0 else OracleDisc(disc.mesh, p, disc.eqn), sm[k])
                        for k, p in enumerate(degs)]
+        for lev, kind in zip(self.levels, kinds):
+            lev.smoother = kind
         self.ops = [transfer_operators(degs[k], degs[k + 1]) for k in range(len(degs) - 1)]
         self.fallbacks = 0
         self.cycles_done = 0
+
+    def _effective_smoother(self, k):
+        if self.switch_after is not None and self.cycles_done >= self.switch_after:
+            return "mbnk"
+        return self.levels[k].smoother
 
     def _restrict(self, k, data):
         hi, lo = self.levels[k].disc, self.levels[k + 1].disc
@@ -195,13 +333,25 @@ class Pmg:
             if k:
                 qk = self._restrict(k - 1, qk)
             lev.shift = shift
+            lev.frozen_q = qk.copy()
             lev.blocks = assemble_blocks(lev.disc, qk, shift + self.smoother_shift)
+            lev.sparse = lev.ilu = None
         self.cycles_done = 0
 
     def _smooth(self, k):
         lev = self.levels[k]
-        for _ in range(lev.nsweeps):
-            lev.q = lev.q + self.omega * lev.blocks.apply(lev.defect())
+        if self._effective_smoother(k) == "ej":
+            for _ in range(lev.nsweeps):
+                lev.q = lev.q + self.omega * lev.blocks.apply(lev.defect())
+            return
+        if lev.sparse is None:   # _ensure_sparse (pmg.py:239-243): the level's current shift
+            lev.sparse = assemble_sparse(lev.disc, lev.frozen_q, lev.shift)
+            lev.ilu = ilu0_factor(lev.sparse)
+        for _ in range(lev.nsweeps):   # smooth_mbnk (pmg.py:167-175)
+            r = lev.defect()
+            dq, _, _ = gmres_solve(lev.sparse.matvec, r, kdim=self.mbnk_maxiter, max_restarts=1,
+                                   rtol=self.mbnk_rtol, precond=lev.ilu.apply)
+            lev.q = lev.q + dq
 
     def vcycle(self, k=0):
         lev = self.levels[k]
