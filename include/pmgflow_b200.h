@@ -122,6 +122,29 @@ PMGB_API int pmgb_blocks_assemble(pmgb_disc* d, const double* q, double shift, d
 PMGB_API int pmgb_blocks_invert(int64_t n_elem, int32_t sz, const double* blocksT, double* XT, uint8_t* perm,
                                 void* stream);
 
+/* assemble_sparse_blocks (newton_krylov.py:281-311) with coupling_block
+ * (:254-278) and Discretization.neighbor_face_record / element_residual
+ * face_override (spatial.py:768-903): the block-CSR values of
+ * A = shift I - dR/dq on the element-adjacency pattern, every block
+ * column-major (blocks[k][c][r] = A_k[r][c]).  The host supplies the
+ * pattern: diag_slot[e] = CSR slot of (e, e); pairs (pair_e, pair_f) are
+ * the interior (element, face) couplings in the reference's accumulation
+ * order, grouped into nwaves waves (pairs [wave_ptr[w], wave_ptr[w+1]))
+ * in which every target slot pair_slot appears at most once; pair_add = 1
+ * adds onto the slot (second face of a periodic pair, or a self-coupling
+ * onto the diagonal).  wave_ptr is a HOST array of nwaves+1 offsets; all
+ * other arrays are device arrays; q is the level state. */
+PMGB_API int pmgb_sparse_assemble(pmgb_disc* d, const double* q, double shift, double eps, double* blocks,
+                                  const int32_t* diag_slot, int64_t npairs, const int32_t* pair_e,
+                                  const int8_t* pair_f, const int32_t* pair_slot, const int8_t* pair_add,
+                                  const int64_t* wave_ptr, int32_t nwaves, void* stream);
+
+/* SparseBlockMatrix.matvec (newton_krylov.py:243-251): y_i = sum over the
+ * row's CSR entries k of A_k x_{indices[k]}, blocks column-major, int32
+ * device CSR arrays. */
+PMGB_API int pmgb_sparse_matvec(int64_t n_rows, int32_t sz, const int32_t* indptr, const int32_t* indices,
+                                const double* blocks, const double* x, double* y, void* stream);
+
 /* BlockJacobian.apply / ej_apply (newton_krylov.py:166-171, 213-214):
  * y_e = B_e^-1 x_e from (XT, perm).  pmgb_ej_update: out = base + omega *
  * B^-1 d (smooth_ej, pmg.py:162-164); out may alias base. */

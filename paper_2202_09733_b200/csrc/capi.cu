@@ -204,6 +204,36 @@ PMGB_API int pmgb_blocks_assemble(pmgb_disc* h, const double* q, double shift, d
   return 0;
 }
 
+PMGB_API int pmgb_sparse_assemble(pmgb_disc* h, const double* q, double shift, double eps, double* blocks,
+                                  const int32_t* diag_slot, int64_t npairs, const int32_t* pair_e,
+                                  const int8_t* pair_f, const int32_t* pair_slot, const int8_t* pair_add,
+                                  const int64_t* wave_ptr, int32_t nwaves, void* stream) {
+  if (!h || !q || !blocks || !diag_slot || nwaves < 0 || (npairs > 0 && (!pair_e || !pair_f || !pair_slot ||
+                                                                         !pair_add || !wave_ptr)))
+    return -1;
+  const DiscDev& d = h->d;
+  int rc = launch_freeze(d, q, d.qtr, d.fvn, S(stream));
+  if (rc) return rc;
+  rc = launch_blocks(d, q, d.qtr, d.fvn, shift, eps, blocks, S(stream), diag_slot);
+  if (rc) return rc;
+  g_launches += n_res_launches(d);
+  for (int32_t w = 0; w < nwaves; ++w) {
+    const int64_t b = wave_ptr[w], n = wave_ptr[w + 1] - wave_ptr[w];
+    rc = launch_coupling(d, q, d.qtr, d.fvn, eps, n, pair_e + b, (const signed char*)pair_f + b, pair_slot + b,
+                         (const signed char*)pair_add + b, blocks, S(stream));
+    if (rc) return rc;
+    g_launches += 1;
+  }
+  return 0;
+}
+
+PMGB_API int pmgb_sparse_matvec(int64_t n_rows, int32_t sz, const int32_t* indptr, const int32_t* indices,
+                                const double* blocks, const double* x, double* y, void* stream) {
+  if (!indptr || !indices || !blocks || !x || !y) return -1;
+  g_launches += 1;
+  return launch_sparse_matvec(n_rows, sz, indptr, indices, blocks, x, y, S(stream));
+}
+
 PMGB_API int pmgb_ej_apply(int64_t M, int32_t sz, const double* XT, const uint8_t* perm, const double* x, double* y,
                            void* stream) {
   g_launches += 1;

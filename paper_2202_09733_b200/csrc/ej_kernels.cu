@@ -290,6 +290,36 @@ k_block_gemv2(int64_t M, int SZ, const double* __restrict__ XT, const uint8_t* _
   }
 }
 
+// Block-CSR matvec y_i = sum_k A_k x_{j_k} (SparseBlockMatrix.matvec,
+// newton_krylov.py:243-251): thread per (row, component r); each block's
+// product is summed first and then added to the row accumulator, in the
+// row's column order, as the reference does.  Blocks column-major.
+__global__ void __launch_bounds__(256)
+k_sparse_matvec(int64_t n_rows, int SZ, const int* __restrict__ indptr, const int* __restrict__ indices,
+                const double* __restrict__ blocks, const double* __restrict__ x, double* __restrict__ y) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_rows * SZ) return;
+  const int64_t i = t / SZ;
+  const int r = (int)(t - i * SZ);
+  double acc = 0.0;
+  for (int k = indptr[i]; k < indptr[i + 1]; ++k) {
+    const double* A = blocks + (int64_t)k * SZ * SZ + r;
+    const double* xj = x + (int64_t)indices[k] * SZ;
+    double s = 0.0;
+    for (int c = 0; c < SZ; ++c) s = fma(A[(int64_t)c * SZ], __ldg(xj + c), s);
+    acc += s;
+  }
+  y[t] = acc;
+}
+
+int launch_sparse_matvec(int64_t n_rows, int SZ, const int* indptr, const int* indices, const double* blocks,
+                         const double* x, double* y, cudaStream_t st) {
+  const int64_t n = n_rows * SZ;
+  if (n <= 0) return 0;
+  k_sparse_matvec<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n_rows, SZ, indptr, indices, blocks, x, y);
+  return (int)cudaGetLastError();
+}
+
 template <int SZ>
 static int run_gj(int64_t M, const double* BT, double* XT, uint8_t* perm, cudaStream_t st, Status* stp) {
   k_gj_inverse<SZ><<<(unsigned)M, GJShape<SZ>::THREADS, 0, st>>>(BT, XT, perm, stp);

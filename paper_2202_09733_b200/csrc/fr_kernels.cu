@@ -58,6 +58,9 @@ struct SL {
   static constexpr int TR = GR + 2 * NW * NPT;    // [NV] face planes    own traces (local pipeline)
   static constexpr int R0 = TR + NV * NFT;        // [NP*NV]             unperturbed local residual
   static constexpr int END_LOCAL = R0 + NP * NV;
+  static constexpr int OVQ = END_LOCAL;           // [E][N][NV]  face-record override: neighbour trace
+  static constexpr int OVF = OVQ + E * N * NV;    // [E][N][NV]  face-record override: neighbour fvn
+  static constexpr size_t BYTES_COUPLING = sizeof(double) * (OVF + E * N * NV);
   // Padded point planes of k_fvn / k_assemble_async (bank spread): point
   // (el, a, b) of a plane at el*ES + a*RS + b, planes PS apart.  The strides
   // minimise modelled shared wavefronts over the point-, row- and
@@ -1578,10 +1581,14 @@ k_assemble_async(const FrConst C, const FrMesh m, const double* __restrict__ q, 
 // local residual of point thread t in R (valid when t < NPT and the slot
 // is live).
 
-template <int P, int KIND>
+// OV: face ov_face of every slot takes its neighbour data from the
+// per-slot records in shared memory (sm + OVQ / OVF, aligned to the slot's
+// own face points) instead of the frozen buffers -- the reference's
+// element_residual face_override (spatial.py:787-790).
+template <int P, int KIND, bool OV = false>
 __device__ __forceinline__ void local_pipeline(const FrConst& C, const FrMesh& m, const Ops& op, double* sm,
                                                const int64_t* slot_elem, const double* __restrict__ qtr,
-                                               const double* __restrict__ fvn, double* R) {
+                                               const double* __restrict__ fvn, double* R, int ov_face = -1) {
   using L = SL<P, KIND>;
   constexpr int N = BC<P>::N, NP = BC<P>::NP, NF = BC<P>::NF, E = BC<P>::EPB;
   constexpr int NV = KT<KIND>::NV, NW = KT<KIND>::NW, NPT = L::NPT, NFT = L::NFT;
@@ -1618,7 +1625,10 @@ __device__ __forceinline__ void local_pipeline(const FrConst& C, const FrMesh& m
     double tr[NV], nb[NV], F[NV];
 #pragma unroll
     for (int v = 0; v < NV; ++v) tr[v] = line_sum<N>(op, sQ + v * NPT + el * NP, f, k);
-    if (lk.x >= 0) {
+    if (OV && f == ov_face) {
+#pragma unroll
+      for (int v = 0; v < NV; ++v) nb[v] = sm[L::OVQ + (el * N + k) * NV + v];
+    } else if (lk.x >= 0) {
       const int kk = lk_rev(lk.y) ? N - 1 - k : k;
       ld_face<NV>(qtr + (((int64_t)lk.x * 4 + lk_face(lk.y)) * N + kk) * NV, nb);
     } else {
@@ -1693,7 +1703,10 @@ __device__ __forceinline__ void local_pipeline(const FrConst& C, const FrMesh& m
       double Fv[NV];
 #pragma unroll
       for (int v = 0; v < NV; ++v) Fv[v] = fx[v] * nx + fy[v] * ny;
-      if (lk.x >= 0) {
+      if (OV && f == ov_face) {
+#pragma unroll
+        for (int v = 0; v < NV; ++v) Fv[v] = 0.5 * (Fv[v] + (-sm[L::OVF + (el * N + k) * NV + v]));
+      } else if (lk.x >= 0) {
         const int kk = lk_rev(lk.y) ? N - 1 - k : k;
         double Fn[NV];
         ld_face<NV>(fvn + (((int64_t)lk.x * 4 + lk_face(lk.y)) * N + kk) * NV, Fn);
@@ -1755,7 +1768,8 @@ k_local(const FrConst C, const FrMesh m, const int64_t* __restrict__ elems, int6
 template <int P, int KIND>
 __global__ void __launch_bounds__(BC<P>::THREADS, MinBlocks<P>::ASM)
 k_blocks(const FrConst C, const FrMesh m, const double* __restrict__ q, const double* __restrict__ qtr,
-         const double* __restrict__ fvn, double shift, double eps, double* __restrict__ BT) {
+         const double* __restrict__ fvn, double shift, double eps, double* __restrict__ BT,
+         const int* __restrict__ out_slot) {
   extern __shared__ double sm[];
   using L = SL<P, KIND>;
   constexpr int NP = BC<P>::NP, E = BC<P>::EPB, NV = KT<KIND>::NV, NPT = L::NPT;
@@ -1767,7 +1781,7 @@ k_blocks(const FrConst C, const FrMesh m, const double* __restrict__ q, const do
   double* sR0 = sm + L::R0;
   const double* qe = q + e * SZ;
   const int t0 = threadIdx.x;
-  double* BTe = BT + e * (int64_t)SZ * SZ;
+  double* BTe = BT + (out_slot ? (int64_t)out_slot[e] : e) * (int64_t)SZ * SZ;
   for (int i = threadIdx.x; i < E * 20; i += BC<P>::THREADS) sm[L::G + i] = __ldg(m.geom + e * 20 + i % 20);
   for (int c0 = 0; c0 <= SZ; c0 += E) {
     __syncthreads();
@@ -1794,6 +1808,182 @@ k_blocks(const FrConst C, const FrMesh m, const double* __restrict__ q, const do
         double val = -(R[v] - sR0[i]) / eps;
         if (i == c - 1) val = val + shift;
         col[i] = val;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// neighbour face records and FD coupling blocks (spatial.py:855-903,
+// newton_krylov.py:254-311)
+//
+// record_pipeline: the slots hold (perturbed) states of the neighbour nb of
+// element e across e's face f; it runs nb's own trace / BR1 / gradient
+// pipeline with nb's other neighbours frozen and leaves, aligned to e's face
+// points, nb's trace (OVQ) and one-sided viscous normal flux (OVF) on the
+// shared face fnb.
+
+template <int P, int KIND>
+__device__ __forceinline__ void record_pipeline(const FrConst& C, const FrMesh& m, const Ops& op, double* sm,
+                                                const int64_t* slot_elem, const double* __restrict__ qtr,
+                                                int fnb, bool rev) {
+  using L = SL<P, KIND>;
+  constexpr int N = BC<P>::N, NP = BC<P>::NP, NF = BC<P>::NF, E = BC<P>::EPB;
+  constexpr int NV = KT<KIND>::NV, NW = KT<KIND>::NW, NPT = L::NPT, NFT = L::NFT;
+  constexpr bool VISC = KT<KIND>::VISC;
+  double* sQ = sm + L::Q;
+  double* sG = sm + L::G;
+  double* sW = sm + L::W;
+  double* sWH = sm + L::WH;
+  double* sCG = sm + L::CG;
+  double* sGR = sm + L::GR;
+  double* sTR = sm + L::TR;
+  const Phys ph = phys_of(C);
+  const int t0 = threadIdx.x;
+  if constexpr (VISC) {
+    if (t0 < NPT) {
+      double qq[NV], w[NW];
+      gather_point<NV, NPT>(sQ, t0, qq);
+      grad_vars<KIND>(qq, ph.gamma, w);
+#pragma unroll
+      for (int c = 0; c < NW; ++c) sW[c * NPT + t0] = w[c];
+    }
+  }
+  for (int t = threadIdx.x; t < E * NF; t += BC<P>::THREADS) {
+    const int el = t / NF, r = t % NF, f = r / N, k = r % N;
+    const int64_t e = slot_elem[el];
+    if (e < 0) continue;
+    double tr[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) tr[v] = line_sum<N>(op, sQ + v * NPT + el * NP, f, k);
+    if (f == fnb) {
+      const int ke = rev ? N - 1 - k : k;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) sm[L::OVQ + (el * N + ke) * NV + v] = tr[v];
+    }
+    if constexpr (VISC) {
+      const int2 lk = m.link[e * 4 + f];
+      const double* gq = sG + el * 20;
+      double nb[NV];
+      if (lk.x >= 0) {
+        const int kk = lk_rev(lk.y) ? N - 1 - k : k;
+        ld_face<NV>(qtr + (((int64_t)lk.x * 4 + lk_face(lk.y)) * N + kk) * NV, nb);
+      } else {
+        ghost<KIND>(tr, lk_tag(lk.y), gq[8 + 2 * f], gq[9 + 2 * f], C.qinf, nb);
+      }
+      double wa[NW], wc[NW];
+      grad_vars<KIND>(tr, ph.gamma, wa);
+      grad_vars<KIND>(nb, ph.gamma, wc);
+#pragma unroll
+      for (int c = 0; c < NW; ++c) sWH[c * NFT + t] = 0.5 * (wa[c] + wc[c]);
+#pragma unroll
+      for (int v = 0; v < NV; ++v) sTR[v * NFT + t] = tr[v];
+    }
+  }
+  if constexpr (VISC) {
+    __syncthreads();
+    for (int t = threadIdx.x; t < E * NF; t += BC<P>::THREADS) {
+      const int el = t / NF, r = t % NF, f = r / N, k = r % N;
+      if (slot_elem[el] < 0) continue;
+      grad_corrections<P, KIND>(op, sW, sG + el * 20, sWH, sCG, el, f, k);
+    }
+    __syncthreads();
+    if (t0 < NPT) {
+      const int el = t0 / NP, pt = t0 % NP;
+      double gx[NW], gy[NW];
+      gradient_at<P, KIND>(op, sW, sG + el * 20, sCG, el, pt / N, pt % N, gx, gy);
+#pragma unroll
+      for (int c = 0; c < NW; ++c) {
+        sGR[c * NPT + t0] = gx[c];
+        sGR[(NW + c) * NPT + t0] = gy[c];
+      }
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < E * N; t += BC<P>::THREADS) {
+      const int el = t / N, k = t % N;
+      if (slot_elem[el] < 0) continue;
+      const int fi = el * NF + fnb * N + k;
+      double gx[NW], gy[NW], tr[NV], fx[NV], fy[NV];
+#pragma unroll
+      for (int c = 0; c < NW; ++c) {
+        gx[c] = line_sum<N>(op, sGR + c * NPT + el * NP, fnb, k);
+        gy[c] = line_sum<N>(op, sGR + (NW + c) * NPT + el * NP, fnb, k);
+      }
+#pragma unroll
+      for (int v = 0; v < NV; ++v) tr[v] = sTR[v * NFT + fi];
+      visc_flux<KIND>(tr, gx, gy, ph, fx, fy);
+      const double nx = sG[el * 20 + 8 + 2 * fnb], ny = sG[el * 20 + 9 + 2 * fnb];
+      const int ke = rev ? N - 1 - k : k;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) sm[L::OVF + (el * N + ke) * NV + v] = fx[v] * nx + fy[v] * ny;
+    }
+  }
+}
+
+// One CTA per (element e, face f) coupling: column c of -dR_e/dq_nb from
+// instance c (nb's state with DoF c-1 raised by eps; instance 0 is the base).
+// Output column-major into the block slot (BT[c][r] = B[r][c]); pair_add
+// accumulates onto what an earlier wave (or the element block) wrote there (periodic pairs meeting
+// through two faces, newton_krylov.py:307-310).
+template <int P, int KIND>
+__global__ void __launch_bounds__(BC<P>::THREADS)
+k_coupling(const FrConst C, const FrMesh m, const double* __restrict__ q, const double* __restrict__ qtr,
+           const double* __restrict__ fvn, double eps, const int* __restrict__ pair_e,
+           const signed char* __restrict__ pair_f, const int* __restrict__ pair_slot,
+           const signed char* __restrict__ pair_add, double* __restrict__ blocks) {
+  extern __shared__ double sm[];
+  using L = SL<P, KIND>;
+  constexpr int NP = BC<P>::NP, E = BC<P>::EPB, NV = KT<KIND>::NV, NPT = L::NPT;
+  constexpr int SZ = NP * NV;
+  __shared__ int64_t slot[E];
+  const Ops op = stage_ops<BC<P>::THREADS>(C, sm);
+  const int64_t e = pair_e[blockIdx.x];
+  const int f = pair_f[blockIdx.x];
+  const int2 lk = m.link[e * 4 + f];
+  const int64_t nb = lk.x;
+  const int fnb = lk_face(lk.y);
+  const bool rev = lk_rev(lk.y);
+  double* sQ = sm + L::Q;
+  double* sR0 = sm + L::R0;
+  double* out = blocks + (int64_t)pair_slot[blockIdx.x] * SZ * SZ;
+  const bool add = pair_add[blockIdx.x] != 0;
+  const int t0 = threadIdx.x;
+  for (int c0 = 0; c0 <= SZ; c0 += E) {
+    // neighbour records for instances c0 .. c0+E-1
+    __syncthreads();
+    for (int i = threadIdx.x; i < E * 20; i += BC<P>::THREADS) sm[L::G + i] = __ldg(m.geom + nb * 20 + i % 20);
+    for (int s = threadIdx.x; s < E; s += BC<P>::THREADS) slot[s] = (c0 + s <= SZ) ? nb : -1;
+    for (int i = threadIdx.x; i < E * SZ; i += BC<P>::THREADS) {
+      const int s = i / SZ, d = i % SZ, c = c0 + s;
+      const double v = __ldg(q + nb * SZ + d);
+      sQ[(d % NV) * NPT + s * NP + d / NV] = (c >= 1 && d == c - 1) ? v + eps : v;
+    }
+    __syncthreads();
+    record_pipeline<P, KIND>(C, m, op, sm, slot, qtr, fnb, rev);
+    // element e (unperturbed) with face f overridden by the records
+    __syncthreads();
+    for (int i = threadIdx.x; i < E * 20; i += BC<P>::THREADS) sm[L::G + i] = __ldg(m.geom + e * 20 + i % 20);
+    for (int s = threadIdx.x; s < E; s += BC<P>::THREADS) slot[s] = (c0 + s <= SZ) ? e : -1;
+    for (int i = threadIdx.x; i < E * SZ; i += BC<P>::THREADS) {
+      const int s = i / SZ, d = i % SZ;
+      sQ[(d % NV) * NPT + s * NP + d / NV] = __ldg(q + e * SZ + d);
+    }
+    __syncthreads();
+    double R[NV];
+    local_pipeline<P, KIND, true>(C, m, op, sm, slot, qtr, fvn, R, f);
+    const int s = t0 / NP, pt = t0 % NP, c = c0 + s;
+    if (c0 == 0 && t0 < NP) {
+#pragma unroll
+      for (int v = 0; v < NV; ++v) sR0[pt * NV + v] = R[v];
+    }
+    __syncthreads();
+    if (t0 < NPT && c >= 1 && c <= SZ) {
+      double* col = out + (int64_t)(c - 1) * SZ;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const int i = pt * NV + v;
+        const double val = -(R[v] - sR0[i]) / eps;
+        col[i] = add ? col[i] + val : val;
       }
     }
   }
@@ -1898,7 +2088,7 @@ static int run_local(const DiscDev& d, const int64_t* elems, int64_t B, const do
 
 template <int P, int KIND>
 static int run_blocks(const DiscDev& d, const double* q, const double* qtr, const double* fvn, double shift,
-                      double eps, double* BT, cudaStream_t st) {
+                      double eps, double* BT, const int* out_slot, cudaStream_t st) {
   using L = SL<P, KIND>;
   constexpr int TH = BC<P>::THREADS;
   static bool attr = false;
@@ -1907,7 +2097,25 @@ static int run_blocks(const DiscDev& d, const double* q, const double* qtr, cons
     attr = true;
   }
   if (d.M <= 0) return 0;
-  k_blocks<P, KIND><<<(unsigned)d.M, TH, L::BYTES_LOCAL, st>>>(d.C, d.mesh, q, qtr, fvn, shift, eps, BT);
+  k_blocks<P, KIND><<<(unsigned)d.M, TH, L::BYTES_LOCAL, st>>>(d.C, d.mesh, q, qtr, fvn, shift, eps, BT, out_slot);
+  return (int)cudaGetLastError();
+}
+
+template <int P, int KIND>
+static int run_coupling(const DiscDev& d, const double* q, const double* qtr, const double* fvn, double eps,
+                        int64_t npairs, const int* pair_e, const signed char* pair_f, const int* pair_slot,
+                        const signed char* pair_add, double* blocks, cudaStream_t st) {
+  using L = SL<P, KIND>;
+  constexpr int TH = BC<P>::THREADS;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_coupling<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)L::BYTES_COUPLING);
+    attr = true;
+  }
+  if (npairs <= 0) return 0;
+  k_coupling<P, KIND><<<(unsigned)npairs, TH, L::BYTES_COUPLING, st>>>(d.C, d.mesh, q, qtr, fvn, eps, pair_e,
+                                                                         pair_f, pair_slot, pair_add, blocks);
   return (int)cudaGetLastError();
 }
 
@@ -1974,8 +2182,14 @@ int launch_local_residual(const DiscDev& d, const int64_t* elems, int64_t B, con
 }
 
 int launch_blocks(const DiscDev& d, const double* q, const double* qtr, const double* fvn, double shift,
-                  double eps, double* BT, cudaStream_t st) {
-  PMGB_DISPATCH(run_blocks, d, q, qtr, fvn, shift, eps, BT, st)
+                  double eps, double* BT, cudaStream_t st, const int* out_slot) {
+  PMGB_DISPATCH(run_blocks, d, q, qtr, fvn, shift, eps, BT, out_slot, st)
+}
+
+int launch_coupling(const DiscDev& d, const double* q, const double* qtr, const double* fvn, double eps,
+                    int64_t npairs, const int* pair_e, const signed char* pair_f, const int* pair_slot,
+                    const signed char* pair_add, double* blocks, cudaStream_t st) {
+  PMGB_DISPATCH(run_coupling, d, q, qtr, fvn, eps, npairs, pair_e, pair_f, pair_slot, pair_add, blocks, st)
 }
 
 Status* status_ptr() {

@@ -114,7 +114,12 @@ int launch_freeze(const DiscDev& d, const double* q, double* qtr, double* fvn, c
 int launch_local_residual(const DiscDev& d, const int64_t* elems, int64_t B, const double* Q,
                           const double* qtr, const double* fvn, double* out, cudaStream_t st);
 int launch_blocks(const DiscDev& d, const double* q, const double* qtr, const double* fvn,
-                  double shift, double eps, double* blocksT, cudaStream_t st);
+                  double shift, double eps, double* blocksT, cudaStream_t st, const int* out_slot = nullptr);
+int launch_coupling(const DiscDev& d, const double* q, const double* qtr, const double* fvn, double eps,
+                    int64_t npairs, const int* pair_e, const signed char* pair_f, const int* pair_slot,
+                    const signed char* pair_add, double* blocks, cudaStream_t st);
+int launch_sparse_matvec(int64_t n_rows, int SZ, const int* indptr, const int* indices, const double* blocks,
+                         const double* x, double* y, cudaStream_t st);
 int status_clear_async(cudaStream_t st);
 int status_read(cudaStream_t st, Status* out, int clear);
 }  // namespace pmgb

@@ -237,6 +237,131 @@ class BlockJacobian:
         return out
 
 
+# ---------------------------------------------------------------------------
+# block-sparse Jacobian (newton_krylov.py:215-311)
+
+class _SparsePattern:
+    """Element-adjacency block-CSR pattern (diagonal + face neighbours,
+    columns sorted per row) and the coupling pairs in the reference's
+    accumulation order, grouped into waves with distinct target slots
+    (assemble_sparse_blocks, newton_krylov.py:281-311)."""
+
+    def __init__(self, disc: Discretization):
+        mesh = disc.mesh
+        M = mesh.n_elements
+        faces = np.asarray(mesh.interior_faces, dtype=np.int64).reshape(-1, 5)
+        adj = [{i} for i in range(M)]
+        for eL, fL, eR, fR, _ in faces.tolist():
+            adj[eL].add(eR)
+            adj[eR].add(eL)
+        counts = np.array([len(a) for a in adj], dtype=np.int64)
+        self.indptr = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+        self.indices = np.concatenate([sorted(a) for a in adj]).astype(np.int64) if M else np.zeros(0, np.int64)
+        self.nnz = int(self.indptr[-1])
+        rows = np.repeat(np.arange(M), counts)
+        self.diag_slot = np.nonzero(self.indices == rows)[0]
+        slot_of = {(int(r), int(c)): k for k, (r, c) in enumerate(zip(rows, self.indices))}
+        pe, pf, ps, pa, pw = [], [], [], [], []
+        contrib = np.zeros(self.nnz, dtype=np.int64)
+        is_diag = self.indices == rows
+        for eL, fL, eR, fR, _ in faces.tolist():
+            for e, f, nb in ((eL, fL, eR), (eR, fR, eL)):
+                k = slot_of[(e, nb)]
+                pe.append(e)
+                pf.append(f)
+                ps.append(k)
+                pa.append(1 if (is_diag[k] or contrib[k] > 0) else 0)
+                pw.append(contrib[k])
+                contrib[k] += 1
+        order = np.argsort(np.asarray(pw, dtype=np.int64), kind="stable")
+        self.pair_e = np.asarray(pe, dtype=np.int32)[order]
+        self.pair_f = np.asarray(pf, dtype=np.int8)[order]
+        self.pair_slot = np.asarray(ps, dtype=np.int32)[order]
+        self.pair_add = np.asarray(pa, dtype=np.int8)[order]
+        nw = int(max(pw) + 1) if pw else 0
+        self.wave_ptr = np.concatenate([[0], np.cumsum(np.bincount(np.asarray(pw, dtype=np.int64),
+                                                                    minlength=nw))]).astype(np.int64)
+        dev = disc.device
+        self.d = {name: torch.as_tensor(np.ascontiguousarray(getattr(self, name)), device=dev)
+                  for name in ("pair_e", "pair_f", "pair_slot", "pair_add")}
+        self.d["diag_slot"] = torch.as_tensor(self.diag_slot.astype(np.int32), device=dev)
+        self.d["indptr"] = torch.as_tensor(self.indptr.astype(np.int32), device=dev)
+        self.d["indices"] = torch.as_tensor(self.indices.astype(np.int32), device=dev)
+
+    def entry(self, i: int, j: int) -> int:
+        lo, hi = int(self.indptr[i]), int(self.indptr[i + 1])
+        k = lo + int(np.searchsorted(self.indices[lo:hi], j))
+        return k if k < hi and self.indices[k] == j else -1
+
+
+def sparse_pattern(disc: Discretization) -> _SparsePattern:
+    pat = getattr(disc, "_sparse_pattern", None)
+    if pat is None:
+        pat = disc._sparse_pattern = _SparsePattern(disc)
+    return pat
+
+
+class SparseBlockMatrix:
+    """Block-CSR over element adjacency (newton_krylov.py:218-251), on the
+    device: ``blocksT`` (nnz, sz, sz) column-major (blocksT[k][c][r] =
+    A_k[r][c]); ``indptr`` / ``indices`` as NumPy (host) with int32 device
+    copies inside the pattern."""
+
+    def __init__(self, disc: Discretization, pattern: _SparsePattern, blocksT: torch.Tensor):
+        self.disc = disc
+        self.pattern = pattern
+        self.blocksT = blocksT
+        self.n = disc.mesh.n_elements
+        self.indptr = pattern.indptr
+        self.indices = pattern.indices
+        self.sizes = np.full(self.n, disc.elem_size, dtype=np.int64)
+
+    @property
+    def blocks(self):
+        return self.blocksT.transpose(1, 2)
+
+    def entry(self, i: int, j: int) -> int:
+        return self.pattern.entry(i, j)
+
+    def check_symmetric_pattern(self):
+        for i in range(self.n):
+            for k in range(self.indptr[i], self.indptr[i + 1]):
+                j = int(self.indices[k])
+                if self.entry(j, i) < 0:
+                    raise ValueError(f"asymmetric sparsity: ({i},{j}) present, ({j},{i}) missing")
+
+    def matvec(self, X, offsets=None):
+        is_np = not isinstance(X, torch.Tensor)
+        Xd = to_device(X, self.disc.device)
+        out = torch.empty_like(Xd)
+        pd = self.pattern.d
+        check(load().pmgb_sparse_matvec(self.n, self.disc.elem_size, pd["indptr"].data_ptr(),
+                                        pd["indices"].data_ptr(), self.blocksT.data_ptr(), ptr(Xd), ptr(out),
+                                        stream()), "sparse_matvec")
+        return out.cpu().numpy() if is_np else out
+
+
+def assemble_sparse_blocks(disc: Discretization, data, shift: float, frozen=None,
+                           eps: float = FD_EPS) -> SparseBlockMatrix:
+    """A = shift I - dR/dq restricted to the element-adjacency pattern
+    (newton_krylov.py:281-311): FD element blocks on the diagonal, FD
+    coupling blocks through every interior face (neighbour face records
+    recomputed from the perturbed neighbour, spatial.py:855-903),
+    accumulated in the reference's face order."""
+    del frozen  # the device freeze of ``data`` is recomputed (same values)
+    q = to_device(data, disc.device)
+    pat = sparse_pattern(disc)
+    sz = disc.elem_size
+    blocksT = torch.empty((pat.nnz, sz, sz), dtype=torch.float64, device=disc.device)
+    d = pat.d
+    wave_ptr = np.ascontiguousarray(pat.wave_ptr, dtype=np.int64)
+    check(load().pmgb_sparse_assemble(disc._h, ptr(q), float(shift), float(eps), blocksT.data_ptr(),
+                                      d["diag_slot"].data_ptr(), len(pat.pair_e), d["pair_e"].data_ptr(),
+                                      d["pair_f"].data_ptr(), d["pair_slot"].data_ptr(), d["pair_add"].data_ptr(),
+                                      wave_ptr.ctypes.data, len(wave_ptr) - 1, stream()), "sparse_assemble")
+    return SparseBlockMatrix(disc, pat, blocksT)
+
+
 def assemble_element_blocks(disc: Discretization, data, shift: float, frozen=None, eps: float = FD_EPS,
                             keep_blocks: bool = True) -> BlockJacobian:
     """FD element blocks of shift I - dR/dq and their inverses.
