@@ -826,7 +826,7 @@ k_trace_lines(const FrConst C, const FrMesh m, const double* __restrict__ q, con
 template <int P, int KIND>
 __global__ void __launch_bounds__(BC<P>::THREADS, MinBlocks<P>::FVN)
 k_fvn(const FrConst C, const FrMesh m, const double* __restrict__ q, const double* __restrict__ qtr,
-      double* __restrict__ fvn, double* __restrict__ grad) {
+      double* __restrict__ fvn, double* __restrict__ grad, int q_dep) {
   extern __shared__ double sm[];
   using L = SL<P, KIND>;
   constexpr int N = BC<P>::N, NP = BC<P>::NP, NF = BC<P>::NF, E = BC<P>::EPB;
@@ -846,7 +846,9 @@ k_fvn(const FrConst C, const FrMesh m, const double* __restrict__ q, const doubl
   // (own + neighbour) into registers, all before the first barrier.
   constexpr bool ONE_FACE = (E * NF <= BC<P>::THREADS);
   const int t0 = threadIdx.x;
-  load_points_pad<P, NV, L>(q, e0, M, sQ);
+  // q_dep: q is the q + eps X written by the preceding k_trace_lines (Jv
+  // forms), so it may only be read after the dependency wait
+  if (!q_dep) load_points_pad<P, NV, L>(q, e0, M, sQ);
   load_geom<P>(m.geom, e0, M, sG);
   double tr[NV], nb[NV];
   int2 lk = make_int2(-1, 0);
@@ -861,7 +863,8 @@ k_fvn(const FrConst C, const FrMesh m, const double* __restrict__ q, const doubl
       if (face_live) lk = m.link[(e0 + fel) * 4 + ff];
     }
   }
-  pdl_wait();  // traces come from k_trace
+  pdl_wait();  // traces (and for Jv the perturbed state) come from k_trace
+  if (q_dep) load_points_pad<P, NV, L>(q, e0, M, sQ);
   if constexpr (ONE_FACE) {
     if (t0 < E * NF) {
       const int fk = (t0 % NF) % N;
@@ -1388,7 +1391,7 @@ template <int P, int KIND>
 __global__ void __launch_bounds__(BC<P>::THREADS, MinBlocks<P>::ASM)
 k_assemble_async(const FrConst C, const FrMesh m, const double* __restrict__ q, const double* __restrict__ qtr,
                  const double* __restrict__ fvn, const double* __restrict__ grad, const Epi ep,
-                 double* __restrict__ out, int* bad, Status* st) {
+                 double* __restrict__ out, int* bad, Status* st, int q_dep) {
   extern __shared__ __align__(16) double sm[];
   using L = SL<P, KIND>;
   constexpr int TH = BC<P>::THREADS;
@@ -1406,9 +1409,13 @@ k_assemble_async(const FrConst C, const FrMesh m, const double* __restrict__ q, 
   const int64_t M = m.M;
   const int ne = (int)((M - e0) < E ? (M - e0) : E);
   const int t0 = threadIdx.x;
-  {
+  // q_dep: q is k_trace's q + eps X (Jv forms): copied only after the wait
+  auto copy_q = [&]() {
     const double* qs = q + e0 * NP * NV;
     for (int i = t0; i < E * NP * NV / 2; i += TH) cp_async16(sQA + 2 * i, qs + 2 * i, 2 * i < ne * NP * NV);
+  };
+  {
+    if (!q_dep) copy_q();
     const double* gsrc = m.geom + e0 * 20;
     for (int i = t0; i < E * 10; i += TH) cp_async16(sG + 2 * i, gsrc + 2 * i, 2 * i < ne * 20);
     cp_async_commit();
@@ -1428,6 +1435,10 @@ k_assemble_async(const FrConst C, const FrMesh m, const double* __restrict__ q, 
   const Ops op = stage_ops<TH>(C, sm);
   const Phys ph = phys_of(C);
   pdl_wait();  // gradients / fvn from k_fvn, traces and status flags from k_trace
+  if (q_dep) {
+    copy_q();
+    cp_async_commit();
+  }
   if (blockIdx.x == 0 && threadIdx.x == 0) commit_status(bad, st);
   // point gradients into registers
   double gx[NW], gy[NW];
@@ -2039,11 +2050,12 @@ static int run_residual(const DiscDev& d, const double* q, const double* X, doub
   } else {
     k_trace<P, KIND><<<grid, TH, L::BYTES_TRACE, st>>>(d.C, d.mesh, q, X, eps, d.qp, d.qtr, bad);
   }
+  const int q_dep = X != nullptr;
   if (KT<KIND>::VISC) launch_pdl(k_fvn<P, KIND>, grid, TH, L::BYTES_FVN, st, d.C, d.mesh, qq, (const double*)d.qtr,
-                                 d.fvn, d.grad);
+                                 d.fvn, d.grad, q_dep);
   if constexpr (KT<KIND>::NV == 4 && E * BC<P>::NF <= TH)
     launch_pdl(k_assemble_async<P, KIND>, grid, TH, L::BYTES_ASYNC, st, d.C, d.mesh, qq, (const double*)d.qtr,
-               (const double*)d.fvn, (const double*)d.grad, epi, out, bad, stp);
+               (const double*)d.fvn, (const double*)d.grad, epi, out, bad, stp, q_dep);
   else
     k_assemble<P, KIND><<<grid, TH, L::BYTES_ASM, st>>>(d.C, d.mesh, qq, d.qtr, d.fvn, d.grad, epi, out, bad, stp);
   return (int)cudaGetLastError();
@@ -2066,7 +2078,7 @@ static int run_freeze(const DiscDev& d, const double* q, double* qtr, double* fv
   } else {
     k_trace<P, KIND><<<grid, TH, L::BYTES_TRACE, st>>>(d.C, d.mesh, q, nullptr, 0.0, nullptr, qtr, nullptr);
   }
-  if (KT<KIND>::VISC) k_fvn<P, KIND><<<grid, TH, L::BYTES_FVN, st>>>(d.C, d.mesh, q, qtr, fvn, nullptr);
+  if (KT<KIND>::VISC) k_fvn<P, KIND><<<grid, TH, L::BYTES_FVN, st>>>(d.C, d.mesh, q, qtr, fvn, nullptr, 0);
   return (int)cudaGetLastError();
 }
 

@@ -90,3 +90,20 @@ def test_fullsize_properties(cuda, k):
         J1 = nk.jfnk_matvec(X, q, R, d.residual, 3.0)
         J2 = nk.jfnk_matvec(2.0 * X, q, R, d.residual, 3.0)
         assert float((J2 - 2.0 * J1).norm() / J1.norm()) <= 1e-4  # O(eps |X|), eps = 1e-6
+
+
+def test_fullsize_jv_bitwise_deterministic(cuda):
+    # the fused Jv reads k_trace's q + eps X in k_fvn / k_assemble, which run
+    # under programmatic dependent launch: those reads must follow the
+    # dependency wait (a read-before-write race made steps nondeterministic)
+    from paper_2202_09733_b200 import _lib
+    c = cases.config(2)
+    d = Discretization(c.mesh, c.p, c.eqn)
+    q = torch.as_tensor(c.q0, device="cuda")
+    R0 = d.residual(q)
+    X = torch.randn(d.n_dofs, dtype=torch.float64, device="cuda", generator=torch.Generator("cuda").manual_seed(5))
+    outs = [torch.empty_like(q) for _ in range(12)]
+    for o in outs:
+        d.eval(q, _lib.EPI_JV, o, X=X, eps=1e-6, s=2.5, R0=R0)
+    torch.cuda.synchronize()
+    assert all(torch.equal(outs[0], o) for o in outs[1:])
