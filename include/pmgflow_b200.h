@@ -21,7 +21,8 @@
  *    first one seen is latched in a device status word and read back
  *    by pmgb_status (kind 1 = state, 2 = trace, with the smallest
  *    offending element of that residual evaluation).  Kind 3 = singular
- *    element-Jacobi block (newton_krylov.py:202-208).
+ *    element-Jacobi block (newton_krylov.py:202-208); kind 4 = singular
+ *    ILU0 pivot block (newton_krylov.py:340-343).
  */
 #ifndef PMGFLOW_B200_H
 #define PMGFLOW_B200_H
@@ -144,6 +145,27 @@ PMGB_API int pmgb_sparse_assemble(pmgb_disc* d, const double* q, double shift, d
  * device CSR arrays. */
 PMGB_API int pmgb_sparse_matvec(int64_t n_rows, int32_t sz, const int32_t* indptr, const int32_t* indices,
                                 const double* blocks, const double* x, double* y, void* stream);
+
+/* ilu0_factor (newton_krylov.py:319-345): block ILU with zero fill, in
+ * place on F (a copy of the CSR values), level-scheduled: level L holds the
+ * rows level_rows[level_ptr[L] .. level_ptr[L+1]) of the lower-neighbour
+ * DAG (level_diag = their diagonal CSR slots); every row performs the
+ * reference's block operations in its order.  The pivot-block inverses
+ * are stored as Gauss-Jordan factors (DX, DP) like the EJ blocks; a
+ * singular pivot block latches status kind 4 (RuntimeError "singular ILU0
+ * pivot block at element i").  level_ptr is a HOST array. */
+PMGB_API int pmgb_ilu0_factor(int64_t n_rows, int32_t sz, const int32_t* indptr, const int32_t* indices,
+                               double* F, double* DX, uint8_t* DP, int32_t n_levels, const int64_t* level_ptr,
+                               const int32_t* level_rows, const int32_t* level_diag, void* stream);
+
+/* ilu0_apply (newton_krylov.py:348-368): forward sweep with the unit lower
+ * factor over the lower-DAG levels (into y), backward sweep with the upper
+ * factor and the pivot inverses over the upper-DAG levels (into out).
+ * lo_ptr / up_ptr are HOST arrays. */
+PMGB_API int pmgb_ilu0_apply(int64_t n_rows, int32_t sz, const int32_t* indptr, const int32_t* indices,
+                              const double* F, const double* DX, const uint8_t* DP, int32_t n_lo,
+                              const int64_t* lo_ptr, const int32_t* lo_rows, int32_t n_up, const int64_t* up_ptr,
+                              const int32_t* up_rows, const double* x, double* y, double* out, void* stream);
 
 /* BlockJacobian.apply / ej_apply (newton_krylov.py:166-171, 213-214):
  * y_e = B_e^-1 x_e from (XT, perm).  pmgb_ej_update: out = base + omega *

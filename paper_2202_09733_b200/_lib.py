@@ -61,6 +61,11 @@ SIGNATURES = {
     "pmgb_blocks_invert": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int32, c_void_p, c_void_p, c_void_p, c_void_p]),
     "pmgb_sparse_matvec": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int32, c_void_p, c_void_p, c_void_p, c_void_p,
                                           c_void_p, c_void_p]),
+    "pmgb_ilu0_factor": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int32, c_void_p, c_void_p, c_void_p, c_void_p,
+                                        c_void_p, ctypes.c_int32, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "pmgb_ilu0_apply": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int32, c_void_p, c_void_p, c_void_p, c_void_p,
+                                       c_void_p, ctypes.c_int32, c_void_p, c_void_p, ctypes.c_int32, c_void_p,
+                                       c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "pmgb_sparse_assemble": (ctypes.c_int, [c_void_p, c_void_p, ctypes.c_double, ctypes.c_double, c_void_p,
                                             c_void_p, ctypes.c_int64, c_void_p, c_void_p, c_void_p, c_void_p,
                                             c_void_p, ctypes.c_int32, c_void_p]),

@@ -8,7 +8,13 @@
 #include "pmgb_internal.cuh"
 
 namespace pmgb {
-int launch_inverse(int64_t M, int SZ, const double* BT, double* XT, uint8_t* perm, cudaStream_t st, Status* stp);
+int launch_inverse(int64_t M, int SZ, const double* BT, double* XT, uint8_t* perm, cudaStream_t st, Status* stp,
+                   const int* in_slot = nullptr, const int* out_idx = nullptr, int bad_kind = 3);
+int launch_ilu_level(int64_t n, int SZ, const int* rows, const int* indptr, const int* indices, double* F,
+                     const double* DX, const uint8_t* DP, cudaStream_t st);
+int launch_ilu_sweep(int backward, int64_t n, int SZ, const int* rows, const int* indptr, const int* indices,
+                     const double* F, const double* DX, const uint8_t* DP, const double* in, double* out,
+                     cudaStream_t st);
 int launch_block_gemv(int64_t M, int SZ, const double* XT, const uint8_t* perm, const double* x, double omega,
                       const double* base, double* out, cudaStream_t st);
 int launch_transfer(int64_t M, int nv, int nin, int nout, const double* T, const double* src,
@@ -232,6 +238,43 @@ PMGB_API int pmgb_sparse_matvec(int64_t n_rows, int32_t sz, const int32_t* indpt
   if (!indptr || !indices || !blocks || !x || !y) return -1;
   g_launches += 1;
   return launch_sparse_matvec(n_rows, sz, indptr, indices, blocks, x, y, S(stream));
+}
+
+PMGB_API int pmgb_ilu0_factor(int64_t n_rows, int32_t sz, const int32_t* indptr, const int32_t* indices,
+                               double* F, double* DX, uint8_t* DP, int32_t n_levels, const int64_t* level_ptr,
+                               const int32_t* level_rows, const int32_t* level_diag, void* stream) {
+  if (!indptr || !indices || !F || !DX || !DP || (n_levels > 0 && (!level_ptr || !level_rows || !level_diag)))
+    return -1;
+  (void)n_rows;
+  for (int32_t L = 0; L < n_levels; ++L) {
+    const int64_t b = level_ptr[L], n = level_ptr[L + 1] - level_ptr[L];
+    int rc = launch_ilu_level(n, sz, level_rows + b, indptr, indices, F, DX, DP, S(stream));
+    if (rc) return rc;
+    rc = launch_inverse(n, sz, F, DX, DP, S(stream), status_ptr(), level_diag + b, level_rows + b, 4);
+    if (rc) return rc;
+    g_launches += 2;
+  }
+  return 0;
+}
+
+PMGB_API int pmgb_ilu0_apply(int64_t n_rows, int32_t sz, const int32_t* indptr, const int32_t* indices,
+                              const double* F, const double* DX, const uint8_t* DP, int32_t n_lo,
+                              const int64_t* lo_ptr, const int32_t* lo_rows, int32_t n_up, const int64_t* up_ptr,
+                              const int32_t* up_rows, const double* x, double* y, double* out, void* stream) {
+  if (!indptr || !indices || !F || !DX || !DP || !x || !y || !out) return -1;
+  (void)n_rows;
+  for (int32_t L = 0; L < n_lo; ++L) {
+    const int64_t b = lo_ptr[L], n = lo_ptr[L + 1] - lo_ptr[L];
+    int rc = launch_ilu_sweep(0, n, sz, lo_rows + b, indptr, indices, F, DX, DP, x, y, S(stream));
+    if (rc) return rc;
+  }
+  for (int32_t L = 0; L < n_up; ++L) {
+    const int64_t b = up_ptr[L], n = up_ptr[L + 1] - up_ptr[L];
+    int rc = launch_ilu_sweep(1, n, sz, up_rows + b, indptr, indices, F, DX, DP, y, out, S(stream));
+    if (rc) return rc;
+  }
+  g_launches += n_lo + n_up;
+  return 0;
 }
 
 PMGB_API int pmgb_ej_apply(int64_t M, int32_t sz, const double* XT, const uint8_t* perm, const double* x, double* y,

@@ -49,20 +49,23 @@ template <int SZ> struct GJShape {
 // the pivot row's multiplier is 1).
 template <int SZ>
 __global__ void __launch_bounds__(GJShape<SZ>::THREADS, (GJShape<SZ>::THREADS <= 256 ? 2 : 1))
-k_gj_inverse(const double* __restrict__ BT, double* __restrict__ XT, uint8_t* __restrict__ perm, Status* st) {
+k_gj_inverse(const double* __restrict__ BT, double* __restrict__ XT, uint8_t* __restrict__ perm, Status* st,
+             const int* __restrict__ in_slot, const int* __restrict__ out_idx, int bad_kind) {
   using S = GJShape<SZ>;
   constexpr int TR = S::TR, TC = S::TC, NRG = S::NRG, NCG = S::NCG, RPL = S::ROWS_PER_LANE;
   __shared__ double colbuf[2][SZ];
   __shared__ double rowbuf[2][SZ];
   __shared__ int pivs[SZ];
   __shared__ int s_bad;
-  const int64_t e = blockIdx.x;
+  // optional gather / scatter: block in_slot[b] of BT -> factor out_idx[b]
+  const int64_t e = out_idx ? (int64_t)out_idx[blockIdx.x] : (int64_t)blockIdx.x;
+  const int64_t e_in = in_slot ? (int64_t)in_slot[blockIdx.x] : (int64_t)blockIdx.x;
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const bool active = tid < NRG * NCG;
   const int rg = tid % NRG, cg = tid / NRG;
   const int r0 = rg * TR, c0 = cg * TC;
-  const double* src = BT + e * (int64_t)SZ * SZ;
+  const double* src = BT + e_in * (int64_t)SZ * SZ;
   double a[TR][TC];
 #pragma unroll
   for (int j = 0; j < TC; ++j) {
@@ -165,7 +168,7 @@ k_gj_inverse(const double* __restrict__ BT, double* __restrict__ XT, uint8_t* __
   }
   __syncthreads();
   if (tid == 0 && s_bad && st != nullptr) {
-    if (atomicCAS(&st->kind, 0, 3) == 0) st->element = e;
+    if (atomicCAS(&st->kind, 0, bad_kind) == 0) st->element = e;
   }
   double* dst = XT + e * (int64_t)SZ * SZ;
   if (active) {
@@ -320,25 +323,205 @@ int launch_sparse_matvec(int64_t n_rows, int SZ, const int* indptr, const int* i
   return (int)cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// Block ILU0 with zero fill (ilu0_factor / ilu0_apply, newton_krylov.py:
+// 319-368), level-scheduled: the host groups rows into levels of the
+// lower-neighbour DAG (factor, forward sweep) and of the upper-neighbour
+// DAG (backward sweep); rows of one level are independent and each row
+// does exactly the reference's sequence of block operations.  Blocks are
+// column-major (B[c*SZ + r] = B[r][c]); the inverted pivot blocks are kept
+// in Gauss-Jordan factor form (XT, perm): Dinv[t][c] = XT[q_c*SZ + p_t].
+
+// acc[i][j] = sum_t A[r0+i][t] B[t][c0+j]   (t ascending)
+template <int SZ, bool BPERM>
+__device__ __forceinline__ void tile_gemm(const double* __restrict__ A, const double* __restrict__ B,
+                                          const uint8_t* __restrict__ perm, int r0, int c0,
+                                          double (&acc)[GJShape<SZ>::TR][GJShape<SZ>::TC]) {
+  constexpr int TR = GJShape<SZ>::TR, TC = GJShape<SZ>::TC;
+#pragma unroll
+  for (int i = 0; i < TR; ++i)
+#pragma unroll
+    for (int j = 0; j < TC; ++j) acc[i][j] = 0.0;
+  int qc[TC];
+#pragma unroll
+  for (int j = 0; j < TC; ++j) qc[j] = (c0 + j < SZ) ? (BPERM ? (int)perm[SZ + c0 + j] : c0 + j) : 0;
+  for (int t = 0; t < SZ; ++t) {
+    const int pt = BPERM ? (int)perm[t] : t;
+    double a[TR], b[TC];
+#pragma unroll
+    for (int i = 0; i < TR; ++i) a[i] = (r0 + i < SZ) ? A[t * SZ + r0 + i] : 0.0;
+#pragma unroll
+    for (int j = 0; j < TC; ++j) b[j] = (c0 + j < SZ) ? B[qc[j] * SZ + pt] : 0.0;
+#pragma unroll
+    for (int i = 0; i < TR; ++i)
+#pragma unroll
+      for (int j = 0; j < TC; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+  }
+}
+
+// One CTA per row i of the level: for every lower entry k (column kk < i,
+// ascending): F_k <- F_k Dinv_kk, then F_k2 -= F_k F_(kk,j) for the row's
+// entries k2 with column j > kk present in row kk.
 template <int SZ>
-static int run_gj(int64_t M, const double* BT, double* XT, uint8_t* perm, cudaStream_t st, Status* stp) {
-  k_gj_inverse<SZ><<<(unsigned)M, GJShape<SZ>::THREADS, 0, st>>>(BT, XT, perm, stp);
+__global__ void __launch_bounds__(GJShape<SZ>::THREADS)
+k_ilu_level(const int* __restrict__ rows, const int* __restrict__ indptr, const int* __restrict__ indices,
+            double* __restrict__ F, const double* __restrict__ DX, const uint8_t* __restrict__ DP) {
+  using S = GJShape<SZ>;
+  constexpr int TR = S::TR, TC = S::TC, NRG = S::NRG;
+  const int i = rows[blockIdx.x];
+  const int tid = threadIdx.x;
+  const bool active = tid < NRG * S::NCG;
+  const int r0 = (tid % NRG) * TR, c0 = (tid / NRG) * TC;
+  const int lo = indptr[i], hi = indptr[i + 1];
+  constexpr int64_t BB = (int64_t)SZ * SZ;
+  double acc[TR][TC];
+  for (int k = lo; k < hi; ++k) {
+    const int kk = indices[k];
+    if (kk >= i) break;  // columns are sorted: the lower entries come first
+    double* Fk = F + k * BB;
+    if (active) tile_gemm<SZ, true>(Fk, DX + kk * BB, DP + (int64_t)kk * 2 * SZ, r0, c0, acc);
+    __syncthreads();  // every read of F_k done before it is overwritten
+    if (active) {
+#pragma unroll
+      for (int j = 0; j < TC; ++j)
+#pragma unroll
+        for (int ii = 0; ii < TR; ++ii)
+          if (r0 + ii < SZ && c0 + j < SZ) Fk[(c0 + j) * SZ + r0 + ii] = acc[ii][j];
+    }
+    __syncthreads();
+    const int klo = indptr[kk], khi = indptr[kk + 1];
+    for (int k2 = lo; k2 < hi; ++k2) {
+      const int j2 = indices[k2];
+      if (j2 <= kk) continue;
+      int u = -1;
+      for (int t = klo; t < khi; ++t)
+        if (indices[t] == j2) u = t;
+      if (u < 0) continue;
+      if (active) {
+        tile_gemm<SZ, false>(Fk, F + u * BB, nullptr, r0, c0, acc);
+        double* Fk2 = F + k2 * BB;
+#pragma unroll
+        for (int j = 0; j < TC; ++j)
+#pragma unroll
+          for (int ii = 0; ii < TR; ++ii)
+            if (r0 + ii < SZ && c0 + j < SZ) {
+              double* x = Fk2 + (c0 + j) * SZ + r0 + ii;
+              *x = *x - acc[ii][j];
+            }
+      }
+    }
+    __syncthreads();  // row blocks final before the next lower entry reads them
+  }
+}
+
+// forward sweep, unit lower factor: y_i = x_i - sum_{j<i} F_k y_j
+__global__ void __launch_bounds__(128)
+k_ilu_forward(int SZ, const int* __restrict__ rows, const int* __restrict__ indptr,
+              const int* __restrict__ indices, const double* __restrict__ F, const double* __restrict__ x,
+              double* __restrict__ y) {
+  const int i = rows[blockIdx.x];
+  const int64_t BB = (int64_t)SZ * SZ;
+  for (int r = threadIdx.x; r < SZ; r += blockDim.x) {
+    double acc = x[(int64_t)i * SZ + r];
+    for (int k = indptr[i]; k < indptr[i + 1]; ++k) {
+      const int j = indices[k];
+      if (j >= i) break;
+      const double* A = F + k * BB + r;
+      const double* yj = y + (int64_t)j * SZ;
+      double s = 0.0;
+      for (int c = 0; c < SZ; ++c) s = fma(A[(int64_t)c * SZ], yj[c], s);
+      acc -= s;
+    }
+    y[(int64_t)i * SZ + r] = acc;
+  }
+}
+
+// backward sweep: out_i = Dinv_i (y_i - sum_{j>i} F_k out_j)
+__global__ void __launch_bounds__(128)
+k_ilu_backward(int SZ, const int* __restrict__ rows, const int* __restrict__ indptr,
+               const int* __restrict__ indices, const double* __restrict__ F, const double* __restrict__ DX,
+               const uint8_t* __restrict__ DP, const double* __restrict__ y, double* __restrict__ out) {
+  extern __shared__ double sacc[];
+  const int i = rows[blockIdx.x];
+  const int64_t BB = (int64_t)SZ * SZ;
+  for (int r = threadIdx.x; r < SZ; r += blockDim.x) {
+    double acc = y[(int64_t)i * SZ + r];
+    for (int k = indptr[i]; k < indptr[i + 1]; ++k) {
+      const int j = indices[k];
+      if (j <= i) continue;
+      const double* A = F + k * BB + r;
+      const double* oj = out + (int64_t)j * SZ;
+      double s = 0.0;
+      for (int c = 0; c < SZ; ++c) s = fma(A[(int64_t)c * SZ], oj[c], s);
+      acc -= s;
+    }
+    sacc[r] = acc;
+  }
+  __syncthreads();
+  const double* XT = DX + (int64_t)i * BB;
+  const uint8_t* pp = DP + (int64_t)i * 2 * SZ;
+  for (int r = threadIdx.x; r < SZ; r += blockDim.x) {
+    double s = 0.0;
+    for (int c = 0; c < SZ; ++c) s = fma(XT[(int64_t)c * SZ + r], sacc[pp[c]], s);
+    out[(int64_t)i * SZ + pp[SZ + r]] = s;
+  }
+}
+
+template <int SZ>
+static int run_ilu_level(int64_t n, const int* rows, const int* indptr, const int* indices, double* F,
+                         const double* DX, const uint8_t* DP, cudaStream_t st) {
+  k_ilu_level<SZ><<<(unsigned)n, GJShape<SZ>::THREADS, 0, st>>>(rows, indptr, indices, F, DX, DP);
+  return (int)cudaGetLastError();
+}
+
+int launch_ilu_level(int64_t n, int SZ, const int* rows, const int* indptr, const int* indices, double* F,
+                     const double* DX, const uint8_t* DP, cudaStream_t st) {
+  if (n <= 0) return 0;
+  switch (SZ) {
+    case 1: return run_ilu_level<1>(n, rows, indptr, indices, F, DX, DP, st);
+    case 4: return run_ilu_level<4>(n, rows, indptr, indices, F, DX, DP, st);
+    case 9: return run_ilu_level<9>(n, rows, indptr, indices, F, DX, DP, st);
+    case 16: return run_ilu_level<16>(n, rows, indptr, indices, F, DX, DP, st);
+    case 25: return run_ilu_level<25>(n, rows, indptr, indices, F, DX, DP, st);
+    case 36: return run_ilu_level<36>(n, rows, indptr, indices, F, DX, DP, st);
+    case 64: return run_ilu_level<64>(n, rows, indptr, indices, F, DX, DP, st);
+    case 100: return run_ilu_level<100>(n, rows, indptr, indices, F, DX, DP, st);
+    case 144: return run_ilu_level<144>(n, rows, indptr, indices, F, DX, DP, st);
+  }
+  return -1000;
+}
+
+int launch_ilu_sweep(int backward, int64_t n, int SZ, const int* rows, const int* indptr, const int* indices,
+                     const double* F, const double* DX, const uint8_t* DP, const double* in, double* out,
+                     cudaStream_t st) {
+  if (n <= 0) return 0;
+  if (backward)
+    k_ilu_backward<<<(unsigned)n, 128, sizeof(double) * SZ, st>>>(SZ, rows, indptr, indices, F, DX, DP, in, out);
+  else
+    k_ilu_forward<<<(unsigned)n, 128, 0, st>>>(SZ, rows, indptr, indices, F, in, out);
+  return (int)cudaGetLastError();
+}
+
+template <int SZ>
+static int run_gj(int64_t M, const double* BT, double* XT, uint8_t* perm, cudaStream_t st, Status* stp,
+                  const int* in_slot, const int* out_idx, int bad_kind) {
+  k_gj_inverse<SZ><<<(unsigned)M, GJShape<SZ>::THREADS, 0, st>>>(BT, XT, perm, stp, in_slot, out_idx, bad_kind);
   return (int)cudaGetLastError();
 }
 
 int launch_inverse(int64_t M, int SZ, const double* BT, double* XT, uint8_t* perm, cudaStream_t st,
-                   Status* stp) {
+                   Status* stp, const int* in_slot, const int* out_idx, int bad_kind) {
   if (M <= 0) return 0;
   switch (SZ) {
-    case 1: return run_gj<1>(M, BT, XT, perm, st, stp);
-    case 4: return run_gj<4>(M, BT, XT, perm, st, stp);
-    case 9: return run_gj<9>(M, BT, XT, perm, st, stp);
-    case 16: return run_gj<16>(M, BT, XT, perm, st, stp);
-    case 25: return run_gj<25>(M, BT, XT, perm, st, stp);
-    case 36: return run_gj<36>(M, BT, XT, perm, st, stp);
-    case 64: return run_gj<64>(M, BT, XT, perm, st, stp);
-    case 100: return run_gj<100>(M, BT, XT, perm, st, stp);
-    case 144: return run_gj<144>(M, BT, XT, perm, st, stp);
+    case 1: return run_gj<1>(M, BT, XT, perm, st, stp, in_slot, out_idx, bad_kind);
+    case 4: return run_gj<4>(M, BT, XT, perm, st, stp, in_slot, out_idx, bad_kind);
+    case 9: return run_gj<9>(M, BT, XT, perm, st, stp, in_slot, out_idx, bad_kind);
+    case 16: return run_gj<16>(M, BT, XT, perm, st, stp, in_slot, out_idx, bad_kind);
+    case 25: return run_gj<25>(M, BT, XT, perm, st, stp, in_slot, out_idx, bad_kind);
+    case 36: return run_gj<36>(M, BT, XT, perm, st, stp, in_slot, out_idx, bad_kind);
+    case 64: return run_gj<64>(M, BT, XT, perm, st, stp, in_slot, out_idx, bad_kind);
+    case 100: return run_gj<100>(M, BT, XT, perm, st, stp, in_slot, out_idx, bad_kind);
+    case 144: return run_gj<144>(M, BT, XT, perm, st, stp, in_slot, out_idx, bad_kind);
   }
   return -1000;
 }

@@ -281,9 +281,29 @@ class _SparsePattern:
         nw = int(max(pw) + 1) if pw else 0
         self.wave_ptr = np.concatenate([[0], np.cumsum(np.bincount(np.asarray(pw, dtype=np.int64),
                                                                     minlength=nw))]).astype(np.int64)
+        # level schedules of the ILU0 sweeps: level(i) = 1 + max level of the
+        # row's lower (upper) neighbours -- rows of one level are independent
+        lo_lev = np.zeros(M, dtype=np.int64)
+        for i in range(M):
+            cols = self.indices[self.indptr[i]:self.indptr[i + 1]]
+            low = cols[cols < i]
+            lo_lev[i] = 1 + lo_lev[low].max() if low.size else 0
+        up_lev = np.zeros(M, dtype=np.int64)
+        for i in range(M - 1, -1, -1):
+            cols = self.indices[self.indptr[i]:self.indptr[i + 1]]
+            high = cols[cols > i]
+            up_lev[i] = 1 + up_lev[high].max() if high.size else 0
+
+        def schedule(lev):
+            order = np.argsort(lev, kind="stable")
+            ptr = np.concatenate([[0], np.cumsum(np.bincount(lev, minlength=int(lev.max()) + 1 if M else 0))])
+            return order.astype(np.int32), ptr.astype(np.int64)
+        self.lo_rows, self.lo_ptr = schedule(lo_lev)
+        self.up_rows, self.up_ptr = schedule(up_lev)
+        self.lo_diag = self.diag_slot[self.lo_rows].astype(np.int32)
         dev = disc.device
         self.d = {name: torch.as_tensor(np.ascontiguousarray(getattr(self, name)), device=dev)
-                  for name in ("pair_e", "pair_f", "pair_slot", "pair_add")}
+                  for name in ("pair_e", "pair_f", "pair_slot", "pair_add", "lo_rows", "up_rows", "lo_diag")}
         self.d["diag_slot"] = torch.as_tensor(self.diag_slot.astype(np.int32), device=dev)
         self.d["indptr"] = torch.as_tensor(self.indptr.astype(np.int32), device=dev)
         self.d["indices"] = torch.as_tensor(self.indices.astype(np.int32), device=dev)
@@ -360,6 +380,57 @@ def assemble_sparse_blocks(disc: Discretization, data, shift: float, frozen=None
                                       d["pair_f"].data_ptr(), d["pair_slot"].data_ptr(), d["pair_add"].data_ptr(),
                                       wave_ptr.ctypes.data, len(wave_ptr) - 1, stream()), "sparse_assemble")
     return SparseBlockMatrix(disc, pat, blocksT)
+
+
+class Ilu0Factors:
+    """Block ILU0 factors on A's pattern (newton_krylov.py:314-316): ``F``
+    the factored CSR values (column-major blocks), the pivot-block
+    inverses as Gauss-Jordan factors (DX, DP)."""
+
+    def __init__(self, pattern: SparseBlockMatrix, DX: torch.Tensor, DP: torch.Tensor):
+        self.pattern = pattern
+        self.DX = DX
+        self.DP = DP
+
+    @property
+    def diag_inv(self):
+        return BlockJacobian(self.pattern.disc, 0.0, self.DX, self.DP).inv[0]
+
+
+def ilu0_factor(A: SparseBlockMatrix) -> Ilu0Factors:
+    """Block ILU with zero fill on A's own pattern (newton_krylov.py:319-345),
+    level-scheduled on the device.  Raises RuntimeError("singular ILU0 pivot
+    block at element i")."""
+    disc, pat = A.disc, A.pattern
+    sz, M = disc.elem_size, A.n
+    F = A.blocksT.clone()
+    DX = torch.empty((M, sz, sz), dtype=torch.float64, device=disc.device)
+    DP = torch.empty((M, 2 * sz), dtype=torch.uint8, device=disc.device)
+    d = pat.d
+    lp = np.ascontiguousarray(pat.lo_ptr, dtype=np.int64)
+    check(load().pmgb_ilu0_factor(M, sz, d["indptr"].data_ptr(), d["indices"].data_ptr(), F.data_ptr(),
+                                  DX.data_ptr(), DP.data_ptr(), len(lp) - 1, lp.ctypes.data,
+                                  d["lo_rows"].data_ptr(), d["lo_diag"].data_ptr(), stream()), "ilu0_factor")
+    raise_status()
+    return Ilu0Factors(SparseBlockMatrix(disc, pat, F), DX, DP)
+
+
+def ilu0_apply(fac: Ilu0Factors, X, offsets=None):
+    """Solve LU y = X with the incomplete factors (newton_krylov.py:348-368)."""
+    Fm = fac.pattern
+    disc, pat = Fm.disc, Fm.pattern
+    is_np = not isinstance(X, torch.Tensor)
+    Xd = to_device(X, disc.device)
+    y = torch.empty_like(Xd)
+    out = torch.empty_like(Xd)
+    d = pat.d
+    lp = np.ascontiguousarray(pat.lo_ptr, dtype=np.int64)
+    up = np.ascontiguousarray(pat.up_ptr, dtype=np.int64)
+    check(load().pmgb_ilu0_apply(Fm.n, disc.elem_size, d["indptr"].data_ptr(), d["indices"].data_ptr(),
+                                 Fm.blocksT.data_ptr(), fac.DX.data_ptr(), fac.DP.data_ptr(), len(lp) - 1,
+                                 lp.ctypes.data, d["lo_rows"].data_ptr(), len(up) - 1, up.ctypes.data,
+                                 d["up_rows"].data_ptr(), ptr(Xd), ptr(y), ptr(out), stream()), "ilu0_apply")
+    return out.cpu().numpy() if is_np else out
 
 
 def assemble_element_blocks(disc: Discretization, data, shift: float, frozen=None, eps: float = FD_EPS,

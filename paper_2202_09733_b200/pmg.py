@@ -8,11 +8,13 @@ line for line; vectors live on the device:
 * ``LevelState.F`` / ``defect``                  :142-159 -> fused R epilogues
 * ``smooth_ej``                                  :162-164 -> defect kernel chain +
                                                  fused block-GEMV update
-* ``PmgContext.prepare/vcycle/precondition``     :181-298
+* ``smooth_mbnk``                                :167-175 -> GMRES on the device
+                                                 block-sparse Jacobian + block ILU0
+* ``PmgContext.prepare/vcycle/precondition``     :181-298 (incl. switch_after,
+                                                 _ensure_sparse :213-253)
 * ``pmg_solve``                                  :308-374
 
-Uniform-degree levels only; the MBNK smoother and ``switch_after``
-(:167-175, :215-219, :239-243) are outside this round.
+Uniform-degree levels only (mixed degrees: SURVEY 8(f) rank 3).
 """
 
 from __future__ import annotations
@@ -130,6 +132,8 @@ class LevelState:
         self.smoother = smoother
         self.blocks = blocks
         self.frozen_q = None
+        self.sparse = None  # SparseBlockMatrix (MBNK)
+        self.ilu = None     # Ilu0Factors (MBNK)
 
     def F(self, q) -> torch.Tensor:
         return self.disc.eval(to_device(q, self.disc.device), _lib.EPI_F, s=self.shift)
@@ -144,6 +148,16 @@ def smooth_ej(level: LevelState, n: int, omega: float = 1.0):
         level.q = level.blocks.update(level.defect(), omega, level.q)
 
 
+def smooth_mbnk(level: LevelState, rtol: float = 0.1, maxiter: int = 5):
+    """One Newton update with the assembled block matrix and ILU0
+    (pmg.py:167-175): GMRES(maxiter), one cycle, right-preconditioned by
+    the block ILU0 of the level's block-sparse Jacobian."""
+    r = level.defect()
+    cfg = nk.KrylovConfig(kdim=maxiter, max_restarts=1, rtol=rtol)
+    dq, _, _ = nk.gmres_solve(level.sparse.matvec, r, cfg, precond=lambda v: nk.ilu0_apply(level.ilu, v))
+    level.q = lincomb((1.0, 1.0), (level.q, dq))
+
+
 class PmgContext:
     """Level hierarchy, transfers and smoother state for one discretization."""
 
@@ -151,8 +165,6 @@ class PmgContext:
         self.disc = disc
         self.cfg = cfg
         h = cfg.hierarchy
-        if h.switch_after is not None or any(s != "ej" for s in h.smoothers):
-            raise NotImplementedError("MBNK smoothing is not on the device path yet (SURVEY 8(f))")
         if disc.p != h.levels[0]:
             raise NotImplementedError("device pMG needs the discretization at the hierarchy top degree")
         self.levels = []
@@ -183,12 +195,34 @@ class PmgContext:
             lev.frozen_q = qk
             lev.blocks = nk.assemble_element_blocks(lev.disc, qk, shift + self.cfg.smoother_shift,
                                                     keep_blocks=False)
+            lev.sparse = lev.ilu = None
         raise_status()
         self.cycles_done = 0
 
+    # -- smoother state (pmg.py:213-253) ----------------------------------
+
+    def _effective_smoother(self, k: int) -> str:
+        h = self.cfg.hierarchy
+        if h.switch_after is not None and self.cycles_done >= h.switch_after:
+            return "mbnk"
+        return h.smoothers[k]
+
+    def _ensure_sparse(self, lev: LevelState):
+        """Block-sparse Jacobian at the frozen state and the level's current
+        shift (no smoother_shift: that only damps the EJ blocks), and its
+        block ILU0 -- built on first MBNK use after prepare()."""
+        if lev.sparse is None:
+            lev.sparse = nk.assemble_sparse_blocks(lev.disc, lev.frozen_q, lev.shift)
+            lev.ilu = nk.ilu0_factor(lev.sparse)
+
     def _smooth(self, k: int):
         lev = self.levels[k]
-        smooth_ej(lev, lev.nsweeps, self.cfg.omega)
+        if self._effective_smoother(k) == "ej":
+            smooth_ej(lev, lev.nsweeps, self.cfg.omega)
+        else:
+            self._ensure_sparse(lev)
+            for _ in range(lev.nsweeps):
+                smooth_mbnk(lev, self.cfg.mbnk_rtol, self.cfg.mbnk_maxiter)
 
     def vcycle(self, k: int = 0):
         lev = self.levels[k]

@@ -40,7 +40,8 @@ __all__ = ["Discretization", "SolutionField", "FrozenState", "NonPhysicalStateEr
 def raise_status(clear: bool = True):
     """Synchronise and turn the device status word into the reference's
     exceptions: NonPhysicalStateError(element, what) (spatial.py:27-32,
-    439-446) or RuntimeError for a singular block (newton_krylov.py:207)."""
+    439-446) or RuntimeError for a singular block (newton_krylov.py:207) or
+    a singular ILU0 pivot block (newton_krylov.py:343)."""
     kind = ctypes.c_int32(0)
     elem = ctypes.c_int64(0)
     check(load().pmgb_status(stream(), ctypes.byref(kind), ctypes.byref(elem), int(clear)), "status")
@@ -50,6 +51,8 @@ def raise_status(clear: bool = True):
         raise NonPhysicalStateError(elem.value, "trace")
     if kind.value == 3:
         raise RuntimeError(f"singular Jacobi block for element {elem.value}")
+    if kind.value == 4:
+        raise RuntimeError(f"singular ILU0 pivot block at element {elem.value}")
 
 
 def clear_status():

@@ -46,3 +46,58 @@ def test_sparse_blocks_match_reference(cuda, name):
     assert np.array_equal(A.indptr, G[pre + "indptr"]) and np.array_equal(A.indices, G[pre + "indices"])
     assert scaled(A.blocks, G[pre + "blocks"]) <= 1e-7
     assert scaled(A.matvec(t(G[pre + "X"])), G[pre + "AX"]) <= 1e-7
+
+
+@pytest.mark.parametrize("name", list(SPARSE_CASES))
+def test_ilu0_factor_and_apply_match_reference(cuda, name):
+    mk, kw, p = SPARSE_CASES[name]
+    d = Discretization(mk(), p, EquationSpec(**kw))
+    pre = f"sp/{name}/"
+    A = nk.assemble_sparse_blocks(d, t(G[pre + "q"]), 40.0)
+    fac = nk.ilu0_factor(A)
+    assert scaled(fac.pattern.blocks, G[pre + "lu"]) <= 1e-6
+    assert scaled(fac.diag_inv, G[pre + "dinv"]) <= 1e-6
+    assert scaled(nk.ilu0_apply(fac, t(G[pre + "X"])), G[pre + "iluX"]) <= 1e-6
+
+
+@pytest.mark.parametrize("kinds", ["mbnk", "ej-mbnk"])
+def test_mbnk_precondition_matches_reference(cuda, kinds):
+    from paper_2202_09733_b200 import pmg
+    c = cases.config(1, nx=4)
+    d = Discretization(c.mesh, 3, c.eqn)
+    ctx = pmg.PmgContext(d, pmg.PmgPrecondConfig(pmg.PHierarchy.parse("3-2", "1", kinds), smoother_shift=50.0))
+    ctx.prepare(t(G["mb/q"]), float(G["mb/shift"]))
+    assert scaled(ctx.precondition(t(G["mb/v"])), G[f"mb/{kinds}/Y"]) <= 1e-6
+
+
+def test_switch_after_pmg_solve_matches_reference(cuda):
+    from paper_2202_09733_b200 import pmg
+    c = cases.config(1, nx=4)
+    d = Discretization(c.mesh, 3, c.eqn)
+    h = pmg.PHierarchy.parse("3-2", "1", "ej", switch_after=1)
+    ctx = pmg.PmgContext(d, pmg.PmgPrecondConfig(h, smoother_shift=50.0))
+    q, st = pmg.pmg_solve(ctx, t(G["sw/q0"]), nk.PtcConfig(dtau_init=0.05, max_iters=3, rtol=1e-12))
+    hist, ref = np.array(st["history"]), G["sw/history"]
+    assert hist.shape == ref.shape
+    assert np.allclose(hist[:, 1], ref[:, 1], rtol=1e-5)
+    assert scaled(q, G["sw/q"]) <= 1e-7
+
+
+def test_mbnk_driver_step_matches_oracle(cuda):
+    # an ESDIRK2 step with MBNK smoothing on the coarse level, device vs oracle
+    from oracle import solver_oracle as so
+    from oracle.fr_oracle import OracleDisc
+    from paper_2202_09733_b200 import time_integration as ti
+    from paper_2202_09733_b200.harness import ImplicitDriver
+    c = cases.config(1, nx=4)
+    d = Discretization(c.mesh, 3, c.eqn)
+    o = OracleDisc(c.mesh, 3, c.eqn)
+    cfg = {"case.precond": "pmg", "pmg.levels": "3-2", "pmg.smooth": "1", "pmg.smoother": "ej-mbnk",
+           "pmg.smoother_shift": 50.0, "gmres.rtol": 1e-3, "ptc.dtau_init": c.dt}
+    s = ti.get_scheme("esdirk2")
+    q1, info = ImplicitDriver(d, cfg).step(t(c.q0), c.dt, s)
+    drv = so.Driver(o, "pmg", "3-2", 1, smoother_shift=50.0, gmres_rtol=1e-3, dtau_init=c.dt)
+    drv.ctx = so.Pmg(o, "3-2", 1, smoother_shift=50.0, smoother="ej-mbnk")
+    q1_o = drv.esdirk_step(c.q0, c.dt, s.a, s.b)
+    assert [i["iters"] for i in info] == [r[1] for r in drv.records]
+    assert scaled(q1, q1_o) <= 1e-7
