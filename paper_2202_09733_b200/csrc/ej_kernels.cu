@@ -414,56 +414,119 @@ k_ilu_level(const int* __restrict__ rows, const int* __restrict__ indptr, const 
   }
 }
 
-// forward sweep, unit lower factor: y_i = x_i - sum_{j<i} F_k y_j
-__global__ void __launch_bounds__(128)
-k_ilu_forward(int SZ, const int* __restrict__ rows, const int* __restrict__ indptr,
-              const int* __restrict__ indices, const double* __restrict__ F, const double* __restrict__ x,
-              double* __restrict__ y) {
-  const int i = rows[blockIdx.x];
-  const int64_t BB = (int64_t)SZ * SZ;
-  for (int r = threadIdx.x; r < SZ; r += blockDim.x) {
-    double acc = x[(int64_t)i * SZ + r];
-    for (int k = indptr[i]; k < indptr[i + 1]; ++k) {
-      const int j = indices[k];
-      if (j >= i) break;
-      const double* A = F + k * BB + r;
-      const double* yj = y + (int64_t)j * SZ;
-      double s = 0.0;
-      for (int c = 0; c < SZ; ++c) s = fma(A[(int64_t)c * SZ], yj[c], s);
-      acc -= s;
+// Sweeps.  One CTA per row of the level; the row's CSR entries go to
+// shared memory first so that every block-row product of the row is issued
+// at once (compile-time SZ, entries bounded by MAXNZ): the chain of
+// dependent global loads is what bounds these tiny kernels.
+constexpr int ILU_MAXNZ = 9;  // diagonal + at most 4 face neighbours (+ headroom)
+
+// sum_c A[c][r] v[c] (column-major A offset to row r), loads batched ahead
+// of their FMAs (12 in flight) -- the FMA order stays c ascending
+template <int SZ>
+__device__ __forceinline__ double dot_col(const double* __restrict__ A, const double* v) {
+  constexpr int CH = 12;
+  double s = 0.0;
+#pragma unroll
+  for (int c0 = 0; c0 < SZ; c0 += CH) {
+    double a[CH], b[CH];
+#pragma unroll
+    for (int u = 0; u < CH; ++u) {
+      if (c0 + u < SZ) {
+        a[u] = __ldg(A + (c0 + u) * SZ);
+        b[u] = v[c0 + u];
+      }
     }
-    y[(int64_t)i * SZ + r] = acc;
+#pragma unroll
+    for (int u = 0; u < CH; ++u)
+      if (c0 + u < SZ) s = fma(a[u], b[u], s);
   }
+  return s;
+}
+
+template <int SZ, bool UPPER>
+__device__ __forceinline__ double ilu_row_sum(int i, int r, const int* __restrict__ indptr,
+                                              const int* __restrict__ indices, const double* __restrict__ F,
+                                              const double* __restrict__ v, int* sk, int* sj, int& nsel,
+                                              double base) {
+  if (threadIdx.x == 0) {
+    const int lo = indptr[i], hi = indptr[i + 1];
+    int n = 0;
+    for (int k = lo; k < hi && n < ILU_MAXNZ; ++k) {
+      const int j = indices[k];
+      if (UPPER ? (j > i) : (j < i)) {
+        sk[n] = k;
+        sj[n] = j;
+        ++n;
+      }
+    }
+    sk[ILU_MAXNZ] = n;
+  }
+  __syncthreads();
+  nsel = sk[ILU_MAXNZ];
+  constexpr int64_t BB = (int64_t)SZ * SZ;
+  double part[ILU_MAXNZ];
+#pragma unroll
+  for (int e = 0; e < ILU_MAXNZ; ++e) {
+    part[e] = 0.0;
+    if (e < nsel && r < SZ) {
+      part[e] = dot_col<SZ>(F + sk[e] * BB + r, v + (int64_t)sj[e] * SZ);
+    }
+  }
+  // subtract in the row's column order, as acc -= block @ v_j does
+  double acc = base;
+#pragma unroll
+  for (int e = 0; e < ILU_MAXNZ; ++e)
+    if (e < nsel) acc -= part[e];
+  return acc;
+}
+
+// forward sweep, unit lower factor: y_i = x_i - sum_{j<i} F_k y_j
+template <int SZ>
+__global__ void __launch_bounds__((SZ + 31) / 32 * 32)
+k_ilu_forward(const int* __restrict__ rows, const int* __restrict__ indptr, const int* __restrict__ indices,
+              const double* __restrict__ F, const double* __restrict__ x, double* __restrict__ y) {
+  __shared__ int sk[ILU_MAXNZ + 1], sj[ILU_MAXNZ];
+  const int i = rows[blockIdx.x];
+  const int r = threadIdx.x;
+  int nsel;
+  const double xr = r < SZ ? x[(int64_t)i * SZ + r] : 0.0;
+  const double acc = ilu_row_sum<SZ, false>(i, r, indptr, indices, F, y, sk, sj, nsel, xr);
+  if (r < SZ) y[(int64_t)i * SZ + r] = acc;
 }
 
 // backward sweep: out_i = Dinv_i (y_i - sum_{j>i} F_k out_j)
-__global__ void __launch_bounds__(128)
-k_ilu_backward(int SZ, const int* __restrict__ rows, const int* __restrict__ indptr,
-               const int* __restrict__ indices, const double* __restrict__ F, const double* __restrict__ DX,
-               const uint8_t* __restrict__ DP, const double* __restrict__ y, double* __restrict__ out) {
-  extern __shared__ double sacc[];
+template <int SZ>
+__global__ void __launch_bounds__((SZ + 31) / 32 * 32)
+k_ilu_backward(const int* __restrict__ rows, const int* __restrict__ indptr, const int* __restrict__ indices,
+               const double* __restrict__ F, const double* __restrict__ DX, const uint8_t* __restrict__ DP,
+               const double* __restrict__ y, double* __restrict__ out) {
+  __shared__ int sk[ILU_MAXNZ + 1], sj[ILU_MAXNZ];
+  __shared__ double sacc[SZ];
+  __shared__ uint8_t sp[2 * SZ];
   const int i = rows[blockIdx.x];
-  const int64_t BB = (int64_t)SZ * SZ;
-  for (int r = threadIdx.x; r < SZ; r += blockDim.x) {
-    double acc = y[(int64_t)i * SZ + r];
-    for (int k = indptr[i]; k < indptr[i + 1]; ++k) {
-      const int j = indices[k];
-      if (j <= i) continue;
-      const double* A = F + k * BB + r;
-      const double* oj = out + (int64_t)j * SZ;
-      double s = 0.0;
-      for (int c = 0; c < SZ; ++c) s = fma(A[(int64_t)c * SZ], oj[c], s);
-      acc -= s;
-    }
-    sacc[r] = acc;
-  }
+  const int r = threadIdx.x;
+  constexpr int64_t BB = (int64_t)SZ * SZ;
+  for (int t = r; t < 2 * SZ; t += blockDim.x) sp[t] = DP[(int64_t)i * 2 * SZ + t];
+  int nsel;
+  const double yr = r < SZ ? y[(int64_t)i * SZ + r] : 0.0;
+  const double acc = ilu_row_sum<SZ, true>(i, r, indptr, indices, F, out, sk, sj, nsel, yr);
+  if (r < SZ) sacc[r] = acc;
   __syncthreads();
-  const double* XT = DX + (int64_t)i * BB;
-  const uint8_t* pp = DP + (int64_t)i * 2 * SZ;
-  for (int r = threadIdx.x; r < SZ; r += blockDim.x) {
+  if (r < SZ) {
+    const double* XT = DX + (int64_t)i * BB + r;
+    constexpr int CH = 12;
     double s = 0.0;
-    for (int c = 0; c < SZ; ++c) s = fma(XT[(int64_t)c * SZ + r], sacc[pp[c]], s);
-    out[(int64_t)i * SZ + pp[SZ + r]] = s;
+#pragma unroll
+    for (int c0 = 0; c0 < SZ; c0 += CH) {
+      double a[CH];
+#pragma unroll
+      for (int u = 0; u < CH; ++u)
+        if (c0 + u < SZ) a[u] = __ldg(XT + (c0 + u) * SZ);
+#pragma unroll
+      for (int u = 0; u < CH; ++u)
+        if (c0 + u < SZ) s = fma(a[u], sacc[sp[c0 + u]], s);
+    }
+    out[(int64_t)i * SZ + sp[SZ + r]] = s;
   }
 }
 
@@ -491,15 +554,28 @@ int launch_ilu_level(int64_t n, int SZ, const int* rows, const int* indptr, cons
   return -1000;
 }
 
+template <int SZ>
+static int run_ilu_sweep(int backward, int64_t n, const int* rows, const int* indptr, const int* indices,
+                         const double* F, const double* DX, const uint8_t* DP, const double* in, double* out,
+                         cudaStream_t st) {
+  constexpr int TH = (SZ + 31) / 32 * 32;
+  if (backward)
+    k_ilu_backward<SZ><<<(unsigned)n, TH, 0, st>>>(rows, indptr, indices, F, DX, DP, in, out);
+  else
+    k_ilu_forward<SZ><<<(unsigned)n, TH, 0, st>>>(rows, indptr, indices, F, in, out);
+  return (int)cudaGetLastError();
+}
+
 int launch_ilu_sweep(int backward, int64_t n, int SZ, const int* rows, const int* indptr, const int* indices,
                      const double* F, const double* DX, const uint8_t* DP, const double* in, double* out,
                      cudaStream_t st) {
   if (n <= 0) return 0;
-  if (backward)
-    k_ilu_backward<<<(unsigned)n, 128, sizeof(double) * SZ, st>>>(SZ, rows, indptr, indices, F, DX, DP, in, out);
-  else
-    k_ilu_forward<<<(unsigned)n, 128, 0, st>>>(SZ, rows, indptr, indices, F, in, out);
-  return (int)cudaGetLastError();
+  switch (SZ) {
+#define PMGB_SW(Z) case Z: return run_ilu_sweep<Z>(backward, n, rows, indptr, indices, F, DX, DP, in, out, st);
+    PMGB_SW(1) PMGB_SW(4) PMGB_SW(9) PMGB_SW(16) PMGB_SW(25) PMGB_SW(36) PMGB_SW(64) PMGB_SW(100) PMGB_SW(144)
+#undef PMGB_SW
+  }
+  return -1000;
 }
 
 template <int SZ>
