@@ -167,6 +167,14 @@ PMGB_API int pmgb_ilu0_apply(int64_t n_rows, int32_t sz, const int32_t* indptr, 
                               const int64_t* lo_ptr, const int32_t* lo_rows, int32_t n_up, const int64_t* up_ptr,
                               const int32_t* up_rows, const double* x, double* y, double* out, void* stream);
 
+/* compute_forces (spatial.py:633-695): per wall (element, face) pair the
+ * integrated force 2-vector  sum_k w_k face_jac (p n - tau n)  at state q
+ * (traces and BR1 gradients recomputed on the device), out (n_wall, 2);
+ * the caller sums the pairs (Fd, Fl) and forms the coefficients.  weights
+ * = the n Gauss weights (host array).  Flow kinds only (-5 otherwise). */
+PMGB_API int pmgb_wall_forces(pmgb_disc* d, const double* q, int64_t n_wall, const int32_t* wall_e,
+                              const int8_t* wall_f, const double* weights, double* out, void* stream);
+
 /* BlockJacobian.apply / ej_apply (newton_krylov.py:166-171, 213-214):
  * y_e = B_e^-1 x_e from (XT, perm).  pmgb_ej_update: out = base + omega *
  * B^-1 d (smooth_ej, pmg.py:162-164); out may alias base. */

@@ -17,7 +17,8 @@ Reference citations (``/root/reference/pkg/src/pmgflow/spatial.py``):
   _divergence 407-430, _transformed 432-437, _check_physical 439-446,
   _grad_vars 448-454, _one_sided_fvn 456-464, residual 501-570,
   _br1_gradient 594-603, _assemble 605-629, freeze 700-766,
-  element_residual 768-853, neighbor_face_record 855-903.
+  element_residual 768-853, neighbor_face_record 855-903,
+  compute_forces 633-695.
 """
 
 from __future__ import annotations
@@ -291,6 +292,48 @@ class OracleDisc:
             wall = (self.tag == WALL_ADIABATIC)[..., None]
             Fv[..., 3] = np.where(wall, 0.0, Fv[..., 3])
         return self._assemble(e, Q, Fc - Fv, grads).reshape(-1)
+
+    # -- forces (spatial.py:633-695) ------------------------------------------
+
+    def compute_forces(self, q):
+        """(Fd, Fl, Cd, Cl): pressure p n minus the BR1 viscous traction
+        tau n, integrated over the wall-tagged faces with the face weights
+        and face_jac; coefficients with the reference length as area."""
+        eqn = self.eqn
+        if eqn.kind == "advection-diffusion":
+            raise ValueError("forces are only defined for flow equations")
+        wall = (self.tag == WALL_ADIABATIC) | (self.tag == WALL_SLIP)
+        if not wall.any():
+            raise ValueError("mesh has no wall boundary faces")
+        n, nv = self.n, self.nv
+        Q = np.asarray(q, dtype=float).reshape(-1, n, n, nv)
+        tr = self._traces(Q)
+        grads = None
+        if eqn.viscous:
+            inter = self.interior[..., None, None]
+            nb_tr = np.where(inter, self._gather_nb(tr), self._ghosts(slice(None), tr))
+            What = 0.5 * (self._grad_vars(tr) + self._grad_vars(nb_tr))
+            grads = self._gradient(slice(None), self._grad_vars(Q), What)
+        from paper_2202_09733_b200.operators import gauss_rule
+        wq = gauss_rule(n)[1]
+        F = np.zeros(2)
+        for e, f in np.argwhere(wall):
+            t = tr[e, f]                                   # (n, 4)
+            nrm = self.nrm[e, f]
+            p = primitive(t, eqn.gamma)[3]
+            contrib = p[:, None] * nrm[None, :]
+            if grads is not None:
+                gx_tr = self._traces(grads[0][e])[f]
+                gy_tr = self._traces(grads[1][e])[f]
+                ux, vx, uy, vy = gx_tr[:, 0], gx_tr[:, 1], gy_tr[:, 0], gy_tr[:, 1]
+                div = ux + vy
+                txx = eqn.mu * (2 * ux - (2.0 / 3.0) * div)
+                tyy = eqn.mu * (2 * vy - (2.0 / 3.0) * div)
+                txy = eqn.mu * (uy + vx)
+                contrib = contrib - np.stack([txx * nrm[0] + txy * nrm[1], txy * nrm[0] + tyy * nrm[1]], axis=-1)
+            F += np.einsum("k,kj->j", wq * self.js[e, f], contrib)
+        qref = 0.5 * 1.0 * 1.0 ** 2 * eqn.ref_length
+        return F[0], F[1], F[0] / qref, F[1] / qref
 
     # -- the same residual on all host cores (bench.py's reference arm) -------
 

@@ -51,6 +51,7 @@ PMGB_API const char* pmgb_error_string(int code) {
     case -2: return "unsupported polynomial degree (0..5)";
     case -3: return "unsupported equation kind";
     case -4: return "mesh too large for one device context (face offsets exceed 2^31)";
+    case -5: return "forces are only defined for flow equations";
     case -1000: return "no kernel instance for this degree/kind";
     case -1001: return "vector count out of range";
   }
@@ -275,6 +276,15 @@ PMGB_API int pmgb_ilu0_apply(int64_t n_rows, int32_t sz, const int32_t* indptr, 
   }
   g_launches += n_lo + n_up;
   return 0;
+}
+
+PMGB_API int pmgb_wall_forces(pmgb_disc* h, const double* q, int64_t n_wall, const int32_t* wall_e,
+                              const int8_t* wall_f, const double* weights, double* out, void* stream) {
+  if (!h || !q || !weights || (n_wall > 0 && (!wall_e || !wall_f || !out))) return -1;
+  const DiscDev& d = h->d;
+  if (d.kind != K_EULER && d.kind != K_NS) return -5;
+  g_launches += (d.kind == K_NS) ? 3 : 2;
+  return launch_forces(d, q, n_wall, wall_e, (const signed char*)wall_f, weights, out, S(stream));
 }
 
 PMGB_API int pmgb_ej_apply(int64_t M, int32_t sz, const double* XT, const uint8_t* perm, const double* x, double* y,

@@ -2001,6 +2001,71 @@ k_coupling(const FrConst C, const FrMesh m, const double* __restrict__ q, const 
 }
 
 // ---------------------------------------------------------------------------
+// wall forces (compute_forces, spatial.py:633-695): thread per wall
+// (element, face); pressure p n minus the viscous traction tau n at every
+// face point, from the traces of q (qtr) and of k_fvn's BR1 point
+// gradients (padded block scratch), weighted by w_k * face_jac.  One
+// 2-vector per face; the host sums them in face order.
+struct FaceWeights {
+  double w[6];
+};
+
+template <int P, int KIND>
+__global__ void __launch_bounds__(128)
+k_wall_forces(const FrConst C, const FrMesh m, const double* __restrict__ qtr, const double* __restrict__ grad,
+              const int* __restrict__ wall_e, const signed char* __restrict__ wall_f, int64_t nwall,
+              const FaceWeights fw, double* __restrict__ out) {
+  using L = SL<P, KIND>;
+  constexpr int N = BC<P>::N, E = BC<P>::EPB, NW = KT<KIND>::NW;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nwall) return;
+  const int64_t e = wall_e[t];
+  const int f = wall_f[t];
+  const double* g = m.geom + e * 20;
+  const double nx = g[8 + 2 * f], ny = g[9 + 2 * f], js = g[16 + f];
+  const double* eline = (f == 0 || f == 3) ? C.eL : C.eR;
+  const int64_t blk = e / E;
+  const int el = (int)(e - blk * E);
+  const double* gb = grad + blk * (2 * NW * L::PS);
+  double Fx = 0.0, Fy = 0.0;
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    double q[4];
+    ld_face<4>(qtr + ((e * 4 + f) * N + k) * 4, q);
+    double r, ir, u, v, p;
+    prim(q, C.gamma, r, ir, u, v, p);
+    double cx = p * nx, cy = p * ny;
+    if constexpr (KT<KIND>::VISC) {
+      // face line of (f, k): points base + i * stride (face_line)
+      const int base = f == 0 ? k : f == 1 ? k * N : f == 2 ? (N - 1 - k) : (N - 1 - k) * N;
+      const int stride = (f == 0 || f == 2) ? N : 1;
+      double gt[2 * NW];
+#pragma unroll
+      for (int c = 0; c < 2 * NW; ++c) {
+        double s = 0.0;
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          const int pt = base + i * stride;
+          s += eline[i] * __ldg(gb + c * L::PS + L::pix(el, pt / N, pt % N));
+        }
+        gt[c] = s;
+      }
+      const double ux = gt[0], vx = gt[1], uy = gt[NW + 0], vy = gt[NW + 1];
+      const double div = ux + vy;
+      const double txx = C.mu * (2 * ux - (2.0 / 3.0) * div);
+      const double tyy = C.mu * (2 * vy - (2.0 / 3.0) * div);
+      const double txy = C.mu * (uy + vx);
+      cx = cx - (txx * nx + txy * ny);
+      cy = cy - (txy * nx + tyy * ny);
+    }
+    Fx += fw.w[k] * (js * cx);
+    Fy += fw.w[k] * (js * cy);
+  }
+  out[2 * t] = Fx;
+  out[2 * t + 1] = Fy;
+}
+
+// ---------------------------------------------------------------------------
 // host-side dispatch
 
 static __device__ int g_bad[2] = {INT_MAX, INT_MAX};
@@ -2131,6 +2196,34 @@ static int run_coupling(const DiscDev& d, const double* q, const double* qtr, co
   return (int)cudaGetLastError();
 }
 
+template <int P, int KIND>
+static int run_forces(const DiscDev& d, const double* q, int64_t nwall, const int* wall_e,
+                      const signed char* wall_f, const double* weights, double* out, cudaStream_t st) {
+  using L = SL<P, KIND>;
+  constexpr int E = BC<P>::EPB, TH = BC<P>::THREADS;
+  if constexpr (!KT<KIND>::FLOW) {
+    return -5;
+  } else {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_trace<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES_TRACE);
+      cudaFuncSetAttribute(k_fvn<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES_FVN);
+      attr = true;
+    }
+    const unsigned grid = (unsigned)((d.M + E - 1) / E);
+    const unsigned gl = (unsigned)((d.M * 2 * (P + 1) + 127) / 128);
+    k_trace_lines<P, KIND><<<gl, 128, 0, st>>>(d.C, d.mesh, q, nullptr, 0.0, nullptr, d.qtr, nullptr);
+    if constexpr (KT<KIND>::VISC)
+      k_fvn<P, KIND><<<grid, TH, L::BYTES_FVN, st>>>(d.C, d.mesh, q, d.qtr, d.fvn, d.grad, 0);
+    FaceWeights fw{};
+    for (int k = 0; k <= P; ++k) fw.w[k] = weights[k];
+    if (nwall > 0)
+      k_wall_forces<P, KIND><<<(unsigned)((nwall + 127) / 128), 128, 0, st>>>(d.C, d.mesh, d.qtr, d.grad, wall_e,
+                                                                               wall_f, nwall, fw, out);
+    return (int)cudaGetLastError();
+  }
+}
+
 #define PMGB_DISPATCH(FN, ...)                                              \
   switch (d.kind * 8 + d.p) {                                               \
     case K_EULER * 8 + 0: return FN<0, K_EULER>(__VA_ARGS__);               \
@@ -2196,6 +2289,11 @@ int launch_local_residual(const DiscDev& d, const int64_t* elems, int64_t B, con
 int launch_blocks(const DiscDev& d, const double* q, const double* qtr, const double* fvn, double shift,
                   double eps, double* BT, cudaStream_t st, const int* out_slot) {
   PMGB_DISPATCH(run_blocks, d, q, qtr, fvn, shift, eps, BT, out_slot, st)
+}
+
+int launch_forces(const DiscDev& d, const double* q, int64_t nwall, const int* wall_e, const signed char* wall_f,
+                  const double* weights, double* out, cudaStream_t st) {
+  PMGB_DISPATCH(run_forces, d, q, nwall, wall_e, wall_f, weights, out, st)
 }
 
 int launch_coupling(const DiscDev& d, const double* q, const double* qtr, const double* fvn, double eps,

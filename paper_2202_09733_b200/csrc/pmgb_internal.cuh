@@ -120,6 +120,8 @@ int launch_coupling(const DiscDev& d, const double* q, const double* qtr, const 
                     const signed char* pair_add, double* blocks, cudaStream_t st);
 int launch_sparse_matvec(int64_t n_rows, int SZ, const int* indptr, const int* indices, const double* blocks,
                          const double* x, double* y, cudaStream_t st);
+int launch_forces(const DiscDev& d, const double* q, int64_t nwall, const int* wall_e, const signed char* wall_f,
+                  const double* weights, double* out, cudaStream_t st);
 int status_clear_async(cudaStream_t st);
 int status_read(cudaStream_t st, Status* out, int clear);
 }  // namespace pmgb

@@ -29,8 +29,8 @@ import torch
 from . import _lib
 from ._lib import check, load
 from .equation import KIND_CODE, EquationSpec, NonPhysicalStateError
-from .mesh import Mesh, face_links, pack_geometry, solution_point_coords, element_geometry
-from .operators import basis, face_operators
+from .mesh import TAG_CODE, Mesh, face_links, pack_geometry, solution_point_coords, element_geometry
+from .operators import basis, face_operators, gauss_rule
 from .vec import ptr, require_cuda, stream, to_device
 
 __all__ = ["Discretization", "SolutionField", "FrozenState", "NonPhysicalStateError",
@@ -188,6 +188,35 @@ class Discretization:
         f = self.new_field()
         f.data.copy_(torch.as_tensor(vals))
         return f
+
+    # -- forces (spatial.py:633-695) ---------------------------------------------
+
+    def compute_forces(self, data):
+        """Integrated wall force and coefficients (Fd, Fl, Cd, Cl): pressure
+        plus BR1 viscous traction over all wall-tagged faces, computed on the
+        device per wall face and summed here in face order; the coefficients
+        use the reference length as the projected area."""
+        eqn = self.eqn
+        if eqn.kind == "advection-diffusion":
+            raise ValueError("forces are only defined for flow equations")
+        walls = getattr(self, "_wall_pairs", None)
+        if walls is None:
+            ef = np.argwhere((self._tags >= 0) & (self._tags <= TAG_CODE["wall-slip"]))
+            walls = self._wall_pairs = (
+                len(ef),
+                torch.as_tensor(ef[:, 0].astype(np.int32), device=self.device),
+                torch.as_tensor(ef[:, 1].astype(np.int8), device=self.device))
+        n_wall, we, wf = walls
+        if n_wall == 0:
+            raise ValueError("mesh has no wall boundary faces")
+        q = to_device(data, self.device)
+        out = torch.empty((n_wall, 2), dtype=torch.float64, device=self.device)
+        w = np.ascontiguousarray(gauss_rule(self.n)[1], dtype=np.float64)
+        check(load().pmgb_wall_forces(self._h, ptr(q), n_wall, we.data_ptr(), wf.data_ptr(),
+                                      w.ctypes.data, out.data_ptr(), stream()), "wall_forces")
+        F = out.cpu().numpy().sum(axis=0)
+        qref = 0.5 * 1.0 * 1.0 ** 2 * eqn.ref_length  # rho_inf U_inf^2 A / 2
+        return float(F[0]), float(F[1]), float(F[0] / qref), float(F[1] / qref)
 
     # -- device entry points ---------------------------------------------------
 
