@@ -49,13 +49,14 @@ BYTES_PER_DOF_JV = 32.0                                         # read q, v, R0;
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--no-step", action="store_true", help="skip the JFNK-pMG time-step timings")
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU-oracle baseline sample")
     ap.add_argument("--no-configs", action="store_true", help="skip the configs 3-5 measurements")
+    ap.add_argument("--no-mbnk", action="store_true", help="skip the MBNK smoother timings")
     return ap.parse_args()
 
 
@@ -301,6 +302,12 @@ def run_ours(args):
     others = {}
     if not args.no_configs and rank == 0 and args.config == 2:
         others = time_other_configs(torch, args)
+    mbnk = {}
+    if not args.no_mbnk and rank == 0 and args.config == 2:
+        try:
+            mbnk = time_mbnk(torch, case)
+        except Exception as exc:  # pragma: no cover
+            mbnk = {"error": str(exc)[:200]}
 
     if rank != 0:
         pdist.barrier()
@@ -339,6 +346,7 @@ def run_ours(args):
         "clocks": clk.summary(),
         "step_time": step,
         "configs": others,
+        "mbnk": mbnk,
     }
     # CPU baseline: the oracle on this host, bounded sample
     try:
@@ -427,6 +435,42 @@ def time_other_configs(torch, args):
             rec["error"] = str(exc)[:200]
         torch.cuda.empty_cache()
         out[f"config{k}"] = rec
+    return out
+
+
+def time_mbnk(torch, case2):
+    """MBNK smoother pieces on config 2's p=2 coarse
+    level (65,536 elements, 327,680 36x36 blocks): block-sparse FD Jacobian,
+    level-scheduled block ILU0 factor / apply, block SpMV."""
+    from paper_2202_09733_b200 import cases, newton_krylov as nk, pmg
+    from paper_2202_09733_b200.spatial import Discretization
+    d4 = Discretization(case2.mesh, 4, case2.eqn)
+    ctx = pmg.PmgContext(d4, pmg.PmgPrecondConfig(pmg.PHierarchy.parse("4-2")))
+    qc = ctx.tables[0].restrict(torch.as_tensor(case2.q0, device="cuda"))
+    dc = ctx.levels[1].disc
+    nk.sparse_pattern(dc)
+
+    def wall(fn, n=1):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(n):
+            r = fn()
+        torch.cuda.synchronize()
+        return (time.perf_counter() - t0) / n, r
+    nk.ilu0_factor(nk.assemble_sparse_blocks(dc, qc, 40.0))  # first calls load the kernels
+    t_a, A = wall(lambda: nk.assemble_sparse_blocks(dc, qc, 40.0))
+    t_f, F = wall(lambda: nk.ilu0_factor(A))
+    v = torch.randn(dc.n_dofs, dtype=torch.float64, device="cuda", generator=torch.Generator("cuda").manual_seed(3))
+    nk.ilu0_apply(F, v)
+    t_ap, _ = wall(lambda: nk.ilu0_apply(F, v), 5)
+    t_mv, _ = wall(lambda: A.matvec(v), 20)
+    pat = A.pattern
+    out = {"level": "config2 coarse p=2", "n_elements": dc.mesh.n_elements, "nnz_blocks": pat.nnz,
+           "block": dc.elem_size, "ilu_levels": [len(pat.lo_ptr) - 1, len(pat.up_ptr) - 1],
+           "assemble_ms": t_a * 1e3, "ilu0_factor_ms": t_f * 1e3, "ilu0_apply_ms": t_ap * 1e3,
+           "spmv_ms": t_mv * 1e3, "timing": "wall clock around synchronised calls"}
+    del A, F, ctx
+    torch.cuda.empty_cache()
     return out
 
 
