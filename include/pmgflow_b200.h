@@ -175,6 +175,19 @@ PMGB_API int pmgb_ilu0_apply(int64_t n_rows, int32_t sz, const int32_t* indptr, 
 PMGB_API int pmgb_wall_forces(pmgb_disc* d, const double* q, int64_t n_wall, const int32_t* wall_e,
                               const int8_t* wall_f, const double* weights, double* out, void* stream);
 
+/* The same ilu0_apply as ONE cooperative launch: a co-resident grid walks
+ * the forward then the backward levels with a global barrier between
+ * levels (same per-row arithmetic).  row_entries (n_rows, 8, 2) int32:
+ * the (CSR slot, column) of each row's lower (first 4) and upper (last 4)
+ * blocks in column order, -1 padded.  Level pointers are DEVICE int32
+ * arrays here; barrier = 2 device uint32 words of scratch; max_level_rows
+ * = the largest level (caps the grid). */
+PMGB_API int pmgb_ilu0_apply_fused(int32_t sz, const int32_t* row_entries, const double* F,
+                                    const double* DX, const uint8_t* DP, int32_t n_lo, const int32_t* lo_ptr_dev,
+                                    const int32_t* lo_rows, int32_t n_up, const int32_t* up_ptr_dev,
+                                    const int32_t* up_rows, int32_t max_level_rows, const double* x, double* y,
+                                    double* out, uint32_t* barrier, void* stream);
+
 /* BlockJacobian.apply / ej_apply (newton_krylov.py:166-171, 213-214):
  * y_e = B_e^-1 x_e from (XT, perm).  pmgb_ej_update: out = base + omega *
  * B^-1 d (smooth_ej, pmg.py:162-164); out may alias base. */

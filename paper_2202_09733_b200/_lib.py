@@ -68,6 +68,9 @@ SIGNATURES = {
                                        c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "pmgb_wall_forces": (ctypes.c_int, [c_void_p, c_void_p, ctypes.c_int64, c_void_p, c_void_p, c_void_p, c_void_p,
                                         c_void_p]),
+    "pmgb_ilu0_apply_fused": (ctypes.c_int, [ctypes.c_int32, c_void_p, c_void_p, c_void_p, c_void_p,
+                                             ctypes.c_int32, c_void_p, c_void_p, ctypes.c_int32, c_void_p, c_void_p,
+                                             ctypes.c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "pmgb_sparse_assemble": (ctypes.c_int, [c_void_p, c_void_p, ctypes.c_double, ctypes.c_double, c_void_p,
                                             c_void_p, ctypes.c_int64, c_void_p, c_void_p, c_void_p, c_void_p,
                                             c_void_p, ctypes.c_int32, c_void_p]),

@@ -15,6 +15,10 @@ int launch_ilu_level(int64_t n, int SZ, const int* rows, const int* indptr, cons
 int launch_ilu_sweep(int backward, int64_t n, int SZ, const int* rows, const int* indptr, const int* indices,
                      const double* F, const double* DX, const uint8_t* DP, const double* in, double* out,
                      cudaStream_t st);
+int launch_ilu_persistent(int SZ, int n_lo, const int* lo_ptr, const int* lo_rows, int n_up, const int* up_ptr,
+                          const int* up_rows, const int* ent, const double* F,
+                          const double* DX, const uint8_t* DP, const double* x, double* y, double* out,
+                          unsigned* bar, int max_rows, cudaStream_t st);
 int launch_block_gemv(int64_t M, int SZ, const double* XT, const uint8_t* perm, const double* x, double omega,
                       const double* base, double* out, cudaStream_t st);
 int launch_transfer(int64_t M, int nv, int nin, int nout, const double* T, const double* src,
@@ -285,6 +289,18 @@ PMGB_API int pmgb_wall_forces(pmgb_disc* h, const double* q, int64_t n_wall, con
   if (d.kind != K_EULER && d.kind != K_NS) return -5;
   g_launches += (d.kind == K_NS) ? 3 : 2;
   return launch_forces(d, q, n_wall, wall_e, (const signed char*)wall_f, weights, out, S(stream));
+}
+
+PMGB_API int pmgb_ilu0_apply_fused(int32_t sz, const int32_t* row_entries, const double* F,
+                                    const double* DX, const uint8_t* DP, int32_t n_lo, const int32_t* lo_ptr_dev,
+                                    const int32_t* lo_rows, int32_t n_up, const int32_t* up_ptr_dev,
+                                    const int32_t* up_rows, int32_t max_level_rows, const double* x, double* y,
+                                    double* out, uint32_t* barrier, void* stream) {
+  if (!row_entries || !F || !DX || !DP || !x || !y || !out || !barrier || !lo_ptr_dev || !up_ptr_dev)
+    return -1;
+  g_launches += 1;
+  return launch_ilu_persistent(sz, n_lo, lo_ptr_dev, lo_rows, n_up, up_ptr_dev, up_rows, row_entries, F, DX,
+                               DP, x, y, out, barrier, max_level_rows, S(stream));
 }
 
 PMGB_API int pmgb_ej_apply(int64_t M, int32_t sz, const double* XT, const uint8_t* perm, const double* x, double* y,

@@ -530,6 +530,180 @@ k_ilu_backward(const int* __restrict__ rows, const int* __restrict__ indptr, con
   }
 }
 
+// Persistent sweeps: one co-resident grid walks all forward levels, then
+// all backward levels, with a global barrier between levels; each CTA
+// takes rows b, b + G, ... of a level.  Same per-row arithmetic as the
+// per-level kernels above.
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ unsigned atom_add_acq_rel_gpu(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
+// sense barrier over a co-resident grid: the generation is read (acquire,
+// device scope -- a volatile load would be system scope and slow) before
+// arriving; the last arriver resets the count and bumps the generation
+__device__ __forceinline__ void grid_barrier(unsigned* count, unsigned* gen, unsigned nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned g = ld_acquire_gpu(gen);
+    __threadfence();  // this CTA's writes before the arrival
+    if (atom_add_acq_rel_gpu(count, 1u) == nblocks - 1) {
+      *count = 0;
+      atom_add_acq_rel_gpu(gen, 1u);
+    } else {
+      while (ld_acquire_gpu(gen) == g) {
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// dense per-row entry lists: ent[i*8 + e] = (slot, column) of the row's
+// e-th lower (e < 4) / upper (4 <= e < 8) block in CSR order, -1 padded
+constexpr int ILU_ENT = 4;
+
+template <int SZ>
+__device__ __forceinline__ double ilu_row_dense(int i, int r, const int2* __restrict__ ent, int half,
+                                                const double* __restrict__ F, const double* __restrict__ v,
+                                                double base) {
+  constexpr int64_t BB = (int64_t)SZ * SZ;
+  int2 en[ILU_ENT];
+#pragma unroll
+  for (int e = 0; e < ILU_ENT; ++e) en[e] = __ldg(ent + (int64_t)i * 2 * ILU_ENT + half * ILU_ENT + e);
+  double part[ILU_ENT];
+#pragma unroll
+  for (int e = 0; e < ILU_ENT; ++e) {
+    part[e] = 0.0;
+    if (en[e].x >= 0 && r < SZ) part[e] = dot_col<SZ>(F + en[e].x * BB + r, v + (int64_t)en[e].y * SZ);
+  }
+  double acc = base;
+#pragma unroll
+  for (int e = 0; e < ILU_ENT; ++e)
+    if (en[e].x >= 0) acc -= part[e];
+  return acc;
+}
+
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
+// prefetch into L2 the blocks of this CTA's rows in the next level
+template <int SZ>
+__device__ __forceinline__ void ilu_prefetch(const int* __restrict__ lptr, const int* __restrict__ lrows, int L1,
+                                             int nlev, const int2* __restrict__ ent, int half,
+                                             const double* __restrict__ F) {
+  if (L1 >= nlev) return;
+  constexpr int64_t BB = (int64_t)SZ * SZ;
+  constexpr int LINES = (int)((BB * 8 + 127) / 128);
+  for (int t = lptr[L1] + blockIdx.x; t < lptr[L1 + 1]; t += gridDim.x) {
+    const int i = lrows[t];
+#pragma unroll
+    for (int e = 0; e < ILU_ENT; ++e) {
+      const int2 en = __ldg(ent + (int64_t)i * 2 * ILU_ENT + half * ILU_ENT + e);
+      if (en.x < 0) continue;
+      const char* b = reinterpret_cast<const char*>(F + en.x * BB);
+      for (int l = threadIdx.x; l < LINES; l += blockDim.x) prefetch_l2(b + l * 128);
+    }
+  }
+}
+
+template <int SZ>
+__global__ void __launch_bounds__((SZ + 31) / 32 * 32)
+k_ilu_apply_persistent(int n_lo, const int* __restrict__ lo_ptr, const int* __restrict__ lo_rows, int n_up,
+                       const int* __restrict__ up_ptr, const int* __restrict__ up_rows,
+                       const int2* __restrict__ ent, const double* __restrict__ F, const double* __restrict__ DX,
+                       const uint8_t* __restrict__ DP, const double* __restrict__ x, double* __restrict__ y,
+                       double* __restrict__ out, unsigned* bar) {
+  __shared__ double sacc[SZ];
+  __shared__ uint8_t sp[2 * SZ];
+  const unsigned G = gridDim.x;
+  const int r = threadIdx.x;
+  constexpr int64_t BB = (int64_t)SZ * SZ;
+  ilu_prefetch<SZ>(lo_ptr, lo_rows, 0, n_lo, ent, 0, F);
+  for (int L = 0; L < n_lo; ++L) {
+    for (int t = lo_ptr[L] + blockIdx.x; t < lo_ptr[L + 1]; t += G) {
+      const int i = lo_rows[t];
+      const double xr = r < SZ ? x[(int64_t)i * SZ + r] : 0.0;
+      const double acc = ilu_row_dense<SZ>(i, r, ent, 0, F, y, xr);
+      if (r < SZ) y[(int64_t)i * SZ + r] = acc;
+    }
+    ilu_prefetch<SZ>(lo_ptr, lo_rows, L + 1, n_lo, ent, 0, F);
+    if (L + 1 == n_lo) ilu_prefetch<SZ>(up_ptr, up_rows, 0, n_up, ent, 1, F);
+    grid_barrier(bar, bar + 1, G);
+  }
+  for (int L = 0; L < n_up; ++L) {
+    for (int t = up_ptr[L] + blockIdx.x; t < up_ptr[L + 1]; t += G) {
+      const int i = up_rows[t];
+      for (int u = r; u < 2 * SZ; u += blockDim.x) sp[u] = DP[(int64_t)i * 2 * SZ + u];
+      const double yr = r < SZ ? y[(int64_t)i * SZ + r] : 0.0;
+      const double acc = ilu_row_dense<SZ>(i, r, ent, 1, F, out, yr);
+      if (r < SZ) sacc[r] = acc;
+      __syncthreads();
+      if (r < SZ) {
+        const double* XT = DX + (int64_t)i * BB + r;
+        constexpr int CH = 12;
+        double s = 0.0;
+#pragma unroll
+        for (int c0 = 0; c0 < SZ; c0 += CH) {
+          double a[CH];
+#pragma unroll
+          for (int u = 0; u < CH; ++u)
+            if (c0 + u < SZ) a[u] = __ldg(XT + (c0 + u) * SZ);
+#pragma unroll
+          for (int u = 0; u < CH; ++u)
+            if (c0 + u < SZ) s = fma(a[u], sacc[sp[c0 + u]], s);
+        }
+        out[(int64_t)i * SZ + sp[SZ + r]] = s;
+      }
+      __syncthreads();
+    }
+    ilu_prefetch<SZ>(up_ptr, up_rows, L + 1, n_up, ent, 1, F);
+    grid_barrier(bar, bar + 1, G);
+  }
+}
+
+template <int SZ>
+static int run_ilu_persistent(int n_lo, const int* lo_ptr, const int* lo_rows, int n_up, const int* up_ptr,
+                              const int* up_rows, const int2* ent, const double* F,
+                              const double* DX, const uint8_t* DP, const double* x, double* y, double* out,
+                              unsigned* bar, int max_rows, cudaStream_t st) {
+  constexpr int TH = (SZ + 31) / 32 * 32;
+  static int resident = 0;
+  if (resident == 0) {
+    int per_sm = 0, dev = 0, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ilu_apply_persistent<SZ>, TH, 0);
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    resident = per_sm * sms;
+  }
+  int grid = max_rows < resident ? max_rows : resident;
+  if (grid < 1) grid = 1;
+  cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned), st);
+  void* args[] = {&n_lo, &lo_ptr, &lo_rows, &n_up, &up_ptr, &up_rows, &ent, &F, &DX, &DP, &x, &y, &out, &bar};
+  cudaLaunchCooperativeKernel((void*)k_ilu_apply_persistent<SZ>, dim3(grid), dim3(TH), args, 0, st);
+  return (int)cudaGetLastError();
+}
+
+int launch_ilu_persistent(int SZ, int n_lo, const int* lo_ptr, const int* lo_rows, int n_up, const int* up_ptr,
+                          const int* up_rows, const int* ent, const double* F,
+                          const double* DX, const uint8_t* DP, const double* x, double* y, double* out,
+                          unsigned* bar, int max_rows, cudaStream_t st) {
+  switch (SZ) {
+#define PMGB_PS(Z) \
+  case Z: return run_ilu_persistent<Z>(n_lo, lo_ptr, lo_rows, n_up, up_ptr, up_rows, \
+                                       reinterpret_cast<const int2*>(ent), F, DX, DP, \
+                                       x, y, out, bar, max_rows, st);
+    PMGB_PS(1) PMGB_PS(4) PMGB_PS(9) PMGB_PS(16) PMGB_PS(25) PMGB_PS(36) PMGB_PS(64) PMGB_PS(100) PMGB_PS(144)
+#undef PMGB_PS
+  }
+  return -1000;
+}
+
 template <int SZ>
 static int run_ilu_level(int64_t n, const int* rows, const int* indptr, const int* indices, double* F,
                          const double* DX, const uint8_t* DP, cudaStream_t st) {

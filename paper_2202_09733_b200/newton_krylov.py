@@ -301,12 +301,34 @@ class _SparsePattern:
         self.lo_rows, self.lo_ptr = schedule(lo_lev)
         self.up_rows, self.up_ptr = schedule(up_lev)
         self.lo_diag = self.diag_slot[self.lo_rows].astype(np.int32)
+        self.max_level_rows = int(max(np.diff(self.lo_ptr).max(), np.diff(self.up_ptr).max())) if M else 1
+        # dense (slot, column) lists of each row's lower / upper blocks, CSR order
+        ent = np.full((M, 2, 4, 2), -1, dtype=np.int32)
+        for i in range(M):
+            lo_n = up_n = 0
+            for k in range(self.indptr[i], self.indptr[i + 1]):
+                j = int(self.indices[k])
+                if j < i:
+                    if lo_n >= 4:
+                        raise NotImplementedError("more than 4 lower block neighbours")
+                    ent[i, 0, lo_n] = (k, j)
+                    lo_n += 1
+                elif j > i:
+                    if up_n >= 4:
+                        raise NotImplementedError("more than 4 upper block neighbours")
+                    ent[i, 1, up_n] = (k, j)
+                    up_n += 1
+        self.row_entries = ent
         dev = disc.device
         self.d = {name: torch.as_tensor(np.ascontiguousarray(getattr(self, name)), device=dev)
                   for name in ("pair_e", "pair_f", "pair_slot", "pair_add", "lo_rows", "up_rows", "lo_diag")}
         self.d["diag_slot"] = torch.as_tensor(self.diag_slot.astype(np.int32), device=dev)
         self.d["indptr"] = torch.as_tensor(self.indptr.astype(np.int32), device=dev)
         self.d["indices"] = torch.as_tensor(self.indices.astype(np.int32), device=dev)
+        self.d["lo_ptr"] = torch.as_tensor(self.lo_ptr.astype(np.int32), device=dev)
+        self.d["up_ptr"] = torch.as_tensor(self.up_ptr.astype(np.int32), device=dev)
+        self.d["barrier"] = torch.zeros(2, dtype=torch.int32, device=dev)
+        self.d["row_entries"] = torch.as_tensor(self.row_entries, device=dev)
 
     def entry(self, i: int, j: int) -> int:
         lo, hi = int(self.indptr[i]), int(self.indptr[i + 1])
@@ -415,8 +437,10 @@ def ilu0_factor(A: SparseBlockMatrix) -> Ilu0Factors:
     return Ilu0Factors(SparseBlockMatrix(disc, pat, F), DX, DP)
 
 
-def ilu0_apply(fac: Ilu0Factors, X, offsets=None):
-    """Solve LU y = X with the incomplete factors (newton_krylov.py:348-368)."""
+def ilu0_apply(fac: Ilu0Factors, X, offsets=None, fused: bool = True):
+    """Solve LU y = X with the incomplete factors (newton_krylov.py:348-368):
+    one cooperative launch walking the level schedule (``fused``), or one
+    launch per level."""
     Fm = fac.pattern
     disc, pat = Fm.disc, Fm.pattern
     is_np = not isinstance(X, torch.Tensor)
@@ -424,12 +448,20 @@ def ilu0_apply(fac: Ilu0Factors, X, offsets=None):
     y = torch.empty_like(Xd)
     out = torch.empty_like(Xd)
     d = pat.d
-    lp = np.ascontiguousarray(pat.lo_ptr, dtype=np.int64)
-    up = np.ascontiguousarray(pat.up_ptr, dtype=np.int64)
-    check(load().pmgb_ilu0_apply(Fm.n, disc.elem_size, d["indptr"].data_ptr(), d["indices"].data_ptr(),
-                                 Fm.blocksT.data_ptr(), fac.DX.data_ptr(), fac.DP.data_ptr(), len(lp) - 1,
-                                 lp.ctypes.data, d["lo_rows"].data_ptr(), len(up) - 1, up.ctypes.data,
-                                 d["up_rows"].data_ptr(), ptr(Xd), ptr(y), ptr(out), stream()), "ilu0_apply")
+    nlo, nup = len(pat.lo_ptr) - 1, len(pat.up_ptr) - 1
+    if fused:
+        check(load().pmgb_ilu0_apply_fused(disc.elem_size, d["row_entries"].data_ptr(), Fm.blocksT.data_ptr(),
+                                           fac.DX.data_ptr(), fac.DP.data_ptr(), nlo, d["lo_ptr"].data_ptr(), d["lo_rows"].data_ptr(), nup,
+                                           d["up_ptr"].data_ptr(), d["up_rows"].data_ptr(), pat.max_level_rows,
+                                           ptr(Xd), ptr(y), ptr(out), d["barrier"].data_ptr(), stream()),
+              "ilu0_apply_fused")
+    else:
+        lp = np.ascontiguousarray(pat.lo_ptr, dtype=np.int64)
+        up = np.ascontiguousarray(pat.up_ptr, dtype=np.int64)
+        check(load().pmgb_ilu0_apply(Fm.n, disc.elem_size, d["indptr"].data_ptr(), d["indices"].data_ptr(),
+                                     Fm.blocksT.data_ptr(), fac.DX.data_ptr(), fac.DP.data_ptr(), nlo,
+                                     lp.ctypes.data, d["lo_rows"].data_ptr(), nup, up.ctypes.data,
+                                     d["up_rows"].data_ptr(), ptr(Xd), ptr(y), ptr(out), stream()), "ilu0_apply")
     return out.cpu().numpy() if is_np else out
 
 

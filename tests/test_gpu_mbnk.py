@@ -101,3 +101,15 @@ def test_mbnk_driver_step_matches_oracle(cuda):
     q1_o = drv.esdirk_step(c.q0, c.dt, s.a, s.b)
     assert [i["iters"] for i in info] == [r[1] for r in drv.records]
     assert scaled(q1, q1_o) <= 1e-7
+
+
+@pytest.mark.parametrize("name", list(SPARSE_CASES))
+def test_ilu0_fused_apply_is_bitwise_the_level_path(cuda, name):
+    mk, kw, p = SPARSE_CASES[name]
+    d = Discretization(mk(), p, EquationSpec(**kw))
+    pre = f"sp/{name}/"
+    fac = nk.ilu0_factor(nk.assemble_sparse_blocks(d, t(G[pre + "q"]), 40.0))
+    X = t(G[pre + "X"])
+    a = nk.ilu0_apply(fac, X, fused=True)
+    b = nk.ilu0_apply(fac, X, fused=False)
+    assert torch.equal(a, b)
