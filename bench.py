@@ -11,9 +11,12 @@ DoF-updates/s (GDoF/s) over all ranks.  Also timed: the fused Jv
 (the GMRES matvec) and one ESDIRK2 JFNK-pMG p{4-2} time step at config 2
 (the metric's second half), plus config 1's step beside the CPU oracle.
 
-Multi-GPU: each rank evaluates its own replica of the config-2 mesh
-(weak scaling, no data-path collective).  Times
-are CUDA-event device times on the launching stream, max over ranks.
+Multi-GPU: the headline numbers are replicas (each rank its own config-2
+mesh: weak scaling, no data-path collective); the "partitioned" block
+times the sharded residual -- each rank a 256 x 256 slab of one
+256 x 256N periodic mesh with an NCCL halo exchange every step
+(paper_2202_09733_b200/partition.py).  Times are
+CUDA-event device times on the launching stream, max over ranks.
 
 --impl reference: the reference arm -- the CPU oracle (NumPy restatement
 of the reference, oracle/, pinned to the reference's golden vectors)
@@ -295,6 +298,12 @@ def run_ours(args):
     t_dup, = pdist.max_over_ranks([t_dup], "cuda")
     ceil_e2e = pdist.job_rate(n * K, ws, t_dup) / 1e9
 
+    # the sharded residual with its halo exchange (all ranks take part)
+    try:
+        partitioned = time_partitioned(torch, case, K, W, ws, rank)
+    except Exception as exc:  # pragma: no cover
+        partitioned = {"error": str(exc)[:200]}
+
     # JFNK-pMG time step (the metric's second half)
     step = {}
     if not args.no_step and rank == 0:
@@ -347,6 +356,7 @@ def run_ours(args):
         "step_time": step,
         "configs": others,
         "mbnk": mbnk,
+        "partitioned": partitioned,
     }
     # CPU baseline: the oracle on this host, bounded sample
     try:
@@ -436,6 +446,37 @@ def time_other_configs(torch, args):
         torch.cuda.empty_cache()
         out[f"config{k}"] = rec
     return out
+
+
+def time_partitioned(torch, case2, K, W, ws, rank):
+    """The sharded residual: rank r owns a 256 x 256 slab of a
+    256 x 256N periodic box (the config-2 field on every slab, which is
+    y-periodic) plus 2 halo element rows each side; every step is one
+    all_gather halo exchange over NCCL + R on the local strip.  Owned DoF
+    per second over all ranks, device time max over ranks."""
+    from paper_2202_09733_b200 import dist as pdist
+    from paper_2202_09733_b200.partition import PartitionedResidual, SlabPartition
+    n1 = int(round(np.sqrt(case2.mesh.n_elements)))
+    part = SlabPartition(n1, n1 * ws, 10.0, 10.0 * ws, ws, rank)
+    pr = PartitionedResidual(part, case2.p, case2.eqn)
+    sz = pr.sz
+    pr.q_owned.copy_(torch.as_tensor(case2.q0, device="cuda"))
+    out = torch.empty_like(pr.q_local)
+    step = lambda i: pr.residual(out)
+    xchg = lambda i: part.exchange(pr.q_local, sz)
+    for i in range(W):
+        step(i)
+    torch.cuda.synchronize()
+    pdist.barrier()
+    t_r = event_time(torch, step, K)
+    pdist.barrier()
+    t_x = event_time(torch, xchg, K)
+    t_r, t_x = pdist.max_over_ranks([t_r, t_x], "cuda")
+    owned = part.rows * n1 * sz
+    return {"global_mesh": f"{n1} x {n1 * ws} periodic, {ws} slab(s) of {n1} x {n1}", "halo_rows": part.halo,
+            "collective": "all_gather of the slabs' boundary rows (NCCL)" if ws > 1 else "local wrap copy",
+            "r_gdofs": owned * K * ws / t_r / 1e9, "ms_per_step": t_r / K * 1e3,
+            "exchange_ms": t_x / K * 1e3, "local_dofs_per_rank": pr.disc.n_dofs, "owned_dofs_per_rank": owned}
 
 
 def time_mbnk(torch, case2):

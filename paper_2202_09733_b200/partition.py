@@ -1,0 +1,114 @@
+"""Element-row slabs of a periodic box over ranks, with halo exchange.
+
+SURVEY 8(e): the residual shards by element partition with two neighbour
+exchanges per R, because BR1 reaches two elements deep (traces, then the
+one-sided viscous fluxes).  This module uses one q-halo exchange per R
+instead.  Each rank keeps its owned element rows plus ``halo = 2`` rows on
+either side of its slab.  One collective refreshes the halo rows.  The
+rank then evaluates R on its local strip with the unmodified kernels.  R is
+exact on the owned rows: every owned element's residual sees only q within
+two elements, and all of that is local.  The halo rows' own residuals are
+discarded.  The strip's open top and bottom edges are tagged far-field;
+they only touch halo elements.
+
+The exchange is one ``all_gather`` of every rank's first and last ``halo``
+owned rows (NCCL on GPUs, gloo in the CPU tests).  Each rank copies its
+neighbours' rows into its halo.  Periodic in y: rank 0's lower halo is the
+last rank's top rows.  With one rank it degenerates to a local wrap copy.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from .mesh import build_mesh
+
+
+class SlabPartition:
+    """Rows [rank * rows, (rank + 1) * rows) of a periodic nx x ny box
+    (generate_box numbering e = j * nx + i) plus ``halo`` rows each side."""
+
+    def __init__(self, nx: int, ny: int, Lx: float, Ly: float, world: int, rank: int, halo: int = 2):
+        if ny % world:
+            raise ValueError("ny must be a multiple of the rank count")
+        rows = ny // world
+        if rows < halo:
+            raise ValueError("each rank needs at least `halo` owned element rows")
+        self.nx, self.ny, self.world, self.rank, self.halo, self.rows = nx, ny, world, rank, halo, rows
+        self.j0 = rank * rows
+        nr = rows + 2 * halo
+        dy = Ly / ny
+        xs = np.linspace(0.0, Lx, nx + 1)
+        ys = (self.j0 - halo + np.arange(nr + 1)) * dy
+        X, Y = np.meshgrid(xs, ys)
+        nodes = np.stack([X.ravel(), Y.ravel()], axis=1)
+        jj, ii = np.meshgrid(np.arange(nr), np.arange(nx), indexing="ij")
+        base = (jj * (nx + 1) + ii).ravel()
+        elements = np.stack([base, base + 1, base + nx + 2, base + nx + 1], axis=1)
+        eid = lambda i, j: j * nx + i
+        pairs = [(eid(nx - 1, j), 1, eid(0, j), 3) for j in range(nr)]
+        boundary = {}
+        for i in range(nx):
+            boundary[(eid(i, 0), 0)] = "far-field"
+            boundary[(eid(i, nr - 1), 2)] = "far-field"
+        self.mesh = build_mesh(nodes, elements, boundary, pairs)
+        self.n_local = nr * nx
+        self.owned = slice(halo * nx, (halo + rows) * nx)          # local element range
+        gj = (self.j0 - halo + np.arange(nr)) % ny
+        self.global_elements = (gj[:, None] * nx + np.arange(nx)[None, :]).ravel()
+
+    # -- element-row slices of a local vector (elem_size doubles per element) --
+    def _rows(self, v, r0, nrows, sz):
+        return v[r0 * self.nx * sz:(r0 + nrows) * self.nx * sz]
+
+    def exchange(self, q_local: torch.Tensor, elem_size: int, group=None):
+        """Fill the halo rows of ``q_local`` (local strip layout) in place
+        from the neighbouring ranks' owned rows."""
+        H, R, sz = self.halo, self.rows, elem_size
+        send = torch.cat([self._rows(q_local, H, H, sz), self._rows(q_local, R, H, sz)])
+        if self.world == 1 or not (dist.is_available() and dist.is_initialized()):
+            got = [send]
+        else:
+            got = [torch.empty_like(send) for _ in range(self.world)]
+            dist.all_gather(got, send, group=group)
+        half = H * self.nx * sz
+        below = got[(self.rank - 1) % self.world][half:]   # previous rank's top owned rows
+        above = got[(self.rank + 1) % self.world][:half]   # next rank's bottom owned rows
+        self._rows(q_local, 0, H, sz).copy_(below)
+        self._rows(q_local, H + R, H, sz).copy_(above)
+        return q_local
+
+    def scatter_global(self, q_global, elem_size: int):
+        """Local strip vector (owned + halo) cut from a global vector."""
+        Q = q_global.reshape(-1, elem_size)
+        idx = torch.as_tensor(self.global_elements, device=Q.device) if isinstance(Q, torch.Tensor) \
+            else self.global_elements
+        return Q[idx].reshape(-1)
+
+
+class PartitionedResidual:
+    """R on the owned rows of a slab: halo exchange, then the local strip's
+    residual (owned part returned as a view)."""
+
+    def __init__(self, part: SlabPartition, degree: int, eqn, device=None):
+        from .spatial import Discretization
+        self.part = part
+        self.disc = Discretization(part.mesh, degree, eqn, device=device)
+        self.sz = self.disc.elem_size
+        self.q_local = torch.zeros(self.disc.n_dofs, dtype=torch.float64, device=self.disc.device)
+        o = part.owned
+        self.owned_dofs = slice(o.start * self.sz, o.stop * self.sz)
+
+    @property
+    def q_owned(self) -> torch.Tensor:
+        return self.q_local[self.owned_dofs]
+
+    def residual(self, out=None):
+        """Exchange the halos of ``q_local`` and evaluate R; returns the
+        owned rows of R."""
+        from . import _lib
+        self.part.exchange(self.q_local, self.sz)
+        R = self.disc.eval(self.q_local, _lib.EPI_R, out)
+        return R[self.owned_dofs]

@@ -47,3 +47,53 @@ def test_two_rank_replicas_gloo():
     n = res[0][1] * 0.2 / world
     assert res[0][1] == res[1][1] and n == pytest.approx(4 * 4 * 16 * 4)
     assert res[0][2] == res[1][2] == res[0][3] == res[1][3]
+
+
+def _halo_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), WORLD_SIZE=str(world),
+                      RANK=str(rank), LOCAL_RANK=str(rank))
+    import torch
+    from paper_2202_09733_b200 import dist
+    from paper_2202_09733_b200.partition import SlabPartition
+    dist.init("gloo")
+    nx, ny, sz = 4, 3 * world, 7
+    part = SlabPartition(nx, ny, 1.0, 1.0, world, rank)
+    q_global = torch.from_numpy(np.random.default_rng(0).standard_normal(nx * ny * sz))
+    q_local = torch.zeros(part.n_local * sz, dtype=torch.float64)
+    o = part.owned
+    q_local[o.start * sz:o.stop * sz] = part.scatter_global(q_global, sz)[o.start * sz:o.stop * sz]
+    part.exchange(q_local, sz)
+    out[rank] = bool(torch.equal(q_local, part.scatter_global(q_global, sz)))
+    dist.barrier()
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("world", [2, 3])
+def test_slab_halo_exchange_gloo(world):
+    # the multi-GPU partitioned residual's only data-path collective: every
+    # rank's halo rows must come back equal to the global field there
+    port = _free_port()
+    with mp.Manager() as m:
+        out = m.dict()
+        mp.spawn(_halo_worker, args=(world, port, out), nprocs=world, join=True)
+        res = dict(out)
+    assert all(res[r] for r in range(world))
+
+
+@pytest.mark.parametrize("world", [1, 2, 4])
+def test_slab_owned_residual_is_exact_oracle(world):
+    # two halo rows make the owned rows' residual exact (BR1 reaches two
+    # elements deep): oracle R on each strip == global R at those elements
+    from oracle.fr_oracle import OracleDisc
+    from paper_2202_09733_b200 import cases
+    from paper_2202_09733_b200.partition import SlabPartition
+    c = cases.config(2, nx=8)
+    g = OracleDisc(c.mesh, c.p, c.eqn)
+    Rg = g.residual(c.q0).reshape(-1, g.offsets[1])
+    Q = c.q0.reshape(-1, g.offsets[1])
+    for rank in range(world):
+        part = SlabPartition(8, 8, 10.0, 10.0, world, rank)
+        lo = OracleDisc(part.mesh, c.p, c.eqn)
+        Rl = lo.residual(Q[part.global_elements].reshape(-1)).reshape(-1, g.offsets[1])
+        own = part.global_elements[part.owned]
+        assert np.max(np.abs(Rl[part.owned] - Rg[own])) <= 1e-13 * np.max(np.abs(Rg))

@@ -107,3 +107,22 @@ def test_fullsize_jv_bitwise_deterministic(cuda):
         d.eval(q, _lib.EPI_JV, o, X=X, eps=1e-6, s=2.5, R0=R0)
     torch.cuda.synchronize()
     assert all(torch.equal(outs[0], o) for o in outs[1:])
+
+
+@pytest.mark.parametrize("world", [1, 2, 4])
+def test_slab_partition_owned_residual_bitwise(cuda, world):
+    # the multi-GPU path's strips (owned rows + 2 halo rows) reproduce the
+    # global residual on their owned rows bit for bit (one process, ranks
+    # simulated, halos filled from the global field)
+    from paper_2202_09733_b200.partition import PartitionedResidual, SlabPartition
+    c = cases.config(2, nx=32)
+    d = Discretization(c.mesh, c.p, c.eqn)
+    q = torch.as_tensor(c.q0, device="cuda")
+    Rg = d.residual(q).reshape(-1, d.elem_size)
+    for rank in range(world):
+        part = SlabPartition(32, 32, 10.0, 10.0, world, rank)
+        pr = PartitionedResidual(part, c.p, c.eqn)
+        pr.q_local.copy_(part.scatter_global(q, d.elem_size))
+        Rl = pr.disc.residual(pr.q_local).reshape(-1, d.elem_size)
+        own = torch.as_tensor(part.global_elements[part.owned], device="cuda")
+        assert torch.equal(Rl[part.owned], Rg[own]), rank
