@@ -2093,14 +2093,13 @@ static int run_residual(const DiscDev& d, const double* q, const double* X, doub
                         double* out, cudaStream_t st) {
   using L = SL<P, KIND>;
   constexpr int E = BC<P>::EPB, TH = BC<P>::THREADS;
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr_seen{0};
+  if (first_use_on_device(attr_seen)) {
     cudaFuncSetAttribute(k_trace<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES_TRACE);
     cudaFuncSetAttribute(k_fvn<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES_FVN);
     cudaFuncSetAttribute(k_assemble<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES_ASM);
     if constexpr (KT<KIND>::NV == 4 && E * BC<P>::NF <= TH)
       cudaFuncSetAttribute(k_assemble_async<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES_ASYNC);
-    attr = true;
   }
   int* bad = nullptr;
   Status* stp = nullptr;
@@ -2130,11 +2129,10 @@ template <int P, int KIND>
 static int run_freeze(const DiscDev& d, const double* q, double* qtr, double* fvn, cudaStream_t st) {
   using L = SL<P, KIND>;
   constexpr int E = BC<P>::EPB, TH = BC<P>::THREADS;
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr_seen{0};
+  if (first_use_on_device(attr_seen)) {
     cudaFuncSetAttribute(k_trace<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES_TRACE);
     cudaFuncSetAttribute(k_fvn<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES_FVN);
-    attr = true;
   }
   const unsigned grid = (unsigned)((d.M + E - 1) / E);
   if constexpr (KT<KIND>::FLOW) {
@@ -2152,10 +2150,9 @@ static int run_local(const DiscDev& d, const int64_t* elems, int64_t B, const do
                      const double* fvn, double* out, cudaStream_t st) {
   using L = SL<P, KIND>;
   constexpr int E = BC<P>::EPB, TH = BC<P>::THREADS;
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr_seen{0};
+  if (first_use_on_device(attr_seen)) {
     cudaFuncSetAttribute(k_local<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES_LOCAL);
-    attr = true;
   }
   if (B <= 0) return 0;
   const unsigned grid = (unsigned)((B + E - 1) / E);
@@ -2168,10 +2165,9 @@ static int run_blocks(const DiscDev& d, const double* q, const double* qtr, cons
                       double eps, double* BT, const int* out_slot, cudaStream_t st) {
   using L = SL<P, KIND>;
   constexpr int TH = BC<P>::THREADS;
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr_seen{0};
+  if (first_use_on_device(attr_seen)) {
     cudaFuncSetAttribute(k_blocks<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES_LOCAL);
-    attr = true;
   }
   if (d.M <= 0) return 0;
   k_blocks<P, KIND><<<(unsigned)d.M, TH, L::BYTES_LOCAL, st>>>(d.C, d.mesh, q, qtr, fvn, shift, eps, BT, out_slot);
@@ -2184,11 +2180,10 @@ static int run_coupling(const DiscDev& d, const double* q, const double* qtr, co
                         const signed char* pair_add, double* blocks, cudaStream_t st) {
   using L = SL<P, KIND>;
   constexpr int TH = BC<P>::THREADS;
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr_seen{0};
+  if (first_use_on_device(attr_seen)) {
     cudaFuncSetAttribute(k_coupling<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)L::BYTES_COUPLING);
-    attr = true;
   }
   if (npairs <= 0) return 0;
   k_coupling<P, KIND><<<(unsigned)npairs, TH, L::BYTES_COUPLING, st>>>(d.C, d.mesh, q, qtr, fvn, eps, pair_e,
@@ -2204,11 +2199,10 @@ static int run_forces(const DiscDev& d, const double* q, int64_t nwall, const in
   if constexpr (!KT<KIND>::FLOW) {
     return -5;
   } else {
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<unsigned long long> attr_seen{0};
+    if (first_use_on_device(attr_seen)) {
       cudaFuncSetAttribute(k_trace<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES_TRACE);
       cudaFuncSetAttribute(k_fvn<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES_FVN);
-      attr = true;
     }
     const unsigned grid = (unsigned)((d.M + E - 1) / E);
     const unsigned gl = (unsigned)((d.M * 2 * (P + 1) + 127) / 128);

@@ -12,7 +12,18 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 namespace pmgb {
+
+// Per-device one-time setup (kernel attributes are per device): true the
+// first time it is called for the current device with this flag word.
+inline bool first_use_on_device(std::atomic<unsigned long long>& seen) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  return (seen.fetch_or(bit) & bit) == 0;
+}
 
 enum Kind { K_EULER = 0, K_NS = 1, K_ADV = 2, K_ADVD = 3 };
 enum Tag { T_WALL_ADIABATIC = 0, T_WALL_SLIP = 1, T_FAR_FIELD = 2 };
