@@ -113,3 +113,31 @@ def test_ilu0_fused_apply_is_bitwise_the_level_path(cuda, name):
     a = nk.ilu0_apply(fac, X, fused=True)
     b = nk.ilu0_apply(fac, X, fused=False)
     assert torch.equal(a, b)
+
+
+def test_ilu0_singular_pivot_raises_like_reference(cuda):
+    # newton_krylov.py:340-343: a singular pivot block raises RuntimeError
+    # naming the element
+    mk, kw, p = SPARSE_CASES["box3p_ns1"]
+    d = Discretization(mk(), p, EquationSpec(**kw))
+    A = nk.assemble_sparse_blocks(d, t(G["sp/box3p_ns1/q"]), 40.0)
+    A.blocksT[A.entry(0, 0)].zero_()
+    with pytest.raises(RuntimeError, match="singular ILU0 pivot block at element 0"):
+        nk.ilu0_factor(A)
+
+
+def test_sparse_blocks_and_ilu0_advection_diffusion_match_oracle(cuda):
+    # scalar kind (one variable, viscous): not in the reference goldens, so
+    # against the oracle restatement
+    from oracle import solver_oracle as so
+    from oracle.fr_oracle import OracleDisc
+    m = mm.generate_box(3, 3, 2.0, 1.5)
+    eqn = EquationSpec(kind="advection-diffusion", advection=(0.7, 0.4), diffusivity=0.02)
+    d, o = Discretization(m, 2, eqn), OracleDisc(m, 2, eqn)
+    q = np.random.default_rng(4).standard_normal(o.n_dofs)
+    A = nk.assemble_sparse_blocks(d, t(q), 25.0)
+    S = so.assemble_sparse(o, q, 25.0)
+    assert np.array_equal(A.indices, S.indices)
+    assert scaled(A.blocks, np.stack(S.blocks)) <= 1e-7
+    X = np.random.default_rng(5).standard_normal(o.n_dofs)
+    assert scaled(nk.ilu0_apply(nk.ilu0_factor(A), t(X)), so.ilu0_factor(S).apply(X)) <= 1e-6
