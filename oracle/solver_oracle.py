@@ -269,11 +269,53 @@ def ilu0_factor(A: SparseBlocks) -> Ilu0:
 # ---------------------------------------------------------------------------
 # pMG
 
+RK_ALPHAS = (0.25, 1.0 / 3.0, 0.5, 1.0)
+RK_CFL = 1.5
+
+
+def rk_spectral_radius(disc: OracleDisc, q):
+    """Per-element spectral-radius estimate lambda_e of dR/dq for the
+    pseudo-transient RK smoother (NOT in the reference -- BASELINE.json's
+    north star item (3); DESIGN.md section 4 "RK smoother"):
+
+        h_e      = 4 |det J(0,0)| / max(L_xi, L_eta)   (L = centre-line lengths)
+        lambda_e = (2p+1) max_pts(|u| + c) / h_e + (p+1)^4 max_pts(nu) / h_e^2
+        nu       = max(4/3 mu, kappa (gamma-1)) / rho   (NS), diffusivity (ADVD)
+    """
+    from paper_2202_09733_b200.mesh import pack_geometry
+    g = pack_geometry(disc.mesh)
+    a0, b0, c0, d0 = g[:, 0], g[:, 2], g[:, 4], g[:, 6]
+    Lx = 2.0 * np.sqrt(a0 * a0 + b0 * b0)
+    Ly = 2.0 * np.sqrt(c0 * c0 + d0 * d0)
+    h = 4.0 * np.abs(a0 * d0 - c0 * b0) / np.maximum(Lx, Ly)
+    M = disc.mesh.n_elements
+    eqn = disc.eqn
+    P = disc.p
+    if eqn.kind == "advection-diffusion":
+        ax, ay = eqn.advection
+        a = np.full(M, np.sqrt(ax * ax + ay * ay))
+        nu = np.full(M, float(eqn.diffusivity))
+    else:
+        Q = q.reshape(M, -1, 4)
+        gam = eqn.gamma
+        rho = Q[..., 0]
+        u = Q[..., 1] / rho
+        v = Q[..., 2] / rho
+        p = (gam - 1.0) * (Q[..., 3] - 0.5 * rho * (u * u + v * v))
+        a = (np.sqrt(u * u + v * v) + np.sqrt(gam * p / rho)).max(axis=1)
+        if eqn.kind == "navier-stokes":
+            nu = max(4.0 / 3.0 * eqn.mu, eqn.heat_conductivity * (gam - 1.0)) / rho.min(axis=1)
+        else:
+            nu = np.zeros(M)
+    return (2 * P + 1) * a / h + float((P + 1) ** 4) * nu / (h * h)
+
+
 class Level:
     def __init__(self, disc, nsweeps):
         self.disc, self.nsweeps = disc, nsweeps
         self.shift, self.q, self.S_base, self.S_extra, self.blocks = 0.0, None, 0.0, 0.0, None
         self.smoother, self.frozen_q, self.sparse, self.ilu = "ej", None, None, None
+        self.lam = None  # RK smoother: per-element spectral radius at the frozen state
 
     def F(self, q):
         return self.shift * q - self.disc.residual(q)
@@ -292,7 +334,9 @@ class Pmg:
     optional switch to MBNK after ``switch_after`` solver cycles."""
 
     def __init__(self, disc: OracleDisc, levels, smooth=2, omega=1.0, smoother_shift=0.0, m_max=1,
-                 smoother="ej", switch_after=None, mbnk_rtol=0.1, mbnk_maxiter=5):
+                 smoother="ej", switch_after=None, mbnk_rtol=0.1, mbnk_maxiter=5,
+                 rk_cfl=RK_CFL, rk_alphas=RK_ALPHAS):
+        self.rk_cfl, self.rk_alphas = float(rk_cfl), tuple(float(a) for a in rk_alphas)
         degs = [int(t) for t in str(levels).split("-")]
         L = len(degs)
 
@@ -334,12 +378,27 @@ class Pmg:
                 qk = self._restrict(k - 1, qk)
             lev.shift = shift
             lev.frozen_q = qk.copy()
-            lev.blocks = assemble_blocks(lev.disc, qk, shift + self.smoother_shift)
+            if lev.smoother == "rk":   # matrix-free: no blocks on this level
+                lev.blocks = None
+                lev.lam = rk_spectral_radius(lev.disc, qk)
+            else:
+                lev.blocks = assemble_blocks(lev.disc, qk, shift + self.smoother_shift)
             lev.sparse = lev.ilu = None
         self.cycles_done = 0
 
     def _smooth(self, k):
         lev = self.levels[k]
+        if lev.smoother == "rk" and self._effective_smoother(k) == "rk":
+            # pseudo-transient explicit RK with local (per-element) pseudo-time
+            # steps dtau_e = cfl / (s + lambda_e):  q <- q0 + alpha_j dtau_e d(q)
+            npe = lev.disc.n * lev.disc.n * lev.disc.nv
+            for _ in range(lev.nsweeps):
+                q0 = lev.q
+                dtau = self.rk_cfl / (lev.shift + lev.lam)
+                for a in self.rk_alphas:
+                    c = np.repeat(a * dtau, npe)
+                    lev.q = q0 + c * lev.defect()
+            return
         if self._effective_smoother(k) == "ej":
             for _ in range(lev.nsweeps):
                 lev.q = lev.q + self.omega * lev.blocks.apply(lev.defect())
@@ -379,6 +438,8 @@ class Pmg:
                 self.vcycle()
         except NonPhysicalStateError:
             self.fallbacks += 1
+            if fine.blocks is None:   # RK fine level: the diagonal (shift) part of the EJ fallback
+                return X * (1.0 / (self.shift + self.smoother_shift))
             return fine.blocks.apply(X)
         return fine.q - self.q_outer
 
@@ -488,11 +549,12 @@ class Driver:
 
     def __init__(self, disc: OracleDisc, precond="pmg", levels="3-2", smooth=2, smoother_shift=0.0,
                  kdim=30, max_restarts=10, gmres_rtol=1e-3, dtau_init=1e-3, ptc_rtol=1e-4,
-                 max_iters=100, max_halvings=8):
+                 max_iters=100, max_halvings=8, smoother="ej", rk_cfl=RK_CFL, rk_alphas=RK_ALPHAS):
         self.disc, self.precond = disc, precond
         self.krylov = dict(kdim=kdim, max_restarts=max_restarts, rtol=gmres_rtol)
         self.ptc = dict(dtau_init=dtau_init, rtol=ptc_rtol, max_iters=max_iters, max_halvings=max_halvings)
-        self.ctx = Pmg(disc, levels, smooth, smoother_shift=smoother_shift) if precond == "pmg" else None
+        self.ctx = (Pmg(disc, levels, smooth, smoother_shift=smoother_shift, smoother=smoother, rk_cfl=rk_cfl,
+                        rk_alphas=rk_alphas) if precond == "pmg" else None)
         self.records = []
 
     def _factory(self, shift0):

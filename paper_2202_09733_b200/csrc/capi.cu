@@ -157,6 +157,12 @@ PMGB_API int pmgb_eval(pmgb_disc* h, const double* q, const double* X, double ep
   ep.E = e->E;
   ep.Sb = e->Sb;
   ep.Se = e->Se;
+  ep.Q0 = e->Q0;
+  ep.lam = e->lam;
+  ep.alpha = e->alpha;
+  ep.cfl = e->cfl;
+  ep.npe = (int)((h->d.p + 1) * (h->d.p + 1) * h->d.nv);
+  if (ep.mode == EPI_RK && (!ep.Q0 || !ep.lam)) return -1;
   g_launches += n_res_launches(h->d);
   return launch_residual(h->d, q, X, eps, ep, out, S(stream));
 }
@@ -178,6 +184,12 @@ PMGB_API int pmgb_jfnk_matvec(pmgb_disc* h, const double* X, const double* q, co
   e.X = X;
   e.R0 = R0;
   return pmgb_eval(h, q, X, eps, &e, out, stream);
+}
+
+PMGB_API int pmgb_rk_lambda(pmgb_disc* h, const double* q, double* lam, void* stream) {
+  if (!h || (h->d.M > 0 && (!q || !lam))) return -1;
+  g_launches += 1;
+  return launch_rk_lambda(h->d, q, lam, S(stream));
 }
 
 PMGB_API int pmgb_freeze(pmgb_disc* h, const double* q, double* qtr, double* fvn, void* stream) {

@@ -1094,6 +1094,17 @@ k_fvn(const FrConst C, const FrMesh m, const double* __restrict__ q, const doubl
 // ---------------------------------------------------------------------------
 // phase 3: common fluxes, volume fluxes, FR divergence, fused epilogue
 
+// RK smoother stage (EPI_RK), rounded as the oracle's NumPy expression
+//   dtau_e = cfl / (s + lam_e);  c = alpha dtau_e;  q0 + c ((Sb - (s q - R)) + Se)
+__device__ __forceinline__ double epi_rk_coef(const Epi& ep, int64_t e) {
+  return __dmul_rn(ep.alpha, __ddiv_rn(ep.cfl, __dadd_rn(ep.s, __ldg(ep.lam + e))));
+}
+__device__ __forceinline__ double epi_rk(const Epi& ep, double c, double R, double qv, double sb, double se,
+                                         double q0) {
+  const double d = __dadd_rn(__dsub_rn(sb, __dsub_rn(__dmul_rn(ep.s, qv), R)), se);
+  return __dadd_rn(q0, __dmul_rn(c, d));
+}
+
 __device__ __forceinline__ double epi_apply(const Epi& ep, int64_t i, double R, double qv) {
   switch (ep.mode) {
     case EPI_R:
@@ -1119,6 +1130,11 @@ __device__ __forceinline__ double epi_apply(const Epi& ep, int64_t i, double R, 
       const double se = ep.Se ? ep.Se[i] : ep.se_scalar;
       return (ep.s * qv - R) - se;
     }
+    case EPI_RK: {
+      const double sb = ep.Sb ? ep.Sb[i] : ep.sb_scalar;
+      const double se = ep.Se ? ep.Se[i] : ep.se_scalar;
+      return epi_rk(ep, epi_rk_coef(ep, i / ep.npe), R, qv, sb, se, ep.Q0[i]);
+    }
   }
   return R;
 }
@@ -1126,8 +1142,11 @@ __device__ __forceinline__ double epi_apply(const Epi& ep, int64_t i, double R, 
 // Epilogue with operands preloaded by the caller:
 //   JV: o1 = X, o2 = R0;  STAGE_F: o3 = E;  STAGE_JV: o1 = X, o2 = Fk, o3 = E;
 //   DEFECT: o1 = Sb, o2 = Se;  OUTER_F: o2 = Se
-__device__ __forceinline__ double epi_pre(const Epi& ep, double R, double qv, double o1, double o2, double o3) {
+__device__ __forceinline__ double epi_pre(const Epi& ep, double R, double qv, double o1, double o2, double o3,
+                                          double ce = 0.0) {
   switch (ep.mode) {
+    case EPI_RK:
+      return epi_rk(ep, ce, R, qv, o1, o2, o3);
     case EPI_R:
       return R;
     case EPI_F:
@@ -1171,6 +1190,11 @@ __device__ __forceinline__ void epi_load(const Epi& ep, int64_t i, double& o1, d
       break;
     case EPI_OUTER_F:
       o2 = ep.Se ? __ldg(ep.Se + i) : ep.se_scalar;
+      break;
+    case EPI_RK:
+      o1 = ep.Sb ? __ldg(ep.Sb + i) : ep.sb_scalar;
+      o2 = ep.Se ? __ldg(ep.Se + i) : ep.se_scalar;
+      o3 = __ldg(ep.Q0 + i);
       break;
     default:
       break;
@@ -1564,6 +1588,7 @@ k_assemble_async(const FrConst C, const FrMesh m, const double* __restrict__ q, 
       double o1[N], o2[N], o3[N];
 #pragma unroll
       for (int a = 0; a < N; ++a) epi_load(ep, (e * NP + a * N + b) * NV + v, o1[a], o2[a], o3[a]);
+      const double ce = ep.mode == EPI_RK ? epi_rk_coef(ep, e) : 0.0;
 #pragma unroll
       for (int a = 0; a < N; ++a) {
         double ta = 0.0;
@@ -1576,7 +1601,7 @@ k_assemble_async(const FrConst C, const FrMesh m, const double* __restrict__ q, 
         const double R = -(d * idet);
         const int pt = a * N + b;
         const int64_t gi = (e * NP + pt) * NV + v;
-        out[gi] = epi_pre(ep, R, sQA[(el * NP + pt) * NV + v], o1[a], o2[a], o3[a]);
+        out[gi] = epi_pre(ep, R, sQA[(el * NP + pt) * NV + v], o1[a], o2[a], o3[a], ce);
       }
     }
   }
@@ -2067,6 +2092,57 @@ k_wall_forces(const FrConst C, const FrMesh m, const double* __restrict__ qtr, c
 
 // ---------------------------------------------------------------------------
 // host-side dispatch
+
+// ---------------------------------------------------------------------------
+// RK smoother: per-element spectral-radius estimate (oracle:
+// solver_oracle.rk_spectral_radius).  One warp per element, lanes over the
+// points; max / min are order-independent, so the result is deterministic.
+__global__ void __launch_bounds__(256)
+k_rk_lambda(const FrConst C, const FrMesh m, int p, int kind, const double* __restrict__ q,
+            double* __restrict__ lam) {
+  const int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (e >= m.M) return;
+  const int n = p + 1, NP = n * n;
+  double amax = 0.0, rmin = INFINITY;
+  if (kind == K_ADV || kind == K_ADVD) {
+    amax = sqrt(C.adv_x * C.adv_x + C.adv_y * C.adv_y);
+  } else {
+    const double g = C.gamma;
+    for (int t = lane; t < NP; t += 32) {
+      const double* qp = q + (e * NP + t) * 4;
+      const double r = qp[0];
+      const double u = qp[1] / r, v = qp[2] / r;
+      const double pr = (g - 1.0) * (qp[3] - 0.5 * r * (u * u + v * v));
+      const double a = sqrt(u * u + v * v) + sqrt(g * pr / r);
+      amax = fmax(amax, a);
+      rmin = fmin(rmin, r);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+      rmin = fmin(rmin, __shfl_xor_sync(0xffffffffu, rmin, o));
+    }
+  }
+  if (lane != 0) return;
+  const double* gq = m.geom + e * 20;
+  const double a0 = gq[0], b0 = gq[2], c0 = gq[4], d0 = gq[6];
+  const double Lx = 2.0 * sqrt(a0 * a0 + b0 * b0);
+  const double Ly = 2.0 * sqrt(c0 * c0 + d0 * d0);
+  const double h = 4.0 * fabs(a0 * d0 - c0 * b0) / fmax(Lx, Ly);
+  double nu = 0.0;
+  if (kind == K_NS) nu = fmax(4.0 / 3.0 * C.mu, C.kappa * (C.gamma - 1.0)) / rmin;
+  else if (kind == K_ADVD) nu = C.diff;
+  const double pp = (double)(n * n) * (double)(n * n);
+  lam[e] = (2 * p + 1) * amax / h + pp * nu / (h * h);
+}
+
+int launch_rk_lambda(const DiscDev& d, const double* q, double* lam, cudaStream_t st) {
+  if (d.M == 0) return 0;
+  const unsigned grid = (unsigned)((d.M * 32 + 255) / 256);
+  k_rk_lambda<<<grid, 256, 0, st>>>(d.C, d.mesh, d.p, d.kind, q, lam);
+  return (int)cudaGetLastError();
+}
 
 static __device__ int g_bad[2] = {INT_MAX, INT_MAX};
 static __device__ Status g_status = {0, 0, 0};

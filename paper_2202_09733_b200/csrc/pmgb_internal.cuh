@@ -80,6 +80,7 @@ enum EpiMode {
   EPI_STAGE_JV = 5,  // out = X/dtau + (F(q+eps X) - Fk)/eps        newton_krylov.py:402-405
   EPI_NEG_R = 6,     // out = -R(q)       (steady stage function)   time_integration.py:139-140
   EPI_OUTER_F = 7,   // out = s q - R(q) - Se                       pmg.py:325-326
+  EPI_RK = 8,        // out = Q0 + alpha cfl/(s+lam_e) ((Sb - (s q - R)) + Se)   RK smoother stage
 };
 
 struct Epi {
@@ -90,6 +91,10 @@ struct Epi {
   const double* E;    // explicit stage part
   const double* Sb;   // S_base array (or null -> sb_scalar)
   const double* Se;   // S_extra array (or null -> se_scalar)
+  const double* Q0;   // RK stage base state
+  const double* lam;  // RK per-element spectral radius (M)
+  double alpha, cfl;  // RK stage coefficient, pseudo-time CFL
+  int npe;            // dofs per element (set by the C ABI)
 };
 
 // Device-global status: first non-physical state seen since the last clear.
@@ -121,6 +126,7 @@ struct DiscDev {
 int launch_residual(const DiscDev& d, const double* q, const double* X, double eps,
                     const Epi& epi, double* out, cudaStream_t st);
 size_t fr_grad_scratch_doubles(int p, int kind, int64_t M);
+int launch_rk_lambda(const DiscDev& d, const double* q, double* lam, cudaStream_t st);
 int launch_freeze(const DiscDev& d, const double* q, double* qtr, double* fvn, cudaStream_t st);
 int launch_local_residual(const DiscDev& d, const int64_t* elems, int64_t B, const double* Q,
                           const double* qtr, const double* fvn, double* out, cudaStream_t st);

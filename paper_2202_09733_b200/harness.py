@@ -34,8 +34,22 @@ DEFAULTS = {
     "gmres.kdim": 30, "gmres.max_restarts": 10, "gmres.rtol": 1e-4,
     "pmg.levels": "3-1", "pmg.smooth": "2", "pmg.smoother": "ej", "pmg.switch_after": None,
     "pmg.mbnk.rtol": 0.1, "pmg.mbnk.maxiter": 5, "pmg.smoother_shift": 0.0,
+    "pmg.rk.cfl": 1.5, "pmg.rk.stages": "0.25,0.3333333333333333,0.5,1.0",
     "case.precond": "ej",
 }
+
+
+def pmg_precond_config(cfg) -> "pmg_mod.PmgPrecondConfig":
+    """pmg.* keys -> PmgPrecondConfig.  pmg.rk.* configure the pseudo-transient
+    RK smoother (smoother kind "rk", an extension: the reference knows only
+    ej / mbnk, harness.py:97)."""
+    h = pmg_mod.PHierarchy.parse(cfg["pmg.levels"], cfg["pmg.smooth"], cfg["pmg.smoother"],
+                                 cfg["pmg.switch_after"])
+    alphas = tuple(float(a) for a in str(cfg["pmg.rk.stages"]).split(","))
+    return pmg_mod.PmgPrecondConfig(h, mbnk_rtol=cfg["pmg.mbnk.rtol"], mbnk_maxiter=cfg["pmg.mbnk.maxiter"],
+                                    smoother_shift=cfg["pmg.smoother_shift"],
+                                    rk_cfl=float(cfg["pmg.rk.cfl"]),
+                                    rk_alphas=alphas)
 
 
 @dataclass
@@ -106,11 +120,7 @@ class ImplicitDriver:
         self.stats = SolverStats(kdim=self.krylov.kdim)
         self.ctx = None
         if self.precond == "pmg":
-            h = pmg_mod.PHierarchy.parse(cfg["pmg.levels"], cfg["pmg.smooth"], cfg["pmg.smoother"],
-                                         cfg["pmg.switch_after"])
-            pc = pmg_mod.PmgPrecondConfig(h, mbnk_rtol=cfg["pmg.mbnk.rtol"], mbnk_maxiter=cfg["pmg.mbnk.maxiter"],
-                                          smoother_shift=cfg["pmg.smoother_shift"])
-            self.ctx = pmg_mod.PmgContext(disc, pc)
+            self.ctx = pmg_mod.PmgContext(disc, pmg_precond_config(cfg))
         self._step = 0
         self._stage = 0
 
@@ -221,7 +231,8 @@ SCHEMA = {
     "gmres.kdim": (int, 30), "gmres.max_restarts": (int, 10), "gmres.rtol": (float, 1e-4),
     "pmg.levels": (str, "3-1"), "pmg.smooth": (str, "2"), "pmg.smoother": (str, "ej"),
     "pmg.switch_after": (int, None), "pmg.mbnk.rtol": (float, 0.1), "pmg.mbnk.maxiter": (int, 5),
-    "pmg.smoother_shift": (float, 0.0),
+    "pmg.smoother_shift": (float, 0.0), "pmg.rk.cfl": (float, 1.5),
+    "pmg.rk.stages": (str, "0.25,0.3333333333333333,0.5,1.0"),
     "adapt.enable": (_as_bool, False), "adapt.variable": (str, "momentum-x"), "adapt.nu_max": (float, 0.2),
     "adapt.nu_min": (float, 0.001), "adapt.p_min": (int, 1), "adapt.p_max": (int, 4),
     "adapt.every_n_steps": (int, 10),
@@ -230,7 +241,7 @@ SCHEMA = {
 _VALID_CHOICES = {
     "mesh.kind": ("box", "cylinder", "file"),
     "equation.kind": ("euler", "navier-stokes", "advection-diffusion"),
-    "case.scheme": ("esdirk2", "esdirk4", "row2", "row4"),
+    "case.scheme": ("esdirk2", "esdirk3", "esdirk4", "row2", "row4"),
     "case.solver": ("jfnk", "pmg-solver"),
     "case.precond": ("ej", "pmg", "none"),
     "case.init": ("free-stream", "zero"),
@@ -344,12 +355,7 @@ def run_case(cfg, out_dir, mesh=None) -> dict:
     try:
         if cfg["case.steady"]:
             if cfg["case.solver"] == "pmg-solver":
-                h = pmg_mod.PHierarchy.parse(cfg["pmg.levels"], cfg["pmg.smooth"], cfg["pmg.smoother"],
-                                             cfg["pmg.switch_after"])
-                pc = pmg_mod.PmgPrecondConfig(h, mbnk_rtol=cfg["pmg.mbnk.rtol"],
-                                              mbnk_maxiter=cfg["pmg.mbnk.maxiter"],
-                                              smoother_shift=cfg["pmg.smoother_shift"])
-                ctx = pmg_mod.PmgContext(disc, pc)
+                ctx = pmg_mod.PmgContext(disc, pmg_precond_config(cfg))
                 q, stats = pmg_mod.pmg_solve(ctx, q, driver.ptc)
                 driver.stats.records.append(StageRecord(0, 0, stats["iters"], 0, stats["vcycles"], 0.0))
                 for it, (absr, relr, dtau) in enumerate(stats["history"]):

@@ -10,6 +10,10 @@ line for line; vectors live on the device:
                                                  fused block-GEMV update
 * ``smooth_mbnk``                                :167-175 -> GMRES on the device
                                                  block-sparse Jacobian + block ILU0
+* ``smooth_rk`` (no reference counterpart; BASELINE north star item 3):
+  matrix-free pseudo-transient explicit RK with local pseudo-time steps,
+  one fused residual epilogue per stage (PMGB_EPI_RK) -- no element blocks
+  on that level, which is what lets config 5's p=5 fine level fit
 * ``PmgContext.prepare/vcycle/precondition``     :181-298 (incl. switch_after,
                                                  _ensure_sparse :213-253)
 * ``pmg_solve``                                  :308-374
@@ -47,8 +51,8 @@ class PHierarchy:
             raise ValueError("per-level settings must match the level count")
         if any(n < 1 for n in self.smooth):
             raise ValueError("smoothing counts must be positive")
-        if any(s not in ("ej", "mbnk") for s in self.smoothers):
-            raise ValueError("smoother kinds are 'ej' or 'mbnk'")
+        if any(s not in ("ej", "mbnk", "rk") for s in self.smoothers):
+            raise ValueError("smoother kinds are 'ej', 'mbnk' or 'rk'")
 
     @classmethod
     def parse(cls, levels: str, smooth: str = "2", smoother: str = "ej", switch_after=None):
@@ -77,10 +81,14 @@ class PmgPrecondConfig:
     mbnk_maxiter: int = 5
     omega: float = 1.0
     smoother_shift: float = 0.0
+    rk_cfl: float = 1.5
+    rk_alphas: tuple = (0.25, 1.0 / 3.0, 0.5, 1.0)
 
     def __post_init__(self):
         if self.m_max < 1:
             raise ValueError("m_max must be >= 1")
+        if self.rk_cfl <= 0.0 or not self.rk_alphas:
+            raise ValueError("RK smoother needs rk_cfl > 0 and at least one stage")
 
 
 class _Transfer:
@@ -134,6 +142,7 @@ class LevelState:
         self.frozen_q = None
         self.sparse = None  # SparseBlockMatrix (MBNK)
         self.ilu = None     # Ilu0Factors (MBNK)
+        self.lam = None     # per-element spectral radius at the frozen state (RK)
 
     def F(self, q) -> torch.Tensor:
         return self.disc.eval(to_device(q, self.disc.device), _lib.EPI_F, s=self.shift)
@@ -146,6 +155,19 @@ def smooth_ej(level: LevelState, n: int, omega: float = 1.0):
     """n sweeps of q <- q + omega B^-1 defect(q) (pmg.py:162-164)."""
     for _ in range(n):
         level.q = level.blocks.update(level.defect(), omega, level.q)
+
+
+def smooth_rk(level: LevelState, n: int, cfl: float, alphas):
+    """n sweeps of the pseudo-transient RK smoother: per sweep, from q0,
+    stage j sets q <- q0 + alpha_j dtau_e defect(q) with the local step
+    dtau_e = cfl / (s + lambda_e); each stage is one fused residual launch
+    chain (oracle: solver_oracle.Pmg._smooth, "rk")."""
+    d = level.disc
+    for _ in range(n):
+        q0 = level.q
+        for a in alphas:
+            level.q = d.eval(level.q, _lib.EPI_RK, s=level.shift, Sb=level.S_base, Se=level.S_extra,
+                             Q0=q0, lam=level.lam, alpha=a, cfl=cfl)
 
 
 def smooth_mbnk(level: LevelState, rtol: float = 0.1, maxiter: int = 5):
@@ -193,8 +215,12 @@ class PmgContext:
                 qk = self.tables[k - 1].restrict(qk)
             lev.shift = shift
             lev.frozen_q = qk
-            lev.blocks = nk.assemble_element_blocks(lev.disc, qk, shift + self.cfg.smoother_shift,
-                                                    keep_blocks=False)
+            if lev.smoother == "rk":   # matrix-free level: no element blocks
+                lev.blocks = None
+                lev.lam = lev.disc.rk_lambda(qk)
+            else:
+                lev.blocks = nk.assemble_element_blocks(lev.disc, qk, shift + self.cfg.smoother_shift,
+                                                        keep_blocks=False)
             lev.sparse = lev.ilu = None
         raise_status()
         self.cycles_done = 0
@@ -217,7 +243,10 @@ class PmgContext:
 
     def _smooth(self, k: int):
         lev = self.levels[k]
-        if self._effective_smoother(k) == "ej":
+        kind = self._effective_smoother(k)
+        if kind == "rk":
+            smooth_rk(lev, lev.nsweeps, self.cfg.rk_cfl, self.cfg.rk_alphas)
+        elif kind == "ej":
             smooth_ej(lev, lev.nsweeps, self.cfg.omega)
         else:
             self._ensure_sparse(lev)
@@ -255,7 +284,10 @@ class PmgContext:
             raise_status()
         except NonPhysicalStateError:
             self.fallbacks += 1
-            Y = fine.blocks.apply(X)
+            if fine.blocks is None:   # RK fine level: the shift (diagonal) part of the EJ fallback
+                Y = lincomb((1.0 / (self.shift + self.cfg.smoother_shift),), (X,))
+            else:
+                Y = fine.blocks.apply(X)
         else:
             Y = lincomb((1.0, -1.0), (fine.q, self.q_outer))
         return Y.cpu().numpy() if is_np else Y

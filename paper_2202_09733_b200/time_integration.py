@@ -3,7 +3,7 @@
 Drop-in for pmgflow.time_integration
 (``/root/reference/pkg/src/pmgflow/time_integration.py``): the same
 schemes (esdirk2, esdirk4, row2, row4 -- the published tableaux,
-:45-106), ``StageProblem`` / ``stage_function`` (:117-141),
+:45-106, plus a derived esdirk3 for the BASELINE configs), ``StageProblem`` / ``stage_function`` (:117-141),
 ``esdirk_step`` (:144-168) and ``row_step`` (:171-197).  The stage
 algebra runs as fused device linear combinations and the stage function
 F(q) = (q - explicit)/(a_ii dt) - R(q) is one fused residual epilogue;
@@ -100,7 +100,31 @@ def _row4():
     return StageScheme("row4", "row", 4, a, m, alpha, cm, 0.25)
 
 
-_SCHEMES = {"esdirk2": _esdirk2, "esdirk4": _esdirk4, "row2": _row2, "row4": _row4}
+def _esdirk3():
+    """Four-stage, third-order, stiffly accurate, L-stable ESDIRK (BASELINE
+    configs 1, 2 and 5 ask for "ESDIRK3"; the reference ships only esdirk2 /
+    esdirk4, time_integration.py:105-106).
+
+    Not typed in from a table: derived here from the order conditions.
+    gamma is the root in (0.4, 0.5) of gamma^3 - 3 gamma^2 + 3/2 gamma - 1/6
+    (R(inf) = 0, i.e. L-stability), c3 = 3/5, and with b = last row of A
+    (stiffly accurate), b1..b3 solve sum b = 1, b.c = 1/2, b.c^2 = 1/3 and
+    a32 solves b.(A c) = 1/6.  The result is Kennedy & Carpenter's
+    ESDIRK3(2)4L[2]SA.  tests/test_schemes.py checks it with the reference's
+    own validate_tableau / stability_function (time_integration.py:200-251)."""
+    g = 0.4358665215
+    for _ in range(4):   # Newton on the L-stability cubic
+        g -= (g ** 3 - 3.0 * g * g + 1.5 * g - 1.0 / 6.0) / (3.0 * g * g - 6.0 * g + 1.5)
+    c3 = 0.6
+    b1, b2, b3 = np.linalg.solve(np.array([[1.0, 1.0, 1.0], [0.0, 2.0 * g, c3], [0.0, 4.0 * g * g, c3 * c3]]),
+                                 np.array([1.0 - g, 0.5 - g, 1.0 / 3.0 - g]))
+    a32 = ((1.0 / 6.0 - 0.5 * g - 2.0 * g * g * b2) / b3 - g * c3) / (2.0 * g)
+    a31 = c3 - g - a32
+    a = _lower([[0.0], [g, g], [a31, a32, g], [b1, b2, b3, g]], 4)
+    return StageScheme("esdirk3", "esdirk", 3, a, a[-1].copy(), a.sum(axis=1))
+
+
+_SCHEMES = {"esdirk2": _esdirk2, "esdirk3": _esdirk3, "esdirk4": _esdirk4, "row2": _row2, "row4": _row4}
 
 
 def get_scheme(name: str) -> StageScheme:

@@ -291,3 +291,106 @@ def test_row4_step_config4_channel_walls(cuda, nx):
     q_d, info = ImplicitDriver(d, cfg).step(t(c.q0), c.dt, s)
     assert all(abs(a["iters"] - b[2]) <= 1 for a, b in zip(info, drv_o.records))
     assert rel(q_d, q_o) <= 1e-7
+
+
+# ---------------------------------------------------------------------------
+# ESDIRK3 (derived tableau, pinned by the reference's own stepper) and the
+# pseudo-transient RK smoother (north star item 3; oracle-pinned only)
+
+GE = np.load(Path(__file__).parent / "golden" / "golden_esdirk3.npz")
+
+
+def test_esdirk3_step_config1_matches_reference(cuda):
+    c = cases.config(1)
+    d = Discretization(c.mesh, c.p, c.eqn)
+    cfg = {"case.precond": "pmg", "pmg.levels": "3-2", "pmg.smooth": "2", "pmg.smoother_shift": 50.0,
+           "gmres.kdim": 30, "gmres.rtol": 1e-3, "ptc.dtau_init": c.dt, "ptc.rtol": 1e-4}
+    counts = []
+    orig = nk.gmres_solve
+
+    def logged(*a, **k):
+        r = orig(*a, **k)
+        counts.append(r[1])
+        return r
+    nk.gmres_solve = logged
+    try:
+        q1, info = ImplicitDriver(d, cfg).step(t(c.q0), c.dt, ti.get_scheme("esdirk3"))
+    finally:
+        nk.gmres_solve = orig
+    ref = list(GE["c1/esdirk3/gmres_counts"])
+    assert len(counts) == len(ref) and all(abs(a - b) <= 1 for a, b in zip(counts, ref)), (counts, ref)
+    assert [i["iters"] for i in info] == list(GE["c1/esdirk3/ptc_iters"])
+    assert rel(q1, GE["c1/esdirk3/q1"]) <= 1e-7
+
+
+@pytest.mark.parametrize("kind,p", [("ns", 3), ("ns", 4), ("euler", 2), ("advd", 3)])
+def test_rk_lambda_matches_oracle(cuda, kind, p):
+    if kind == "advd":
+        m = mm.generate_box(5, 4, 1.0, 1.0, periodic=True)
+        eqn = EquationSpec(kind="advection-diffusion", advection=(0.7, -0.3), diffusivity=0.02)
+        q0 = np.random.default_rng(2).standard_normal(m.n_elements * (p + 1) ** 2)
+    else:
+        c = cases.config(1, nx=6)
+        m, eqn = c.mesh, c.eqn if kind == "ns" else EquationSpec(kind="euler", mach=0.5)
+        o0 = OracleDisc(m, p, eqn)
+        q0 = cases._noise(np.tile(eqn.free_stream(), o0.n_dofs // 4), 1e-2, seed=4)
+    o = OracleDisc(m, p, eqn)
+    d = Discretization(m, p, eqn)
+    lam = d.rk_lambda(t(q0))
+    assert rel(lam, so.rk_spectral_radius(o, q0)) <= 1e-14
+
+
+def test_rk_stage_epilogue_matches_oracle(cuda):
+    c = cases.config(1, nx=8)
+    o = OracleDisc(c.mesh, c.p, c.eqn)
+    d = Discretization(c.mesh, c.p, c.eqn)
+    rng = np.random.default_rng(9)
+    q = c.q0
+    q0 = c.q0 * (1.0 + 1e-3 * rng.standard_normal(o.n_dofs))
+    Sb = rng.standard_normal(o.n_dofs)
+    Se = rng.standard_normal(o.n_dofs)
+    s, alpha, cfl = 7.5, 1.0 / 3.0, 1.5
+    lam = so.rk_spectral_radius(o, q)
+    out = d.eval(t(q), _lib.EPI_RK, s=s, Sb=t(Sb), Se=t(Se), Q0=t(q0), lam=t(lam), alpha=alpha, cfl=cfl)
+    npe = o.n * o.n * o.nv
+    ref = q0 + np.repeat(alpha * (cfl / (s + lam)), npe) * ((Sb - (s * q - o.residual(q))) + Se)
+    assert rel(out - t(q0), ref - q0) <= 1e-12
+    # scalar S_base / S_extra path
+    out2 = d.eval(t(q), _lib.EPI_RK, s=s, Sb=0.0, Se=0.0, Q0=t(q0), lam=t(lam), alpha=alpha, cfl=cfl)
+    ref2 = q0 + np.repeat(alpha * (cfl / (s + lam)), npe) * ((0.0 - (s * q - o.residual(q))) + 0.0)
+    assert rel(out2 - t(q0), ref2 - q0) <= 1e-12
+
+
+@pytest.mark.parametrize("nx,p,levels", [(8, 3, "3-2"), (6, 4, "4-2"), (4, 5, "5-4")])
+def test_precondition_rk_ej_matches_oracle(cuda, nx, p, levels):
+    c = cases.config(1, nx=nx)
+    o = OracleDisc(c.mesh, p, c.eqn)
+    q0 = cases._noise(cases._project(c.mesh, p, cases.isentropic_vortex(c.eqn)), 1e-6)
+    d = Discretization(c.mesh, p, c.eqn)
+    shift = 1.0 / (0.4358665215 * c.dt) + 1.0 / c.dt
+    ctx = pmg.PmgContext(d, pmg.PmgPrecondConfig(pmg.PHierarchy.parse(levels, "2", "rk-ej"), smoother_shift=50.0))
+    ctx.prepare(t(q0), shift)
+    assert ctx.levels[0].blocks is None
+    om = so.Pmg(o, levels, 2, smoother_shift=50.0, smoother="rk-ej", rk_cfl=1.5)
+    om.prepare(q0, shift)
+    X = np.random.default_rng(5).standard_normal(o.n_dofs)
+    X /= np.linalg.norm(X)
+    Y = ctx.precondition(t(X))
+    assert rel(Y, om.precondition(X)) <= 1e-9
+    assert torch.equal(Y, ctx.precondition(t(X)))
+
+
+def test_esdirk2_step_rk_ej_matches_oracle(cuda):
+    c = cases.config(1, nx=8)
+    o = OracleDisc(c.mesh, c.p, c.eqn)
+    d = Discretization(c.mesh, c.p, c.eqn)
+    s = ti.get_scheme("esdirk2")
+    drv_o = so.Driver(o, "pmg", "3-2", 2, smoother_shift=50.0, gmres_rtol=1e-3, dtau_init=c.dt, smoother="rk-ej")
+    q_o = drv_o.esdirk_step(c.q0, c.dt, s.a, s.b)
+    cfg = {"case.precond": "pmg", "pmg.levels": "3-2", "pmg.smooth": "2", "pmg.smoother": "rk-ej",
+           "pmg.smoother_shift": 50.0, "gmres.kdim": 30, "gmres.rtol": 1e-3, "ptc.dtau_init": c.dt,
+           "ptc.rtol": 1e-4}
+    q_d, info = ImplicitDriver(d, cfg).step(t(c.q0), c.dt, s)
+    assert [i["iters"] for i in info] == [r[1] for r in drv_o.records]
+    assert all(abs(a - b) <= 1 for a, b in zip([i["gmres_iters"] for i in info], [r[2] for r in drv_o.records]))
+    assert rel(q_d, q_o) <= 1e-7

@@ -31,9 +31,10 @@ def test_parse_config_errors():
     with pytest.raises(hz.ConfigError, match="bad value"):
         hz.parse_config_text("case.degree = two")
     with pytest.raises(hz.ConfigError, match="must be one of"):
-        hz.parse_config_text("case.scheme = esdirk3")
+        hz.parse_config_text("case.scheme = esdirk5")
     with pytest.raises(hz.ConfigError, match="expected 'section.key = value'"):
         hz.parse_config_text("just words")
+    assert hz.parse_config_text("case.scheme = esdirk3")["case.scheme"] == "esdirk3"  # derived tableau (extension)
     cfg = hz.parse_config_text("# comment\ncase.degree = 3  # trailing\nmesh.periodic = yes")
     assert cfg["case.degree"] == 3 and cfg["mesh.periodic"] is True and cfg["gmres.kdim"] == 30
 
