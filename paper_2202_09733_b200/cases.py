@@ -93,7 +93,7 @@ def config(k: int, seed: int = 0, nx: int | None = None) -> Case:
         eqn = EquationSpec(kind="navier-stokes", mach=0.5, reynolds=100.0, ref_length=10.0)
         q0 = _noise(_project(mesh, 3, isentropic_vortex(eqn)), 1e-6, seed)
         dt = 20.0 * explicit_dt(mesh, 3, eqn, q0)
-        return Case("config1", mesh, 3, eqn, q0, dt, "esdirk2", "3-2", 30, 1,
+        return Case("config1", mesh, 3, eqn, q0, dt, "esdirk3", "3-2", 30, 1,
                     {"smoother_shift": 50.0, "rtol": 1e-3})
     if k == 2:
         n = nx or 256
@@ -105,7 +105,7 @@ def config(k: int, seed: int = 0, nx: int | None = None) -> Case:
         # exceeds ~half the viscous spectral radius (mu (p+1)^4 / h^2 ~ 4e3
         # here); 50 (config 1's value) stalls GMRES on the device and in the
         # oracle alike, 5000 converges (4 PTC / 75 GMRES per stage)
-        return Case("config2", mesh, 4, eqn, q0, dt, "esdirk2", "4-2", 30, 10,
+        return Case("config2", mesh, 4, eqn, q0, dt, "esdirk3", "4-2", 30, 10,
                     {"smoother_shift": 5000.0, "rtol": 1e-3})
     if k == 3:
         n = nx or 128
@@ -186,5 +186,6 @@ def config(k: int, seed: int = 0, nx: int | None = None) -> Case:
         q0 = np.stack([rho, rho * u, rho * v, E], axis=-1).reshape(-1)
         del fs
         dt = 100.0 * explicit_dt(mesh, 5, eqn, q0)
-        return Case("config5", mesh, 5, eqn, q0, dt, "esdirk2", "5-4", 30, 5, {"smoother_shift": 50.0})
+        return Case("config5", mesh, 5, eqn, q0, dt, "esdirk3", "5-4", 30, 5,
+                    {"smoother_shift": 50.0, "smoother": "rk-ej"})
     raise ValueError("config index is 1..5")

@@ -215,6 +215,7 @@ class PmgContext:
                 qk = self.tables[k - 1].restrict(qk)
             lev.shift = shift
             lev.frozen_q = qk
+            lev.blocks = lev.sparse = lev.ilu = None   # free the old factors before assembling new ones
             if lev.smoother == "rk":   # matrix-free level: no element blocks
                 lev.blocks = None
                 lev.lam = lev.disc.rk_lambda(qk)

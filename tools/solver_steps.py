@@ -1,0 +1,62 @@
+"""Time JFNK-pMG steps on a BASELINE config with solver variants.
+
+    python tools/solver_steps.py CONFIG NSTEPS VARIANT [VARIANT ...]
+    VARIANT = scheme:smoothers:smoother_shift[:rk_cfl]   e.g. esdirk3:rk-ej:50:1.5
+
+Prints one JSON line per variant: per-step device wall time (synchronised),
+PTC / GMRES iteration counts, peak device memory.  Used for the DESIGN.md
+solver tables (config 2 EJ vs RK fine smoothing, config 5 at capacity).
+"""
+import json
+import sys
+import time
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+import torch  # noqa: E402
+
+from paper_2202_09733_b200 import cases  # noqa: E402
+from paper_2202_09733_b200 import time_integration as ti  # noqa: E402
+from paper_2202_09733_b200.harness import ImplicitDriver  # noqa: E402
+from paper_2202_09733_b200.spatial import Discretization  # noqa: E402
+
+
+def main():
+    k, nsteps = int(sys.argv[1]), int(sys.argv[2])
+    nx = None
+    c = cases.config(k)
+    d = Discretization(c.mesh, c.p, c.eqn)
+    for var in sys.argv[3:]:
+        parts = var.split(":")
+        scheme, smoothers, shift = parts[0], parts[1], float(parts[2])
+        cfl = float(parts[3]) if len(parts) > 3 else 1.5
+        cfg = {"case.precond": "pmg", "pmg.levels": c.levels, "pmg.smooth": "2", "pmg.smoother": smoothers,
+               "pmg.smoother_shift": shift, "pmg.rk.cfl": cfl, "gmres.kdim": c.kdim, "gmres.rtol": 1e-3,
+               "ptc.dtau_init": c.dt, "ptc.rtol": 1e-4}
+        sch = ti.get_scheme(scheme)
+        q = torch.as_tensor(c.q0, device="cuda")
+        torch.cuda.reset_peak_memory_stats()
+        rec = {"config": k, "variant": var, "dt": c.dt, "n_dofs": d.n_dofs, "steps": []}
+        try:
+            drv = ImplicitDriver(d, cfg)
+            for st in range(nsteps):
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                q, info = drv.step(q, c.dt, sch)
+                torch.cuda.synchronize()
+                el = time.perf_counter() - t0
+                rec["steps"].append({"s": round(el, 4),
+                                     "ptc": [i.get("iters") for i in info] if sch.kind == "esdirk" else None,
+                                     "gmres": [i.get("gmres_iters", i.get("iters")) for i in info]})
+                print(json.dumps({"variant": var, "step": st, **rec["steps"][-1]}), flush=True)
+        except Exception as exc:
+            rec["error"] = f"{type(exc).__name__}: {str(exc)[:300]}"
+        rec["peak_gb"] = torch.cuda.max_memory_allocated() / 1e9
+        print(json.dumps(rec), flush=True)
+        del drv
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()
