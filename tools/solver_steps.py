@@ -2,12 +2,14 @@
 
     python tools/solver_steps.py CONFIG NSTEPS VARIANT [VARIANT ...]
     VARIANT = scheme:smoothers:smoother_shift[:rk_cfl]   e.g. esdirk3:rk-ej:50:1.5
+    env: NX (mesh override), MAX_PTC, RESTARTS (caps for exploration runs)
 
 Prints one JSON line per variant: per-step device wall time (synchronised),
 PTC / GMRES iteration counts, peak device memory.  Used for the DESIGN.md
 solver tables (config 2 EJ vs RK fine smoothing, config 5 at capacity).
 """
 import json
+import os
 import sys
 import time
 from pathlib import Path
@@ -24,8 +26,10 @@ from paper_2202_09733_b200.spatial import Discretization  # noqa: E402
 
 def main():
     k, nsteps = int(sys.argv[1]), int(sys.argv[2])
-    nx = None
-    c = cases.config(k)
+    nx = int(os.environ["NX"]) if os.environ.get("NX") else None
+    t0 = time.perf_counter()
+    c = cases.config(k, nx=nx)
+    print(json.dumps({"case_built_s": round(time.perf_counter() - t0, 1), "nx": nx}), flush=True)
     d = Discretization(c.mesh, c.p, c.eqn)
     for var in sys.argv[3:]:
         parts = var.split(":")
@@ -33,13 +37,26 @@ def main():
         cfl = float(parts[3]) if len(parts) > 3 else 1.5
         cfg = {"case.precond": "pmg", "pmg.levels": c.levels, "pmg.smooth": "2", "pmg.smoother": smoothers,
                "pmg.smoother_shift": shift, "pmg.rk.cfl": cfl, "gmres.kdim": c.kdim, "gmres.rtol": 1e-3,
-               "ptc.dtau_init": c.dt, "ptc.rtol": 1e-4}
+               "ptc.dtau_init": c.dt, "ptc.rtol": 1e-4,
+               "ptc.max_iters": int(os.environ.get("MAX_PTC", 100)),
+               "gmres.max_restarts": int(os.environ.get("RESTARTS", 10))}
         sch = ti.get_scheme(scheme)
         q = torch.as_tensor(c.q0, device="cuda")
         torch.cuda.reset_peak_memory_stats()
         rec = {"config": k, "variant": var, "dt": c.dt, "n_dofs": d.n_dofs, "steps": []}
         try:
             drv = ImplicitDriver(d, cfg)
+            orig = drv.solve_stage
+
+            def logged(prob, q0, orig=orig):
+                ts = time.perf_counter()
+                qn, stt = orig(prob, q0)
+                torch.cuda.synchronize()
+                print(json.dumps({"stage_s": round(time.perf_counter() - ts, 3), "ptc": stt["iters"],
+                                  "gmres": stt["gmres_iters"], "converged": stt["converged"],
+                                  "rel": [round(h[1], 6) for h in stt["history"]][-3:]}), flush=True)
+                return qn, stt
+            drv.solve_stage = logged
             for st in range(nsteps):
                 torch.cuda.synchronize()
                 t0 = time.perf_counter()
