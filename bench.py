@@ -415,18 +415,21 @@ def time_other_configs(torch, args):
                        jv_gdofs=n * reps / t_jv / 1e9, rotating_pairs=nb)
             del qs, Rs
             if k == 3:
-                hier = pmg.PHierarchy.parse(c.levels, "2")
-                ctx = pmg.PmgContext(d, pmg.PmgPrecondConfig(hier, smoother_shift=c.extra["smoother_shift"]))
-                pmg.pmg_solve(ctx, q0, nk.PtcConfig(dtau_init=0.1, max_iters=1, rtol=1e-14))
-                torch.cuda.synchronize()
-                t0 = time.perf_counter()
-                _, stt = pmg.pmg_solve(ctx, q0, nk.PtcConfig(dtau_init=0.1, max_iters=3, rtol=1e-14))
-                torch.cuda.synchronize()
-                el = time.perf_counter() - t0
-                rec.update(pmg_solve={"levels": c.levels, "outer_iters": stt["iters"], "s": el,
-                                      "ms_per_outer_iter_incl_prepare": el / max(1, stt["iters"]) * 1e3,
-                                      "rel_history": [h[1] for h in stt["history"]]})
-                del ctx
+                # EJ on every level (reference smoothers) and BASELINE's
+                # pseudo-time RK on the levels above p=0 with EJ at p=0
+                for key, sm in (("pmg_solve", "ej"), ("pmg_solve_rk", "rk-rk-rk-rk-ej")):
+                    hier = pmg.PHierarchy.parse(c.levels, "2", sm)
+                    ctx = pmg.PmgContext(d, pmg.PmgPrecondConfig(hier, smoother_shift=c.extra["smoother_shift"]))
+                    pmg.pmg_solve(ctx, q0, nk.PtcConfig(dtau_init=0.1, max_iters=1, rtol=1e-14))
+                    torch.cuda.synchronize()
+                    t0 = time.perf_counter()
+                    _, stt = pmg.pmg_solve(ctx, q0, nk.PtcConfig(dtau_init=0.1, max_iters=3, rtol=1e-14))
+                    torch.cuda.synchronize()
+                    el = time.perf_counter() - t0
+                    rec[key] = {"levels": c.levels, "smoothers": sm, "outer_iters": stt["iters"], "s": el,
+                                "ms_per_outer_iter_incl_prepare": el / max(1, stt["iters"]) * 1e3,
+                                "rel_history": [h[1] for h in stt["history"]]}
+                    del ctx
             if k == 4:
                 cfg = {"case.precond": "pmg", "pmg.levels": c.levels, "pmg.smooth": "2",
                        "pmg.smoother_shift": c.extra["smoother_shift"], "gmres.kdim": c.kdim, "gmres.rtol": 1e-3}
@@ -516,45 +519,54 @@ def time_mbnk(torch, case2):
 
 
 def time_steps(torch, case2, args):
-    """One ESDIRK2 JFNK-pMG step at config 2 (after one warm-up step) and
-    one at config 1 beside the CPU oracle's config-1 step."""
+    """JFNK-pMG time steps (after one warm-up step each): config 1 (one
+    ESDIRK3 step, beside the CPU oracle's same step) and config 2 (ESDIRK3
+    with the reference's EJ smoothers, and with the pseudo-transient RK
+    smoother on the fine level -- north star item 3)."""
     from paper_2202_09733_b200 import cases
     from paper_2202_09733_b200 import time_integration as ti
     from paper_2202_09733_b200.harness import ImplicitDriver
     from paper_2202_09733_b200.spatial import Discretization
     out = {}
-    for k, c in ((1, cases.config(1)), (2, case2)):
-        d = Discretization(c.mesh, c.p, c.eqn)
-        cfg = {"case.precond": "pmg", "pmg.levels": c.levels, "pmg.smooth": "2",
+    c1 = cases.config(1)
+    runs = (("config1", c1, "ej-ej"), ("config2", case2, "ej-ej"), ("config2_rk", case2, "rk-ej"))
+    discs = {}
+    for key, c, smoothers in runs:
+        d = discs.setdefault(c.name, Discretization(c.mesh, c.p, c.eqn))
+        cfg = {"case.precond": "pmg", "pmg.levels": c.levels, "pmg.smooth": "2", "pmg.smoother": smoothers,
                "pmg.smoother_shift": c.extra["smoother_shift"], "gmres.kdim": c.kdim,
                "gmres.rtol": 1e-3, "ptc.dtau_init": c.dt, "ptc.rtol": 1e-4}
         q = torch.as_tensor(c.q0, device="cuda")
-        sch = ti.get_scheme("esdirk2")
-        rec = {"scheme": "esdirk2", "pmg": c.levels, "smoother_shift": c.extra["smoother_shift"],
-               "dt": c.dt}
+        sch = ti.get_scheme(c.scheme)
+        rec = {"scheme": c.scheme, "pmg": c.levels, "smoothers": smoothers,
+               "smoother_shift": c.extra["smoother_shift"], "dt": c.dt}
         try:
             drv = ImplicitDriver(d, cfg)
             drv.step(q, c.dt, sch)  # warm-up (allocator + caches)
             torch.cuda.synchronize()
+            torch.cuda.reset_peak_memory_stats()
             drv = ImplicitDriver(d, cfg)
             t0 = time.perf_counter()
             q1, info = drv.step(q, c.dt, sch)
             torch.cuda.synchronize()
             rec.update(gpu_s=time.perf_counter() - t0, ptc_iters=[i["iters"] for i in info],
-                       gmres_iters=[i["gmres_iters"] for i in info])
+                       gmres_iters=[i["gmres_iters"] for i in info],
+                       peak_device_gb=torch.cuda.max_memory_allocated() / 1e9)
+            del drv
         except Exception as exc:
             rec.update(gpu_s=None, error=str(exc)[:200])
-        out[f"config{k}"] = rec
+        torch.cuda.empty_cache()
+        out[key] = rec
     try:
         from oracle import solver_oracle as so
         from oracle.fr_oracle import OracleDisc
-        c = cases.config(1)
-        od = OracleDisc(c.mesh, c.p, c.eqn)
-        drv = so.Driver(od, "pmg", c.levels, 2, smoother_shift=50.0, gmres_rtol=1e-3, dtau_init=c.dt)
-        s = ti.get_scheme("esdirk2")
+        od = OracleDisc(c1.mesh, c1.p, c1.eqn)
+        drv = so.Driver(od, "pmg", c1.levels, 2, smoother_shift=50.0, gmres_rtol=1e-3, dtau_init=c1.dt)
+        s = ti.get_scheme(c1.scheme)
         t0 = time.perf_counter()
-        drv.esdirk_step(c.q0, c.dt, s.a, s.b)
+        drv.esdirk_step(c1.q0, c1.dt, s.a, s.b)
         out["config1"]["cpu_oracle_s"] = time.perf_counter() - t0
+        out["config1"]["cpu_oracle_gmres_iters"] = [r[2] for r in drv.records]
         out["config1"]["speedup_vs_cpu"] = out["config1"]["cpu_oracle_s"] / out["config1"]["gpu_s"]
     except Exception as exc:  # pragma: no cover
         out["config1"]["cpu_oracle_s"] = f"failed: {exc}"

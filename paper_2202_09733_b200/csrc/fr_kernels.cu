@@ -86,7 +86,8 @@ struct SL {
   // k_assemble_async: AoS q (cp.async), face fluxes, padded flux planes
   static constexpr int P_FT = Q + NV * NPT + NV * NFT;  // after A_FC (AoS q, face fluxes)
   static constexpr int P_GT = P_FT + NV * PS;
-  static constexpr size_t BYTES_ASYNC = sizeof(double) * (P_GT + NV * PS);
+  static constexpr int P_ID = P_GT + NV * PS;     // [1] padded point plane  1/det J
+  static constexpr size_t BYTES_ASYNC = sizeof(double) * (P_ID + PS);
   // compact layout of k_assemble (gradients come from k_fvn)
   static constexpr int A_FC = Q + NV * NPT;
   static constexpr int A_FT = A_FC + NV * NFT;
@@ -880,6 +881,9 @@ k_fvn(const FrConst C, const FrMesh m, const double* __restrict__ q, const doubl
     }
   }
   __syncthreads();
+  // point stage: viscous variables, and 1/det J once per point into the
+  // (now dead) q plane 0 for the column pass
+  double* sID = sQ;
   if (t0 < NPT) {
     double qq[NV], w[NW];
     const int px0 = L::pix(t0);
@@ -888,6 +892,10 @@ k_fvn(const FrConst C, const FrMesh m, const double* __restrict__ q, const doubl
     grad_vars<KIND>(qq, ph.gamma, w);
 #pragma unroll
     for (int c = 0; c < NW; ++c) sW[c * PS + px0] = w[c];
+    const int el = t0 / NP, pt = t0 % NP;
+    const Metric mt = metric(sG + el * 20);
+    const double xa = C.xg[pt / N], xb = C.xg[pt % N];
+    sID[px0] = rcp(mt.J00(xa) * mt.J11(xb) - mt.J01(xb) * mt.J10(xa));
   }
   auto face_avg = [&](int t, int el, int f, int2 lkk, double* tr_, double* nb_) {
     if (lkk.x < 0) {
@@ -1011,8 +1019,7 @@ k_fvn(const FrConst C, const FrMesh m, const double* __restrict__ q, const doubl
         dx += C.D[a * N + i] * vx[i];
         dy += C.D[a * N + i] * vy[i];
       }
-      const double xa = C.xg[a];
-      const double idet = rcp(mt.J00(xa) * j11b - j01b * mt.J10(xa));
+      const double idet = sID[el * ES + a * RS + b];
       double* px = sPX + c * PS + el * ES + a * RS + b;
       double* py = sPY + c * PS + el * ES + a * RS + b;
       const double gxv = (((*px) + dx) + C.lR[a] * cx2 - C.lL[a] * cx0) * idet;
@@ -1429,6 +1436,7 @@ k_assemble_async(const FrConst C, const FrMesh m, const double* __restrict__ q, 
   double* sFC = sm + L::A_FC;
   double* sFT = sm + L::P_FT;  // [NV] padded point planes
   double* sGT = sm + L::P_GT;
+  double* sID = sm + L::P_ID;  // 1/det J per point (point stage -> column pass)
   const int64_t e0 = (int64_t)blockIdx.x * E;
   const int64_t M = m.M;
   const int ne = (int)((M - e0) < E ? (M - e0) : E);
@@ -1532,6 +1540,8 @@ k_assemble_async(const FrConst C, const FrMesh m, const double* __restrict__ q, 
       sFT[v * PS + px0] = Ft[v];
       sGT[v * PS + px0] = Gt[v];
     }
+    const double xa = op.xg[a], xb = op.xg[b];
+    sID[px0] = rcp(mt.J00(xa) * mt.J11(xb) - mt.J01(xb) * mt.J10(xa));
   }
   __syncthreads();
   // FR divergence by line threads (one per element, line, variable); the
@@ -1582,8 +1592,6 @@ k_assemble_async(const FrConst C, const FrMesh m, const double* __restrict__ q, 
       const Metric mt = metric(gq);
       const double c2 = gq[18] * sFC[v * NFT + el * 4 * N + 2 * N + (N - 1 - b)] - t2;
       const double c0 = -gq[16] * sFC[v * NFT + el * 4 * N + 0 * N + b] - t0f;
-      const double xb = C.xg[b];
-      const double j11 = mt.J11(xb), j01 = mt.J01(xb);
       const int64_t e = e0 + el;
       double o1[N], o2[N], o3[N];
 #pragma unroll
@@ -1594,8 +1602,7 @@ k_assemble_async(const FrConst C, const FrMesh m, const double* __restrict__ q, 
         double ta = 0.0;
 #pragma unroll
         for (int i = 0; i < N; ++i) ta += C.D[a * N + i] * y[i];
-        const double xa = C.xg[a];
-        const double idet = rcp(mt.J00(xa) * j11 - j01 * mt.J10(xa));
+        const double idet = sID[el * ES + a * RS + b];
         double d = sFT[v * PS + el * ES + a * RS + b] + ta;
         d = (d + C.lR[a] * c2) - C.lL[a] * c0;
         const double R = -(d * idet);

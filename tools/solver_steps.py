@@ -1,13 +1,15 @@
 """Time JFNK-pMG steps on a BASELINE config with solver variants.
 
     python tools/solver_steps.py CONFIG NSTEPS VARIANT [VARIANT ...]
-    VARIANT = scheme:smoothers:smoother_shift[:rk_cfl]   e.g. esdirk3:rk-ej:50:1.5
+    VARIANT = scheme:smoothers:smoother_shift[:rk_cfl[:smooth[:stages]]]
+              e.g. esdirk3:rk-ej:50:1.5:1-2:0.25/0.5/1  (stages '/'-separated)
     env: NX (mesh override), MAX_PTC, RESTARTS (caps for exploration runs)
 
 Prints one JSON line per variant: per-step device wall time (synchronised),
 PTC / GMRES iteration counts, peak device memory.  Used for the DESIGN.md
 solver tables (config 2 EJ vs RK fine smoothing, config 5 at capacity).
 """
+import gc
 import json
 import os
 import sys
@@ -35,7 +37,10 @@ def main():
         parts = var.split(":")
         scheme, smoothers, shift = parts[0], parts[1], float(parts[2])
         cfl = float(parts[3]) if len(parts) > 3 else 1.5
-        cfg = {"case.precond": "pmg", "pmg.levels": c.levels, "pmg.smooth": "2", "pmg.smoother": smoothers,
+        smooth = parts[4] if len(parts) > 4 else "2"
+        stages = parts[5].replace("/", ",") if len(parts) > 5 else "0.25,0.3333333333333333,0.5,1.0"
+        cfg = {"case.precond": "pmg", "pmg.levels": c.levels, "pmg.smooth": smooth, "pmg.smoother": smoothers,
+               "pmg.rk.stages": stages,
                "pmg.smoother_shift": shift, "pmg.rk.cfl": cfl, "gmres.kdim": c.kdim, "gmres.rtol": 1e-3,
                "ptc.dtau_init": c.dt, "ptc.rtol": 1e-4,
                "ptc.max_iters": int(os.environ.get("MAX_PTC", 100)),
@@ -71,7 +76,8 @@ def main():
             rec["error"] = f"{type(exc).__name__}: {str(exc)[:300]}"
         rec["peak_gb"] = torch.cuda.max_memory_allocated() / 1e9
         print(json.dumps(rec), flush=True)
-        del drv
+        drv = None
+        gc.collect()   # drv.solve_stage = logged closes a reference cycle
         torch.cuda.empty_cache()
 
 
