@@ -79,10 +79,10 @@ enum {
   PMGB_EPI_STAGE_JV = 5, /* out = X/dtau + (F(q + eps X) - R0) / eps  */
   PMGB_EPI_NEG_R = 6,    /* out = -R                                  */
   PMGB_EPI_OUTER_F = 7,  /* out = (s q - R) - Se                      */
-  PMGB_EPI_RK = 8        /* out = Q0 + alpha dtau_e ((Sb - (s q - R)) + Se),
-                          * dtau_e = cfl / (s + lam[e]): one stage of the
-                          * pseudo-transient RK smoother (not in the
-                          * reference; BASELINE north star item 3)     */
+  PMGB_EPI_RK = 8        /* out = Q0 + alpha dtau_e[e] ((Sb - (s q - R)) + Se):
+                          * one stage of the pseudo-transient RK smoother
+                          * (not in the reference; BASELINE north star
+                          * item 3); dtau_e from pmgb_rk_dtau          */
 };
 typedef struct pmgb_epilogue {
   int32_t mode;
@@ -93,9 +93,9 @@ typedef struct pmgb_epilogue {
   const double* E;   /* device; explicit stage part */
   const double* Sb;  /* device or NULL -> sb_scalar */
   const double* Se;  /* device or NULL -> se_scalar */
-  const double* Q0;  /* device; RK stage base state  */
-  const double* lam; /* device (M); RK per-element spectral radius */
-  double alpha, cfl; /* RK stage coefficient, pseudo-time CFL */
+  const double* Q0;      /* device; RK stage base state  */
+  const double* dtau_e;  /* device (M); RK per-element pseudo-time step */
+  double alpha;          /* RK stage coefficient */
 } pmgb_epilogue;
 PMGB_API int pmgb_eval(pmgb_disc* d, const double* q, const double* X, double eps,
                        const pmgb_epilogue* epi, double* out, void* stream);
@@ -106,6 +106,10 @@ PMGB_API int pmgb_eval(pmgb_disc* d, const double* q, const double* X, double ep
  *   h_e = 4 |det J(0,0)| / max(centre-line lengths).  No reference
  * counterpart (the reference's smoothers are EJ / MBNK, pmg.py:162-175). */
 PMGB_API int pmgb_rk_lambda(pmgb_disc* d, const double* q, double* lam, void* stream);
+
+/* RK local pseudo-time steps dtau[e] = cfl / (s + lam[e]) (M elements,
+ * device buffers), once per smoothing sweep set. */
+PMGB_API int pmgb_rk_dtau(int64_t M, const double* lam, double s, double cfl, double* dtau, void* stream);
 
 /* (shift I - dR/dq) X ~ shift X - (R(q+eps X) - R0)/eps
  * -- newton_krylov.py:71-76. */

@@ -38,7 +38,7 @@ class Epilogue(ctypes.Structure):
         ("s", ctypes.c_double), ("eps", ctypes.c_double), ("adt", ctypes.c_double),
         ("dtau", ctypes.c_double), ("sb_scalar", ctypes.c_double), ("se_scalar", ctypes.c_double),
         ("X", c_void_p), ("R0", c_void_p), ("E", c_void_p), ("Sb", c_void_p), ("Se", c_void_p),
-        ("Q0", c_void_p), ("lam", c_void_p), ("alpha", ctypes.c_double), ("cfl", ctypes.c_double),
+        ("Q0", c_void_p), ("dtau_e", c_void_p), ("alpha", ctypes.c_double),
     ]
 
 
@@ -51,6 +51,8 @@ SIGNATURES = {
     "pmgb_disc_n_dofs": (ctypes.c_int64, [c_void_p]),
     "pmgb_residual": (ctypes.c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
     "pmgb_rk_lambda": (ctypes.c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
+    "pmgb_rk_dtau": (ctypes.c_int, [ctypes.c_int64, c_void_p, ctypes.c_double, ctypes.c_double, c_void_p,
+                                    c_void_p]),
     "pmgb_eval": (ctypes.c_int, [c_void_p, c_void_p, c_void_p, ctypes.c_double,
                                  ctypes.POINTER(Epilogue), c_void_p, c_void_p]),
     "pmgb_jfnk_matvec": (ctypes.c_int, [c_void_p, c_void_p, c_void_p, c_void_p, ctypes.c_double,

@@ -27,6 +27,7 @@ int launch_dot(int64_t n, const double* x, const double* y, double* out, int do_
 int launch_mgs(int64_t n, double* V, int64_t ld, int j, double* w, double* H, double thresh, int* finite_flag,
                cudaStream_t st);
 int launch_lincomb(int64_t n, int k, const double* c, const double* const* xs, double* out, cudaStream_t st);
+int launch_rk_dtau(int64_t M, const double* lam, double s, double cfl, double* dtau, cudaStream_t st);
 int launch_gemv_t(int64_t n, int k, const double* V, int64_t ld, const double* y, double* out, cudaStream_t st);
 int launch_any_nonzero(int64_t n, const double* x, int* flag_dev, cudaStream_t st);
 int launch_probe_fp64(int64_t iters, int blocks, double* out, cudaStream_t st);
@@ -158,11 +159,10 @@ PMGB_API int pmgb_eval(pmgb_disc* h, const double* q, const double* X, double ep
   ep.Sb = e->Sb;
   ep.Se = e->Se;
   ep.Q0 = e->Q0;
-  ep.lam = e->lam;
+  ep.dtau_e = e->dtau_e;
   ep.alpha = e->alpha;
-  ep.cfl = e->cfl;
   ep.npe = (int)((h->d.p + 1) * (h->d.p + 1) * h->d.nv);
-  if (ep.mode == EPI_RK && (!ep.Q0 || !ep.lam)) return -1;
+  if (ep.mode == EPI_RK && (!ep.Q0 || !ep.dtau_e)) return -1;
   g_launches += n_res_launches(h->d);
   return launch_residual(h->d, q, X, eps, ep, out, S(stream));
 }
@@ -190,6 +190,12 @@ PMGB_API int pmgb_rk_lambda(pmgb_disc* h, const double* q, double* lam, void* st
   if (!h || (h->d.M > 0 && (!q || !lam))) return -1;
   g_launches += 1;
   return launch_rk_lambda(h->d, q, lam, S(stream));
+}
+
+PMGB_API int pmgb_rk_dtau(int64_t M, const double* lam, double s, double cfl, double* dtau, void* stream) {
+  if (M > 0 && (!lam || !dtau)) return -1;
+  g_launches += 1;
+  return launch_rk_dtau(M, lam, s, cfl, dtau, S(stream));
 }
 
 PMGB_API int pmgb_freeze(pmgb_disc* h, const double* q, double* qtr, double* fvn, void* stream) {

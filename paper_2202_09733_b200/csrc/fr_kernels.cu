@@ -26,6 +26,9 @@
 #ifndef PMGB_FVN_REGS_P5
 #define PMGB_FVN_REGS_P5 80
 #endif
+#ifndef PMGB_IDET_SMEM
+#define PMGB_IDET_SMEM 0   // 1/det J once per point in shared memory (measured: slower)
+#endif
 #ifndef PMGB_TRACE_REGS
 #define PMGB_TRACE_REGS 40
 #endif
@@ -87,7 +90,7 @@ struct SL {
   static constexpr int P_FT = Q + NV * NPT + NV * NFT;  // after A_FC (AoS q, face fluxes)
   static constexpr int P_GT = P_FT + NV * PS;
   static constexpr int P_ID = P_GT + NV * PS;     // [1] padded point plane  1/det J
-  static constexpr size_t BYTES_ASYNC = sizeof(double) * (P_ID + PS);
+  static constexpr size_t BYTES_ASYNC = sizeof(double) * (P_ID + (PMGB_IDET_SMEM ? PS : 0));
   // compact layout of k_assemble (gradients come from k_fvn)
   static constexpr int A_FC = Q + NV * NPT;
   static constexpr int A_FT = A_FC + NV * NFT;
@@ -892,10 +895,12 @@ k_fvn(const FrConst C, const FrMesh m, const double* __restrict__ q, const doubl
     grad_vars<KIND>(qq, ph.gamma, w);
 #pragma unroll
     for (int c = 0; c < NW; ++c) sW[c * PS + px0] = w[c];
-    const int el = t0 / NP, pt = t0 % NP;
-    const Metric mt = metric(sG + el * 20);
-    const double xa = C.xg[pt / N], xb = C.xg[pt % N];
-    sID[px0] = rcp(mt.J00(xa) * mt.J11(xb) - mt.J01(xb) * mt.J10(xa));
+    if constexpr (PMGB_IDET_SMEM) {
+      const int el = t0 / NP, pt = t0 % NP;
+      const Metric mt = metric(sG + el * 20);
+      const double xa = C.xg[pt / N], xb = C.xg[pt % N];
+      sID[px0] = rcp(mt.J00(xa) * mt.J11(xb) - mt.J01(xb) * mt.J10(xa));
+    }
   }
   auto face_avg = [&](int t, int el, int f, int2 lkk, double* tr_, double* nb_) {
     if (lkk.x < 0) {
@@ -1019,7 +1024,13 @@ k_fvn(const FrConst C, const FrMesh m, const double* __restrict__ q, const doubl
         dx += C.D[a * N + i] * vx[i];
         dy += C.D[a * N + i] * vy[i];
       }
-      const double idet = sID[el * ES + a * RS + b];
+      double idet;
+      if constexpr (PMGB_IDET_SMEM) {
+        idet = sID[el * ES + a * RS + b];
+      } else {
+        const double xa = C.xg[a];
+        idet = rcp(mt.J00(xa) * j11b - j01b * mt.J10(xa));
+      }
       double* px = sPX + c * PS + el * ES + a * RS + b;
       double* py = sPY + c * PS + el * ES + a * RS + b;
       const double gxv = (((*px) + dx) + C.lR[a] * cx2 - C.lL[a] * cx0) * idet;
@@ -1102,9 +1113,11 @@ k_fvn(const FrConst C, const FrMesh m, const double* __restrict__ q, const doubl
 // phase 3: common fluxes, volume fluxes, FR divergence, fused epilogue
 
 // RK smoother stage (EPI_RK), rounded as the oracle's NumPy expression
-//   dtau_e = cfl / (s + lam_e);  c = alpha dtau_e;  q0 + c ((Sb - (s q - R)) + Se)
+//   c = alpha dtau_e;  q0 + c ((Sb - (s q - R)) + Se)
+// (dtau_e = cfl / (s + lam_e) comes precomputed per element from k_rk_dtau,
+// so the epilogue carries no division)
 __device__ __forceinline__ double epi_rk_coef(const Epi& ep, int64_t e) {
-  return __dmul_rn(ep.alpha, __ddiv_rn(ep.cfl, __dadd_rn(ep.s, __ldg(ep.lam + e))));
+  return __dmul_rn(ep.alpha, __ldg(ep.dtau_e + e));
 }
 __device__ __forceinline__ double epi_rk(const Epi& ep, double c, double R, double qv, double sb, double se,
                                          double q0) {
@@ -1112,7 +1125,13 @@ __device__ __forceinline__ double epi_rk(const Epi& ep, double c, double R, doub
   return __dadd_rn(q0, __dmul_rn(c, d));
 }
 
+template <bool RKE = false>
 __device__ __forceinline__ double epi_apply(const Epi& ep, int64_t i, double R, double qv) {
+  if constexpr (RKE) {
+    const double sb = ep.Sb ? ep.Sb[i] : ep.sb_scalar;
+    const double se = ep.Se ? ep.Se[i] : ep.se_scalar;
+    return epi_rk(ep, epi_rk_coef(ep, i / ep.npe), R, qv, sb, se, ep.Q0[i]);
+  }
   switch (ep.mode) {
     case EPI_R:
       return R;
@@ -1137,11 +1156,6 @@ __device__ __forceinline__ double epi_apply(const Epi& ep, int64_t i, double R, 
       const double se = ep.Se ? ep.Se[i] : ep.se_scalar;
       return (ep.s * qv - R) - se;
     }
-    case EPI_RK: {
-      const double sb = ep.Sb ? ep.Sb[i] : ep.sb_scalar;
-      const double se = ep.Se ? ep.Se[i] : ep.se_scalar;
-      return epi_rk(ep, epi_rk_coef(ep, i / ep.npe), R, qv, sb, se, ep.Q0[i]);
-    }
   }
   return R;
 }
@@ -1149,11 +1163,8 @@ __device__ __forceinline__ double epi_apply(const Epi& ep, int64_t i, double R, 
 // Epilogue with operands preloaded by the caller:
 //   JV: o1 = X, o2 = R0;  STAGE_F: o3 = E;  STAGE_JV: o1 = X, o2 = Fk, o3 = E;
 //   DEFECT: o1 = Sb, o2 = Se;  OUTER_F: o2 = Se
-__device__ __forceinline__ double epi_pre(const Epi& ep, double R, double qv, double o1, double o2, double o3,
-                                          double ce = 0.0) {
+__device__ __forceinline__ double epi_pre(const Epi& ep, double R, double qv, double o1, double o2, double o3) {
   switch (ep.mode) {
-    case EPI_RK:
-      return epi_rk(ep, ce, R, qv, o1, o2, o3);
     case EPI_R:
       return R;
     case EPI_F:
@@ -1176,7 +1187,14 @@ __device__ __forceinline__ double epi_pre(const Epi& ep, double R, double qv, do
   return R;
 }
 
+template <bool RKE = false>
 __device__ __forceinline__ void epi_load(const Epi& ep, int64_t i, double& o1, double& o2, double& o3) {
+  if constexpr (RKE) {   // RK stage: o1 = Sb, o2 = Se, o3 = Q0
+    o1 = ep.Sb ? __ldg(ep.Sb + i) : ep.sb_scalar;
+    o2 = ep.Se ? __ldg(ep.Se + i) : ep.se_scalar;
+    o3 = __ldg(ep.Q0 + i);
+    return;
+  }
   o1 = o2 = o3 = 0.0;
   switch (ep.mode) {
     case EPI_JV:
@@ -1198,11 +1216,6 @@ __device__ __forceinline__ void epi_load(const Epi& ep, int64_t i, double& o1, d
     case EPI_OUTER_F:
       o2 = ep.Se ? __ldg(ep.Se + i) : ep.se_scalar;
       break;
-    case EPI_RK:
-      o1 = ep.Sb ? __ldg(ep.Sb + i) : ep.sb_scalar;
-      o2 = ep.Se ? __ldg(ep.Se + i) : ep.se_scalar;
-      o3 = __ldg(ep.Q0 + i);
-      break;
     default:
       break;
   }
@@ -1221,7 +1234,7 @@ __device__ __forceinline__ void commit_status(int* bad, Status* st) {
   }
 }
 
-template <int P, int KIND>
+template <int P, int KIND, bool RKE = false>
 __global__ void __launch_bounds__(BC<P>::THREADS, MinBlocks<P>::ASM)
 k_assemble(const FrConst C, const FrMesh m, const double* __restrict__ q, const double* __restrict__ qtr,
            const double* __restrict__ fvn, const double* __restrict__ grad, const Epi ep,
@@ -1398,7 +1411,7 @@ k_assemble(const FrConst C, const FrMesh m, const double* __restrict__ q, const 
       const int64_t base = (e * NP + pt) * NV;
       double o[NV];
 #pragma unroll
-      for (int v = 0; v < NV; ++v) o[v] = epi_apply(ep, base + v, R[v], sQ[v * NPT + t0]);
+      for (int v = 0; v < NV; ++v) o[v] = epi_apply<RKE>(ep, base + v, R[v], sQ[v * NPT + t0]);
       st_face<NV>(out + base, o);
     }
   }
@@ -1418,7 +1431,9 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // q and geometry go to shared memory by cp.async while the face threads
 // gather their traces / fluxes and evaluate the common face fluxes straight
 // from registers; the first barrier only guards the point stage.
-template <int P, int KIND>
+// RKE: the RK-smoother stage epilogue is a separate instantiation (carrying
+// its operand path in the R / Jv kernels measured 2.5 % on R at config 2)
+template <int P, int KIND, bool RKE = false>
 __global__ void __launch_bounds__(BC<P>::THREADS, MinBlocks<P>::ASM)
 k_assemble_async(const FrConst C, const FrMesh m, const double* __restrict__ q, const double* __restrict__ qtr,
                  const double* __restrict__ fvn, const double* __restrict__ grad, const Epi ep,
@@ -1540,8 +1555,10 @@ k_assemble_async(const FrConst C, const FrMesh m, const double* __restrict__ q, 
       sFT[v * PS + px0] = Ft[v];
       sGT[v * PS + px0] = Gt[v];
     }
-    const double xa = op.xg[a], xb = op.xg[b];
-    sID[px0] = rcp(mt.J00(xa) * mt.J11(xb) - mt.J01(xb) * mt.J10(xa));
+    if constexpr (PMGB_IDET_SMEM) {
+      const double xa = op.xg[a], xb = op.xg[b];
+      sID[px0] = rcp(mt.J00(xa) * mt.J11(xb) - mt.J01(xb) * mt.J10(xa));
+    }
   }
   __syncthreads();
   // FR divergence by line threads (one per element, line, variable); the
@@ -1592,23 +1609,32 @@ k_assemble_async(const FrConst C, const FrMesh m, const double* __restrict__ q, 
       const Metric mt = metric(gq);
       const double c2 = gq[18] * sFC[v * NFT + el * 4 * N + 2 * N + (N - 1 - b)] - t2;
       const double c0 = -gq[16] * sFC[v * NFT + el * 4 * N + 0 * N + b] - t0f;
+      const double xb = C.xg[b];
+      const double j11 = mt.J11(xb), j01 = mt.J01(xb);
       const int64_t e = e0 + el;
       double o1[N], o2[N], o3[N];
 #pragma unroll
-      for (int a = 0; a < N; ++a) epi_load(ep, (e * NP + a * N + b) * NV + v, o1[a], o2[a], o3[a]);
-      const double ce = ep.mode == EPI_RK ? epi_rk_coef(ep, e) : 0.0;
+      for (int a = 0; a < N; ++a) epi_load<RKE>(ep, (e * NP + a * N + b) * NV + v, o1[a], o2[a], o3[a]);
+      const double ce = RKE ? epi_rk_coef(ep, e) : 0.0;
 #pragma unroll
       for (int a = 0; a < N; ++a) {
         double ta = 0.0;
 #pragma unroll
         for (int i = 0; i < N; ++i) ta += C.D[a * N + i] * y[i];
-        const double idet = sID[el * ES + a * RS + b];
+        double idet;
+        if constexpr (PMGB_IDET_SMEM) {
+          idet = sID[el * ES + a * RS + b];
+        } else {
+          const double xa = C.xg[a];
+          idet = rcp(mt.J00(xa) * j11 - j01 * mt.J10(xa));
+        }
         double d = sFT[v * PS + el * ES + a * RS + b] + ta;
         d = (d + C.lR[a] * c2) - C.lL[a] * c0;
         const double R = -(d * idet);
         const int pt = a * N + b;
         const int64_t gi = (e * NP + pt) * NV + v;
-        out[gi] = epi_pre(ep, R, sQA[(el * NP + pt) * NV + v], o1[a], o2[a], o3[a], ce);
+        const double qv = sQA[(el * NP + pt) * NV + v];
+        out[gi] = RKE ? epi_rk(ep, ce, R, qv, o1[a], o2[a], o3[a]) : epi_pre(ep, R, qv, o1[a], o2[a], o3[a]);
       }
     }
   }
@@ -2181,8 +2207,12 @@ static int run_residual(const DiscDev& d, const double* q, const double* X, doub
     cudaFuncSetAttribute(k_trace<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES_TRACE);
     cudaFuncSetAttribute(k_fvn<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES_FVN);
     cudaFuncSetAttribute(k_assemble<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES_ASM);
-    if constexpr (KT<KIND>::NV == 4 && E * BC<P>::NF <= TH)
+    cudaFuncSetAttribute(k_assemble<P, KIND, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES_ASM);
+    if constexpr (KT<KIND>::NV == 4 && E * BC<P>::NF <= TH) {
       cudaFuncSetAttribute(k_assemble_async<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES_ASYNC);
+      cudaFuncSetAttribute(k_assemble_async<P, KIND, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)L::BYTES_ASYNC);
+    }
   }
   int* bad = nullptr;
   Status* stp = nullptr;
@@ -2200,9 +2230,14 @@ static int run_residual(const DiscDev& d, const double* q, const double* X, doub
   const int q_dep = X != nullptr;
   if (KT<KIND>::VISC) launch_pdl(k_fvn<P, KIND>, grid, TH, L::BYTES_FVN, st, d.C, d.mesh, qq, (const double*)d.qtr,
                                  d.fvn, d.grad, q_dep);
+  const bool rk = epi.mode == EPI_RK;
   if constexpr (KT<KIND>::NV == 4 && E * BC<P>::NF <= TH)
-    launch_pdl(k_assemble_async<P, KIND>, grid, TH, L::BYTES_ASYNC, st, d.C, d.mesh, qq, (const double*)d.qtr,
-               (const double*)d.fvn, (const double*)d.grad, epi, out, bad, stp, q_dep);
+    launch_pdl(rk ? k_assemble_async<P, KIND, true> : k_assemble_async<P, KIND, false>, grid, TH, L::BYTES_ASYNC,
+               st, d.C, d.mesh, qq, (const double*)d.qtr, (const double*)d.fvn, (const double*)d.grad, epi, out,
+               bad, stp, q_dep);
+  else if (rk)
+    k_assemble<P, KIND, true><<<grid, TH, L::BYTES_ASM, st>>>(d.C, d.mesh, qq, d.qtr, d.fvn, d.grad, epi, out, bad,
+                                                               stp);
   else
     k_assemble<P, KIND><<<grid, TH, L::BYTES_ASM, st>>>(d.C, d.mesh, qq, d.qtr, d.fvn, d.grad, epi, out, bad, stp);
   return (int)cudaGetLastError();

@@ -248,6 +248,20 @@ int launch_lincomb(int64_t n, int k, const double* c, const double* const* xs, d
   return (int)cudaGetLastError();
 }
 
+// RK smoother local pseudo-time steps: dtau[e] = cfl / (s + lam[e])
+// (IEEE division, rounded as the oracle's NumPy expression)
+__global__ void k_rk_dtau(int64_t M, const double* __restrict__ lam, double s, double cfl,
+                          double* __restrict__ dtau) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < M; e += (int64_t)gridDim.x * blockDim.x)
+    dtau[e] = __ddiv_rn(cfl, __dadd_rn(s, lam[e]));
+}
+
+int launch_rk_dtau(int64_t M, const double* lam, double s, double cfl, double* dtau, cudaStream_t st) {
+  if (M == 0) return 0;
+  k_rk_dtau<<<ew_grid(M), 256, 0, st>>>(M, lam, s, cfl, dtau);
+  return (int)cudaGetLastError();
+}
+
 int launch_gemv_t(int64_t n, int k, const double* V, int64_t ld, const double* y, double* out, cudaStream_t st) {
   if (k < 1 || k > 128) return -1001;
   k_gemv_t<<<ew_grid(n), 256, 0, st>>>(n, k, V, ld, y, out);

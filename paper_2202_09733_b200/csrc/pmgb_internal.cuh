@@ -80,7 +80,7 @@ enum EpiMode {
   EPI_STAGE_JV = 5,  // out = X/dtau + (F(q+eps X) - Fk)/eps        newton_krylov.py:402-405
   EPI_NEG_R = 6,     // out = -R(q)       (steady stage function)   time_integration.py:139-140
   EPI_OUTER_F = 7,   // out = s q - R(q) - Se                       pmg.py:325-326
-  EPI_RK = 8,        // out = Q0 + alpha cfl/(s+lam_e) ((Sb - (s q - R)) + Se)   RK smoother stage
+  EPI_RK = 8,        // out = Q0 + alpha dtau_e ((Sb - (s q - R)) + Se)   RK smoother stage
 };
 
 struct Epi {
@@ -92,8 +92,8 @@ struct Epi {
   const double* Sb;   // S_base array (or null -> sb_scalar)
   const double* Se;   // S_extra array (or null -> se_scalar)
   const double* Q0;   // RK stage base state
-  const double* lam;  // RK per-element spectral radius (M)
-  double alpha, cfl;  // RK stage coefficient, pseudo-time CFL
+  const double* dtau_e;  // RK per-element pseudo-time step (M)
+  double alpha;          // RK stage coefficient
   int npe;            // dofs per element (set by the C ABI)
 };
 

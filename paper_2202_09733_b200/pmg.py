@@ -163,11 +163,12 @@ def smooth_rk(level: LevelState, n: int, cfl: float, alphas):
     dtau_e = cfl / (s + lambda_e); each stage is one fused residual launch
     chain (oracle: solver_oracle.Pmg._smooth, "rk")."""
     d = level.disc
+    dtau_e = d.rk_dtau(level.lam, level.shift, cfl)
     for _ in range(n):
         q0 = level.q
         for a in alphas:
             level.q = d.eval(level.q, _lib.EPI_RK, s=level.shift, Sb=level.S_base, Se=level.S_extra,
-                             Q0=q0, lam=level.lam, alpha=a, cfl=cfl)
+                             Q0=q0, dtau_e=dtau_e, alpha=a)
 
 
 def smooth_mbnk(level: LevelState, rtol: float = 0.1, maxiter: int = 5):

@@ -221,8 +221,8 @@ class Discretization:
     # -- device entry points ---------------------------------------------------
 
     def eval(self, q: torch.Tensor, mode: int, out: torch.Tensor | None = None, *, X=None, eps=0.0,
-             s=0.0, adt=0.0, dtau=0.0, R0=None, E=None, Sb=0.0, Se=0.0, Q0=None, lam=None, alpha=0.0,
-             cfl=0.0, check_status=False):
+             s=0.0, adt=0.0, dtau=0.0, R0=None, E=None, Sb=0.0, Se=0.0, Q0=None, dtau_e=None, alpha=0.0,
+             check_status=False):
         """Fused residual + epilogue (see include/pmgflow_b200.h, PMGB_EPI_*)."""
         if out is None:
             out = torch.empty(self.n_dofs, dtype=torch.float64, device=self.device)
@@ -241,8 +241,8 @@ class Discretization:
         else:
             ep.se_scalar = float(Se)
         ep.Q0 = ptr(Q0) if Q0 is not None else None
-        ep.lam = ptr(lam) if lam is not None else None
-        ep.alpha, ep.cfl = float(alpha), float(cfl)
+        ep.dtau_e = ptr(dtau_e) if dtau_e is not None else None
+        ep.alpha = float(alpha)
         xp = ptr(X) if (X is not None and mode in (_lib.EPI_JV, _lib.EPI_STAGE_JV)) else None
         check(load().pmgb_eval(self._h, ptr(q), xp, float(eps), ctypes.byref(ep), ptr(out), stream()), "eval")
         if check_status:
@@ -255,6 +255,13 @@ class Discretization:
         lam = torch.empty(self.mesh.n_elements, dtype=torch.float64, device=self.device)
         check(load().pmgb_rk_lambda(self._h, ptr(q), lam.data_ptr(), stream()), "rk_lambda")
         return lam
+
+    def rk_dtau(self, lam: torch.Tensor, s: float, cfl: float) -> torch.Tensor:
+        """Local pseudo-time steps cfl / (s + lam_e) (pmgb_rk_dtau)."""
+        out = torch.empty_like(lam)
+        check(load().pmgb_rk_dtau(lam.numel(), lam.data_ptr(), float(s), float(cfl), out.data_ptr(), stream()),
+              "rk_dtau")
+        return out
 
     def residual(self, data):
         """R(q); NumPy in -> NumPy out (end-to-end), CUDA tensor -> tensor."""

@@ -351,12 +351,14 @@ def test_rk_stage_epilogue_matches_oracle(cuda):
     Se = rng.standard_normal(o.n_dofs)
     s, alpha, cfl = 7.5, 1.0 / 3.0, 1.5
     lam = so.rk_spectral_radius(o, q)
-    out = d.eval(t(q), _lib.EPI_RK, s=s, Sb=t(Sb), Se=t(Se), Q0=t(q0), lam=t(lam), alpha=alpha, cfl=cfl)
+    dtau = d.rk_dtau(t(lam), s, cfl)
+    assert np.array_equal(dtau.cpu().numpy(), cfl / (s + lam))   # IEEE division, bitwise
+    out = d.eval(t(q), _lib.EPI_RK, s=s, Sb=t(Sb), Se=t(Se), Q0=t(q0), dtau_e=dtau, alpha=alpha)
     npe = o.n * o.n * o.nv
     ref = q0 + np.repeat(alpha * (cfl / (s + lam)), npe) * ((Sb - (s * q - o.residual(q))) + Se)
     assert rel(out - t(q0), ref - q0) <= 1e-12
     # scalar S_base / S_extra path
-    out2 = d.eval(t(q), _lib.EPI_RK, s=s, Sb=0.0, Se=0.0, Q0=t(q0), lam=t(lam), alpha=alpha, cfl=cfl)
+    out2 = d.eval(t(q), _lib.EPI_RK, s=s, Sb=0.0, Se=0.0, Q0=t(q0), dtau_e=dtau, alpha=alpha)
     ref2 = q0 + np.repeat(alpha * (cfl / (s + lam)), npe) * ((0.0 - (s * q - o.residual(q))) + 0.0)
     assert rel(out2 - t(q0), ref2 - q0) <= 1e-12
 
