@@ -3,7 +3,8 @@
     python tools/solver_steps.py CONFIG NSTEPS VARIANT [VARIANT ...]
     VARIANT = scheme:smoothers:smoother_shift[:rk_cfl[:smooth[:stages]]]
               e.g. esdirk3:rk-ej:50:1.5:1-2:0.25/0.5/1  (stages '/'-separated)
-    env: NX (mesh override), MAX_PTC, RESTARTS (caps for exploration runs)
+    env: NX (mesh override), MAX_PTC, RESTARTS (caps for exploration runs),
+         DT_SCALE (multiplies the case's dt)
 
 Prints one JSON line per variant: per-step device wall time (synchronised),
 PTC / GMRES iteration counts, peak device memory.  Used for the DESIGN.md
@@ -31,7 +32,9 @@ def main():
     nx = int(os.environ["NX"]) if os.environ.get("NX") else None
     t0 = time.perf_counter()
     c = cases.config(k, nx=nx)
-    print(json.dumps({"case_built_s": round(time.perf_counter() - t0, 1), "nx": nx}), flush=True)
+    if os.environ.get("DT_SCALE"):
+        c.dt *= float(os.environ["DT_SCALE"])
+    print(json.dumps({"case_built_s": round(time.perf_counter() - t0, 1), "nx": nx, "dt": c.dt}), flush=True)
     d = Discretization(c.mesh, c.p, c.eqn)
     for var in sys.argv[3:]:
         parts = var.split(":")
