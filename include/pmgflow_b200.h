@@ -56,6 +56,8 @@ typedef struct pmgb_disc_desc {
   const double* geom;         /* (M, 20) see mesh.pack_geometry          */
   const int64_t* links;       /* (M, 4, 4) nb elem|-1, nb face, rev, is_left */
   const int32_t* tags;        /* (M, 4) boundary tag code, -1 interior    */
+  int32_t riemann;            /* 0 Roe (reference), 1 Rusanov (option)   */
+  int32_t viscous_scheme;     /* 0 BR1 (reference), 1 LDG (option)       */
 } pmgb_disc_desc;
 
 PMGB_API int pmgb_disc_create(const pmgb_disc_desc* desc, pmgb_disc** out);

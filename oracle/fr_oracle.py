@@ -90,6 +90,23 @@ def roe_flux(qL, qR, nrm, gamma):
     return fn - 0.5 * diss
 
 
+def rusanov_flux(qL, qR, nrm, gamma):
+    """Local Lax-Friedrichs flux along the unit normal (BASELINE configs'
+    interface flux; not in the reference -- parity unpinned):
+    F = 1/2 (f(qL) + f(qR)).n - 1/2 lambda (qR - qL),
+    lambda = max(|u_L.n| + c_L, |u_R.n| + c_R)."""
+    nx, ny = nrm[..., 0], nrm[..., 1]
+    rL, uL, vL, pL = primitive(qL, gamma)
+    rR, uR, vR, pR = primitive(qR, gamma)
+    aL = np.abs(uL * nx + vL * ny) + np.sqrt(gamma * pL / rL)
+    aR = np.abs(uR * nx + vR * ny) + np.sqrt(gamma * pR / rR)
+    lam = np.maximum(aL, aR)
+    fxL, fyL = euler_flux(qL, gamma)
+    fxR, fyR = euler_flux(qR, gamma)
+    fn = 0.5 * (fxL + fxR) * nx[..., None] + 0.5 * (fyL + fyR) * ny[..., None]
+    return fn - (0.5 * lam)[..., None] * (qR - qL)
+
+
 def viscous_flux(q, gx, gy, mu, kappa):
     """Stokes stress + Fourier heat flux from grads of (u, v, T)."""
     rho = q[..., 0]
@@ -212,7 +229,27 @@ class OracleDisc:
             ax, ay = self.eqn.advection
             an = (ax * nrm[..., 0] + ay * nrm[..., 1])[..., None]
             return 0.5 * an * (qa + qc) - 0.5 * np.abs(an) * (qc - qa)
+        if self.eqn.riemann == "rusanov":
+            return rusanov_flux(qa, qc, nrm, self.eqn.gamma)
         return roe_flux(qa, qc, nrm, self.eqn.gamma)
+
+    # -- viscous interface values: BR1 (reference) or LDG (option) ----------
+    # LDG with C11 = 0 and the switch pointing from each interior face's L
+    # element (is_left) to its R element: the common solution value is L's
+    # trace, the common viscous flux R's one-sided flux.  Boundary faces keep
+    # the BR1 treatment (ghost average, own one-sided flux).
+
+    def _common_w(self, inter, left_own, w_own, w_out):
+        if self.eqn.viscous_scheme == "ldg":
+            return np.where(inter, np.where(left_own, w_own, w_out), 0.5 * (w_own + w_out))
+        return 0.5 * (w_own + w_out)
+
+    def _common_fv(self, inter, left_own, fvn, fvn_nb):
+        """fvn: own one-sided viscous normal flux; fvn_nb: MINUS the
+        neighbour's (i.e. the neighbour's flux on our normal)."""
+        if self.eqn.viscous_scheme == "ldg":
+            return np.where(inter, np.where(left_own, fvn_nb, fvn), fvn)
+        return np.where(inter, 0.5 * (fvn + fvn_nb), fvn)
 
     def _vflux(self, Q, gx, gy):
         if self.eqn.kind == "advection-diffusion":
@@ -284,10 +321,11 @@ class OracleDisc:
             return self._assemble(e, Q, Fc, None).reshape(-1)
         W = self._grad_vars(Q)
         w_own = self._grad_vars(tr)
-        What = 0.5 * (w_own + self._grad_vars(nb_tr))
+        lo = self.is_left[..., None, None]
+        What = self._common_w(inter, lo, w_own, self._grad_vars(nb_tr))
         grads = self._gradient(e, W, What)
         fvn = self._fvn(e, tr, *grads)
-        Fv = np.where(inter, 0.5 * (fvn - self._gather_nb(fvn)), fvn)
+        Fv = self._common_fv(inter, lo, fvn, -self._gather_nb(fvn))
         if eqn.kind == "navier-stokes":
             wall = (self.tag == WALL_ADIABATIC)[..., None]
             Fv[..., 3] = np.where(wall, 0.0, Fv[..., 3])
@@ -312,7 +350,8 @@ class OracleDisc:
         if eqn.viscous:
             inter = self.interior[..., None, None]
             nb_tr = np.where(inter, self._gather_nb(tr), self._ghosts(slice(None), tr))
-            What = 0.5 * (self._grad_vars(tr) + self._grad_vars(nb_tr))
+            What = self._common_w(inter, self.is_left[..., None, None], self._grad_vars(tr),
+                                  self._grad_vars(nb_tr))
             grads = self._gradient(slice(None), self._grad_vars(Q), What)
         from paper_2202_09733_b200.operators import gauss_rule
         wq = gauss_rule(n)[1]
@@ -415,7 +454,8 @@ class OracleDisc:
         fvn = np.empty_like(tr)
 
         def p3(s):
-            What = 0.5 * (self._grad_vars(tr[s]) + self._grad_vars(nb_tr[s]))
+            What = self._common_w(inter[s], self.is_left[s][..., None, None], self._grad_vars(tr[s]),
+                                  self._grad_vars(nb_tr[s]))
             gxs, gys = self._gradient(s, self._grad_vars(Q[s]), What)
             gx[s], gy[s] = gxs, gys
             fvn[s] = self._fvn(s, tr[s], gxs, gys)
@@ -423,7 +463,8 @@ class OracleDisc:
         run(p3)
 
         def p4(s):
-            Fv = np.where(inter[s], 0.5 * (fvn[s] - self._gather_nb_chunk(s, fvn)), fvn[s])
+            Fv = self._common_fv(inter[s], self.is_left[s][..., None, None], fvn[s],
+                                 -self._gather_nb_chunk(s, fvn))
             if eqn.kind == "navier-stokes":
                 wall = (self.tag[s] == WALL_ADIABATIC)[..., None]
                 Fv[..., 3] = np.where(wall, 0.0, Fv[..., 3])
@@ -444,7 +485,8 @@ class OracleDisc:
             inter = self.interior[..., None, None]
             gh = self._ghosts(slice(None), tr)
             nb_tr = np.where(inter, q_nb, gh)
-            What = 0.5 * (self._grad_vars(tr) + self._grad_vars(nb_tr))
+            What = self._common_w(inter, self.is_left[..., None, None], self._grad_vars(tr),
+                                  self._grad_vars(nb_tr))
             fvn = self._fvn(slice(None), tr, *self._gradient(slice(None), self._grad_vars(Q), What))
             fvn_nb = -self._gather_nb(fvn)
         return Frozen(q_nb, fvn_nb)
@@ -473,10 +515,11 @@ class OracleDisc:
         Fc = self._num_flux(tr, q_out, nrm)
         grads = None
         if self.eqn.viscous:
-            What = 0.5 * (self._grad_vars(tr) + self._grad_vars(q_out))
+            lo = self.is_left[e][:, None, None]
+            What = self._common_w(inter, lo, self._grad_vars(tr), self._grad_vars(q_out))
             grads = self._gradient(e, self._grad_vars(Q), What)
             fvn = self._fvn(e, tr, *grads)
-            Fv = np.where(inter, 0.5 * (fvn + fvn_nb), fvn)
+            Fv = self._common_fv(inter, lo, fvn, fvn_nb)
             if self.eqn.kind == "navier-stokes":
                 wall = (self.tag[e] == WALL_ADIABATIC)[:, None]
                 Fv[..., 3] = np.where(wall, 0.0, Fv[..., 3])
@@ -500,7 +543,8 @@ class OracleDisc:
             inter = self.interior[nb][:, None, None]
             gh = self._ghosts(nb, tr)
             q_out = np.where(inter, frozen.q_nb[nb], gh)
-            What = 0.5 * (self._grad_vars(tr) + self._grad_vars(q_out))
+            What = self._common_w(inter, self.is_left[nb][:, None, None], self._grad_vars(tr),
+                                  self._grad_vars(q_out))
             gx, gy = self._gradient(nb, self._grad_vars(Q_nb), What)
             fv = self._fvn(nb, tr, gx, gy)[..., fnb, :, :]
             if rev:

@@ -29,6 +29,7 @@ class DiscDesc(ctypes.Structure):
         ("free_stream", c_double_p), ("D", c_double_p), ("eL", c_double_p), ("eR", c_double_p),
         ("lL", c_double_p), ("lR", c_double_p), ("xg", c_double_p), ("geom", c_double_p),
         ("links", c_int64_p), ("tags", c_int32_p),
+        ("riemann", ctypes.c_int32), ("viscous_scheme", ctypes.c_int32),
     ]
 
 

@@ -67,6 +67,7 @@ PMGB_API int pmgb_disc_create(const pmgb_disc_desc* desc, pmgb_disc** out) {
   if (!desc || !out) return -1;
   if (desc->degree < 0 || desc->degree > 5) return -2;
   if (desc->kind < 0 || desc->kind > 2) return -3;
+  if (desc->riemann < 0 || desc->riemann > 1 || desc->viscous_scheme < 0 || desc->viscous_scheme > 1) return -1;
   if (desc->n_elem * 4 * (desc->degree + 1) * 4 >= ((int64_t)1 << 31)) return -4;  // 32-bit face offsets
   pmgb_disc* h = new pmgb_disc();
   DiscDev& d = h->d;
@@ -92,6 +93,8 @@ PMGB_API int pmgb_disc_create(const pmgb_disc_desc* desc, pmgb_disc** out) {
   d.C.adv_x = desc->adv_x;
   d.C.adv_y = desc->adv_y;
   d.C.diff = desc->diffusivity;
+  d.C.riemann = desc->riemann;
+  d.C.ldg = desc->viscous_scheme;
   std::vector<int2> lk((size_t)d.M * 4);
   for (int64_t e = 0; e < d.M; ++e) {
     for (int f = 0; f < 4; ++f) {

@@ -175,6 +175,7 @@ __device__ __forceinline__ double fsqrt(double x) {
 
 struct Phys {
   double gamma, mu, kappa, ax, ay, diff;
+  int riemann, ldg;  // FrConst options (Rusanov flux, LDG viscous scheme)
 };
 
 __device__ __forceinline__ void prim(const double* q, double g, double& r, double& ir, double& u, double& v,
@@ -226,11 +227,30 @@ __device__ __forceinline__ void roe(const double* qL, const double* qR, double n
   F[3] = 0.5 * (EpL * qnL + EpR * qnR) - 0.5 * d3;
 }
 
+// Rusanov (local Lax-Friedrichs) flux -- the BASELINE configs' interface
+// flux, not in the reference (oracle: fr_oracle.rusanov_flux)
+__device__ __forceinline__ void rusanov(const double* qL, const double* qR, double nx, double ny, double g,
+                                        double* F) {
+  double rL, irL, uL, vL, pL, rR, irR, uR, vR, pR;
+  prim(qL, g, rL, irL, uL, vL, pL);
+  prim(qR, g, rR, irR, uR, vR, pR);
+  const double qnL = uL * nx + vL * ny, qnR = uR * nx + vR * ny;
+  const double lam = fmax(fabs(qnL) + fsqrt(g * pL * irL), fabs(qnR) + fsqrt(g * pR * irR));
+  const double hl = 0.5 * lam;
+  F[0] = 0.5 * (qL[0] * qnL + qR[0] * qnR) - hl * (qR[0] - qL[0]);
+  F[1] = 0.5 * ((qL[1] * qnL + pL * nx) + (qR[1] * qnR + pR * nx)) - hl * (qR[1] - qL[1]);
+  F[2] = 0.5 * ((qL[2] * qnL + pL * ny) + (qR[2] * qnR + pR * ny)) - hl * (qR[2] - qL[2]);
+  F[3] = 0.5 * ((qL[3] + pL) * qnL + (qR[3] + pR) * qnR) - hl * (qR[3] - qL[3]);
+}
+
 template <int KIND>
 __device__ __forceinline__ void num_flux(const double* qa, const double* qc, double nx, double ny,
                                          const Phys& ph, double* F) {
   if constexpr (KT<KIND>::FLOW) {
-    roe(qa, qc, nx, ny, ph.gamma, F);
+    if (ph.riemann)
+      rusanov(qa, qc, nx, ny, ph.gamma, F);
+    else
+      roe(qa, qc, nx, ny, ph.gamma, F);
   } else {
     const double an = ph.ax * nx + ph.ay * ny;
     F[0] = 0.5 * an * (qa[0] + qc[0]) - 0.5 * fabs(an) * (qc[0] - qa[0]);
@@ -258,6 +278,20 @@ __device__ __forceinline__ void ghost(const double* q, int tag, double nx, doubl
   } else {
     gq[0] = (tag == T_FAR_FIELD) ? 0.0 : q[0];
   }
+}
+
+// Common viscous-variable value on a face: BR1 average (reference,
+// spatial.py:536-546) or LDG (C11 = 0, switch from the face's L element):
+// L's trace on interior faces; boundary faces keep the BR1 ghost average.
+__device__ __forceinline__ double common_w(const Phys& ph, bool interior, bool left, double wa, double wc) {
+  return (ph.ldg && interior) ? (left ? wa : wc) : 0.5 * (wa + wc);
+}
+// Common viscous normal flux on the own normal from the own one-sided flux
+// Fo and the neighbour's on ITS normal Fn: BR1 0.5 (Fo - Fn) (spatial.py:
+// 559-568); LDG R's flux: -Fn seen from L, Fo seen from R.
+__device__ __forceinline__ double common_fv(const Phys& ph, bool interior, bool left, double Fo, double Fn) {
+  if (!interior) return Fo;
+  return ph.ldg ? (left ? -Fn : Fo) : 0.5 * (Fo - Fn);
 }
 
 // viscous variables W = (u, v, T = p/rho) (spatial.py:448-454)
@@ -319,7 +353,7 @@ __device__ __forceinline__ Metric metric(const double* g) {
 }
 
 __device__ __forceinline__ Phys phys_of(const FrConst& C) {
-  return Phys{C.gamma, C.mu, C.kappa, C.adv_x, C.adv_y, C.diff};
+  return Phys{C.gamma, C.mu, C.kappa, C.adv_x, C.adv_y, C.diff, C.riemann, C.ldg};
 }
 
 // ---------------------------------------------------------------------------
@@ -910,8 +944,9 @@ k_fvn(const FrConst C, const FrMesh m, const double* __restrict__ q, const doubl
     double wa[NW], wc[NW];
     grad_vars<KIND>(tr_, ph.gamma, wa);
     grad_vars<KIND>(nb_, ph.gamma, wc);
+    const bool inter = lkk.x >= 0, lft = inter && lk_left(lkk.y);
 #pragma unroll
-    for (int c = 0; c < NW; ++c) sWH[c * NFTP + el * NFS + (t - el * NF)] = 0.5 * (wa[c] + wc[c]);
+    for (int c = 0; c < NW; ++c) sWH[c * NFTP + el * NFS + (t - el * NF)] = common_w(ph, inter, lft, wa[c], wc[c]);
   };
   if constexpr (ONE_FACE) {
     if (face_live) face_avg(t0, fel, ff, lk, tr, nb);
@@ -1341,7 +1376,7 @@ k_assemble(const FrConst C, const FrMesh m, const double* __restrict__ q, const 
     if constexpr (VISC) {
       double Fv[NV];
 #pragma unroll
-      for (int v = 0; v < NV; ++v) Fv[v] = interior ? 0.5 * (Fo_[v] - Fn_[v]) : Fo_[v];
+      for (int v = 0; v < NV; ++v) Fv[v] = common_fv(ph, interior, left, Fo_[v], Fn_[v]);
       if (KT<KIND>::FLOW && !interior && lk_tag(lkk.y) == T_WALL_ADIABATIC) Fv[NV - 1] = 0.0;
 #pragma unroll
       for (int v = 0; v < NV; ++v) F[v] = F[v] - Fv[v];
@@ -1530,7 +1565,7 @@ k_assemble_async(const FrConst C, const FrMesh m, const double* __restrict__ q, 
       if constexpr (VISC) {
         double Fv[NV];
 #pragma unroll
-        for (int v = 0; v < NV; ++v) Fv[v] = interior ? 0.5 * (Fo[v] - Fn[v]) : Fo[v];
+        for (int v = 0; v < NV; ++v) Fv[v] = common_fv(ph, interior, left, Fo[v], Fn[v]);
         if (!interior && lk_tag(lk.y) == T_WALL_ADIABATIC) Fv[NV - 1] = 0.0;
 #pragma unroll
         for (int v = 0; v < NV; ++v) F[v] = F[v] - Fv[v];
@@ -1713,8 +1748,9 @@ __device__ __forceinline__ void local_pipeline(const FrConst& C, const FrMesh& m
       double wa[NW], wc[NW];
       grad_vars<KIND>(tr, ph.gamma, wa);
       grad_vars<KIND>(nb, ph.gamma, wc);
+      const bool inter = lk.x >= 0, lft = inter && lk_left(lk.y);
 #pragma unroll
-      for (int c = 0; c < NW; ++c) sWH[c * NFT + t] = 0.5 * (wa[c] + wc[c]);
+      for (int c = 0; c < NW; ++c) sWH[c * NFT + t] = common_w(ph, inter, lft, wa[c], wc[c]);
     }
   }
   __syncthreads();
@@ -1773,14 +1809,16 @@ __device__ __forceinline__ void local_pipeline(const FrConst& C, const FrMesh& m
 #pragma unroll
       for (int v = 0; v < NV; ++v) Fv[v] = fx[v] * nx + fy[v] * ny;
       if (OV && f == ov_face) {
+        const bool lft = lk_left(lk.y);
 #pragma unroll
-        for (int v = 0; v < NV; ++v) Fv[v] = 0.5 * (Fv[v] + (-sm[L::OVF + (el * N + k) * NV + v]));
+        for (int v = 0; v < NV; ++v) Fv[v] = common_fv(ph, true, lft, Fv[v], sm[L::OVF + (el * N + k) * NV + v]);
       } else if (lk.x >= 0) {
         const int kk = lk_rev(lk.y) ? N - 1 - k : k;
+        const bool lft = lk_left(lk.y);
         double Fn[NV];
         ld_face<NV>(fvn + (((int64_t)lk.x * 4 + lk_face(lk.y)) * N + kk) * NV, Fn);
 #pragma unroll
-        for (int v = 0; v < NV; ++v) Fv[v] = 0.5 * (Fv[v] + (-Fn[v]));
+        for (int v = 0; v < NV; ++v) Fv[v] = common_fv(ph, true, lft, Fv[v], Fn[v]);
       } else if (KT<KIND>::FLOW && lk_tag(lk.y) == T_WALL_ADIABATIC) {
         Fv[NV - 1] = 0.0;
       }
@@ -1943,8 +1981,9 @@ __device__ __forceinline__ void record_pipeline(const FrConst& C, const FrMesh& 
       double wa[NW], wc[NW];
       grad_vars<KIND>(tr, ph.gamma, wa);
       grad_vars<KIND>(nb, ph.gamma, wc);
+      const bool inter = lk.x >= 0, lft = inter && lk_left(lk.y);
 #pragma unroll
-      for (int c = 0; c < NW; ++c) sWH[c * NFT + t] = 0.5 * (wa[c] + wc[c]);
+      for (int c = 0; c < NW; ++c) sWH[c * NFT + t] = common_w(ph, inter, lft, wa[c], wc[c]);
 #pragma unroll
       for (int v = 0; v < NV; ++v) sTR[v * NFT + t] = tr[v];
     }

@@ -62,6 +62,8 @@ struct FrConst {
   double eL[6], eR[6], lL[6], lR[6], xg[6];
   double qinf[4];
   double gamma, mu, kappa, adv_x, adv_y, diff;
+  int riemann;  // 0 Roe (reference), 1 Rusanov (BASELINE option)
+  int ldg;      // 0 BR1 (reference), 1 LDG, C11 = 0, switch from the L element
 };
 
 struct FrMesh {

@@ -34,10 +34,19 @@ class EquationSpec:
     prandtl: float = 0.72
     advection: tuple = (1.0, 0.0)
     diffusivity: float = 0.0
+    # interface schemes: the reference has Roe + BR1 only (spatial.py:113-163,
+    # 536-603); "rusanov" / "ldg" are the BASELINE configs' choices (SURVEY
+    # 8.0), parity-pinned to the oracle only
+    riemann: str = "roe"
+    viscous_scheme: str = "br1"
 
     def __post_init__(self):
         if self.kind not in KIND_CODE:
             raise ValueError(f"unknown equation kind {self.kind!r}")
+        if self.riemann not in ("roe", "rusanov"):
+            raise ValueError(f"unknown Riemann flux {self.riemann!r}")
+        if self.viscous_scheme not in ("br1", "ldg"):
+            raise ValueError(f"unknown viscous scheme {self.viscous_scheme!r}")
         if self.kind != "advection-diffusion" and self.mach <= 0:
             raise ValueError("Mach number must be positive")
         if self.kind == "navier-stokes" and self.reynolds <= 0:

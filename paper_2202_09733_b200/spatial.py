@@ -148,7 +148,8 @@ class Discretization:
             adv_x=float(eqn.advection[0]), adv_y=float(eqn.advection[1]), diffusivity=eqn.diffusivity,
             free_stream=dp(self._qinf), D=dp(self._ops["D"]), eL=dp(self._ops["eL"]), eR=dp(self._ops["eR"]),
             lL=dp(self._ops["lL"]), lR=dp(self._ops["lR"]), xg=dp(self._ops["xg"]), geom=dp(self._geom),
-            links=self._links.ctypes.data_as(_lib.c_int64_p), tags=self._tags.ctypes.data_as(_lib.c_int32_p))
+            links=self._links.ctypes.data_as(_lib.c_int64_p), tags=self._tags.ctypes.data_as(_lib.c_int32_p),
+            riemann=1 if eqn.riemann == "rusanov" else 0, viscous_scheme=1 if eqn.viscous_scheme == "ldg" else 0)
         h = ctypes.c_void_p()
         with torch.cuda.device(self.device):
             check(load().pmgb_disc_create(ctypes.byref(desc), ctypes.byref(h)), "disc_create")

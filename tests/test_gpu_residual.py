@@ -152,3 +152,54 @@ def test_residual_batch_host_pipeline(cuda):
     outs = dev.residual_batch([torch.from_numpy(q).pin_memory() for q in qs])
     for q, R in zip(qs, outs):
         assert np.array_equal(R.numpy(), dev.residual(q))
+
+
+# ---------------------------------------------------------------------------
+# BASELINE interface options (Rusanov flux, LDG viscous scheme): not in the
+# reference, pinned to the oracle restatement (fr_oracle.rusanov_flux,
+# OracleDisc._common_w / _common_fv) at the same 1e-12 bar
+
+SCHEMES = [("rusanov", "br1"), ("roe", "ldg"), ("rusanov", "ldg")]
+
+
+@pytest.mark.parametrize("riemann,visc", SCHEMES)
+@pytest.mark.parametrize("kind", ["euler", "ns", "advd"])
+@pytest.mark.parametrize("mesh", ["box4p", "box3ff", "cyl_adiab", "cyl_slip", "chan", "box1p"])
+def test_residual_options_match_oracle(cuda, riemann, visc, kind, mesh):
+    m = MESHES[mesh]()
+    eqn = EquationSpec(**KINDS[kind], riemann=riemann, viscous_scheme=visc)
+    for p in (1, 3, 4):
+        orc = OracleDisc(m, p, eqn)
+        dev = Discretization(m, p, eqn)
+        q = _state(orc, kind)
+        assert _rel(dev.residual(q), orc.residual(q)) <= RTOL, (mesh, kind, p)
+
+
+@pytest.mark.parametrize("riemann,visc", SCHEMES)
+@pytest.mark.parametrize("mesh", ["box4p", "cyl_adiab", "chan"])
+def test_element_residual_options_match_oracle(cuda, riemann, visc, mesh):
+    m = MESHES[mesh]()
+    eqn = EquationSpec(**KINDS["ns"], riemann=riemann, viscous_scheme=visc)
+    p = 2
+    orc = OracleDisc(m, p, eqn)
+    dev = Discretization(m, p, eqn)
+    q = _state(orc, "ns")
+    fo, fd = orc.freeze(q), dev.freeze(q)
+    R = dev.residual(q)
+    for e in (0, 3, m.n_elements - 1):
+        Q = q[orc.offsets[e]:orc.offsets[e + 1]].reshape(3, 3, 4)
+        B = np.stack([Q, Q * 1.001, Q * 0.999])
+        assert _rel(dev.element_residual(e, B, fd), orc.element_residual(e, B, fo)) <= RTOL, e
+        # local == global holds for every interface scheme
+        Re = dev.element_residual(e, Q, fd)
+        assert np.max(np.abs(Re.reshape(-1) - R[orc.offsets[e]:orc.offsets[e + 1]])) <= 1e-12
+
+
+@pytest.mark.parametrize("riemann,visc", SCHEMES)
+def test_free_stream_preserved_options(cuda, riemann, visc):
+    eqn = EquationSpec(**KINDS["ns"], riemann=riemann, viscous_scheme=visc)
+    for mesh in ("box4p", "chan"):
+        m = MESHES[mesh]()
+        dev = Discretization(m, 3, eqn)
+        q = OracleDisc(m, 3, eqn).free_stream_field()
+        assert np.max(np.abs(dev.residual(q))) <= 1e-11

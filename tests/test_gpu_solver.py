@@ -396,3 +396,42 @@ def test_esdirk2_step_rk_ej_matches_oracle(cuda):
     assert [i["iters"] for i in info] == [r[1] for r in drv_o.records]
     assert all(abs(a - b) <= 1 for a, b in zip([i["gmres_iters"] for i in info], [r[2] for r in drv_o.records]))
     assert rel(q_d, q_o) <= 1e-7
+
+
+# ---------------------------------------------------------------------------
+# BASELINE interface options (Rusanov / LDG) through the solver stack
+
+@pytest.mark.parametrize("riemann,visc", [("rusanov", "ldg"), ("roe", "ldg")])
+@pytest.mark.parametrize("p", [2, 4])
+def test_blocks_and_sparse_options_match_oracle(cuda, riemann, visc, p):
+    m = mm.generate_box(3, 3, 1.0, 1.0, periodic=True)
+    eqn = EquationSpec(kind="navier-stokes", mach=0.3, reynolds=50.0, riemann=riemann, viscous_scheme=visc)
+    o = OracleDisc(m, p, eqn)
+    rng = np.random.default_rng(3)
+    q = o.free_stream_field() * (1 + 0.01 * rng.standard_normal(o.n_dofs))
+    ob = so.assemble_blocks(o, q, 5.0)
+    d = Discretization(m, p, eqn)
+    db = nk.assemble_element_blocks(d, t(q), 5.0)
+    B = db.blocks[0].cpu().numpy()
+    assert np.abs(B - ob.blocks).max() / np.abs(ob.blocks).max() <= 1e-7
+    if p == 2:   # coupling blocks (MBNK) re-run the neighbour pipeline with the option
+        A = nk.assemble_sparse_blocks(d, t(q), 5.0)
+        S = so.assemble_sparse(o, q, 5.0)
+        assert rel(A.blocks, np.stack(S.blocks)) <= 1e-7
+
+
+def test_esdirk3_step_rusanov_ldg_matches_oracle(cuda):
+    import dataclasses
+    c = cases.config(1, nx=8)
+    eqn = dataclasses.replace(c.eqn, riemann="rusanov", viscous_scheme="ldg")
+    o = OracleDisc(c.mesh, c.p, eqn)
+    d = Discretization(c.mesh, c.p, eqn)
+    s = ti.get_scheme("esdirk3")
+    drv_o = so.Driver(o, "pmg", "3-2", 2, smoother_shift=50.0, gmres_rtol=1e-3, dtau_init=c.dt)
+    q_o = drv_o.esdirk_step(c.q0, c.dt, s.a, s.b)
+    cfg = {"case.precond": "pmg", "pmg.levels": "3-2", "pmg.smooth": "2", "pmg.smoother_shift": 50.0,
+           "gmres.kdim": 30, "gmres.rtol": 1e-3, "ptc.dtau_init": c.dt, "ptc.rtol": 1e-4}
+    q_d, info = ImplicitDriver(d, cfg).step(t(c.q0), c.dt, s)
+    assert [i["iters"] for i in info] == [r[1] for r in drv_o.records]
+    assert all(abs(a - b) <= 1 for a, b in zip([i["gmres_iters"] for i in info], [r[2] for r in drv_o.records]))
+    assert rel(q_d, q_o) <= 1e-7

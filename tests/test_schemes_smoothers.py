@@ -125,3 +125,46 @@ def test_rk_hierarchy_parse_and_config():
     assert pc.hierarchy.smoothers == ("rk", "rk", "ej")
     with pytest.raises(ValueError):
         pmg.PmgPrecondConfig(h, rk_cfl=0.0)
+
+
+# ---------------------------------------------------------------------------
+# Rusanov / LDG options of the oracle (BASELINE interface schemes)
+
+@pytest.mark.parametrize("riemann,visc", [("rusanov", "br1"), ("roe", "ldg"), ("rusanov", "ldg")])
+def test_oracle_options_conservative_and_free_stream(riemann, visc):
+    m = mm.generate_box(4, 4, 2.0, 2.0, periodic=True)
+    eqn = EquationSpec(kind="navier-stokes", mach=0.3, reynolds=100.0, riemann=riemann, viscous_scheme=visc)
+    o = OracleDisc(m, 3, eqn)
+    qf = o.free_stream_field()
+    assert np.max(np.abs(o.residual(qf))) <= 1e-11
+    rng = np.random.default_rng(2)
+    q = qf * (1.0 + 0.01 * rng.standard_normal(qf.shape))
+    R = o.residual(q).reshape(-1, 4, 4, 4)
+    from paper_2202_09733_b200.operators import gauss_rule
+    w = gauss_rule(4)[1]
+    tot = np.einsum("a,b,mab,mabv->v", w, w, o.det, R)
+    assert np.max(np.abs(tot)) <= 1e-11 * np.max(np.abs(R))
+
+
+def test_rusanov_consistency_and_dissipation():
+    from oracle.fr_oracle import euler_flux, roe_flux, rusanov_flux
+    rng = np.random.default_rng(4)
+    g = 1.4
+    q = np.stack([1 + 0.1 * rng.random(50), rng.random(50), rng.random(50), 3 + rng.random(50)], axis=-1)
+    th = rng.random(50) * 2 * np.pi
+    nrm = np.stack([np.cos(th), np.sin(th)], axis=-1)
+    fx, fy = euler_flux(q, g)
+    exact = fx * nrm[:, :1] + fy * nrm[:, 1:]
+    assert np.allclose(rusanov_flux(q, q, nrm, g), exact, rtol=1e-14, atol=1e-14)
+    # Rusanov dissipates at least as much as Roe on a density jump
+    q2 = q.copy()
+    q2[:, 0] *= 1.2
+    d_rus = np.abs(rusanov_flux(q, q2, nrm, g) - 0.5 * (exact + (euler_flux(q2, g)[0] * nrm[:, :1]
+                                                               + euler_flux(q2, g)[1] * nrm[:, 1:])))
+    d_roe = np.abs(roe_flux(q, q2, nrm, g) - 0.5 * (exact + (euler_flux(q2, g)[0] * nrm[:, :1]
+                                                             + euler_flux(q2, g)[1] * nrm[:, 1:])))
+    assert np.all(d_rus[:, 0] >= d_roe[:, 0] - 1e-12)
+    with pytest.raises(ValueError):
+        EquationSpec(kind="euler", riemann="hllc")
+    with pytest.raises(ValueError):
+        EquationSpec(kind="euler", viscous_scheme="ip")
