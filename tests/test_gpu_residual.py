@@ -198,7 +198,7 @@ def test_element_residual_options_match_oracle(cuda, riemann, visc, mesh):
 @pytest.mark.parametrize("riemann,visc", SCHEMES)
 def test_free_stream_preserved_options(cuda, riemann, visc):
     eqn = EquationSpec(**KINDS["ns"], riemann=riemann, viscous_scheme=visc)
-    for mesh in ("box4p", "chan"):
+    for mesh in ("box4p", "box3ff"):   # periodic and far-field (walls are not free-stream steady)
         m = MESHES[mesh]()
         dev = Discretization(m, 3, eqn)
         q = OracleDisc(m, 3, eqn).free_stream_field()
