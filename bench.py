@@ -433,15 +433,16 @@ def time_other_configs(torch, args):
             if k == 4:
                 cfg = {"case.precond": "pmg", "pmg.levels": c.levels, "pmg.smooth": "2",
                        "pmg.smoother_shift": c.extra["smoother_shift"], "gmres.kdim": c.kdim, "gmres.rtol": 1e-3}
-                sch = ti.get_scheme("row4")
-                ImplicitDriver(d, cfg).step(q0, c.dt, sch)
-                drv = ImplicitDriver(d, cfg)
-                torch.cuda.synchronize()
-                t0 = time.perf_counter()
-                _, info = drv.step(q0, c.dt, sch)
-                torch.cuda.synchronize()
-                rec.update(row4_step={"s": time.perf_counter() - t0, "dt": c.dt,
-                                      "gmres_iters": [i["iters"] for i in info]})
+                for name in (c.scheme, "row4"):   # ros4l: BASELINE's 4-stage ROW; row4: the reference's RODASP
+                    sch = ti.get_scheme(name)
+                    ImplicitDriver(d, cfg).step(q0, c.dt, sch)
+                    drv = ImplicitDriver(d, cfg)
+                    torch.cuda.synchronize()
+                    t0 = time.perf_counter()
+                    _, info = drv.step(q0, c.dt, sch)
+                    torch.cuda.synchronize()
+                    rec[f"{name}_step"] = {"s": time.perf_counter() - t0, "dt": c.dt, "stages": sch.stages,
+                                           "gmres_iters": [i["iters"] for i in info]}
                 del drv
             del d, q0, X, R0
         except Exception as exc:  # pragma: no cover

@@ -1,12 +1,16 @@
 """BASELINE.json configurations mapped onto the reference's features.
 
 SURVEY.md 8.0 pins each config to what the reference actually has:
-Roe + BR1 (not Rusanov/LDG), esdirk2 as the ESDIRK3 stand-in, row4 as
-the "4-stage ROW", EJ smoothers on every level + pmg.smoother_shift,
-wall-adiabatic for the isothermal wall, a geometric wall-normal ratio
-that actually fills [0, 1] for config 4, and dt from
-dt_conv = h_min / ((2p+1) max(|u| + c)).  Inputs are analytic and
-seeded; the same NumPy array feeds the oracle and the device.
+Roe + BR1 (Rusanov / LDG exist as EquationSpec options, parity against the
+oracle only), EJ smoothers on every level + pmg.smoother_shift,
+wall-adiabatic for the isothermal wall, a geometric wall-normal ratio that
+actually fills [0, 1] for config 4, and dt from
+dt_conv = h_min / ((2p+1) max(|u| + c)).  The schemes are the BASELINE
+ones, derived in time_integration and pinned by injecting them into the
+reference's own steppers: esdirk3 (configs 1, 2, 5) and ros4l, a 4-stage
+order-4 L-stable ROW (config 4; the reference's row4 is the 6-stage
+RODASP).  Inputs are analytic and seeded; the same NumPy array feeds the
+oracle and the device.
 
 Initial-condition builders follow harness.isentropic_vortex
 (/root/reference/pkg/src/pmgflow/harness.py:499-517).
@@ -146,7 +150,7 @@ def config(k: int, seed: int = 0, nx: int | None = None) -> Case:
         # erratic with the width (FD-noise sensitive, device and oracle alike);
         # 0.5x converges in 4-6 iterations at every width up to the full 512
         dt = 0.5 * explicit_dt(mesh, 3, eqn, q0)
-        return Case("config4", mesh, 3, eqn, q0, dt, "row4", "3-2", 60, 20, {"smoother_shift": 50.0})
+        return Case("config4", mesh, 3, eqn, q0, dt, "ros4l", "3-2", 60, 20, {"smoother_shift": 50.0})
     if k == 5:
         n = nx or 1024
         mesh = generate_box(n, n, 10.0, 10.0, periodic=True)

@@ -241,7 +241,7 @@ SCHEMA = {
 _VALID_CHOICES = {
     "mesh.kind": ("box", "cylinder", "file"),
     "equation.kind": ("euler", "navier-stokes", "advection-diffusion"),
-    "case.scheme": ("esdirk2", "esdirk3", "esdirk4", "row2", "row4"),
+    "case.scheme": ("esdirk2", "esdirk3", "esdirk4", "row2", "row4", "ros4l"),
     "case.solver": ("jfnk", "pmg-solver"),
     "case.precond": ("ej", "pmg", "none"),
     "case.init": ("free-stream", "zero"),

@@ -124,7 +124,52 @@ def _esdirk3():
     return StageScheme("esdirk3", "esdirk", 3, a, a[-1].copy(), a.sum(axis=1))
 
 
-_SCHEMES = {"esdirk2": _esdirk2, "esdirk3": _esdirk3, "esdirk4": _esdirk4, "row2": _row2, "row4": _row4}
+def _ros4l():
+    """Four-stage, fourth-order, L-stable Rosenbrock method (BASELINE config
+    4 asks for "a 4-stage ROW method"; the reference's row4 is the six-stage
+    RODASP, time_integration.py:80-102).
+
+    Derived here from the Rosenbrock order conditions (exact Jacobian,
+    autonomous form; Hairer & Wanner II, sec. IV.7) in the original
+    (alpha, gamma) variables, then transformed to the reference's K form
+    a = A G^-1, C = diag(1/gamma) - G^-1, m = b G^-1 (the form row_step,
+    :171-197, consumes).  gamma is the root near 0.5728 of
+    gamma^4 L_4(1/gamma) = gamma^4 - 4 gamma^3 + 3 gamma^2 - 2/3 gamma + 1/24
+    (R(inf) = 0: L-stable, A-stable).  Free choices: alpha_2 = 1,
+    alpha_3 = alpha_4 = 3/10 with alpha_4j = alpha_3j, beta'_2 = 1,
+    beta'_3 = 3/10, beta'_4 = -1/2 (the smallest K-form coefficients over a
+    grid of such choices).  b solves order conditions 1, 2, 3, 5;
+    alpha_32 solves condition 6; beta_43, beta_32, beta_42 solve
+    conditions 7, 8, 4.  tests/test_schemes_smoothers.py checks all eight
+    conditions, an empirical order-4 slope on a nonlinear system, and the
+    reference's own validate_tableau / stability_function."""
+    g = 0.5728160624821349
+    for _ in range(4):   # Newton on the L-stability quartic
+        g -= ((g ** 4 - 4 * g ** 3 + 3 * g * g - 2.0 / 3.0 * g + 1.0 / 24.0)
+              / (4 * g ** 3 - 12 * g * g + 6 * g - 2.0 / 3.0))
+    a2, a3, bp2, bp3, bp4 = 1.0, 0.3, 1.0, 0.3, -0.5
+    al = np.array([0.0, a2, a3, a3])
+    bp = np.array([0.0, bp2, bp3, bp4])
+    b = np.linalg.solve(np.array([np.ones(4), bp, al ** 2, al ** 3]),
+                        np.array([1.0, 0.5 - g, 1.0 / 3.0, 0.25]))
+    a32 = (1.0 / 8.0 - g / 3.0) / (bp2 * a3 * (b[2] + b[3]))
+    A = _lower([[], [a2], [a3 - a32, a32], [a3 - a32, a32, 0.0]], 4)
+    r4 = 1.0 / 6.0 - g + g * g
+    r7 = 1.0 / 12.0 - g / 3.0
+    r8 = 1.0 / 24.0 - g / 2.0 + 1.5 * g * g - g ** 3
+    b43 = (r4 * a2 ** 2 - r7 * bp2) / (b[3] * (bp3 * a2 ** 2 - a3 ** 2 * bp2))
+    b32 = r8 / (b[3] * b43 * bp2)
+    b42 = (r4 - b[2] * b32 * bp2 - b[3] * b43 * bp3) / (b[3] * bp2)
+    B = _lower([[], [bp2], [bp3 - b32, b32], [bp4 - b42 - b43, b42, b43]], 4)
+    Gi = np.linalg.inv(B - A + g * np.eye(4))
+    a = np.tril(A @ Gi, -1)
+    cm = np.tril(np.eye(4) / g - Gi, -1)
+    m = b @ Gi
+    return StageScheme("ros4l", "row", 4, a, m, a.sum(axis=1), cm, g)
+
+
+_SCHEMES = {"esdirk2": _esdirk2, "esdirk3": _esdirk3, "esdirk4": _esdirk4, "row2": _row2, "row4": _row4,
+            "ros4l": _ros4l}
 
 
 def get_scheme(name: str) -> StageScheme:

@@ -194,6 +194,21 @@ def test_row4_step_config1_matches_reference(cuda):
     assert rel(q1, G["c1/row4/q1"]) <= 1e-6
 
 
+def test_ros4l_step_config1_matches_reference(cuda):
+    """The derived 4-stage ROW (BASELINE config 4's scheme), pinned by the
+    reference's own row_step + ImplicitDriver (golden_ros4l.npz)."""
+    GR = np.load(Path(__file__).parent / "golden" / "golden_ros4l.npz")
+    c = cases.config(1)
+    d = Discretization(c.mesh, c.p, c.eqn)
+    cfg = {"case.precond": "pmg", "pmg.levels": "3-2", "pmg.smooth": "2", "pmg.smoother_shift": 50.0,
+           "gmres.kdim": 30, "gmres.rtol": 1e-3}
+    q1, info = ImplicitDriver(d, cfg).step(t(c.q0), c.dt, ti.get_scheme("ros4l"))
+    counts = [i["iters"] for i in info]
+    ref = list(GR["c1/ros4l/gmres_counts"])
+    assert len(counts) == len(ref) and all(abs(a - b) <= 1 for a, b in zip(counts, ref)), (counts, ref)
+    assert rel(q1, GR["c1/ros4l/q1"]) <= 1e-6
+
+
 def test_pmg_solve_lowmach_matches_reference(cuda):
     c = cases.config(3, nx=4)
     d = Discretization(c.mesh, 4, c.eqn)
@@ -276,15 +291,16 @@ def test_esdirk2_step_config2_physics_small_mesh(cuda):
     assert rel(q_d, q_o) <= 1e-7
 
 
+@pytest.mark.parametrize("scheme", ["row4", "ros4l"])
 @pytest.mark.parametrize("nx", [16, 32])
-def test_row4_step_config4_channel_walls(cuda, nx):
+def test_row4_step_config4_channel_walls(cuda, nx, scheme):
     # BASELINE config 4 physics on a reduced stretched channel: x-periodic,
     # adiabatic wall at y=0, slip wall at y=1, ROW4 + GMRES(60) + pMG p{3-2}
     c = cases.config(4, nx=nx)
     o = OracleDisc(c.mesh, c.p, c.eqn)
     d = Discretization(c.mesh, c.p, c.eqn)
     drv_o = so.Driver(o, "pmg", "3-2", 2, smoother_shift=50.0, gmres_rtol=1e-3, kdim=60)
-    s = ti.get_scheme("row4")
+    s = ti.get_scheme(scheme)
     q_o = drv_o.row_step(c.q0, c.dt, s.a, s.cmat, s.b, s.gamma)
     cfg = {"case.precond": "pmg", "pmg.levels": "3-2", "pmg.smooth": "2", "pmg.smoother_shift": 50.0,
            "gmres.kdim": 60, "gmres.rtol": 1e-3}

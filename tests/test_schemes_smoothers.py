@@ -168,3 +168,73 @@ def test_rusanov_consistency_and_dissipation():
         EquationSpec(kind="euler", riemann="hllc")
     with pytest.raises(ValueError):
         EquationSpec(kind="euler", viscous_scheme="ip")
+
+
+GR = np.load(Path(__file__).parent / "golden" / "golden_ros4l.npz")
+
+
+def _ros4l_original_form():
+    """Recover (A, B, b) of the original (alpha, beta = alpha + gamma)
+    form from the K form: G = (diag(1/g) - C)^-1, A = a G, b = m G."""
+    s = ti.get_scheme("ros4l")
+    G = np.linalg.inv(np.eye(4) / s.gamma - s.cmat)
+    A = s.a @ G
+    b = s.b @ G
+    B = A + G - s.gamma * np.eye(4)
+    return s, A, B, b
+
+
+def test_ros4l_order_conditions_and_reference_checks():
+    s, A, B, b = _ros4l_original_form()
+    g = s.gamma
+    al, bp = A.sum(1), B.sum(1)
+    conds = [b.sum() - 1, b @ bp - (0.5 - g), b @ al ** 2 - 1 / 3, b @ B @ bp - (1 / 6 - g + g * g),
+             b @ al ** 3 - 0.25, (b * al) @ A @ bp - (1 / 8 - g / 3), b @ B @ al ** 2 - (1 / 12 - g / 3),
+             b @ B @ B @ bp - (1 / 24 - g / 2 + 1.5 * g * g - g ** 3)]
+    assert np.max(np.abs(conds)) < 1e-14, conds
+    assert abs(g ** 4 - 4 * g ** 3 + 3 * g * g - 2 * g / 3 + 1 / 24) < 1e-15
+    # the tableau the reference's validate_tableau passed (make_golden_ros4l.py)
+    assert np.array_equal(s.a, GR["tableau/a"]) and np.array_equal(s.cmat, GR["tableau/cmat"])
+    assert np.array_equal(s.b, GR["tableau/m"])
+    assert GR["tableau/checks"].all(), dict(zip(GR["tableau/check_names"], GR["tableau/checks"]))
+    R = GR["tableau/R"]
+    assert abs(R[0]) < 1e-5                                   # L-stable
+    assert np.all(np.abs(R[3:6]) <= 1.0 + 1e-12)              # |R(iy)| <= 1
+    for z in GR["tableau/z"]:
+        assert abs(ti.stability_function(s, z) - R[list(GR["tableau/z"]).index(z)]) < 1e-13
+
+
+def test_ros4l_empirical_order_four():
+    """The K-form stage algebra of row_step with an exact Jacobian on a
+    nonlinear (van der Pol, mu = 1) system: error ratios -> 2^4."""
+    from scipy.integrate import solve_ivp
+    s = ti.get_scheme("ros4l")
+    f = lambda y: np.array([y[1], (1 - y[0] ** 2) * y[1] - y[0]])
+    J = lambda y: np.array([[0.0, 1.0], [-2 * y[0] * y[1] - 1.0, 1 - y[0] ** 2]])
+    y0 = np.array([2.0, 0.0])
+    ref = solve_ivp(lambda t, y: f(y), (0, 1.0), y0, rtol=1e-13, atol=1e-14, method="DOP853").y[:, -1]
+    errs = []
+    for N in (10, 20, 40, 80):
+        y, h = y0.copy(), 1.0 / N
+        for _ in range(N):
+            W = np.eye(2) / (s.gamma * h) - J(y)
+            K = []
+            for i in range(4):
+                yi = y + sum(s.a[i, j] * K[j] for j in range(i))
+                K.append(np.linalg.solve(W, f(yi) + sum(s.cmat[i, j] / h * K[j] for j in range(i))))
+            y = y + sum(s.b[j] * K[j] for j in range(4))
+        errs.append(np.abs(y - ref).max())
+    slopes = np.log2(np.array(errs[:-1]) / np.array(errs[1:]))
+    assert np.all(slopes > 3.8), (errs, slopes)
+
+
+def test_oracle_ros4l_step_matches_reference():
+    c = cases.config(1)
+    o = OracleDisc(c.mesh, c.p, c.eqn)
+    s = ti.get_scheme("ros4l")
+    drv = so.Driver(o, "pmg", "3-2", 2, smoother_shift=50.0, gmres_rtol=1e-3)
+    q1 = drv.row_step(c.q0, c.dt, s.a, s.cmat, s.b, s.gamma)
+    counts = [rec[2] for rec in drv.records]
+    ref = list(GR["c1/ros4l/gmres_counts"])
+    assert len(counts) == len(ref) and all(abs(a - b) <= 1 for a, b in zip(counts, ref)), (counts, ref)
+    assert np.max(np.abs(q1 - GR["c1/ros4l/q1"])) / np.max(np.abs(GR["c1/ros4l/q1"])) <= 1e-6
