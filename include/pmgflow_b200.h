@@ -58,6 +58,8 @@ typedef struct pmgb_disc_desc {
   const int32_t* tags;        /* (M, 4) boundary tag code, -1 interior    */
   int32_t riemann;            /* 0 Roe (reference), 1 Rusanov (option)   */
   int32_t viscous_scheme;     /* 0 BR1 (reference), 1 LDG (option)       */
+  double wall_temperature;    /* T = p/rho on tag-3 "wall-isothermal"
+                                 faces (option; EquationSpec.t_wall)      */
 } pmgb_disc_desc;
 
 PMGB_API int pmgb_disc_create(const pmgb_disc_desc* desc, pmgb_disc** out);
@@ -107,7 +109,7 @@ PMGB_API int pmgb_eval(pmgb_disc* d, const double* q, const double* X, double ep
  *   = (2p+1) max(|u|+c)/h_e + (p+1)^4 max(nu)/h_e^2,
  *   h_e = 4 |det J(0,0)| / max(centre-line lengths).  No reference
  * counterpart (the reference's smoothers are EJ / MBNK, pmg.py:162-175). */
-PMGB_API int pmgb_rk_lambda(pmgb_disc* d, const double* q, double* lam, void* stream);
+PMGB_API int pmgb_rk_lambda(pmgb_disc* d, const double* q, double adv_coef, double* lam, void* stream);
 
 /* RK local pseudo-time steps dtau[e] = cfl / (s + lam[e]) (M elements,
  * device buffers), once per smoothing sweep set. */

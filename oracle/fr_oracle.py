@@ -31,7 +31,7 @@ from paper_2202_09733_b200.equation import EquationSpec, NonPhysicalStateError
 from paper_2202_09733_b200.mesh import Mesh, element_geometry, face_links
 from paper_2202_09733_b200.operators import face_operators
 
-WALL_ADIABATIC, WALL_SLIP, FAR_FIELD = 0, 1, 2
+WALL_ADIABATIC, WALL_SLIP, FAR_FIELD, WALL_ISOTHERMAL = 0, 1, 2, 3
 
 
 # ---------------------------------------------------------------------------
@@ -239,6 +239,19 @@ class OracleDisc:
     # trace, the common viscous flux R's one-sided flux.  Boundary faces keep
     # the BR1 treatment (ghost average, own one-sided flux).
 
+    def _w_out(self, e, w_own, q_out):
+        """Viscous variables of the outside state.  On "wall-isothermal"
+        faces (BASELINE config 4; not in the reference) the ghost keeps the
+        mirrored no-slip state of the inviscid flux but its temperature is
+        2 T_w - T, so the BR1 common value holds T = T_w exactly."""
+        w = self._grad_vars(q_out)
+        if self.eqn.kind == "navier-stokes":
+            iso = (self.tag[e] == WALL_ISOTHERMAL)[..., None]
+            if np.any(iso):
+                w = w.copy()
+                w[..., 2] = np.where(iso, 2.0 * self.eqn.t_wall - w_own[..., 2], w[..., 2])
+        return w
+
     def _common_w(self, inter, left_own, w_own, w_out):
         if self.eqn.viscous_scheme == "ldg":
             return np.where(inter, np.where(left_own, w_own, w_out), 0.5 * (w_own + w_out))
@@ -275,7 +288,7 @@ class OracleDisc:
         """Ghost states on every boundary face of elements e (others 0)."""
         gh = np.zeros_like(tr)
         tag = self.tag[e]
-        for t in (WALL_ADIABATIC, WALL_SLIP, FAR_FIELD):
+        for t in (WALL_ADIABATIC, WALL_SLIP, FAR_FIELD, WALL_ISOTHERMAL):
             sel = np.broadcast_to(tag == t, tr.shape[:-2])
             if sel.any():
                 nrm = np.broadcast_to(self.nrm[e][..., None, :], tr.shape[:-1] + (2,))
@@ -322,7 +335,7 @@ class OracleDisc:
         W = self._grad_vars(Q)
         w_own = self._grad_vars(tr)
         lo = self.is_left[..., None, None]
-        What = self._common_w(inter, lo, w_own, self._grad_vars(nb_tr))
+        What = self._common_w(inter, lo, w_own, self._w_out(e, w_own, nb_tr))
         grads = self._gradient(e, W, What)
         fvn = self._fvn(e, tr, *grads)
         Fv = self._common_fv(inter, lo, fvn, -self._gather_nb(fvn))
@@ -340,7 +353,7 @@ class OracleDisc:
         eqn = self.eqn
         if eqn.kind == "advection-diffusion":
             raise ValueError("forces are only defined for flow equations")
-        wall = (self.tag == WALL_ADIABATIC) | (self.tag == WALL_SLIP)
+        wall = (self.tag == WALL_ADIABATIC) | (self.tag == WALL_SLIP) | (self.tag == WALL_ISOTHERMAL)
         if not wall.any():
             raise ValueError("mesh has no wall boundary faces")
         n, nv = self.n, self.nv
@@ -350,8 +363,9 @@ class OracleDisc:
         if eqn.viscous:
             inter = self.interior[..., None, None]
             nb_tr = np.where(inter, self._gather_nb(tr), self._ghosts(slice(None), tr))
-            What = self._common_w(inter, self.is_left[..., None, None], self._grad_vars(tr),
-                                  self._grad_vars(nb_tr))
+            w_own = self._grad_vars(tr)
+            What = self._common_w(inter, self.is_left[..., None, None], w_own,
+                                  self._w_out(slice(None), w_own, nb_tr))
             grads = self._gradient(slice(None), self._grad_vars(Q), What)
         from paper_2202_09733_b200.operators import gauss_rule
         wq = gauss_rule(n)[1]
@@ -454,8 +468,9 @@ class OracleDisc:
         fvn = np.empty_like(tr)
 
         def p3(s):
-            What = self._common_w(inter[s], self.is_left[s][..., None, None], self._grad_vars(tr[s]),
-                                  self._grad_vars(nb_tr[s]))
+            w_own = self._grad_vars(tr[s])
+            What = self._common_w(inter[s], self.is_left[s][..., None, None], w_own,
+                                  self._w_out(s, w_own, nb_tr[s]))
             gxs, gys = self._gradient(s, self._grad_vars(Q[s]), What)
             gx[s], gy[s] = gxs, gys
             fvn[s] = self._fvn(s, tr[s], gxs, gys)
@@ -485,8 +500,9 @@ class OracleDisc:
             inter = self.interior[..., None, None]
             gh = self._ghosts(slice(None), tr)
             nb_tr = np.where(inter, q_nb, gh)
-            What = self._common_w(inter, self.is_left[..., None, None], self._grad_vars(tr),
-                                  self._grad_vars(nb_tr))
+            w_own = self._grad_vars(tr)
+            What = self._common_w(inter, self.is_left[..., None, None], w_own,
+                                  self._w_out(slice(None), w_own, nb_tr))
             fvn = self._fvn(slice(None), tr, *self._gradient(slice(None), self._grad_vars(Q), What))
             fvn_nb = -self._gather_nb(fvn)
         return Frozen(q_nb, fvn_nb)
@@ -516,7 +532,8 @@ class OracleDisc:
         grads = None
         if self.eqn.viscous:
             lo = self.is_left[e][:, None, None]
-            What = self._common_w(inter, lo, self._grad_vars(tr), self._grad_vars(q_out))
+            w_own = self._grad_vars(tr)
+            What = self._common_w(inter, lo, w_own, self._w_out(e, w_own, q_out))
             grads = self._gradient(e, self._grad_vars(Q), What)
             fvn = self._fvn(e, tr, *grads)
             Fv = self._common_fv(inter, lo, fvn, fvn_nb)
@@ -543,8 +560,9 @@ class OracleDisc:
             inter = self.interior[nb][:, None, None]
             gh = self._ghosts(nb, tr)
             q_out = np.where(inter, frozen.q_nb[nb], gh)
-            What = self._common_w(inter, self.is_left[nb][:, None, None], self._grad_vars(tr),
-                                  self._grad_vars(q_out))
+            w_own = self._grad_vars(tr)
+            What = self._common_w(inter, self.is_left[nb][:, None, None], w_own,
+                                  self._w_out(nb, w_own, q_out))
             gx, gy = self._gradient(nb, self._grad_vars(Q_nb), What)
             fv = self._fvn(nb, tr, gx, gy)[..., fnb, :, :]
             if rev:

@@ -279,7 +279,10 @@ def rk_spectral_radius(disc: OracleDisc, q):
     north star item (3); DESIGN.md section 4 "RK smoother"):
 
         h_e      = 4 |det J(0,0)| / max(L_xi, L_eta)   (L = centre-line lengths)
-        lambda_e = (2p+1) max_pts(|u| + c) / h_e + (p+1)^4 max_pts(nu) / h_e^2
+        lambda_e = A_p max_pts(|u| + c) / h_e + (p+1)^4 max_pts(nu) / h_e^2
+        A_p      = 2 sqrt(2) rho_p, rho_p the spectral radius of the 1-D
+                   upwind FR advection operator on [-1, 1] (Bloch analysis,
+                   operators.fr_advection_radius)
         nu       = max(4/3 mu, kappa (gamma-1)) / rho   (NS), diffusivity (ADVD)
     """
     from paper_2202_09733_b200.mesh import pack_geometry
@@ -307,7 +310,8 @@ def rk_spectral_radius(disc: OracleDisc, q):
             nu = max(4.0 / 3.0 * eqn.mu, eqn.heat_conductivity * (gam - 1.0)) / rho.min(axis=1)
         else:
             nu = np.zeros(M)
-    return (2 * P + 1) * a / h + float((P + 1) ** 4) * nu / (h * h)
+    from paper_2202_09733_b200.operators import rk_adv_coef
+    return rk_adv_coef(P) * a / h + float((P + 1) ** 4) * nu / (h * h)
 
 
 class Level:

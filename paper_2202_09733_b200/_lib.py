@@ -30,6 +30,7 @@ class DiscDesc(ctypes.Structure):
         ("lL", c_double_p), ("lR", c_double_p), ("xg", c_double_p), ("geom", c_double_p),
         ("links", c_int64_p), ("tags", c_int32_p),
         ("riemann", ctypes.c_int32), ("viscous_scheme", ctypes.c_int32),
+        ("wall_temperature", ctypes.c_double),
     ]
 
 
@@ -51,7 +52,7 @@ SIGNATURES = {
     "pmgb_disc_destroy": (ctypes.c_int, [c_void_p]),
     "pmgb_disc_n_dofs": (ctypes.c_int64, [c_void_p]),
     "pmgb_residual": (ctypes.c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
-    "pmgb_rk_lambda": (ctypes.c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
+    "pmgb_rk_lambda": (ctypes.c_int, [c_void_p, c_void_p, ctypes.c_double, c_void_p, c_void_p]),
     "pmgb_rk_dtau": (ctypes.c_int, [ctypes.c_int64, c_void_p, ctypes.c_double, ctypes.c_double, c_void_p,
                                     c_void_p]),
     "pmgb_eval": (ctypes.c_int, [c_void_p, c_void_p, c_void_p, ctypes.c_double,

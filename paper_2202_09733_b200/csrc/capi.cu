@@ -95,6 +95,7 @@ PMGB_API int pmgb_disc_create(const pmgb_disc_desc* desc, pmgb_disc** out) {
   d.C.diff = desc->diffusivity;
   d.C.riemann = desc->riemann;
   d.C.ldg = desc->viscous_scheme;
+  d.C.twall = desc->wall_temperature;
   std::vector<int2> lk((size_t)d.M * 4);
   for (int64_t e = 0; e < d.M; ++e) {
     for (int f = 0; f < 4; ++f) {
@@ -189,10 +190,10 @@ PMGB_API int pmgb_jfnk_matvec(pmgb_disc* h, const double* X, const double* q, co
   return pmgb_eval(h, q, X, eps, &e, out, stream);
 }
 
-PMGB_API int pmgb_rk_lambda(pmgb_disc* h, const double* q, double* lam, void* stream) {
-  if (!h || (h->d.M > 0 && (!q || !lam))) return -1;
+PMGB_API int pmgb_rk_lambda(pmgb_disc* h, const double* q, double adv_coef, double* lam, void* stream) {
+  if (!h || (h->d.M > 0 && (!q || !lam)) || !(adv_coef > 0.0)) return -1;
   g_launches += 1;
-  return launch_rk_lambda(h->d, q, lam, S(stream));
+  return launch_rk_lambda(h->d, q, adv_coef, lam, S(stream));
 }
 
 PMGB_API int pmgb_rk_dtau(int64_t M, const double* lam, double s, double cfl, double* dtau, void* stream) {

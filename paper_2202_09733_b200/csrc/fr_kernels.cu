@@ -174,7 +174,7 @@ __device__ __forceinline__ double fsqrt(double x) {
 // pointwise physics (spatial.py:94-203)
 
 struct Phys {
-  double gamma, mu, kappa, ax, ay, diff;
+  double gamma, mu, kappa, ax, ay, diff, twall;
   int riemann, ldg;  // FrConst options (Rusanov flux, LDG viscous scheme)
 };
 
@@ -280,6 +280,16 @@ __device__ __forceinline__ void ghost(const double* q, int tag, double nx, doubl
   }
 }
 
+// Viscous variables of a boundary face's ghost: on wall-isothermal faces
+// (BASELINE config 4; not in the reference) the ghost keeps the mirrored
+// no-slip state of the inviscid flux but carries T = 2 T_w - T, so the BR1
+// common value holds T_w (oracle: OracleDisc._w_out).
+template <int KIND>
+__device__ __forceinline__ void ghost_w(const Phys& ph, int tag, const double* wa, double* wc) {
+  if constexpr (KT<KIND>::FLOW)
+    if (tag == T_WALL_ISOTHERMAL) wc[2] = 2.0 * ph.twall - wa[2];
+}
+
 // Common viscous-variable value on a face: BR1 average (reference,
 // spatial.py:536-546) or LDG (C11 = 0, switch from the face's L element):
 // L's trace on interior faces; boundary faces keep the BR1 ghost average.
@@ -353,7 +363,7 @@ __device__ __forceinline__ Metric metric(const double* g) {
 }
 
 __device__ __forceinline__ Phys phys_of(const FrConst& C) {
-  return Phys{C.gamma, C.mu, C.kappa, C.adv_x, C.adv_y, C.diff, C.riemann, C.ldg};
+  return Phys{C.gamma, C.mu, C.kappa, C.adv_x, C.adv_y, C.diff, C.twall, C.riemann, C.ldg};
 }
 
 // ---------------------------------------------------------------------------
@@ -944,6 +954,7 @@ k_fvn(const FrConst C, const FrMesh m, const double* __restrict__ q, const doubl
     double wa[NW], wc[NW];
     grad_vars<KIND>(tr_, ph.gamma, wa);
     grad_vars<KIND>(nb_, ph.gamma, wc);
+    if (lkk.x < 0) ghost_w<KIND>(ph, lk_tag(lkk.y), wa, wc);
     const bool inter = lkk.x >= 0, lft = inter && lk_left(lkk.y);
 #pragma unroll
     for (int c = 0; c < NW; ++c) sWH[c * NFTP + el * NFS + (t - el * NF)] = common_w(ph, inter, lft, wa[c], wc[c]);
@@ -1748,6 +1759,7 @@ __device__ __forceinline__ void local_pipeline(const FrConst& C, const FrMesh& m
       double wa[NW], wc[NW];
       grad_vars<KIND>(tr, ph.gamma, wa);
       grad_vars<KIND>(nb, ph.gamma, wc);
+      if (lk.x < 0) ghost_w<KIND>(ph, lk_tag(lk.y), wa, wc);
       const bool inter = lk.x >= 0, lft = inter && lk_left(lk.y);
 #pragma unroll
       for (int c = 0; c < NW; ++c) sWH[c * NFT + t] = common_w(ph, inter, lft, wa[c], wc[c]);
@@ -1981,6 +1993,7 @@ __device__ __forceinline__ void record_pipeline(const FrConst& C, const FrMesh& 
       double wa[NW], wc[NW];
       grad_vars<KIND>(tr, ph.gamma, wa);
       grad_vars<KIND>(nb, ph.gamma, wc);
+      if (lk.x < 0) ghost_w<KIND>(ph, lk_tag(lk.y), wa, wc);
       const bool inter = lk.x >= 0, lft = inter && lk_left(lk.y);
 #pragma unroll
       for (int c = 0; c < NW; ++c) sWH[c * NFT + t] = common_w(ph, inter, lft, wa[c], wc[c]);
@@ -2170,7 +2183,7 @@ k_wall_forces(const FrConst C, const FrMesh m, const double* __restrict__ qtr, c
 // solver_oracle.rk_spectral_radius).  One warp per element, lanes over the
 // points; max / min are order-independent, so the result is deterministic.
 __global__ void __launch_bounds__(256)
-k_rk_lambda(const FrConst C, const FrMesh m, int p, int kind, const double* __restrict__ q,
+k_rk_lambda(const FrConst C, const FrMesh m, int p, int kind, const double* __restrict__ q, double adv,
             double* __restrict__ lam) {
   const int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -2206,13 +2219,13 @@ k_rk_lambda(const FrConst C, const FrMesh m, int p, int kind, const double* __re
   if (kind == K_NS) nu = fmax(4.0 / 3.0 * C.mu, C.kappa * (C.gamma - 1.0)) / rmin;
   else if (kind == K_ADVD) nu = C.diff;
   const double pp = (double)(n * n) * (double)(n * n);
-  lam[e] = (2 * p + 1) * amax / h + pp * nu / (h * h);
+  lam[e] = adv * amax / h + pp * nu / (h * h);
 }
 
-int launch_rk_lambda(const DiscDev& d, const double* q, double* lam, cudaStream_t st) {
+int launch_rk_lambda(const DiscDev& d, const double* q, double adv, double* lam, cudaStream_t st) {
   if (d.M == 0) return 0;
   const unsigned grid = (unsigned)((d.M * 32 + 255) / 256);
-  k_rk_lambda<<<grid, 256, 0, st>>>(d.C, d.mesh, d.p, d.kind, q, lam);
+  k_rk_lambda<<<grid, 256, 0, st>>>(d.C, d.mesh, d.p, d.kind, q, adv, lam);
   return (int)cudaGetLastError();
 }
 

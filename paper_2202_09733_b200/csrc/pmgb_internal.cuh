@@ -26,7 +26,7 @@ inline bool first_use_on_device(std::atomic<unsigned long long>& seen) {
 }
 
 enum Kind { K_EULER = 0, K_NS = 1, K_ADV = 2, K_ADVD = 3 };
-enum Tag { T_WALL_ADIABATIC = 0, T_WALL_SLIP = 1, T_FAR_FIELD = 2 };
+enum Tag { T_WALL_ADIABATIC = 0, T_WALL_SLIP = 1, T_FAR_FIELD = 2, T_WALL_ISOTHERMAL = 3 };
 
 // link.y bit layout
 __host__ __device__ inline int lk_face(int y) { return y & 3; }
@@ -62,6 +62,7 @@ struct FrConst {
   double eL[6], eR[6], lL[6], lR[6], xg[6];
   double qinf[4];
   double gamma, mu, kappa, adv_x, adv_y, diff;
+  double twall;  // T = p/rho on wall-isothermal faces (BASELINE option)
   int riemann;  // 0 Roe (reference), 1 Rusanov (BASELINE option)
   int ldg;      // 0 BR1 (reference), 1 LDG, C11 = 0, switch from the L element
 };
@@ -128,7 +129,7 @@ struct DiscDev {
 int launch_residual(const DiscDev& d, const double* q, const double* X, double eps,
                     const Epi& epi, double* out, cudaStream_t st);
 size_t fr_grad_scratch_doubles(int p, int kind, int64_t M);
-int launch_rk_lambda(const DiscDev& d, const double* q, double* lam, cudaStream_t st);
+int launch_rk_lambda(const DiscDev& d, const double* q, double adv, double* lam, cudaStream_t st);
 int launch_freeze(const DiscDev& d, const double* q, double* qtr, double* fvn, cudaStream_t st);
 int launch_local_residual(const DiscDev& d, const int64_t* elems, int64_t B, const double* Q,
                           const double* qtr, const double* fvn, double* out, cudaStream_t st);

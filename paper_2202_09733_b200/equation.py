@@ -39,6 +39,10 @@ class EquationSpec:
     # 8.0), parity-pinned to the oracle only
     riemann: str = "roe"
     viscous_scheme: str = "br1"
+    # temperature T = p / rho held by "wall-isothermal" faces (BASELINE
+    # config 4's no-slip isothermal wall; not in the reference, whose walls
+    # are adiabatic / slip, spatial.py:183-203).  None = free-stream T.
+    wall_temperature: float | None = None
 
     def __post_init__(self):
         if self.kind not in KIND_CODE:
@@ -47,6 +51,8 @@ class EquationSpec:
             raise ValueError(f"unknown Riemann flux {self.riemann!r}")
         if self.viscous_scheme not in ("br1", "ldg"):
             raise ValueError(f"unknown viscous scheme {self.viscous_scheme!r}")
+        if self.wall_temperature is not None and not self.wall_temperature > 0:
+            raise ValueError("wall temperature must be positive")
         if self.kind != "advection-diffusion" and self.mach <= 0:
             raise ValueError("Mach number must be positive")
         if self.kind == "navier-stokes" and self.reynolds <= 0:
@@ -70,6 +76,13 @@ class EquationSpec:
     def heat_conductivity(self) -> float:
         g = self.gamma
         return self.mu * g / ((g - 1.0) * self.prandtl)
+
+    @property
+    def t_wall(self) -> float:
+        """Isothermal wall temperature (p / rho); free-stream 1/(gamma Ma^2)."""
+        if self.wall_temperature is not None:
+            return float(self.wall_temperature)
+        return 0.0 if self.kind == "advection-diffusion" else 1.0 / (self.gamma * self.mach ** 2)
 
     def free_stream(self) -> np.ndarray:
         if self.kind == "advection-diffusion":

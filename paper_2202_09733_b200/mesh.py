@@ -29,7 +29,7 @@ import numpy as np
 from .operators import basis
 
 FACE_NODES = ((0, 1), (1, 2), (2, 3), (3, 0))
-BOUNDARY_TAGS = ("wall-adiabatic", "wall-slip", "far-field")
+BOUNDARY_TAGS = ("wall-adiabatic", "wall-slip", "far-field", "wall-isothermal")
 TAG_CODE = {t: i for i, t in enumerate(BOUNDARY_TAGS)}
 
 

@@ -149,7 +149,8 @@ class Discretization:
             free_stream=dp(self._qinf), D=dp(self._ops["D"]), eL=dp(self._ops["eL"]), eR=dp(self._ops["eR"]),
             lL=dp(self._ops["lL"]), lR=dp(self._ops["lR"]), xg=dp(self._ops["xg"]), geom=dp(self._geom),
             links=self._links.ctypes.data_as(_lib.c_int64_p), tags=self._tags.ctypes.data_as(_lib.c_int32_p),
-            riemann=1 if eqn.riemann == "rusanov" else 0, viscous_scheme=1 if eqn.viscous_scheme == "ldg" else 0)
+            riemann=1 if eqn.riemann == "rusanov" else 0, viscous_scheme=1 if eqn.viscous_scheme == "ldg" else 0,
+            wall_temperature=eqn.t_wall)
         h = ctypes.c_void_p()
         with torch.cuda.device(self.device):
             check(load().pmgb_disc_create(ctypes.byref(desc), ctypes.byref(h)), "disc_create")
@@ -202,7 +203,7 @@ class Discretization:
             raise ValueError("forces are only defined for flow equations")
         walls = getattr(self, "_wall_pairs", None)
         if walls is None:
-            ef = np.argwhere((self._tags >= 0) & (self._tags <= TAG_CODE["wall-slip"]))
+            ef = np.argwhere((self._tags >= 0) & (self._tags != TAG_CODE["far-field"]))
             walls = self._wall_pairs = (
                 len(ef),
                 torch.as_tensor(ef[:, 0].astype(np.int32), device=self.device),
@@ -253,8 +254,9 @@ class Discretization:
     def rk_lambda(self, q: torch.Tensor) -> torch.Tensor:
         """Per-element spectral-radius estimate for the RK smoother's local
         pseudo-time step (pmgb_rk_lambda; oracle: rk_spectral_radius)."""
+        from .operators import rk_adv_coef
         lam = torch.empty(self.mesh.n_elements, dtype=torch.float64, device=self.device)
-        check(load().pmgb_rk_lambda(self._h, ptr(q), lam.data_ptr(), stream()), "rk_lambda")
+        check(load().pmgb_rk_lambda(self._h, ptr(q), rk_adv_coef(self.p), lam.data_ptr(), stream()), "rk_lambda")
         return lam
 
     def rk_dtau(self, lam: torch.Tensor, s: float, cfl: float) -> torch.Tensor:

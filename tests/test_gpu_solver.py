@@ -221,6 +221,26 @@ def test_pmg_solve_lowmach_matches_reference(cuda):
     assert rel(q, G["c3/q"]) <= 1e-9
 
 
+def test_pmg_solve_rk_lowmach_matches_oracle(cuda):
+    """Config-3 physics (Ma 1e-3) with BASELINE's smoothers: pseudo-time RK
+    on p = 4..1, EJ on p = 0.  Acoustic-dominated, so it relies on the
+    Bloch-analysis advective radius in lambda_e (with (2p+1) it diverges,
+    device and oracle alike)."""
+    c = cases.config(3, nx=8)
+    d = Discretization(c.mesh, 4, c.eqn)
+    hier = pmg.PHierarchy.parse("4-3-2-1-0", "2", "rk-rk-rk-rk-ej")
+    ctx = pmg.PmgContext(d, pmg.PmgPrecondConfig(hier, smoother_shift=1e3))
+    q, st = pmg.pmg_solve(ctx, t(c.q0), nk.PtcConfig(dtau_init=0.1, max_iters=4, rtol=1e-14))
+    o = OracleDisc(c.mesh, 4, c.eqn)
+    octx = so.Pmg(o, "4-3-2-1-0", 2, smoother_shift=1e3, smoother="rk-rk-rk-rk-ej")
+    qo, sto = so.pmg_solve(octx, c.q0, 0.1, max_iters=4, rtol=1e-14)
+    assert not st["aborted"] and st["iters"] == sto["iters"] == 4
+    h, ho = np.array(st["history"]), np.array(sto["history"])
+    assert h[-1, 1] < 0.1
+    assert np.allclose(h[:, 1], ho[:, 1], rtol=1e-6, atol=1e-12)
+    assert rel(q, qo) <= 1e-9
+
+
 def test_ptc_halves_on_nonphysical(cuda):
     # a stage solve that drives the state non-physical must halve dtau
     m = mm.generate_box(2, 2, 1.0, 1.0, periodic=True)

@@ -21,6 +21,7 @@ from paper_2202_09733_b200 import cases, mesh as mm, pmg
 from paper_2202_09733_b200 import time_integration as ti
 from paper_2202_09733_b200.equation import EquationSpec
 from paper_2202_09733_b200.harness import DEFAULTS, pmg_precond_config
+from paper_2202_09733_b200.operators import fr_advection_radius, rk_adv_coef
 
 GE = np.load(Path(__file__).parent / "golden" / "golden_esdirk3.npz")
 
@@ -59,7 +60,7 @@ def test_oracle_esdirk3_step_matches_reference():
 
 
 def test_rk_spectral_radius_free_stream():
-    # uniform free stream on a uniform box: lambda = (2p+1)(|u|+c)/h + (p+1)^4 nu/h^2
+    # uniform free stream on a uniform box: lambda = A_p (|u|+c)/h + (p+1)^4 nu/h^2
     m = mm.generate_box(4, 3, 2.0, 3.0, periodic=True)
     eqn = EquationSpec(kind="navier-stokes", mach=0.4, reynolds=50.0, ref_length=2.0)
     p = 3
@@ -71,21 +72,33 @@ def test_rk_spectral_radius_free_stream():
     a = np.hypot(u / rho, v / rho) + np.sqrt(eqn.gamma * pr / rho)
     h = 0.5  # 0.5 x 1.0 cells: 4 |det| / max(L) = 4 (0.25 * 0.5) / 1.0
     nu = max(4.0 / 3.0 * eqn.mu, eqn.heat_conductivity * (eqn.gamma - 1.0)) / rho
-    ref = (2 * p + 1) * a / h + (p + 1) ** 4 * nu / h ** 2
+    ref = rk_adv_coef(p) * a / h + (p + 1) ** 4 * nu / h ** 2
     assert np.allclose(lam, ref, rtol=1e-14, atol=0)
     # scalar advection-diffusion: state independent
     e2 = EquationSpec(kind="advection-diffusion", advection=(0.6, 0.8), diffusivity=0.01)
     o2 = OracleDisc(m, 2, e2)
     lam2 = so.rk_spectral_radius(o2, np.zeros(o2.n_dofs))
-    assert np.allclose(lam2, 5 * 1.0 / h + 81 * 0.01 / h ** 2, rtol=1e-14)
+    assert np.allclose(lam2, rk_adv_coef(2) * 1.0 / h + 81 * 0.01 / h ** 2, rtol=1e-14)
+
+
+def test_fr_advection_radius():
+    # p = 0 is first-order upwind FV (radius 2/h = 2 rho_0 / h), p = 1 is 3;
+    # larger p grow faster than 2p+1 (Bloch analysis of the FR operator)
+    assert abs(fr_advection_radius(0) - 1.0) < 1e-13
+    assert abs(fr_advection_radius(1) - 3.0) < 1e-12
+    r = [fr_advection_radius(p) for p in range(6)]
+    assert all(b > a for a, b in zip(r, r[1:]))
+    assert 13.8 < r[4] < 14.0 and 18.8 < r[5] < 19.0
+    assert rk_adv_coef(3) == 2.0 * np.sqrt(2.0) * r[3]
 
 
 def test_rk_smoother_contracts_the_level_defect():
-    # ten sweeps on a single level reduce ||defect|| (after a non-normal
-    # transient growth of the first sweeps, measured: x1.4 then decay)
+    # twenty sweeps on a single level reduce ||defect|| (after a non-normal
+    # transient growth of the first sweeps; measured ratios after 1 / 10 /
+    # 20 / 40 sweeps: 1.18, 0.86, 0.38, 0.10)
     c = cases.config(1, nx=6)
     o = OracleDisc(c.mesh, c.p, c.eqn)
-    ctx = so.Pmg(o, "3", 10, smoother="rk")
+    ctx = so.Pmg(o, "3", 20, smoother="rk")
     shift = 1.0 / (0.43 * c.dt) + 1.0 / c.dt
     ctx.prepare(c.q0, shift)
     lev = ctx.levels[0]
