@@ -535,16 +535,19 @@ def time_steps(torch, case2, args):
     from paper_2202_09733_b200.spatial import Discretization
     out = {}
     c1 = cases.config(1)
-    runs = (("config1", c1, "ej-ej"), ("config2", case2, "ej-ej"), ("config2_rk", case2, "rk-ej"))
+    # config2_fp32: pmg.block_precision = fp32 (FP32-stored EJ factors, FP64
+    # arithmetic; not in the reference) -- the EJ apply is the step's top kernel
+    runs = (("config1", c1, "ej-ej", "fp64"), ("config2", case2, "ej-ej", "fp64"),
+            ("config2_rk", case2, "rk-ej", "fp64"), ("config2_fp32", case2, "ej-ej", "fp32"))
     discs = {}
-    for key, c, smoothers in runs:
+    for key, c, smoothers, prec in runs:
         d = discs.setdefault(c.name, Discretization(c.mesh, c.p, c.eqn))
         cfg = {"case.precond": "pmg", "pmg.levels": c.levels, "pmg.smooth": "2", "pmg.smoother": smoothers,
                "pmg.smoother_shift": c.extra["smoother_shift"], "gmres.kdim": c.kdim,
-               "gmres.rtol": 1e-3, "ptc.dtau_init": c.dt, "ptc.rtol": 1e-4}
+               "gmres.rtol": 1e-3, "ptc.dtau_init": c.dt, "ptc.rtol": 1e-4, "pmg.block_precision": prec}
         q = torch.as_tensor(c.q0, device="cuda")
         sch = ti.get_scheme(c.scheme)
-        rec = {"scheme": c.scheme, "pmg": c.levels, "smoothers": smoothers,
+        rec = {"scheme": c.scheme, "pmg": c.levels, "smoothers": smoothers, "block_precision": prec,
                "smoother_shift": c.extra["smoother_shift"], "dt": c.dt}
         try:
             drv = ImplicitDriver(d, cfg)

@@ -218,6 +218,16 @@ PMGB_API int pmgb_ej_apply(int64_t n_elem, int32_t sz, const double* XT, const u
 PMGB_API int pmgb_ej_update(int64_t n_elem, int32_t sz, const double* XT, const uint8_t* perm, const double* d,
                             double omega, const double* base, double* out, void* stream);
 
+/* Option pmg.block_precision = fp32 (not in the reference, whose blocks are
+ * float64): the factor XT stored in FP32 (round to nearest), applied with
+ * FP64 arithmetic -- half the bytes of the step's dominant HBM stream and
+ * of the per-level block memory.  Same (perm, layout) as the FP64 calls. */
+PMGB_API int pmgb_blocks_demote(int64_t n_elem, int32_t sz, const double* XT, float* XT32, void* stream);
+PMGB_API int pmgb_ej_apply_f32(int64_t n_elem, int32_t sz, const float* XT32, const uint8_t* perm,
+                               const double* x, double* y, void* stream);
+PMGB_API int pmgb_ej_update_f32(int64_t n_elem, int32_t sz, const float* XT32, const uint8_t* perm,
+                                const double* d, double omega, const double* base, double* out, void* stream);
+
 /* pMG transfers (pmg.py:117-136).  T is a HOST (n_out x n_in) matrix:
  * Gamma for restriction, Pi for prolongation.
  *   pmgb_transfer:     dst = (T (x) T) (src - src_base)   [src_base may be NULL]

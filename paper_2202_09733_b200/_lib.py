@@ -84,6 +84,11 @@ SIGNATURES = {
                                      c_void_p]),
     "pmgb_ej_update": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int32, c_void_p, c_void_p, c_void_p,
                                       ctypes.c_double, c_void_p, c_void_p, c_void_p]),
+    "pmgb_blocks_demote": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int32, c_void_p, c_void_p, c_void_p]),
+    "pmgb_ej_apply_f32": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int32, c_void_p, c_void_p, c_void_p, c_void_p,
+                                         c_void_p]),
+    "pmgb_ej_update_f32": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int32, c_void_p, c_void_p, c_void_p,
+                                          ctypes.c_double, c_void_p, c_void_p, c_void_p]),
     "pmgb_transfer": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                                      c_double_p, c_void_p, c_void_p, c_void_p, ctypes.c_int32, c_void_p]),
     "pmgb_dot": (ctypes.c_int, [ctypes.c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),

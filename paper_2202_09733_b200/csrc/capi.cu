@@ -21,6 +21,9 @@ int launch_ilu_persistent(int SZ, int n_lo, const int* lo_ptr, const int* lo_row
                           unsigned* bar, int max_rows, cudaStream_t st);
 int launch_block_gemv(int64_t M, int SZ, const double* XT, const uint8_t* perm, const double* x, double omega,
                       const double* base, double* out, cudaStream_t st);
+int launch_block_gemv_f32(int64_t M, int SZ, const float* XT, const uint8_t* perm, const double* x, double omega,
+                          const double* base, double* out, cudaStream_t st);
+int launch_demote(int64_t n, const double* src, float* dst, cudaStream_t st);
 int launch_transfer(int64_t M, int nv, int nin, int nout, const double* T, const double* src,
                     const double* src_base, double* dst, int accumulate, cudaStream_t st);
 int launch_dot(int64_t n, const double* x, const double* y, double* out, int do_sqrt, cudaStream_t st);
@@ -336,6 +339,25 @@ PMGB_API int pmgb_ej_update(int64_t M, int32_t sz, const double* XT, const uint8
   if (!base) return -1;
   g_launches += 1;
   return launch_block_gemv(M, sz, XT, perm, dd, omega, base, out, S(stream));
+}
+
+PMGB_API int pmgb_blocks_demote(int64_t M, int32_t sz, const double* XT, float* XT32, void* stream) {
+  if (M < 0 || sz <= 0 || (M > 0 && (!XT || !XT32))) return -1;
+  g_launches += 1;
+  return launch_demote(M * (int64_t)sz * sz, XT, XT32, S(stream));
+}
+
+PMGB_API int pmgb_ej_apply_f32(int64_t M, int32_t sz, const float* XT32, const uint8_t* perm, const double* x,
+                               double* y, void* stream) {
+  g_launches += 1;
+  return launch_block_gemv_f32(M, sz, XT32, perm, x, 0.0, nullptr, y, S(stream));
+}
+
+PMGB_API int pmgb_ej_update_f32(int64_t M, int32_t sz, const float* XT32, const uint8_t* perm, const double* dd,
+                                double omega, const double* base, double* out, void* stream) {
+  if (!base) return -1;
+  g_launches += 1;
+  return launch_block_gemv_f32(M, sz, XT32, perm, dd, omega, base, out, S(stream));
 }
 
 PMGB_API int pmgb_transfer(int64_t M, int32_t nv, int32_t nin, int32_t nout, const double* T, const double* src,

@@ -293,6 +293,90 @@ k_block_gemv2(int64_t M, int SZ, const double* __restrict__ XT, const uint8_t* _
   }
 }
 
+// FP32-stored factor (pmg.block_precision = fp32: half the bytes of the
+// dominant HBM stream of a pMG step), FP64 arithmetic: the same map, four
+// adjacent rows per thread with 16-byte float4 loads (SZ % 4 == 0), or one
+// row per thread otherwise.  Each product is formed in FP64 from the
+// widened FP32 entry.
+template <bool UPDATE>
+__global__ void __launch_bounds__(256)
+k_block_gemv4f(int64_t M, int SZ, const float* __restrict__ XT, const uint8_t* __restrict__ perm,
+               const double* __restrict__ x, double omega, const double* __restrict__ base,
+               double* __restrict__ out) {
+  extern __shared__ double xs[];
+  const int Q = SZ >> 2;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x;
+  const int64_t total = M * Q;
+  const int64_t e_first = t0 / Q;
+  int64_t e_last = (t0 + blockDim.x - 1) / Q;
+  if (e_last > M - 1) e_last = M - 1;
+  const int span = (int)(e_last - e_first + 1);
+  for (int i = threadIdx.x; i < span * SZ; i += blockDim.x) {
+    const int el = i / SZ, c = i - el * SZ;
+    const int64_t e = e_first + el;
+    xs[i] = __ldg(x + e * SZ + perm[e * 2 * SZ + c]);
+  }
+  __syncthreads();
+  const int64_t t = t0 + threadIdx.x;
+  if (t >= total) return;
+  const int64_t e = t / Q;
+  const int r = 4 * (int)(t - e * Q);
+  const float4* Ae = reinterpret_cast<const float4*>(XT + e * (int64_t)SZ * SZ + r);
+  const double* xe = xs + (e - e_first) * SZ;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, b0 = 0.0, b1 = 0.0, b2 = 0.0, b3 = 0.0;
+  int c = 0;
+  for (; c + 2 <= SZ; c += 2) {
+    const float4 v = __ldg(Ae + (int64_t)c * Q);
+    const float4 w = __ldg(Ae + (int64_t)(c + 1) * Q);
+    const double x0 = xe[c], x1 = xe[c + 1];
+    a0 += (double)v.x * x0;
+    a1 += (double)v.y * x0;
+    a2 += (double)v.z * x0;
+    a3 += (double)v.w * x0;
+    b0 += (double)w.x * x1;
+    b1 += (double)w.y * x1;
+    b2 += (double)w.z * x1;
+    b3 += (double)w.w * x1;
+  }
+  if (c < SZ) {
+    const float4 v = __ldg(Ae + (int64_t)c * Q);
+    const double x0 = xe[c];
+    a0 += (double)v.x * x0;
+    a1 += (double)v.y * x0;
+    a2 += (double)v.z * x0;
+    a3 += (double)v.w * x0;
+  }
+  const uint8_t* q = perm + e * 2 * SZ + SZ;
+  const double y[4] = {a0 + b0, a1 + b1, a2 + b2, a3 + b3};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int64_t o = e * SZ + q[r + k];
+    out[o] = UPDATE ? base[o] + omega * y[k] : y[k];
+  }
+}
+
+template <bool UPDATE>
+__global__ void __launch_bounds__(256)
+k_block_gemv1f(int64_t M, int SZ, const float* __restrict__ XT, const uint8_t* __restrict__ perm,
+               const double* __restrict__ x, double omega, const double* __restrict__ base,
+               double* __restrict__ out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= M * SZ) return;
+  const int64_t e = t / SZ;
+  const int r = (int)(t - e * SZ);
+  const float* Ae = XT + e * (int64_t)SZ * SZ + r;
+  const uint8_t* pe = perm + e * 2 * SZ;
+  double a = 0.0;
+  for (int c = 0; c < SZ; ++c) a += (double)__ldg(Ae + (int64_t)c * SZ) * __ldg(x + e * SZ + pe[c]);
+  const int64_t o = e * SZ + pe[SZ + r];
+  out[o] = UPDATE ? base[o] + omega * a : a;
+}
+
+__global__ void __launch_bounds__(256) k_demote(int64_t n, const double* __restrict__ src, float* __restrict__ dst) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = __double2float_rn(src[i]);
+}
+
 // Block-CSR matvec y_i = sum_k A_k x_{j_k} (SparseBlockMatrix.matvec,
 // newton_krylov.py:243-251): thread per (row, component r); each block's
 // product is summed first and then added to the row accumulator, in the
@@ -798,6 +882,34 @@ int launch_block_gemv(int64_t M, int SZ, const double* XT, const uint8_t* perm, 
     k_block_gemv<true><<<grid, 256, smem, st>>>(M, SZ, XT, perm, x, omega, base, out);
   else
     k_block_gemv<false><<<grid, 256, smem, st>>>(M, SZ, XT, perm, x, 0.0, nullptr, out);
+  return (int)cudaGetLastError();
+}
+
+int launch_block_gemv_f32(int64_t M, int SZ, const float* XT, const uint8_t* perm, const double* x, double omega,
+                          const double* base, double* out, cudaStream_t st) {
+  const int64_t n = M * SZ;
+  if (n <= 0) return 0;
+  if ((SZ & 3) == 0) {
+    const int64_t nt = M * (SZ / 4);
+    const unsigned grid = (unsigned)((nt + 255) / 256);
+    const size_t smem = sizeof(double) * (size_t)((255 / (SZ / 4)) + 2) * SZ;
+    if (base)
+      k_block_gemv4f<true><<<grid, 256, smem, st>>>(M, SZ, XT, perm, x, omega, base, out);
+    else
+      k_block_gemv4f<false><<<grid, 256, smem, st>>>(M, SZ, XT, perm, x, 0.0, nullptr, out);
+    return (int)cudaGetLastError();
+  }
+  const unsigned grid = (unsigned)((n + 255) / 256);
+  if (base)
+    k_block_gemv1f<true><<<grid, 256, 0, st>>>(M, SZ, XT, perm, x, omega, base, out);
+  else
+    k_block_gemv1f<false><<<grid, 256, 0, st>>>(M, SZ, XT, perm, x, 0.0, nullptr, out);
+  return (int)cudaGetLastError();
+}
+
+int launch_demote(int64_t n, const double* src, float* dst, cudaStream_t st) {
+  if (n <= 0) return 0;
+  k_demote<<<148 * 8, 256, 0, st>>>(n, src, dst);
   return (int)cudaGetLastError();
 }
 

@@ -200,14 +200,28 @@ class BlockJacobian:
     def __init__(self, disc: Discretization, shift: float, XT: torch.Tensor, perm: torch.Tensor, blocksT=None):
         self.disc = disc
         self.shift = shift
-        self.XT = XT
+        self.XT = XT          # float64, or float32 with pmg.block_precision = fp32
         self.perm = perm
         self.blocksT = blocksT
 
     @property
+    def precision(self) -> str:
+        return "fp32" if self.XT.dtype == torch.float32 else "fp64"
+
+    def demote(self) -> "BlockJacobian":
+        """Store the factor in FP32 (round to nearest) and free the FP64
+        copy; apply/update then read half the bytes (pmgb_blocks_demote)."""
+        if self.XT.dtype == torch.float64:
+            X32 = torch.empty(self.XT.shape, dtype=torch.float32, device=self.XT.device)
+            check(load().pmgb_blocks_demote(self.XT.shape[0], self.XT.shape[1], self.XT.data_ptr(),
+                                            X32.data_ptr(), stream()), "blocks_demote")
+            self.XT = X32
+        return self
+
+    @property
     def inv(self):
         M, sz = self.XT.shape[0], self.XT.shape[1]
-        X = self.XT.transpose(1, 2)
+        X = self.XT.double().transpose(1, 2)
         p = self.perm[:, :sz].long()
         q = self.perm[:, sz:].long()
         rows = torch.gather(X, 1, p[:, :, None].expand(M, sz, sz))
@@ -223,17 +237,18 @@ class BlockJacobian:
         is_np = not isinstance(X, torch.Tensor)
         Xd = to_device(X, self.disc.device)
         out = torch.empty_like(Xd)
-        check(load().pmgb_ej_apply(self.disc.mesh.n_elements, self.disc.elem_size, self.XT.data_ptr(),
-                                   self.perm.data_ptr(), ptr(Xd), ptr(out), stream()), "ej_apply")
+        fn = load().pmgb_ej_apply_f32 if self.XT.dtype == torch.float32 else load().pmgb_ej_apply
+        check(fn(self.disc.mesh.n_elements, self.disc.elem_size, self.XT.data_ptr(),
+                 self.perm.data_ptr(), ptr(Xd), ptr(out), stream()), "ej_apply")
         return out.cpu().numpy() if is_np else out
 
     def update(self, d: torch.Tensor, omega: float, base: torch.Tensor, out=None) -> torch.Tensor:
         """out = base + omega * B^-1 d (smooth_ej, pmg.py:164)."""
         if out is None:
             out = torch.empty_like(base)
-        check(load().pmgb_ej_update(self.disc.mesh.n_elements, self.disc.elem_size, self.XT.data_ptr(),
-                                    self.perm.data_ptr(), ptr(d), float(omega), ptr(base), ptr(out), stream()),
-              "ej_update")
+        fn = load().pmgb_ej_update_f32 if self.XT.dtype == torch.float32 else load().pmgb_ej_update
+        check(fn(self.disc.mesh.n_elements, self.disc.elem_size, self.XT.data_ptr(),
+                 self.perm.data_ptr(), ptr(d), float(omega), ptr(base), ptr(out), stream()), "ej_update")
         return out
 
 
@@ -466,7 +481,7 @@ def ilu0_apply(fac: Ilu0Factors, X, offsets=None, fused: bool = True):
 
 
 def assemble_element_blocks(disc: Discretization, data, shift: float, frozen=None, eps: float = FD_EPS,
-                            keep_blocks: bool = True) -> BlockJacobian:
+                            keep_blocks: bool = True, precision: str = "fp64") -> BlockJacobian:
     """FD element blocks of shift I - dR/dq and their inverses.
 
     ``frozen`` is accepted for signature parity; the device freeze of
@@ -481,7 +496,12 @@ def assemble_element_blocks(disc: Discretization, data, shift: float, frozen=Non
     check(load().pmgb_blocks_assemble(disc._h, ptr(q), float(shift), float(eps), blocksT.data_ptr(),
                                       XT.data_ptr(), perm.data_ptr(), stream()), "blocks_assemble")
     raise_status()
-    return BlockJacobian(disc, shift, XT, perm, blocksT if keep_blocks else None)
+    bj = BlockJacobian(disc, shift, XT, perm, blocksT if keep_blocks else None)
+    if precision == "fp32":
+        bj.demote()
+    elif precision != "fp64":
+        raise ValueError(f"unknown block precision {precision!r}")
+    return bj
 
 
 def ej_apply(blocks: BlockJacobian, X):

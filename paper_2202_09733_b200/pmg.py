@@ -83,8 +83,13 @@ class PmgPrecondConfig:
     smoother_shift: float = 0.0
     rk_cfl: float = 1.5
     rk_alphas: tuple = (0.25, 1.0 / 3.0, 0.5, 1.0)
+    # storage of the EJ block factors: fp64 (reference) or fp32 (option:
+    # FP32 storage, FP64 arithmetic -- halves the EJ apply's HBM bytes)
+    block_precision: str = "fp64"
 
     def __post_init__(self):
+        if self.block_precision not in ("fp64", "fp32"):
+            raise ValueError(f"unknown block precision {self.block_precision!r}")
         if self.m_max < 1:
             raise ValueError("m_max must be >= 1")
         if self.rk_cfl <= 0.0 or not self.rk_alphas:
@@ -222,7 +227,7 @@ class PmgContext:
                 lev.lam = lev.disc.rk_lambda(qk)
             else:
                 lev.blocks = nk.assemble_element_blocks(lev.disc, qk, shift + self.cfg.smoother_shift,
-                                                        keep_blocks=False)
+                                                        keep_blocks=False, precision=self.cfg.block_precision)
             lev.sparse = lev.ilu = None
         raise_status()
         self.cycles_done = 0
