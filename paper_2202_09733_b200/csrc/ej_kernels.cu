@@ -15,6 +15,7 @@
 // perm[sz:2sz] = q (uint8).  The GEMV applies the permutations on the fly:
 //     y[q_r] = sum_c XT[c][r] x[p_c]
 // so nothing is ever un-permuted in memory.
+#include <cstdlib>
 #include <climits>
 #include <cstdint>
 
@@ -298,7 +299,7 @@ k_block_gemv2(int64_t M, int SZ, const double* __restrict__ XT, const uint8_t* _
 // adjacent rows per thread with 16-byte float4 loads (SZ % 4 == 0), or one
 // row per thread otherwise.  Each product is formed in FP64 from the
 // widened FP32 entry.
-template <bool UPDATE>
+template <bool UPDATE, int U>
 __global__ void __launch_bounds__(256)
 k_block_gemv4f(int64_t M, int SZ, const float* __restrict__ XT, const uint8_t* __restrict__ perm,
                const double* __restrict__ x, double omega, const double* __restrict__ base,
@@ -311,47 +312,50 @@ k_block_gemv4f(int64_t M, int SZ, const float* __restrict__ XT, const uint8_t* _
   int64_t e_last = (t0 + blockDim.x - 1) / Q;
   if (e_last > M - 1) e_last = M - 1;
   const int span = (int)(e_last - e_first + 1);
+  const int64_t t = t0 + threadIdx.x;
+  const bool live = t < total;
+  const int64_t e = live ? t / Q : e_first;
+  const int r = live ? 4 * (int)(t - e * Q) : 0;
+  const float4* Ae = reinterpret_cast<const float4*>(XT + e * (int64_t)SZ * SZ + r);
+  // software pipeline: the first U factor columns are in flight while the
+  // CTA gathers x[p_c] into shared memory (the gather is a dependent
+  // perm -> x load chain, the fixed cost of every CTA)
+  float4 v[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) v[u] = live ? __ldg(Ae + (int64_t)u * Q) : make_float4(0.f, 0.f, 0.f, 0.f);
   for (int i = threadIdx.x; i < span * SZ; i += blockDim.x) {
     const int el = i / SZ, c = i - el * SZ;
-    const int64_t e = e_first + el;
-    xs[i] = __ldg(x + e * SZ + perm[e * 2 * SZ + c]);
+    const int64_t ee = e_first + el;
+    xs[i] = __ldg(x + ee * SZ + perm[ee * 2 * SZ + c]);
   }
   __syncthreads();
-  const int64_t t = t0 + threadIdx.x;
-  if (t >= total) return;
-  const int64_t e = t / Q;
-  const int r = 4 * (int)(t - e * Q);
-  const float4* Ae = reinterpret_cast<const float4*>(XT + e * (int64_t)SZ * SZ + r);
+  if (!live) return;
   const double* xe = xs + (e - e_first) * SZ;
-  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, b0 = 0.0, b1 = 0.0, b2 = 0.0, b3 = 0.0;
-  int c = 0;
-  for (; c + 2 <= SZ; c += 2) {
-    const float4 v = __ldg(Ae + (int64_t)c * Q);
-    const float4 w = __ldg(Ae + (int64_t)(c + 1) * Q);
-    const double x0 = xe[c], x1 = xe[c + 1];
-    a0 += (double)v.x * x0;
-    a1 += (double)v.y * x0;
-    a2 += (double)v.z * x0;
-    a3 += (double)v.w * x0;
-    b0 += (double)w.x * x1;
-    b1 += (double)w.y * x1;
-    b2 += (double)w.z * x1;
-    b3 += (double)w.w * x1;
-  }
-  if (c < SZ) {
-    const float4 v = __ldg(Ae + (int64_t)c * Q);
-    const double x0 = xe[c];
-    a0 += (double)v.x * x0;
-    a1 += (double)v.y * x0;
-    a2 += (double)v.z * x0;
-    a3 += (double)v.w * x0;
+  double a[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
+  // SZ % 4 == 0 and U = 4: whole batches; the next batch loads while this
+  // one is consumed
+  for (int c = 0; c < SZ; c += U) {
+    float4 w[U];
+    const bool more = c + U < SZ;
+#pragma unroll
+    for (int u = 0; u < U; ++u) w[u] = more ? __ldg(Ae + (int64_t)(c + U + u) * Q) : v[u];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const double xu = xe[c + u];
+      a[u & 1][0] += (double)v[u].x * xu;
+      a[u & 1][1] += (double)v[u].y * xu;
+      a[u & 1][2] += (double)v[u].z * xu;
+      a[u & 1][3] += (double)v[u].w * xu;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = w[u];
   }
   const uint8_t* q = perm + e * 2 * SZ + SZ;
-  const double y[4] = {a0 + b0, a1 + b1, a2 + b2, a3 + b3};
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
+    const double y = a[0][k] + a[1][k];
     const int64_t o = e * SZ + q[r + k];
-    out[o] = UPDATE ? base[o] + omega * y[k] : y[k];
+    out[o] = UPDATE ? base[o] + omega * y : y;
   }
 }
 
@@ -894,9 +898,9 @@ int launch_block_gemv_f32(int64_t M, int SZ, const float* XT, const uint8_t* per
     const unsigned grid = (unsigned)((nt + 255) / 256);
     const size_t smem = sizeof(double) * (size_t)((255 / (SZ / 4)) + 2) * SZ;
     if (base)
-      k_block_gemv4f<true><<<grid, 256, smem, st>>>(M, SZ, XT, perm, x, omega, base, out);
+      k_block_gemv4f<true, 4><<<grid, 256, smem, st>>>(M, SZ, XT, perm, x, omega, base, out);
     else
-      k_block_gemv4f<false><<<grid, 256, smem, st>>>(M, SZ, XT, perm, x, 0.0, nullptr, out);
+      k_block_gemv4f<false, 4><<<grid, 256, smem, st>>>(M, SZ, XT, perm, x, 0.0, nullptr, out);
     return (int)cudaGetLastError();
   }
   const unsigned grid = (unsigned)((n + 255) / 256);
