@@ -4,7 +4,7 @@
     VARIANT = scheme:smoothers:smoother_shift[:rk_cfl[:smooth[:stages]]]
               e.g. esdirk3:rk-ej:50:1.5:1-2:0.25/0.5/1  (stages '/'-separated)
     env: NX (mesh override), MAX_PTC, RESTARTS (caps for exploration runs),
-         DT_SCALE (multiplies the case's dt)
+         DT_SCALE (multiplies the case's dt), BLOCK_PRECISION (fp64 | fp32)
 
 Prints one JSON line per variant: per-step device wall time (synchronised),
 PTC / GMRES iteration counts, peak device memory.  Used for the DESIGN.md
@@ -47,7 +47,8 @@ def main():
                "pmg.smoother_shift": shift, "pmg.rk.cfl": cfl, "gmres.kdim": c.kdim, "gmres.rtol": 1e-3,
                "ptc.dtau_init": c.dt, "ptc.rtol": 1e-4,
                "ptc.max_iters": int(os.environ.get("MAX_PTC", 100)),
-               "gmres.max_restarts": int(os.environ.get("RESTARTS", 10))}
+               "gmres.max_restarts": int(os.environ.get("RESTARTS", 10)),
+               "pmg.block_precision": os.environ.get("BLOCK_PRECISION", "fp64")}
         sch = ti.get_scheme(scheme)
         q = torch.as_tensor(c.q0, device="cuda")
         torch.cuda.reset_peak_memory_stats()
