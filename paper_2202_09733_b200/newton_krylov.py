@@ -33,7 +33,7 @@ from . import _lib
 from ._lib import check, load
 from .equation import NonPhysicalStateError
 from .spatial import Discretization, raise_status
-from .vec import any_nonzero, lincomb, nrm2, ptr, stream, to_device
+from .vec import active_partition, any_nonzero, dot, lincomb, nrm2, ptr, stream, to_device
 
 FD_EPS = 1e-6
 
@@ -106,6 +106,24 @@ def _back_substitute(H, g):
     return y
 
 
+def _mgs_partitioned(V, j, w, thresh):
+    """Element-partitioned modified Gram-Schmidt: each
+    projection h_ij = V_i . w is an owned-range dot summed over the ranks
+    before w -= h_ij V_i, i.e. j+1 sequential all-reduces per Arnoldi step,
+    the reference's MGS order (newton_krylov.py:119-127)."""
+    ww = dot(w, w)
+    if not np.isfinite(ww):
+        return None, True
+    h = np.zeros(j + 2)
+    for i in range(j + 1):
+        h[i] = dot(V[i], w)
+        lincomb((1.0, -h[i]), (w, V[i]), out=w)
+    h[j + 1] = np.sqrt(dot(w, w))
+    if h[j + 1] > thresh:
+        lincomb((1.0 / h[j + 1],), (w,), out=V[j + 1])
+    return h, False
+
+
 def gmres_solve(matvec, b, cfg: KrylovConfig, x0=None, precond=None):
     """Right-preconditioned restarted GMRES(m), newton_krylov.py:79-151.
 
@@ -147,11 +165,16 @@ def gmres_solve(matvec, b, cfg: KrylovConfig, x0=None, precond=None):
         breakdown = False
         for j in range(m):
             w = matvec(precond(V[j]))
-            check(lib.pmgb_mgs(n, V.data_ptr(), n, j, ptr(w), Hd[j].data_ptr(), thresh,
-                               flag.data_ptr(), stream()), "mgs")
-            hcol = Hd[j, :j + 2].cpu().numpy()
-            raise_status()
-            if int(flag.item()):
+            if active_partition() is None:
+                check(lib.pmgb_mgs(n, V.data_ptr(), n, j, ptr(w), Hd[j].data_ptr(), thresh,
+                                   flag.data_ptr(), stream()), "mgs")
+                hcol = Hd[j, :j + 2].cpu().numpy()
+                raise_status()
+                nonfinite = bool(int(flag.item()))
+            else:
+                raise_status()
+                hcol, nonfinite = _mgs_partitioned(V, j, w, thresh)
+            if nonfinite:
                 raise RuntimeError(f"non-finite Arnoldi vector at inner iteration {total + 1}")
             H[:j + 2, j] = hcol
             total += 1
@@ -493,6 +516,7 @@ def assemble_element_blocks(disc: Discretization, data, shift: float, frozen=Non
     XT = torch.empty((M, sz, sz), dtype=torch.float64, device=disc.device)
     perm = torch.empty((M, 2 * sz), dtype=torch.uint8, device=disc.device)
     blocksT = torch.empty_like(XT) if keep_blocks else XT
+    disc.sync_halo(q)
     check(load().pmgb_blocks_assemble(disc._h, ptr(q), float(shift), float(eps), blocksT.data_ptr(),
                                       XT.data_ptr(), perm.data_ptr(), stream()), "blocks_assemble")
     raise_status()

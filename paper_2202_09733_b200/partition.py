@@ -15,6 +15,18 @@ The exchange is one ``all_gather`` of every rank's first and last ``halo``
 owned rows (NCCL on GPUs, gloo in the CPU tests).  Each rank copies its
 neighbours' rows into its halo.  Periodic in y: rank 0's lower halo is the
 last rank's top rows.  With one rank it degenerates to a local wrap copy.
+
+The partitioned SOLVER (``HaloDiscretization`` + ``vec.set_partition``)
+reuses the same strips for the whole JFNK-pMG step: every kernel that
+reads neighbours (R and its fused epilogues on every pMG level, the EJ
+block assembly) first refreshes the halo rows of its input vectors; the
+element-local work (EJ apply, RK stages, transfers, vector algebra) runs
+on the strip as is, halo entries included (they are overwritten before
+anything reads them); and every reduction -- norms, dots, the Arnoldi MGS
+(one all-reduce per projection, the reference's order), the status word --
+covers the owned elements only and is summed over the ranks.  So each
+rank's owned rows follow the single-mesh solver up to the rounding of the
+rank-split sums.
 """
 
 from __future__ import annotations
@@ -24,6 +36,7 @@ import torch
 import torch.distributed as dist
 
 from .mesh import build_mesh
+from .spatial import Discretization
 
 
 class SlabPartition:
@@ -63,6 +76,11 @@ class SlabPartition:
     def _rows(self, v, r0, nrows, sz):
         return v[r0 * self.nx * sz:(r0 + nrows) * self.nx * sz]
 
+    @staticmethod
+    def _staged(t: torch.Tensor) -> torch.Tensor:
+        """gloo moves host tensors: stage device data through the host."""
+        return t.cpu() if (t.is_cuda and dist.get_backend() == "gloo") else t
+
     def exchange(self, q_local: torch.Tensor, elem_size: int, group=None):
         """Fill the halo rows of ``q_local`` (local strip layout) in place
         from the neighbouring ranks' owned rows."""
@@ -71,14 +89,37 @@ class SlabPartition:
         if self.world == 1 or not (dist.is_available() and dist.is_initialized()):
             got = [send]
         else:
-            got = [torch.empty_like(send) for _ in range(self.world)]
-            dist.all_gather(got, send, group=group)
+            s = self._staged(send)
+            got = [torch.empty_like(s) for _ in range(self.world)]
+            dist.all_gather(got, s, group=group)
+            got = [g.to(send.device) for g in got]
         half = H * self.nx * sz
         below = got[(self.rank - 1) % self.world][half:]   # previous rank's top owned rows
         above = got[(self.rank + 1) % self.world][:half]   # next rank's bottom owned rows
         self._rows(q_local, 0, H, sz).copy_(below)
         self._rows(q_local, H + R, H, sz).copy_(above)
         return q_local
+
+    def allreduce(self, value: float, op: str = "sum", group=None) -> float:
+        """A scalar reduced over the ranks (sum / max / min)."""
+        if self.world == 1 or not (dist.is_available() and dist.is_initialized()):
+            return float(value)
+        dev = "cpu" if dist.get_backend() == "gloo" else torch.device("cuda", torch.cuda.current_device())
+        t = torch.tensor([float(value)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op={"sum": dist.ReduceOp.SUM, "max": dist.ReduceOp.MAX,
+                               "min": dist.ReduceOp.MIN}[op], group=group)
+        return float(t.item())
+
+    def reduce_status(self, kind: int, elem: int, group=None):
+        """(kind, element) of the device status word made global: the
+        smallest (kind, global element id) over the ranks; (0, 0) if none.
+        Halo elements are reported by their global id, like their owner."""
+        key = float(kind) * 2.0 ** 40 + float(self.global_elements[elem]) if kind > 0 else float("inf")
+        key = self.allreduce(key, "min", group)
+        if key == float("inf"):
+            return 0, 0
+        k = int(key // 2.0 ** 40)
+        return k, int(key - k * 2.0 ** 40)
 
     def scatter_global(self, q_global, elem_size: int):
         """Local strip vector (owned + halo) cut from a global vector."""
@@ -112,3 +153,23 @@ class PartitionedResidual:
         self.part.exchange(self.q_local, self.sz)
         R = self.disc.eval(self.q_local, _lib.EPI_R, out)
         return R[self.owned_dofs]
+
+
+class HaloDiscretization(Discretization):
+    """A Discretization of a rank's strip whose neighbour-reading kernels
+    refresh the halo rows first (see the module docstring).  Construct one
+    per rank, ``vec.set_partition(part)`` around the solve, scatter the
+    initial state with ``part.scatter_global`` and read the owned rows of
+    the result with ``vec.owned``."""
+
+    def __init__(self, part: SlabPartition, degree: int, eqn, device=None):
+        super().__init__(part.mesh, degree, eqn, device=device)
+        self.part = part
+
+    def sync_halo(self, *vectors):
+        for v in vectors:
+            if v is not None:
+                self.part.exchange(v, self.elem_size)
+
+    def coarsen(self, p: int) -> "HaloDiscretization":
+        return HaloDiscretization(self.part, p, self.eqn, device=self.device)

@@ -34,7 +34,7 @@ from ._lib import check, load
 from .equation import NonPhysicalStateError
 from .operators import transfer_operators
 from .spatial import Discretization, raise_status
-from .vec import lincomb, nrm2, ptr, stream, to_device
+from .vec import active_partition, lincomb, nrm2, ptr, stream, to_device
 
 
 @dataclass(frozen=True)
@@ -197,7 +197,7 @@ class PmgContext:
             raise NotImplementedError("device pMG needs the discretization at the hierarchy top degree")
         self.levels = []
         for k, p in enumerate(h.levels):
-            d = disc if k == 0 else Discretization(disc.mesh, p, disc.eqn, device=disc.device)
+            d = disc if k == 0 else disc.coarsen(p)
             self.levels.append(LevelState(d, nsweeps=h.smooth[k], smoother=h.smoothers[k]))
         self.tables = [_Transfer(self.levels[k].disc, self.levels[k + 1].disc)
                        for k in range(len(self.levels) - 1)]
@@ -245,6 +245,9 @@ class PmgContext:
         shift (no smoother_shift: that only damps the EJ blocks), and its
         block ILU0 -- built on first MBNK use after prepare()."""
         if lev.sparse is None:
+            if active_partition() is not None:
+                # block ILU0 is a global sequential sweep (newton_krylov.py:319-368)
+                raise NotImplementedError("the MBNK smoother is not element-partitioned; use ej / rk")
             lev.sparse = nk.assemble_sparse_blocks(lev.disc, lev.frozen_q, lev.shift)
             lev.ilu = nk.ilu0_factor(lev.sparse)
 

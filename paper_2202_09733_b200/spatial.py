@@ -31,7 +31,7 @@ from ._lib import check, load
 from .equation import KIND_CODE, EquationSpec, NonPhysicalStateError
 from .mesh import TAG_CODE, Mesh, face_links, pack_geometry, solution_point_coords, element_geometry
 from .operators import basis, face_operators, gauss_rule
-from .vec import ptr, require_cuda, stream, to_device
+from .vec import active_partition, ptr, require_cuda, stream, to_device
 
 __all__ = ["Discretization", "SolutionField", "FrozenState", "NonPhysicalStateError",
            "EquationSpec", "raise_status"]
@@ -45,6 +45,12 @@ def raise_status(clear: bool = True):
     kind = ctypes.c_int32(0)
     elem = ctypes.c_int64(0)
     check(load().pmgb_status(stream(), ctypes.byref(kind), ctypes.byref(elem), int(clear)), "status")
+    part = active_partition()
+    if part is not None:
+        # every rank raises the same exception: the smallest (kind, global
+        # element) over the ranks (halo rows map to their owner's ids)
+        k, e = part.reduce_status(kind.value, elem.value)
+        kind.value, elem.value = k, e
     if kind.value == 1:
         raise NonPhysicalStateError(elem.value, "state")
     if kind.value == 2:
@@ -222,10 +228,20 @@ class Discretization:
 
     # -- device entry points ---------------------------------------------------
 
+    def sync_halo(self, *vectors):
+        """Refresh halo rows before a neighbour-reading kernel; a no-op on a
+        whole mesh (partition.HaloDiscretization exchanges them)."""
+
+    def coarsen(self, p: int) -> "Discretization":
+        """The same mesh at degree p (pMG coarse levels, pmg.py:57-69)."""
+        return Discretization(self.mesh, p, self.eqn, device=self.device)
+
     def eval(self, q: torch.Tensor, mode: int, out: torch.Tensor | None = None, *, X=None, eps=0.0,
              s=0.0, adt=0.0, dtau=0.0, R0=None, E=None, Sb=0.0, Se=0.0, Q0=None, dtau_e=None, alpha=0.0,
              check_status=False):
         """Fused residual + epilogue (see include/pmgflow_b200.h, PMGB_EPI_*)."""
+        jv = X is not None and mode in (_lib.EPI_JV, _lib.EPI_STAGE_JV)
+        self.sync_halo(q, X) if jv else self.sync_halo(q)
         if out is None:
             out = torch.empty(self.n_dofs, dtype=torch.float64, device=self.device)
         ep = _lib.Epilogue()
@@ -245,7 +261,7 @@ class Discretization:
         ep.Q0 = ptr(Q0) if Q0 is not None else None
         ep.dtau_e = ptr(dtau_e) if dtau_e is not None else None
         ep.alpha = float(alpha)
-        xp = ptr(X) if (X is not None and mode in (_lib.EPI_JV, _lib.EPI_STAGE_JV)) else None
+        xp = ptr(X) if jv else None
         check(load().pmgb_eval(self._h, ptr(q), xp, float(eps), ctypes.byref(ep), ptr(out), stream()), "eval")
         if check_status:
             raise_status()
@@ -322,6 +338,7 @@ class Discretization:
 
     def freeze(self, data) -> FrozenState:
         q = to_device(data, self.device)
+        self.sync_halo(q)
         qtr = torch.empty(self._face_shape, dtype=torch.float64, device=self.device)
         fvn = torch.empty(self._face_shape, dtype=torch.float64, device=self.device)
         check(load().pmgb_freeze(self._h, ptr(q), qtr.data_ptr(), fvn.data_ptr(), stream()), "freeze")

@@ -15,6 +15,32 @@ from ._lib import check, load
 
 _scratch = {}
 
+# Element-partitioned solves (paper_2202_09733_b200.partition): while a
+# partition is active, every reduction on the solver path (nrm2, dot,
+# any_nonzero, the GMRES Arnoldi step, the status word) runs over the
+# rank's OWNED elements and is summed / max-ed over the ranks; the halo
+# entries of a strip vector are never reduced.
+_PART = None
+
+
+def set_partition(part):
+    """Activate (or, with None, clear) the partition reductions use."""
+    global _PART
+    _PART = part
+
+
+def active_partition():
+    return _PART
+
+
+def owned(x: torch.Tensor) -> torch.Tensor:
+    """The owned-element range of an element-major strip vector (any level:
+    the per-element size is x.numel() / n_local)."""
+    if _PART is None:
+        return x
+    sz = x.numel() // _PART.n_local
+    return x[_PART.owned.start * sz:_PART.owned.stop * sz]
+
 
 def stream() -> int:
     return torch.cuda.current_stream().cuda_stream
@@ -74,7 +100,10 @@ def nrm2_dev(x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
 
 
 def nrm2(x: torch.Tensor) -> float:
-    """||x||_2 = sqrt(x . x) with a fixed-order reduction (synchronising)."""
+    """||x||_2 = sqrt(x . x) with a fixed-order reduction (synchronising);
+    partitioned: sqrt of the rank-summed owned x . x."""
+    if _PART is not None:
+        return float(np.sqrt(dot(x, x)))
     s = _scalars(x.device)
     nrm2_dev(x, s[0:1])
     return float(s[0].item())
@@ -82,13 +111,20 @@ def nrm2(x: torch.Tensor) -> float:
 
 def dot(x: torch.Tensor, y: torch.Tensor) -> float:
     s = _scalars(x.device)
+    if _PART is not None:
+        xo, yo = owned(x), owned(y)
+        check(load().pmgb_dot(xo.numel(), ptr(xo), ptr(yo), s.data_ptr(), stream()), "dot")
+        return _PART.allreduce(float(s[0].item()), "sum")
     check(load().pmgb_dot(x.numel(), ptr(x), ptr(y), s.data_ptr(), stream()), "dot")
     return float(s[0].item())
 
 
 def any_nonzero(x: torch.Tensor) -> bool:
     f = torch.zeros(1, dtype=torch.int32, device=x.device)
-    check(load().pmgb_any_nonzero(x.numel(), ptr(x), f.data_ptr(), stream()), "any_nonzero")
+    xo = owned(x)
+    check(load().pmgb_any_nonzero(xo.numel(), ptr(xo), f.data_ptr(), stream()), "any_nonzero")
+    if _PART is not None:
+        return _PART.allreduce(float(f.item()), "max") > 0.0
     return bool(f.item())
 
 

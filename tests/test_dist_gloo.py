@@ -97,3 +97,41 @@ def test_slab_owned_residual_is_exact_oracle(world):
         Rl = lo.residual(Q[part.global_elements].reshape(-1)).reshape(-1, g.offsets[1])
         own = part.global_elements[part.owned]
         assert np.max(np.abs(Rl[part.owned] - Rg[own])) <= 1e-13 * np.max(np.abs(Rg))
+
+
+def _reduce_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), WORLD_SIZE=str(world),
+                      RANK=str(rank), LOCAL_RANK=str(rank))
+    from paper_2202_09733_b200 import dist
+    from paper_2202_09733_b200.partition import SlabPartition
+    dist.init("gloo")
+    part = SlabPartition(4, 2 * world, 1.0, 1.0, world, rank)
+    s = part.allreduce(rank + 1.0, "sum")
+    mx = part.allreduce(rank + 1.0, "max")
+    # rank 1 sees a non-physical state in its first owned element, rank 0 in
+    # a halo element (a global id owned by the last rank): every rank must
+    # agree on the smallest global id
+    loc = part.owned.start if rank == 1 else 0
+    st = part.reduce_status(1, loc)
+    none = part.reduce_status(0, 0)
+    out[rank] = (s, mx, st, none, int(part.global_elements[loc]))
+    dist.barrier()
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("world", [2, 3])
+def test_partition_reductions_gloo(world):
+    # the partitioned solver's scalar collectives: owned-range sums, the
+    # non-finite / any-nonzero max, and the status word (smallest
+    # (kind, global element) over the ranks)
+    port = _free_port()
+    with mp.Manager() as m:
+        out = m.dict()
+        mp.spawn(_reduce_worker, args=(world, port, out), nprocs=world, join=True)
+        res = dict(out)
+    total = world * (world + 1) / 2
+    gids = [res[r][4] for r in range(world) if r in (0, 1)]
+    for r in range(world):
+        s, mx, st, none, _ = res[r]
+        assert s == total and mx == world
+        assert st == (1, min(gids)) and none == (0, 0)
