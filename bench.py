@@ -482,10 +482,53 @@ def time_partitioned(torch, case2, K, W, ws, rank):
     t_x = event_time(torch, xchg, K)
     t_r, t_x = pdist.max_over_ranks([t_r, t_x], "cuda")
     owned = part.rows * n1 * sz
-    return {"global_mesh": f"{n1} x {n1 * ws} periodic, {ws} slab(s) of {n1} x {n1}", "halo_rows": part.halo,
-            "collective": "all_gather of the slabs' boundary rows (NCCL)" if ws > 1 else "local wrap copy",
-            "r_gdofs": owned * K * ws / t_r / 1e9, "ms_per_step": t_r / K * 1e3,
-            "exchange_ms": t_x / K * 1e3, "local_dofs_per_rank": pr.disc.n_dofs, "owned_dofs_per_rank": owned}
+    rec = {"global_mesh": f"{n1} x {n1 * ws} periodic, {ws} slab(s) of {n1} x {n1}", "halo_rows": part.halo,
+           "collective": "all_gather of the slabs' boundary rows (NCCL)" if ws > 1 else "local wrap copy",
+           "r_gdofs": owned * K * ws / t_r / 1e9, "ms_per_step": t_r / K * 1e3,
+           "exchange_ms": t_x / K * 1e3, "local_dofs_per_rank": pr.disc.n_dofs, "owned_dofs_per_rank": owned}
+    del pr, out
+    try:
+        rec["solver_step"] = time_partitioned_step(torch, ws, rank)
+    except Exception as exc:  # pragma: no cover
+        rec["solver_step"] = {"error": str(exc)[:200]}
+    return rec
+
+
+def time_partitioned_step(torch, ws, rank):
+    """The partitioned JFNK-pMG solver (partition.HaloDiscretization):
+    config-1 physics, one ESDIRK3 step with pMG p{3-2} EJ, every rank a
+    16 x 16 slab of a 16 x 16N periodic box (the config-1 field on every
+    slab), halo refresh before every neighbour-reading kernel and
+    owned-range reductions all-reduced over the ranks."""
+    from paper_2202_09733_b200 import cases, dist as pdist, vec
+    from paper_2202_09733_b200 import time_integration as ti
+    from paper_2202_09733_b200.harness import ImplicitDriver
+    from paper_2202_09733_b200.partition import HaloDiscretization, SlabPartition
+    c = cases.config(1)
+    part = SlabPartition(16, 16 * ws, 10.0, 10.0 * ws, ws, rank)
+    d = HaloDiscretization(part, c.p, c.eqn)
+    q0 = torch.zeros(d.n_dofs, dtype=torch.float64, device="cuda")
+    vec.set_partition(part)
+    try:
+        vec.owned(q0).copy_(torch.as_tensor(c.q0, device="cuda"))
+        cfg = {"case.precond": "pmg", "pmg.levels": c.levels, "pmg.smooth": "2", "pmg.smoother_shift": 50.0,
+               "gmres.kdim": c.kdim, "gmres.rtol": 1e-3, "ptc.dtau_init": c.dt, "ptc.rtol": 1e-4}
+        sch = ti.get_scheme(c.scheme)
+        ImplicitDriver(d, cfg).step(q0, c.dt, sch)
+        drv = ImplicitDriver(d, cfg)
+        torch.cuda.synchronize()
+        pdist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        _, info = drv.step(q0, c.dt, sch)
+        e1.record()
+        torch.cuda.synchronize()
+        t, = pdist.max_over_ranks([e0.elapsed_time(e1) * 1e-3], "cuda")
+    finally:
+        vec.set_partition(None)
+    return {"scheme": c.scheme, "pmg": c.levels, "global_mesh": f"16 x {16 * ws}", "s": t,
+            "ptc_iters": [i["iters"] for i in info], "gmres_iters": [i["gmres_iters"] for i in info],
+            "collectives": "halo all_gather per R + all_reduce per dot (NCCL)" if ws > 1 else "local"}
 
 
 def time_mbnk(torch, case2):
