@@ -244,6 +244,16 @@ PMGB_API int pmgb_nrm2(int64_t n, const double* x, double* result_dev, void* str
  * H[j+1] > thresh, *finite_dev = 1 if w entered with a non-finite. */
 PMGB_API int pmgb_mgs(int64_t n, double* V, int64_t ld, int32_t j, double* w, double* H_dev, double thresh,
                       int32_t* finite_dev, void* stream);
+/* The partitioned Arnoldi step as separate passes over a
+ * rank's owned range, so each partial dot can be all-reduced in-stream
+ * between them: pmgb_mgs_pass does w -= (*hprev) Vprev (Vprev may be NULL)
+ * then *out = Vnext . w (first != 0: reset the finite flag and check w as
+ * it enters; finite_dev may be NULL); pmgb_normalize_sqrt sets
+ * *h = sqrt(*h) (the all-reduced w . w) and V_{j+1} = w / *h if > thresh. */
+PMGB_API int pmgb_mgs_pass(int64_t n, double* w, const double* Vprev, const double* hprev, const double* Vnext,
+                           double* out, int32_t first, int32_t* finite_dev, void* stream);
+PMGB_API int pmgb_normalize_sqrt(int64_t n, const double* w, double* h_dev, double thresh, double* v,
+                                 void* stream);
 /* out = sum_i c[i] x[i], k <= 8, c and the pointer array on the HOST. */
 PMGB_API int pmgb_lincomb(int64_t n, int32_t k, const double* c, const double* const* xs, double* out,
                           void* stream);

@@ -93,6 +93,10 @@ SIGNATURES = {
                                      c_double_p, c_void_p, c_void_p, c_void_p, ctypes.c_int32, c_void_p]),
     "pmgb_dot": (ctypes.c_int, [ctypes.c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
     "pmgb_nrm2": (ctypes.c_int, [ctypes.c_int64, c_void_p, c_void_p, c_void_p]),
+    "pmgb_mgs_pass": (ctypes.c_int, [ctypes.c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                     ctypes.c_int32, c_void_p, c_void_p]),
+    "pmgb_normalize_sqrt": (ctypes.c_int, [ctypes.c_int64, c_void_p, c_void_p, ctypes.c_double, c_void_p,
+                                           c_void_p]),
     "pmgb_mgs": (ctypes.c_int, [ctypes.c_int64, c_void_p, ctypes.c_int64, ctypes.c_int32, c_void_p,
                                 c_void_p, ctypes.c_double, c_void_p, c_void_p]),
     "pmgb_lincomb": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int32, c_double_p,

@@ -29,6 +29,9 @@ int launch_transfer(int64_t M, int nv, int nin, int nout, const double* T, const
 int launch_dot(int64_t n, const double* x, const double* y, double* out, int do_sqrt, cudaStream_t st);
 int launch_mgs(int64_t n, double* V, int64_t ld, int j, double* w, double* H, double thresh, int* finite_flag,
                cudaStream_t st);
+int launch_mgs_pass(int64_t n, double* w, const double* Vprev, const double* hprev, const double* Vnext,
+                    double* out, int first, int* finite_flag, cudaStream_t st);
+int launch_normalize_sqrt(int64_t n, const double* w, double* h, double thresh, double* v, cudaStream_t st);
 int launch_lincomb(int64_t n, int k, const double* c, const double* const* xs, double* out, cudaStream_t st);
 int launch_rk_dtau(int64_t M, const double* lam, double s, double cfl, double* dtau, cudaStream_t st);
 int launch_gemv_t(int64_t n, int k, const double* V, int64_t ld, const double* y, double* out, cudaStream_t st);
@@ -381,6 +384,20 @@ PMGB_API int pmgb_mgs(int64_t n, double* V, int64_t ld, int32_t j, double* w, do
                       int32_t* finite_dev, void* stream) {
   g_launches += j + 3;
   return launch_mgs(n, V, ld, j, w, H, thresh, finite_dev, S(stream));
+}
+
+PMGB_API int pmgb_mgs_pass(int64_t n, double* w, const double* Vprev, const double* hprev, const double* Vnext,
+                           double* out, int32_t first, int32_t* finite_dev, void* stream) {
+  if (n < 0 || !w || !Vnext || !out || (Vprev && !hprev)) return -1;
+  g_launches += 1;
+  return launch_mgs_pass(n, w, Vprev, hprev, Vnext, out, first, finite_dev, S(stream));
+}
+
+PMGB_API int pmgb_normalize_sqrt(int64_t n, const double* w, double* h_dev, double thresh, double* v,
+                                 void* stream) {
+  if (n < 0 || !w || !h_dev || !v) return -1;
+  g_launches += 2;
+  return launch_normalize_sqrt(n, w, h_dev, thresh, v, S(stream));
 }
 
 PMGB_API int pmgb_lincomb(int64_t n, int32_t k, const double* c, const double* const* xs, double* out,

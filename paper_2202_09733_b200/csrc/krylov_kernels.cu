@@ -236,6 +236,30 @@ int launch_mgs(int64_t n, double* V, int64_t ld, int j, double* w, double* H, do
   return (int)cudaGetLastError();
 }
 
+// One MGS pass on its own (the partitioned Arnoldi step all-reduces each
+// partial dot between passes): w -= (*hprev) Vprev (Vprev may be NULL),
+// then *out = Vnext . w over these n entries; first = 1 clears the finite
+// flag and checks w as it enters.
+int launch_mgs_pass(int64_t n, double* w, const double* Vprev, const double* hprev, const double* Vnext,
+                    double* out, int first, int* finite_flag, cudaStream_t st) {
+  RedScratch rs;
+  int e = red_scratch(&rs);
+  if (e) return e;
+  if (first) cudaMemsetAsync(rs.flag, 0, sizeof(int), st);
+  k_mgs_pass<<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, w, Vprev, hprev, Vnext, out, 0, first, rs);
+  if (finite_flag) cudaMemcpyAsync(finite_flag, rs.flag, sizeof(int), cudaMemcpyDeviceToDevice, st);
+  return (int)cudaGetLastError();
+}
+
+__global__ void k_sqrt1(double* h) { *h = sqrt(*h); }
+
+// *h = sqrt(*h) (the all-reduced w . w), then V_{j+1} = w / *h if > thresh
+int launch_normalize_sqrt(int64_t n, const double* w, double* h, double thresh, double* v, cudaStream_t st) {
+  k_sqrt1<<<1, 1, 0, st>>>(h);
+  k_normalize<<<ew_grid(n), 256, 0, st>>>(n, w, h, thresh, v);
+  return (int)cudaGetLastError();
+}
+
 int launch_lincomb(int64_t n, int k, const double* c, const double* const* xs, double* out, cudaStream_t st) {
   if (k < 1 || k > 8) return -1001;
   Lin L;

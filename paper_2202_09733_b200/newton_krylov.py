@@ -106,22 +106,40 @@ def _back_substitute(H, g):
     return y
 
 
-def _mgs_partitioned(V, j, w, thresh):
-    """Element-partitioned modified Gram-Schmidt: each
-    projection h_ij = V_i . w is an owned-range dot summed over the ranks
-    before w -= h_ij V_i, i.e. j+1 sequential all-reduces per Arnoldi step,
-    the reference's MGS order (newton_krylov.py:119-127)."""
-    ww = dot(w, w)
-    if not np.isfinite(ww):
-        return None, True
-    h = np.zeros(j + 2)
-    for i in range(j + 1):
-        h[i] = dot(V[i], w)
-        lincomb((1.0, -h[i]), (w, V[i]), out=w)
-    h[j + 1] = np.sqrt(dot(w, w))
-    if h[j + 1] > thresh:
-        lincomb((1.0 / h[j + 1],), (w,), out=V[j + 1])
-    return h, False
+def _mgs_partitioned(V, j, w, thresh, Hd, flag):
+    """Element-partitioned modified Gram-Schmidt over the
+    rank's OWNED range of the strip vectors (halo entries are refreshed
+    before anything reads them).  One rank: the fused pmgb_mgs on that
+    range.  Several: pmgb_mgs_pass per projection with each partial dot
+    all-reduced in-stream before the next pass applies it -- j+1 sequential
+    all-reduces per Arnoldi step, the reference's MGS order
+    (newton_krylov.py:119-127) -- then ||w|| from the all-reduced w . w.
+    One host synchronisation per step (the Hessenberg column)."""
+    lib = load()
+    part = active_partition()
+    n = V.shape[1]
+    sz = n // part.n_local
+    a0, n_o = part.owned.start * sz, (part.owned.stop - part.owned.start) * sz
+    w_o = w[a0:a0 + n_o]
+    row = lambda i: V.data_ptr() + (i * n + a0) * 8
+    H = Hd[j]
+    if part.world == 1:
+        check(lib.pmgb_mgs(n_o, row(0), n, j, ptr(w_o), H.data_ptr(), thresh, flag.data_ptr(), stream()), "mgs")
+    else:
+        for i in range(j + 1):
+            check(lib.pmgb_mgs_pass(n_o, ptr(w_o), row(i - 1) if i else None, H[i - 1:].data_ptr() if i else None,
+                                    row(i), H[i:].data_ptr(), int(i == 0), flag.data_ptr() if i == 0 else None,
+                                    stream()), "mgs_pass")
+            part.allreduce_(H[i:i + 1], "sum")
+            if i == 0:
+                part.allreduce_(flag, "max")
+        check(lib.pmgb_mgs_pass(n_o, ptr(w_o), row(j), H[j:].data_ptr(), ptr(w_o), H[j + 1:].data_ptr(), 0, None,
+                                stream()), "mgs_pass")
+        part.allreduce_(H[j + 1:j + 2], "sum")
+        check(lib.pmgb_normalize_sqrt(n_o, ptr(w_o), H[j + 1:].data_ptr(), thresh, row(j + 1), stream()),
+              "normalize_sqrt")
+    hcol = H[:j + 2].cpu().numpy()
+    return hcol, bool(int(flag.item()))
 
 
 def gmres_solve(matvec, b, cfg: KrylovConfig, x0=None, precond=None):
@@ -172,8 +190,8 @@ def gmres_solve(matvec, b, cfg: KrylovConfig, x0=None, precond=None):
                 raise_status()
                 nonfinite = bool(int(flag.item()))
             else:
+                hcol, nonfinite = _mgs_partitioned(V, j, w, thresh, Hd, flag)
                 raise_status()
-                hcol, nonfinite = _mgs_partitioned(V, j, w, thresh)
             if nonfinite:
                 raise RuntimeError(f"non-finite Arnoldi vector at inner iteration {total + 1}")
             H[:j + 2, j] = hcol

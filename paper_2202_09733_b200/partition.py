@@ -85,8 +85,12 @@ class SlabPartition:
         """Fill the halo rows of ``q_local`` (local strip layout) in place
         from the neighbouring ranks' owned rows."""
         H, R, sz = self.halo, self.rows, elem_size
+        if self.world == 1:   # periodic wrap of the one slab: two device copies
+            self._rows(q_local, 0, H, sz).copy_(self._rows(q_local, R, H, sz))
+            self._rows(q_local, H + R, H, sz).copy_(self._rows(q_local, H, H, sz))
+            return q_local
         send = torch.cat([self._rows(q_local, H, H, sz), self._rows(q_local, R, H, sz)])
-        if self.world == 1 or not (dist.is_available() and dist.is_initialized()):
+        if not (dist.is_available() and dist.is_initialized()):
             got = [send]
         else:
             s = self._staged(send)
@@ -109,6 +113,20 @@ class SlabPartition:
         dist.all_reduce(t, op={"sum": dist.ReduceOp.SUM, "max": dist.ReduceOp.MAX,
                                "min": dist.ReduceOp.MIN}[op], group=group)
         return float(t.item())
+
+    def allreduce_(self, t: torch.Tensor, op: str = "sum", group=None) -> torch.Tensor:
+        """In-place all-reduce of a (device) tensor, enqueued on the stream
+        with NCCL (no host synchronisation); gloo stages through the host."""
+        if self.world == 1 or not (dist.is_available() and dist.is_initialized()):
+            return t
+        o = {"sum": dist.ReduceOp.SUM, "max": dist.ReduceOp.MAX, "min": dist.ReduceOp.MIN}[op]
+        if t.is_cuda and dist.get_backend() == "gloo":
+            h = t.cpu()
+            dist.all_reduce(h, op=o, group=group)
+            t.copy_(h)
+        else:
+            dist.all_reduce(t, op=o, group=group)
+        return t
 
     def reduce_status(self, kind: int, elem: int, group=None):
         """(kind, element) of the device status word made global: the
