@@ -68,7 +68,7 @@ def _halo_worker(rank, world, port, out):
 
 
 @pytest.mark.timeout(300)
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [1, 2, 3])
 def test_slab_halo_exchange_gloo(world):
     # the multi-GPU partitioned residual's only data-path collective: every
     # rank's halo rows must come back equal to the global field there
