@@ -17,6 +17,7 @@
 // two neighbour exchanges (traces, then one-sided viscous fluxes).
 #include <climits>
 #include <cstdio>
+#include <cstdlib>
 
 #include "pmgb_internal.cuh"
 
@@ -106,6 +107,8 @@ struct SL {
 template <int P> struct MinBlocks {
   static constexpr int cap(int v) { return v < 1 ? 1 : (v > 32 ? 32 : v); }
   static constexpr int ASM = cap(65536 / (BC<P>::THREADS * PMGB_REG_TARGET));
+  static constexpr int ASM_R = cap(65536 / (BC<P>::THREADS * PMGB_REG_TARGET_R));
+  static constexpr int ASM_K = cap(65536 / (BC<P>::THREADS * PMGB_REG_TARGET_K));
   static constexpr int FVN = cap(65536 / (BC<P>::THREADS * (P == 5 ? PMGB_FVN_REGS_P5 : PMGB_FVN_REGS)));
   static constexpr int TRACE = cap(65536 / (BC<P>::THREADS * PMGB_TRACE_REGS));
 };
@@ -1267,6 +1270,41 @@ __device__ __forceinline__ void epi_load(const Epi& ep, int64_t i, double& o1, d
   }
 }
 
+// Compile-time epilogue mode EK for k_assemble_async: EK < 0 keeps the
+// runtime switch over ep.mode; otherwise the switch is on the constant EK
+// and folds away (no dead operand registers).
+template <int EK>
+__device__ __forceinline__ void epi_load_k(const Epi& ep, int64_t i, double& o1, double& o2, double& o3) {
+  if constexpr (EK < 0) {
+    epi_load<false>(ep, i, o1, o2, o3);
+  } else if constexpr (EK == EPI_RK) {
+    epi_load<true>(ep, i, o1, o2, o3);
+  } else {
+    o1 = o2 = o3 = 0.0;
+    if constexpr (EK == EPI_JV || EK == EPI_STAGE_JV) {
+      o1 = __ldg(ep.X + i);
+      o2 = __ldg(ep.R0 + i);
+    }
+    if constexpr (EK == EPI_STAGE_F || EK == EPI_STAGE_JV) o3 = __ldg(ep.E + i);
+    if constexpr (EK == EPI_DEFECT) {
+      o1 = ep.Sb ? __ldg(ep.Sb + i) : ep.sb_scalar;
+      o2 = ep.Se ? __ldg(ep.Se + i) : ep.se_scalar;
+    }
+    if constexpr (EK == EPI_OUTER_F) o2 = ep.Se ? __ldg(ep.Se + i) : ep.se_scalar;
+  }
+}
+
+template <int EK>
+__device__ __forceinline__ double epi_pre_k(const Epi& ep, double R, double qv, double o1, double o2, double o3) {
+  if constexpr (EK < 0) {
+    return epi_pre(ep, R, qv, o1, o2, o3);
+  } else {
+    Epi e = ep;
+    e.mode = EK;   // a constant: epi_pre's switch folds
+    return epi_pre(e, R, qv, o1, o2, o3);
+  }
+}
+
 __device__ __forceinline__ void commit_status(int* bad, Status* st) {
   if (bad == nullptr) return;
   const int bs = bad[0], bt = bad[1];
@@ -1479,8 +1517,13 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // from registers; the first barrier only guards the point stage.
 // RKE: the RK-smoother stage epilogue is a separate instantiation (carrying
 // its operand path in the R / Jv kernels measured 2.5 % on R at config 2)
-template <int P, int KIND, bool RKE = false>
-__global__ void __launch_bounds__(BC<P>::THREADS, MinBlocks<P>::ASM)
+// EK: the epilogue mode as a template constant for the hot modes (R, Jv,
+// PTC Jv, defect, F; see run_residual), -1 = runtime switch for the rest.
+// The plain-R instantiation carries no epilogue operands and gets its own
+// register target (72 at p=4: 176.8 -> 162.4 us per R at config 2).
+template <int P, int KIND, bool RKE = false, int EK = -1>
+__global__ void __launch_bounds__(BC<P>::THREADS, EK == EPI_R ? MinBlocks<P>::ASM_R
+                                                 : (EK >= 0 && EK != EPI_RK ? MinBlocks<P>::ASM_K : MinBlocks<P>::ASM))
 k_assemble_async(const FrConst C, const FrMesh m, const double* __restrict__ q, const double* __restrict__ qtr,
                  const double* __restrict__ fvn, const double* __restrict__ grad, const Epi ep,
                  double* __restrict__ out, int* bad, Status* st, int q_dep) {
@@ -1659,8 +1702,10 @@ k_assemble_async(const FrConst C, const FrMesh m, const double* __restrict__ q, 
       const double j11 = mt.J11(xb), j01 = mt.J01(xb);
       const int64_t e = e0 + el;
       double o1[N], o2[N], o3[N];
+      if constexpr (EK != EPI_R) {
 #pragma unroll
-      for (int a = 0; a < N; ++a) epi_load<RKE>(ep, (e * NP + a * N + b) * NV + v, o1[a], o2[a], o3[a]);
+        for (int a = 0; a < N; ++a) epi_load_k<RKE ? EPI_RK : EK>(ep, (e * NP + a * N + b) * NV + v, o1[a], o2[a], o3[a]);
+      }
       const double ce = RKE ? epi_rk_coef(ep, e) : 0.0;
 #pragma unroll
       for (int a = 0; a < N; ++a) {
@@ -1680,7 +1725,10 @@ k_assemble_async(const FrConst C, const FrMesh m, const double* __restrict__ q, 
         const int pt = a * N + b;
         const int64_t gi = (e * NP + pt) * NV + v;
         const double qv = sQA[(el * NP + pt) * NV + v];
-        out[gi] = RKE ? epi_rk(ep, ce, R, qv, o1[a], o2[a], o3[a]) : epi_pre(ep, R, qv, o1[a], o2[a], o3[a]);
+        if constexpr (EK == EPI_R)
+          out[gi] = R;
+        else
+          out[gi] = RKE ? epi_rk(ep, ce, R, qv, o1[a], o2[a], o3[a]) : epi_pre_k<EK>(ep, R, qv, o1[a], o2[a], o3[a]);
       }
     }
   }
@@ -2249,6 +2297,32 @@ static void launch_pdl(void (*kernel)(KArgs...), unsigned grid, int threads, siz
   cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 
+// PMGB_EPI_SPECIALIZE=0 forces the runtime-switch instantiation (A/B)
+static bool epi_specialize() {
+  static const bool on = [] {
+    const char* v = std::getenv("PMGB_EPI_SPECIALIZE");
+    return v == nullptr || v[0] != '0';
+  }();
+  return on;
+}
+
+using AsmAsyncFn = void (*)(const FrConst, const FrMesh, const double*, const double*, const double*, const double*,
+                            const Epi, double*, int*, Status*, int);
+
+template <int P, int KIND>
+static AsmAsyncFn asm_async_for(int mode) {
+  if (mode == EPI_RK) return k_assemble_async<P, KIND, true>;
+  if (!epi_specialize()) return k_assemble_async<P, KIND, false>;
+  switch (mode) {
+    case EPI_R: return k_assemble_async<P, KIND, false, EPI_R>;
+    case EPI_JV: return k_assemble_async<P, KIND, false, EPI_JV>;
+    case EPI_STAGE_JV: return k_assemble_async<P, KIND, false, EPI_STAGE_JV>;
+    case EPI_DEFECT: return k_assemble_async<P, KIND, false, EPI_DEFECT>;
+    case EPI_F: return k_assemble_async<P, KIND, false, EPI_F>;
+  }
+  return k_assemble_async<P, KIND, false>;
+}
+
 template <int P, int KIND>
 static int run_residual(const DiscDev& d, const double* q, const double* X, double eps, const Epi& epi,
                         double* out, cudaStream_t st) {
@@ -2262,6 +2336,9 @@ static int run_residual(const DiscDev& d, const double* q, const double* X, doub
     cudaFuncSetAttribute(k_assemble<P, KIND, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES_ASM);
     if constexpr (KT<KIND>::NV == 4 && E * BC<P>::NF <= TH) {
       cudaFuncSetAttribute(k_assemble_async<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES_ASYNC);
+      for (int md : {(int)EPI_R, (int)EPI_JV, (int)EPI_STAGE_JV, (int)EPI_DEFECT, (int)EPI_F})
+        cudaFuncSetAttribute(asm_async_for<P, KIND>(md), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)L::BYTES_ASYNC);
       cudaFuncSetAttribute(k_assemble_async<P, KIND, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)L::BYTES_ASYNC);
     }
@@ -2284,9 +2361,8 @@ static int run_residual(const DiscDev& d, const double* q, const double* X, doub
                                  d.fvn, d.grad, q_dep);
   const bool rk = epi.mode == EPI_RK;
   if constexpr (KT<KIND>::NV == 4 && E * BC<P>::NF <= TH)
-    launch_pdl(rk ? k_assemble_async<P, KIND, true> : k_assemble_async<P, KIND, false>, grid, TH, L::BYTES_ASYNC,
-               st, d.C, d.mesh, qq, (const double*)d.qtr, (const double*)d.fvn, (const double*)d.grad, epi, out,
-               bad, stp, q_dep);
+    launch_pdl(asm_async_for<P, KIND>(epi.mode), grid, TH, L::BYTES_ASYNC, st, d.C, d.mesh, qq,
+               (const double*)d.qtr, (const double*)d.fvn, (const double*)d.grad, epi, out, bad, stp, q_dep);
   else if (rk)
     k_assemble<P, KIND, true><<<grid, TH, L::BYTES_ASM, st>>>(d.C, d.mesh, qq, d.qtr, d.fvn, d.grad, epi, out, bad,
                                                                stp);
