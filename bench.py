@@ -300,7 +300,7 @@ def run_ours(args):
 
     # the sharded residual with its halo exchange (all ranks take part)
     try:
-        partitioned = time_partitioned(torch, case, K, W, ws, rank)
+        partitioned = time_partitioned(torch, case, K, W, ws, rank, args.no_step)
     except Exception as exc:  # pragma: no cover
         partitioned = {"error": str(exc)[:200]}
 
@@ -457,7 +457,7 @@ def time_other_configs(torch, args):
     return out
 
 
-def time_partitioned(torch, case2, K, W, ws, rank):
+def time_partitioned(torch, case2, K, W, ws, rank, no_step=False):
     """The sharded residual: rank r owns a 256 x 256 slab of a
     256 x 256N periodic box (the config-2 field on every slab, which is
     y-periodic) plus 2 halo element rows each side; every step is one
@@ -487,6 +487,8 @@ def time_partitioned(torch, case2, K, W, ws, rank):
            "r_gdofs": owned * K * ws / t_r / 1e9, "ms_per_step": t_r / K * 1e3,
            "exchange_ms": t_x / K * 1e3, "local_dofs_per_rank": pr.disc.n_dofs, "owned_dofs_per_rank": owned}
     del pr, out
+    if no_step:
+        return rec
     try:
         rec["solver_step"] = time_partitioned_step(torch, ws, rank)
     except Exception as exc:  # pragma: no cover

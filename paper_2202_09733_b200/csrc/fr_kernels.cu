@@ -1523,7 +1523,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // register target (72 at p=4: 176.8 -> 162.4 us per R at config 2).
 template <int P, int KIND, bool RKE = false, int EK = -1>
 __global__ void __launch_bounds__(BC<P>::THREADS, EK == EPI_R ? MinBlocks<P>::ASM_R
-                                                 : (EK >= 0 && EK != EPI_RK ? MinBlocks<P>::ASM_K : MinBlocks<P>::ASM))
+                                                 : (RKE || EK >= 0 ? MinBlocks<P>::ASM_K : MinBlocks<P>::ASM))
 k_assemble_async(const FrConst C, const FrMesh m, const double* __restrict__ q, const double* __restrict__ qtr,
                  const double* __restrict__ fvn, const double* __restrict__ grad, const Epi ep,
                  double* __restrict__ out, int* bad, Status* st, int q_dep) {
