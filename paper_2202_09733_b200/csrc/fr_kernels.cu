@@ -800,8 +800,12 @@ k_trace(const FrConst C, const FrMesh m, const double* __restrict__ q, const dou
 // the two face traces at that line's ends.  Row threads also check the
 // points of their row and write the perturbed state.  No shared memory,
 // no barrier.
-template <int P, int KIND>
-__global__ void __launch_bounds__(128)
+// HASX: the Jv forms (q + eps X, written to qp) are their own instantiation:
+// the plain trace fits 64 registers (8 CTAs/SM), the Jv one runs best
+// without a register cap (R 164.0 -> 162.1 us, Jv 206.7 -> 198.9 us at
+// config 2, profiles/r1/ab_trace_regs_r1m.log)
+template <int P, int KIND, bool HASX = false>
+__global__ void __launch_bounds__(128, HASX ? 1 : 8)
 k_trace_lines(const FrConst C, const FrMesh m, const double* __restrict__ q, const double* __restrict__ X,
               double eps, double* __restrict__ qp, double* __restrict__ qtr, int* __restrict__ bad) {
   constexpr int N = P + 1, NP = N * N, NV = 4;
@@ -824,7 +828,7 @@ k_trace_lines(const FrConst C, const FrMesh m, const double* __restrict__ q, con
     v[i][2] = b.x;
     v[i][3] = b.y;
   }
-  if (X != nullptr) {
+  if (HASX) {
 #pragma unroll
     for (int i = 0; i < N; ++i) {
       const double2 a = __ldg(reinterpret_cast<const double2*>(X + base + i * stride));
@@ -2352,7 +2356,10 @@ static int run_residual(const DiscDev& d, const double* q, const double* X, doub
   if (X != nullptr) qq = d.qp;
   if constexpr (KT<KIND>::FLOW) {
     const unsigned gl = (unsigned)((d.M * 2 * (P + 1) + 127) / 128);
-    k_trace_lines<P, KIND><<<gl, 128, 0, st>>>(d.C, d.mesh, q, X, eps, d.qp, d.qtr, bad);
+    if (X != nullptr)
+      k_trace_lines<P, KIND, true><<<gl, 128, 0, st>>>(d.C, d.mesh, q, X, eps, d.qp, d.qtr, bad);
+    else
+      k_trace_lines<P, KIND, false><<<gl, 128, 0, st>>>(d.C, d.mesh, q, X, eps, d.qp, d.qtr, bad);
   } else {
     k_trace<P, KIND><<<grid, TH, L::BYTES_TRACE, st>>>(d.C, d.mesh, q, X, eps, d.qp, d.qtr, bad);
   }

@@ -1,0 +1,9 @@
+#!/bin/bash
+# A/B of the k_trace_lines register cap (none vs 8 CTAs/SM = 64 registers)
+for rep in 1 2; do
+  for lib in libpmgflow_b200.so libv_t8.so; do
+    for k in 2 4; do
+      echo -n "$lib "; PMGB_LIB=$PWD/paper_2202_09733_b200/$lib python tools/time_residual.py $k 100 2>/dev/null | tr '\n' ' '; echo
+    done
+  done
+done
