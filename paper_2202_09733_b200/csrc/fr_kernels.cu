@@ -107,8 +107,12 @@ struct SL {
 template <int P> struct MinBlocks {
   static constexpr int cap(int v) { return v < 1 ? 1 : (v > 32 ? 32 : v); }
   static constexpr int ASM = cap(65536 / (BC<P>::THREADS * PMGB_REG_TARGET));
-  static constexpr int ASM_R = cap(65536 / (BC<P>::THREADS * (P == 5 ? PMGB_REG_TARGET_R_P5 : PMGB_REG_TARGET_R)));
-  static constexpr int ASM_K = cap(65536 / (BC<P>::THREADS * (P == 5 ? PMGB_REG_TARGET_K_P5 : PMGB_REG_TARGET_K)));
+  static constexpr int ASM_R = cap(65536 / (BC<P>::THREADS * (P == 5   ? PMGB_REG_TARGET_R_P5
+                                                             : P == 3 ? PMGB_REG_TARGET_R_P3
+                                                                      : PMGB_REG_TARGET_R)));
+  static constexpr int ASM_K = cap(65536 / (BC<P>::THREADS * (P == 5   ? PMGB_REG_TARGET_K_P5
+                                                             : P == 3 ? PMGB_REG_TARGET_K_P3
+                                                                      : PMGB_REG_TARGET_K)));
   static constexpr int FVN = cap(65536 / (BC<P>::THREADS * (P == 5 ? PMGB_FVN_REGS_P5 : PMGB_FVN_REGS)));
   static constexpr int TRACE = cap(65536 / (BC<P>::THREADS * PMGB_TRACE_REGS));
 };

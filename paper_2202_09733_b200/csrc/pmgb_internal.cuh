@@ -50,6 +50,12 @@ template <> struct KT<K_ADVD>  { static constexpr int NV = 1, NW = 1; static con
 #ifndef PMGB_REG_TARGET_R   // R-only (EPI_R) instantiation of k_assemble_async
 #define PMGB_REG_TARGET_R 72
 #endif
+#ifndef PMGB_REG_TARGET_R_P3
+#define PMGB_REG_TARGET_R_P3 72
+#endif
+#ifndef PMGB_REG_TARGET_K_P3
+#define PMGB_REG_TARGET_K_P3 72
+#endif
 #ifndef PMGB_REG_TARGET_R_P5   // p = 5 (256-thread CTAs)
 #define PMGB_REG_TARGET_R_P5 64
 #endif
