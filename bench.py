@@ -433,9 +433,9 @@ def time_other_configs(torch, args):
             if k == 4:
                 cfg = {"case.precond": "pmg", "pmg.levels": c.levels, "pmg.smooth": "2",
                        "pmg.smoother_shift": c.extra["smoother_shift"], "gmres.kdim": c.kdim, "gmres.rtol": 1e-3}
-                # ros4l: BASELINE's 4-stage ROW at the case dt (0.25 dt_conv);
-                # row4: the reference's 6-stage RODASP at 0.5 dt_conv (cases.py)
-                for name, dt in ((c.scheme, c.dt), ("row4", 2.0 * c.dt)):
+                # ros4l: BASELINE's 4-stage ROW; row4: the reference's 6-stage
+                # RODASP; both at the case dt (0.125 dt_conv, cases.py)
+                for name, dt in ((c.scheme, c.dt), ("row4", c.dt)):
                     sch = ti.get_scheme(name)
                     try:
                         ImplicitDriver(d, cfg).step(q0, dt, sch)
