@@ -203,3 +203,21 @@ def test_free_stream_preserved_options(cuda, riemann, visc):
         dev = Discretization(m, 3, eqn)
         q = OracleDisc(m, 3, eqn).free_stream_field()
         assert np.max(np.abs(dev.residual(q))) <= 1e-11
+
+
+def test_epilogue_specialization_is_bitwise(cuda):
+    # k_assemble_async's compile-time epilogue instantiations (R, Jv, PTC Jv,
+    # defect, F at their own register targets) must give the runtime-switch
+    # kernel's bits in every mode
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    script = str(Path(__file__).parent / "_epi_modes_digest.py")
+    runs = []
+    for flag in ("1", "0"):
+        env = dict(os.environ, PMGB_EPI_SPECIALIZE=flag)
+        r = subprocess.run([sys.executable, script], env=env, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        runs.append(r.stdout.split())
+    assert len(runs[0]) == 8 and runs[0] == runs[1]
