@@ -21,9 +21,10 @@ c = cases.config(k, nx=nx)
 d = Discretization(c.mesh, c.p, c.eqn)
 cfg = {"case.precond": "pmg", "pmg.levels": c.levels, "pmg.smooth": "2",
        "pmg.smoother_shift": c.extra["smoother_shift"], "gmres.kdim": c.kdim, "gmres.rtol": 1e-3,
-       "ptc.dtau_init": c.dt, "ptc.rtol": 1e-4}
+       "ptc.dtau_init": c.dt, "ptc.rtol": 1e-4,
+       "pmg.block_precision": "fp32" if "--fp32" in sys.argv else "fp64"}
 q = torch.as_tensor(c.q0, device="cuda")
-sch = ti.get_scheme("esdirk2")
+sch = ti.get_scheme(c.scheme if "--case-scheme" in sys.argv else "esdirk2")
 if warm:
     ImplicitDriver(d, cfg).step(q, c.dt, sch)
 torch.cuda.synchronize()
