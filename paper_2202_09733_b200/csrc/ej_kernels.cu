@@ -969,11 +969,75 @@ k_transfer(int64_t M, int nv, int nin, int nout, int epb, const TransferOp op, c
   }
 }
 
+// Compile-time sizes for the flow kinds' level pairs (nv = 4): the same
+// contractions in the same order as k_transfer (bitwise equal), without
+// runtime divisions / loop bounds.  One CTA of 256 threads per EPB elements.
+template <int NIN, int NOUT, int NV>
+__global__ void __launch_bounds__(TR_THREADS)
+k_transfer_t(int64_t M, const TransferOp op, const double* __restrict__ src, const double* __restrict__ src_base,
+             double* __restrict__ dst, int accumulate) {
+  constexpr int IN = NIN * NIN * NV, MID = NIN * NOUT * NV, OUT = NOUT * NOUT * NV;
+  constexpr int EPB = (1024 / IN) < 1 ? 1 : ((1024 / IN) > 256 ? 256 : 1024 / IN);
+  __shared__ double s_in[EPB * IN];
+  __shared__ double s_mid[EPB * MID];
+  const int64_t e0 = (int64_t)blockIdx.x * EPB;
+  const int ne = (int)((M - e0) < EPB ? (M - e0) : EPB);
+  const double* sb = src + e0 * IN;
+  const double* bb = src_base ? src_base + e0 * IN : nullptr;
+  for (int i = threadIdx.x; i < ne * IN; i += TR_THREADS) {
+    double v = __ldg(sb + i);
+    if (bb) v = v - __ldg(bb + i);
+    s_in[i] = v;
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < ne * MID; t += TR_THREADS) {
+    const int el = t / MID, r = t - el * MID;
+    const int v = r % NV, ib = r / NV, i = ib / NOUT, b = ib % NOUT;
+    const double* s = s_in + el * IN + i * NIN * NV + v;
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < NIN; ++j) acc += op.T[b * NIN + j] * s[j * NV];
+    s_mid[t] = acc;
+  }
+  __syncthreads();
+  double* db = dst + e0 * OUT;
+  for (int t = threadIdx.x; t < ne * OUT; t += TR_THREADS) {
+    const int el = t / OUT, r = t - el * OUT;
+    const int v = r % NV, ab = r / NV, a = ab / NOUT, b = ab % NOUT;
+    const double* mm = s_mid + el * MID + b * NV + v;
+    double acc = 0.0;
+#pragma unroll
+    for (int i = 0; i < NIN; ++i) acc += op.T[a * NIN + i] * mm[i * NOUT * NV];
+    if (accumulate) db[t] = db[t] + acc;
+    else db[t] = acc;
+  }
+}
+
+template <int NIN, int NOUT>
+static int run_transfer_t(int64_t M, const TransferOp& op, const double* src, const double* src_base, double* dst,
+                          int accumulate, cudaStream_t st) {
+  constexpr int IN = NIN * NIN * 4;
+  constexpr int EPB = (1024 / IN) < 1 ? 1 : ((1024 / IN) > 256 ? 256 : 1024 / IN);
+  const unsigned grid = (unsigned)((M + EPB - 1) / EPB);
+  k_transfer_t<NIN, NOUT, 4><<<grid, TR_THREADS, 0, st>>>(M, op, src, src_base, dst, accumulate);
+  return (int)cudaGetLastError();
+}
+
 int launch_transfer(int64_t M, int nv, int nin, int nout, const double* T, const double* src,
                     const double* src_base, double* dst, int accumulate, cudaStream_t st) {
   TransferOp op;
   for (int i = 0; i < 36; ++i) op.T[i] = (i < nin * nout) ? T[i] : 0.0;
   if (M <= 0) return 0;
+  static const bool generic = std::getenv("PMGB_TRANSFER_GENERIC") != nullptr;  // A/B only
+  if (nv == 4 && !generic) {
+    switch (nin * 8 + nout) {
+#define PMGB_TR(A, B) case A * 8 + B: return run_transfer_t<A, B>(M, op, src, src_base, dst, accumulate, st);
+      PMGB_TR(6, 5) PMGB_TR(5, 6) PMGB_TR(5, 4) PMGB_TR(4, 5) PMGB_TR(5, 3) PMGB_TR(3, 5) PMGB_TR(4, 3)
+      PMGB_TR(3, 4) PMGB_TR(3, 2) PMGB_TR(2, 3) PMGB_TR(2, 1) PMGB_TR(1, 2) PMGB_TR(4, 2) PMGB_TR(2, 4)
+#undef PMGB_TR
+      default: break;
+    }
+  }
   const int in_sz = nin * nin * nv, mid_sz = nin * nout * nv;
   int epb = 1024 / (in_sz > 1 ? in_sz : 1);
   if (epb < 1) epb = 1;
