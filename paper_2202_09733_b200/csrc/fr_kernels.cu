@@ -1326,8 +1326,9 @@ __device__ __forceinline__ void commit_status(int* bad, Status* st) {
   }
 }
 
-template <int P, int KIND, bool RKE = false>
-__global__ void __launch_bounds__(BC<P>::THREADS, MinBlocks<P>::ASM)
+// EK: compile-time epilogue mode as in k_assemble_async (-1 = runtime switch)
+template <int P, int KIND, bool RKE = false, int EK = -1>
+__global__ void __launch_bounds__(BC<P>::THREADS, EK >= 0 ? MinBlocks<P>::ASM_K : MinBlocks<P>::ASM)
 k_assemble(const FrConst C, const FrMesh m, const double* __restrict__ q, const double* __restrict__ qtr,
            const double* __restrict__ fvn, const double* __restrict__ grad, const Epi ep,
            double* __restrict__ out, int* bad, Status* st) {
@@ -1503,7 +1504,15 @@ k_assemble(const FrConst C, const FrMesh m, const double* __restrict__ q, const 
       const int64_t base = (e * NP + pt) * NV;
       double o[NV];
 #pragma unroll
-      for (int v = 0; v < NV; ++v) o[v] = epi_apply<RKE>(ep, base + v, R[v], sQ[v * NPT + t0]);
+      for (int v = 0; v < NV; ++v) {
+        if constexpr (EK >= 0 && !RKE) {
+          Epi ek = ep;
+          ek.mode = EK;   // constant: epi_apply's switch folds
+          o[v] = epi_apply<false>(ek, base + v, R[v], sQ[v * NPT + t0]);
+        } else {
+          o[v] = epi_apply<RKE>(ep, base + v, R[v], sQ[v * NPT + t0]);
+        }
+      }
       st_face<NV>(out + base, o);
     }
   }
@@ -2317,6 +2326,22 @@ static bool epi_specialize() {
 using AsmAsyncFn = void (*)(const FrConst, const FrMesh, const double*, const double*, const double*, const double*,
                             const Epi, double*, int*, Status*, int);
 
+using AsmFn = void (*)(const FrConst, const FrMesh, const double*, const double*, const double*, const double*,
+                       const Epi, double*, int*, Status*);
+
+template <int P, int KIND>
+static AsmFn asm_for(int mode) {
+  if (!epi_specialize()) return k_assemble<P, KIND>;
+  switch (mode) {
+    case EPI_R: return k_assemble<P, KIND, false, EPI_R>;
+    case EPI_JV: return k_assemble<P, KIND, false, EPI_JV>;
+    case EPI_STAGE_JV: return k_assemble<P, KIND, false, EPI_STAGE_JV>;
+    case EPI_DEFECT: return k_assemble<P, KIND, false, EPI_DEFECT>;
+    case EPI_F: return k_assemble<P, KIND, false, EPI_F>;
+  }
+  return k_assemble<P, KIND>;
+}
+
 template <int P, int KIND>
 static AsmAsyncFn asm_async_for(int mode) {
   if (mode == EPI_RK) return k_assemble_async<P, KIND, true>;
@@ -2342,6 +2367,8 @@ static int run_residual(const DiscDev& d, const double* q, const double* X, doub
     cudaFuncSetAttribute(k_fvn<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES_FVN);
     cudaFuncSetAttribute(k_assemble<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES_ASM);
     cudaFuncSetAttribute(k_assemble<P, KIND, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES_ASM);
+    for (int md : {(int)EPI_R, (int)EPI_JV, (int)EPI_STAGE_JV, (int)EPI_DEFECT, (int)EPI_F})
+      cudaFuncSetAttribute(asm_for<P, KIND>(md), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES_ASM);
     if constexpr (KT<KIND>::NV == 4 && E * BC<P>::NF <= TH) {
       cudaFuncSetAttribute(k_assemble_async<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES_ASYNC);
       for (int md : {(int)EPI_R, (int)EPI_JV, (int)EPI_STAGE_JV, (int)EPI_DEFECT, (int)EPI_F})
@@ -2378,7 +2405,8 @@ static int run_residual(const DiscDev& d, const double* q, const double* X, doub
     k_assemble<P, KIND, true><<<grid, TH, L::BYTES_ASM, st>>>(d.C, d.mesh, qq, d.qtr, d.fvn, d.grad, epi, out, bad,
                                                                stp);
   else
-    k_assemble<P, KIND><<<grid, TH, L::BYTES_ASM, st>>>(d.C, d.mesh, qq, d.qtr, d.fvn, d.grad, epi, out, bad, stp);
+    asm_for<P, KIND>(epi.mode)<<<grid, TH, L::BYTES_ASM, st>>>(d.C, d.mesh, qq, d.qtr, d.fvn, d.grad, epi, out, bad,
+                                                              stp);
   return (int)cudaGetLastError();
 }
 

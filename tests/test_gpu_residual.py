@@ -206,9 +206,9 @@ def test_free_stream_preserved_options(cuda, riemann, visc):
 
 
 def test_epilogue_specialization_is_bitwise(cuda):
-    # k_assemble_async's compile-time epilogue instantiations (R, Jv, PTC Jv,
-    # defect, F at their own register targets) must give the runtime-switch
-    # kernel's bits in every mode
+    # the assemble kernels' compile-time epilogue instantiations (R, Jv, PTC
+    # Jv, defect, F at their own register targets; async at p=4, plain at
+    # p=2) must give the runtime-switch kernels' bits in every mode
     import os
     import subprocess
     import sys
@@ -220,4 +220,4 @@ def test_epilogue_specialization_is_bitwise(cuda):
         r = subprocess.run([sys.executable, script], env=env, capture_output=True, text=True, timeout=600)
         assert r.returncode == 0, r.stderr[-2000:]
         runs.append(r.stdout.split())
-    assert len(runs[0]) == 8 and runs[0] == runs[1]
+    assert len(runs[0]) == 16 and runs[0] == runs[1]
