@@ -31,7 +31,13 @@ template <> struct GJTile<16>  { static constexpr int TR = 2, TC = 4; };
 template <> struct GJTile<25>  { static constexpr int TR = 5, TC = 5; };
 template <> struct GJTile<36>  { static constexpr int TR = 3, TC = 6; };
 template <> struct GJTile<64>  { static constexpr int TR = 4, TC = 8; };
-template <> struct GJTile<100> { static constexpr int TR = 4, TC = 10; };
+#ifndef PMGB_GJ100_TR
+#define PMGB_GJ100_TR 4
+#endif
+#ifndef PMGB_GJ100_TC
+#define PMGB_GJ100_TC 10
+#endif
+template <> struct GJTile<100> { static constexpr int TR = PMGB_GJ100_TR, TC = PMGB_GJ100_TC; };
 template <> struct GJTile<144> { static constexpr int TR = 8, TC = 6; };
 
 template <int SZ> struct GJShape {
