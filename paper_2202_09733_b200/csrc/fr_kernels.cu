@@ -115,6 +115,7 @@ template <int P> struct MinBlocks {
                                                                       : PMGB_REG_TARGET_K)));
   static constexpr int FVN = cap(65536 / (BC<P>::THREADS * (P == 5 ? PMGB_FVN_REGS_P5 : PMGB_FVN_REGS)));
   static constexpr int TRACE = cap(65536 / (BC<P>::THREADS * PMGB_TRACE_REGS));
+  static constexpr int BLK = cap(65536 / (BC<P>::THREADS * PMGB_BLOCKS_REGS));
 };
 
 struct Ops {
@@ -1950,7 +1951,7 @@ k_local(const FrConst C, const FrMesh m, const int64_t* __restrict__ elems, int6
 // slots; column c perturbs local DoF c-1 by +eps (newton_krylov.py:174-184).
 // Writes B^T (column-major block) so each column is a contiguous store.
 template <int P, int KIND>
-__global__ void __launch_bounds__(BC<P>::THREADS, MinBlocks<P>::ASM)
+__global__ void __launch_bounds__(BC<P>::THREADS, MinBlocks<P>::BLK)
 k_blocks(const FrConst C, const FrMesh m, const double* __restrict__ q, const double* __restrict__ qtr,
          const double* __restrict__ fvn, double shift, double eps, double* __restrict__ BT,
          const int* __restrict__ out_slot) {

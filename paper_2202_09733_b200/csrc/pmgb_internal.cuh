@@ -50,6 +50,9 @@ template <> struct KT<K_ADVD>  { static constexpr int NV = 1, NW = 1; static con
 #ifndef PMGB_REG_TARGET_R   // R-only (EPI_R) instantiation of k_assemble_async
 #define PMGB_REG_TARGET_R 72
 #endif
+#ifndef PMGB_BLOCKS_REGS   // k_blocks (FD element-block assembly)
+#define PMGB_BLOCKS_REGS 80
+#endif
 #ifndef PMGB_REG_TARGET_R_P3
 #define PMGB_REG_TARGET_R_P3 72
 #endif
