@@ -21,6 +21,9 @@
 
 #include "pmgb_internal.cuh"
 
+#ifndef PMGB_FVN_REGS_P3   // p = 3: 72 (R 118 -> 111 us at config 4, profiles/r1/ab_fvn_regs_r1q.log)
+#define PMGB_FVN_REGS_P3 72
+#endif
 #ifndef PMGB_FVN_REGS
 #define PMGB_FVN_REGS 64
 #endif
@@ -113,7 +116,9 @@ template <int P> struct MinBlocks {
   static constexpr int ASM_K = cap(65536 / (BC<P>::THREADS * (P == 5   ? PMGB_REG_TARGET_K_P5
                                                              : P == 3 ? PMGB_REG_TARGET_K_P3
                                                                       : PMGB_REG_TARGET_K)));
-  static constexpr int FVN = cap(65536 / (BC<P>::THREADS * (P == 5 ? PMGB_FVN_REGS_P5 : PMGB_FVN_REGS)));
+  static constexpr int FVN = cap(65536 / (BC<P>::THREADS * (P == 5   ? PMGB_FVN_REGS_P5
+                                                           : P == 3 ? PMGB_FVN_REGS_P3
+                                                                    : PMGB_FVN_REGS)));
   static constexpr int TRACE = cap(65536 / (BC<P>::THREADS * PMGB_TRACE_REGS));
   static constexpr int BLK = cap(65536 / (BC<P>::THREADS * PMGB_BLOCKS_REGS));
 };
