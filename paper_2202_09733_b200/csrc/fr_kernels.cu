@@ -21,6 +21,9 @@
 
 #include "pmgb_internal.cuh"
 
+#ifndef PMGB_FVN_REGS_P2
+#define PMGB_FVN_REGS_P2 64
+#endif
 #ifndef PMGB_FVN_REGS_P3   // p = 3: 72 (R 118 -> 111 us at config 4, profiles/r1/ab_fvn_regs_r1q.log)
 #define PMGB_FVN_REGS_P3 72
 #endif
@@ -118,6 +121,7 @@ template <int P> struct MinBlocks {
                                                                       : PMGB_REG_TARGET_K)));
   static constexpr int FVN = cap(65536 / (BC<P>::THREADS * (P == 5   ? PMGB_FVN_REGS_P5
                                                            : P == 3 ? PMGB_FVN_REGS_P3
+                                                           : P == 2 ? PMGB_FVN_REGS_P2
                                                                     : PMGB_FVN_REGS)));
   static constexpr int TRACE = cap(65536 / (BC<P>::THREADS * PMGB_TRACE_REGS));
   static constexpr int BLK = cap(65536 / (BC<P>::THREADS * PMGB_BLOCKS_REGS));
