@@ -156,18 +156,23 @@ class Frozen:
 class OracleDisc:
     """FR residual on a uniform-degree quad mesh (CPU, NumPy)."""
 
-    def __init__(self, mesh: Mesh, p: int, eqn: EquationSpec):
+    def __init__(self, mesh: Mesh, p: int, eqn: EquationSpec, dtype=np.float64):
+        """``dtype=np.longdouble`` evaluates the same algorithm in x87
+        extended precision (64-bit significand) on the float64 operators and
+        geometry: the "truth" the full-size parity tests measure both the
+        reference's and the device's float64 rounding against."""
         self.mesh, self.p, self.eqn = mesh, int(p), eqn
+        self.dtype = dt = np.dtype(dtype)
         self.n = n = self.p + 1
         self.nv = eqn.nvars
         M = mesh.n_elements
         self.n_dofs = M * n * n * self.nv
         self.offsets = np.arange(M + 1) * (n * n * self.nv)
         self.degrees = np.full(M, self.p)
-        self.D, self.eL, self.eR, self.lL, self.lR = face_operators(self.p)
+        self.D, self.eL, self.eR, self.lL, self.lR = (a.astype(dt) for a in face_operators(self.p))
         g = element_geometry(mesh, self.p)
-        self.jac, self.det = g.jac, g.det
-        self.nrm, self.js = g.face_normals, g.face_jac
+        self.jac, self.det = g.jac.astype(dt), g.det.astype(dt)
+        self.nrm, self.js = g.face_normals.astype(dt), g.face_jac.astype(dt)
         self.link, self.tag = face_links(mesh)
         self.interior = self.link[..., 0] >= 0
         k = np.arange(n)
@@ -314,7 +319,7 @@ class OracleDisc:
     def residual(self, q):
         n, nv, eqn = self.n, self.nv, self.eqn
         e = slice(None)
-        Q = np.asarray(q, dtype=float).reshape(-1, n, n, nv)
+        Q = np.asarray(q, dtype=self.dtype).reshape(-1, n, n, nv)
         self._check(Q, "state")
         tr = self._traces(Q)
         self._check(tr, "trace")
@@ -357,7 +362,7 @@ class OracleDisc:
         if not wall.any():
             raise ValueError("mesh has no wall boundary faces")
         n, nv = self.n, self.nv
-        Q = np.asarray(q, dtype=float).reshape(-1, n, n, nv)
+        Q = np.asarray(q, dtype=self.dtype).reshape(-1, n, n, nv)
         tr = self._traces(Q)
         grads = None
         if eqn.viscous:
@@ -412,7 +417,7 @@ class OracleDisc:
         import os
         T = int(threads or len(os.sched_getaffinity(0)))
         n, nv, eqn = self.n, self.nv, self.eqn
-        Q = np.asarray(q, dtype=float).reshape(-1, n, n, nv)
+        Q = np.asarray(q, dtype=self.dtype).reshape(-1, n, n, nv)
         M = Q.shape[0]
         C = int(chunk or max(64, -(-M // (4 * T))))
         sl = [slice(a, min(a + C, M)) for a in range(0, M, C)]
@@ -424,7 +429,7 @@ class OracleDisc:
         def run(fn):
             return list(pool.map(fn, sl))
 
-        tr = np.empty((M, 4, n, nv))
+        tr = np.empty((M, 4, n, nv), dtype=self.dtype)
 
         def p1(s):
             bs = self._first_bad(Q[s])
@@ -463,8 +468,8 @@ class OracleDisc:
             run(pe)
             return R.reshape(-1)
         nw = self._grad_vars(Q[:1]).shape[-1]
-        gx = np.empty((M, n, n, nw))
-        gy = np.empty((M, n, n, nw))
+        gx = np.empty((M, n, n, nw), dtype=self.dtype)
+        gy = np.empty((M, n, n, nw), dtype=self.dtype)
         fvn = np.empty_like(tr)
 
         def p3(s):
@@ -492,7 +497,7 @@ class OracleDisc:
 
     def freeze(self, q) -> Frozen:
         n, nv = self.n, self.nv
-        Q = np.asarray(q, dtype=float).reshape(-1, n, n, nv)
+        Q = np.asarray(q, dtype=self.dtype).reshape(-1, n, n, nv)
         tr = self._traces(Q)
         q_nb = self._gather_nb(tr)
         fvn_nb = None
@@ -513,7 +518,7 @@ class OracleDisc:
         = (f, q_rec, fvn_rec) replaces face f's frozen record by batched
         records from ``neighbor_record`` (the reference's face_override,
         spatial.py:787-790)."""
-        Q = np.asarray(Q, dtype=float)
+        Q = np.asarray(Q, dtype=self.dtype)
         tr = self._traces(Q)
         inter = self.interior[e][:, None, None]
         q_nb = frozen.q_nb[e]
@@ -550,7 +555,7 @@ class OracleDisc:
         one-sided viscous flux, aligned to e's face points, in the Frozen
         sign convention (fvn = -neighbour flux)."""
         nb, fnb, rev = int(self.nb[e, f]), int(self.fnb[e, f]), bool(self.link[e, f, 2])
-        Q_nb = np.asarray(Q_nb, dtype=float)
+        Q_nb = np.asarray(Q_nb, dtype=self.dtype)
         tr = self._traces(Q_nb)
         q_rec = tr[..., fnb, :, :]
         if rev:

@@ -1,7 +1,7 @@
 """Device Jv / EJ blocks / transfers / GMRES / pMG / steppers vs the oracle
 and the reference golden vectors, all through the C ABI.
 
-Tolerances: Jv 1e-8 (the fixed eps = 1e-6 amplifies
+Tolerances: Jv 1e-9 (the fixed eps = 1e-6 amplifies
 R rounding by 1e6); FD blocks 1e-7 of the block scale; solver iteration
 counts +-1; one-step solutions 1e-7 (esdirk2, floor 1.2e-8) and 1e-6 (row4,
 floor 7.4e-8)."""
@@ -43,7 +43,7 @@ def test_jv_matches_reference_and_own_residual(cuda):
     R0 = d.residual(q)
     v = t(G["c1/v"])
     Jv = nk.jfnk_matvec(v, q, R0, d.residual, 3.7)
-    assert rel(Jv, G["c1/Jv"]) <= 1e-8
+    assert rel(Jv, G["c1/Jv"]) <= 1e-9  # measured floor 1.4e-10
     # bitwise consistency with the device's own R(q + eps v) and R(q)
     qp = torch.as_tensor(c.q0 + 1e-6 * G["c1/v"], device="cuda")
     # (torch turns division by a Python scalar into a reciprocal multiply)

@@ -166,3 +166,16 @@ def test_oracle_threaded_residual_raises_like_residual():
             f(q.reshape(-1))
         errs.append(str(ei.value))
     assert errs[0] == errs[1]
+
+
+def test_oracle_long_double_truth_pins_reference_config1():
+    # the extended-precision oracle the full-size parity tests use as truth
+    # (tests/test_gpu_fullsize_oracle.py) agrees with the reference's own
+    # float64 config-1 residual to the reference's rounding floor
+    c = cases.config(1)
+    tl = OracleDisc(c.mesh, c.p, c.eqn, dtype=np.longdouble)
+    truth = tl.residual(c.q0)
+    assert truth.dtype == np.longdouble
+    assert np.array_equal(truth, tl.residual_mt(c.q0))
+    err = float(np.max(np.abs(G["c1/R0"] - truth)) / np.max(np.abs(truth)))
+    assert err <= 1e-12
