@@ -65,6 +65,12 @@ typedef struct pmgb_disc_desc {
 PMGB_API int pmgb_disc_create(const pmgb_disc_desc* desc, pmgb_disc** out);
 PMGB_API int pmgb_disc_destroy(pmgb_disc* d);
 PMGB_API int64_t pmgb_disc_n_dofs(const pmgb_disc* d);
+/* Residual kernel family of a context: 1 = the axis-aligned-rectangle
+   path (fr_rect.cu; chosen at creation when every element qualifies),
+   0 = the general bilinear path.  `want` < 0 only queries; 1 is honoured
+   only when the mesh qualifies.  Returns the path now in effect.  (No
+   reference counterpart: both paths implement spatial.py:501-570.) */
+PMGB_API int pmgb_disc_residual_path(pmgb_disc* d, int32_t want);
 
 /* R(q) -- replaces Discretization.residual (spatial.py:501-570). */
 PMGB_API int pmgb_residual(pmgb_disc* d, const double* q, double* R, void* stream);

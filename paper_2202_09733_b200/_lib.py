@@ -51,6 +51,7 @@ SIGNATURES = {
     "pmgb_disc_create": (ctypes.c_int, [ctypes.POINTER(DiscDesc), ctypes.POINTER(c_void_p)]),
     "pmgb_disc_destroy": (ctypes.c_int, [c_void_p]),
     "pmgb_disc_n_dofs": (ctypes.c_int64, [c_void_p]),
+    "pmgb_disc_residual_path": (ctypes.c_int, [c_void_p, ctypes.c_int32]),
     "pmgb_residual": (ctypes.c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
     "pmgb_rk_lambda": (ctypes.c_int, [c_void_p, c_void_p, ctypes.c_double, c_void_p, c_void_p]),
     "pmgb_rk_dtau": (ctypes.c_int, [ctypes.c_int64, c_void_p, ctypes.c_double, ctypes.c_double, c_void_p,

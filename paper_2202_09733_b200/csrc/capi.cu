@@ -69,6 +69,63 @@ PMGB_API const char* pmgb_error_string(int code) {
   return "unknown pmgflow_b200 error";
 }
 
+// Rectangle fast path (fr_rect.cu): taken when every element is an
+// axis-aligned rectangle whose geometry record has exactly zero cross
+// metric terms, axis-aligned unit normals and face_jac equal to the
+// half-widths -- then the reference's metric expressions reduce to
+// per-element constants with no rounding of their own.  Builds the
+// unique-face list (sorted by owner element) and the face records.
+static int setup_rect(const pmgb_disc_desc* desc, DiscDev& d) {
+  d.has_rect = 0;
+  if (!rect_supported(d.p, d.kind) || d.M == 0) return 0;
+  const double* G = desc->geom;
+  std::vector<double2> rg((size_t)d.M);
+  for (int64_t e = 0; e < d.M; ++e) {
+    const double* g = G + e * 20;
+    const double a0 = g[0], d0 = g[6];
+    const bool ok = g[1] == 0.0 && g[2] == 0.0 && g[3] == 0.0 && g[4] == 0.0 && g[5] == 0.0 && g[7] == 0.0 &&
+                    a0 > 0.0 && d0 > 0.0 && g[8] == 0.0 && g[9] == -1.0 && g[10] == 1.0 && g[11] == 0.0 &&
+                    g[12] == 0.0 && g[13] == 1.0 && g[14] == -1.0 && g[15] == 0.0 && g[16] == a0 &&
+                    g[18] == a0 && g[17] == d0 && g[19] == d0;
+    if (!ok) return 0;
+    rg[(size_t)e] = make_double2(1.0 / a0, 1.0 / d0);
+  }
+  std::vector<int4> faces;
+  faces.reserve((size_t)d.M * 2 + 16);
+  std::vector<int> fslot((size_t)d.M * 4, -1);
+  for (int64_t e = 0; e < d.M; ++e)
+    for (int f = 0; f < 4; ++f) {
+      const int64_t* r = desc->links + (e * 4 + f) * 4;
+      const bool bnd = r[0] < 0;
+      if (!bnd && !(r[3] & 1)) continue;  // the L side owns the face
+      const int tag = desc->tags[e * 4 + f];
+      int4 v;
+      v.x = (int)e;
+      v.y = f | ((int)(r[2] & 1) << 2) | ((int)bnd << 3) | ((tag < 0 ? 0 : tag & 15) << 4);
+      v.z = bnd ? -1 : (int)r[0];
+      v.w = bnd ? 0 : (int)r[1];
+      const int phi = (int)faces.size();
+      faces.push_back(v);
+      fslot[(size_t)e * 4 + f] = phi;
+      if (!bnd) fslot[(size_t)r[0] * 4 + r[1]] = phi;
+    }
+  for (int v : fslot)
+    if (v < 0) return -1;
+  RectDev& R = d.rect;
+  R.nface = (int64_t)faces.size();
+  const int n = d.p + 1;
+  cudaError_t err = cudaMalloc(&R.faces, sizeof(int4) * faces.size());
+  if (!err) err = cudaMalloc(&R.fslot, sizeof(int) * fslot.size());
+  if (!err) err = cudaMalloc(&R.rgeo, sizeof(double2) * rg.size());
+  if (!err) err = cudaMalloc(&R.fw, sizeof(double) * 8 * (size_t)R.nface * n);
+  if (!err) err = cudaMemcpy(R.faces, faces.data(), sizeof(int4) * faces.size(), cudaMemcpyHostToDevice);
+  if (!err) err = cudaMemcpy(R.fslot, fslot.data(), sizeof(int) * fslot.size(), cudaMemcpyHostToDevice);
+  if (!err) err = cudaMemcpy(R.rgeo, rg.data(), sizeof(double2) * rg.size(), cudaMemcpyHostToDevice);
+  if (err) return (int)err;
+  d.has_rect = 1;
+  return 0;
+}
+
 PMGB_API int pmgb_disc_create(const pmgb_disc_desc* desc, pmgb_disc** out) {
   if (!desc || !out) return -1;
   if (desc->degree < 0 || desc->degree > 5) return -2;
@@ -132,6 +189,11 @@ PMGB_API int pmgb_disc_create(const pmgb_disc_desc* desc, pmgb_disc** out) {
   d.mesh.M = d.M;
   d.mesh.geom = d.geom;
   d.mesh.link = d.link;
+  err = (cudaError_t)setup_rect(desc, d);
+  if (err) {
+    pmgb_disc_destroy(h);
+    return (int)err;
+  }
   *out = h;
   return 0;
 }
@@ -144,11 +206,21 @@ PMGB_API int pmgb_disc_destroy(pmgb_disc* h) {
   cudaFree(h->d.fvn);
   cudaFree(h->d.qp);
   cudaFree(h->d.grad);
+  cudaFree(h->d.rect.faces);
+  cudaFree(h->d.rect.fslot);
+  cudaFree(h->d.rect.rgeo);
+  cudaFree(h->d.rect.fw);
   delete h;
   return 0;
 }
 
 PMGB_API int64_t pmgb_disc_n_dofs(const pmgb_disc* h) { return h ? h->d.n_dofs : -1; }
+
+PMGB_API int pmgb_disc_residual_path(pmgb_disc* h, int32_t want) {
+  if (!h) return -1;
+  if (want >= 0) h->d.has_rect = (want != 0 && h->d.rect.fw != nullptr) ? 1 : 0;
+  return h->d.has_rect;
+}
 
 static int n_res_launches(const DiscDev& d) { return (d.kind == K_NS || d.kind == K_ADVD) ? 3 : 2; }
 

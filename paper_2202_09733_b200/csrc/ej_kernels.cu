@@ -767,15 +767,16 @@ static int run_ilu_persistent(int n_lo, const int* lo_ptr, const int* lo_rows, i
                               const double* DX, const uint8_t* DP, const double* x, double* y, double* out,
                               unsigned* bar, int max_rows, cudaStream_t st) {
   constexpr int TH = (SZ + 31) / 32 * 32;
-  static int resident_of[64] = {0};  // co-resident CTAs, per device
+  static std::atomic<int> resident_of[64];  // co-resident CTAs, per device (0 = not yet known)
   int dev = 0;
   cudaGetDevice(&dev);
-  int& resident = resident_of[dev & 63];
-  if (resident == 0) {
+  int resident = resident_of[dev & 63].load();
+  if (resident == 0) {  // idempotent: racing threads compute the same value
     int per_sm = 0, sms = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ilu_apply_persistent<SZ>, TH, 0);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     resident = per_sm * sms;
+    resident_of[dev & 63].store(resident);
   }
   int grid = max_rows < resident ? max_rows : resident;
   if (grid < 1) grid = 1;

@@ -20,6 +20,7 @@
 #include <cstdlib>
 
 #include "pmgb_internal.cuh"
+#include "fr_device.cuh"
 
 #ifndef PMGB_FVN_REGS_P2
 #define PMGB_FVN_REGS_P2 64
@@ -149,238 +150,6 @@ __device__ __forceinline__ Ops stage_ops(const FrConst& C, double* sm) {
     sm[i] = v;
   }
   return Ops{sm, sm + 36, sm + 42, sm + 48, sm + 54, sm + 60};
-}
-
-// point on face f, face point k, interpolation-line position i
-template <int N>
-__device__ __forceinline__ int fpt(int f, int k, int i) {
-  return f == 0 ? i * N + k : f == 1 ? k * N + i : f == 2 ? i * N + (N - 1 - k) : (N - 1 - k) * N + i;
-}
-
-// Reciprocal and square root without the IEEE slow-path branches of
-// __drcp_rn / sqrt: MUFU seed + two Newton steps (~1 ulp; parity budget
-// is 1e-12 relative).  Valid states only feed positive normal inputs;
-// non-physical inputs still produce NaN/Inf, and the physicality flags are
-// evaluated on the raw state, not through these.
-// Programmatic dependent launch: a kernel launched with the PDL attribute
-// may start while its predecessor drains; it must wait before touching the
-// predecessor's outputs.  Both are no-ops for ordinary launches.
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
-__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::); }
-
-__device__ __forceinline__ double rcp(double x) {
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  double e = fma(-x, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-x, r, 1.0);
-  return fma(r, e, r);
-}
-
-__device__ __forceinline__ double fsqrt(double x) {
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  // two Newton steps on y ~ 1/sqrt(x), then s = x y with one correction
-  y = y * fma(-0.5 * x * y, y, 1.5);
-  y = y * fma(-0.5 * x * y, y, 1.5);
-  const double s = x * y;
-  return fma(0.5 * y, fma(-s, s, x), s);
-}
-
-// ---------------------------------------------------------------------------
-// pointwise physics (spatial.py:94-203)
-
-struct Phys {
-  double gamma, mu, kappa, ax, ay, diff, twall;
-  int riemann, ldg;  // FrConst options (Rusanov flux, LDG viscous scheme)
-};
-
-__device__ __forceinline__ void prim(const double* q, double g, double& r, double& ir, double& u, double& v,
-                                     double& p) {
-  r = q[0];
-  ir = rcp(r);
-  u = q[1] * ir;
-  v = q[2] * ir;
-  p = (g - 1.0) * (q[3] - 0.5 * r * (u * u + v * v));
-}
-
-// Roe flux along (nx, ny), no entropy fix (spatial.py:113-163)
-__device__ __forceinline__ void roe(const double* qL, const double* qR, double nx, double ny, double g,
-                                    double* F) {
-  double rL, irL, uL, vL, pL, rR, irR, uR, vR, pR;
-  prim(qL, g, rL, irL, uL, vL, pL);
-  prim(qR, g, rR, irR, uR, vR, pR);
-  const double EpL = qL[3] + pL, EpR = qR[3] + pR;
-  const double HL = EpL * irL;
-  const double HR = EpR * irR;
-  const double sL = fsqrt(rL), sR = fsqrt(rR);
-  const double w = sL * rcp(sL + sR), w1 = 1.0 - w;
-  const double u = w * uL + w1 * uR;
-  const double v = w * vL + w1 * vR;
-  const double H = w * HL + w1 * HR;
-  const double ke = 0.5 * (u * u + v * v);
-  const double c2 = (g - 1.0) * (H - ke);
-  const double c = fsqrt(c2);
-  const double ic2 = rcp(c2);
-  const double rb = sL * sR;
-  const double un = u * nx + v * ny;
-  const double du = uR - uL, dv = vR - vL;
-  const double dn = du * nx + dv * ny;
-  const double dtg = -du * ny + dv * nx;
-  const double dp = pR - pL;
-  const double k1 = fabs(un - c) * ((dp - rb * c * dn) * (0.5 * ic2));
-  const double k2 = fabs(un) * ((rR - rL) - dp * ic2);
-  const double k3 = fabs(un) * (rb * dtg);
-  const double k4 = fabs(un + c) * ((dp + rb * c * dn) * (0.5 * ic2));
-  const double ut = -u * ny + v * nx;
-  const double d0 = k1 + k2 + k4;
-  const double d1 = k1 * (u - c * nx) + k2 * u - k3 * ny + k4 * (u + c * nx);
-  const double d2 = k1 * (v - c * ny) + k2 * v + k3 * nx + k4 * (v + c * ny);
-  const double d3 = k1 * (H - c * un) + k2 * ke + k3 * ut + k4 * (H + c * un);
-  const double qnL = uL * nx + vL * ny, qnR = uR * nx + vR * ny;
-  F[0] = 0.5 * (qL[0] * qnL + qR[0] * qnR) - 0.5 * d0;
-  F[1] = 0.5 * ((qL[1] * qnL + pL * nx) + (qR[1] * qnR + pR * nx)) - 0.5 * d1;
-  F[2] = 0.5 * ((qL[2] * qnL + pL * ny) + (qR[2] * qnR + pR * ny)) - 0.5 * d2;
-  F[3] = 0.5 * (EpL * qnL + EpR * qnR) - 0.5 * d3;
-}
-
-// Rusanov (local Lax-Friedrichs) flux -- the BASELINE configs' interface
-// flux, not in the reference (oracle: fr_oracle.rusanov_flux)
-__device__ __forceinline__ void rusanov(const double* qL, const double* qR, double nx, double ny, double g,
-                                        double* F) {
-  double rL, irL, uL, vL, pL, rR, irR, uR, vR, pR;
-  prim(qL, g, rL, irL, uL, vL, pL);
-  prim(qR, g, rR, irR, uR, vR, pR);
-  const double qnL = uL * nx + vL * ny, qnR = uR * nx + vR * ny;
-  const double lam = fmax(fabs(qnL) + fsqrt(g * pL * irL), fabs(qnR) + fsqrt(g * pR * irR));
-  const double hl = 0.5 * lam;
-  F[0] = 0.5 * (qL[0] * qnL + qR[0] * qnR) - hl * (qR[0] - qL[0]);
-  F[1] = 0.5 * ((qL[1] * qnL + pL * nx) + (qR[1] * qnR + pR * nx)) - hl * (qR[1] - qL[1]);
-  F[2] = 0.5 * ((qL[2] * qnL + pL * ny) + (qR[2] * qnR + pR * ny)) - hl * (qR[2] - qL[2]);
-  F[3] = 0.5 * ((qL[3] + pL) * qnL + (qR[3] + pR) * qnR) - hl * (qR[3] - qL[3]);
-}
-
-template <int KIND>
-__device__ __forceinline__ void num_flux(const double* qa, const double* qc, double nx, double ny,
-                                         const Phys& ph, double* F) {
-  if constexpr (KT<KIND>::FLOW) {
-    if (ph.riemann)
-      rusanov(qa, qc, nx, ny, ph.gamma, F);
-    else
-      roe(qa, qc, nx, ny, ph.gamma, F);
-  } else {
-    const double an = ph.ax * nx + ph.ay * ny;
-    F[0] = 0.5 * an * (qa[0] + qc[0]) - 0.5 * fabs(an) * (qc[0] - qa[0]);
-  }
-}
-
-template <int KIND>
-__device__ __forceinline__ void ghost(const double* q, int tag, double nx, double ny, const double* qinf,
-                                      double* gq) {
-  if constexpr (KT<KIND>::FLOW) {
-    if (tag == T_FAR_FIELD) {
-      for (int v = 0; v < 4; ++v) gq[v] = qinf[v];
-    } else if (tag == T_WALL_SLIP) {
-      const double un = q[1] * nx + q[2] * ny;
-      gq[0] = q[0];
-      gq[1] = q[1] - 2.0 * un * nx;
-      gq[2] = q[2] - 2.0 * un * ny;
-      gq[3] = q[3];
-    } else {
-      gq[0] = q[0];
-      gq[1] = -q[1];
-      gq[2] = -q[2];
-      gq[3] = q[3];
-    }
-  } else {
-    gq[0] = (tag == T_FAR_FIELD) ? 0.0 : q[0];
-  }
-}
-
-// Viscous variables of a boundary face's ghost: on wall-isothermal faces
-// (BASELINE config 4; not in the reference) the ghost keeps the mirrored
-// no-slip state of the inviscid flux but carries T = 2 T_w - T, so the BR1
-// common value holds T_w (oracle: OracleDisc._w_out).
-template <int KIND>
-__device__ __forceinline__ void ghost_w(const Phys& ph, int tag, const double* wa, double* wc) {
-  if constexpr (KT<KIND>::FLOW)
-    if (tag == T_WALL_ISOTHERMAL) wc[2] = 2.0 * ph.twall - wa[2];
-}
-
-// Common viscous-variable value on a face: BR1 average (reference,
-// spatial.py:536-546) or LDG (C11 = 0, switch from the face's L element):
-// L's trace on interior faces; boundary faces keep the BR1 ghost average.
-__device__ __forceinline__ double common_w(const Phys& ph, bool interior, bool left, double wa, double wc) {
-  return (ph.ldg && interior) ? (left ? wa : wc) : 0.5 * (wa + wc);
-}
-// Common viscous normal flux on the own normal from the own one-sided flux
-// Fo and the neighbour's on ITS normal Fn: BR1 0.5 (Fo - Fn) (spatial.py:
-// 559-568); LDG R's flux: -Fn seen from L, Fo seen from R.
-__device__ __forceinline__ double common_fv(const Phys& ph, bool interior, bool left, double Fo, double Fn) {
-  if (!interior) return Fo;
-  return ph.ldg ? (left ? -Fn : Fo) : 0.5 * (Fo - Fn);
-}
-
-// viscous variables W = (u, v, T = p/rho) (spatial.py:448-454)
-template <int KIND>
-__device__ __forceinline__ void grad_vars(const double* q, double g, double* w) {
-  if constexpr (KT<KIND>::FLOW) {
-    double r, ir, u, v, p;
-    prim(q, g, r, ir, u, v, p);
-    w[0] = u;
-    w[1] = v;
-    w[2] = p * ir;
-  } else {
-    w[0] = q[0];
-  }
-}
-
-// viscous flux vectors (spatial.py:166-180) -- ADVD: k grad
-template <int KIND>
-__device__ __forceinline__ void visc_flux(const double* q, const double* gx, const double* gy, const Phys& ph,
-                                          double* fx, double* fy) {
-  if constexpr (KT<KIND>::FLOW) {
-    const double ir = rcp(q[0]);
-    const double u = q[1] * ir, v = q[2] * ir;
-    const double d = gx[0] + gy[1];
-    const double txx = ph.mu * (2.0 * gx[0] - (2.0 / 3.0) * d);
-    const double tyy = ph.mu * (2.0 * gy[1] - (2.0 / 3.0) * d);
-    const double txy = ph.mu * (gy[0] + gx[1]);
-    fx[0] = 0.0;
-    fx[1] = txx;
-    fx[2] = txy;
-    fx[3] = u * txx + v * txy + ph.kappa * gx[2];
-    fy[0] = 0.0;
-    fy[1] = txy;
-    fy[2] = tyy;
-    fy[3] = u * txy + v * tyy + ph.kappa * gy[2];
-  } else {
-    fx[0] = ph.diff * gx[0];
-    fy[0] = ph.diff * gy[0];
-  }
-}
-
-__device__ __forceinline__ bool physical(const double* q, double g) {
-  double r, ir, u, v, p;
-  prim(q, g, r, ir, u, v, p);
-  return (r > 0.0) && (p > 0.0);
-}
-
-// bilinear metrics from the packed geometry record (mesh.pack_geometry)
-struct Metric {
-  double a0, a1, b0, b1, c0, c1, d0, d1;
-  __device__ __forceinline__ double J00(double eta) const { return a0 + a1 * eta; }  // x_xi
-  __device__ __forceinline__ double J10(double eta) const { return b0 + b1 * eta; }  // y_xi
-  __device__ __forceinline__ double J01(double xi) const { return c0 + c1 * xi; }    // x_eta
-  __device__ __forceinline__ double J11(double xi) const { return d0 + d1 * xi; }    // y_eta
-  __device__ __forceinline__ bool affine() const { return a1 == 0.0 && b1 == 0.0 && c1 == 0.0 && d1 == 0.0; }
-};
-__device__ __forceinline__ Metric metric(const double* g) {
-  return Metric{g[0], g[1], g[2], g[3], g[4], g[5], g[6], g[7]};
-}
-
-__device__ __forceinline__ Phys phys_of(const FrConst& C) {
-  return Phys{C.gamma, C.mu, C.kappa, C.adv_x, C.adv_y, C.diff, C.twall, C.riemann, C.ldg};
 }
 
 // ---------------------------------------------------------------------------
@@ -1179,162 +948,6 @@ k_fvn(const FrConst C, const FrMesh m, const double* __restrict__ q, const doubl
 // ---------------------------------------------------------------------------
 // phase 3: common fluxes, volume fluxes, FR divergence, fused epilogue
 
-// RK smoother stage (EPI_RK), rounded as the oracle's NumPy expression
-//   c = alpha dtau_e;  q0 + c ((Sb - (s q - R)) + Se)
-// (dtau_e = cfl / (s + lam_e) comes precomputed per element from k_rk_dtau,
-// so the epilogue carries no division)
-__device__ __forceinline__ double epi_rk_coef(const Epi& ep, int64_t e) {
-  return __dmul_rn(ep.alpha, __ldg(ep.dtau_e + e));
-}
-__device__ __forceinline__ double epi_rk(const Epi& ep, double c, double R, double qv, double sb, double se,
-                                         double q0) {
-  const double d = __dadd_rn(__dsub_rn(sb, __dsub_rn(__dmul_rn(ep.s, qv), R)), se);
-  return __dadd_rn(q0, __dmul_rn(c, d));
-}
-
-template <bool RKE = false>
-__device__ __forceinline__ double epi_apply(const Epi& ep, int64_t i, double R, double qv) {
-  if constexpr (RKE) {
-    const double sb = ep.Sb ? ep.Sb[i] : ep.sb_scalar;
-    const double se = ep.Se ? ep.Se[i] : ep.se_scalar;
-    return epi_rk(ep, epi_rk_coef(ep, i / ep.npe), R, qv, sb, se, ep.Q0[i]);
-  }
-  switch (ep.mode) {
-    case EPI_R:
-      return R;
-    case EPI_F:
-      return ep.s * qv - R;
-    case EPI_DEFECT: {
-      const double sb = ep.Sb ? ep.Sb[i] : ep.sb_scalar;
-      const double se = ep.Se ? ep.Se[i] : ep.se_scalar;
-      return (sb - (ep.s * qv - R)) + se;
-    }
-    case EPI_JV:
-      return __dsub_rn(__dmul_rn(ep.s, ep.X[i]), __ddiv_rn(__dsub_rn(R, ep.R0[i]), ep.eps));
-    case EPI_STAGE_F:
-      return __dsub_rn(__ddiv_rn(__dsub_rn(qv, ep.E[i]), ep.adt), R);
-    case EPI_STAGE_JV: {
-      const double F = __dsub_rn(__ddiv_rn(__dsub_rn(qv, ep.E[i]), ep.adt), R);
-      return __dadd_rn(__ddiv_rn(ep.X[i], ep.dtau), __ddiv_rn(__dsub_rn(F, ep.R0[i]), ep.eps));
-    }
-    case EPI_NEG_R:
-      return -R;
-    case EPI_OUTER_F: {
-      const double se = ep.Se ? ep.Se[i] : ep.se_scalar;
-      return (ep.s * qv - R) - se;
-    }
-  }
-  return R;
-}
-
-// Epilogue with operands preloaded by the caller:
-//   JV: o1 = X, o2 = R0;  STAGE_F: o3 = E;  STAGE_JV: o1 = X, o2 = Fk, o3 = E;
-//   DEFECT: o1 = Sb, o2 = Se;  OUTER_F: o2 = Se
-__device__ __forceinline__ double epi_pre(const Epi& ep, double R, double qv, double o1, double o2, double o3) {
-  switch (ep.mode) {
-    case EPI_R:
-      return R;
-    case EPI_F:
-      return ep.s * qv - R;
-    case EPI_DEFECT:
-      return (o1 - (ep.s * qv - R)) + o2;
-    case EPI_JV:
-      return __dsub_rn(__dmul_rn(ep.s, o1), __ddiv_rn(__dsub_rn(R, o2), ep.eps));
-    case EPI_STAGE_F:
-      return __dsub_rn(__ddiv_rn(__dsub_rn(qv, o3), ep.adt), R);
-    case EPI_STAGE_JV: {
-      const double F = __dsub_rn(__ddiv_rn(__dsub_rn(qv, o3), ep.adt), R);
-      return __dadd_rn(__ddiv_rn(o1, ep.dtau), __ddiv_rn(__dsub_rn(F, o2), ep.eps));
-    }
-    case EPI_NEG_R:
-      return -R;
-    case EPI_OUTER_F:
-      return (ep.s * qv - R) - o2;
-  }
-  return R;
-}
-
-template <bool RKE = false>
-__device__ __forceinline__ void epi_load(const Epi& ep, int64_t i, double& o1, double& o2, double& o3) {
-  if constexpr (RKE) {   // RK stage: o1 = Sb, o2 = Se, o3 = Q0
-    o1 = ep.Sb ? __ldg(ep.Sb + i) : ep.sb_scalar;
-    o2 = ep.Se ? __ldg(ep.Se + i) : ep.se_scalar;
-    o3 = __ldg(ep.Q0 + i);
-    return;
-  }
-  o1 = o2 = o3 = 0.0;
-  switch (ep.mode) {
-    case EPI_JV:
-      o1 = __ldg(ep.X + i);
-      o2 = __ldg(ep.R0 + i);
-      break;
-    case EPI_STAGE_F:
-      o3 = __ldg(ep.E + i);
-      break;
-    case EPI_STAGE_JV:
-      o1 = __ldg(ep.X + i);
-      o2 = __ldg(ep.R0 + i);
-      o3 = __ldg(ep.E + i);
-      break;
-    case EPI_DEFECT:
-      o1 = ep.Sb ? __ldg(ep.Sb + i) : ep.sb_scalar;
-      o2 = ep.Se ? __ldg(ep.Se + i) : ep.se_scalar;
-      break;
-    case EPI_OUTER_F:
-      o2 = ep.Se ? __ldg(ep.Se + i) : ep.se_scalar;
-      break;
-    default:
-      break;
-  }
-}
-
-// Compile-time epilogue mode EK for k_assemble_async: EK < 0 keeps the
-// runtime switch over ep.mode; otherwise the switch is on the constant EK
-// and folds away (no dead operand registers).
-template <int EK>
-__device__ __forceinline__ void epi_load_k(const Epi& ep, int64_t i, double& o1, double& o2, double& o3) {
-  if constexpr (EK < 0) {
-    epi_load<false>(ep, i, o1, o2, o3);
-  } else if constexpr (EK == EPI_RK) {
-    epi_load<true>(ep, i, o1, o2, o3);
-  } else {
-    o1 = o2 = o3 = 0.0;
-    if constexpr (EK == EPI_JV || EK == EPI_STAGE_JV) {
-      o1 = __ldg(ep.X + i);
-      o2 = __ldg(ep.R0 + i);
-    }
-    if constexpr (EK == EPI_STAGE_F || EK == EPI_STAGE_JV) o3 = __ldg(ep.E + i);
-    if constexpr (EK == EPI_DEFECT) {
-      o1 = ep.Sb ? __ldg(ep.Sb + i) : ep.sb_scalar;
-      o2 = ep.Se ? __ldg(ep.Se + i) : ep.se_scalar;
-    }
-    if constexpr (EK == EPI_OUTER_F) o2 = ep.Se ? __ldg(ep.Se + i) : ep.se_scalar;
-  }
-}
-
-template <int EK>
-__device__ __forceinline__ double epi_pre_k(const Epi& ep, double R, double qv, double o1, double o2, double o3) {
-  if constexpr (EK < 0) {
-    return epi_pre(ep, R, qv, o1, o2, o3);
-  } else {
-    Epi e = ep;
-    e.mode = EK;   // a constant: epi_pre's switch folds
-    return epi_pre(e, R, qv, o1, o2, o3);
-  }
-}
-
-__device__ __forceinline__ void commit_status(int* bad, Status* st) {
-  if (bad == nullptr) return;
-  const int bs = bad[0], bt = bad[1];
-  if (bs != INT_MAX || bt != INT_MAX) {
-    if (st->kind == 0) {
-      st->kind = (bs != INT_MAX) ? 1 : 2;
-      st->element = (bs != INT_MAX) ? bs : bt;
-    }
-    bad[0] = INT_MAX;
-    bad[1] = INT_MAX;
-  }
-}
 
 // EK: compile-time epilogue mode as in k_assemble_async (-1 = runtime switch)
 template <int P, int KIND, bool RKE = false, int EK = -1>
@@ -2324,6 +1937,15 @@ static void launch_pdl(void (*kernel)(KArgs...), unsigned grid, int threads, siz
   cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 
+// PMGB_RECT=0 forces the general (bilinear) kernels on rectangle meshes (A/B)
+static bool rect_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("PMGB_RECT");
+    return v == nullptr || v[0] != '0';
+  }();
+  return on;
+}
+
 // PMGB_EPI_SPECIALIZE=0 forces the runtime-switch instantiation (A/B)
 static bool epi_specialize() {
   static const bool on = [] {
@@ -2372,7 +1994,7 @@ static int run_residual(const DiscDev& d, const double* q, const double* X, doub
   using L = SL<P, KIND>;
   constexpr int E = BC<P>::EPB, TH = BC<P>::THREADS;
   static std::atomic<unsigned long long> attr_seen{0};
-  if (first_use_on_device(attr_seen)) {
+  once_per_device(attr_seen, [&] {
     cudaFuncSetAttribute(k_trace<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES_TRACE);
     cudaFuncSetAttribute(k_fvn<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES_FVN);
     cudaFuncSetAttribute(k_assemble<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES_ASM);
@@ -2387,11 +2009,13 @@ static int run_residual(const DiscDev& d, const double* q, const double* X, doub
       cudaFuncSetAttribute(k_assemble_async<P, KIND, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)L::BYTES_ASYNC);
     }
-  }
+  });
   int* bad = nullptr;
   Status* stp = nullptr;
   cudaGetSymbolAddress((void**)&bad, g_bad);
   cudaGetSymbolAddress((void**)&stp, g_status);
+  if (d.has_rect && rect_enabled() && rect_supported(P, KIND))
+    return launch_residual_rect(d.rect, d, q, X, eps, epi, out, bad, stp, st);
   const unsigned grid = (unsigned)((d.M + E - 1) / E);
   const double* qq = q;
   if (X != nullptr) qq = d.qp;
@@ -2425,10 +2049,10 @@ static int run_freeze(const DiscDev& d, const double* q, double* qtr, double* fv
   using L = SL<P, KIND>;
   constexpr int E = BC<P>::EPB, TH = BC<P>::THREADS;
   static std::atomic<unsigned long long> attr_seen{0};
-  if (first_use_on_device(attr_seen)) {
+  once_per_device(attr_seen, [&] {
     cudaFuncSetAttribute(k_trace<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES_TRACE);
     cudaFuncSetAttribute(k_fvn<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES_FVN);
-  }
+  });
   const unsigned grid = (unsigned)((d.M + E - 1) / E);
   if constexpr (KT<KIND>::FLOW) {
     const unsigned gl = (unsigned)((d.M * 2 * (P + 1) + 127) / 128);
@@ -2446,9 +2070,9 @@ static int run_local(const DiscDev& d, const int64_t* elems, int64_t B, const do
   using L = SL<P, KIND>;
   constexpr int E = BC<P>::EPB, TH = BC<P>::THREADS;
   static std::atomic<unsigned long long> attr_seen{0};
-  if (first_use_on_device(attr_seen)) {
+  once_per_device(attr_seen, [&] {
     cudaFuncSetAttribute(k_local<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES_LOCAL);
-  }
+  });
   if (B <= 0) return 0;
   const unsigned grid = (unsigned)((B + E - 1) / E);
   k_local<P, KIND><<<grid, TH, L::BYTES_LOCAL, st>>>(d.C, d.mesh, elems, B, Q, qtr, fvn, out);
@@ -2461,9 +2085,9 @@ static int run_blocks(const DiscDev& d, const double* q, const double* qtr, cons
   using L = SL<P, KIND>;
   constexpr int TH = BC<P>::THREADS;
   static std::atomic<unsigned long long> attr_seen{0};
-  if (first_use_on_device(attr_seen)) {
+  once_per_device(attr_seen, [&] {
     cudaFuncSetAttribute(k_blocks<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES_LOCAL);
-  }
+  });
   if (d.M <= 0) return 0;
   k_blocks<P, KIND><<<(unsigned)d.M, TH, L::BYTES_LOCAL, st>>>(d.C, d.mesh, q, qtr, fvn, shift, eps, BT, out_slot);
   return (int)cudaGetLastError();
@@ -2476,10 +2100,10 @@ static int run_coupling(const DiscDev& d, const double* q, const double* qtr, co
   using L = SL<P, KIND>;
   constexpr int TH = BC<P>::THREADS;
   static std::atomic<unsigned long long> attr_seen{0};
-  if (first_use_on_device(attr_seen)) {
+  once_per_device(attr_seen, [&] {
     cudaFuncSetAttribute(k_coupling<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)L::BYTES_COUPLING);
-  }
+  });
   if (npairs <= 0) return 0;
   k_coupling<P, KIND><<<(unsigned)npairs, TH, L::BYTES_COUPLING, st>>>(d.C, d.mesh, q, qtr, fvn, eps, pair_e,
                                                                          pair_f, pair_slot, pair_add, blocks);
@@ -2495,10 +2119,10 @@ static int run_forces(const DiscDev& d, const double* q, int64_t nwall, const in
     return -5;
   } else {
     static std::atomic<unsigned long long> attr_seen{0};
-    if (first_use_on_device(attr_seen)) {
+    once_per_device(attr_seen, [&] {
       cudaFuncSetAttribute(k_trace<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES_TRACE);
       cudaFuncSetAttribute(k_fvn<P, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES_FVN);
-    }
+    });
     const unsigned grid = (unsigned)((d.M + E - 1) / E);
     const unsigned gl = (unsigned)((d.M * 2 * (P + 1) + 127) / 128);
     k_trace_lines<P, KIND><<<gl, 128, 0, st>>>(d.C, d.mesh, q, nullptr, 0.0, nullptr, d.qtr, nullptr);

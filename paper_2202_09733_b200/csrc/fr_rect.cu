@@ -1,0 +1,835 @@
+// FR residual R(u) and its fused epilogues on meshes of axis-aligned
+// rectangles (every BASELINE.json mesh: periodic boxes and the stretched
+// channel) -- hand-written FP64 kernels for sm_100a.
+//
+// Reference: /root/reference/pkg/src/pmgflow/spatial.py:501-570 (residual),
+// 594-603 (BR1 gradients), 407-430 (FR divergence), 113-203 (fluxes).
+//
+// On a rectangle the bilinear map is x = x0 + a0 xi, y = y0 + d0 eta with
+// exactly axis-aligned unit normals and face_jac = a0 (faces 0, 2) and d0
+// (faces 1, 3), so the reference's metric terms reduce to per-element
+// constants and every cross term is an exact zero:
+//   gx = (1/a0) [D_xi W + lR (What_1 - tr_1 W) - lL (What_3 - tr_3 W)]
+//   gy = (1/d0) [D_eta W + lR (What_2 - tr_2 W) - lL (What_0 - tr_0 W)]
+//   R  = -[(1/a0) X_xi + (1/d0) X_eta],
+//   X_xi  = D_xi fx + lR (Fc_1 - tr_1 fx) - lL (-Fc_3 - tr_3 fx)
+//   X_eta = D_eta fy + lR (Fc_2 - tr_2 fy) - lL (-Fc_0 - tr_0 fy)
+// (the reference's expressions with J = diag(a0, d0) substituted; they
+// differ from it only in rounding).  The one-sided viscous normal flux on a
+// face is +-fx or +-fy, so only that row of the stress is formed.
+//
+// Three kernels chained with programmatic dependent launch:
+//   k_rface  one thread per point of each UNIQUE face: the two face traces
+//            straight from the elements' q lines, the interface flux (Roe /
+//            Rusanov, once per face instead of once per side) and the BR1
+//            common value What, stored per face [face][point][F0..3, W0..2]
+//   k_rgrad  one thread per (element, line): BR1 gradients by line passes
+//            (rows for gx, columns for gy, one shared-memory transpose per
+//            pass), their face traces and the one-sided viscous fluxes fvn
+//   k_rasm   one thread per (element, line): gradients again (cheaper than
+//            a 2x79 MB round trip at config 2), point fluxes, the FR
+//            divergence by line passes, the fused epilogue
+// Line threads keep each line in registers, so the operator contractions
+// read shared memory only for the transposes (blocks of one line, stride
+// with an odd number of 16-byte units: conflict-free 128-bit accesses).
+#include <climits>
+
+#include "fr_device.cuh"
+
+namespace pmgb {
+
+struct RectMesh {
+  int64_t M;
+  int64_t nface;
+  const int4* __restrict__ faces;    // {eL, fL | rev<<2 | bnd<<3 | tag<<4, eR, fR}
+  const int* __restrict__ fslot;     // (M,4) face index of every element face
+  const int2* __restrict__ link;     // (M,4) the general link table
+  const double2* __restrict__ rgeo;  // (M) {1/a0, 1/d0}
+  const double* __restrict__ geom;   // (M,20) for the face normals
+};
+
+template <int P> struct RC {
+  static constexpr int N = P + 1, NP = N * N;
+  static constexpr int EPB = 128 / N;  // elements per CTA
+  static constexpr int TH = EPB * N;   // one thread per (element, line)
+  // line block stride in doubles: >= 4N, even, odd number of 16-B units
+  static constexpr int BS = ((4 * N) / 2) % 2 == 1 ? 4 * N : 4 * N + 2;
+  static constexpr int BUF = EPB * N * BS;            // one transpose buffer
+  static constexpr size_t SMEM = 2 * sizeof(double) * BUF;
+};
+
+// q (+ eps X with the reference's rounding, newton_krylov.py:76) of point pt
+template <bool HASX>
+__device__ __forceinline__ void ld_q(const double* __restrict__ q, const double* __restrict__ X, double eps,
+                                     int64_t pt, double* o) {
+  const double2 a = __ldg(reinterpret_cast<const double2*>(q + pt * 4));
+  const double2 b = __ldg(reinterpret_cast<const double2*>(q + pt * 4) + 1);
+  o[0] = a.x;
+  o[1] = a.y;
+  o[2] = b.x;
+  o[3] = b.y;
+  if constexpr (HASX) {
+    const double2 c = __ldg(reinterpret_cast<const double2*>(X + pt * 4));
+    const double2 d = __ldg(reinterpret_cast<const double2*>(X + pt * 4) + 1);
+    o[0] = __dadd_rn(o[0], __dmul_rn(eps, c.x));
+    o[1] = __dadd_rn(o[1], __dmul_rn(eps, c.y));
+    o[2] = __dadd_rn(o[2], __dmul_rn(eps, d.x));
+    o[3] = __dadd_rn(o[3], __dmul_rn(eps, d.y));
+  }
+}
+
+// primitive variables of one state, exactly as prim() (spatial.py:94-101)
+struct Pr {
+  double r, ir, u, v, p;
+};
+__device__ __forceinline__ Pr prim_of(const double* q, double g) {
+  Pr s;
+  prim(q, g, s.r, s.ir, s.u, s.v, s.p);
+  return s;
+}
+
+// Roe flux from precomputed primitives: the same expressions as roe()
+// (spatial.py:113-163), so the result is bitwise roe(qL, qR, ...)
+__device__ __forceinline__ void roe_pr(const double* qL, const Pr& L, const double* qR, const Pr& R, double nx,
+                                       double ny, double g, double* F) {
+  const double EpL = qL[3] + L.p, EpR = qR[3] + R.p;
+  const double HL = EpL * L.ir;
+  const double HR = EpR * R.ir;
+  const double sL = fsqrt(L.r), sR = fsqrt(R.r);
+  const double w = sL * rcp(sL + sR), w1 = 1.0 - w;
+  const double u = w * L.u + w1 * R.u;
+  const double v = w * L.v + w1 * R.v;
+  const double H = w * HL + w1 * HR;
+  const double ke = 0.5 * (u * u + v * v);
+  const double c2 = (g - 1.0) * (H - ke);
+  const double c = fsqrt(c2);
+  const double ic2 = rcp(c2);
+  const double rb = sL * sR;
+  const double un = u * nx + v * ny;
+  const double du = R.u - L.u, dv = R.v - L.v;
+  const double dn = du * nx + dv * ny;
+  const double dtg = -du * ny + dv * nx;
+  const double dp = R.p - L.p;
+  const double k1 = fabs(un - c) * ((dp - rb * c * dn) * (0.5 * ic2));
+  const double k2 = fabs(un) * ((R.r - L.r) - dp * ic2);
+  const double k3 = fabs(un) * (rb * dtg);
+  const double k4 = fabs(un + c) * ((dp + rb * c * dn) * (0.5 * ic2));
+  const double ut = -u * ny + v * nx;
+  const double d0 = k1 + k2 + k4;
+  const double d1 = k1 * (u - c * nx) + k2 * u - k3 * ny + k4 * (u + c * nx);
+  const double d2 = k1 * (v - c * ny) + k2 * v + k3 * nx + k4 * (v + c * ny);
+  const double d3 = k1 * (H - c * un) + k2 * ke + k3 * ut + k4 * (H + c * un);
+  const double qnL = L.u * nx + L.v * ny, qnR = R.u * nx + R.v * ny;
+  F[0] = 0.5 * (qL[0] * qnL + qR[0] * qnR) - 0.5 * d0;
+  F[1] = 0.5 * ((qL[1] * qnL + L.p * nx) + (qR[1] * qnR + R.p * nx)) - 0.5 * d1;
+  F[2] = 0.5 * ((qL[2] * qnL + L.p * ny) + (qR[2] * qnR + R.p * ny)) - 0.5 * d2;
+  F[3] = 0.5 * (EpL * qnL + EpR * qnR) - 0.5 * d3;
+}
+
+// Rusanov from primitives: the same expressions as rusanov()
+__device__ __forceinline__ void rusanov_pr(const double* qL, const Pr& L, const double* qR, const Pr& R, double nx,
+                                           double ny, double g, double* F) {
+  const double qnL = L.u * nx + L.v * ny, qnR = R.u * nx + R.v * ny;
+  const double lam = fmax(fabs(qnL) + fsqrt(g * L.p * L.ir), fabs(qnR) + fsqrt(g * R.p * R.ir));
+  const double hl = 0.5 * lam;
+  F[0] = 0.5 * (qL[0] * qnL + qR[0] * qnR) - hl * (qR[0] - qL[0]);
+  F[1] = 0.5 * ((qL[1] * qnL + L.p * nx) + (qR[1] * qnR + R.p * nx)) - hl * (qR[1] - qL[1]);
+  F[2] = 0.5 * ((qL[2] * qnL + L.p * ny) + (qR[2] * qnR + R.p * ny)) - hl * (qR[2] - qL[2]);
+  F[3] = 0.5 * ((qL[3] + L.p) * qnL + (qR[3] + R.p) * qnR) - hl * (qR[3] - qL[3]);
+}
+
+// trace of q (+ eps X) on face f at face point k: line sum over the line
+// through that point in line_sum's order (i = 0..N-1 along the line)
+// chk: also report whether every point of the line is physical (Euler
+// kinds, which have no k_rgrad to check the states)
+template <int P, bool HASX>
+__device__ __forceinline__ void face_trace(const FrConst& C, const double* __restrict__ q,
+                                           const double* __restrict__ X, double eps, int64_t e, int f, int k,
+                                           double* tr, bool chk = false, bool* ok = nullptr) {
+  constexpr int N = P + 1, NP = N * N;
+  const bool col = (f == 0 || f == 2);
+  const int kk = (f >= 2) ? N - 1 - k : k;   // the row / column index
+  const int start = col ? kk : kk * N;
+  const int step = col ? N : 1;
+  const double* w = (f == 1 || f == 2) ? C.eR : C.eL;
+  tr[0] = tr[1] = tr[2] = tr[3] = 0.0;
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    double x[4];
+    ld_q<HASX>(q, X, eps, e * NP + start + i * step, x);
+    if (chk) *ok = *ok && physical(x, C.gamma);
+    const double wi = w[i];
+#pragma unroll
+    for (int v = 0; v < 4; ++v) tr[v] += wi * x[v];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_rface: traces, interface flux and BR1 common value, once per face point
+
+template <int P, int KIND, bool HASX>
+__global__ void __launch_bounds__(128) k_rface(const FrConst C, const RectMesh m, const double* __restrict__ q,
+                                               const double* __restrict__ X, double eps, double* __restrict__ fw,
+                                               int* __restrict__ bad) {
+  constexpr int N = P + 1;
+  constexpr bool VISC = KT<KIND>::VISC;
+  pdl_trigger();
+  const int64_t t = (int64_t)blockIdx.x * 128 + threadIdx.x;
+  if (t >= m.nface * N) return;
+  const int64_t phi = t / N;
+  const int k = (int)(t - phi * N);
+  const int4 fr = __ldg(m.faces + phi);
+  const int fL = fr.y & 3, rev = (fr.y >> 2) & 1, bnd = (fr.y >> 3) & 1, tag = (fr.y >> 4) & 15;
+  const double2 nrm = __ldg(reinterpret_cast<const double2*>(m.geom + (int64_t)fr.x * 20 + 8 + 2 * fL));
+  const double g = C.gamma;
+  const Phys ph = phys_of(C);
+  double qa[4], qc[4];
+  // Euler: the states are checked here, on the rows of each element's face 1
+  bool okL = true, okR = true;
+  const bool chk = !VISC && bad != nullptr;
+  face_trace<P, HASX>(C, q, X, eps, fr.x, fL, k, qa, chk && fL == 1, &okL);
+  if (bnd)
+    ghost<KIND>(qa, tag, nrm.x, nrm.y, C.qinf, qc);
+  else
+    face_trace<P, HASX>(C, q, X, eps, fr.z, fr.w, rev ? N - 1 - k : k, qc, chk && fr.w == 1, &okR);
+  if (!okL) atomicMin(bad, fr.x);
+  if (!okR) atomicMin(bad, fr.z);
+  const Pr A = prim_of(qa, g), B = prim_of(qc, g);
+  if (bad != nullptr) {
+    if (!(A.r > 0.0 && A.p > 0.0)) atomicMin(bad + 1, fr.x);
+    if (!bnd && !(B.r > 0.0 && B.p > 0.0)) atomicMin(bad + 1, fr.z);
+  }
+  double F[4];
+  if (ph.riemann)
+    rusanov_pr(qa, A, qc, B, nrm.x, nrm.y, g, F);
+  else
+    roe_pr(qa, A, qc, B, nrm.x, nrm.y, g, F);
+  double2* o = reinterpret_cast<double2*>(fw + t * 8);
+  o[0] = make_double2(F[0], F[1]);
+  o[1] = make_double2(F[2], F[3]);
+  if constexpr (VISC) {
+    double wa[3] = {A.u, A.v, A.p * A.ir}, wc[3] = {B.u, B.v, B.p * B.ir};
+    if (bnd) ghost_w<KIND>(ph, tag, wa, wc);
+    double wh[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) wh[c] = common_w(ph, !bnd, true, wa[c], wc[c]);
+    o[2] = make_double2(wh[0], wh[1]);
+    o[3] = make_double2(wh[2], 0.0);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// shared by k_rgrad and k_rasm
+
+// face point (f, k) of element e: index of its record in fw (L side order)
+// and whether e is that face's L side (or a boundary face's only side)
+struct FaceRef {
+  int64_t rec;   // (phi * N + kL) * 8
+  bool left, inter;
+  int2 lk;
+};
+template <int N>
+__device__ __forceinline__ FaceRef face_ref(const RectMesh& m, int64_t e, int f, int k) {
+  FaceRef r;
+  r.lk = __ldg(m.link + e * 4 + f);
+  r.inter = r.lk.x >= 0;
+  r.left = !r.inter || lk_left(r.lk.y);
+  const int kL = (!r.left && lk_rev(r.lk.y)) ? N - 1 - k : k;
+  r.rec = ((int64_t)__ldg(m.fslot + e * 4 + f) * N + kL) * 8;
+  return r;
+}
+
+__device__ __forceinline__ void ld_what(const double* __restrict__ fw, int64_t rec, double* wh) {
+  const double2 a = __ldg(reinterpret_cast<const double2*>(fw + rec + 4));
+  wh[0] = a.x;
+  wh[1] = a.y;
+  wh[2] = __ldg(fw + rec + 6);
+}
+
+// BR1 gradient along one line (row: gx with ia; column: gy with id) from
+// the line's viscous variables w[c][i] and the common values at its two
+// ends: wp on the +1 end (eR, lR), wm on the -1 end (eL, lL)
+template <int N>
+__device__ __forceinline__ void line_gradient(const FrConst& C, const double (&w)[3][N], const double* wp,
+                                              const double* wm, double s, double (&gr)[3][N]) {
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    double tp = 0.0, tm = 0.0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      tp += C.eR[i] * w[c][i];
+      tm += C.eL[i] * w[c][i];
+    }
+    const double cp = wp[c] - tp, cm = wm[c] - tm;
+#pragma unroll
+    for (int b = 0; b < N; ++b) {
+      double d = 0.0;
+#pragma unroll
+      for (int i = 0; i < N; ++i) d += C.D[b * N + i] * w[c][i];
+      gr[c][b] = s * ((d + C.lR[b] * cp) - C.lL[b] * cm);
+    }
+  }
+}
+
+// x-row (fx) / y-row (fy) of the viscous flux at one state, exactly the
+// corresponding components of visc_flux() (spatial.py:166-180)
+__device__ __forceinline__ void visc_fx(const double* q, const double* gx, const double* gy, const Phys& ph,
+                                        double* fx) {
+  const double ir = rcp(q[0]);
+  const double u = q[1] * ir, v = q[2] * ir;
+  const double d = gx[0] + gy[1];
+  const double txx = ph.mu * (2.0 * gx[0] - (2.0 / 3.0) * d);
+  const double txy = ph.mu * (gy[0] + gx[1]);
+  fx[0] = 0.0;
+  fx[1] = txx;
+  fx[2] = txy;
+  fx[3] = u * txx + v * txy + ph.kappa * gx[2];
+}
+__device__ __forceinline__ void visc_fy(const double* q, const double* gx, const double* gy, const Phys& ph,
+                                        double* fy) {
+  const double ir = rcp(q[0]);
+  const double u = q[1] * ir, v = q[2] * ir;
+  const double d = gx[0] + gy[1];
+  const double tyy = ph.mu * (2.0 * gy[1] - (2.0 / 3.0) * d);
+  const double txy = ph.mu * (gy[0] + gx[1]);
+  fy[0] = 0.0;
+  fy[1] = txy;
+  fy[2] = tyy;
+  fy[3] = u * txy + v * tyy + ph.kappa * gy[2];
+}
+
+__device__ __forceinline__ void ld4(const double* __restrict__ src, double* o) {
+  const double2 a = __ldg(reinterpret_cast<const double2*>(src));
+  const double2 b = __ldg(reinterpret_cast<const double2*>(src) + 1);
+  o[0] = a.x;
+  o[1] = a.y;
+  o[2] = b.x;
+  o[3] = b.y;
+}
+
+__device__ __forceinline__ void st4(double* dst, const double* v) {
+  reinterpret_cast<double2*>(dst)[0] = make_double2(v[0], v[1]);
+  reinterpret_cast<double2*>(dst)[1] = make_double2(v[2], v[3]);
+}
+
+// ---------------------------------------------------------------------------
+// k_rgrad: BR1 gradients, their face traces, one-sided viscous fluxes
+
+template <int P, bool HASX>
+__global__ void __launch_bounds__(RC<P>::TH, 4)
+k_rgrad(const FrConst C, const RectMesh m, const double* __restrict__ q, const double* __restrict__ X, double eps,
+        const double* __restrict__ fw, double* __restrict__ fvn, int* __restrict__ bad) {
+  using R = RC<P>;
+  constexpr int N = R::N, NP = R::NP, E = R::EPB, BS = R::BS;
+  extern __shared__ __align__(16) double sm[];
+  double* sX = sm;           // column blocks: W, then gx
+  double* sY = sm + R::BUF;  // row blocks: gy
+  pdl_trigger();
+  const int t = threadIdx.x;
+  const int el = t / N, a = t % N;  // row a of element el; also column a
+  const int64_t e = (int64_t)blockIdx.x * E + el;
+  const bool live = t < E * N && e < m.M;
+  const Phys ph = phys_of(C);
+  const double g = C.gamma;
+  // rows: q, primitives, W; the row's q traces on faces 1 and 3
+  double w[3][N];
+  double t1q[4] = {0, 0, 0, 0}, t3q[4] = {0, 0, 0, 0};
+  double2 rg = make_double2(0.0, 0.0);
+  if (live) {
+    rg = __ldg(m.rgeo + e);
+    bool ok = true;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      double x[4];
+      ld_q<HASX>(q, X, eps, e * NP + a * N + i, x);
+      const Pr s = prim_of(x, g);
+      ok = ok && (s.r > 0.0) && (s.p > 0.0);
+      w[0][i] = s.u;
+      w[1][i] = s.v;
+      w[2][i] = s.p * s.ir;
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        t1q[v] += C.eR[i] * x[v];
+        t3q[v] += C.eL[i] * x[v];
+      }
+    }
+    if (!ok && bad != nullptr) atomicMin(bad, (int)e);
+  } else {
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int i = 0; i < N; ++i) w[c][i] = 1.0;
+  }
+  // W into column blocks: block (el, i) holds column i, [c][row]
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) sX[(el * N + i) * BS + c * N + a] = w[c][i];
+  pdl_wait();  // fw (k_rface)
+  // faces 1 (point a) and 3 (point N-1-a): common values, then gx along the row
+  double gx[3][N];
+  FaceRef f1{}, f3{};
+  double wh1[3] = {0, 0, 0}, wh3[3] = {0, 0, 0};
+  if (live) {
+    f1 = face_ref<N>(m, e, 1, a);
+    f3 = face_ref<N>(m, e, 3, N - 1 - a);
+    ld_what(fw, f1.rec, wh1);
+    ld_what(fw, f3.rec, wh3);
+  }
+  line_gradient<N>(C, w, wh1, wh3, rg.x, gx);
+  __syncthreads();
+  // columns: W of column a, common values on faces 0 (point a) and 2 (point N-1-a), gy
+  double gy[3][N];
+  {
+    const double* blk = sX + t * BS;
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int i = 0; i < N; ++i) w[c][i] = blk[c * N + i];
+  }
+  FaceRef f0{}, f2{};
+  double wh0[3] = {0, 0, 0}, wh2[3] = {0, 0, 0};
+  if (live) {
+    f0 = face_ref<N>(m, e, 0, a);
+    f2 = face_ref<N>(m, e, 2, N - 1 - a);
+    ld_what(fw, f0.rec, wh0);
+    ld_what(fw, f2.rec, wh2);
+  }
+  line_gradient<N>(C, w, wh2, wh0, rg.y, gy);
+  __syncthreads();  // W reads done
+  // gx rows -> column blocks of sX; gy columns -> row blocks of sY
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      sX[(el * N + i) * BS + c * N + a] = gx[c][i];
+      sY[(el * N + i) * BS + c * N + a] = gy[c][i];
+    }
+  // traces of the own-line components: gx on faces 1/3, gy on faces 0/2
+  double tgx1[3], tgx3[3], tgy0[3], tgy2[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    double s1 = 0.0, s3 = 0.0, s0 = 0.0, s2 = 0.0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      s1 += C.eR[i] * gx[c][i];
+      s3 += C.eL[i] * gx[c][i];
+      s2 += C.eR[i] * gy[c][i];
+      s0 += C.eL[i] * gy[c][i];
+    }
+    tgx1[c] = s1;
+    tgx3[c] = s3;
+    tgy2[c] = s2;
+    tgy0[c] = s0;
+  }
+  __syncthreads();
+  if (!live) return;
+  // rows: gy along row a (block (el, a) of sY) -> gy traces on faces 1/3
+  double tgy1[2], tgy3[2], tgx0[2], tgx2[2];
+  {
+    const double* blk = sY + t * BS;
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      double s1 = 0.0, s3 = 0.0;
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        const double y = blk[c * N + i];
+        s1 += C.eR[i] * y;
+        s3 += C.eL[i] * y;
+      }
+      tgy1[c] = s1;
+      tgy3[c] = s3;
+    }
+    const double* bx = sX + t * BS;
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      double s0 = 0.0, s2 = 0.0;
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        const double x = bx[c * N + i];
+        s2 += C.eR[i] * x;
+        s0 += C.eL[i] * x;
+      }
+      tgx2[c] = s2;
+      tgx0[c] = s0;
+    }
+  }
+  // q traces on faces 0 (point a) and 2 (point N-1-a) from column a
+  double t0q[4] = {0, 0, 0, 0}, t2q[4] = {0, 0, 0, 0};
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    double x[4];
+    ld_q<HASX>(q, X, eps, e * NP + i * N + a, x);
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      t2q[v] += C.eR[i] * x[v];
+      t0q[v] += C.eL[i] * x[v];
+    }
+  }
+  // one-sided viscous normal fluxes (spatial.py:456-464): face 1 +fx,
+  // face 3 -fx, face 2 +fy, face 0 -fy
+  double o[4];
+  {
+    const double gyv[2] = {tgy1[0], tgy1[1]};
+    visc_fx(t1q, tgx1, gyv, ph, o);
+    st4(fvn + ((e * 4 + 1) * N + a) * 4, o);
+  }
+  {
+    const double gyv[2] = {tgy3[0], tgy3[1]};
+    visc_fx(t3q, tgx3, gyv, ph, o);
+    o[1] = -o[1], o[2] = -o[2], o[3] = -o[3];
+    st4(fvn + ((e * 4 + 3) * N + (N - 1 - a)) * 4, o);
+  }
+  {
+    const double gxv[2] = {tgx2[0], tgx2[1]};
+    visc_fy(t2q, gxv, tgy2, ph, o);
+    st4(fvn + ((e * 4 + 2) * N + (N - 1 - a)) * 4, o);
+  }
+  {
+    const double gxv[2] = {tgx0[0], tgx0[1]};
+    visc_fy(t0q, gxv, tgy0, ph, o);
+    o[1] = -o[1], o[2] = -o[2], o[3] = -o[3];
+    st4(fvn + ((e * 4 + 0) * N + a) * 4, o);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_rasm: common fluxes, point fluxes, FR divergence, fused epilogue
+
+// common total normal flux on own face point: +-F (interface flux on L's
+// normal) minus the common viscous flux (spatial.py:559-568)
+template <int N, bool VISC>
+__device__ __forceinline__ void common_flux(const RectMesh& m, const double* __restrict__ fw,
+                                            const double* __restrict__ fvn, const Phys& ph, const FaceRef& r,
+                                            int64_t e, int f, int k, double* Fc) {
+  const double2 a = __ldg(reinterpret_cast<const double2*>(fw + r.rec));
+  const double2 b = __ldg(reinterpret_cast<const double2*>(fw + r.rec) + 1);
+  double F[4] = {a.x, a.y, b.x, b.y};
+#pragma unroll
+  for (int v = 0; v < 4; ++v) F[v] = r.left ? F[v] : -F[v];
+  if constexpr (VISC) {
+    double Fo[4], Fn[4];
+    ld4(fvn + ((e * 4 + f) * N + k) * 4, Fo);
+    if (r.inter) {
+      const int kk = lk_rev(r.lk.y) ? N - 1 - k : k;
+      ld4(fvn + (((int64_t)r.lk.x * 4 + lk_face(r.lk.y)) * N + kk) * 4, Fn);
+    } else {
+#pragma unroll
+      for (int v = 0; v < 4; ++v) Fn[v] = Fo[v];
+    }
+    double Fv[4];
+#pragma unroll
+    for (int v = 0; v < 4; ++v) Fv[v] = common_fv(ph, r.inter, r.left, Fo[v], Fn[v]);
+    if (!r.inter && lk_tag(r.lk.y) == T_WALL_ADIABATIC) Fv[3] = 0.0;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) F[v] = F[v] - Fv[v];
+  }
+#pragma unroll
+  for (int v = 0; v < 4; ++v) Fc[v] = F[v];
+}
+
+// divergence along one line of a 4-variable flux x[v][i]: the +1 end takes
+// (Fp - trace), the -1 end (-Fm - trace)  (the reference's c1/c3, c2/c0)
+template <int N>
+__device__ __forceinline__ void line_div(const FrConst& C, const double (&x)[4][N], const double* Fp,
+                                         const double* Fm, double (&out)[4][N]) {
+#pragma unroll
+  for (int v = 0; v < 4; ++v) {
+    double tp = 0.0, tm = 0.0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      tp += C.eR[i] * x[v][i];
+      tm += C.eL[i] * x[v][i];
+    }
+    const double cp = Fp[v] - tp, cm = -Fm[v] - tm;
+#pragma unroll
+    for (int b = 0; b < N; ++b) {
+      double d = 0.0;
+#pragma unroll
+      for (int i = 0; i < N; ++i) d += C.D[b * N + i] * x[v][i];
+      out[v][b] = (d + C.lR[b] * cp) - C.lL[b] * cm;
+    }
+  }
+}
+
+template <int P, int KIND, int EK, bool HASX>
+__global__ void __launch_bounds__(RC<P>::TH, 4)
+k_rasm(const FrConst C, const RectMesh m, const double* __restrict__ q, const double* __restrict__ X, double eps,
+       const double* __restrict__ fw, const double* __restrict__ fvn, const Epi ep, double* __restrict__ out,
+       int* bad, Status* st) {
+  using R = RC<P>;
+  constexpr int N = R::N, NP = R::NP, E = R::EPB, BS = R::BS;
+  constexpr bool VISC = KT<KIND>::VISC;
+  extern __shared__ __align__(16) double sm[];
+  double* sX = sm;           // column blocks: W, then fy
+  double* sY = sm + R::BUF;  // row blocks gy, then column blocks X_xi
+  const int t = threadIdx.x;
+  const int el = t / N, a = t % N;
+  const int64_t e = (int64_t)blockIdx.x * E + el;
+  const bool live = t < E * N && e < m.M;
+  const Phys ph = phys_of(C);
+  const double g = C.gamma;
+  // row a: q (an input: read before the dependency wait); its viscous
+  // variables into column blocks for the column pass
+  double qr[4][N];
+  double2 rg = make_double2(1.0, 1.0);
+  if (live) {
+    rg = __ldg(m.rgeo + e);
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      double x[4];
+      ld_q<HASX>(q, X, eps, e * NP + a * N + i, x);
+#pragma unroll
+      for (int v = 0; v < 4; ++v) qr[v][i] = x[v];
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < N; ++i) qr[0][i] = qr[3][i] = 1.0, qr[1][i] = qr[2][i] = 0.0;
+  }
+  if constexpr (VISC) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const double x[4] = {qr[0][i], qr[1][i], qr[2][i], qr[3][i]};
+      const Pr s = prim_of(x, g);
+      sX[(el * N + i) * BS + 0 * N + a] = s.u;
+      sX[(el * N + i) * BS + 1 * N + a] = s.v;
+      sX[(el * N + i) * BS + 2 * N + a] = s.p * s.ir;
+    }
+  }
+  pdl_wait();  // fw (k_rface), fvn (k_rgrad), status flags
+  if (blockIdx.x == 0 && threadIdx.x == 0) commit_status(bad, st);
+  double gy[3][N];
+  if constexpr (VISC) {
+    __syncthreads();
+    // column a: gy -> row blocks
+    {
+      double w[3][N];
+      const double* blk = sX + t * BS;
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int i = 0; i < N; ++i) w[c][i] = blk[c * N + i];
+      double wp[3] = {0, 0, 0}, wm[3] = {0, 0, 0};
+      if (live) {
+        ld_what(fw, face_ref<N>(m, e, 2, N - 1 - a).rec, wp);
+        ld_what(fw, face_ref<N>(m, e, 0, a).rec, wm);
+      }
+      double gc[3][N];
+      line_gradient<N>(C, w, wp, wm, rg.y, gc);
+#pragma unroll
+      for (int i = 0; i < N; ++i)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) sY[(el * N + i) * BS + c * N + a] = gc[c][i];
+    }
+    __syncthreads();
+    const double* blk = sY + t * BS;
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int i = 0; i < N; ++i) gy[c][i] = blk[c * N + i];
+  }
+  // row a: primitives (again: cheaper than holding them through the column
+  // pass), gx, point fluxes -- fx stays in registers, fy -> column blocks
+  Pr pr[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    const double x[4] = {qr[0][i], qr[1][i], qr[2][i], qr[3][i]};
+    pr[i] = prim_of(x, g);
+  }
+  double gx[3][N];
+  if constexpr (VISC) {
+    double w[3][N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      w[0][i] = pr[i].u;
+      w[1][i] = pr[i].v;
+      w[2][i] = pr[i].p * pr[i].ir;
+    }
+    double wp[3] = {0, 0, 0}, wm[3] = {0, 0, 0};
+    if (live) {
+      ld_what(fw, face_ref<N>(m, e, 1, a).rec, wp);
+      ld_what(fw, face_ref<N>(m, e, 3, N - 1 - a).rec, wm);
+    }
+    line_gradient<N>(C, w, wp, wm, rg.x, gx);
+  }
+  double fx[4][N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    const Pr& s = pr[i];
+    double Fx[4], Fy[4];
+    Fx[0] = qr[1][i];
+    Fx[1] = qr[1][i] * s.u + s.p;
+    Fx[2] = qr[1][i] * s.v;
+    Fx[3] = s.u * (qr[3][i] + s.p);
+    Fy[0] = qr[2][i];
+    Fy[1] = qr[2][i] * s.u;
+    Fy[2] = qr[2][i] * s.v + s.p;
+    Fy[3] = s.v * (qr[3][i] + s.p);
+    if constexpr (VISC) {
+      const double gxx[3] = {gx[0][i], gx[1][i], gx[2][i]};
+      const double gyy[3] = {gy[0][i], gy[1][i], gy[2][i]};
+      const double d = gxx[0] + gyy[1];
+      const double txx = ph.mu * (2.0 * gxx[0] - (2.0 / 3.0) * d);
+      const double tyy = ph.mu * (2.0 * gyy[1] - (2.0 / 3.0) * d);
+      const double txy = ph.mu * (gyy[0] + gxx[1]);
+      Fx[1] = Fx[1] - txx;
+      Fx[2] = Fx[2] - txy;
+      Fx[3] = Fx[3] - (s.u * txx + s.v * txy + ph.kappa * gxx[2]);
+      Fy[1] = Fy[1] - txy;
+      Fy[2] = Fy[2] - tyy;
+      Fy[3] = Fy[3] - (s.u * txy + s.v * tyy + ph.kappa * gyy[2]);
+      Fx[0] = Fx[0] - 0.0;
+      Fy[0] = Fy[0] - 0.0;
+    }
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      fx[v][i] = Fx[v];
+      sX[(el * N + i) * BS + v * N + a] = Fy[v];
+    }
+  }
+  // X_xi along row a
+  double Fc1[4] = {0, 0, 0, 0}, Fc3[4] = {0, 0, 0, 0};
+  if (live) {
+    common_flux<N, VISC>(m, fw, fvn, ph, face_ref<N>(m, e, 1, a), e, 1, a, Fc1);
+    common_flux<N, VISC>(m, fw, fvn, ph, face_ref<N>(m, e, 3, N - 1 - a), e, 3, N - 1 - a, Fc3);
+  }
+  double xx[4][N];
+  line_div<N>(C, fx, Fc1, Fc3, xx);
+  if constexpr (VISC) __syncthreads();  // gy row reads of sY done
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) sY[(el * N + i) * BS + v * N + a] = xx[v][i];
+  __syncthreads();
+  if (!live) return;
+  // column a: fy and X_xi of the column, faces 0 / 2, X_eta, R, epilogue
+  double fc[4][N];
+  {
+    const double* blk = sX + t * BS;
+#pragma unroll
+    for (int v = 0; v < 4; ++v)
+#pragma unroll
+      for (int i = 0; i < N; ++i) fc[v][i] = blk[v * N + i];
+  }
+  double Fc0[4], Fc2[4];
+  common_flux<N, VISC>(m, fw, fvn, ph, face_ref<N>(m, e, 0, a), e, 0, a, Fc0);
+  common_flux<N, VISC>(m, fw, fvn, ph, face_ref<N>(m, e, 2, N - 1 - a), e, 2, N - 1 - a, Fc2);
+  double xe[4][N];
+  line_div<N>(C, fc, Fc2, Fc0, xe);
+  const double* bx = sY + t * BS;
+  constexpr bool NEEDQ = !(EK == EPI_R || EK == EPI_JV || EK == EPI_NEG_R);
+  const double ce = (EK == EPI_RK) ? epi_rk_coef(ep, e) : 0.0;
+#pragma unroll
+  for (int i = 0; i < N; ++i) {   // point (i, a)
+    const int64_t pt = e * NP + i * N + a;
+    double qv[4] = {0, 0, 0, 0};
+    if constexpr (NEEDQ) ld_q<HASX>(q, X, eps, pt, qv);
+    double o[4];
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const double Rv = -(rg.x * bx[v * N + i] + rg.y * xe[v][i]);
+      if constexpr (EK == EPI_R) {
+        o[v] = Rv;
+      } else {
+        double o1, o2, o3;
+        epi_load_k<EK>(ep, pt * 4 + v, o1, o2, o3);
+        o[v] = (EK == EPI_RK) ? epi_rk(ep, ce, Rv, qv[v], o1, o2, o3) : epi_pre_k<EK>(ep, Rv, qv[v], o1, o2, o3);
+      }
+    }
+    st4(out + pt * 4, o);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+
+template <typename... KArgs, typename... Args>
+static void launch_pdl_r(void (*kernel)(KArgs...), unsigned grid, int threads, size_t smem, cudaStream_t st,
+                         Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
+using RasmFn = void (*)(const FrConst, const RectMesh, const double*, const double*, double, const double*,
+                        const double*, const Epi, double*, int*, Status*);
+
+template <int P, int KIND, bool HASX>
+static RasmFn rasm_for(int mode) {
+  switch (mode) {
+    case EPI_R: return k_rasm<P, KIND, EPI_R, HASX>;
+    case EPI_JV: return k_rasm<P, KIND, EPI_JV, HASX>;
+    case EPI_STAGE_JV: return k_rasm<P, KIND, EPI_STAGE_JV, HASX>;
+    case EPI_DEFECT: return k_rasm<P, KIND, EPI_DEFECT, HASX>;
+    case EPI_F: return k_rasm<P, KIND, EPI_F, HASX>;
+    case EPI_RK: return k_rasm<P, KIND, EPI_RK, HASX>;
+  }
+  return k_rasm<P, KIND, -1, HASX>;
+}
+
+template <int P, int KIND, bool HASX>
+static void set_rect_attrs() {
+  using R = RC<P>;
+  for (int md : {(int)EPI_R, (int)EPI_JV, (int)EPI_STAGE_JV, (int)EPI_DEFECT, (int)EPI_F, (int)EPI_RK, -1})
+    cudaFuncSetAttribute(rasm_for<P, KIND, HASX>(md), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)R::SMEM);
+  if constexpr (KT<KIND>::VISC)
+    cudaFuncSetAttribute(k_rgrad<P, HASX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)R::SMEM);
+}
+
+template <int P, int KIND>
+static int run_rect(const RectDev& rd, const DiscDev& d, const double* q, const double* X, double eps,
+                    const Epi& epi, double* out, int* bad, Status* stp, cudaStream_t st) {
+  using R = RC<P>;
+  static std::atomic<unsigned long long> attr_seen{0};
+  once_per_device(attr_seen, [&] {
+    set_rect_attrs<P, KIND, false>();
+    set_rect_attrs<P, KIND, true>();
+  });
+  const RectMesh m{d.M, rd.nface, rd.faces, rd.fslot, d.link, rd.rgeo, d.geom};
+  const unsigned gf = (unsigned)((rd.nface * (P + 1) + 127) / 128);
+  const unsigned ge = (unsigned)((d.M + R::EPB - 1) / R::EPB);
+  const bool hx = X != nullptr;
+  if (hx)
+    k_rface<P, KIND, true><<<gf, 128, 0, st>>>(d.C, m, q, X, eps, rd.fw, bad);
+  else
+    k_rface<P, KIND, false><<<gf, 128, 0, st>>>(d.C, m, q, X, eps, rd.fw, bad);
+  if constexpr (KT<KIND>::VISC) {
+    if (hx)
+      launch_pdl_r(k_rgrad<P, true>, ge, R::TH, R::SMEM, st, d.C, m, q, X, eps, (const double*)rd.fw, d.fvn, bad);
+    else
+      launch_pdl_r(k_rgrad<P, false>, ge, R::TH, R::SMEM, st, d.C, m, q, X, eps, (const double*)rd.fw, d.fvn, bad);
+  }
+  RasmFn fn = hx ? rasm_for<P, KIND, true>(epi.mode) : rasm_for<P, KIND, false>(epi.mode);
+  launch_pdl_r(fn, ge, R::TH, R::SMEM, st, d.C, m, q, X, eps, (const double*)rd.fw, (const double*)d.fvn, epi, out,
+               bad, stp);
+  return (int)cudaGetLastError();
+}
+
+int launch_residual_rect(const RectDev& rd, const DiscDev& d, const double* q, const double* X, double eps,
+                         const Epi& epi, double* out, int* bad, Status* stp, cudaStream_t st) {
+  switch (d.kind * 8 + d.p) {
+    case K_EULER * 8 + 1: return run_rect<1, K_EULER>(rd, d, q, X, eps, epi, out, bad, stp, st);
+    case K_EULER * 8 + 2: return run_rect<2, K_EULER>(rd, d, q, X, eps, epi, out, bad, stp, st);
+    case K_EULER * 8 + 3: return run_rect<3, K_EULER>(rd, d, q, X, eps, epi, out, bad, stp, st);
+    case K_EULER * 8 + 4: return run_rect<4, K_EULER>(rd, d, q, X, eps, epi, out, bad, stp, st);
+    case K_EULER * 8 + 5: return run_rect<5, K_EULER>(rd, d, q, X, eps, epi, out, bad, stp, st);
+    case K_NS * 8 + 1: return run_rect<1, K_NS>(rd, d, q, X, eps, epi, out, bad, stp, st);
+    case K_NS * 8 + 2: return run_rect<2, K_NS>(rd, d, q, X, eps, epi, out, bad, stp, st);
+    case K_NS * 8 + 3: return run_rect<3, K_NS>(rd, d, q, X, eps, epi, out, bad, stp, st);
+    case K_NS * 8 + 4: return run_rect<4, K_NS>(rd, d, q, X, eps, epi, out, bad, stp, st);
+    case K_NS * 8 + 5: return run_rect<5, K_NS>(rd, d, q, X, eps, epi, out, bad, stp, st);
+  }
+  return -1000;
+}
+
+bool rect_supported(int p, int kind) { return p >= 1 && p <= 5 && (kind == K_EULER || kind == K_NS); }
+
+}  // namespace pmgb

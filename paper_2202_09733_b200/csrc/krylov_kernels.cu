@@ -10,6 +10,8 @@
 // are bitwise reproducible run to run -- the reference's residual logs
 // are bitwise deterministic (tests/test_acceptance.py:472-501).
 #include <cstdlib>
+#include <map>
+#include <mutex>
 
 #include "pmgb_internal.cuh"
 
@@ -24,20 +26,38 @@ struct RedScratch {
   int* flag;                // 1
 };
 
-static RedScratch g_red = {nullptr, nullptr, nullptr};
+// One scratch per (device, stream): a reduction's partials, its arrival
+// counter and the finite flag are only ever touched by work queued on one
+// stream, so reductions on different streams or devices never share them
+// (reductions on one stream are ordered by the stream itself).
+struct RedKey {
+  int dev;
+  cudaStream_t st;
+  bool operator<(const RedKey& o) const { return dev != o.dev ? dev < o.dev : st < o.st; }
+};
+static std::mutex g_red_mu;
+static std::map<RedKey, RedScratch> g_red;
 
-static int red_scratch(RedScratch* out) {
-  if (g_red.partial == nullptr) {
+static int red_scratch(RedScratch* out, cudaStream_t st) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return (int)e;
+  std::lock_guard<std::mutex> lock(g_red_mu);
+  auto it = g_red.find(RedKey{dev, st});
+  if (it == g_red.end()) {
     void* p = nullptr;
-    cudaError_t e = cudaMalloc(&p, sizeof(double) * RED_BLOCKS + 64);
+    e = cudaMalloc(&p, sizeof(double) * RED_BLOCKS + 64);
     if (e != cudaSuccess) return (int)e;
-    cudaMemset(p, 0, sizeof(double) * RED_BLOCKS + 64);
-    g_red.partial = (double*)p;
-    g_red.counter = (unsigned int*)((char*)p + sizeof(double) * RED_BLOCKS);
-    g_red.flag = (int*)((char*)p + sizeof(double) * RED_BLOCKS + 16);
-    cudaDeviceSynchronize();
+    e = cudaMemset(p, 0, sizeof(double) * RED_BLOCKS + 64);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();  // zeroed before any stream uses it
+    if (e != cudaSuccess) return (int)e;
+    RedScratch rs;
+    rs.partial = (double*)p;
+    rs.counter = (unsigned int*)((char*)p + sizeof(double) * RED_BLOCKS);
+    rs.flag = (int*)((char*)p + sizeof(double) * RED_BLOCKS + 16);
+    it = g_red.emplace(RedKey{dev, st}, rs).first;
   }
-  *out = g_red;
+  *out = it->second;
   return 0;
 }
 
@@ -220,10 +240,13 @@ __global__ void k_lincomb(int64_t n, const Lin L, double* __restrict__ out) {
 }
 
 // out = V^T y with y on the device (x += P(V[:j].T @ y))
+// (y staged in dynamic shared memory: any Krylov dimension up to
+// GEMV_T_MAX_K, same summation order for every k)
+constexpr int GEMV_T_MAX_K = 227 * 1024 / 8 - 64;
 __global__ void k_gemv_t(int64_t n, int k, const double* __restrict__ V, int64_t ld, const double* y,
                          double* __restrict__ out) {
-  __shared__ double ys[128];
-  for (int j = threadIdx.x; j < k && j < 128; j += blockDim.x) ys[j] = y[j];
+  extern __shared__ double ys[];
+  for (int j = threadIdx.x; j < k; j += blockDim.x) ys[j] = y[j];
   __syncthreads();
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
@@ -250,7 +273,7 @@ static unsigned ew_grid(int64_t n) {
 
 int launch_dot(int64_t n, const double* x, const double* y, double* out, int do_sqrt, cudaStream_t st) {
   RedScratch rs;
-  int e = red_scratch(&rs);
+  int e = red_scratch(&rs, st);
   if (e) return e;
   k_dot<<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, x, y, out, do_sqrt, rs);
   return (int)cudaGetLastError();
@@ -262,7 +285,7 @@ int launch_dot(int64_t n, const double* x, const double* y, double* out, int do_
 int launch_mgs(int64_t n, double* V, int64_t ld, int j, double* w, double* H, double thresh, int* finite_flag,
                cudaStream_t st) {
   RedScratch rs;
-  int e = red_scratch(&rs);
+  int e = red_scratch(&rs, st);
   if (e) return e;
   cudaMemsetAsync(rs.flag, 0, sizeof(int), st);
   for (int i = 0; i <= j; ++i) {
@@ -284,7 +307,7 @@ int launch_mgs(int64_t n, double* V, int64_t ld, int j, double* w, double* H, do
 int launch_mgs_pass(int64_t n, double* w, const double* Vprev, const double* hprev, const double* Vnext,
                     double* out, int first, int* finite_flag, cudaStream_t st) {
   RedScratch rs;
-  int e = red_scratch(&rs);
+  int e = red_scratch(&rs, st);
   if (e) return e;
   if (first) cudaMemsetAsync(rs.flag, 0, sizeof(int), st);
   k_mgs_pass<<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, w, Vprev, hprev, Vnext, out, 0, first, rs);
@@ -328,8 +351,15 @@ int launch_rk_dtau(int64_t M, const double* lam, double s, double cfl, double* d
 }
 
 int launch_gemv_t(int64_t n, int k, const double* V, int64_t ld, const double* y, double* out, cudaStream_t st) {
-  if (k < 1 || k > 128) return -1001;
-  k_gemv_t<<<ew_grid(n), 256, 0, st>>>(n, k, V, ld, y, out);
+  if (k < 1 || k > GEMV_T_MAX_K) return -1001;
+  const size_t smem = sizeof(double) * (size_t)k;
+  if (smem > 48 * 1024) {
+    static std::atomic<unsigned long long> seen{0};
+    once_per_device(seen, [&] {
+      cudaFuncSetAttribute(k_gemv_t, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(double) * GEMV_T_MAX_K));
+    });
+  }
+  k_gemv_t<<<ew_grid(n), 256, smem, st>>>(n, k, V, ld, y, out);
   return (int)cudaGetLastError();
 }
 

@@ -13,16 +13,28 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <mutex>
 
 namespace pmgb {
 
-// Per-device one-time setup (kernel attributes are per device): true the
-// first time it is called for the current device with this flag word.
-inline bool first_use_on_device(std::atomic<unsigned long long>& seen) {
+// Per-device one-time setup (kernel attributes are per device): runs f
+// once for the current device and this flag word.  The bit is published
+// only after f has run, under a lock, so a second host thread never
+// launches before the attributes are set.
+inline std::mutex& setup_mutex() {
+  static std::mutex m;
+  return m;
+}
+template <class F>
+inline void once_per_device(std::atomic<unsigned long long>& seen, F&& f) {
   int dev = 0;
   cudaGetDevice(&dev);
   const unsigned long long bit = 1ull << (dev & 63);
-  return (seen.fetch_or(bit) & bit) == 0;
+  if (seen.load(std::memory_order_acquire) & bit) return;
+  std::lock_guard<std::mutex> lock(setup_mutex());
+  if (seen.load(std::memory_order_acquire) & bit) return;
+  f();
+  seen.fetch_or(bit, std::memory_order_release);
 }
 
 enum Kind { K_EULER = 0, K_NS = 1, K_ADV = 2, K_ADVD = 3 };
@@ -132,6 +144,15 @@ struct Status {
 
 // host-side launch helpers (defined in fr_kernels.cu etc.)
 namespace pmgb {
+// Rectangle fast path (fr_rect.cu): unique-face list and per-face records
+struct RectDev {
+  int64_t nface = 0;
+  int4* faces = nullptr;    // {eL, fL | rev<<2 | bnd<<3 | tag<<4, eR, fR}
+  int* fslot = nullptr;     // (M,4) face index of every element face
+  double2* rgeo = nullptr;  // (M) {1/a0, 1/d0}
+  double* fw = nullptr;     // (nface, n, 8): interface flux F (L normal), BR1 What
+};
+
 struct DiscDev {
   int p, kind;
   int64_t M;
@@ -145,10 +166,15 @@ struct DiscDev {
   double* qp;    // scratch perturbed state
   int nv;
   int64_t n_dofs;
+  int has_rect = 0;  // every element an axis-aligned rectangle (fr_rect.cu)
+  RectDev rect;
 };
 
 int launch_residual(const DiscDev& d, const double* q, const double* X, double eps,
                     const Epi& epi, double* out, cudaStream_t st);
+int launch_residual_rect(const RectDev& rd, const DiscDev& d, const double* q, const double* X, double eps,
+                         const Epi& epi, double* out, int* bad, Status* stp, cudaStream_t st);
+bool rect_supported(int p, int kind);
 size_t fr_grad_scratch_doubles(int p, int kind, int64_t M);
 int launch_rk_lambda(const DiscDev& d, const double* q, double adv, double* lam, cudaStream_t st);
 int launch_freeze(const DiscDev& d, const double* q, double* qtr, double* fvn, cudaStream_t st);

@@ -18,8 +18,9 @@ operation runs in libpmgflow_b200 on device-resident FP64 tensors:
 Non-physical states are latched on the device and raised at the same
 control-flow points the reference raises them (after the enqueued work
 of a residual call is synchronised), so the PTC halving and pMG
-fallback decisions are unchanged.  The block-ILU0 / MBNK machinery
-(:220-371) is outside this round's scope.
+fallback decisions are unchanged.  The MBNK smoother's block-sparse FD
+Jacobian and block ILU0 (:220-371) are built here too
+(``assemble_sparse_blocks``, ``ilu0_factor``, ``ilu0_apply``).
 """
 
 from __future__ import annotations
@@ -64,6 +65,10 @@ class KrylovConfig:
     def __post_init__(self):
         if self.kdim < 1:
             raise ValueError("kdim must be >= 1")
+        # the device update x += P(V^T y) stages y in shared memory
+        # (csrc/krylov_kernels.cu, GEMV_T_MAX_K); reject larger bases up front
+        if self.kdim > 28991:
+            raise ValueError("kdim must be <= 28991")
 
 
 def ser_update(dtau, f_old, f_new, dtau_max, as_printed=False):
@@ -579,11 +584,16 @@ def ptc_solve(F, q0, cfg: PtcConfig, krylov: KrylovConfig, precond_factory=None,
     halvings = 0
     k = 0
     while k < cfg.max_iters:
+        # X = 0 returns 0 without evaluating F (newton_krylov.py:402-404)
         if fused is not None:
             def matvec(X, q=q, Fk=Fk, dtau=dtau):
+                if not any_nonzero(X):
+                    return torch.zeros_like(X)
                 return fused(X, q, Fk, dtau, eps)
         else:
             def matvec(X, q=q, Fk=Fk, dtau=dtau):
+                if not any_nonzero(X):
+                    return torch.zeros_like(X)
                 Fp = F(lincomb((1.0, eps), (q, X)))
                 return lincomb((1.0 / dtau, 1.0 / eps, -1.0 / eps), (X, Fp, Fk))
         try:

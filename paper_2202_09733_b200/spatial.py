@@ -173,6 +173,17 @@ class Discretization:
                 pass
             self._h = None
 
+    def residual_path(self, want: str | None = None) -> str:
+        """Residual kernel family in use: "rect" (axis-aligned rectangles,
+        csrc/fr_rect.cu; chosen automatically when every element
+        qualifies) or "general" (bilinear elements, csrc/fr_kernels.cu).
+        ``want`` switches an eligible context (for A/B runs and tests)."""
+        code = {None: -1, "general": 0, "rect": 1}[want]
+        r = load().pmgb_disc_residual_path(self._h, code)
+        if r < 0:
+            raise RuntimeError("residual_path: invalid context")
+        return "rect" if r == 1 else "general"
+
     # -- host-side conveniences ------------------------------------------------
 
     @property

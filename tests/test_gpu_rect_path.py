@@ -1,0 +1,151 @@
+"""The axis-aligned-rectangle residual path (csrc/fr_rect.cu) against the
+general bilinear kernels (csrc/fr_kernels.cu) and the oracle.
+
+Every BASELINE mesh is made of axis-aligned rectangles, so the rectangle
+kernels carry the headline numbers; the general kernels keep serving
+curved / skewed meshes.  Both implement spatial.py:501-570: they must agree
+to rounding on every kind, degree, boundary tag, option and fused
+epilogue, and the rectangle path must be chosen exactly when the mesh
+qualifies."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle.fr_oracle import OracleDisc
+from paper_2202_09733_b200 import _lib, cases, mesh as mm
+from paper_2202_09733_b200.equation import EquationSpec, NonPhysicalStateError
+from paper_2202_09733_b200.spatial import Discretization
+
+pytestmark = pytest.mark.gpu
+
+
+def _rel(a, b):
+    a = a.cpu().numpy() if isinstance(a, torch.Tensor) else a
+    b = b.cpu().numpy() if isinstance(b, torch.Tensor) else b
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300))
+
+
+def _both(d, fn):
+    assert d.residual_path() == "rect"
+    r = fn()
+    d.residual_path("general")
+    g = fn()
+    d.residual_path("rect")
+    return r, g
+
+
+def test_path_selection():
+    c = cases.config(1, nx=4)
+    assert Discretization(c.mesh, 3, c.eqn).residual_path() == "rect"
+    cyl = mm.generate_cylinder_omesh(12, 4, 0.5, 8.0, 1.3)
+    eq = EquationSpec(kind="navier-stokes", mach=0.3, reynolds=200.0)
+    assert Discretization(cyl, 3, eq).residual_path() == "general"
+    adv = EquationSpec(kind="advection-diffusion", advection=(1.0, 0.5), diffusivity=0.1)
+    assert Discretization(c.mesh, 3, adv).residual_path() == "general"
+    assert Discretization(c.mesh, 0, c.eqn).residual_path() == "general"
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("kind", ["euler", "navier-stokes"])
+@pytest.mark.parametrize("opts", [{}, {"riemann": "rusanov", "viscous_scheme": "ldg"}])
+def test_rect_matches_general_and_oracle(cuda, p, kind, opts):
+    m = mm.generate_box(5, 4, 2.0, 1.5, periodic=True)
+    eqn = EquationSpec(kind=kind, mach=0.4, reynolds=80.0, **opts)
+    o = OracleDisc(m, p, eqn)
+    rng = np.random.default_rng(p)
+    q = o.free_stream_field() * (1 + 0.05 * rng.standard_normal(o.n_dofs))
+    d = Discretization(m, p, eqn)
+    qd = torch.as_tensor(q, device="cuda")
+    r, g = _both(d, lambda: d.residual(qd))
+    Ro = o.residual(q)
+    assert _rel(r, Ro) <= 1e-12
+    assert _rel(r, g) <= 1e-12
+
+
+@pytest.mark.parametrize("tags", [("wall-adiabatic", "wall-slip"), ("wall-isothermal", "far-field"),
+                                  ("far-field", "wall-adiabatic")])
+@pytest.mark.parametrize("p", [2, 3, 4])
+def test_rect_channel_walls(cuda, tags, p):
+    yn = np.array([0.0, 0.02, 0.07, 0.2, 0.45, 1.0])
+    ch = mm.generate_channel(6, 5, 2.0, yn, bottom=tags[0], top=tags[1])
+    eqn = EquationSpec(kind="navier-stokes", mach=0.3, reynolds=300.0, wall_temperature=1.1 / (1.4 * 0.09))
+    o = OracleDisc(ch, p, eqn)
+    q = o.free_stream_field() * (1 + 0.02 * np.random.default_rng(3).standard_normal(o.n_dofs))
+    d = Discretization(ch, p, eqn)
+    qd = torch.as_tensor(q, device="cuda")
+    r, g = _both(d, lambda: d.residual(qd))
+    assert _rel(r, o.residual(q)) <= 1e-12
+    assert _rel(r, g) <= 1e-12
+
+
+def test_rect_self_periodic_single_element(cuda):
+    m = mm.generate_box(1, 1, 1.0, 1.0, periodic=True)
+    eqn = EquationSpec(kind="navier-stokes", mach=0.3, reynolds=50.0)
+    o = OracleDisc(m, 3, eqn)
+    q = o.free_stream_field() * (1 + 0.02 * np.random.default_rng(4).standard_normal(o.n_dofs))
+    d = Discretization(m, 3, eqn)
+    assert d.residual_path() == "rect"
+    assert _rel(d.residual(torch.as_tensor(q, device="cuda")), o.residual(q)) <= 1e-12
+
+
+@pytest.mark.parametrize("mode", range(9))
+def test_rect_epilogues_match_general(cuda, mode):
+    c = cases.config(1, nx=6)
+    d = Discretization(c.mesh, c.p, c.eqn)
+    n = d.n_dofs
+    gen = torch.Generator("cuda").manual_seed(mode)
+    q = torch.as_tensor(c.q0, device="cuda")
+    rnd = lambda: torch.randn(n, dtype=torch.float64, device="cuda", generator=gen)  # noqa: E731
+    X, R0, E, Sb, Se, Q0 = rnd(), rnd(), rnd(), rnd(), rnd(), rnd()
+    lam = torch.rand(c.mesh.n_elements, dtype=torch.float64, device="cuda", generator=gen) + 0.5
+    kw = dict(X=X if mode in (_lib.EPI_JV, _lib.EPI_STAGE_JV) else None, eps=1e-6, s=2.5, adt=0.3, dtau=0.7,
+              R0=R0, E=E, Sb=Sb, Se=Se, Q0=Q0, dtau_e=lam, alpha=0.5)
+    r, g = _both(d, lambda: d.eval(q, mode, **kw))
+    # the Jv forms divide R rounding by eps: compare at the FD noise floor
+    tol = 1e-8 if mode in (_lib.EPI_JV, _lib.EPI_STAGE_JV) else 1e-12
+    assert _rel(r, g) <= tol
+
+
+def test_rect_jv_bitwise_own_residual(cuda):
+    c = cases.config(1)
+    d = Discretization(c.mesh, c.p, c.eqn)
+    q = torch.as_tensor(c.q0, device="cuda")
+    R0 = d.residual(q)
+    v = torch.randn(d.n_dofs, dtype=torch.float64, device="cuda", generator=torch.Generator("cuda").manual_seed(9))
+    out = d.eval(q, _lib.EPI_JV, X=v, eps=1e-6, s=3.7, R0=R0)
+    qp = q + 1e-6 * v  # same rounding as the kernel's q + eps X
+    ref = 3.7 * v - (d.residual(qp) - R0) / torch.full_like(R0, 1e-6)
+    assert torch.equal(out, ref)
+
+
+@pytest.mark.parametrize("kind", ["euler", "navier-stokes"])
+@pytest.mark.parametrize("where", ["state", "trace"])
+def test_rect_nonphysical_reports_smallest_element(cuda, kind, where):
+    m = mm.generate_box(6, 5, 1.0, 1.0, periodic=True)
+    eqn = EquationSpec(kind=kind, mach=0.3, reynolds=100.0)
+    o = OracleDisc(m, 3, eqn)
+    q = o.free_stream_field().copy().reshape(-1, 4, 4, 4)
+    if where == "state":
+        q[17, 2, 1, 0] = -1.0
+        q[23, 0, 0, 0] = -1.0
+    else:  # physical at the points, negative pressure on a face-1 trace
+        q[11, 1, :, 3] = [q[11, 1, 0, 3]] * 3 + [0.6]
+        q[19, 2, :, 3] = [q[19, 2, 0, 3]] * 3 + [0.6]
+    d = Discretization(m, 3, eqn)
+    assert d.residual_path() == "rect"
+    with pytest.raises(NonPhysicalStateError) as ei:
+        o.residual(q.reshape(-1))
+    with pytest.raises(NonPhysicalStateError) as ed:
+        d.residual(torch.as_tensor(q.reshape(-1), device="cuda"))
+    assert ei.value.what == where
+    assert (ed.value.element, ed.value.what) == (ei.value.element, ei.value.what)
+
+
+def test_rect_config2_matches_general_full_size(cuda):
+    c = cases.config(2)
+    d = Discretization(c.mesh, c.p, c.eqn)
+    q = torch.as_tensor(c.q0, device="cuda")
+    r, g = _both(d, lambda: d.residual(q))
+    assert _rel(r, g) <= 2e-9  # both within the reference's own floor of the truth (1.2e-9)
+    assert torch.equal(r, d.residual(q)), "bitwise determinism"
