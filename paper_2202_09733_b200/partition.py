@@ -11,10 +11,15 @@ two elements, and all of that is local.  The halo rows' own residuals are
 discarded.  The strip's open top and bottom edges are tagged far-field;
 they only touch halo elements.
 
-The exchange is one ``all_gather`` of every rank's first and last ``halo``
-owned rows (NCCL on GPUs, gloo in the CPU tests).  Each rank copies its
-neighbours' rows into its halo.  Periodic in y: rank 0's lower halo is the
+The exchange is two-neighbour point-to-point: element rows are contiguous
+in the element-major layout, so each rank sends its first ``halo`` owned
+rows to the previous rank (that rank's upper halo) and its last ``halo``
+owned rows to the next rank (its lower halo), and receives straight into
+its own halo slices -- no pack/unpack, O(1) bytes per rank whatever the
+rank count (``dist.batch_isend_irecv``: NCCL send/recv over NVLink on
+GPUs, gloo in the CPU tests).  Periodic in y: rank 0's lower halo is the
 last rank's top rows.  With one rank it degenerates to a local wrap copy.
+(``exchange_allgather`` keeps the round-1 all_gather form for A/B.)
 
 The partitioned SOLVER (``HaloDiscretization`` + ``vec.set_partition``)
 reuses the same strips for the whole JFNK-pMG step: every kernel that
@@ -89,6 +94,37 @@ class SlabPartition:
             self._rows(q_local, 0, H, sz).copy_(self._rows(q_local, R, H, sz))
             self._rows(q_local, H + R, H, sz).copy_(self._rows(q_local, H, H, sz))
             return q_local
+        if not (dist.is_available() and dist.is_initialized()):
+            raise RuntimeError("SlabPartition.exchange with world > 1 needs torch.distributed")
+        prev, nxt = (self.rank - 1) % self.world, (self.rank + 1) % self.world
+        lo_halo, hi_halo = self._rows(q_local, 0, H, sz), self._rows(q_local, H + R, H, sz)
+        lo_own, hi_own = self._rows(q_local, H, H, sz), self._rows(q_local, R, H, sz)
+        staged = q_local.is_cuda and dist.get_backend() == "gloo"
+        if staged:   # gloo moves host tensors
+            lo_r, hi_r = torch.empty_like(lo_halo, device="cpu"), torch.empty_like(hi_halo, device="cpu")
+            lo_s, hi_s = lo_own.cpu(), hi_own.cpu()
+        else:
+            lo_r, hi_r, lo_s, hi_s = lo_halo, hi_halo, lo_own, hi_own
+        # receives (prev, next) and sends (next, prev) in this order on every
+        # rank: with two ranks prev == next and NCCL pairs the messages
+        # between two peers in posting order; the tags keep gloo unambiguous
+        # (tag 0: a lower halo's rows, tag 1: an upper halo's rows)
+        P = dist.P2POp
+        ops = [P(dist.irecv, lo_r, prev, group, 0), P(dist.irecv, hi_r, nxt, group, 1),
+               P(dist.isend, hi_s, nxt, group, 0), P(dist.isend, lo_s, prev, group, 1)]
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+        if staged:
+            lo_halo.copy_(lo_r)
+            hi_halo.copy_(hi_r)
+        return q_local
+
+    def exchange_allgather(self, q_local: torch.Tensor, elem_size: int, group=None):
+        """Round-1 form of ``exchange``: one all_gather of every rank's
+        boundary rows (O(world) bytes per rank)."""
+        H, R, sz = self.halo, self.rows, elem_size
+        if self.world == 1:
+            return self.exchange(q_local, elem_size, group)
         send = torch.cat([self._rows(q_local, H, H, sz), self._rows(q_local, R, H, sz)])
         if not (dist.is_available() and dist.is_initialized()):
             got = [send]

@@ -62,16 +62,19 @@ def _halo_worker(rank, world, port, out):
     q_local = torch.zeros(part.n_local * sz, dtype=torch.float64)
     o = part.owned
     q_local[o.start * sz:o.stop * sz] = part.scatter_global(q_global, sz)[o.start * sz:o.stop * sz]
+    q_ag = q_local.clone()
     part.exchange(q_local, sz)
-    out[rank] = bool(torch.equal(q_local, part.scatter_global(q_global, sz)))
+    part.exchange_allgather(q_ag, sz)
+    out[rank] = bool(torch.equal(q_local, part.scatter_global(q_global, sz))) and bool(torch.equal(q_local, q_ag))
     dist.barrier()
 
 
 @pytest.mark.timeout(300)
-@pytest.mark.parametrize("world", [1, 2, 3])
+@pytest.mark.parametrize("world", [1, 2, 3, 4])
 def test_slab_halo_exchange_gloo(world):
-    # the multi-GPU partitioned residual's only data-path collective: every
-    # rank's halo rows must come back equal to the global field there
+    # the multi-GPU partitioned residual's only data-path exchange (two-
+    # neighbour send/recv): every rank's halo rows must come back equal to
+    # the global field there, and to the round-1 all_gather form
     port = _free_port()
     with mp.Manager() as m:
         out = m.dict()
