@@ -117,7 +117,9 @@ static int setup_rect(const pmgb_disc_desc* desc, DiscDev& d) {
   cudaError_t err = cudaMalloc(&R.faces, sizeof(int4) * faces.size());
   if (!err) err = cudaMalloc(&R.fslot, sizeof(int) * fslot.size());
   if (!err) err = cudaMalloc(&R.rgeo, sizeof(double2) * rg.size());
-  if (!err) err = cudaMalloc(&R.fw, sizeof(double) * 8 * (size_t)R.nface * n);
+  if (!err) err = cudaMalloc(&R.frec, sizeof(double) * 12 * (size_t)R.nface * n);
+  if (!err) err = cudaMalloc(&R.wh, sizeof(double) * 3 * 4 * (size_t)d.M * n);
+  if (!err) err = cudaMalloc(&R.fc, sizeof(double) * 4 * 4 * (size_t)d.M * n);
   if (!err) err = cudaMemcpy(R.faces, faces.data(), sizeof(int4) * faces.size(), cudaMemcpyHostToDevice);
   if (!err) err = cudaMemcpy(R.fslot, fslot.data(), sizeof(int) * fslot.size(), cudaMemcpyHostToDevice);
   if (!err) err = cudaMemcpy(R.rgeo, rg.data(), sizeof(double2) * rg.size(), cudaMemcpyHostToDevice);
@@ -209,7 +211,9 @@ PMGB_API int pmgb_disc_destroy(pmgb_disc* h) {
   cudaFree(h->d.rect.faces);
   cudaFree(h->d.rect.fslot);
   cudaFree(h->d.rect.rgeo);
-  cudaFree(h->d.rect.fw);
+  cudaFree(h->d.rect.frec);
+  cudaFree(h->d.rect.wh);
+  cudaFree(h->d.rect.fc);
   delete h;
   return 0;
 }
@@ -218,7 +222,7 @@ PMGB_API int64_t pmgb_disc_n_dofs(const pmgb_disc* h) { return h ? h->d.n_dofs :
 
 PMGB_API int pmgb_disc_residual_path(pmgb_disc* h, int32_t want) {
   if (!h) return -1;
-  if (want >= 0) h->d.has_rect = (want != 0 && h->d.rect.fw != nullptr) ? 1 : 0;
+  if (want >= 0) h->d.has_rect = (want != 0 && h->d.rect.frec != nullptr) ? 1 : 0;
   return h->d.has_rect;
 }
 

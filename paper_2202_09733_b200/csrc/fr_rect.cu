@@ -18,20 +18,27 @@
 // differ from it only in rounding).  The one-sided viscous normal flux on a
 // face is +-fx or +-fy, so only that row of the stress is formed.
 //
-// Three kernels chained with programmatic dependent launch:
+// Four kernels chained with programmatic dependent launch.  Element
+// kernels read only contiguous per-element blocks, staged by TMA bulk
+// copies (UBLKCP) completed on an mbarrier; gathers happen only in the two
+// face kernels, scattered writes wherever a result belongs to other
+// elements:
 //   k_rface  one thread per point of each UNIQUE face: the two face traces
-//            straight from the elements' q lines, the interface flux (Roe /
-//            Rusanov, once per face instead of once per side) and the BR1
-//            common value What, stored per face [face][point][F0..3, W0..2]
+//            from the elements' q lines, the interface flux F (Roe /
+//            Rusanov, once per face) into the face record, the BR1 common
+//            value What into both sides' per-element What blocks
 //   k_rgrad  one thread per (element, line): BR1 gradients by line passes
-//            (rows for gx, columns for gy, one shared-memory transpose per
-//            pass), their face traces and the one-sided viscous fluxes fvn
-//   k_rasm   one thread per (element, line): gradients again (cheaper than
-//            a 2x79 MB round trip at config 2), point fluxes, the FR
+//            (rows gx, columns gy, one shared-memory transpose each), their
+//            face traces, the one-sided viscous fluxes into the face record
+//   k_rfc    one thread per unique face point: the common total normal
+//            flux Fc = F - Fv (spatial.py:559-568) into both sides'
+//            per-element Fc blocks (R side negated: bitwise its own value)
+//   k_rasm   one thread per (element, line): gradients again (cheaper than a
+//            2 x 79 MB round trip at config 2), point fluxes, the FR
 //            divergence by line passes, the fused epilogue
 // Line threads keep each line in registers, so the operator contractions
 // read shared memory only for the transposes (blocks of one line, stride
-// with an odd number of 16-byte units: conflict-free 128-bit accesses).
+// an odd number of 16-byte units: conflict-free 128-bit accesses).
 #include <climits>
 
 #include "fr_device.cuh"
@@ -48,33 +55,37 @@ struct RectMesh {
   const double* __restrict__ geom;   // (M,20) for the face normals
 };
 
+// per-face-point record of the unique-face array: F on L's normal, then the
+// one-sided viscous fluxes of the L and R sides on their own normals
+constexpr int FREC = 12;
+
 template <int P> struct RC {
   static constexpr int N = P + 1, NP = N * N;
   static constexpr int EPB = 128 / N;  // elements per CTA
   static constexpr int TH = EPB * N;   // one thread per (element, line)
-  // line block stride in doubles: >= 4N, even, odd number of 16-B units
-  static constexpr int BS = ((4 * N) / 2) % 2 == 1 ? 4 * N : 4 * N + 2;
-  static constexpr int BUF = EPB * N * BS;            // one transpose buffer
-  static constexpr size_t SMEM = 2 * sizeof(double) * BUF;
+  // line block strides in doubles: >= 3N (gradient passes) / 4N (flux
+  // passes), even, an odd number of 16-byte units
+  static constexpr int odd16(int x) { return ((x + 1) / 2) % 2 == 1 ? (x + 1) / 2 * 2 : (x + 1) / 2 * 2 + 2; }
+  static constexpr int BS3 = odd16(3 * N), BS4 = odd16(4 * N);
+  static constexpr int QD = EPB * NP * 4;   // doubles of a q block
+  static constexpr int WD = EPB * 4 * N * 3;  // of a What block
+  static constexpr int FD = EPB * 4 * N * 4;  // of an Fc block
+  // CTAs per SM the register target is set for
+  static constexpr int MINB = P == 5 ? 2 : (P >= 3 ? 3 : 4);
 };
 
 // q (+ eps X with the reference's rounding, newton_krylov.py:76) of point pt
 template <bool HASX>
 __device__ __forceinline__ void ld_q(const double* __restrict__ q, const double* __restrict__ X, double eps,
                                      int64_t pt, double* o) {
-  const double2 a = __ldg(reinterpret_cast<const double2*>(q + pt * 4));
-  const double2 b = __ldg(reinterpret_cast<const double2*>(q + pt * 4) + 1);
-  o[0] = a.x;
-  o[1] = a.y;
-  o[2] = b.x;
-  o[3] = b.y;
+  asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(o[0]), "=d"(o[1]), "=d"(o[2]), "=d"(o[3])
+               : "l"(q + pt * 4));
   if constexpr (HASX) {
-    const double2 c = __ldg(reinterpret_cast<const double2*>(X + pt * 4));
-    const double2 d = __ldg(reinterpret_cast<const double2*>(X + pt * 4) + 1);
-    o[0] = __dadd_rn(o[0], __dmul_rn(eps, c.x));
-    o[1] = __dadd_rn(o[1], __dmul_rn(eps, c.y));
-    o[2] = __dadd_rn(o[2], __dmul_rn(eps, d.x));
-    o[3] = __dadd_rn(o[3], __dmul_rn(eps, d.y));
+    double x[4];
+    asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(x[0]), "=d"(x[1]), "=d"(x[2]), "=d"(x[3])
+                 : "l"(X + pt * 4));
+#pragma unroll
+    for (int v = 0; v < 4; ++v) o[v] = __dadd_rn(o[v], __dmul_rn(eps, x[v]));
   }
 }
 
@@ -165,12 +176,27 @@ __device__ __forceinline__ void face_trace(const FrConst& C, const double* __res
 }
 
 // ---------------------------------------------------------------------------
+// 256-bit global accesses (LDG/STG.E.ENL2.256 on sm_100a)
+
+__device__ __forceinline__ void ldg4(const double* __restrict__ p, double* o) {
+  asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(o[0]), "=d"(o[1]), "=d"(o[2]), "=d"(o[3]) : "l"(p));
+}
+// coherent (L1-bypassing is not needed: written by an earlier kernel)
+__device__ __forceinline__ void ldg4c(const double* p, double* o) {
+  asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(o[0]), "=d"(o[1]), "=d"(o[2]), "=d"(o[3]) : "l"(p));
+}
+__device__ __forceinline__ void stg4(double* p, const double* v) {
+  asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3])
+               : "memory");
+}
+
+// ---------------------------------------------------------------------------
 // k_rface: traces, interface flux and BR1 common value, once per face point
 
 template <int P, int KIND, bool HASX>
 __global__ void __launch_bounds__(128) k_rface(const FrConst C, const RectMesh m, const double* __restrict__ q,
-                                               const double* __restrict__ X, double eps, double* __restrict__ fw,
-                                               int* __restrict__ bad) {
+                                               const double* __restrict__ X, double eps, double* __restrict__ frec,
+                                               double* __restrict__ wh, int* __restrict__ bad) {
   constexpr int N = P + 1;
   constexpr bool VISC = KT<KIND>::VISC;
   pdl_trigger();
@@ -183,6 +209,7 @@ __global__ void __launch_bounds__(128) k_rface(const FrConst C, const RectMesh m
   const double2 nrm = __ldg(reinterpret_cast<const double2*>(m.geom + (int64_t)fr.x * 20 + 8 + 2 * fL));
   const double g = C.gamma;
   const Phys ph = phys_of(C);
+  const int kk = rev ? N - 1 - k : k;
   double qa[4], qc[4];
   // Euler: the states are checked here, on the rows of each element's face 1
   bool okL = true, okR = true;
@@ -191,7 +218,7 @@ __global__ void __launch_bounds__(128) k_rface(const FrConst C, const RectMesh m
   if (bnd)
     ghost<KIND>(qa, tag, nrm.x, nrm.y, C.qinf, qc);
   else
-    face_trace<P, HASX>(C, q, X, eps, fr.z, fr.w, rev ? N - 1 - k : k, qc, chk && fr.w == 1, &okR);
+    face_trace<P, HASX>(C, q, X, eps, fr.z, fr.w, kk, qc, chk && fr.w == 1, &okR);
   if (!okL) atomicMin(bad, fr.x);
   if (!okR) atomicMin(bad, fr.z);
   const Pr A = prim_of(qa, g), B = prim_of(qc, g);
@@ -204,46 +231,118 @@ __global__ void __launch_bounds__(128) k_rface(const FrConst C, const RectMesh m
     rusanov_pr(qa, A, qc, B, nrm.x, nrm.y, g, F);
   else
     roe_pr(qa, A, qc, B, nrm.x, nrm.y, g, F);
-  double2* o = reinterpret_cast<double2*>(fw + t * 8);
-  o[0] = make_double2(F[0], F[1]);
-  o[1] = make_double2(F[2], F[3]);
+  stg4(frec + t * FREC, F);
   if constexpr (VISC) {
     double wa[3] = {A.u, A.v, A.p * A.ir}, wc[3] = {B.u, B.v, B.p * B.ir};
     if (bnd) ghost_w<KIND>(ph, tag, wa, wc);
-    double wh[3];
+    double w[3];
 #pragma unroll
-    for (int c = 0; c < 3; ++c) wh[c] = common_w(ph, !bnd, true, wa[c], wc[c]);
-    o[2] = make_double2(wh[0], wh[1]);
-    o[3] = make_double2(wh[2], 0.0);
+    for (int c = 0; c < 3; ++c) w[c] = common_w(ph, !bnd, true, wa[c], wc[c]);
+    double* dL = wh + (((int64_t)fr.x * 4 + fL) * N + k) * 3;
+    dL[0] = w[0], dL[1] = w[1], dL[2] = w[2];
+    if (!bnd) {
+      double* dR = wh + (((int64_t)fr.z * 4 + fr.w) * N + kk) * 3;
+      dR[0] = w[0], dR[1] = w[1], dR[2] = w[2];
+    }
   }
 }
 
 // ---------------------------------------------------------------------------
-// shared by k_rgrad and k_rasm
+// k_rfc: the common total normal flux, once per face point, to both sides
 
-// face point (f, k) of element e: index of its record in fw (L side order)
-// and whether e is that face's L side (or a boundary face's only side)
-struct FaceRef {
-  int64_t rec;   // (phi * N + kL) * 8
-  bool left, inter;
-  int2 lk;
-};
-template <int N>
-__device__ __forceinline__ FaceRef face_ref(const RectMesh& m, int64_t e, int f, int k) {
-  FaceRef r;
-  r.lk = __ldg(m.link + e * 4 + f);
-  r.inter = r.lk.x >= 0;
-  r.left = !r.inter || lk_left(r.lk.y);
-  const int kL = (!r.left && lk_rev(r.lk.y)) ? N - 1 - k : k;
-  r.rec = ((int64_t)__ldg(m.fslot + e * 4 + f) * N + kL) * 8;
-  return r;
+template <int P, int KIND>
+__global__ void __launch_bounds__(128) k_rfc(const FrConst C, const RectMesh m, const double* __restrict__ frec,
+                                             double* __restrict__ fc) {
+  constexpr int N = P + 1;
+  pdl_trigger();
+  const int64_t t = (int64_t)blockIdx.x * 128 + threadIdx.x;
+  const bool live = t < m.nface * N;
+  const int64_t phi = live ? t / N : 0;
+  const int k = (int)(t - phi * N);
+  const int4 fr = live ? __ldg(m.faces + phi) : make_int4(0, 0, 0, 0);
+  pdl_wait();  // frec (k_rface F, k_rgrad fvn)
+  if (!live) return;
+  const int fL = fr.y & 3, rev = (fr.y >> 2) & 1, bnd = (fr.y >> 3) & 1, tag = (fr.y >> 4) & 15;
+  const Phys ph = phys_of(C);
+  const double* rec = frec + t * FREC;
+  double Fc[4];
+  ldg4c(rec, Fc);
+  if constexpr (KT<KIND>::VISC) {
+    double fl[4], fr_[4], Fv[4];
+    ldg4c(rec + 4, fl);
+    if (bnd) {
+#pragma unroll
+      for (int v = 0; v < 4; ++v) Fv[v] = common_fv(ph, false, true, fl[v], fl[v]);
+      if (tag == T_WALL_ADIABATIC) Fv[3] = 0.0;
+    } else {
+      ldg4c(rec + 8, fr_);
+#pragma unroll
+      for (int v = 0; v < 4; ++v) Fv[v] = common_fv(ph, true, true, fl[v], fr_[v]);
+    }
+#pragma unroll
+    for (int v = 0; v < 4; ++v) Fc[v] = Fc[v] - Fv[v];
+  }
+  stg4(fc + (((int64_t)fr.x * 4 + fL) * N + k) * 4, Fc);
+  if (!bnd) {
+    const double n[4] = {-Fc[0], -Fc[1], -Fc[2], -Fc[3]};
+    stg4(fc + (((int64_t)fr.z * 4 + fr.w) * N + (rev ? N - 1 - k : k)) * 4, n);
+  }
 }
 
-__device__ __forceinline__ void ld_what(const double* __restrict__ fw, int64_t rec, double* wh) {
-  const double2 a = __ldg(reinterpret_cast<const double2*>(fw + rec + 4));
-  wh[0] = a.x;
-  wh[1] = a.y;
-  wh[2] = __ldg(fw + rec + 6);
+// ---------------------------------------------------------------------------
+// shared by the element kernels
+
+// TMA bulk copy of a contiguous global block into shared memory, completed
+// on an mbarrier (UBLKCP + SYNCS)
+__device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(saddr(bar)));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   saddr(dst)),
+               "l"(src), "r"(bytes), "r"(saddr(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n RW%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra RW%=;\n}" ::"r"(
+          saddr(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+// q + eps X formed in place in the staged q block (the reference's rounding)
+template <int TH>
+__device__ __forceinline__ void form_qp(double* sQ, const double* sXb, double eps, int nd) {
+  for (int i = 2 * threadIdx.x; i < nd; i += 2 * TH) {
+    double2 a = *reinterpret_cast<const double2*>(sQ + i);
+    const double2 x = *reinterpret_cast<const double2*>(sXb + i);
+    a.x = __dadd_rn(a.x, __dmul_rn(eps, x.x));
+    a.y = __dadd_rn(a.y, __dmul_rn(eps, x.y));
+    *reinterpret_cast<double2*>(sQ + i) = a;
+  }
+}
+
+// one point of a staged q block
+__device__ __forceinline__ void lds4(const double* p, double* o) {
+  const double2 a = reinterpret_cast<const double2*>(p)[0];
+  const double2 b = reinterpret_cast<const double2*>(p)[1];
+  o[0] = a.x;
+  o[1] = a.y;
+  o[2] = b.x;
+  o[3] = b.y;
+}
+
+// face points of line thread a: [0] face 0 point a, [1] face 1 point a,
+// [2] face 2 point N-1-a, [3] face 3 point N-1-a
+template <int N>
+__device__ __forceinline__ int fpt_of(int f, int a) {
+  return f * N + ((f >= 2) ? N - 1 - a : a);
 }
 
 // BR1 gradient along one line (row: gx with ia; column: gy with id) from
@@ -298,50 +397,117 @@ __device__ __forceinline__ void visc_fy(const double* q, const double* gx, const
   fy[3] = u * txy + v * tyy + ph.kappa * gy[2];
 }
 
-__device__ __forceinline__ void ld4(const double* __restrict__ src, double* o) {
-  const double2 a = __ldg(reinterpret_cast<const double2*>(src));
-  const double2 b = __ldg(reinterpret_cast<const double2*>(src) + 1);
-  o[0] = a.x;
-  o[1] = a.y;
-  o[2] = b.x;
-  o[3] = b.y;
-}
-
-__device__ __forceinline__ void st4(double* dst, const double* v) {
-  reinterpret_cast<double2*>(dst)[0] = make_double2(v[0], v[1]);
-  reinterpret_cast<double2*>(dst)[1] = make_double2(v[2], v[3]);
+// divergence along one line of a 4-variable flux x[v][i]: the +1 end takes
+// (Fp - trace), the -1 end (-Fm - trace)  (the reference's c1/c3, c2/c0)
+template <int N>
+__device__ __forceinline__ void line_div(const FrConst& C, const double (&x)[4][N], const double* Fp,
+                                         const double* Fm, double (&out)[4][N]) {
+#pragma unroll
+  for (int v = 0; v < 4; ++v) {
+    double tp = 0.0, tm = 0.0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      tp += C.eR[i] * x[v][i];
+      tm += C.eL[i] * x[v][i];
+    }
+    const double cp = Fp[v] - tp, cm = -Fm[v] - tm;
+#pragma unroll
+    for (int b = 0; b < N; ++b) {
+      double d = 0.0;
+#pragma unroll
+      for (int i = 0; i < N; ++i) d += C.D[b * N + i] * x[v][i];
+      out[v][b] = (d + C.lR[b] * cp) - C.lL[b] * cm;
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
 // k_rgrad: BR1 gradients, their face traces, one-sided viscous fluxes
 
-template <int P, bool HASX>
-__global__ void __launch_bounds__(RC<P>::TH, 4)
-k_rgrad(const FrConst C, const RectMesh m, const double* __restrict__ q, const double* __restrict__ X, double eps,
-        const double* __restrict__ fw, double* __restrict__ fvn, int* __restrict__ bad) {
+// shared memory: [q block | stage]; the stage first holds the X block (Jv
+// forms, at its start) and the What block (at its end), then the two
+// line-block transposes
+template <int P, bool HASX> struct GL {
   using R = RC<P>;
-  constexpr int N = R::N, NP = R::NP, E = R::EPB, BS = R::BS;
-  extern __shared__ __align__(16) double sm[];
-  double* sX = sm;           // column blocks: W, then gx
-  double* sY = sm + R::BUF;  // row blocks: gy
+  static constexpr int BUF = R::EPB * R::N * R::BS3;
+  static constexpr int A = 2 * BUF, B = R::WD + (HASX ? R::QD : 0);
+  static constexpr int STAGE = A > B ? A : B;
+  static constexpr int OFF_W = R::QD + STAGE - R::WD, OFF_BAR = R::QD + STAGE;
+  static constexpr size_t BYTES = sizeof(double) * (OFF_BAR + 2);
+};
+
+template <int P, bool HASX>
+__global__ void __launch_bounds__(RC<P>::TH, RC<P>::MINB)
+k_rgrad(const FrConst C, const RectMesh m, const double* __restrict__ q, const double* __restrict__ X, double eps,
+        const double* __restrict__ wh, double* __restrict__ frec, int* __restrict__ bad) {
+  using R = RC<P>;
+  using L = GL<P, HASX>;
+  constexpr int N = R::N, NP = R::NP, E = R::EPB, BS = R::BS3;
+  extern __shared__ __align__(128) double sm[];
+  double* sQ = sm;
+  double* sX = sm + R::QD;            // X block; then W, then gx (column blocks)
+  double* sY = sm + R::QD + L::BUF;   // gy (row blocks)
+  const double* sWb = sm + L::OFF_W;  // What block [el][f][k][3]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::OFF_BAR);
   pdl_trigger();
   const int t = threadIdx.x;
   const int el = t / N, a = t % N;  // row a of element el; also column a
-  const int64_t e = (int64_t)blockIdx.x * E + el;
-  const bool live = t < E * N && e < m.M;
+  const int64_t e0 = (int64_t)blockIdx.x * E;
+  const int ne = (int)((m.M - e0) < E ? (m.M - e0) : E);
+  const int64_t e = e0 + el;
+  const bool live = t < E * N && el < ne;
   const Phys ph = phys_of(C);
   const double g = C.gamma;
-  // rows: q, primitives, W; the row's q traces on faces 1 and 3
+  if (t == 0) {
+    mbar_init(bar);
+    mbar_init(bar + 1);
+  }
+  __syncthreads();
+  const uint32_t qbytes = (uint32_t)ne * NP * 32;
+  if (t == 0) {  // q (+ X): inputs of the chain, before the dependency wait
+    mbar_expect(bar, HASX ? 2 * qbytes : qbytes);
+    bulk_g2s(sQ, q + e0 * NP * 4, qbytes, bar);
+    if (HASX) bulk_g2s(sX, X + e0 * NP * 4, qbytes, bar);
+  }
+  // static face data of the thread's four face points
+  int ri[4] = {0, 0, 0, 0};
+  bool lft[4] = {true, true, true, true};
+  const double2 rg = live ? __ldg(m.rgeo + e) : make_double2(0.0, 0.0);
+  if (live) {
+    const int4 sl = __ldg(reinterpret_cast<const int4*>(m.fslot) + e);
+    const int4 l01 = __ldg(reinterpret_cast<const int4*>(m.link) + 2 * e);
+    const int4 l23 = __ldg(reinterpret_cast<const int4*>(m.link) + 2 * e + 1);
+    const int slot[4] = {sl.x, sl.y, sl.z, sl.w};
+    const int2 lk[4] = {make_int2(l01.x, l01.y), make_int2(l01.z, l01.w), make_int2(l23.x, l23.y),
+                        make_int2(l23.z, l23.w)};
+#pragma unroll
+    for (int f = 0; f < 4; ++f) {
+      const int k = (f >= 2) ? N - 1 - a : a;
+      lft[f] = lk[f].x < 0 || lk_left(lk[f].y);
+      const int kL = (!lft[f] && lk_rev(lk[f].y)) ? N - 1 - k : k;
+      ri[f] = slot[f] * N + kL;
+    }
+  }
+  pdl_wait();  // What (k_rface)
+  if (t == 0) {
+    mbar_expect(bar + 1, (uint32_t)ne * 4 * N * 24);
+    bulk_g2s(sm + L::OFF_W, wh + e0 * 4 * N * 3, (uint32_t)ne * 4 * N * 24, bar + 1);
+  }
+  mbar_wait(bar, 0);
+  if constexpr (HASX) {
+    form_qp<R::TH>(sQ, sX, eps, ne * NP * 4);
+    __syncthreads();
+  }
+  // rows: primitives, W, the row's q traces on faces 1 and 3
   double w[3][N];
   double t1q[4] = {0, 0, 0, 0}, t3q[4] = {0, 0, 0, 0};
-  double2 rg = make_double2(0.0, 0.0);
-  if (live) {
-    rg = __ldg(m.rgeo + e);
+  {
     bool ok = true;
+    const double* row = sQ + (el * N + a) * N * 4;
 #pragma unroll
     for (int i = 0; i < N; ++i) {
       double x[4];
-      ld_q<HASX>(q, X, eps, e * NP + a * N + i, x);
+      lds4(row + 4 * i, x);
       const Pr s = prim_of(x, g);
       ok = ok && (s.r > 0.0) && (s.p > 0.0);
       w[0][i] = s.u;
@@ -353,32 +519,25 @@ k_rgrad(const FrConst C, const RectMesh m, const double* __restrict__ q, const d
         t3q[v] += C.eL[i] * x[v];
       }
     }
-    if (!ok && bad != nullptr) atomicMin(bad, (int)e);
-  } else {
-#pragma unroll
-    for (int c = 0; c < 3; ++c)
-#pragma unroll
-      for (int i = 0; i < N; ++i) w[c][i] = 1.0;
+    if (live && !ok && bad != nullptr) atomicMin(bad, (int)e);
   }
+  mbar_wait(bar + 1, 0);
+  double whv[4][3];
+#pragma unroll
+  for (int f = 0; f < 4; ++f)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) whv[f][c] = sWb[(el * 4 * N + fpt_of<N>(f, a)) * 3 + c];
+  __syncthreads();  // the stage (X, What blocks) is free
   // W into column blocks: block (el, i) holds column i, [c][row]
 #pragma unroll
   for (int i = 0; i < N; ++i)
 #pragma unroll
     for (int c = 0; c < 3; ++c) sX[(el * N + i) * BS + c * N + a] = w[c][i];
-  pdl_wait();  // fw (k_rface)
-  // faces 1 (point a) and 3 (point N-1-a): common values, then gx along the row
+  // gx along row a (faces 1 and 3)
   double gx[3][N];
-  FaceRef f1{}, f3{};
-  double wh1[3] = {0, 0, 0}, wh3[3] = {0, 0, 0};
-  if (live) {
-    f1 = face_ref<N>(m, e, 1, a);
-    f3 = face_ref<N>(m, e, 3, N - 1 - a);
-    ld_what(fw, f1.rec, wh1);
-    ld_what(fw, f3.rec, wh3);
-  }
-  line_gradient<N>(C, w, wh1, wh3, rg.x, gx);
+  line_gradient<N>(C, w, whv[1], whv[3], rg.x, gx);
   __syncthreads();
-  // columns: W of column a, common values on faces 0 (point a) and 2 (point N-1-a), gy
+  // column a: W of the column, gy (faces 2 and 0)
   double gy[3][N];
   {
     const double* blk = sX + t * BS;
@@ -386,16 +545,8 @@ k_rgrad(const FrConst C, const RectMesh m, const double* __restrict__ q, const d
     for (int c = 0; c < 3; ++c)
 #pragma unroll
       for (int i = 0; i < N; ++i) w[c][i] = blk[c * N + i];
+    line_gradient<N>(C, w, whv[2], whv[0], rg.y, gy);
   }
-  FaceRef f0{}, f2{};
-  double wh0[3] = {0, 0, 0}, wh2[3] = {0, 0, 0};
-  if (live) {
-    f0 = face_ref<N>(m, e, 0, a);
-    f2 = face_ref<N>(m, e, 2, N - 1 - a);
-    ld_what(fw, f0.rec, wh0);
-    ld_what(fw, f2.rec, wh2);
-  }
-  line_gradient<N>(C, w, wh2, wh0, rg.y, gy);
   __syncthreads();  // W reads done
   // gx rows -> column blocks of sX; gy columns -> row blocks of sY
 #pragma unroll
@@ -424,7 +575,7 @@ k_rgrad(const FrConst C, const RectMesh m, const double* __restrict__ q, const d
   }
   __syncthreads();
   if (!live) return;
-  // rows: gy along row a (block (el, a) of sY) -> gy traces on faces 1/3
+  // rows: gy along row a -> gy traces on faces 1/3; columns: gx -> faces 0/2
   double tgy1[2], tgy3[2], tgx0[2], tgx2[2];
   {
     const double* blk = sY + t * BS;
@@ -459,163 +610,144 @@ k_rgrad(const FrConst C, const RectMesh m, const double* __restrict__ q, const d
 #pragma unroll
   for (int i = 0; i < N; ++i) {
     double x[4];
-    ld_q<HASX>(q, X, eps, e * NP + i * N + a, x);
+    lds4(sQ + ((el * N + i) * N + a) * 4, x);
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
       t2q[v] += C.eR[i] * x[v];
       t0q[v] += C.eL[i] * x[v];
     }
   }
-  // one-sided viscous normal fluxes (spatial.py:456-464): face 1 +fx,
-  // face 3 -fx, face 2 +fy, face 0 -fy
+  // one-sided viscous normal fluxes (spatial.py:456-464) into the face
+  // records: face 1 +fx, face 3 -fx, face 2 +fy, face 0 -fy
   double o[4];
   {
     const double gyv[2] = {tgy1[0], tgy1[1]};
     visc_fx(t1q, tgx1, gyv, ph, o);
-    st4(fvn + ((e * 4 + 1) * N + a) * 4, o);
+    stg4(frec + (int64_t)ri[1] * FREC + (lft[1] ? 4 : 8), o);
   }
   {
     const double gyv[2] = {tgy3[0], tgy3[1]};
     visc_fx(t3q, tgx3, gyv, ph, o);
     o[1] = -o[1], o[2] = -o[2], o[3] = -o[3];
-    st4(fvn + ((e * 4 + 3) * N + (N - 1 - a)) * 4, o);
+    stg4(frec + (int64_t)ri[3] * FREC + (lft[3] ? 4 : 8), o);
   }
   {
     const double gxv[2] = {tgx2[0], tgx2[1]};
     visc_fy(t2q, gxv, tgy2, ph, o);
-    st4(fvn + ((e * 4 + 2) * N + (N - 1 - a)) * 4, o);
+    stg4(frec + (int64_t)ri[2] * FREC + (lft[2] ? 4 : 8), o);
   }
   {
     const double gxv[2] = {tgx0[0], tgx0[1]};
     visc_fy(t0q, gxv, tgy0, ph, o);
     o[1] = -o[1], o[2] = -o[2], o[3] = -o[3];
-    st4(fvn + ((e * 4 + 0) * N + a) * 4, o);
+    stg4(frec + (int64_t)ri[0] * FREC + (lft[0] ? 4 : 8), o);
   }
 }
 
 // ---------------------------------------------------------------------------
-// k_rasm: common fluxes, point fluxes, FR divergence, fused epilogue
+// k_rasm: point fluxes, FR divergence, fused epilogue
 
-// common total normal flux on own face point: +-F (interface flux on L's
-// normal) minus the common viscous flux (spatial.py:559-568)
-template <int N, bool VISC>
-__device__ __forceinline__ void common_flux(const RectMesh& m, const double* __restrict__ fw,
-                                            const double* __restrict__ fvn, const Phys& ph, const FaceRef& r,
-                                            int64_t e, int f, int k, double* Fc) {
-  const double2 a = __ldg(reinterpret_cast<const double2*>(fw + r.rec));
-  const double2 b = __ldg(reinterpret_cast<const double2*>(fw + r.rec) + 1);
-  double F[4] = {a.x, a.y, b.x, b.y};
-#pragma unroll
-  for (int v = 0; v < 4; ++v) F[v] = r.left ? F[v] : -F[v];
-  if constexpr (VISC) {
-    double Fo[4], Fn[4];
-    ld4(fvn + ((e * 4 + f) * N + k) * 4, Fo);
-    if (r.inter) {
-      const int kk = lk_rev(r.lk.y) ? N - 1 - k : k;
-      ld4(fvn + (((int64_t)r.lk.x * 4 + lk_face(r.lk.y)) * N + kk) * 4, Fn);
-    } else {
-#pragma unroll
-      for (int v = 0; v < 4; ++v) Fn[v] = Fo[v];
-    }
-    double Fv[4];
-#pragma unroll
-    for (int v = 0; v < 4; ++v) Fv[v] = common_fv(ph, r.inter, r.left, Fo[v], Fn[v]);
-    if (!r.inter && lk_tag(r.lk.y) == T_WALL_ADIABATIC) Fv[3] = 0.0;
-#pragma unroll
-    for (int v = 0; v < 4; ++v) F[v] = F[v] - Fv[v];
-  }
-#pragma unroll
-  for (int v = 0; v < 4; ++v) Fc[v] = F[v];
-}
-
-// divergence along one line of a 4-variable flux x[v][i]: the +1 end takes
-// (Fp - trace), the -1 end (-Fm - trace)  (the reference's c1/c3, c2/c0)
-template <int N>
-__device__ __forceinline__ void line_div(const FrConst& C, const double (&x)[4][N], const double* Fp,
-                                         const double* Fm, double (&out)[4][N]) {
-#pragma unroll
-  for (int v = 0; v < 4; ++v) {
-    double tp = 0.0, tm = 0.0;
-#pragma unroll
-    for (int i = 0; i < N; ++i) {
-      tp += C.eR[i] * x[v][i];
-      tm += C.eL[i] * x[v][i];
-    }
-    const double cp = Fp[v] - tp, cm = -Fm[v] - tm;
-#pragma unroll
-    for (int b = 0; b < N; ++b) {
-      double d = 0.0;
-#pragma unroll
-      for (int i = 0; i < N; ++i) d += C.D[b * N + i] * x[v][i];
-      out[v][b] = (d + C.lR[b] * cp) - C.lL[b] * cm;
-    }
-  }
-}
+template <int P, int KIND, bool HASX> struct AL {
+  using R = RC<P>;
+  static constexpr bool VISC = KT<KIND>::VISC;
+  static constexpr int BUF = R::EPB * R::N * R::BS4;
+  static constexpr int WD = VISC ? R::WD : 0;
+  static constexpr int A = 2 * BUF, B = WD + R::FD + (HASX ? R::QD : 0);
+  static constexpr int STAGE = A > B ? A : B;
+  static constexpr int OFF_F = R::QD + STAGE - R::FD, OFF_W = OFF_F - WD, OFF_BAR = R::QD + STAGE;
+  static constexpr size_t BYTES = sizeof(double) * (OFF_BAR + 2);
+};
 
 template <int P, int KIND, int EK, bool HASX>
-__global__ void __launch_bounds__(RC<P>::TH, 4)
+__global__ void __launch_bounds__(RC<P>::TH, RC<P>::MINB)
 k_rasm(const FrConst C, const RectMesh m, const double* __restrict__ q, const double* __restrict__ X, double eps,
-       const double* __restrict__ fw, const double* __restrict__ fvn, const Epi ep, double* __restrict__ out,
+       const double* __restrict__ wh, const double* __restrict__ fc, const Epi ep, double* __restrict__ out,
        int* bad, Status* st) {
   using R = RC<P>;
-  constexpr int N = R::N, NP = R::NP, E = R::EPB, BS = R::BS;
+  using L = AL<P, KIND, HASX>;
+  constexpr int N = R::N, NP = R::NP, E = R::EPB, BS = R::BS4;
   constexpr bool VISC = KT<KIND>::VISC;
-  extern __shared__ __align__(16) double sm[];
-  double* sX = sm;           // column blocks: W, then fy
-  double* sY = sm + R::BUF;  // row blocks gy, then column blocks X_xi
+  extern __shared__ __align__(128) double sm[];
+  double* sQ = sm;
+  double* sX = sm + R::QD;            // X block; then W, then fy (column blocks)
+  double* sY = sm + R::QD + L::BUF;   // gy (row blocks), then X_xi (column blocks)
+  const double* sWb = sm + L::OFF_W;  // What block [el][f][k][3]
+  const double* sFb = sm + L::OFF_F;  // Fc block [el][f][k][4]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::OFF_BAR);
   const int t = threadIdx.x;
   const int el = t / N, a = t % N;
-  const int64_t e = (int64_t)blockIdx.x * E + el;
-  const bool live = t < E * N && e < m.M;
+  const int64_t e0 = (int64_t)blockIdx.x * E;
+  const int ne = (int)((m.M - e0) < E ? (m.M - e0) : E);
+  const int64_t e = e0 + el;
+  const bool live = t < E * N && el < ne;
   const Phys ph = phys_of(C);
   const double g = C.gamma;
-  // row a: q (an input: read before the dependency wait); its viscous
-  // variables into column blocks for the column pass
-  double qr[4][N];
-  double2 rg = make_double2(1.0, 1.0);
-  if (live) {
-    rg = __ldg(m.rgeo + e);
+  if (t == 0) {
+    mbar_init(bar);
+    mbar_init(bar + 1);
+  }
+  __syncthreads();
+  const uint32_t qbytes = (uint32_t)ne * NP * 32;
+  if (t == 0) {
+    mbar_expect(bar, HASX ? 2 * qbytes : qbytes);
+    bulk_g2s(sQ, q + e0 * NP * 4, qbytes, bar);
+    if (HASX) bulk_g2s(sX, X + e0 * NP * 4, qbytes, bar);
+  }
+  const double2 rg = live ? __ldg(m.rgeo + e) : make_double2(1.0, 1.0);
+  pdl_wait();  // What (k_rface), Fc (k_rfc), status flags
+  if (t == 0) {
+    const uint32_t fb = (uint32_t)ne * 4 * N * 32, wb = (uint32_t)ne * 4 * N * 24;
+    mbar_expect(bar + 1, VISC ? fb + wb : fb);
+    bulk_g2s(sm + L::OFF_F, fc + e0 * 4 * N * 4, fb, bar + 1);
+    if (VISC) bulk_g2s(sm + L::OFF_W, wh + e0 * 4 * N * 3, wb, bar + 1);
+    if (blockIdx.x == 0) commit_status(bad, st);
+  }
+  mbar_wait(bar, 0);
+  if constexpr (HASX) {
+    form_qp<R::TH>(sQ, sX, eps, ne * NP * 4);
+    __syncthreads();
+  }
+  const double* row = sQ + (el * N + a) * N * 4;
+  double w[3][N];
+  if constexpr (VISC) {
 #pragma unroll
     for (int i = 0; i < N; ++i) {
       double x[4];
-      ld_q<HASX>(q, X, eps, e * NP + a * N + i, x);
-#pragma unroll
-      for (int v = 0; v < 4; ++v) qr[v][i] = x[v];
-    }
-  } else {
-#pragma unroll
-    for (int i = 0; i < N; ++i) qr[0][i] = qr[3][i] = 1.0, qr[1][i] = qr[2][i] = 0.0;
-  }
-  if constexpr (VISC) {
-#pragma unroll
-    for (int i = 0; i < N; ++i) {
-      const double x[4] = {qr[0][i], qr[1][i], qr[2][i], qr[3][i]};
+      lds4(row + 4 * i, x);
       const Pr s = prim_of(x, g);
-      sX[(el * N + i) * BS + 0 * N + a] = s.u;
-      sX[(el * N + i) * BS + 1 * N + a] = s.v;
-      sX[(el * N + i) * BS + 2 * N + a] = s.p * s.ir;
+      w[0][i] = s.u;
+      w[1][i] = s.v;
+      w[2][i] = s.p * s.ir;
     }
   }
-  pdl_wait();  // fw (k_rface), fvn (k_rgrad), status flags
-  if (blockIdx.x == 0 && threadIdx.x == 0) commit_status(bad, st);
+  mbar_wait(bar + 1, 0);
+  double whv[4][3], fcv[4][4];
+#pragma unroll
+  for (int f = 0; f < 4; ++f) {
+    const int fp = el * 4 * N + fpt_of<N>(f, a);
+    if constexpr (VISC) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) whv[f][c] = sWb[fp * 3 + c];
+    }
+    lds4(sFb + fp * 4, fcv[f]);
+  }
+  __syncthreads();  // the stage (X, What, Fc blocks) is free
   double gy[3][N];
   if constexpr (VISC) {
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) sX[(el * N + i) * BS + c * N + a] = w[c][i];
     __syncthreads();
     // column a: gy -> row blocks
     {
-      double w[3][N];
       const double* blk = sX + t * BS;
 #pragma unroll
       for (int c = 0; c < 3; ++c)
 #pragma unroll
         for (int i = 0; i < N; ++i) w[c][i] = blk[c * N + i];
-      double wp[3] = {0, 0, 0}, wm[3] = {0, 0, 0};
-      if (live) {
-        ld_what(fw, face_ref<N>(m, e, 2, N - 1 - a).rec, wp);
-        ld_what(fw, face_ref<N>(m, e, 0, a).rec, wm);
-      }
       double gc[3][N];
-      line_gradient<N>(C, w, wp, wm, rg.y, gc);
+      line_gradient<N>(C, w, whv[2], whv[0], rg.y, gc);
 #pragma unroll
       for (int i = 0; i < N; ++i)
 #pragma unroll
@@ -630,27 +762,25 @@ k_rasm(const FrConst C, const RectMesh m, const double* __restrict__ q, const do
   }
   // row a: primitives (again: cheaper than holding them through the column
   // pass), gx, point fluxes -- fx stays in registers, fy -> column blocks
+  double qr[4][N];
   Pr pr[N];
 #pragma unroll
   for (int i = 0; i < N; ++i) {
-    const double x[4] = {qr[0][i], qr[1][i], qr[2][i], qr[3][i]};
+    double x[4];
+    lds4(row + 4 * i, x);
+#pragma unroll
+    for (int v = 0; v < 4; ++v) qr[v][i] = x[v];
     pr[i] = prim_of(x, g);
   }
   double gx[3][N];
   if constexpr (VISC) {
-    double w[3][N];
 #pragma unroll
     for (int i = 0; i < N; ++i) {
       w[0][i] = pr[i].u;
       w[1][i] = pr[i].v;
       w[2][i] = pr[i].p * pr[i].ir;
     }
-    double wp[3] = {0, 0, 0}, wm[3] = {0, 0, 0};
-    if (live) {
-      ld_what(fw, face_ref<N>(m, e, 1, a).rec, wp);
-      ld_what(fw, face_ref<N>(m, e, 3, N - 1 - a).rec, wm);
-    }
-    line_gradient<N>(C, w, wp, wm, rg.x, gx);
+    line_gradient<N>(C, w, whv[1], whv[3], rg.x, gx);
   }
   double fx[4][N];
 #pragma unroll
@@ -688,13 +818,8 @@ k_rasm(const FrConst C, const RectMesh m, const double* __restrict__ q, const do
     }
   }
   // X_xi along row a
-  double Fc1[4] = {0, 0, 0, 0}, Fc3[4] = {0, 0, 0, 0};
-  if (live) {
-    common_flux<N, VISC>(m, fw, fvn, ph, face_ref<N>(m, e, 1, a), e, 1, a, Fc1);
-    common_flux<N, VISC>(m, fw, fvn, ph, face_ref<N>(m, e, 3, N - 1 - a), e, 3, N - 1 - a, Fc3);
-  }
   double xx[4][N];
-  line_div<N>(C, fx, Fc1, Fc3, xx);
+  line_div<N>(C, fx, fcv[1], fcv[3], xx);
   if constexpr (VISC) __syncthreads();  // gy row reads of sY done
 #pragma unroll
   for (int i = 0; i < N; ++i)
@@ -702,20 +827,17 @@ k_rasm(const FrConst C, const RectMesh m, const double* __restrict__ q, const do
     for (int v = 0; v < 4; ++v) sY[(el * N + i) * BS + v * N + a] = xx[v][i];
   __syncthreads();
   if (!live) return;
-  // column a: fy and X_xi of the column, faces 0 / 2, X_eta, R, epilogue
-  double fc[4][N];
+  // column a: fy and X_xi of the column, faces 2 / 0, X_eta, R, epilogue
+  double fyc[4][N];
   {
     const double* blk = sX + t * BS;
 #pragma unroll
     for (int v = 0; v < 4; ++v)
 #pragma unroll
-      for (int i = 0; i < N; ++i) fc[v][i] = blk[v * N + i];
+      for (int i = 0; i < N; ++i) fyc[v][i] = blk[v * N + i];
   }
-  double Fc0[4], Fc2[4];
-  common_flux<N, VISC>(m, fw, fvn, ph, face_ref<N>(m, e, 0, a), e, 0, a, Fc0);
-  common_flux<N, VISC>(m, fw, fvn, ph, face_ref<N>(m, e, 2, N - 1 - a), e, 2, N - 1 - a, Fc2);
   double xe[4][N];
-  line_div<N>(C, fc, Fc2, Fc0, xe);
+  line_div<N>(C, fyc, fcv[2], fcv[0], xe);
   const double* bx = sY + t * BS;
   constexpr bool NEEDQ = !(EK == EPI_R || EK == EPI_JV || EK == EPI_NEG_R);
   const double ce = (EK == EPI_RK) ? epi_rk_coef(ep, e) : 0.0;
@@ -723,7 +845,7 @@ k_rasm(const FrConst C, const RectMesh m, const double* __restrict__ q, const do
   for (int i = 0; i < N; ++i) {   // point (i, a)
     const int64_t pt = e * NP + i * N + a;
     double qv[4] = {0, 0, 0, 0};
-    if constexpr (NEEDQ) ld_q<HASX>(q, X, eps, pt, qv);
+    if constexpr (NEEDQ) lds4(sQ + ((el * N + i) * N + a) * 4, qv);
     double o[4];
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
@@ -736,7 +858,7 @@ k_rasm(const FrConst C, const RectMesh m, const double* __restrict__ q, const do
         o[v] = (EK == EPI_RK) ? epi_rk(ep, ce, Rv, qv[v], o1, o2, o3) : epi_pre_k<EK>(ep, Rv, qv[v], o1, o2, o3);
       }
     }
-    st4(out + pt * 4, o);
+    stg4(out + pt * 4, o);
   }
 }
 
@@ -777,11 +899,11 @@ static RasmFn rasm_for(int mode) {
 
 template <int P, int KIND, bool HASX>
 static void set_rect_attrs() {
-  using R = RC<P>;
   for (int md : {(int)EPI_R, (int)EPI_JV, (int)EPI_STAGE_JV, (int)EPI_DEFECT, (int)EPI_F, (int)EPI_RK, -1})
-    cudaFuncSetAttribute(rasm_for<P, KIND, HASX>(md), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)R::SMEM);
+    cudaFuncSetAttribute(rasm_for<P, KIND, HASX>(md), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)AL<P, KIND, HASX>::BYTES);
   if constexpr (KT<KIND>::VISC)
-    cudaFuncSetAttribute(k_rgrad<P, HASX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)R::SMEM);
+    cudaFuncSetAttribute(k_rgrad<P, HASX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GL<P, HASX>::BYTES);
 }
 
 template <int P, int KIND>
@@ -798,17 +920,21 @@ static int run_rect(const RectDev& rd, const DiscDev& d, const double* q, const 
   const unsigned ge = (unsigned)((d.M + R::EPB - 1) / R::EPB);
   const bool hx = X != nullptr;
   if (hx)
-    k_rface<P, KIND, true><<<gf, 128, 0, st>>>(d.C, m, q, X, eps, rd.fw, bad);
+    k_rface<P, KIND, true><<<gf, 128, 0, st>>>(d.C, m, q, X, eps, rd.frec, rd.wh, bad);
   else
-    k_rface<P, KIND, false><<<gf, 128, 0, st>>>(d.C, m, q, X, eps, rd.fw, bad);
+    k_rface<P, KIND, false><<<gf, 128, 0, st>>>(d.C, m, q, X, eps, rd.frec, rd.wh, bad);
   if constexpr (KT<KIND>::VISC) {
     if (hx)
-      launch_pdl_r(k_rgrad<P, true>, ge, R::TH, R::SMEM, st, d.C, m, q, X, eps, (const double*)rd.fw, d.fvn, bad);
+      launch_pdl_r(k_rgrad<P, true>, ge, R::TH, GL<P, true>::BYTES, st, d.C, m, q, X, eps,
+                   (const double*)rd.wh, rd.frec, bad);
     else
-      launch_pdl_r(k_rgrad<P, false>, ge, R::TH, R::SMEM, st, d.C, m, q, X, eps, (const double*)rd.fw, d.fvn, bad);
+      launch_pdl_r(k_rgrad<P, false>, ge, R::TH, GL<P, false>::BYTES, st, d.C, m, q, X, eps,
+                   (const double*)rd.wh, rd.frec, bad);
   }
+  launch_pdl_r(k_rfc<P, KIND>, gf, 128, 0, st, d.C, m, (const double*)rd.frec, rd.fc);
   RasmFn fn = hx ? rasm_for<P, KIND, true>(epi.mode) : rasm_for<P, KIND, false>(epi.mode);
-  launch_pdl_r(fn, ge, R::TH, R::SMEM, st, d.C, m, q, X, eps, (const double*)rd.fw, (const double*)d.fvn, epi, out,
+  const size_t smem = hx ? AL<P, KIND, true>::BYTES : AL<P, KIND, false>::BYTES;
+  launch_pdl_r(fn, ge, R::TH, smem, st, d.C, m, q, X, eps, (const double*)rd.wh, (const double*)rd.fc, epi, out,
                bad, stp);
   return (int)cudaGetLastError();
 }

@@ -150,7 +150,9 @@ struct RectDev {
   int4* faces = nullptr;    // {eL, fL | rev<<2 | bnd<<3 | tag<<4, eR, fR}
   int* fslot = nullptr;     // (M,4) face index of every element face
   double2* rgeo = nullptr;  // (M) {1/a0, 1/d0}
-  double* fw = nullptr;     // (nface, n, 8): interface flux F (L normal), BR1 What
+  double* frec = nullptr;   // (nface, n, 12): F (L normal), fvn of the L and R sides
+  double* wh = nullptr;     // (M, 4, n, 3): BR1 common value What per element side
+  double* fc = nullptr;     // (M, 4, n, 4): common total normal flux per element side
 };
 
 struct DiscDev {
