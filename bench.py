@@ -7,16 +7,20 @@ Workload (BASELINE.json configs[1], "config 2"): 256x256 periodic quad
 mesh, p=4 (25 points/element), compressible Navier-Stokes, Roe + BR1
 (SURVEY 8.0), isentropic vortex + seeded 1e-6 noise; 6,553,600 FP64 DoF.
 A "step" is one residual evaluation R(q) over the whole mesh; value =
-DoF-updates/s (GDoF/s) over all ranks.  Also timed: the fused Jv
-(the GMRES matvec) and one ESDIRK2 JFNK-pMG p{4-2} time step at config 2
-(the metric's second half), plus config 1's step beside the CPU oracle.
+DoF-updates/s (GDoF/s) over all ranks.  Also timed: the fused Jv (the
+GMRES matvec), BASELINE's Rusanov + LDG variant of the same R, ten
+ESDIRK3 JFNK-pMG p{4-2} time steps at config 2 (the metric's second
+half), config 1's step beside the CPU oracle, configs 3-5.
 
-Multi-GPU: the headline numbers are replicas (each rank its own config-2
-mesh: weak scaling, no data-path collective); the "partitioned" block
-times the sharded residual -- each rank a 256 x 256 slab of one
-256 x 256N periodic mesh with an NCCL halo exchange every step
-(paper_2202_09733_b200/partition.py).  Times are
-CUDA-event device times on the launching stream, max over ranks.
+Multi-GPU (N > 1): the headline is the PARTITIONED residual -- rank r
+owns a 256 x 256 slab of one 256 x 256N periodic mesh, and every timed
+step is the two-neighbour halo exchange (NCCL send/recv straight into the
+halo rows) + R on the rank's strip (paper_2202_09733_b200/partition.py,
+DESIGN.md section 6).  The replica number (each rank its own config-2
+mesh) is reported next to it.  At N = 1 the headline is the plain config-2
+mesh.  Times are CUDA-event device times on the launching stream, max over
+ranks.  The rank-0-only extras (steps, other configs, CPU baseline) run at
+N = 1 only.
 
 --impl reference: the reference arm -- the CPU oracle (NumPy restatement
 of the reference, oracle/, pinned to the reference's golden vectors)
@@ -47,6 +51,22 @@ UNIT = "GDoF/s"
 FLOP_PER_DOF_R = {2: 190.2, 3: 185.6, 4: 186.8, 5: 191.0}   # instrumented reference count
 BYTES_PER_DOF_R = 16.0                                          # read q + write R (compulsory)
 BYTES_PER_DOF_JV = 32.0                                         # read q, v, R0; write out
+
+
+def workload(case, config):
+    """The config dict both arms print (identical strings: same_config)."""
+    n1 = int(round(np.sqrt(case.mesh.n_elements)))
+    return {"workload": f"config{config}: R(u) over {case.mesh.n_elements} elements ({n1}^2 periodic), "
+                        f"p={case.p}, {case.n_dofs} DoF, NS Roe+BR1 (SURVEY 8.0)"}
+
+
+def src_hash():
+    """Hash of the CUDA sources: stamps the committed ncu traffic figure."""
+    import hashlib
+    h = hashlib.sha256()
+    for f in sorted((ROOT / "paper_2202_09733_b200" / "csrc").glob("*.cu*")):
+        h.update(f.read_bytes())
+    return h.hexdigest()[:16]
 
 
 def parse():
@@ -122,8 +142,7 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded isentropic vortex + 1e-6 noise, SURVEY 8(d))",
-        "config": {"workload": f"config{args.config}: R(u) over {case.mesh.n_elements} elements, p={case.p}, "
-                               f"{case.n_dofs} DoF, NS Roe+BR1", "parallelism": "cpu"},
+        "config": dict(workload(case, args.config), parallelism="cpu"),
         "cpu_baseline": {"value": rate, "unit": UNIT, "cores": T, "kind": "port",
                          "sample": f"{args.steps} full-mesh residual evaluations of config{args.config} "
                                    f"by the NumPy oracle (oracle/fr_oracle.py residual_mt), {T} threads"},
@@ -137,27 +156,55 @@ def run_reference(args):
 # clocks sampler (B200_PROFILING.md clocks line)
 
 class ClockSampler:
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clock / throttle-reason samples over a whole measurement (NVML
+    every 20 ms in a thread; nvidia-smi if NVML is unavailable)."""
+    NV_REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+                  "sw_power_cap": 0x4}
 
-    def __init__(self, gpu_index):
-        self.gpu = gpu_index
-        self.rows = []
+    def __init__(self, gpu_index, period=0.02):
+        self.gpu, self.period = gpu_index, period
+        self.sm, self.mx, self.reasons = [], [], []
         self._stop = threading.Event()
         self._thr = None
+        self._nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nvml = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(gpu_index)
+        except Exception:
+            self._nvml = None
+
+    def _sample_nvml(self):
+        nv = self._nvml
+        self.sm.append(float(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)))
+        self.mx.append(float(nv.nvmlDeviceGetMaxClockInfo(self._h, nv.NVML_CLOCK_SM)))
+        fn = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            getattr(nv, "nvmlDeviceGetCurrentClocksThrottleReasons")
+        mask = fn(self._h)
+        self.reasons.append({k for k, bit in self.NV_REASONS.items() if mask & bit})
+
+    def _sample_smi(self):
+        fields = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                  "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                  "clocks_event_reasons.sw_power_cap")
+        out = subprocess.run(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={fields}",
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                             timeout=5).stdout.strip()
+        r = [c.strip() for c in out.split(",")]
+        if len(r) >= 6 and r[0].replace(".", "").isdigit():
+            self.sm.append(float(r[0]))
+            self.mx.append(float(r[1]))
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            self.reasons.append({names[i] for i in range(4) if r[2 + i].lower().startswith("active")})
 
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([c.strip() for c in out.split(",")])
+                self._sample_nvml() if self._nvml else self._sample_smi()
             except Exception:
                 pass
-            self._stop.wait(0.1)
+            self._stop.wait(self.period if self._nvml else 0.1)
 
     def __enter__(self):
         self._thr = threading.Thread(target=self._run, daemon=True)
@@ -169,15 +216,11 @@ class ClockSampler:
         self._thr.join(timeout=10)
 
     def summary(self):
-        if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4)
-                          if len(r) > 5 + i and r[5 + i].lower().startswith("active")})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+        if not self.sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no clock samples"], "samples": 0}
+        return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": max(self.mx),
+                "reasons": sorted(set().union(*self.reasons)), "samples": len(self.sm),
+                "source": "NVML, 20 ms period, over every timed section" if self._nvml else "nvidia-smi"}
 
 
 # ---------------------------------------------------------------------------
@@ -211,6 +254,17 @@ def event_time(torch, fn, reps):
     return e0.elapsed_time(e1) * 1e-3
 
 
+def rotating(torch, case, disc, nbuf):
+    q0 = torch.as_tensor(case.q0, device="cuda")
+    n = disc.n_dofs
+    qs = [q0.clone() for _ in range(nbuf)]
+    Rs = [torch.empty_like(q0) for _ in range(nbuf)]
+    Xs = [torch.randn(n, dtype=torch.float64, device="cuda", generator=torch.Generator("cuda").manual_seed(i))
+          for i in range(nbuf)]
+    R0s = [disc.residual(q) for q in qs]
+    return qs, Rs, Xs, R0s
+
+
 def run_ours(args):
     import torch
     from paper_2202_09733_b200 import dist as pdist
@@ -228,18 +282,16 @@ def run_ours(args):
     disc = Discretization(case.mesh, case.p, case.eqn)
     n = disc.n_dofs
     st = stream()
-    fp64_peak = measure_fp64_peak(torch, lib, st)
     measured = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     hbm_peak = float(measured.get("hbm_gbs", 6650.0))
+    clk = ClockSampler(local)
+    clk.__enter__()
+    fp64_peak = measure_fp64_peak(torch, lib, st)
 
-    # 4 rotating q/R buffer pairs (4 x 105 MB > 126 MB L2)
-    q0 = torch.as_tensor(case.q0, device="cuda")
+    # plain config-2 mesh (the N = 1 headline; replicas at N > 1), 4
+    # rotating q/R buffer pairs (4 x 105 MB > 126 MB L2)
     nbuf = 4
-    qs = [q0.clone() for _ in range(nbuf)]
-    Rs = [torch.empty_like(q0) for _ in range(nbuf)]
-    Xs = [torch.randn(n, dtype=torch.float64, device="cuda", generator=torch.Generator("cuda").manual_seed(i))
-          for i in range(nbuf)]
-    R0s = [disc.residual(q) for q in qs]
+    qs, Rs, Xs, R0s = rotating(torch, case, disc, nbuf)
 
     def r_step(i):
         disc.eval(qs[i % nbuf], _lib.EPI_R, Rs[i % nbuf])
@@ -254,15 +306,28 @@ def run_ours(args):
     torch.cuda.synchronize()
     pdist.barrier()
     l0 = launch_count()
-    with ClockSampler(local) as clk:
-        t_r = event_time(torch, r_step, K)
+    t_r = event_time(torch, r_step, K)
     launches_r = launch_count() - l0
     t_jv = event_time(torch, jv_step, K)
     t_r, t_jv = pdist.max_over_ranks([t_r, t_jv], "cuda")
-    ms_r = t_r / K * 1e3
-    rate_r = pdist.job_rate(n * K, ws, t_r) / 1e9
+    rate_plain = pdist.job_rate(n * K, ws, t_r) / 1e9
     rate_jv = pdist.job_rate(n * K, ws, t_jv) / 1e9
     per_gpu_r = n / (t_r / K)
+    per_gpu_jv = n / (t_jv / K)
+
+    # the same R through the general (bilinear-element) kernels: A/B of the
+    # rectangle path on this mesh
+    path = disc.residual_path()
+    general = None
+    if path == "rect":
+        disc.residual_path("general")
+        for i in range(W):
+            r_step(i)
+        t_g = event_time(torch, r_step, K)
+        t_g, = pdist.max_over_ranks([t_g], "cuda")
+        general = {"r_gdofs": pdist.job_rate(n * K, ws, t_g) / 1e9, "r_ms": t_g / K * 1e3,
+                   "kernels": "k_trace_lines + k_fvn + k_assemble_async (csrc/fr_kernels.cu)"}
+        disc.residual_path("rect")
 
     # e2e through the public API with host buffers: every step copies its q
     # from pinned host memory, evaluates R and copies R back; the
@@ -283,7 +348,7 @@ def run_ours(args):
     e2e_ok = bool(np.array_equal(Rh[(K - 1) % 2].numpy(), disc.residual(qs[0]).cpu().numpy()))
     # the e2e ceiling: one step's H2D and D2H copies running concurrently
     s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
-    dq, dR = torch.empty_like(q0), torch.empty_like(q0)
+    dq, dR = torch.empty_like(qs[0]), torch.empty_like(qs[0])
 
     def duplex(i):
         with torch.cuda.stream(s_in):
@@ -297,54 +362,81 @@ def run_ours(args):
     t_dup = event_time(torch, duplex, K)
     t_dup, = pdist.max_over_ranks([t_dup], "cuda")
     ceil_e2e = pdist.job_rate(n * K, ws, t_dup) / 1e9
+    del qs, Rs, Xs, R0s
+    torch.cuda.empty_cache()
 
-    # the sharded residual with its halo exchange (all ranks take part)
+    # the sharded residual with its halo exchange (all ranks take part); an
+    # error on any rank is all-reduced so every rank leaves together
     try:
-        partitioned = time_partitioned(torch, case, K, W, ws, rank, args.no_step)
+        partitioned = time_partitioned(torch, case, K, W, ws, rank, args.no_step or ws > 1)
+        err = 0.0
     except Exception as exc:  # pragma: no cover
         partitioned = {"error": str(exc)[:200]}
+        err = 1.0
+    if max(pdist.max_over_ranks([err], "cuda")) > 0 and "error" not in partitioned:
+        partitioned = {"error": "another rank failed"}
 
-    # JFNK-pMG time step (the metric's second half)
-    step = {}
-    if not args.no_step and rank == 0:
-        step = time_steps(torch, case, args)
-    others = {}
-    if not args.no_configs and rank == 0 and args.config == 2:
-        others = time_other_configs(torch, args)
-    mbnk = {}
-    if not args.no_mbnk and rank == 0 and args.config == 2:
-        try:
-            mbnk = time_mbnk(torch, case)
-        except Exception as exc:  # pragma: no cover
-            mbnk = {"error": str(exc)[:200]}
+    # rank-0 extras (single GPU only: ranks > 0 would wait in a collective)
+    step, others, mbnk = {}, {}, {}
+    if ws == 1:
+        if not args.no_step:
+            step = time_steps(torch, case, args)
+        if not args.no_configs and args.config == 2:
+            others = time_other_configs(torch, args)
+            others["config2_rusanov_ldg"] = time_variant_r(torch, case, K, W, riemann="rusanov",
+                                                           viscous_scheme="ldg")
+        if not args.no_mbnk and args.config == 2:
+            try:
+                mbnk = time_mbnk(torch, case)
+            except Exception as exc:  # pragma: no cover
+                mbnk = {"error": str(exc)[:200]}
+    clk.__exit__()
 
     if rank != 0:
         pdist.barrier()
         return 0
 
+    if ws > 1 and "r_gdofs" in partitioned:
+        value, ms = partitioned["r_gdofs"], partitioned["ms_per_step"]
+        parallelism = f"dp{ws}: partitioned 256 x {256 * ws} mesh, halo send/recv per step (NCCL)"
+    else:
+        value, ms = rate_plain, t_r / K * 1e3
+        parallelism = "single GPU"
     flops = FLOP_PER_DOF_R[case.p] * n
     achieved = flops / (t_r / K) / 1e12
+    flops_jv = (FLOP_PER_DOF_R[case.p] + 4.0) * n
+    achieved_jv = flops_jv / (t_jv / K) / 1e12
+    kern = ("R(u): k_rface + k_rgrad + k_rfc + k_rasm (csrc/fr_rect.cu)" if path == "rect"
+            else "R(u): k_trace_lines + k_fvn + k_assemble_async (csrc/fr_kernels.cu)")
+    cfg = dict(workload(case, args.config), l2="4 rotating q/R buffer pairs (419 MB > 126 MB L2)",
+               parallelism=parallelism, residual_path=path)
     line = {
-        "metric": METRIC, "value": rate_r, "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": W,
-        "ms_per_step": ms_r, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": W,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded isentropic vortex + 1e-6 noise, SURVEY 8(d))",
-        "config": {"workload": f"config{args.config}: R(u) over {case.mesh.n_elements} elements "
-                               f"({int(np.sqrt(case.mesh.n_elements))}^2 periodic), p={case.p}, {n} DoF, "
-                               "NS Roe+BR1 (SURVEY 8.0)",
-                   "l2": "4 rotating q/R buffer pairs (419 MB > 126 MB L2)",
-                   "parallelism": f"replica x{ws}" if ws > 1 else "single GPU"},
+        "config": cfg,
+        "single_mesh": {"r_gdofs": rate_plain, "r_ms": t_r / K * 1e3,
+                        "what": "each rank its own config-2 mesh (replicas)" if ws > 1 else "config-2 mesh"},
         "jv_gdofs": rate_jv,
         "jv_ms": t_jv / K * 1e3,
+        "general_kernels": general,
         "roofline": {
-            "bound": "fp64", "kernel": "R(u): k_trace + k_fvn + k_assemble",
+            "bound": "fp64", "kernel": kern,
             "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak,
-            "peak_source": "measured in this run (DFMA probe, pmgb_probe_fp64)",
+            "peak_source": "measured in this run (DFMA probe, pmgb_probe_fp64; MEASURED_PEAKS.json has no FP64)",
             "flop_per_dof": FLOP_PER_DOF_R[case.p],
             "hbm_view": {"achieved_gbs": BYTES_PER_DOF_R * per_gpu_r / 1e9, "peak_gbs": hbm_peak,
                          "frac": BYTES_PER_DOF_R * per_gpu_r / 1e9 / hbm_peak,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
             "bound_gdofs": min(hbm_peak / BYTES_PER_DOF_R, fp64_peak * 1e3 / FLOP_PER_DOF_R[case.p]),
             "traffic": None,
+        },
+        "roofline_jv": {
+            "bound": "balanced (fp64 and hbm)", "achieved_tflops": achieved_jv, "fp64_frac": achieved_jv / fp64_peak,
+            "flop_per_dof": FLOP_PER_DOF_R[case.p] + 4.0, "bytes_per_dof": BYTES_PER_DOF_JV,
+            "achieved_gbs": BYTES_PER_DOF_JV * per_gpu_jv / 1e9,
+            "hbm_frac": BYTES_PER_DOF_JV * per_gpu_jv / 1e9 / hbm_peak,
+            "bound_gdofs": min(hbm_peak / BYTES_PER_DOF_JV, fp64_peak * 1e3 / (FLOP_PER_DOF_R[case.p] + 4.0)),
         },
         "e2e": {"value": rate_e2e, "unit": UNIT, "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
                 "api": "Discretization.residual_batch (pinned host in/out, copies overlapped with compute)",
@@ -360,24 +452,56 @@ def run_ours(args):
     }
     # CPU baseline: the oracle on this host, bounded sample
     try:
-        if args.no_cpu:
-            raise RuntimeError("skipped (--no-cpu)")
+        if args.no_cpu or ws > 1:
+            raise RuntimeError("skipped (--no-cpu or N > 1)")
         os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
         cpu_rate, best, ncall, T = cpu_residual_rate(case, seconds_budget=15.0)
         line["cpu_baseline"] = {"value": cpu_rate, "unit": UNIT, "cores": T, "kind": "port",
                                 "sample": f"best of {ncall} full-mesh oracle residual evaluations "
                                           f"(config{args.config}, residual_mt on {T} threads, {best:.2f} s each)"}
     except Exception as exc:  # pragma: no cover
-        line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 1, "kind": "port", "sample": f"failed: {exc}"}
-    prof = ROOT / "profiles" / "traffic_r1.json"
+        line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 1, "kind": "port", "sample": f"{exc}"}
+    # ncu DRAM bytes of one R, from the committed capture of the same kernel
+    # sources (stamped with their hash; "stale" if the kernels changed since)
+    prof = ROOT / "profiles" / "traffic_r2.json"
     if prof.exists():
         try:
-            line["roofline"]["traffic"] = json.loads(prof.read_text()).get(f"config{args.config}_R_bytes")
+            tr = json.loads(prof.read_text())
+            line["roofline"]["traffic"] = tr.get(f"config{args.config}_R_bytes")
+            line["roofline"]["traffic_source"] = {"file": "profiles/traffic_r2.json",
+                                                  "sources_match": tr.get("src_hash") == src_hash()}
         except Exception:
             pass
     print(json.dumps(line), flush=True)
     pdist.barrier()
     return 0
+
+
+def time_variant_r(torch, case, K, W, **eqn_changes):
+    """R rate of the config-2 mesh with other EquationSpec options
+    (BASELINE's literal Rusanov + LDG; parity unpinned)."""
+    import dataclasses
+
+    from paper_2202_09733_b200 import _lib
+    from paper_2202_09733_b200.spatial import Discretization
+    try:
+        eqn = dataclasses.replace(case.eqn, **eqn_changes)
+        d = Discretization(case.mesh, case.p, eqn)
+        nb = 4
+        q0 = torch.as_tensor(case.q0, device="cuda")
+        qs = [q0.clone() for _ in range(nb)]
+        Rs = [torch.empty_like(q0) for _ in range(nb)]
+        step = lambda i: d.eval(qs[i % nb], _lib.EPI_R, Rs[i % nb])  # noqa: E731
+        for i in range(W):
+            step(i)
+        t = event_time(torch, step, K)
+        rec = {"options": eqn_changes, "r_gdofs": d.n_dofs * K / t / 1e9, "r_ms": t / K * 1e3,
+               "residual_path": d.residual_path()}
+        del d, qs, Rs
+        torch.cuda.empty_cache()
+        return rec
+    except Exception as exc:  # pragma: no cover
+        return {"options": eqn_changes, "error": str(exc)[:200]}
 
 
 def time_other_configs(torch, args):
@@ -460,9 +584,10 @@ def time_other_configs(torch, args):
 def time_partitioned(torch, case2, K, W, ws, rank, no_step=False):
     """The sharded residual: rank r owns a 256 x 256 slab of a
     256 x 256N periodic box (the config-2 field on every slab, which is
-    y-periodic) plus 2 halo element rows each side; every step is one
-    all_gather halo exchange over NCCL + R on the local strip.  Owned DoF
-    per second over all ranks, device time max over ranks."""
+    y-periodic) plus 2 halo element rows each side; every step is the
+    two-neighbour halo exchange (NCCL send/recv into the halo rows) + R on
+    the local strip.  Owned DoF per second over all ranks, device time max
+    over ranks; halo bytes per rank and step reported."""
     from paper_2202_09733_b200 import dist as pdist
     from paper_2202_09733_b200.partition import PartitionedResidual, SlabPartition
     n1 = int(round(np.sqrt(case2.mesh.n_elements)))
@@ -482,10 +607,14 @@ def time_partitioned(torch, case2, K, W, ws, rank, no_step=False):
     t_x = event_time(torch, xchg, K)
     t_r, t_x = pdist.max_over_ranks([t_r, t_x], "cuda")
     owned = part.rows * n1 * sz
+    halo_bytes = 2 * 2 * part.halo * n1 * sz * 8  # sent + received, both sides
     rec = {"global_mesh": f"{n1} x {n1 * ws} periodic, {ws} slab(s) of {n1} x {n1}", "halo_rows": part.halo,
-           "collective": "all_gather of the slabs' boundary rows (NCCL)" if ws > 1 else "local wrap copy",
+           "collective": "send/recv of 2 halo rows to each neighbour (NCCL, batch_isend_irecv)" if ws > 1
+           else "local wrap copy",
            "r_gdofs": owned * K * ws / t_r / 1e9, "ms_per_step": t_r / K * 1e3,
-           "exchange_ms": t_x / K * 1e3, "local_dofs_per_rank": pr.disc.n_dofs, "owned_dofs_per_rank": owned}
+           "exchange_ms": t_x / K * 1e3, "halo_bytes_per_rank_step": halo_bytes if ws > 1 else 0,
+           "local_dofs_per_rank": pr.disc.n_dofs, "owned_dofs_per_rank": owned,
+           "residual_path": pr.disc.residual_path()}
     del pr, out
     if no_step:
         return rec
@@ -571,9 +700,11 @@ def time_mbnk(torch, case2):
 
 def time_steps(torch, case2, args):
     """JFNK-pMG time steps (after one warm-up step each): config 1 (one
-    ESDIRK3 step, beside the CPU oracle's same step) and config 2 (ESDIRK3
-    with the reference's EJ smoothers, and with the pseudo-transient RK
-    smoother on the fine level -- north star item 3)."""
+    ESDIRK3 step, beside the CPU oracle's same step) and config 2 (BASELINE's
+    ten ESDIRK3 steps with the reference's EJ smoothers in FP64, marching
+    the solution; one step with the pseudo-transient RK smoother on the fine
+    level -- north star item 3 -- and one with FP32-stored EJ factors).
+    Step times are CUDA-event times on the solver's stream."""
     from paper_2202_09733_b200 import cases
     from paper_2202_09733_b200 import time_integration as ti
     from paper_2202_09733_b200.harness import ImplicitDriver
@@ -594,17 +725,25 @@ def time_steps(torch, case2, args):
         sch = ti.get_scheme(c.scheme)
         rec = {"scheme": c.scheme, "pmg": c.levels, "smoothers": smoothers, "block_precision": prec,
                "smoother_shift": c.extra["smoother_shift"], "dt": c.dt}
+        nsteps = c.steps if key == "config2" else 1
         try:
             drv = ImplicitDriver(d, cfg)
             drv.step(q, c.dt, sch)  # warm-up (allocator + caches)
             torch.cuda.synchronize()
             torch.cuda.reset_peak_memory_stats()
             drv = ImplicitDriver(d, cfg)
-            t0 = time.perf_counter()
-            q1, info = drv.step(q, c.dt, sch)
-            torch.cuda.synchronize()
-            rec.update(gpu_s=time.perf_counter() - t0, ptc_iters=[i["iters"] for i in info],
-                       gmres_iters=[i["gmres_iters"] for i in info],
+            times, ptc, gm = [], [], []
+            for _ in range(nsteps):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                q, info = drv.step(q, c.dt, sch)
+                e1.record()
+                e1.synchronize()
+                times.append(e0.elapsed_time(e1) * 1e-3)
+                ptc.append([i["iters"] for i in info])
+                gm.append([i["gmres_iters"] for i in info])
+            rec.update(gpu_s=statistics.mean(times), steps=nsteps, step_s=times, ptc_iters=ptc if nsteps > 1 else ptc[0],
+                       gmres_iters=gm if nsteps > 1 else gm[0],
                        peak_device_gb=torch.cuda.max_memory_allocated() / 1e9)
             del drv
         except Exception as exc:

@@ -1,6 +1,7 @@
 // extern "C" boundary of libpmgflow_b200.so -- see include/pmgflow_b200.h.
 #include <atomic>
 #include <climits>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -78,6 +79,8 @@ PMGB_API const char* pmgb_error_string(int code) {
 static int setup_rect(const pmgb_disc_desc* desc, DiscDev& d) {
   d.has_rect = 0;
   if (!rect_supported(d.p, d.kind) || d.M == 0) return 0;
+  const char* env = std::getenv("PMGB_RECT");  // PMGB_RECT=0: general kernels only (A/B)
+  if (env != nullptr && env[0] == '0') return 0;
   const double* G = desc->geom;
   std::vector<double2> rg((size_t)d.M);
   for (int64_t e = 0; e < d.M; ++e) {
@@ -249,7 +252,9 @@ PMGB_API int pmgb_eval(pmgb_disc* h, const double* q, const double* X, double ep
   ep.alpha = e->alpha;
   ep.npe = (int)((h->d.p + 1) * (h->d.p + 1) * h->d.nv);
   if (ep.mode == EPI_RK && (!ep.Q0 || !ep.dtau_e)) return -1;
-  g_launches += n_res_launches(h->d);
+  // rectangle path: k_rface (+ k_rgrad for NS) + k_rfc + k_rasm
+  const bool rect = h->d.has_rect && rect_supported(h->d.p, h->d.kind);
+  g_launches += rect ? (h->d.kind == K_NS ? 4 : 3) : n_res_launches(h->d);
   return launch_residual(h->d, q, X, eps, ep, out, S(stream));
 }
 

@@ -1937,15 +1937,6 @@ static void launch_pdl(void (*kernel)(KArgs...), unsigned grid, int threads, siz
   cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 
-// PMGB_RECT=0 forces the general (bilinear) kernels on rectangle meshes (A/B)
-static bool rect_enabled() {
-  static const bool on = [] {
-    const char* v = std::getenv("PMGB_RECT");
-    return v == nullptr || v[0] != '0';
-  }();
-  return on;
-}
-
 // PMGB_EPI_SPECIALIZE=0 forces the runtime-switch instantiation (A/B)
 static bool epi_specialize() {
   static const bool on = [] {
@@ -2014,7 +2005,7 @@ static int run_residual(const DiscDev& d, const double* q, const double* X, doub
   Status* stp = nullptr;
   cudaGetSymbolAddress((void**)&bad, g_bad);
   cudaGetSymbolAddress((void**)&stp, g_status);
-  if (d.has_rect && rect_enabled() && rect_supported(P, KIND))
+  if (d.has_rect && rect_supported(P, KIND))
     return launch_residual_rect(d.rect, d, q, X, eps, epi, out, bad, stp, st);
   const unsigned grid = (unsigned)((d.M + E - 1) / E);
   const double* qq = q;

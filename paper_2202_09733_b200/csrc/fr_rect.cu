@@ -55,6 +55,30 @@ struct RectMesh {
   const double* __restrict__ geom;   // (M,20) for the face normals
 };
 
+// Line-block transpose layouts: value pos of line `line` of element el at
+// el * S + line * BS + pos.  Row threads write column blocks (scattered
+// 64-bit stores), column threads read their own block (64-bit loads); S and
+// BS are the smallest strides that keep both patterns at the minimum
+// number of shared-memory wavefronts per warp (or close to it), from an
+// exhaustive search over the thread -> (element, line) map of the CTA
+// (tools/bank_model.py): V = 3 values per line point (W, gx, gy), V = 4
+// (fy, X_xi).
+template <int N, int V> struct TL;
+template <> struct TL<2, 3> { static constexpr int BS = 7, S = 14; };
+template <> struct TL<2, 4> { static constexpr int BS = 9, S = 18; };
+template <> struct TL<3, 3> { static constexpr int BS = 17, S = 51; };
+template <> struct TL<3, 4> { static constexpr int BS = 17, S = 51; };
+template <> struct TL<4, 3> { static constexpr int BS = 13, S = 52; };
+template <> struct TL<4, 4> { static constexpr int BS = 17, S = 68; };
+template <> struct TL<5, 3> { static constexpr int BS = 17, S = 85; };
+template <> struct TL<5, 4> { static constexpr int BS = 20, S = 101; };
+template <> struct TL<6, 3> { static constexpr int BS = 21, S = 126; };
+template <> struct TL<6, 4> { static constexpr int BS = 25, S = 150; };
+template <int N, int V>
+__host__ __device__ constexpr int tl(int el, int line, int pos) {
+  return el * TL<N, V>::S + line * TL<N, V>::BS + pos;
+}
+
 // per-face-point record of the unique-face array: F on L's normal, then the
 // one-sided viscous fluxes of the L and R sides on their own normals
 constexpr int FREC = 12;
@@ -65,8 +89,7 @@ template <int P> struct RC {
   static constexpr int TH = EPB * N;   // one thread per (element, line)
   // line block strides in doubles: >= 3N (gradient passes) / 4N (flux
   // passes), even, an odd number of 16-byte units
-  static constexpr int odd16(int x) { return ((x + 1) / 2) % 2 == 1 ? (x + 1) / 2 * 2 : (x + 1) / 2 * 2 + 2; }
-  static constexpr int BS3 = odd16(3 * N), BS4 = odd16(4 * N);
+
   static constexpr int QD = EPB * NP * 4;   // doubles of a q block
   static constexpr int WD = EPB * 4 * N * 3;  // of a What block
   static constexpr int FD = EPB * 4 * N * 4;  // of an Fc block
@@ -429,7 +452,7 @@ __device__ __forceinline__ void line_div(const FrConst& C, const double (&x)[4][
 // line-block transposes
 template <int P, bool HASX> struct GL {
   using R = RC<P>;
-  static constexpr int BUF = R::EPB * R::N * R::BS3;
+  static constexpr int BUF = R::EPB * TL<R::N, 3>::S;
   static constexpr int A = 2 * BUF, B = R::WD + (HASX ? R::QD : 0);
   static constexpr int STAGE = A > B ? A : B;
   static constexpr int OFF_W = R::QD + STAGE - R::WD, OFF_BAR = R::QD + STAGE;
@@ -442,7 +465,7 @@ k_rgrad(const FrConst C, const RectMesh m, const double* __restrict__ q, const d
         const double* __restrict__ wh, double* __restrict__ frec, int* __restrict__ bad) {
   using R = RC<P>;
   using L = GL<P, HASX>;
-  constexpr int N = R::N, NP = R::NP, E = R::EPB, BS = R::BS3;
+  constexpr int N = R::N, NP = R::NP, E = R::EPB;
   extern __shared__ __align__(128) double sm[];
   double* sQ = sm;
   double* sX = sm + R::QD;            // X block; then W, then gx (column blocks)
@@ -532,7 +555,7 @@ k_rgrad(const FrConst C, const RectMesh m, const double* __restrict__ q, const d
 #pragma unroll
   for (int i = 0; i < N; ++i)
 #pragma unroll
-    for (int c = 0; c < 3; ++c) sX[(el * N + i) * BS + c * N + a] = w[c][i];
+    for (int c = 0; c < 3; ++c) sX[tl<N, 3>(el, i, c * N + a)] = w[c][i];
   // gx along row a (faces 1 and 3)
   double gx[3][N];
   line_gradient<N>(C, w, whv[1], whv[3], rg.x, gx);
@@ -540,7 +563,7 @@ k_rgrad(const FrConst C, const RectMesh m, const double* __restrict__ q, const d
   // column a: W of the column, gy (faces 2 and 0)
   double gy[3][N];
   {
-    const double* blk = sX + t * BS;
+    const double* blk = sX + tl<N, 3>(el, a, 0);
 #pragma unroll
     for (int c = 0; c < 3; ++c)
 #pragma unroll
@@ -553,8 +576,8 @@ k_rgrad(const FrConst C, const RectMesh m, const double* __restrict__ q, const d
   for (int i = 0; i < N; ++i)
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      sX[(el * N + i) * BS + c * N + a] = gx[c][i];
-      sY[(el * N + i) * BS + c * N + a] = gy[c][i];
+      sX[tl<N, 3>(el, i, c * N + a)] = gx[c][i];
+      sY[tl<N, 3>(el, i, c * N + a)] = gy[c][i];
     }
   // traces of the own-line components: gx on faces 1/3, gy on faces 0/2
   double tgx1[3], tgx3[3], tgy0[3], tgy2[3];
@@ -578,7 +601,7 @@ k_rgrad(const FrConst C, const RectMesh m, const double* __restrict__ q, const d
   // rows: gy along row a -> gy traces on faces 1/3; columns: gx -> faces 0/2
   double tgy1[2], tgy3[2], tgx0[2], tgx2[2];
   {
-    const double* blk = sY + t * BS;
+    const double* blk = sY + tl<N, 3>(el, a, 0);
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
       double s1 = 0.0, s3 = 0.0;
@@ -591,7 +614,7 @@ k_rgrad(const FrConst C, const RectMesh m, const double* __restrict__ q, const d
       tgy1[c] = s1;
       tgy3[c] = s3;
     }
-    const double* bx = sX + t * BS;
+    const double* bx = sX + tl<N, 3>(el, a, 0);
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
       double s0 = 0.0, s2 = 0.0;
@@ -650,7 +673,8 @@ k_rgrad(const FrConst C, const RectMesh m, const double* __restrict__ q, const d
 template <int P, int KIND, bool HASX> struct AL {
   using R = RC<P>;
   static constexpr bool VISC = KT<KIND>::VISC;
-  static constexpr int BUF = R::EPB * R::N * R::BS4;
+  static constexpr int S_ = TL<R::N, 3>::S > TL<R::N, 4>::S ? TL<R::N, 3>::S : TL<R::N, 4>::S;
+  static constexpr int BUF = R::EPB * S_;
   static constexpr int WD = VISC ? R::WD : 0;
   static constexpr int A = 2 * BUF, B = WD + R::FD + (HASX ? R::QD : 0);
   static constexpr int STAGE = A > B ? A : B;
@@ -665,7 +689,7 @@ k_rasm(const FrConst C, const RectMesh m, const double* __restrict__ q, const do
        int* bad, Status* st) {
   using R = RC<P>;
   using L = AL<P, KIND, HASX>;
-  constexpr int N = R::N, NP = R::NP, E = R::EPB, BS = R::BS4;
+  constexpr int N = R::N, NP = R::NP, E = R::EPB;
   constexpr bool VISC = KT<KIND>::VISC;
   extern __shared__ __align__(128) double sm[];
   double* sQ = sm;
@@ -737,11 +761,11 @@ k_rasm(const FrConst C, const RectMesh m, const double* __restrict__ q, const do
 #pragma unroll
     for (int i = 0; i < N; ++i)
 #pragma unroll
-      for (int c = 0; c < 3; ++c) sX[(el * N + i) * BS + c * N + a] = w[c][i];
+      for (int c = 0; c < 3; ++c) sX[tl<N, 3>(el, i, c * N + a)] = w[c][i];
     __syncthreads();
     // column a: gy -> row blocks
     {
-      const double* blk = sX + t * BS;
+      const double* blk = sX + tl<N, 3>(el, a, 0);
 #pragma unroll
       for (int c = 0; c < 3; ++c)
 #pragma unroll
@@ -751,10 +775,10 @@ k_rasm(const FrConst C, const RectMesh m, const double* __restrict__ q, const do
 #pragma unroll
       for (int i = 0; i < N; ++i)
 #pragma unroll
-        for (int c = 0; c < 3; ++c) sY[(el * N + i) * BS + c * N + a] = gc[c][i];
+        for (int c = 0; c < 3; ++c) sY[tl<N, 3>(el, i, c * N + a)] = gc[c][i];
     }
     __syncthreads();
-    const double* blk = sY + t * BS;
+    const double* blk = sY + tl<N, 3>(el, a, 0);
 #pragma unroll
     for (int c = 0; c < 3; ++c)
 #pragma unroll
@@ -814,7 +838,7 @@ k_rasm(const FrConst C, const RectMesh m, const double* __restrict__ q, const do
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
       fx[v][i] = Fx[v];
-      sX[(el * N + i) * BS + v * N + a] = Fy[v];
+      sX[tl<N, 4>(el, i, v * N + a)] = Fy[v];
     }
   }
   // X_xi along row a
@@ -824,13 +848,13 @@ k_rasm(const FrConst C, const RectMesh m, const double* __restrict__ q, const do
 #pragma unroll
   for (int i = 0; i < N; ++i)
 #pragma unroll
-    for (int v = 0; v < 4; ++v) sY[(el * N + i) * BS + v * N + a] = xx[v][i];
+    for (int v = 0; v < 4; ++v) sY[tl<N, 4>(el, i, v * N + a)] = xx[v][i];
   __syncthreads();
   if (!live) return;
   // column a: fy and X_xi of the column, faces 2 / 0, X_eta, R, epilogue
   double fyc[4][N];
   {
-    const double* blk = sX + t * BS;
+    const double* blk = sX + tl<N, 4>(el, a, 0);
 #pragma unroll
     for (int v = 0; v < 4; ++v)
 #pragma unroll
@@ -838,7 +862,7 @@ k_rasm(const FrConst C, const RectMesh m, const double* __restrict__ q, const do
   }
   double xe[4][N];
   line_div<N>(C, fyc, fcv[2], fcv[0], xe);
-  const double* bx = sY + t * BS;
+  const double* bx = sY + tl<N, 4>(el, a, 0);
   constexpr bool NEEDQ = !(EK == EPI_R || EK == EPI_JV || EK == EPI_NEG_R);
   const double ce = (EK == EPI_RK) ? epi_rk_coef(ep, e) : 0.0;
 #pragma unroll
@@ -847,15 +871,26 @@ k_rasm(const FrConst C, const RectMesh m, const double* __restrict__ q, const do
     double qv[4] = {0, 0, 0, 0};
     if constexpr (NEEDQ) lds4(sQ + ((el * N + i) * N + a) * 4, qv);
     double o[4];
+    if constexpr (EK == EPI_JV) {  // out = s X - (R - R0)/eps, operands as 256-bit loads
+      double xv[4], r0[4];
+      ldg4(ep.X + pt * 4, xv);
+      ldg4(ep.R0 + pt * 4, r0);
 #pragma unroll
-    for (int v = 0; v < 4; ++v) {
-      const double Rv = -(rg.x * bx[v * N + i] + rg.y * xe[v][i]);
-      if constexpr (EK == EPI_R) {
-        o[v] = Rv;
-      } else {
-        double o1, o2, o3;
-        epi_load_k<EK>(ep, pt * 4 + v, o1, o2, o3);
-        o[v] = (EK == EPI_RK) ? epi_rk(ep, ce, Rv, qv[v], o1, o2, o3) : epi_pre_k<EK>(ep, Rv, qv[v], o1, o2, o3);
+      for (int v = 0; v < 4; ++v) {
+        const double Rv = -(rg.x * bx[v * N + i] + rg.y * xe[v][i]);
+        o[v] = epi_pre_k<EK>(ep, Rv, 0.0, xv[v], r0[v], 0.0);
+      }
+    } else {
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const double Rv = -(rg.x * bx[v * N + i] + rg.y * xe[v][i]);
+        if constexpr (EK == EPI_R) {
+          o[v] = Rv;
+        } else {
+          double o1, o2, o3;
+          epi_load_k<EK>(ep, pt * 4 + v, o1, o2, o3);
+          o[v] = (EK == EPI_RK) ? epi_rk(ep, ce, Rv, qv[v], o1, o2, o3) : epi_pre_k<EK>(ep, Rv, qv[v], o1, o2, o3);
+        }
       }
     }
     stg4(out + pt * 4, o);
