@@ -260,10 +260,19 @@ PMGB_API int pmgb_mgs_pass(int64_t n, double* w, const double* Vprev, const doub
                            double* out, int32_t first, int32_t* finite_dev, void* stream);
 PMGB_API int pmgb_normalize_sqrt(int64_t n, const double* w, double* h_dev, double thresh, double* v,
                                  void* stream);
+/* Classical Gram-Schmidt with reorthogonalisation (option gmres.ortho =
+ * cgs2; the reference orthogonalises by MGS, newton_krylov.py:119-123):
+ * pmgb_multidot sets out_dev[c] = V_c . w for c < k <= 256 (rows of V at
+ * stride ld; deterministic order; *finite_dev |= non-finite w, may be
+ * NULL) and pmgb_gemv_sub does w -= V[0:k]^T y_dev. */
+PMGB_API int pmgb_multidot(int64_t n, const double* V, int64_t ld, int32_t k, const double* w, double* out_dev,
+                           int32_t* finite_dev, void* stream);
+PMGB_API int pmgb_gemv_sub(int64_t n, int32_t k, const double* V, int64_t ld, const double* y_dev, double* w,
+                           void* stream);
 /* out = sum_i c[i] x[i], k <= 8, c and the pointer array on the HOST. */
 PMGB_API int pmgb_lincomb(int64_t n, int32_t k, const double* c, const double* const* xs, double* out,
                           void* stream);
-/* out = V[0:k]^T y, y on the device (k <= 128). */
+/* out = V[0:k]^T y, y on the device (k <= 28992). */
 PMGB_API int pmgb_gemv_t(int64_t n, int32_t k, const double* V, int64_t ld, const double* y_dev, double* out,
                          void* stream);
 /* *flag_dev = any(x != 0) */

@@ -49,7 +49,10 @@ def _back_substitute(H, g):
     return y
 
 
-def gmres_solve(matvec, b, kdim=30, max_restarts=10, rtol=1e-4, x0=None, precond=None):
+def gmres_solve(matvec, b, kdim=30, max_restarts=10, rtol=1e-4, x0=None, precond=None, ortho="mgs"):
+    """newton_krylov.py:79-151; ortho = "cgs2" restates the device option
+    (classical Gram-Schmidt + one reorthogonalisation pass; not in the
+    reference)."""
     n = len(b)
     bnorm = float(np.sqrt(b @ b))
     x = np.zeros(n) if x0 is None else x0.copy()
@@ -74,9 +77,16 @@ def gmres_solve(matvec, b, kdim=30, max_restarts=10, rtol=1e-4, x0=None, precond
             w = matvec(P(V[j]))
             if not np.all(np.isfinite(w)):
                 raise RuntimeError(f"non-finite Arnoldi vector at inner iteration {total + 1}")
-            for i in range(j + 1):
-                H[i, j] = V[i] @ w
-                w = w - H[i, j] * V[i]
+            if ortho == "cgs2":
+                h1 = V[:j + 1] @ w
+                w = w - V[:j + 1].T @ h1
+                h2 = V[:j + 1] @ w
+                w = w - V[:j + 1].T @ h2
+                H[:j + 1, j] = h1 + h2
+            else:
+                for i in range(j + 1):
+                    H[i, j] = V[i] @ w
+                    w = w - H[i, j] * V[i]
             H[j + 1, j] = float(np.sqrt(w @ w))
             total += 1
             if H[j + 1, j] > 1e-14 * bnorm:
@@ -553,9 +563,9 @@ class Driver:
 
     def __init__(self, disc: OracleDisc, precond="pmg", levels="3-2", smooth=2, smoother_shift=0.0,
                  kdim=30, max_restarts=10, gmres_rtol=1e-3, dtau_init=1e-3, ptc_rtol=1e-4,
-                 max_iters=100, max_halvings=8, smoother="ej", rk_cfl=RK_CFL, rk_alphas=RK_ALPHAS):
+                 max_iters=100, max_halvings=8, smoother="ej", rk_cfl=RK_CFL, rk_alphas=RK_ALPHAS, ortho="mgs"):
         self.disc, self.precond = disc, precond
-        self.krylov = dict(kdim=kdim, max_restarts=max_restarts, rtol=gmres_rtol)
+        self.krylov = dict(kdim=kdim, max_restarts=max_restarts, rtol=gmres_rtol, ortho=ortho)
         self.ptc = dict(dtau_init=dtau_init, rtol=ptc_rtol, max_iters=max_iters, max_halvings=max_halvings)
         self.ctx = (Pmg(disc, levels, smooth, smoother_shift=smoother_shift, smoother=smoother, rk_cfl=rk_cfl,
                         rk_alphas=rk_alphas) if precond == "pmg" else None)

@@ -105,6 +105,10 @@ SIGNATURES = {
     "pmgb_gemv_t": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int32, c_void_p, ctypes.c_int64, c_void_p,
                                    c_void_p, c_void_p]),
     "pmgb_any_nonzero": (ctypes.c_int, [ctypes.c_int64, c_void_p, c_void_p, c_void_p]),
+    "pmgb_multidot": (ctypes.c_int, [ctypes.c_int64, c_void_p, ctypes.c_int64, ctypes.c_int32, c_void_p, c_void_p,
+                                     c_void_p, c_void_p]),
+    "pmgb_gemv_sub": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int32, c_void_p, ctypes.c_int64, c_void_p, c_void_p,
+                                     c_void_p]),
     "pmgb_status": (ctypes.c_int, [c_void_p, c_int32_p, c_int64_p, ctypes.c_int32]),
     "pmgb_status_clear": (ctypes.c_int, [c_void_p]),
     "pmgb_sync": (ctypes.c_int, [c_void_p]),

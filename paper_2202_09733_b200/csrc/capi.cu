@@ -37,6 +37,9 @@ int launch_lincomb(int64_t n, int k, const double* c, const double* const* xs, d
 int launch_rk_dtau(int64_t M, const double* lam, double s, double cfl, double* dtau, cudaStream_t st);
 int launch_gemv_t(int64_t n, int k, const double* V, int64_t ld, const double* y, double* out, cudaStream_t st);
 int launch_any_nonzero(int64_t n, const double* x, int* flag_dev, cudaStream_t st);
+int launch_multidot(int64_t n, const double* V, int64_t ld, int k, const double* w, double* out, int* flag,
+                    cudaStream_t st);
+int launch_gemv_sub(int64_t n, int k, const double* V, int64_t ld, const double* y, double* w, cudaStream_t st);
 int launch_probe_fp64(int64_t iters, int blocks, double* out, cudaStream_t st);
 Status* status_ptr();
 }  // namespace pmgb
@@ -472,6 +475,20 @@ PMGB_API int pmgb_mgs_pass(int64_t n, double* w, const double* Vprev, const doub
   if (n < 0 || !w || !Vnext || !out || (Vprev && !hprev)) return -1;
   g_launches += 1;
   return launch_mgs_pass(n, w, Vprev, hprev, Vnext, out, first, finite_dev, S(stream));
+}
+
+PMGB_API int pmgb_multidot(int64_t n, const double* V, int64_t ld, int32_t k, const double* w, double* out_dev,
+                           int32_t* finite_dev, void* stream) {
+  if (n < 0 || !V || !w || !out_dev) return -1;
+  g_launches += 1;
+  return launch_multidot(n, V, ld, k, w, out_dev, finite_dev, S(stream));
+}
+
+PMGB_API int pmgb_gemv_sub(int64_t n, int32_t k, const double* V, int64_t ld, const double* y_dev, double* w,
+                           void* stream) {
+  if (n < 0 || !V || !y_dev || !w) return -1;
+  g_launches += 1;
+  return launch_gemv_sub(n, k, V, ld, y_dev, w, S(stream));
 }
 
 PMGB_API int pmgb_normalize_sqrt(int64_t n, const double* w, double* h_dev, double thresh, double* v,

@@ -369,6 +369,135 @@ int launch_any_nonzero(int64_t n, const double* x, int* flag_dev, cudaStream_t s
   return (int)cudaGetLastError();
 }
 
+
+// ---------------------------------------------------------------------------
+// Classical Gram-Schmidt with reorthogonalisation (CGS2, option
+// gmres.ortho = cgs2): one multi-dot per pass, so a partitioned Arnoldi
+// step needs 3 all-reduces instead of the MGS order's j + 2.
+
+constexpr int MD_BLOCKS = 148 * 4, MD_THREADS = 256, MD_CH = 8, MD_KMAX = 256;
+
+struct MdScratch {
+  double* partial;     // MD_BLOCKS * MD_KMAX
+  unsigned int* counter;
+};
+static std::map<RedKey, MdScratch> g_md;
+
+static int md_scratch(MdScratch* out, cudaStream_t st) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return (int)e;
+  std::lock_guard<std::mutex> lock(g_red_mu);
+  auto it = g_md.find(RedKey{dev, st});
+  if (it == g_md.end()) {
+    void* p = nullptr;
+    const size_t bytes = sizeof(double) * MD_BLOCKS * MD_KMAX + 64;
+    e = cudaMalloc(&p, bytes);
+    if (e == cudaSuccess) e = cudaMemset(p, 0, bytes);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return (int)e;
+    MdScratch ms;
+    ms.partial = (double*)p;
+    ms.counter = (unsigned int*)((char*)p + sizeof(double) * MD_BLOCKS * MD_KMAX);
+    it = g_md.emplace(RedKey{dev, st}, ms).first;
+  }
+  *out = it->second;
+  return 0;
+}
+
+// block-wide sum of one value per thread, valid in thread 0; safe to call
+// back to back (trailing barrier)
+__device__ __forceinline__ double block_sum_md(double v, double* ws) {
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) ws[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x < 32) {
+    s = (lane < MD_THREADS / 32) ? ws[lane] : 0.0;
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off);
+  }
+  __syncthreads();
+  return s;
+}
+
+// out[c] = V_c . w for c < k (fixed grid, fixed per-thread order, fixed
+// trees, last block sums the partials in block order: deterministic);
+// flag |= any non-finite w
+__global__ void __launch_bounds__(MD_THREADS) k_multidot(int64_t n, const double* __restrict__ V, int64_t ld, int k,
+                                                         const double* __restrict__ w, double* __restrict__ out,
+                                                         int* flag, MdScratch ms) {
+  __shared__ double ws[MD_THREADS / 32];
+  __shared__ bool last;
+  bool bad = false;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int c0 = 0; c0 < k; c0 += MD_CH) {
+    double acc[MD_CH];
+#pragma unroll
+    for (int c = 0; c < MD_CH; ++c) acc[c] = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+      const double wi = w[i];
+      if (c0 == 0 && !isfinite(wi)) bad = true;
+#pragma unroll
+      for (int c = 0; c < MD_CH; ++c)
+        if (c0 + c < k) acc[c] += V[(int64_t)(c0 + c) * ld + i] * wi;
+    }
+#pragma unroll
+    for (int c = 0; c < MD_CH; ++c) {
+      if (c0 + c >= k) break;
+      const double sblk = block_sum_md(acc[c], ws);
+      if (threadIdx.x == 0) ms.partial[(int64_t)blockIdx.x * MD_KMAX + c0 + c] = sblk;
+    }
+  }
+  if (flag != nullptr && __syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(ms.counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int c = 0; c < k; ++c) {
+    double v = 0.0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x)
+      v += ((volatile double*)ms.partial)[(int64_t)b * MD_KMAX + c];
+    v = block_sum_md(v, ws);
+    if (threadIdx.x == 0) out[c] = v;
+  }
+  if (threadIdx.x == 0) *ms.counter = 0u;
+}
+
+int launch_multidot(int64_t n, const double* V, int64_t ld, int k, const double* w, double* out, int* flag,
+                    cudaStream_t st) {
+  if (k < 1 || k > MD_KMAX) return -1001;
+  MdScratch ms;
+  int e = md_scratch(&ms, st);
+  if (e) return e;
+  k_multidot<<<MD_BLOCKS, MD_THREADS, 0, st>>>(n, V, ld, k, w, out, flag, ms);
+  return (int)cudaGetLastError();
+}
+
+// w -= V[0:k]^T y (y on the device; the sum in gemv_t's order, then one
+// subtraction)
+__global__ void k_gemv_sub(int64_t n, int k, const double* __restrict__ V, int64_t ld, const double* y,
+                           double* __restrict__ w) {
+  extern __shared__ double ys[];
+  for (int j = threadIdx.x; j < k; j += blockDim.x) ys[j] = y[j];
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    double s = 0.0;
+    for (int j = 0; j < k; ++j) s += V[(int64_t)j * ld + i] * ys[j];
+    w[i] = w[i] - s;
+  }
+}
+
+int launch_gemv_sub(int64_t n, int k, const double* V, int64_t ld, const double* y, double* w, cudaStream_t st) {
+  if (k < 1 || k > MD_KMAX) return -1001;
+  k_gemv_sub<<<ew_grid(n), 256, sizeof(double) * k, st>>>(n, k, V, ld, y, w);
+  return (int)cudaGetLastError();
+}
+
 }  // namespace pmgb
 
 namespace pmgb {

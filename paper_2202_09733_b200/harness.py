@@ -31,7 +31,7 @@ DEFAULTS = {
     "ptc.dtau_init": 1e-3, "ptc.dtau_max": 1e12, "ptc.max_iters": 100, "ptc.rtol": 1e-4,
     "ptc.atol": None, "ptc.ser": True, "ptc.ser_as_printed": False, "ptc.refresh_every_n_ptc": 0,
     "ptc.max_halvings": 8,
-    "gmres.kdim": 30, "gmres.max_restarts": 10, "gmres.rtol": 1e-4,
+    "gmres.kdim": 30, "gmres.max_restarts": 10, "gmres.rtol": 1e-4, "gmres.ortho": "mgs",
     "pmg.levels": "3-1", "pmg.smooth": "2", "pmg.smoother": "ej", "pmg.switch_after": None,
     "pmg.mbnk.rtol": 0.1, "pmg.mbnk.maxiter": 5, "pmg.smoother_shift": 0.0,
     "pmg.rk.cfl": 1.5, "pmg.rk.stages": "0.25,0.3333333333333333,0.5,1.0", "pmg.block_precision": "fp64",
@@ -104,7 +104,7 @@ def ptc_config(cfg) -> nk.PtcConfig:
 
 def krylov_config(cfg) -> nk.KrylovConfig:
     return nk.KrylovConfig(kdim=cfg["gmres.kdim"], max_restarts=cfg["gmres.max_restarts"],
-                           rtol=cfg["gmres.rtol"])
+                           rtol=cfg["gmres.rtol"], ortho=cfg.get("gmres.ortho", "mgs"))
 
 
 class ImplicitDriver:
@@ -230,6 +230,7 @@ SCHEMA = {
     "ptc.rtol": (float, 1e-4), "ptc.atol": (float, None), "ptc.ser": (_as_bool, True),
     "ptc.ser_as_printed": (_as_bool, False), "ptc.refresh_every_n_ptc": (int, 0), "ptc.max_halvings": (int, 8),
     "gmres.kdim": (int, 30), "gmres.max_restarts": (int, 10), "gmres.rtol": (float, 1e-4),
+    "gmres.ortho": (str, "mgs"),
     "pmg.levels": (str, "3-1"), "pmg.smooth": (str, "2"), "pmg.smoother": (str, "ej"),
     "pmg.switch_after": (int, None), "pmg.mbnk.rtol": (float, 0.1), "pmg.mbnk.maxiter": (int, 5),
     "pmg.smoother_shift": (float, 0.0), "pmg.rk.cfl": (float, 1.5),
@@ -243,6 +244,7 @@ _VALID_CHOICES = {
     "mesh.kind": ("box", "cylinder", "file"),
     "equation.kind": ("euler", "navier-stokes", "advection-diffusion"),
     "case.scheme": ("esdirk2", "esdirk3", "esdirk4", "row2", "row4", "ros4l"),
+    "gmres.ortho": ("mgs", "cgs2"),
     "case.solver": ("jfnk", "pmg-solver"),
     "case.precond": ("ej", "pmg", "none"),
     "pmg.block_precision": ("fp64", "fp32"),

@@ -26,7 +26,9 @@ by running the reference (``fullsize_floors.json``):
 * one ESDIRK3 JFNK-pMG step with the bench's config-2 settings (p{4-2},
   GMRES(30), rtol 1e-3, smoother_shift 5000, ptc.dtau_init = dt) on a
   48 x 48 version of config 2, against ``solver_oracle.Driver``: PTC counts
-  exact, GMRES +-1, solution <= 1e-7.
+  exact, every linear solve's GMRES count +-1 (these are restarted
+  GMRES(30) solves of 73-148 iterations: the oracle takes 462/417/446 per
+  stage), solution <= 1e-7.
 """
 
 import json
@@ -63,22 +65,44 @@ def _rel_ld(dev, truth):
     return float(np.max(np.abs(d.astype(np.longdouble) - truth)) / np.max(np.abs(truth)))
 
 
-@pytest.mark.parametrize("k", [2, 3, 4, 5])
-def test_fullsize_residual_matches_oracle(cuda, k):
+def _case(k, variant=None):
+    """BASELINE config k; config 4's "adiabatic" variant swaps the isothermal
+    no-slip wall (not in the reference) for the reference's adiabatic one on
+    the same stretched channel -- the case the reference floor was measured
+    on (tests/golden/make_fullsize_floors.py)."""
+    import dataclasses
+
+    from paper_2202_09733_b200 import mesh as mm
+    c = cases.config(k)
+    if variant == "adiabatic":
+        yn = np.unique(c.mesh.nodes[:, 1])
+        c = dataclasses.replace(c, mesh=mm.generate_channel(512, 128, 4.0, yn, bottom="wall-adiabatic"),
+                                eqn=dataclasses.replace(c.eqn, wall_temperature=None))
+    return c
+
+
+@pytest.mark.parametrize("k,variant", [(2, None), (3, None), (4, "adiabatic"), (4, None), (5, None)])
+def test_fullsize_residual_matches_oracle(cuda, k, variant):
     if k == 5 and _host_memory_gb() < 64:
         pytest.fail(f"config 5 oracle needs ~40 GB of host memory, {_host_memory_gb():.0f} GB available")
-    c = cases.config(k)
+    c = _case(k, variant)
     d = Discretization(c.mesh, c.p, c.eqn)
+    path = d.residual_path()
     R = d.residual(torch.as_tensor(c.q0, device="cuda")).cpu().numpy()
     del d
     torch.cuda.empty_cache()
     truth = OracleDisc(c.mesh, c.p, c.eqn, dtype=np.longdouble).residual_mt(c.q0)
     err = _rel_ld(R, truth)
     floor = FLOORS[f"config{k}"]["reference_R_vs_truth"]
-    err_o = _rel(R, OracleDisc(c.mesh, c.p, c.eqn).residual_mt(c.q0))
-    print(f"config {k}: {c.n_dofs} DoF, R vs long-double truth {err:.3e} (reference {floor:.3e}), "
-          f"vs float64 oracle {err_o:.3e}")
-    assert err <= max(floor, 1e-12)
+    # the isothermal wall has no reference counterpart: its bound is twice
+    # the reference's floor on the same geometry with the adiabatic wall
+    tol = max(floor, 1e-12) * (2.0 if (k == 4 and variant is None) else 1.0)
+    msg = f"config {k}{' ' + variant if variant else ''} ({path} kernels): {c.n_dofs} DoF, R vs long-double " \
+          f"truth {err:.3e} (reference {floor:.3e})"
+    if k != 5:
+        msg += f", vs float64 oracle {_rel(R, OracleDisc(c.mesh, c.p, c.eqn).residual_mt(c.q0)):.3e}"
+    print(msg)
+    assert err <= tol
 
 
 def test_fullsize_jv_matches_oracle(cuda):
@@ -127,10 +151,11 @@ def test_esdirk3_step_bench_config2_settings_matches_oracle(cuda):
     q_d, info = ImplicitDriver(d, cfg).step(torch.as_tensor(c.q0, device="cuda"), c.dt, s)
     ptc_d = [i["iters"] for i in info]
     ptc_o = [r[1] for r in drv_o.records]
-    gm_d = [i["gmres_iters"] for i in info]
-    gm_o = [r[2] for r in drv_o.records]
+    gm_d = [i["gmres_per_iter"] for i in info]
+    gm_o = [r[3] for r in drv_o.records]
     err = _rel(q_d, q_o)
     print(f"48^2 config-2 settings: PTC {ptc_d} vs {ptc_o}, GMRES {gm_d} vs {gm_o}, solution {err:.3e}")
     assert ptc_d == ptc_o
-    assert all(abs(a - b) <= 1 for a, b in zip(gm_d, gm_o))
+    assert all(len(a) == len(b) for a, b in zip(gm_d, gm_o))
+    assert all(abs(x - y) <= 1 for a, b in zip(gm_d, gm_o) for x, y in zip(a, b))
     assert err <= 1e-7

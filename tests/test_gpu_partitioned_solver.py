@@ -23,24 +23,24 @@ CFG = {"case.precond": "pmg", "pmg.levels": "3-2", "pmg.smooth": "2", "pmg.smoot
        "gmres.kdim": 30, "gmres.rtol": 1e-3, "ptc.rtol": 1e-4}
 
 
-def _step(disc, q0, c, scheme, smoother):
+def _step(disc, q0, c, scheme, smoother, ortho="mgs"):
     from paper_2202_09733_b200 import time_integration as ti
     from paper_2202_09733_b200.harness import ImplicitDriver
-    cfg = dict(CFG, **{"ptc.dtau_init": c.dt, "pmg.smoother": smoother})
+    cfg = dict(CFG, **{"ptc.dtau_init": c.dt, "pmg.smoother": smoother, "gmres.ortho": ortho})
     q1, info = ImplicitDriver(disc, cfg).step(torch.as_tensor(q0, device="cuda"), c.dt, ti.get_scheme(scheme))
     return q1, [i.get("iters") for i in info], [i.get("gmres_iters", i.get("iters")) for i in info]
 
 
-def _reference(scheme, smoother):
+def _reference(scheme, smoother, ortho="mgs"):
     from paper_2202_09733_b200 import cases
     from paper_2202_09733_b200.spatial import Discretization
     c = cases.config(1)
     d = Discretization(c.mesh, c.p, c.eqn)
-    q1, ptc, gm = _step(d, c.q0, c, scheme, smoother)
+    q1, ptc, gm = _step(d, c.q0, c, scheme, smoother, ortho)
     return c, q1.cpu().numpy(), ptc, gm
 
 
-def _rank_step(world, rank, scheme, smoother):
+def _rank_step(world, rank, scheme, smoother, ortho="mgs"):
     from paper_2202_09733_b200 import cases, vec
     from paper_2202_09733_b200.partition import HaloDiscretization, SlabPartition
     c = cases.config(1)
@@ -50,7 +50,7 @@ def _rank_step(world, rank, scheme, smoother):
     q0 = part.scatter_global(c.q0, sz)
     vec.set_partition(part)
     try:
-        q1, ptc, gm = _step(d, q0, c, scheme, smoother)
+        q1, ptc, gm = _step(d, q0, c, scheme, smoother, ortho)
         own = vec.owned(q1).cpu().numpy()
     finally:
         vec.set_partition(None)
@@ -68,10 +68,11 @@ def _compare(c, ref, parts, ptc_ref, gm_ref):
     assert np.max(np.abs(got - ref)) / np.max(np.abs(ref)) <= 1e-7
 
 
-@pytest.mark.parametrize("scheme,smoother", [("esdirk3", "ej-ej"), ("ros4l", "rk-ej")])
-def test_partitioned_step_one_rank(cuda, scheme, smoother):
-    c, ref, ptc_ref, gm_ref = _reference(scheme, smoother)
-    _compare(c, ref, [_rank_step(1, 0, scheme, smoother)], ptc_ref, gm_ref)
+@pytest.mark.parametrize("scheme,smoother,ortho", [("esdirk3", "ej-ej", "mgs"), ("ros4l", "rk-ej", "mgs"),
+                                                   ("esdirk3", "ej-ej", "cgs2")])
+def test_partitioned_step_one_rank(cuda, scheme, smoother, ortho):
+    c, ref, ptc_ref, gm_ref = _reference(scheme, smoother, ortho)
+    _compare(c, ref, [_rank_step(1, 0, scheme, smoother, ortho)], ptc_ref, gm_ref)
 
 
 def _free_port():
@@ -82,13 +83,13 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, out):
+def _worker(rank, world, port, out, ortho="mgs"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), WORLD_SIZE=str(world),
                       RANK=str(rank), LOCAL_RANK=str(rank))
     import torch.distributed as dist
     dist.init_process_group("gloo")
     try:
-        ge, own, ptc, gm = _rank_step(world, rank, "esdirk3", "ej-ej")
+        ge, own, ptc, gm = _rank_step(world, rank, "esdirk3", "ej-ej", ortho)
         out[rank] = (ge, own, ptc, gm)
     finally:
         dist.barrier()
@@ -96,12 +97,14 @@ def _worker(rank, world, port, out):
 
 
 @pytest.mark.timeout(900)
-def test_partitioned_step_two_ranks_gloo(cuda):
+@pytest.mark.parametrize("ortho", ["mgs", "cgs2"])
+def test_partitioned_step_two_ranks_gloo(cuda, ortho):
+    # cgs2: 3 all-reduces per Arnoldi step instead of j + 2
     import torch.multiprocessing as mp
-    c, ref, ptc_ref, gm_ref = _reference("esdirk3", "ej-ej")
+    c, ref, ptc_ref, gm_ref = _reference("esdirk3", "ej-ej", ortho)
     world, port = 2, _free_port()
     with mp.Manager() as m:
         out = m.dict()
-        mp.spawn(_worker, args=(world, port, out), nprocs=world, join=True)
+        mp.spawn(_worker, args=(world, port, out, ortho), nprocs=world, join=True)
         parts = [out[r] for r in range(world)]
     _compare(c, ref, parts, ptc_ref, gm_ref)

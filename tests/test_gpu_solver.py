@@ -109,7 +109,8 @@ def test_transfers_match_oracle(cuda):
     assert rel(hi, o._prolong(0, lo.cpu().numpy())) <= 1e-14
 
 
-def test_gmres_dense_kat(cuda):
+@pytest.mark.parametrize("ortho", ["mgs", "cgs2"])
+def test_gmres_dense_kat(cuda, ortho):
     # reference tests/test_newton_krylov.py:29-48 on device vectors
     rng = np.random.default_rng(7)
     n = 40
@@ -117,15 +118,42 @@ def test_gmres_dense_kat(cuda):
     A = A @ A.T + n * np.eye(n)
     b = rng.standard_normal(n)
     Ad = t(A)
-    x, it, rr = nk.gmres_solve(lambda v: Ad @ v, t(b), nk.KrylovConfig(kdim=40, rtol=1e-12))
+    kc = lambda **kw: nk.KrylovConfig(ortho=ortho, **kw)  # noqa: E731
+    x, it, rr = nk.gmres_solve(lambda v: Ad @ v, t(b), kc(kdim=40, rtol=1e-12))
     assert np.allclose(x.cpu().numpy(), np.linalg.solve(A, b), atol=1e-8) and rr <= 1e-12
-    x, it, rr = nk.gmres_solve(lambda v: Ad @ v, t(b), nk.KrylovConfig(kdim=5, max_restarts=60, rtol=1e-10))
+    x, it, rr = nk.gmres_solve(lambda v: Ad @ v, t(b), kc(kdim=5, max_restarts=60, rtol=1e-10))
     assert rr <= 1e-10 and it > 5
+    # the oracle's restatement of the same orthogonalisation: same counts
+    xo, ito, rro = so.gmres_solve(lambda v: A @ v, b, kdim=5, max_restarts=60, rtol=1e-10, ortho=ortho)
+    assert it == ito and rel(x, xo) <= 1e-12
     with pytest.raises(RuntimeError, match="iteration 1"):
-        nk.gmres_solve(lambda v: torch.full_like(v, float("nan")), t(b), nk.KrylovConfig())
+        nk.gmres_solve(lambda v: torch.full_like(v, float("nan")), t(b), kc())
     D = t(np.diag([2.0, 3.0, 4.0, 5.0]))
-    x, it, rr = nk.gmres_solve(lambda v: D @ v, t([1.0, 1.0, 0.0, 0.0]), nk.KrylovConfig(kdim=10, rtol=1e-13))
+    x, it, rr = nk.gmres_solve(lambda v: D @ v, t([1.0, 1.0, 0.0, 0.0]), kc(kdim=10, rtol=1e-13))
     assert it <= 3
+
+
+def test_esdirk3_step_cgs2_matches_oracle_and_reference_counts(cuda):
+    # gmres.ortho = cgs2 (not in the reference): against the oracle's CGS2
+    # restatement (PTC exact, GMRES +-1, solution 1e-7) and the reference's
+    # MGS step (golden_esdirk3.npz) -- a different orthogonalisation, the
+    # same Krylov space: GMRES counts +-1 per solve, solution 1e-7
+    c = cases.config(1)
+    o = OracleDisc(c.mesh, c.p, c.eqn)
+    d = Discretization(c.mesh, c.p, c.eqn)
+    s = ti.get_scheme("esdirk3")
+    drv_o = so.Driver(o, "pmg", "3-2", 2, smoother_shift=50.0, gmres_rtol=1e-3, dtau_init=c.dt, ortho="cgs2")
+    q_o = drv_o.esdirk_step(c.q0, c.dt, s.a, s.b)
+    cfg = {"case.precond": "pmg", "pmg.levels": "3-2", "pmg.smooth": "2", "pmg.smoother_shift": 50.0,
+           "gmres.kdim": 30, "gmres.rtol": 1e-3, "ptc.dtau_init": c.dt, "ptc.rtol": 1e-4, "gmres.ortho": "cgs2"}
+    q_d, info = ImplicitDriver(d, cfg).step(t(c.q0), c.dt, s)
+    assert [i["iters"] for i in info] == [r[1] for r in drv_o.records]
+    per_d = [x for i in info for x in i["gmres_per_iter"]]
+    assert all(abs(a - b) <= 1 for a, b in zip(per_d, [x for r in drv_o.records for x in r[3]]))
+    assert rel(q_d, q_o) <= 1e-7
+    assert [i["iters"] for i in info] == list(GE["c1/esdirk3/ptc_iters"])
+    assert all(abs(a - b) <= 1 for a, b in zip(per_d, GE["c1/esdirk3/gmres_counts"]))
+    assert rel(q_d, GE["c1/esdirk3/q1"]) <= 1e-7
 
 
 def test_precondition_matches_reference(cuda):

@@ -251,3 +251,21 @@ def test_oracle_ros4l_step_matches_reference():
     ref = list(GR["c1/ros4l/gmres_counts"])
     assert len(counts) == len(ref) and all(abs(a - b) <= 1 for a, b in zip(counts, ref)), (counts, ref)
     assert np.max(np.abs(q1 - GR["c1/ros4l/q1"])) / np.max(np.abs(GR["c1/ros4l/q1"])) <= 1e-6
+
+
+def test_oracle_gmres_cgs2_matches_mgs_kat():
+    # gmres.ortho = cgs2 (classical Gram-Schmidt + one reorthogonalisation,
+    # the partitioned solver's 3-all-reduce Arnoldi option): the same
+    # Krylov iterates as the reference's MGS on a well-conditioned SPD
+    # system, to rounding (reference tests/test_newton_krylov.py:29-48)
+    from oracle import solver_oracle as so
+    rng = np.random.default_rng(7)
+    n = 40
+    A = rng.standard_normal((n, n))
+    A = A @ A.T + n * np.eye(n)
+    b = rng.standard_normal(n)
+    xm, im, rm = so.gmres_solve(lambda v: A @ v, b, kdim=5, max_restarts=60, rtol=1e-10)
+    xc, ic, rc = so.gmres_solve(lambda v: A @ v, b, kdim=5, max_restarts=60, rtol=1e-10, ortho="cgs2")
+    assert im == ic and rm <= 1e-10 and rc <= 1e-10
+    assert np.allclose(xc, np.linalg.solve(A, b), atol=1e-8)
+    assert np.max(np.abs(xc - xm)) <= 1e-12 * np.max(np.abs(xm))
