@@ -104,7 +104,7 @@ def ptc_config(cfg) -> nk.PtcConfig:
 
 def krylov_config(cfg) -> nk.KrylovConfig:
     return nk.KrylovConfig(kdim=cfg["gmres.kdim"], max_restarts=cfg["gmres.max_restarts"],
-                           rtol=cfg["gmres.rtol"], ortho=cfg.get("gmres.ortho", "mgs"))
+                           rtol=cfg["gmres.rtol"], ortho=cfg["gmres.ortho"])
 
 
 class ImplicitDriver:
