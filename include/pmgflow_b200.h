@@ -112,7 +112,9 @@ PMGB_API int pmgb_eval(pmgb_disc* d, const double* q, const double* X, double ep
 
 /* Per-element spectral-radius estimate of dR/dq at state q for the RK
  * smoother's local pseudo-time step (PMGB_EPI_RK): lam (M doubles, device)
- *   = (2p+1) max(|u|+c)/h_e + (p+1)^4 max(nu)/h_e^2,
+ *   = adv_coef max(|u|+c)/h_e + (p+1)^4 max(nu)/h_e^2,
+ *   adv_coef = 2 sqrt(2) rho_p, rho_p the Bloch spectral radius of the 1-D
+ *   upwind FR advection operator (operators.rk_adv_coef),
  *   h_e = 4 |det J(0,0)| / max(centre-line lengths).  No reference
  * counterpart (the reference's smoothers are EJ / MBNK, pmg.py:162-175). */
 PMGB_API int pmgb_rk_lambda(pmgb_disc* d, const double* q, double adv_coef, double* lam, void* stream);
