@@ -213,6 +213,48 @@ __device__ __forceinline__ void stg4(double* p, const double* v) {
                : "memory");
 }
 
+// L2 residency hints across the chain (126 MB L2; working set ~190 MB at
+// config 2): intermediates stored evict_last, inputs loaded evict_first on
+// their last read of the chain (k_rasm).  Measured slower (config-2 R
+// 117.1 -> 120.6 us, profiles/r2/ab_l2_hints_r2.log): off by default.
+#ifndef PMGB_RECT_L2_HINTS
+#define PMGB_RECT_L2_HINTS 0
+#endif
+__device__ __forceinline__ uint64_t pol_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t pol_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void stg4_last(double* p, const double* v) {
+#if PMGB_RECT_L2_HINTS
+  asm volatile("st.global.L2::cache_hint.v4.f64 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "d"(v[0]), "d"(v[1]),
+               "d"(v[2]), "d"(v[3]), "l"(pol_last())
+               : "memory");
+#else
+  stg4(p, v);
+#endif
+}
+__device__ __forceinline__ void stg1_last(double* p, double v) {
+#if PMGB_RECT_L2_HINTS
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol_last()) : "memory");
+#else
+  *p = v;
+#endif
+}
+__device__ __forceinline__ void ldg4_first(const double* p, double* o) {
+#if PMGB_RECT_L2_HINTS
+  asm volatile("ld.global.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;" : "=d"(o[0]), "=d"(o[1]), "=d"(o[2]),
+               "=d"(o[3]) : "l"(p), "l"(pol_first()));
+#else
+  ldg4c(p, o);
+#endif
+}
+
 // ---------------------------------------------------------------------------
 // k_rface: traces, interface flux and BR1 common value, once per face point
 
@@ -254,7 +296,7 @@ __global__ void __launch_bounds__(128) k_rface(const FrConst C, const RectMesh m
     rusanov_pr(qa, A, qc, B, nrm.x, nrm.y, g, F);
   else
     roe_pr(qa, A, qc, B, nrm.x, nrm.y, g, F);
-  stg4(frec + t * FREC, F);
+  stg4_last(frec + t * FREC, F);
   if constexpr (VISC) {
     double wa[3] = {A.u, A.v, A.p * A.ir}, wc[3] = {B.u, B.v, B.p * B.ir};
     if (bnd) ghost_w<KIND>(ph, tag, wa, wc);
@@ -262,10 +304,10 @@ __global__ void __launch_bounds__(128) k_rface(const FrConst C, const RectMesh m
 #pragma unroll
     for (int c = 0; c < 3; ++c) w[c] = common_w(ph, !bnd, true, wa[c], wc[c]);
     double* dL = wh + (((int64_t)fr.x * 4 + fL) * N + k) * 3;
-    dL[0] = w[0], dL[1] = w[1], dL[2] = w[2];
+    stg1_last(dL, w[0]), stg1_last(dL + 1, w[1]), stg1_last(dL + 2, w[2]);
     if (!bnd) {
       double* dR = wh + (((int64_t)fr.z * 4 + fr.w) * N + kk) * 3;
-      dR[0] = w[0], dR[1] = w[1], dR[2] = w[2];
+      stg1_last(dR, w[0]), stg1_last(dR + 1, w[1]), stg1_last(dR + 2, w[2]);
     }
   }
 }
@@ -289,26 +331,26 @@ __global__ void __launch_bounds__(128) k_rfc(const FrConst C, const RectMesh m, 
   const Phys ph = phys_of(C);
   const double* rec = frec + t * FREC;
   double Fc[4];
-  ldg4c(rec, Fc);
+  ldg4_first(rec, Fc);
   if constexpr (KT<KIND>::VISC) {
     double fl[4], fr_[4], Fv[4];
-    ldg4c(rec + 4, fl);
+    ldg4_first(rec + 4, fl);
     if (bnd) {
 #pragma unroll
       for (int v = 0; v < 4; ++v) Fv[v] = common_fv(ph, false, true, fl[v], fl[v]);
       if (tag == T_WALL_ADIABATIC) Fv[3] = 0.0;
     } else {
-      ldg4c(rec + 8, fr_);
+      ldg4_first(rec + 8, fr_);
 #pragma unroll
       for (int v = 0; v < 4; ++v) Fv[v] = common_fv(ph, true, true, fl[v], fr_[v]);
     }
 #pragma unroll
     for (int v = 0; v < 4; ++v) Fc[v] = Fc[v] - Fv[v];
   }
-  stg4(fc + (((int64_t)fr.x * 4 + fL) * N + k) * 4, Fc);
+  stg4_last(fc + (((int64_t)fr.x * 4 + fL) * N + k) * 4, Fc);
   if (!bnd) {
     const double n[4] = {-Fc[0], -Fc[1], -Fc[2], -Fc[3]};
-    stg4(fc + (((int64_t)fr.z * 4 + fr.w) * N + (rev ? N - 1 - k : k)) * 4, n);
+    stg4_last(fc + (((int64_t)fr.z * 4 + fr.w) * N + (rev ? N - 1 - k : k)) * 4, n);
   }
 }
 
@@ -330,6 +372,18 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                    saddr(dst)),
                "l"(src), "r"(bytes), "r"(saddr(bar))
                : "memory");
+}
+// the same with an L2 evict_first policy (the block's last read in the chain)
+__device__ __forceinline__ void bulk_g2s_first(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+#if PMGB_RECT_L2_HINTS
+  asm volatile(
+      "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          saddr(dst)),
+      "l"(src), "r"(bytes), "r"(saddr(bar)), "l"(pol_first())
+      : "memory");
+#else
+  bulk_g2s(dst, src, bytes, bar);
+#endif
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   asm volatile(
@@ -646,24 +700,24 @@ k_rgrad(const FrConst C, const RectMesh m, const double* __restrict__ q, const d
   {
     const double gyv[2] = {tgy1[0], tgy1[1]};
     visc_fx(t1q, tgx1, gyv, ph, o);
-    stg4(frec + (int64_t)ri[1] * FREC + (lft[1] ? 4 : 8), o);
+    stg4_last(frec + (int64_t)ri[1] * FREC + (lft[1] ? 4 : 8), o);
   }
   {
     const double gyv[2] = {tgy3[0], tgy3[1]};
     visc_fx(t3q, tgx3, gyv, ph, o);
     o[1] = -o[1], o[2] = -o[2], o[3] = -o[3];
-    stg4(frec + (int64_t)ri[3] * FREC + (lft[3] ? 4 : 8), o);
+    stg4_last(frec + (int64_t)ri[3] * FREC + (lft[3] ? 4 : 8), o);
   }
   {
     const double gxv[2] = {tgx2[0], tgx2[1]};
     visc_fy(t2q, gxv, tgy2, ph, o);
-    stg4(frec + (int64_t)ri[2] * FREC + (lft[2] ? 4 : 8), o);
+    stg4_last(frec + (int64_t)ri[2] * FREC + (lft[2] ? 4 : 8), o);
   }
   {
     const double gxv[2] = {tgx0[0], tgx0[1]};
     visc_fy(t0q, gxv, tgy0, ph, o);
     o[1] = -o[1], o[2] = -o[2], o[3] = -o[3];
-    stg4(frec + (int64_t)ri[0] * FREC + (lft[0] ? 4 : 8), o);
+    stg4_last(frec + (int64_t)ri[0] * FREC + (lft[0] ? 4 : 8), o);
   }
 }
 
@@ -714,7 +768,7 @@ k_rasm(const FrConst C, const RectMesh m, const double* __restrict__ q, const do
   const uint32_t qbytes = (uint32_t)ne * NP * 32;
   if (t == 0) {
     mbar_expect(bar, HASX ? 2 * qbytes : qbytes);
-    bulk_g2s(sQ, q + e0 * NP * 4, qbytes, bar);
+    bulk_g2s_first(sQ, q + e0 * NP * 4, qbytes, bar);
     if (HASX) bulk_g2s(sX, X + e0 * NP * 4, qbytes, bar);
   }
   const double2 rg = live ? __ldg(m.rgeo + e) : make_double2(1.0, 1.0);
@@ -722,8 +776,8 @@ k_rasm(const FrConst C, const RectMesh m, const double* __restrict__ q, const do
   if (t == 0) {
     const uint32_t fb = (uint32_t)ne * 4 * N * 32, wb = (uint32_t)ne * 4 * N * 24;
     mbar_expect(bar + 1, VISC ? fb + wb : fb);
-    bulk_g2s(sm + L::OFF_F, fc + e0 * 4 * N * 4, fb, bar + 1);
-    if (VISC) bulk_g2s(sm + L::OFF_W, wh + e0 * 4 * N * 3, wb, bar + 1);
+    bulk_g2s_first(sm + L::OFF_F, fc + e0 * 4 * N * 4, fb, bar + 1);
+    if (VISC) bulk_g2s_first(sm + L::OFF_W, wh + e0 * 4 * N * 3, wb, bar + 1);
     if (blockIdx.x == 0) commit_status(bad, st);
   }
   mbar_wait(bar, 0);
