@@ -56,7 +56,8 @@ ptc.rtol = 1e-4
     with GmresLog() as log:
         qn, info = rti.esdirk_step(c.q0, c.dt, ref_scheme(), d.residual, drv.solve_stage)
     wall = time.perf_counter() - t0
-    out = {"q0": c.q0, "dt": np.array(c.dt), "q1": qn, "gmres_counts": np.array(log.counts),
+    import hashlib
+    out = {"q0_sha256": np.array(hashlib.sha256(c.q0.tobytes()).hexdigest()), "dt": np.array(c.dt), "q1": qn, "gmres_counts": np.array(log.counts),
            "ptc_iters": np.array([i["iters"] for i in info]), "wall_s": np.array(wall)}
     print("gmres per solve", log.counts, "ptc", [i["iters"] for i in info], f"{wall:.1f}s", flush=True)
     np.savez_compressed(HERE / "golden_c2step.npz", **out)
