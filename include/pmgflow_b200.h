@@ -110,6 +110,34 @@ typedef struct pmgb_epilogue {
 PMGB_API int pmgb_eval(pmgb_disc* d, const double* q, const double* X, double eps,
                        const pmgb_epilogue* epi, double* out, void* stream);
 
+/* Mixed-degree contexts (per-element degree map, p = 0..5; Euler / NS,
+ * Roe or Rusanov, BR1): the reference's degree groups with mortar faces --
+ * both traces interpolated (Pi) to the higher degree's face points, the
+ * common values formed there and restricted (Gamma) back (spatial.py:
+ * 468-497, 501-585).  `desc` as for pmgb_disc_create (its degree field is
+ * ignored), `degrees` (M), `ops` (6, 66): per degree D (n x n packed)
+ * then eL, eR, lL, lR, Gauss points at 36, 42, 48, 54, 60; `xfer`
+ * (6 x 6 degree pairs [pH][pL], 2, 6 x 6): Pi (nH x nL) then Gamma
+ * (nL x nH), row stride 6.  Vectors use the reference's flat layout
+ * (element e at the offset of its degree's block size). */
+typedef struct pmgb_mdisc pmgb_mdisc;
+PMGB_API int pmgb_mdisc_create(const pmgb_disc_desc* desc, const int32_t* degrees, const double* ops,
+                               const double* xfer, pmgb_mdisc** out);
+PMGB_API int pmgb_mdisc_destroy(pmgb_mdisc* d);
+PMGB_API int64_t pmgb_mdisc_n_dofs(const pmgb_mdisc* d);
+/* R(q) with the fused epilogues of pmgb_eval (not PMGB_EPI_RK) */
+PMGB_API int pmgb_mdisc_eval(pmgb_mdisc* d, const double* q, const double* X, double eps,
+                             const pmgb_epilogue* epi, double* out, void* stream);
+/* Frozen neighbour records (spatial.py:700-766) at own points, padded to
+ * 6: rq (M,4,6,4) trace, rw (M,4,6,3) viscous variables, rf (M,4,6,4)
+ * minus the neighbour's one-sided viscous flux; boundary faces untouched */
+PMGB_API int pmgb_mdisc_freeze(pmgb_mdisc* d, const double* q, double* rq, double* rw, double* rf, void* stream);
+/* element_residual (spatial.py:768-853) for B elements of degree p */
+PMGB_API int pmgb_mdisc_element_residual(pmgb_mdisc* d, int32_t p, const int64_t* elems, int64_t B,
+                                         const double* Q, const double* rq, const double* rw, const double* rf,
+                                         double* out, void* stream);
+
+
 /* Per-element spectral-radius estimate of dR/dq at state q for the RK
  * smoother's local pseudo-time step (PMGB_EPI_RK): lam (M doubles, device)
  *   = adv_coef max(|u|+c)/h_e + (p+1)^4 max(nu)/h_e^2,

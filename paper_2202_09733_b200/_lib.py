@@ -52,6 +52,15 @@ SIGNATURES = {
     "pmgb_disc_destroy": (ctypes.c_int, [c_void_p]),
     "pmgb_disc_n_dofs": (ctypes.c_int64, [c_void_p]),
     "pmgb_disc_residual_path": (ctypes.c_int, [c_void_p, ctypes.c_int32]),
+    "pmgb_mdisc_create": (ctypes.c_int, [ctypes.POINTER(DiscDesc), c_int32_p, c_double_p, c_double_p,
+                                         ctypes.POINTER(c_void_p)]),
+    "pmgb_mdisc_destroy": (ctypes.c_int, [c_void_p]),
+    "pmgb_mdisc_n_dofs": (ctypes.c_int64, [c_void_p]),
+    "pmgb_mdisc_eval": (ctypes.c_int, [c_void_p, c_void_p, c_void_p, ctypes.c_double, ctypes.POINTER(Epilogue),
+                                       c_void_p, c_void_p]),
+    "pmgb_mdisc_freeze": (ctypes.c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "pmgb_mdisc_element_residual": (ctypes.c_int, [c_void_p, ctypes.c_int32, c_void_p, ctypes.c_int64, c_void_p,
+                                                   c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "pmgb_residual": (ctypes.c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
     "pmgb_rk_lambda": (ctypes.c_int, [c_void_p, c_void_p, ctypes.c_double, c_void_p, c_void_p]),
     "pmgb_rk_dtau": (ctypes.c_int, [ctypes.c_int64, c_void_p, ctypes.c_double, ctypes.c_double, c_void_p,

@@ -18,7 +18,7 @@ from pathlib import Path
 HERE = Path(__file__).resolve().parent
 CSRC = HERE / "csrc"
 LIB = HERE / "libpmgflow_b200.so"
-SOURCES = ["fr_kernels.cu", "fr_rect.cu", "ej_kernels.cu", "krylov_kernels.cu", "capi.cu"]
+SOURCES = ["fr_kernels.cu", "fr_rect.cu", "fr_mixed.cu", "ej_kernels.cu", "krylov_kernels.cu", "capi.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "--fmad=true"]

@@ -42,6 +42,33 @@ int launch_multidot(int64_t n, const double* V, int64_t ld, int k, const double*
 int launch_gemv_sub(int64_t n, int k, const double* V, int64_t ld, const double* y, double* w, cudaStream_t st);
 int launch_probe_fp64(int64_t iters, int blocks, double* out, cudaStream_t st);
 Status* status_ptr();
+int* bad_ptr();
+
+// mixed-degree path (fr_mixed.cu)
+struct MixDev {
+  int64_t M;
+  int kind;
+  const int8_t* deg;
+  const int64_t* off;
+  const int64_t* poff;
+  const double* geom;
+  const int2* link;
+  const double* ops;
+  const double* xfer;
+  int64_t nface;
+  const int4* faces;
+};
+struct MixGroups {
+  const int* elems[6];
+  int64_t cnt[6];
+};
+int mx_residual(const FrConst& C, const MixDev& m, const MixGroups& gr, const double* q, const double* X,
+                double eps, const Epi& ep, double* qtr, double* fci, double* wh, double* grad, double* fvn,
+                double* fcv, double* out, int* bad, Status* stp, cudaStream_t st);
+int mx_records(const FrConst& C, const MixDev& m, const double* qtr, const double* fvn, double* rq, double* rw,
+               double* rf, cudaStream_t st);
+int mx_local(const FrConst& C, const MixDev& m, int p, const int64_t* elems, int64_t B, const double* Q,
+             const double* rq, const double* rw, const double* rf, double* out, cudaStream_t st);
 }  // namespace pmgb
 
 using namespace pmgb;
@@ -225,6 +252,175 @@ PMGB_API int pmgb_disc_destroy(pmgb_disc* h) {
 }
 
 PMGB_API int64_t pmgb_disc_n_dofs(const pmgb_disc* h) { return h ? h->d.n_dofs : -1; }
+
+// ---------------------------------------------------------------------------
+// mixed-degree contexts (fr_mixed.cu)
+
+struct pmgb_mdisc {
+  FrConst C;
+  MixDev m;
+  MixGroups gr;
+  int8_t* deg = nullptr;
+  int64_t *off = nullptr, *poff = nullptr;
+  double *geom = nullptr, *ops = nullptr, *xfer = nullptr;
+  int2* link = nullptr;
+  int4* faces = nullptr;
+  int* elems = nullptr;
+  double *qtr = nullptr, *fci = nullptr, *wh = nullptr, *grad = nullptr, *fvn = nullptr, *fcv = nullptr;
+  int64_t n_dofs = 0;
+};
+
+PMGB_API int pmgb_mdisc_destroy(pmgb_mdisc* h) {
+  if (!h) return 0;
+  for (void* p : {(void*)h->deg, (void*)h->off, (void*)h->poff, (void*)h->geom, (void*)h->ops, (void*)h->xfer,
+                  (void*)h->link, (void*)h->faces, (void*)h->elems, (void*)h->qtr, (void*)h->fci, (void*)h->wh,
+                  (void*)h->grad, (void*)h->fvn, (void*)h->fcv})
+    cudaFree(p);
+  delete h;
+  return 0;
+}
+
+PMGB_API int pmgb_mdisc_create(const pmgb_disc_desc* desc, const int32_t* degrees, const double* ops,
+                               const double* xfer, pmgb_mdisc** out) {
+  if (!desc || !degrees || !ops || !xfer || !out) return -1;
+  if (desc->kind != 0 && desc->kind != 1) return -3;  // Euler / Navier-Stokes
+  if (desc->viscous_scheme != 0) return -1;            // BR1 (the reference's scheme)
+  const int64_t M = desc->n_elem;
+  pmgb_mdisc* h = new pmgb_mdisc();
+  std::memset(&h->C, 0, sizeof(h->C));
+  FrConst& C = h->C;
+  for (int v = 0; v < 4; ++v) C.qinf[v] = desc->free_stream[v];
+  C.gamma = desc->gamma;
+  C.mu = desc->mu;
+  C.kappa = desc->kappa;
+  C.riemann = desc->riemann;
+  C.twall = desc->wall_temperature;
+  std::vector<int8_t> deg((size_t)M);
+  std::vector<int64_t> off((size_t)M + 1, 0), poff((size_t)M + 1, 0);
+  std::vector<std::vector<int>> groups(6);
+  for (int64_t e = 0; e < M; ++e) {
+    const int p = degrees[e];
+    if (p < 0 || p > 5) {
+      delete h;
+      return -2;
+    }
+    deg[(size_t)e] = (int8_t)p;
+    off[(size_t)e + 1] = off[(size_t)e] + 4 * (p + 1) * (p + 1);
+    poff[(size_t)e + 1] = poff[(size_t)e] + (p + 1) * (p + 1);
+    groups[p].push_back((int)e);
+  }
+  h->n_dofs = off[(size_t)M];
+  std::vector<int2> lk((size_t)M * 4);
+  std::vector<int4> faces;
+  for (int64_t e = 0; e < M; ++e)
+    for (int f = 0; f < 4; ++f) {
+      const int64_t* r = desc->links + (e * 4 + f) * 4;
+      const int tag = desc->tags[e * 4 + f];
+      const bool bnd = r[0] < 0;
+      int2 v;
+      v.x = (int)r[0];
+      v.y = (bnd ? 0 : (int)(r[1] & 3)) | ((int)(r[2] & 1) << 2) | ((int)(r[3] & 1) << 3) |
+            ((tag < 0 ? 0 : tag & 15) << 4);
+      lk[(size_t)e * 4 + f] = v;
+      if (!bnd && !(r[3] & 1)) continue;
+      int4 fa;
+      fa.x = (int)e;
+      fa.y = f | ((int)(r[2] & 1) << 2) | ((int)bnd << 3) | ((tag < 0 ? 0 : tag & 15) << 4);
+      fa.z = bnd ? -1 : (int)r[0];
+      fa.w = bnd ? 0 : (int)r[1];
+      faces.push_back(fa);
+    }
+  std::vector<int> elems;
+  int64_t gstart[6];
+  for (int p = 0; p < 6; ++p) {
+    gstart[p] = (int64_t)elems.size();
+    elems.insert(elems.end(), groups[p].begin(), groups[p].end());
+    h->gr.cnt[p] = (int64_t)groups[p].size();
+  }
+  const size_t fpad = sizeof(double) * (size_t)M * 4 * 6;
+  cudaError_t err = cudaSuccess;
+  auto up = [&](auto** dst, const void* src, size_t bytes) {
+    if (err) return;
+    err = cudaMalloc((void**)dst, bytes > 0 ? bytes : 16);
+    if (!err && bytes) err = cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice);
+  };
+  up(&h->deg, deg.data(), deg.size());
+  up(&h->off, off.data(), sizeof(int64_t) * off.size());
+  up(&h->poff, poff.data(), sizeof(int64_t) * poff.size());
+  up(&h->geom, desc->geom, sizeof(double) * 20 * (size_t)M);
+  up(&h->ops, ops, sizeof(double) * 6 * 66);
+  up(&h->xfer, xfer, sizeof(double) * 36 * 2 * 36);
+  up(&h->link, lk.data(), sizeof(int2) * lk.size());
+  up(&h->faces, faces.data(), sizeof(int4) * faces.size());
+  up(&h->elems, elems.data(), sizeof(int) * elems.size());
+  if (!err) err = cudaMalloc(&h->qtr, fpad * 4);
+  if (!err) err = cudaMalloc(&h->fci, fpad * 4);
+  if (!err) err = cudaMalloc(&h->fvn, fpad * 4);
+  if (!err) err = cudaMalloc(&h->fcv, fpad * 4);
+  if (!err) err = cudaMalloc(&h->wh, fpad * 3);
+  if (!err) err = cudaMalloc(&h->grad, sizeof(double) * 6 * (size_t)(poff[(size_t)M] + 1));
+  if (err) {
+    pmgb_mdisc_destroy(h);
+    return (int)err;
+  }
+  for (int p = 0; p < 6; ++p) h->gr.elems[p] = h->elems + gstart[p];
+  h->m = MixDev{M, desc->kind == 0 ? K_EULER : K_NS, h->deg, h->off, h->poff, h->geom, h->link, h->ops, h->xfer,
+                (int64_t)faces.size(), h->faces};
+  *out = h;
+  return 0;
+}
+
+PMGB_API int64_t pmgb_mdisc_n_dofs(const pmgb_mdisc* h) { return h ? h->n_dofs : -1; }
+
+PMGB_API int pmgb_mdisc_eval(pmgb_mdisc* h, const double* q, const double* X, double eps, const pmgb_epilogue* e,
+                             double* out, void* stream) {
+  if (!h || !q || !out || !e) return -1;
+  if (e->mode == PMGB_EPI_RK) return -1;
+  Epi ep;
+  ep.mode = e->mode;
+  ep.s = e->s;
+  ep.eps = e->eps;
+  ep.adt = e->adt;
+  ep.dtau = e->dtau;
+  ep.sb_scalar = e->sb_scalar;
+  ep.se_scalar = e->se_scalar;
+  ep.X = e->X;
+  ep.R0 = e->R0;
+  ep.E = e->E;
+  ep.Sb = e->Sb;
+  ep.Se = e->Se;
+  ep.Q0 = nullptr;
+  ep.dtau_e = nullptr;
+  ep.alpha = 0.0;
+  ep.npe = 0;
+  int groups = 0;
+  for (int p = 0; p < 6; ++p) groups += h->gr.cnt[p] ? 1 : 0;
+  g_launches += groups * (h->m.kind == K_NS ? 3 : 2) + (h->m.kind == K_NS ? 2 : 1) + 1;
+  return mx_residual(h->C, h->m, h->gr, q, X, eps, ep, h->qtr, h->fci, h->wh, h->grad, h->fvn, h->fcv, out,
+                     bad_ptr(), status_ptr(), S(stream));
+}
+
+PMGB_API int pmgb_mdisc_freeze(pmgb_mdisc* h, const double* q, double* rq, double* rw, double* rf, void* stream) {
+  if (!h || !q || !rq) return -1;
+  // the global pipeline up to the one-sided viscous fluxes, then the records
+  Epi ep;
+  std::memset(&ep, 0, sizeof(ep));
+  int rc = mx_residual(h->C, h->m, h->gr, q, nullptr, 0.0, ep, h->qtr, h->fci, h->wh, h->grad, h->fvn, h->fcv,
+                       nullptr, nullptr, nullptr, S(stream));
+  if (rc) return rc;
+  int groups = 0;
+  for (int p = 0; p < 6; ++p) groups += h->gr.cnt[p] ? 1 : 0;
+  g_launches += groups * (h->m.kind == K_NS ? 2 : 1) + 2;
+  return mx_records(h->C, h->m, h->qtr, h->fvn, rq, rw, rf, S(stream));
+}
+
+PMGB_API int pmgb_mdisc_element_residual(pmgb_mdisc* h, int32_t p, const int64_t* elems, int64_t B,
+                                         const double* Q, const double* rq, const double* rw, const double* rf,
+                                         double* out, void* stream) {
+  if (!h || p < 0 || p > 5 || (B > 0 && (!elems || !Q || !rq || !out))) return -1;
+  g_launches += 1;
+  return mx_local(h->C, h->m, p, elems, B, Q, rq, rw, rf, out, S(stream));
+}
 
 PMGB_API int pmgb_disc_residual_path(pmgb_disc* h, int32_t want) {
   if (!h) return -1;

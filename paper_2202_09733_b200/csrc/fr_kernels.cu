@@ -2206,6 +2206,12 @@ int launch_coupling(const DiscDev& d, const double* q, const double* qtr, const 
   PMGB_DISPATCH(run_coupling, d, q, qtr, fvn, eps, npairs, pair_e, pair_f, pair_slot, pair_add, blocks, st)
 }
 
+int* bad_ptr() {
+  int* p = nullptr;
+  cudaGetSymbolAddress((void**)&p, g_bad);
+  return p;
+}
+
 Status* status_ptr() {
   Status* p = nullptr;
   cudaGetSymbolAddress((void**)&p, g_status);

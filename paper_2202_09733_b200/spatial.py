@@ -14,8 +14,10 @@ polynomial degree, with the arithmetic in libpmgflow_b200 (sm_100a FP64):
 
 Vectors may be NumPy arrays (copied in and out: the reference-facing
 end-to-end path) or contiguous float64 CUDA tensors (device-resident
-path used by the solvers).  Mixed-degree meshes are out of scope for
-this round and rejected loudly.
+path used by the solvers).  A per-element degree map with more than one
+degree constructs a ``MixedDiscretization`` (the reference's degree groups
+with mortar faces, csrc/fr_mixed.cu): residual, freeze and
+element_residual for Euler / Navier-Stokes with BR1.
 """
 
 from __future__ import annotations
@@ -112,7 +114,15 @@ def _mesh_tables(mesh: Mesh):
 
 
 class Discretization:
-    """FR residual operator on the device for a uniform-degree mesh."""
+    """FR residual operator on the device for a uniform-degree mesh (a
+    mixed degree map yields a MixedDiscretization)."""
+
+    def __new__(cls, mesh=None, degrees=None, eqn=None, device=None):
+        if cls is Discretization and degrees is not None:
+            d = np.asarray(degrees)
+            if d.ndim == 1 and d.size and (d != d[0]).any():
+                return super().__new__(MixedDiscretization)
+        return super().__new__(cls)
 
     def __init__(self, mesh: Mesh, degrees, eqn: EquationSpec, device=None):
         require_cuda()
@@ -367,5 +377,139 @@ class Discretization:
         out = torch.empty_like(Qf)
         check(load().pmgb_element_residual(self._h, el.data_ptr(), B, Qf.data_ptr(), frozen.qtr.data_ptr(),
                                            frozen.fvn.data_ptr(), out.data_ptr(), stream()), "element_residual")
+        out = out.reshape(shape)
+        return out.cpu().numpy() if is_np else out
+
+
+@dataclass
+class MixedFrozen:
+    """Frozen neighbour records of a mixed-degree mesh at each element's own
+    face points (spatial.py:700-766), padded to 6 points."""
+
+    rq: torch.Tensor   # (M, 4, 6, 4) neighbour trace
+    rw: torch.Tensor   # (M, 4, 6, 3) neighbour viscous variables
+    rf: torch.Tensor   # (M, 4, 6, 4) minus the neighbour's one-sided viscous flux
+
+
+class MixedDiscretization(Discretization):
+    """Device FR discretization with a per-element degree map (p = 0..5):
+    the reference's degree groups and mortar faces (spatial.py:295-359,
+    468-585) on csrc/fr_mixed.cu.  Euler / Navier-Stokes, Roe or Rusanov,
+    BR1 (the reference's only viscous scheme); flat vectors in the
+    reference's layout (element e at offsets[e])."""
+
+    def __init__(self, mesh: Mesh, degrees, eqn: EquationSpec, device=None):
+        from .operators import mixed_tables
+        require_cuda()
+        self.mesh, self.eqn = mesh, eqn
+        degrees = np.asarray(degrees, dtype=np.int64)
+        if len(degrees) != mesh.n_elements:
+            raise ValueError("degree map length does not match element count")
+        if (degrees < 0).any():
+            raise ValueError("degrees must be >= 0")
+        if degrees.max() > 5:
+            raise NotImplementedError("device kernels cover p = 0..5")
+        if eqn.kind not in ("euler", "navier-stokes"):
+            raise NotImplementedError("mixed-degree device path: Euler / Navier-Stokes")
+        if eqn.viscous_scheme != "br1":
+            raise NotImplementedError("mixed-degree device path: BR1 viscous fluxes (the reference's scheme)")
+        self.degrees = degrees
+        self.p = int(degrees.max())
+        self.nvars = eqn.nvars
+        sizes = self.nvars * (degrees + 1) ** 2
+        self.offsets = np.concatenate(([0], np.cumsum(sizes))).astype(np.int64)
+        self.n_dofs = int(self.offsets[-1])
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        geom, links, tags = _mesh_tables(mesh)
+        self._geom, self._links, self._tags = geom, np.ascontiguousarray(links), np.ascontiguousarray(tags)
+        self._qinf = np.ascontiguousarray(eqn.free_stream(), dtype=np.float64)
+        self._ops, self._xfer = mixed_tables()
+        self._deg32 = np.ascontiguousarray(degrees, dtype=np.int32)
+        z = np.zeros(36)
+        dp = lambda a: a.ctypes.data_as(_lib.c_double_p)  # noqa: E731
+        desc = _lib.DiscDesc(
+            n_elem=mesh.n_elements, degree=0, kind=KIND_CODE[eqn.kind], gamma=eqn.gamma, mu=eqn.mu,
+            kappa=eqn.heat_conductivity if eqn.kind == "navier-stokes" else 0.0, adv_x=0.0, adv_y=0.0,
+            diffusivity=0.0, free_stream=dp(self._qinf), D=dp(z), eL=dp(z), eR=dp(z), lL=dp(z), lR=dp(z),
+            xg=dp(z), geom=dp(self._geom), links=self._links.ctypes.data_as(_lib.c_int64_p),
+            tags=self._tags.ctypes.data_as(_lib.c_int32_p), riemann=1 if eqn.riemann == "rusanov" else 0,
+            viscous_scheme=0, wall_temperature=eqn.t_wall)
+        h = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            check(load().pmgb_mdisc_create(ctypes.byref(desc), self._deg32.ctypes.data_as(_lib.c_int32_p),
+                                           dp(self._ops), dp(self._xfer), ctypes.byref(h)), "mdisc_create")
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                load().pmgb_mdisc_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    def residual_path(self, want=None) -> str:
+        return "mixed"
+
+    def coarsen(self, p):
+        raise NotImplementedError("mixed-degree pMG levels: build the nested degree maps with "
+                                  "p_adapt.nest_hierarchy and construct each level directly")
+
+    def eval(self, q, mode: int, out=None, *, X=None, eps=0.0, s=0.0, adt=0.0, dtau=0.0, R0=None, E=None,
+             Sb=0.0, Se=0.0, Q0=None, dtau_e=None, alpha=0.0, check_status=False):
+        if mode == _lib.EPI_RK:
+            raise NotImplementedError("the RK smoother epilogue is uniform-degree only")
+        if out is None:
+            out = torch.empty(self.n_dofs, dtype=torch.float64, device=self.device)
+        ep = _lib.Epilogue()
+        ep.mode = mode
+        ep.s, ep.eps, ep.adt, ep.dtau = float(s), float(eps), float(adt), float(dtau)
+        ep.X = ptr(X) if X is not None else None
+        ep.R0 = ptr(R0) if R0 is not None else None
+        ep.E = ptr(E) if E is not None else None
+        if isinstance(Sb, torch.Tensor):
+            ep.Sb = ptr(Sb)
+        else:
+            ep.sb_scalar = float(Sb)
+        if isinstance(Se, torch.Tensor):
+            ep.Se = ptr(Se)
+        else:
+            ep.se_scalar = float(Se)
+        jv = X is not None and mode in (_lib.EPI_JV, _lib.EPI_STAGE_JV)
+        check(load().pmgb_mdisc_eval(self._h, ptr(q), ptr(X) if jv else None, float(eps), ctypes.byref(ep),
+                                     ptr(out), stream()), "mdisc_eval")
+        if check_status:
+            raise_status()
+        return out
+
+    def freeze(self, data) -> MixedFrozen:
+        q = to_device(data, self.device)
+        M = self.mesh.n_elements
+        rq = torch.zeros((M, 4, 6, 4), dtype=torch.float64, device=self.device)
+        rw = torch.zeros((M, 4, 6, 3), dtype=torch.float64, device=self.device)
+        rf = torch.zeros((M, 4, 6, 4), dtype=torch.float64, device=self.device)
+        check(load().pmgb_mdisc_freeze(self._h, ptr(q), rq.data_ptr(), rw.data_ptr(), rf.data_ptr(), stream()),
+              "mdisc_freeze")
+        return MixedFrozen(rq, rw, rf)
+
+    def element_residual(self, e, Q, frozen: MixedFrozen):
+        """Element-local residual (spatial.py:768-853); ``e`` an int or an
+        array of elements of one degree, Q (..., n, n, nv)."""
+        is_np = not isinstance(Q, torch.Tensor)
+        els = np.atleast_1d(np.asarray(e, dtype=np.int64))
+        p = int(self.degrees[els[0]])
+        if (self.degrees[els] != p).any():
+            raise ValueError("element_residual: the elements must share one degree")
+        n = p + 1
+        Qd = to_device(Q, self.device)
+        shape = Qd.shape
+        Qf = Qd.reshape(-1, self.nvars * n * n).contiguous()
+        B = Qf.shape[0]
+        el = torch.as_tensor(np.broadcast_to(els, (B,)).copy() if els.size == 1 else els, device=self.device)
+        out = torch.empty_like(Qf)
+        check(load().pmgb_mdisc_element_residual(self._h, p, el.data_ptr(), B, Qf.data_ptr(), frozen.rq.data_ptr(),
+                                                 frozen.rw.data_ptr(), frozen.rf.data_ptr(), out.data_ptr(),
+                                                 stream()), "mdisc_element_residual")
         out = out.reshape(shape)
         return out.cpu().numpy() if is_np else out
