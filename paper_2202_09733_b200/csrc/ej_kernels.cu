@@ -48,12 +48,16 @@ template <int SZ> struct GJShape {
 };
 
 // One CTA per block.  BT: FD blocks, column-major (BT[c][r] = B[r][c]).
-// Per pivot step: column-k owners publish the column, every warp finds the
-// pivot redundantly (lane l owns rows [l*RPL, l*RPL+RPL): one max-reduction
-// + a ballot, the lowest tied lane holds the lowest row), the pivot-row
-// owners publish the normalised row, and every thread updates its tile
-// with exactly one DFMA per entry (pivot row / pivot column zeroed first,
-// the pivot row's multiplier is 1).
+// Thread (rg, cg) holds a TR x TC register tile: rows rg + NRG i (row
+// groups interleaved, so the warp's column-buffer reads are consecutive
+// doubles: conflict-free), columns cg TC + j.  Per pivot step: column-k
+// owners publish the column, every warp finds the pivot redundantly (lane
+// l scans rows l + 32 m; max |a| over unused rows, ties to the lowest row:
+// the candidate set and rule of LAPACK getrf), the pivot-row owners publish
+// the normalised row, and every thread updates its tile with exactly one
+// DFMA per entry (pivot row / pivot column zeroed first, the pivot row's
+// multiplier is 1).  The arithmetic per entry does not depend on the tile
+// mapping: factors are bitwise those of any other mapping.
 template <int SZ>
 __global__ void __launch_bounds__(GJShape<SZ>::THREADS, (GJShape<SZ>::THREADS <= 256 ? 2 : 1))
 k_gj_inverse(const double* __restrict__ BT, double* __restrict__ XT, uint8_t* __restrict__ perm, Status* st,
@@ -71,19 +75,19 @@ k_gj_inverse(const double* __restrict__ BT, double* __restrict__ XT, uint8_t* __
   const int lane = tid & 31;
   const bool active = tid < NRG * NCG;
   const int rg = tid % NRG, cg = tid / NRG;
-  const int r0 = rg * TR, c0 = cg * TC;
+  const int c0 = cg * TC;
   const double* src = BT + e_in * (int64_t)SZ * SZ;
   double a[TR][TC];
 #pragma unroll
   for (int j = 0; j < TC; ++j) {
 #pragma unroll
     for (int i = 0; i < TR; ++i) {
-      const int r = r0 + i, c = c0 + j;
+      const int r = rg + NRG * i, c = c0 + j;
       a[i][j] = (active && r < SZ && c < SZ) ? __ldg(src + (int64_t)c * SZ + r) : 0.0;
     }
   }
   if (tid == 0) s_bad = 0;
-  unsigned used = 0;  // bit m: row lane*RPL + m already pivoted (same in every warp)
+  unsigned used = 0;  // bit m: row lane + 32 m already pivoted (same in every warp)
   for (int kg = 0; kg < NCG; ++kg) {
 #pragma unroll
     for (int kk = 0; kk < TC; ++kk) {
@@ -95,14 +99,14 @@ k_gj_inverse(const double* __restrict__ BT, double* __restrict__ XT, uint8_t* __
       if (colown) {
 #pragma unroll
         for (int i = 0; i < TR; ++i)
-          if (r0 + i < SZ) cb[r0 + i] = a[i][kk];
+          if (rg + NRG * i < SZ) cb[rg + NRG * i] = a[i][kk];
       }
       __syncthreads();
       double best = -1.0;
       int brow = -1;
 #pragma unroll
       for (int m = 0; m < RPL; ++m) {
-        const int r = lane * RPL + m;
+        const int r = lane + 32 * m;
         if (r < SZ && !((used >> m) & 1u)) {
           const double v = fabs(cb[r]);
           if (v > best) {
@@ -111,25 +115,27 @@ k_gj_inverse(const double* __restrict__ BT, double* __restrict__ XT, uint8_t* __
           }
         }
       }
-      double wmax = best;
+      // warp arg-max, ties to the lowest row (rows of different lanes interleave)
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) {
-        const double o = __shfl_xor_sync(0xffffffffu, wmax, off);
-        wmax = o > wmax ? o : wmax;
+        const double ov = __shfl_xor_sync(0xffffffffu, best, off);
+        const int orow = __shfl_xor_sync(0xffffffffu, brow, off);
+        if (orow >= 0 && (brow < 0 || ov > best || (ov == best && orow < brow))) {
+          best = ov;
+          brow = orow;
+        }
       }
-      const unsigned ball = __ballot_sync(0xffffffffu, brow >= 0 && best == wmax);
-      const bool nan_col = (ball == 0u);
-      int p = __shfl_sync(0xffffffffu, brow, nan_col ? 0 : __ffs(ball) - 1);
-      if (nan_col) p = k;  // every candidate NaN: flagged singular below
-      if (lane == p / RPL) used |= 1u << (p - lane * RPL);
+      const bool nan_col = brow < 0;
+      const int p = nan_col ? k : brow;  // every candidate NaN: flagged singular below
+      if (!nan_col && lane == (p & 31)) used |= 1u << (p >> 5);
       const double pv = cb[p];
       if (tid == 0) {
         pivs[k] = p;
         if (nan_col || !(pv != 0.0) || !isfinite(pv)) s_bad = 1;
       }
       const double pinv = 1.0 / pv;
-      const bool rowown = active && rg == p / TR;
-      const int ip = p - r0;
+      const bool rowown = active && rg == p % NRG;
+      const int ip = p / NRG;
       if (rowown) {
 #pragma unroll
         for (int i = 0; i < TR; ++i) {
@@ -147,7 +153,7 @@ k_gj_inverse(const double* __restrict__ BT, double* __restrict__ XT, uint8_t* __
         double g[TR];
 #pragma unroll
         for (int i = 0; i < TR; ++i) {
-          const int r = r0 + i;
+          const int r = rg + NRG * i;
           g[i] = (r < SZ) ? ((r == p) ? 1.0 : -cb[r]) : 0.0;
         }
         if (colown) {
@@ -183,7 +189,7 @@ k_gj_inverse(const double* __restrict__ BT, double* __restrict__ XT, uint8_t* __
     for (int j = 0; j < TC; ++j) {
 #pragma unroll
       for (int i = 0; i < TR; ++i) {
-        const int r = r0 + i, c = c0 + j;
+        const int r = rg + NRG * i, c = c0 + j;
         if (r < SZ && c < SZ) dst[(int64_t)c * SZ + r] = a[i][j];
       }
     }
