@@ -94,6 +94,7 @@ PMGB_API const char* pmgb_error_string(int code) {
     case -3: return "unsupported equation kind";
     case -4: return "mesh too large for one device context (face offsets exceed 2^31)";
     case -5: return "forces are only defined for flow equations";
+    case -6: return "state / operand arrays must be 32-byte aligned (256-bit accesses)";
     case -1000: return "no kernel instance for this degree/kind";
     case -1001: return "vector count out of range";
   }
@@ -424,7 +425,10 @@ PMGB_API int pmgb_mdisc_element_residual(pmgb_mdisc* h, int32_t p, const int64_t
 
 PMGB_API int pmgb_disc_residual_path(pmgb_disc* h, int32_t want) {
   if (!h) return -1;
-  if (want >= 0) h->d.has_rect = (want != 0 && h->d.rect.frec != nullptr) ? 1 : 0;
+  // 0 general, 1 rectangle kernels (the two-kernel chain, its second kernel chosen
+  // per degree), 2 the four-kernel chain, 3 the two-kernel chain with the one-shot
+  // k_rasm, 4 with the persistent k_rasm_p (2-4: A/B runs and cross-checks)
+  if (want >= 0) h->d.has_rect = (want != 0 && h->d.rect.frec != nullptr) ? (want >= 2 && want <= 4 ? want : 1) : 0;
   return h->d.has_rect;
 }
 
@@ -451,9 +455,13 @@ PMGB_API int pmgb_eval(pmgb_disc* h, const double* q, const double* X, double ep
   ep.alpha = e->alpha;
   ep.npe = (int)((h->d.p + 1) * (h->d.p + 1) * h->d.nv);
   if (ep.mode == EPI_RK && (!ep.Q0 || !ep.dtau_e)) return -1;
-  // rectangle path: k_rface (+ k_rgrad for NS) + k_rfc + k_rasm
   const bool rect = h->d.has_rect && rect_supported(h->d.p, h->d.kind);
-  g_launches += rect ? (h->d.kind == K_NS ? 4 : 3) : n_res_launches(h->d);
+  if (rect) {   // the rectangle kernels move whole points (4 doubles) per access
+    const void* ps[] = {q, X, out, ep.X, ep.R0, ep.E, ep.Sb, ep.Se, ep.Q0};
+    for (const void* p : ps)
+      if (((uintptr_t)p & 31u) != 0) return -6;
+  }
+  g_launches += rect ? rect_launches(h->d, X != nullptr) : n_res_launches(h->d);
   return launch_residual(h->d, q, X, eps, ep, out, S(stream));
 }
 

@@ -81,11 +81,35 @@ __host__ __device__ constexpr int tl(int el, int line, int pos) {
 
 // per-face-point record of the unique-face array: F on L's normal, then the
 // one-sided viscous fluxes of the L and R sides on their own normals
-constexpr int FREC = 12;
+constexpr int FREC4 = 12;
+// two-kernel chain: [0..3] G = F - (L's share of the common viscous flux),
+// written by the L side; [4..6] H = the R side's share (component 0 of a
+// viscous flux is identically zero), written by the R side; the common
+// total normal flux on L's normal is Fc = G + H (boundary faces: G)
+constexpr int FREC = 8;
 
+#ifndef PMGB_RECT_TH   // CTA width target of the element kernels (A/B)
+#define PMGB_RECT_TH 128
+#endif
+#ifndef PMGB_RECT_PF   // L2 prefetch distance in CTAs (0: off) (A/B)
+#define PMGB_RECT_PF 0
+#endif
+// k_rasm (two-kernel chain) walks the element blocks in descending order: what
+// k_rgf touched last is still in L2 (config-2 R 110.7 -> 105.0 us, Jv 159.2 ->
+// 152.2 us; profiles/r2/ab_rev_r2q.log)
+#ifndef PMGB_RECT_REV
+#define PMGB_RECT_REV 1
+#endif
+#ifndef PMGB_RECT_XCH_MASK   // degrees whose k_rgf hands traces over inside the CTA (bit P)
+#define PMGB_RECT_XCH_MASK 0x14
+#endif
 template <int P> struct RC {
   static constexpr int N = P + 1, NP = N * N;
-  static constexpr int EPB = 128 / N;  // elements per CTA
+  // k_rgf: neighbours inside the CTA's element run pass their traces
+  // through shared memory instead of being gathered again (measured per
+  // degree, profiles/r2/ab_xch_r2n.log: faster at p = 2 and 4)
+  static constexpr bool XCH = ((PMGB_RECT_XCH_MASK >> P) & 1) != 0;
+  static constexpr int EPB = PMGB_RECT_TH / N;  // elements per CTA
   static constexpr int TH = EPB * N;   // one thread per (element, line)
   // line block strides in doubles: >= 3N (gradient passes) / 4N (flux
   // passes), even, an odd number of 16-byte units
@@ -94,7 +118,7 @@ template <int P> struct RC {
   static constexpr int WD = EPB * 4 * N * 3;  // of a What block
   static constexpr int FD = EPB * 4 * N * 4;  // of an Fc block
   // CTAs per SM the register target is set for
-  static constexpr int MINB = P == 5 ? 2 : (P >= 3 ? 3 : 4);
+  static constexpr int MINB = (P == 5 ? 2 : (P >= 3 ? 3 : 4)) * (128 / PMGB_RECT_TH);
 };
 
 // q (+ eps X with the reference's rounding, newton_krylov.py:76) of point pt
@@ -213,6 +237,60 @@ __device__ __forceinline__ void stg4(double* p, const double* v) {
                : "memory");
 }
 
+// The epilogue operands of one point (4 variables) as 256-bit loads:
+// epi_load_k's operands (fr_device.cuh), o*[v] for variable v
+template <int EK>
+__device__ __forceinline__ void epi_load4_k(const Epi& ep, int64_t i, double* o1, double* o2, double* o3) {
+  if constexpr (EK < 0) {
+#pragma unroll
+    for (int v = 0; v < 4; ++v) epi_load_k<EK>(ep, i + v, o1[v], o2[v], o3[v]);
+  } else {
+#pragma unroll
+    for (int v = 0; v < 4; ++v) o1[v] = o2[v] = o3[v] = 0.0;
+    constexpr bool SBSE = EK == EPI_DEFECT || EK == EPI_RK;
+    if constexpr (EK == EPI_JV || EK == EPI_STAGE_JV) {
+      ldg4(ep.X + i, o1);
+      ldg4(ep.R0 + i, o2);
+    }
+    if constexpr (EK == EPI_STAGE_F || EK == EPI_STAGE_JV) ldg4(ep.E + i, o3);
+    if constexpr (SBSE) {
+      if (ep.Sb)
+        ldg4(ep.Sb + i, o1);
+      else
+        o1[0] = o1[1] = o1[2] = o1[3] = ep.sb_scalar;
+    }
+    if constexpr (SBSE || EK == EPI_OUTER_F) {
+      if (ep.Se)
+        ldg4(ep.Se + i, o2);
+      else
+        o2[0] = o2[1] = o2[2] = o2[3] = ep.se_scalar;
+    }
+    if constexpr (EK == EPI_RK) ldg4(ep.Q0 + i, o3);
+  }
+}
+
+// L2 prefetch of the epilogue operands of a CTA's element block (issued at
+// kernel start: the operands are inputs of the whole chain), so that the
+// loads at the end of the kernel find them in L2
+#ifndef PMGB_RECT_EPF   // measured: config-2 Jv 166.4 -> 161.3 us (profiles/r2/ab_pdl0_epf_r2p.log)
+#define PMGB_RECT_EPF 1
+#endif
+__device__ __forceinline__ void l2_prefetch_blk(const double* p, int64_t off, uint32_t bytes) {
+  if (p != nullptr)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p + off), "r"(bytes) : "memory");
+}
+template <int EK>
+__device__ __forceinline__ void epi_prefetch(const Epi& ep, int64_t off, uint32_t bytes) {
+  if constexpr (EK == EPI_JV || EK == EPI_STAGE_JV) {
+    l2_prefetch_blk(ep.X, off, bytes);
+    l2_prefetch_blk(ep.R0, off, bytes);
+  }
+  if constexpr (EK == EPI_STAGE_F || EK == EPI_STAGE_JV) l2_prefetch_blk(ep.E, off, bytes);
+  if constexpr (EK == EPI_DEFECT || EK == EPI_RK) l2_prefetch_blk(ep.Sb, off, bytes);
+  if constexpr (EK == EPI_DEFECT || EK == EPI_RK || EK == EPI_OUTER_F) l2_prefetch_blk(ep.Se, off, bytes);
+  if constexpr (EK == EPI_RK) l2_prefetch_blk(ep.Q0, off, bytes);
+}
+
 // L2 residency hints across the chain (126 MB L2; working set ~190 MB at
 // config 2): intermediates stored evict_last, inputs loaded evict_first on
 // their last read of the chain (k_rasm).  Measured slower (config-2 R
@@ -258,13 +336,12 @@ __device__ __forceinline__ void ldg4_first(const double* p, double* o) {
 // ---------------------------------------------------------------------------
 // k_rface: traces, interface flux and BR1 common value, once per face point
 
-template <int P, int KIND, bool HASX>
+template <int P, int KIND, bool HASX, int RS = FREC4>
 __global__ void __launch_bounds__(128) k_rface(const FrConst C, const RectMesh m, const double* __restrict__ q,
                                                const double* __restrict__ X, double eps, double* __restrict__ frec,
                                                double* __restrict__ wh, int* __restrict__ bad) {
   constexpr int N = P + 1;
   constexpr bool VISC = KT<KIND>::VISC;
-  pdl_trigger();
   const int64_t t = (int64_t)blockIdx.x * 128 + threadIdx.x;
   if (t >= m.nface * N) return;
   const int64_t phi = t / N;
@@ -275,6 +352,10 @@ __global__ void __launch_bounds__(128) k_rface(const FrConst C, const RectMesh m
   const double g = C.gamma;
   const Phys ph = phys_of(C);
   const int kk = rev ? N - 1 - k : k;
+  // q is k_form's output when the chain evaluates at q + eps X; the
+  // successors (which read q ahead of their own wait) start after it
+  pdl_wait();
+  pdl_trigger();
   double qa[4], qc[4];
   // Euler: the states are checked here, on the rows of each element's face 1
   bool okL = true, okR = true;
@@ -296,7 +377,7 @@ __global__ void __launch_bounds__(128) k_rface(const FrConst C, const RectMesh m
     rusanov_pr(qa, A, qc, B, nrm.x, nrm.y, g, F);
   else
     roe_pr(qa, A, qc, B, nrm.x, nrm.y, g, F);
-  stg4_last(frec + t * FREC, F);
+  stg4_last(frec + t * RS, F);
   if constexpr (VISC) {
     double wa[3] = {A.u, A.v, A.p * A.ir}, wc[3] = {B.u, B.v, B.p * B.ir};
     if (bnd) ghost_w<KIND>(ph, tag, wa, wc);
@@ -329,7 +410,7 @@ __global__ void __launch_bounds__(128) k_rfc(const FrConst C, const RectMesh m, 
   if (!live) return;
   const int fL = fr.y & 3, rev = (fr.y >> 2) & 1, bnd = (fr.y >> 3) & 1, tag = (fr.y >> 4) & 15;
   const Phys ph = phys_of(C);
-  const double* rec = frec + t * FREC;
+  const double* rec = frec + t * FREC4;
   double Fc[4];
   ldg4_first(rec, Fc);
   if constexpr (KT<KIND>::VISC) {
@@ -384,6 +465,9 @@ __device__ __forceinline__ void bulk_g2s_first(void* dst, const void* src, uint3
 #else
   bulk_g2s(dst, src, bytes, bar);
 #endif
+}
+__device__ __forceinline__ void l2_prefetch(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   asm volatile(
@@ -474,6 +558,28 @@ __device__ __forceinline__ void visc_fy(const double* q, const double* gx, const
   fy[3] = u * txy + v * tyy + ph.kappa * gy[2];
 }
 
+// the same from the trace state's velocity (u, v as prim() forms them)
+__device__ __forceinline__ void visc_fx_uv(double u, double v, const double* gx, const double* gy, const Phys& ph,
+                                           double* fx) {
+  const double d = gx[0] + gy[1];
+  const double txx = ph.mu * (2.0 * gx[0] - (2.0 / 3.0) * d);
+  const double txy = ph.mu * (gy[0] + gx[1]);
+  fx[0] = 0.0;
+  fx[1] = txx;
+  fx[2] = txy;
+  fx[3] = u * txx + v * txy + ph.kappa * gx[2];
+}
+__device__ __forceinline__ void visc_fy_uv(double u, double v, const double* gx, const double* gy, const Phys& ph,
+                                           double* fy) {
+  const double d = gx[0] + gy[1];
+  const double tyy = ph.mu * (2.0 * gy[1] - (2.0 / 3.0) * d);
+  const double txy = ph.mu * (gy[0] + gx[1]);
+  fy[0] = 0.0;
+  fy[1] = txy;
+  fy[2] = tyy;
+  fy[3] = u * txy + v * tyy + ph.kappa * gy[2];
+}
+
 // divergence along one line of a 4-variable flux x[v][i]: the +1 end takes
 // (Fp - trace), the -1 end (-Fm - trace)  (the reference's c1/c3, c2/c0)
 template <int N>
@@ -526,7 +632,6 @@ k_rgrad(const FrConst C, const RectMesh m, const double* __restrict__ q, const d
   double* sY = sm + R::QD + L::BUF;   // gy (row blocks)
   const double* sWb = sm + L::OFF_W;  // What block [el][f][k][3]
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::OFF_BAR);
-  pdl_trigger();
   const int t = threadIdx.x;
   const int el = t / N, a = t % N;  // row a of element el; also column a
   const int64_t e0 = (int64_t)blockIdx.x * E;
@@ -700,49 +805,404 @@ k_rgrad(const FrConst C, const RectMesh m, const double* __restrict__ q, const d
   {
     const double gyv[2] = {tgy1[0], tgy1[1]};
     visc_fx(t1q, tgx1, gyv, ph, o);
-    stg4_last(frec + (int64_t)ri[1] * FREC + (lft[1] ? 4 : 8), o);
+    stg4_last(frec + (int64_t)ri[1] * FREC4 + (lft[1] ? 4 : 8), o);
   }
   {
     const double gyv[2] = {tgy3[0], tgy3[1]};
     visc_fx(t3q, tgx3, gyv, ph, o);
     o[1] = -o[1], o[2] = -o[2], o[3] = -o[3];
-    stg4_last(frec + (int64_t)ri[3] * FREC + (lft[3] ? 4 : 8), o);
+    stg4_last(frec + (int64_t)ri[3] * FREC4 + (lft[3] ? 4 : 8), o);
   }
   {
     const double gxv[2] = {tgx2[0], tgx2[1]};
     visc_fy(t2q, gxv, tgy2, ph, o);
-    stg4_last(frec + (int64_t)ri[2] * FREC + (lft[2] ? 4 : 8), o);
+    stg4_last(frec + (int64_t)ri[2] * FREC4 + (lft[2] ? 4 : 8), o);
   }
   {
     const double gxv[2] = {tgx0[0], tgx0[1]};
     visc_fy(t0q, gxv, tgy0, ph, o);
     o[1] = -o[1], o[2] = -o[2], o[3] = -o[3];
-    stg4_last(frec + (int64_t)ri[0] * FREC + (lft[0] ? 4 : 8), o);
+    stg4_last(frec + (int64_t)ri[0] * FREC4 + (lft[0] ? 4 : 8), o);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// The common total normal flux of the two-kernel chain, split by side
+// (spatial.py:559-568; BR1: Fc = F - (fl - fr)/2 = (F - fl/2) + fr/2; LDG:
+// Fc = F + fr; boundary: Fc = F - fl, energy row kept on adiabatic walls)
+__device__ __forceinline__ void gh_left(const Phys& ph, bool bnd, int tag, const double* F, const double* fl,
+                                        double* G) {
+  if (bnd) {
+#pragma unroll
+    for (int v = 0; v < 4; ++v) G[v] = F[v] - ((v == 3 && tag == T_WALL_ADIABATIC) ? 0.0 : fl[v]);
+  } else {
+#pragma unroll
+    for (int v = 0; v < 4; ++v) G[v] = ph.ldg ? F[v] : F[v] - 0.5 * fl[v];
+  }
+}
+__device__ __forceinline__ void gh_right(const Phys& ph, const double* fr, double* H) {
+  H[0] = ph.ldg ? fr[1] : 0.5 * fr[1];
+  H[1] = ph.ldg ? fr[2] : 0.5 * fr[2];
+  H[2] = ph.ldg ? fr[3] : 0.5 * fr[3];
+  H[3] = 0.0;
+}
+// Fc on the own normal from the record halves (H = zeros on boundary faces)
+__device__ __forceinline__ void gh_combine(bool lft, const double* G, const double* H, double* Fc) {
+  const double c0 = G[0], c1 = G[1] + H[0], c2 = G[2] + H[1], c3 = G[3] + H[2];
+  Fc[0] = lft ? c0 : -c0;
+  Fc[1] = lft ? c1 : -c1;
+  Fc[2] = lft ? c2 : -c2;
+  Fc[3] = lft ? c3 : -c3;
+}
+
+// ---------------------------------------------------------------------------
+// Static face data of line thread (el, a): its four face points sit at the
+// ends of row a (faces 1, 3) and of column a (faces 2, 0).
+struct FaceStat {
+  int ri[4];     // face-record index: unique face slot * N + L's point
+  int nb[4];     // neighbour element (-1: boundary face)
+  int fl[4];     // the link flags {neighbour face, rev, is_left, tag}
+};
+template <int N>
+__device__ __forceinline__ void face_stat(const RectMesh& m, int64_t e, int a, bool live, FaceStat& s) {
+#pragma unroll
+  for (int f = 0; f < 4; ++f) s.ri[f] = 0, s.nb[f] = -1, s.fl[f] = 8;
+  if (!live) return;
+  const int4 sl = __ldg(reinterpret_cast<const int4*>(m.fslot) + e);
+  const int4 l01 = __ldg(reinterpret_cast<const int4*>(m.link) + 2 * e);
+  const int4 l23 = __ldg(reinterpret_cast<const int4*>(m.link) + 2 * e + 1);
+  const int slot[4] = {sl.x, sl.y, sl.z, sl.w};
+  const int2 lk[4] = {make_int2(l01.x, l01.y), make_int2(l01.z, l01.w), make_int2(l23.x, l23.y),
+                      make_int2(l23.z, l23.w)};
+#pragma unroll
+  for (int f = 0; f < 4; ++f) {
+    const int k = (f >= 2) ? N - 1 - a : a;
+    const bool lft = lk[f].x < 0 || lk_left(lk[f].y);
+    const int kL = (!lft && lk_rev(lk[f].y)) ? N - 1 - k : k;
+    s.ri[f] = slot[f] * N + kL;
+    s.nb[f] = lk[f].x;
+    s.fl[f] = lk[f].y;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_rgf (NS kinds): k_rface and k_rgrad in one element kernel.  The own
+// traces come from the staged q block; only the neighbours' traces are
+// gathered (issued before the q block is awaited).  Every thread forms the
+// common value What of its four face points (both sides of a face evaluate
+// the same expression on the same operands), the side that owns a face (L)
+// evaluates the interface flux once, and What goes to the element's own
+// What block only -- no What round trip inside this kernel, no scattered
+// What stores.  Bitwise the results of k_rface + k_rgrad.
+
+template <int P, bool HASX> struct GFL {
+  using R = RC<P>;
+  static constexpr int BUF = R::EPB * TL<R::N, 3>::S;
+  static constexpr int A = 2 * BUF, B = HASX ? R::QD : 0;
+  static constexpr int STAGE = A > B ? A : B;
+  static constexpr int OFF_T = R::QD + STAGE;
+  static constexpr int OFF_BAR = OFF_T + (R::XCH ? R::FD : 0);
+  static constexpr size_t BYTES = sizeof(double) * (OFF_BAR + 2);
+};
+
+template <int P, int KIND, bool HASX>
+__global__ void __launch_bounds__(RC<P>::TH, RC<P>::MINB)
+k_rgf(const FrConst C, const RectMesh m, const double* __restrict__ q, const double* __restrict__ X, double eps,
+      double* __restrict__ wh, double* __restrict__ frec, int* __restrict__ bad) {
+  using R = RC<P>;
+  using L = GFL<P, HASX>;
+  constexpr int N = R::N, NP = R::NP, E = R::EPB;
+  extern __shared__ __align__(128) double sm[];
+  double* sQ = sm;
+  double* sX = sm + R::QD;            // X block; then W, then gx (column blocks)
+  double* sY = sm + R::QD + L::BUF;   // gy (row blocks)
+  double* sT = sm + L::OFF_T;         // own traces [el][f][k][4]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::OFF_BAR);
+  const int t = threadIdx.x;
+  const int el = t / N, a = t % N;  // row a of element el; also column a
+  const int64_t e0 = (int64_t)blockIdx.x * E;
+  const int ne = (int)((m.M - e0) < E ? (m.M - e0) : E);
+  const int64_t e = e0 + el;
+  const bool live = t < E * N && el < ne;
+  const Phys ph = phys_of(C);
+  const double g = C.gamma;
+  if (t == 0) mbar_init(bar);
+  __syncthreads();
+  // q is k_form's output when the chain evaluates at q + eps X; k_rasm
+  // (which requests its q block ahead of its own wait) starts after it
+  pdl_wait();
+  pdl_trigger();
+  const uint32_t qbytes = (uint32_t)ne * NP * 32;
+  if (t == 0) {
+    mbar_expect(bar, HASX ? 2 * qbytes : qbytes);
+    bulk_g2s(sQ, q + e0 * NP * 4, qbytes, bar);
+    if (HASX) bulk_g2s(sX, X + e0 * NP * 4, qbytes, bar);
+  }
+  FaceStat fs;
+  face_stat<N>(m, e, a, live, fs);
+  const double2 rg = live ? __ldg(m.rgeo + e) : make_double2(0.0, 0.0);
+  // the neighbours' traces at the thread's four face points: gathered
+  // from q when the neighbour belongs to another CTA; a neighbour of this
+  // CTA's own element run hands over the trace it forms itself (below) --
+  // the same sum in the same order
+  double qn[4][4];
+  double2 nrm[4];
+  bool inb[4];
+#pragma unroll
+  for (int f = 0; f < 4; ++f) {
+    qn[f][0] = qn[f][1] = qn[f][2] = qn[f][3] = 1.0;
+    nrm[f] = make_double2(0.0, 0.0);
+    inb[f] = R::XCH && fs.nb[f] >= e0 && fs.nb[f] < e0 + ne;
+    if (live) {
+      nrm[f] = __ldg(reinterpret_cast<const double2*>(m.geom + e * 20 + 8 + 2 * f));
+      if (fs.nb[f] >= 0 && !inb[f]) {
+        const int k = (f >= 2) ? N - 1 - a : a;
+        face_trace<P, HASX>(C, q, X, eps, fs.nb[f], lk_face(fs.fl[f]), lk_rev(fs.fl[f]) ? N - 1 - k : k, qn[f]);
+      }
+    }
+  }
+  mbar_wait(bar, 0);
+  if constexpr (HASX) {
+    form_qp<R::TH>(sQ, sX, eps, ne * NP * 4);
+    __syncthreads();
+  }
+  // own traces: faces 1 / 3 from row a, faces 2 / 0 from column a
+  double qo[4][4];
+#pragma unroll
+  for (int f = 0; f < 4; ++f) qo[f][0] = qo[f][1] = qo[f][2] = qo[f][3] = 0.0;
+  const double* row = sQ + (el * N + a) * N * 4;
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    double x[4];
+    lds4(row + 4 * i, x);
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      qo[1][v] += C.eR[i] * x[v];
+      qo[3][v] += C.eL[i] * x[v];
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    double x[4];
+    lds4(sQ + ((el * N + i) * N + a) * 4, x);
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      qo[2][v] += C.eR[i] * x[v];
+      qo[0][v] += C.eL[i] * x[v];
+    }
+  }
+  // hand the own traces to the neighbours inside the CTA
+  if constexpr (R::XCH) {
+#pragma unroll
+    for (int f = 0; f < 4; ++f) {
+      double* d = sT + ((el * 4 + f) * N + ((f >= 2) ? N - 1 - a : a)) * 4;
+      reinterpret_cast<double2*>(d)[0] = make_double2(qo[f][0], qo[f][1]);
+      reinterpret_cast<double2*>(d)[1] = make_double2(qo[f][2], qo[f][3]);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int f = 0; f < 4; ++f)
+      if (live && inb[f]) {
+        const int k = (f >= 2) ? N - 1 - a : a;
+        const int kk = lk_rev(fs.fl[f]) ? N - 1 - k : k;
+        lds4(sT + (((int)(fs.nb[f] - e0) * 4 + lk_face(fs.fl[f])) * N + kk) * 4, qn[f]);
+      }
+  }
+  // common values; the interface flux on the faces this element owns
+  double whv[4][3], uv[4][2], Fk[4][4];
+#pragma unroll
+  for (int f = 0; f < 4; ++f) {
+    const bool bnd = fs.nb[f] < 0;
+    const bool lft = bnd || lk_left(fs.fl[f]);
+    const int tag = lk_tag(fs.fl[f]);
+    Fk[f][0] = Fk[f][1] = Fk[f][2] = Fk[f][3] = 0.0;
+    const Pr O = prim_of(qo[f], g);
+    uv[f][0] = O.u;
+    uv[f][1] = O.v;
+    double qc[4];
+    if (bnd)
+      ghost<KIND>(qo[f], tag, nrm[f].x, nrm[f].y, C.qinf, qc);
+    else
+      qc[0] = qn[f][0], qc[1] = qn[f][1], qc[2] = qn[f][2], qc[3] = qn[f][3];
+    const Pr Q = prim_of(qc, g);
+    double wo[3] = {O.u, O.v, O.p * O.ir}, wq[3] = {Q.u, Q.v, Q.p * Q.ir};
+    if (lft) {
+      if (live && bad != nullptr) {
+        if (!(O.r > 0.0 && O.p > 0.0)) atomicMin(bad + 1, (int)e);
+        if (!bnd && !(Q.r > 0.0 && Q.p > 0.0)) atomicMin(bad + 1, fs.nb[f]);
+      }
+      if (ph.riemann)
+        rusanov_pr(qo[f], O, qc, Q, nrm[f].x, nrm[f].y, g, Fk[f]);
+      else
+        roe_pr(qo[f], O, qc, Q, nrm[f].x, nrm[f].y, g, Fk[f]);
+      if (bnd) ghost_w<KIND>(ph, tag, wo, wq);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) whv[f][c] = common_w(ph, !bnd, true, wo[c], wq[c]);
+    } else {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) whv[f][c] = common_w(ph, true, true, wq[c], wo[c]);
+    }
+    if (live) {
+      double* dw = wh + ((e * 4 + f) * N + ((f >= 2) ? N - 1 - a : a)) * 3;
+      stg1_last(dw, whv[f][0]), stg1_last(dw + 1, whv[f][1]), stg1_last(dw + 2, whv[f][2]);
+    }
+  }
+  // rows: primitives, W
+  double w[3][N];
+  {
+    bool ok = true;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      double x[4];
+      lds4(row + 4 * i, x);
+      const Pr s = prim_of(x, g);
+      ok = ok && (s.r > 0.0) && (s.p > 0.0);
+      w[0][i] = s.u;
+      w[1][i] = s.v;
+      w[2][i] = s.p * s.ir;
+    }
+    if (live && !ok && bad != nullptr) atomicMin(bad, (int)e);
+  }
+  // W into column blocks: block (el, i) holds column i, [c][row]
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) sX[tl<N, 3>(el, i, c * N + a)] = w[c][i];
+  // gx along row a (faces 1 and 3)
+  double gx[3][N];
+  line_gradient<N>(C, w, whv[1], whv[3], rg.x, gx);
+  __syncthreads();
+  // column a: W of the column, gy (faces 2 and 0)
+  double gy[3][N];
+  {
+    const double* blk = sX + tl<N, 3>(el, a, 0);
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int i = 0; i < N; ++i) w[c][i] = blk[c * N + i];
+    line_gradient<N>(C, w, whv[2], whv[0], rg.y, gy);
+  }
+  __syncthreads();  // W reads done
+  // gx rows -> column blocks of sX; gy columns -> row blocks of sY
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      sX[tl<N, 3>(el, i, c * N + a)] = gx[c][i];
+      sY[tl<N, 3>(el, i, c * N + a)] = gy[c][i];
+    }
+  // traces of the own-line components: gx on faces 1/3, gy on faces 0/2
+  double tgx1[3], tgx3[3], tgy0[3], tgy2[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    double s1 = 0.0, s3 = 0.0, s0 = 0.0, s2 = 0.0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      s1 += C.eR[i] * gx[c][i];
+      s3 += C.eL[i] * gx[c][i];
+      s2 += C.eR[i] * gy[c][i];
+      s0 += C.eL[i] * gy[c][i];
+    }
+    tgx1[c] = s1;
+    tgx3[c] = s3;
+    tgy2[c] = s2;
+    tgy0[c] = s0;
+  }
+  __syncthreads();
+  if (!live) return;
+  // rows: gy along row a -> gy traces on faces 1/3; columns: gx -> faces 0/2
+  double tgy1[2], tgy3[2], tgx0[2], tgx2[2];
+  {
+    const double* blk = sY + tl<N, 3>(el, a, 0);
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      double s1 = 0.0, s3 = 0.0;
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        const double y = blk[c * N + i];
+        s1 += C.eR[i] * y;
+        s3 += C.eL[i] * y;
+      }
+      tgy1[c] = s1;
+      tgy3[c] = s3;
+    }
+    const double* bx = sX + tl<N, 3>(el, a, 0);
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      double s0 = 0.0, s2 = 0.0;
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        const double x = bx[c * N + i];
+        s2 += C.eR[i] * x;
+        s0 += C.eL[i] * x;
+      }
+      tgx2[c] = s2;
+      tgx0[c] = s0;
+    }
+  }
+  // one-sided viscous normal fluxes (spatial.py:456-464): face 1 +fx, face 3
+  // -fx, face 2 +fy, face 0 -fy; each side's half of the face record
+  auto put = [&](int f, double* o) {
+    const bool bnd = fs.nb[f] < 0;
+    double r[4];
+    if (bnd || lk_left(fs.fl[f])) {
+      gh_left(ph, bnd, lk_tag(fs.fl[f]), Fk[f], o, r);
+      stg4_last(frec + (int64_t)fs.ri[f] * FREC, r);
+    } else {
+      gh_right(ph, o, r);
+      stg4_last(frec + (int64_t)fs.ri[f] * FREC + 4, r);
+    }
+  };
+  double o[4];
+  {
+    const double gyv[2] = {tgy1[0], tgy1[1]};
+    visc_fx_uv(uv[1][0], uv[1][1], tgx1, gyv, ph, o);
+    put(1, o);
+  }
+  {
+    const double gyv[2] = {tgy3[0], tgy3[1]};
+    visc_fx_uv(uv[3][0], uv[3][1], tgx3, gyv, ph, o);
+    o[1] = -o[1], o[2] = -o[2], o[3] = -o[3];
+    put(3, o);
+  }
+  {
+    const double gxv[2] = {tgx2[0], tgx2[1]};
+    visc_fy_uv(uv[2][0], uv[2][1], gxv, tgy2, ph, o);
+    put(2, o);
+  }
+  {
+    const double gxv[2] = {tgx0[0], tgx0[1]};
+    visc_fy_uv(uv[0][0], uv[0][1], gxv, tgy0, ph, o);
+    o[1] = -o[1], o[2] = -o[2], o[3] = -o[3];
+    put(0, o);
   }
 }
 
 // ---------------------------------------------------------------------------
 // k_rasm: point fluxes, FR divergence, fused epilogue
 
-template <int P, int KIND, bool HASX> struct AL {
+// FOLD: no Fc block -- the thread gathers its four face records and forms
+// the common flux itself (k_rfc folded in)
+template <int P, int KIND, bool HASX, bool FOLD = false> struct AL {
   using R = RC<P>;
   static constexpr bool VISC = KT<KIND>::VISC;
   static constexpr int S_ = TL<R::N, 3>::S > TL<R::N, 4>::S ? TL<R::N, 3>::S : TL<R::N, 4>::S;
   static constexpr int BUF = R::EPB * S_;
   static constexpr int WD = VISC ? R::WD : 0;
-  static constexpr int A = 2 * BUF, B = WD + R::FD + (HASX ? R::QD : 0);
+  static constexpr int FD = FOLD ? 0 : R::FD;
+  static constexpr int A = 2 * BUF, B = WD + FD + (HASX ? R::QD : 0);
   static constexpr int STAGE = A > B ? A : B;
-  static constexpr int OFF_F = R::QD + STAGE - R::FD, OFF_W = OFF_F - WD, OFF_BAR = R::QD + STAGE;
+  static constexpr int OFF_F = R::QD + STAGE - FD, OFF_W = OFF_F - WD, OFF_BAR = R::QD + STAGE;
   static constexpr size_t BYTES = sizeof(double) * (OFF_BAR + 2);
 };
 
-template <int P, int KIND, int EK, bool HASX>
+template <int P, int KIND, int EK, bool HASX, bool FOLD = false>
 __global__ void __launch_bounds__(RC<P>::TH, RC<P>::MINB)
 k_rasm(const FrConst C, const RectMesh m, const double* __restrict__ q, const double* __restrict__ X, double eps,
        const double* __restrict__ wh, const double* __restrict__ fc, const Epi ep, double* __restrict__ out,
        int* bad, Status* st) {
   using R = RC<P>;
-  using L = AL<P, KIND, HASX>;
+  using L = AL<P, KIND, HASX, FOLD>;
   constexpr int N = R::N, NP = R::NP, E = R::EPB;
   constexpr bool VISC = KT<KIND>::VISC;
   extern __shared__ __align__(128) double sm[];
@@ -754,7 +1214,11 @@ k_rasm(const FrConst C, const RectMesh m, const double* __restrict__ q, const do
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::OFF_BAR);
   const int t = threadIdx.x;
   const int el = t / N, a = t % N;
-  const int64_t e0 = (int64_t)blockIdx.x * E;
+  // FOLD chain: element blocks in descending order -- the blocks the
+  // previous kernel touched last (its q reads, its What / record writes)
+  // are the ones still in L2
+  const int64_t blk = (FOLD && PMGB_RECT_REV) ? (int64_t)gridDim.x - 1 - blockIdx.x : (int64_t)blockIdx.x;
+  const int64_t e0 = blk * E;
   const int ne = (int)((m.M - e0) < E ? (m.M - e0) : E);
   const int64_t e = e0 + el;
   const bool live = t < E * N && el < ne;
@@ -771,15 +1235,48 @@ k_rasm(const FrConst C, const RectMesh m, const double* __restrict__ q, const do
     bulk_g2s_first(sQ, q + e0 * NP * 4, qbytes, bar);
     if (HASX) bulk_g2s(sX, X + e0 * NP * 4, qbytes, bar);
   }
+#if PMGB_RECT_EPF
+  if (t == 32) epi_prefetch<EK>(ep, e0 * NP * 4, qbytes);
+#endif
   const double2 rg = live ? __ldg(m.rgeo + e) : make_double2(1.0, 1.0);
-  pdl_wait();  // What (k_rface), Fc (k_rfc), status flags
+  FaceStat fs;
+  if constexpr (FOLD) face_stat<N>(m, e, a, live, fs);
+  pdl_wait();  // What and the face records (k_rface / k_rgf; Fc: k_rfc), status flags
   if (t == 0) {
-    const uint32_t fb = (uint32_t)ne * 4 * N * 32, wb = (uint32_t)ne * 4 * N * 24;
-    mbar_expect(bar + 1, VISC ? fb + wb : fb);
-    bulk_g2s_first(sm + L::OFF_F, fc + e0 * 4 * N * 4, fb, bar + 1);
+    const uint32_t fb = FOLD ? 0u : (uint32_t)ne * 4 * N * 32, wb = (uint32_t)ne * 4 * N * 24;
+    if (VISC || !FOLD) mbar_expect(bar + 1, VISC ? fb + wb : fb);
+    if (!FOLD) bulk_g2s_first(sm + L::OFF_F, fc + e0 * 4 * N * 4, fb, bar + 1);
     if (VISC) bulk_g2s_first(sm + L::OFF_W, wh + e0 * 4 * N * 3, wb, bar + 1);
     if (blockIdx.x == 0) commit_status(bad, st);
   }
+  double fcv[4][4];
+  double rG[4][4], rH[4][4];
+  if constexpr (FOLD) {
+    // the four face records (fc here is the face-record array), gathered
+    // while the q block is in flight
+#pragma unroll
+    for (int f = 0; f < 4; ++f) {
+      const double* rec = fc + (int64_t)fs.ri[f] * FREC;
+#pragma unroll
+      for (int v = 0; v < 4; ++v) rG[f][v] = rH[f][v] = 0.0;
+      if (live) {
+        ldg4c(rec, rG[f]);
+        if constexpr (VISC)
+          if (fs.nb[f] >= 0) ldg4c(rec + 4, rH[f]);
+      }
+    }
+  }
+#if PMGB_RECT_PF > 0
+  if (t == 0 && (int64_t)(blockIdx.x + PMGB_RECT_PF) * E + E <= m.M) {
+    const int64_t en = (int64_t)(blockIdx.x + PMGB_RECT_PF) * E;
+    l2_prefetch(q + en * NP * 4, (uint32_t)E * NP * 32);
+    if (VISC) l2_prefetch(wh + en * 4 * N * 3, (uint32_t)E * 4 * N * 24);
+  }
+#endif
+  auto combine = [&]() {
+#pragma unroll
+    for (int f = 0; f < 4; ++f) gh_combine(fs.nb[f] < 0 || lk_left(fs.fl[f]), rG[f], rH[f], fcv[f]);
+  };
   mbar_wait(bar, 0);
   if constexpr (HASX) {
     form_qp<R::TH>(sQ, sX, eps, ne * NP * 4);
@@ -798,8 +1295,9 @@ k_rasm(const FrConst C, const RectMesh m, const double* __restrict__ q, const do
       w[2][i] = s.p * s.ir;
     }
   }
-  mbar_wait(bar + 1, 0);
-  double whv[4][3], fcv[4][4];
+  if constexpr (FOLD) combine();
+  if constexpr (VISC || !FOLD) mbar_wait(bar + 1, 0);
+  double whv[4][3];
 #pragma unroll
   for (int f = 0; f < 4; ++f) {
     const int fp = el * 4 * N + fpt_of<N>(f, a);
@@ -807,7 +1305,7 @@ k_rasm(const FrConst C, const RectMesh m, const double* __restrict__ q, const do
 #pragma unroll
       for (int c = 0; c < 3; ++c) whv[f][c] = sWb[fp * 3 + c];
     }
-    lds4(sFb + fp * 4, fcv[f]);
+    if constexpr (!FOLD) lds4(sFb + fp * 4, fcv[f]);
   }
   __syncthreads();  // the stage (X, What, Fc blocks) is free
   double gy[3][N];
@@ -924,30 +1422,321 @@ k_rasm(const FrConst C, const RectMesh m, const double* __restrict__ q, const do
     const int64_t pt = e * NP + i * N + a;
     double qv[4] = {0, 0, 0, 0};
     if constexpr (NEEDQ) lds4(sQ + ((el * N + i) * N + a) * 4, qv);
-    double o[4];
-    if constexpr (EK == EPI_JV) {  // out = s X - (R - R0)/eps, operands as 256-bit loads
-      double xv[4], r0[4];
-      ldg4(ep.X + pt * 4, xv);
-      ldg4(ep.R0 + pt * 4, r0);
+    double o[4], o1[4], o2[4], o3[4];
+    if constexpr (EK != EPI_R) epi_load4_k<EK>(ep, pt * 4, o1, o2, o3);   // operands as 256-bit loads
 #pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        const double Rv = -(rg.x * bx[v * N + i] + rg.y * xe[v][i]);
-        o[v] = epi_pre_k<EK>(ep, Rv, 0.0, xv[v], r0[v], 0.0);
-      }
-    } else {
-#pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        const double Rv = -(rg.x * bx[v * N + i] + rg.y * xe[v][i]);
-        if constexpr (EK == EPI_R) {
-          o[v] = Rv;
-        } else {
-          double o1, o2, o3;
-          epi_load_k<EK>(ep, pt * 4 + v, o1, o2, o3);
-          o[v] = (EK == EPI_RK) ? epi_rk(ep, ce, Rv, qv[v], o1, o2, o3) : epi_pre_k<EK>(ep, Rv, qv[v], o1, o2, o3);
-        }
-      }
+    for (int v = 0; v < 4; ++v) {
+      const double Rv = -(rg.x * bx[v * N + i] + rg.y * xe[v][i]);
+      if constexpr (EK == EPI_R)
+        o[v] = Rv;
+      else
+        o[v] = (EK == EPI_RK) ? epi_rk(ep, ce, Rv, qv[v], o1[v], o2[v], o3[v])
+                              : epi_pre_k<EK>(ep, Rv, qv[v], o1[v], o2[v], o3[v]);
     }
     stg4(out + pt * 4, o);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_rasm_p: k_rasm as a persistent, software-pipelined kernel.  A CTA walks
+// the element blocks b = blockIdx.x, blockIdx.x + gridDim.x, ...; while block
+// i is computed the TMA copies of block i+1's q (+ X) and What blocks are in
+// flight into the other stage, its four face records per thread are in
+// flight into registers, and the static face data of block i+2 is being
+// fetched -- the load phase of every block but a CTA's first overlaps the
+// arithmetic of its predecessor (the one-shot kernels spend 40-50 % of their
+// warp time waiting at the start of each CTA: T_load + T_compute instead of
+// max(T_load, T_compute)).  Two CTAs of 128 threads per SM, so a thread may
+// hold the in-flight records in registers.
+
+// the arithmetic of one block after its operands are in registers / shared
+// memory: W^T, gy, gx, point fluxes, FR divergence, fused epilogue
+template <int P, int KIND, int EK>
+__device__ __forceinline__ void rasm_body(const FrConst& C, const Phys& ph, const Epi& ep, const double* sQ,
+                                          double* sX, double* sY, double (&w)[3][P + 1],
+                                          const double (&whv)[4][3], const double (&fcv)[4][4], const double2 rg,
+                                          const int el, const int a, const int64_t e, const bool live,
+                                          double* __restrict__ out) {
+  constexpr int N = P + 1, NP = N * N;
+  constexpr bool VISC = KT<KIND>::VISC;
+  const double g = C.gamma;
+  const double* row = sQ + (el * N + a) * N * 4;
+  double gy[3][N];
+  if constexpr (VISC) {
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) sX[tl<N, 3>(el, i, c * N + a)] = w[c][i];
+    __syncthreads();
+    // column a: gy -> row blocks
+    {
+      const double* blk = sX + tl<N, 3>(el, a, 0);
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int i = 0; i < N; ++i) w[c][i] = blk[c * N + i];
+      double gc[3][N];
+      line_gradient<N>(C, w, whv[2], whv[0], rg.y, gc);
+#pragma unroll
+      for (int i = 0; i < N; ++i)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) sY[tl<N, 3>(el, i, c * N + a)] = gc[c][i];
+    }
+    __syncthreads();
+    const double* blk = sY + tl<N, 3>(el, a, 0);
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int i = 0; i < N; ++i) gy[c][i] = blk[c * N + i];
+  }
+  // row a: primitives (again: cheaper than holding them through the column
+  // pass), gx, point fluxes -- fx stays in registers, fy -> column blocks
+  double qr[4][N];
+  Pr pr[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    double x[4];
+    lds4(row + 4 * i, x);
+#pragma unroll
+    for (int v = 0; v < 4; ++v) qr[v][i] = x[v];
+    pr[i] = prim_of(x, g);
+  }
+  double gx[3][N];
+  if constexpr (VISC) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      w[0][i] = pr[i].u;
+      w[1][i] = pr[i].v;
+      w[2][i] = pr[i].p * pr[i].ir;
+    }
+    line_gradient<N>(C, w, whv[1], whv[3], rg.x, gx);
+  }
+  double fx[4][N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    const Pr& s = pr[i];
+    double Fx[4], Fy[4];
+    Fx[0] = qr[1][i];
+    Fx[1] = qr[1][i] * s.u + s.p;
+    Fx[2] = qr[1][i] * s.v;
+    Fx[3] = s.u * (qr[3][i] + s.p);
+    Fy[0] = qr[2][i];
+    Fy[1] = qr[2][i] * s.u;
+    Fy[2] = qr[2][i] * s.v + s.p;
+    Fy[3] = s.v * (qr[3][i] + s.p);
+    if constexpr (VISC) {
+      const double gxx[3] = {gx[0][i], gx[1][i], gx[2][i]};
+      const double gyy[3] = {gy[0][i], gy[1][i], gy[2][i]};
+      const double d = gxx[0] + gyy[1];
+      const double txx = ph.mu * (2.0 * gxx[0] - (2.0 / 3.0) * d);
+      const double tyy = ph.mu * (2.0 * gyy[1] - (2.0 / 3.0) * d);
+      const double txy = ph.mu * (gyy[0] + gxx[1]);
+      Fx[1] = Fx[1] - txx;
+      Fx[2] = Fx[2] - txy;
+      Fx[3] = Fx[3] - (s.u * txx + s.v * txy + ph.kappa * gxx[2]);
+      Fy[1] = Fy[1] - txy;
+      Fy[2] = Fy[2] - tyy;
+      Fy[3] = Fy[3] - (s.u * txy + s.v * tyy + ph.kappa * gyy[2]);
+      Fx[0] = Fx[0] - 0.0;
+      Fy[0] = Fy[0] - 0.0;
+    }
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      fx[v][i] = Fx[v];
+      sX[tl<N, 4>(el, i, v * N + a)] = Fy[v];
+    }
+  }
+  // X_xi along row a
+  double xx[4][N];
+  line_div<N>(C, fx, fcv[1], fcv[3], xx);
+  if constexpr (VISC) __syncthreads();  // gy row reads of sY done
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) sY[tl<N, 4>(el, i, v * N + a)] = xx[v][i];
+  __syncthreads();
+  if (live) {
+  // column a: fy and X_xi of the column, faces 2 / 0, X_eta, R, epilogue
+  double fyc[4][N];
+  {
+    const double* blk = sX + tl<N, 4>(el, a, 0);
+#pragma unroll
+    for (int v = 0; v < 4; ++v)
+#pragma unroll
+      for (int i = 0; i < N; ++i) fyc[v][i] = blk[v * N + i];
+  }
+  double xe[4][N];
+  line_div<N>(C, fyc, fcv[2], fcv[0], xe);
+  const double* bx = sY + tl<N, 4>(el, a, 0);
+  constexpr bool NEEDQ = !(EK == EPI_R || EK == EPI_JV || EK == EPI_NEG_R);
+  const double ce = (EK == EPI_RK) ? epi_rk_coef(ep, e) : 0.0;
+#pragma unroll
+  for (int i = 0; i < N; ++i) {   // point (i, a)
+    const int64_t pt = e * NP + i * N + a;
+    double qv[4] = {0, 0, 0, 0};
+    if constexpr (NEEDQ) lds4(sQ + ((el * N + i) * N + a) * 4, qv);
+    double o[4], o1[4], o2[4], o3[4];
+    if constexpr (EK != EPI_R) epi_load4_k<EK>(ep, pt * 4, o1, o2, o3);   // operands as 256-bit loads
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const double Rv = -(rg.x * bx[v * N + i] + rg.y * xe[v][i]);
+      if constexpr (EK == EPI_R)
+        o[v] = Rv;
+      else
+        o[v] = (EK == EPI_RK) ? epi_rk(ep, ce, Rv, qv[v], o1[v], o2[v], o3[v])
+                              : epi_pre_k<EK>(ep, Rv, qv[v], o1[v], o2[v], o3[v]);
+    }
+    stg4(out + pt * 4, o);
+  }
+  }
+}
+
+template <int P, int KIND, bool HASX> struct PL {
+  using R = RC<P>;
+  static constexpr bool VISC = KT<KIND>::VISC;
+  static constexpr int S_ = TL<R::N, 3>::S > TL<R::N, 4>::S ? TL<R::N, 3>::S : TL<R::N, 4>::S;
+  static constexpr int BUF = R::EPB * S_;
+  static constexpr int OFF_Q1 = R::QD, OFF_XQ = 2 * R::QD, OFF_W = OFF_XQ + (HASX ? R::QD : 0);
+  static constexpr int OFF_X = OFF_W + (VISC ? R::WD : 0), OFF_Y = OFF_X + BUF, OFF_BAR = OFF_Y + BUF;
+  static constexpr size_t BYTES = sizeof(double) * (OFF_BAR + 2);
+};
+
+template <int P, int KIND, int EK, bool HASX>
+__global__ void __launch_bounds__(RC<P>::TH, 2)
+k_rasm_p(const FrConst C, const RectMesh m, const double* __restrict__ q, const double* __restrict__ X, double eps,
+         const double* __restrict__ wh, const double* __restrict__ frec, const Epi ep, double* __restrict__ out,
+         int* bad, Status* st, int nblk) {
+  using R = RC<P>;
+  using L = PL<P, KIND, HASX>;
+  constexpr int N = R::N, NP = R::NP, E = R::EPB;
+  constexpr bool VISC = KT<KIND>::VISC;
+  extern __shared__ __align__(128) double sm[];
+  double* sXq = sm + L::OFF_XQ;
+  const double* sWb = sm + L::OFF_W;
+  double* sX = sm + L::OFF_X;
+  double* sY = sm + L::OFF_Y;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::OFF_BAR);
+  const int t = threadIdx.x;
+  const int el = t / N, a = t % N;
+  const bool inr = t < E * N;
+  const Phys ph = phys_of(C);
+  const double g = C.gamma;
+  if (t == 0) {
+    mbar_init(bar);
+    mbar_init(bar + 1);
+  }
+  __syncthreads();
+  // thread 0: the TMA copies of block blk into stage s
+  auto issue = [&](int blk, int s) {
+    const int64_t e0 = (int64_t)blk * E;
+    const int ne = (int)((m.M - e0) < E ? (m.M - e0) : E);
+    const uint32_t qb = (uint32_t)ne * NP * 32, wb = (uint32_t)ne * 4 * N * 24;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect(bar + s, (HASX ? 2 * qb : qb) + (VISC ? wb : 0u));
+    bulk_g2s(sm + s * R::QD, q + e0 * NP * 4, qb, bar + s);
+    if (HASX) bulk_g2s(sXq, X + e0 * NP * 4, qb, bar + s);
+    if (VISC) bulk_g2s(sm + L::OFF_W, wh + e0 * 4 * N * 3, wb, bar + s);
+  };
+  auto live_of = [&](int blk) { return inr && blk < nblk && (int64_t)blk * E + el < m.M; };
+  // the thread's four face records of a block (static data fs)
+  auto fetch = [&](const FaceStat& fs, bool lv, double (&rG)[4][4], double (&rH)[4][4]) {
+#pragma unroll
+    for (int f = 0; f < 4; ++f) {
+      const double* rec = frec + (int64_t)fs.ri[f] * FREC;
+#pragma unroll
+      for (int v = 0; v < 4; ++v) rG[f][v] = rH[f][v] = 0.0;
+      if (lv) {
+        ldg4c(rec, rG[f]);
+        if constexpr (VISC)
+          if (fs.nb[f] >= 0) ldg4c(rec + 4, rH[f]);
+      }
+    }
+  };
+  int b = blockIdx.x;
+  const int G = gridDim.x;
+  // static data of the first two blocks (no dependence on the predecessor)
+  FaceStat fs0, fs1;
+  face_stat<N>(m, (int64_t)b * E + el, a, live_of(b), fs0);
+  face_stat<N>(m, (int64_t)(b + G) * E + el, a, live_of(b + G), fs1);
+  double2 rg0 = live_of(b) ? __ldg(m.rgeo + (int64_t)b * E + el) : make_double2(1.0, 1.0);
+  double2 rg1 = live_of(b + G) ? __ldg(m.rgeo + (int64_t)(b + G) * E + el) : make_double2(1.0, 1.0);
+  pdl_wait();  // What and the face records (k_rgf / k_rface), status flags
+  if (t == 0) {
+    if (b < nblk) issue(b, 0);
+    if (blockIdx.x == 0) commit_status(bad, st);
+  }
+  double rG[4][4], rH[4][4];
+  fetch(fs0, live_of(b), rG, rH);
+  for (int it = 0; b < nblk; b += G, ++it) {
+    const int s = it & 1;
+    const double* sQ = sm + s * R::QD;
+    const int64_t e = (int64_t)b * E + el;
+    const bool live = live_of(b);
+    const double2 rg = rg0;
+    // this block's common fluxes; then the next block's records and the
+    // static data of the block after it take their place in flight
+    double fcv[4][4];
+#pragma unroll
+    for (int f = 0; f < 4; ++f) gh_combine(fs0.nb[f] < 0 || lk_left(fs0.fl[f]), rG[f], rH[f], fcv[f]);
+    fs0 = fs1;
+    rg0 = rg1;
+    fetch(fs0, live_of(b + G), rG, rH);
+    face_stat<N>(m, (int64_t)(b + 2 * G) * E + el, a, live_of(b + 2 * G), fs1);
+    rg1 = live_of(b + 2 * G) ? __ldg(m.rgeo + (int64_t)(b + 2 * G) * E + el) : make_double2(1.0, 1.0);
+    mbar_wait(bar + s, (it >> 1) & 1);
+    if constexpr (HASX) {
+      const int64_t e0 = (int64_t)b * E;
+      const int ne = (int)((m.M - e0) < E ? (m.M - e0) : E);
+      form_qp<R::TH>(const_cast<double*>(sQ), sXq, eps, ne * NP * 4);
+      __syncthreads();
+    }
+    const double* row = sQ + (el * N + a) * N * 4;
+    double w[3][N];
+    if constexpr (VISC) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        double x[4];
+        lds4(row + 4 * i, x);
+        const Pr sp = prim_of(x, g);
+        w[0][i] = sp.u;
+        w[1][i] = sp.v;
+        w[2][i] = sp.p * sp.ir;
+      }
+    }
+    double whv[4][3];
+    if constexpr (VISC) {
+#pragma unroll
+      for (int f = 0; f < 4; ++f)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) whv[f][c] = sWb[(el * 4 * N + fpt_of<N>(f, a)) * 3 + c];
+    }
+    __syncthreads();  // every thread is past the previous block; the What / X stages are consumed
+    if (t == 0 && b + G < nblk) issue(b + G, s ^ 1);
+    rasm_body<P, KIND, EK>(C, ph, ep, sQ, sX, sY, w, whv, fcv, rg, el, a, e, live, out);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_form: qp = q + eps X once per evaluation (the reference's rounding,
+// newton_krylov.py:76 -- the same two roundings as form_qp / ld_q), so the
+// chain's kernels run their X-free instances on qp: the neighbour gathers
+// and the staged blocks read one array instead of two.
+
+__global__ void __launch_bounds__(256) k_form(const double* __restrict__ q, const double* __restrict__ X, double eps,
+                                              double* __restrict__ qp, int64_t n4, int64_t n) {
+  pdl_trigger();
+  const int64_t stride = (int64_t)gridDim.x * 256;
+  for (int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x; i < n4; i += stride) {
+    double a[4], x[4];
+    ldg4(q + 4 * i, a);
+    ldg4(X + 4 * i, x);
+#pragma unroll
+    for (int v = 0; v < 4; ++v) a[v] = __dadd_rn(a[v], __dmul_rn(eps, x[v]));
+    stg4(qp + 4 * i, a);
+  }
+  if (blockIdx.x == 0 && threadIdx.x < (n & 3)) {   // scalar kinds never come here; kept for safety
+    const int64_t i = 4 * n4 + threadIdx.x;
+    qp[i] = __dadd_rn(q[i], __dmul_rn(eps, X[i]));
   }
 }
 
@@ -973,28 +1762,83 @@ static void launch_pdl_r(void (*kernel)(KArgs...), unsigned grid, int threads, s
 using RasmFn = void (*)(const FrConst, const RectMesh, const double*, const double*, double, const double*,
                         const double*, const Epi, double*, int*, Status*);
 
-template <int P, int KIND, bool HASX>
+template <int P, int KIND, bool HASX, bool FOLD>
 static RasmFn rasm_for(int mode) {
   switch (mode) {
-    case EPI_R: return k_rasm<P, KIND, EPI_R, HASX>;
-    case EPI_JV: return k_rasm<P, KIND, EPI_JV, HASX>;
-    case EPI_STAGE_JV: return k_rasm<P, KIND, EPI_STAGE_JV, HASX>;
-    case EPI_DEFECT: return k_rasm<P, KIND, EPI_DEFECT, HASX>;
-    case EPI_F: return k_rasm<P, KIND, EPI_F, HASX>;
-    case EPI_RK: return k_rasm<P, KIND, EPI_RK, HASX>;
+    case EPI_R: return k_rasm<P, KIND, EPI_R, HASX, FOLD>;
+    case EPI_JV: return k_rasm<P, KIND, EPI_JV, HASX, FOLD>;
+    case EPI_STAGE_JV: return k_rasm<P, KIND, EPI_STAGE_JV, HASX, FOLD>;
+    case EPI_DEFECT: return k_rasm<P, KIND, EPI_DEFECT, HASX, FOLD>;
+    case EPI_F: return k_rasm<P, KIND, EPI_F, HASX, FOLD>;
+    case EPI_RK: return k_rasm<P, KIND, EPI_RK, HASX, FOLD>;
   }
-  return k_rasm<P, KIND, -1, HASX>;
+  return k_rasm<P, KIND, -1, HASX, FOLD>;
+}
+
+using RasmPFn = void (*)(const FrConst, const RectMesh, const double*, const double*, double, const double*,
+                         const double*, const Epi, double*, int*, Status*, int);
+template <int P, int KIND, bool HASX>
+static RasmPFn rasm_p_for(int mode) {
+  switch (mode) {
+    case EPI_R: return k_rasm_p<P, KIND, EPI_R, HASX>;
+    case EPI_JV: return k_rasm_p<P, KIND, EPI_JV, HASX>;
+    case EPI_STAGE_JV: return k_rasm_p<P, KIND, EPI_STAGE_JV, HASX>;
+    case EPI_DEFECT: return k_rasm_p<P, KIND, EPI_DEFECT, HASX>;
+    case EPI_F: return k_rasm_p<P, KIND, EPI_F, HASX>;
+    case EPI_RK: return k_rasm_p<P, KIND, EPI_RK, HASX>;
+  }
+  return k_rasm_p<P, KIND, -1, HASX>;
+}
+
+static int sm_count() {
+  static int n[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (n[dev & 63] == 0) cudaDeviceGetAttribute(&n[dev & 63], cudaDevAttrMultiProcessorCount, dev);
+  return n[dev & 63];
+}
+
+// PMGB_RECT_PREFORM=1: a k_form pass and the chain's X-free instances on qp
+// instead of forming q + eps X in every kernel.  Measured even at config 2
+// (Jv 168.9 vs 167.4 us) and slower at config 5 (4.00 vs 3.75 ms,
+// profiles/r2/negative/ab_preform_r2n.log): off unless asked for.
+static bool rect_preform() {
+  static const bool on = [] {
+    const char* env = std::getenv("PMGB_RECT_PREFORM");
+    return env != nullptr && env[0] == '1';
+  }();
+  return on;
 }
 
 template <int P, int KIND, bool HASX>
 static void set_rect_attrs() {
   for (int md : {(int)EPI_R, (int)EPI_JV, (int)EPI_STAGE_JV, (int)EPI_DEFECT, (int)EPI_F, (int)EPI_RK, -1})
-    cudaFuncSetAttribute(rasm_for<P, KIND, HASX>(md), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)AL<P, KIND, HASX>::BYTES);
-  if constexpr (KT<KIND>::VISC)
+    cudaFuncSetAttribute(rasm_p_for<P, KIND, HASX>(md), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)PL<P, KIND, HASX>::BYTES);
+  for (int md : {(int)EPI_R, (int)EPI_JV, (int)EPI_STAGE_JV, (int)EPI_DEFECT, (int)EPI_F, (int)EPI_RK, -1}) {
+    cudaFuncSetAttribute(rasm_for<P, KIND, HASX, false>(md), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)AL<P, KIND, HASX, false>::BYTES);
+    cudaFuncSetAttribute(rasm_for<P, KIND, HASX, true>(md), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)AL<P, KIND, HASX, true>::BYTES);
+  }
+  if constexpr (KT<KIND>::VISC) {
     cudaFuncSetAttribute(k_rgrad<P, HASX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GL<P, HASX>::BYTES);
+    cudaFuncSetAttribute(k_rgf<P, KIND, HASX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)GFL<P, HASX>::BYTES);
+  }
 }
 
+// d.has_rect: 3 the two-kernel chain k_rgf / k_rface + the one-shot k_rasm
+// (common flux folded in), 4 the same with the persistent k_rasm_p, 1 the
+// faster of the two at this degree (PERSIST below: measured on the B200,
+// profiles/r2/ab_chain_r2m.jsonl), 2 the four-kernel chain they replaced
+// (kept for A/B and as a cross-check)
+#ifndef PMGB_RECT_PDL0   // measured: config-2 R 113.0 -> 110.7 us, config 3 34.1 -> 32.0 us
+#define PMGB_RECT_PDL0 1
+#endif
+#ifndef PMGB_RECT_PERSIST_MAXP
+#define PMGB_RECT_PERSIST_MAXP 0
+#endif
 template <int P, int KIND>
 static int run_rect(const RectDev& rd, const DiscDev& d, const double* q, const double* X, double eps,
                     const Epi& epi, double* out, int* bad, Status* stp, cudaStream_t st) {
@@ -1007,22 +1851,82 @@ static int run_rect(const RectDev& rd, const DiscDev& d, const double* q, const 
   const RectMesh m{d.M, rd.nface, rd.faces, rd.fslot, d.link, rd.rgeo, d.geom};
   const unsigned gf = (unsigned)((rd.nface * (P + 1) + 127) / 128);
   const unsigned ge = (unsigned)((d.M + R::EPB - 1) / R::EPB);
-  const bool hx = X != nullptr;
-  if (hx)
-    k_rface<P, KIND, true><<<gf, 128, 0, st>>>(d.C, m, q, X, eps, rd.frec, rd.wh, bad);
-  else
-    k_rface<P, KIND, false><<<gf, 128, 0, st>>>(d.C, m, q, X, eps, rd.frec, rd.wh, bad);
-  if constexpr (KT<KIND>::VISC) {
-    if (hx)
-      launch_pdl_r(k_rgrad<P, true>, ge, R::TH, GL<P, true>::BYTES, st, d.C, m, q, X, eps,
-                   (const double*)rd.wh, rd.frec, bad);
+  bool hx = X != nullptr;
+  const bool fold = d.has_rect != 2;
+  if (fold && hx && d.qp != nullptr && rect_preform()) {
+    // evaluate at qp = q + eps X formed once; the epilogues still read X
+    const int64_t n = d.M * R::NP * 4;
+    const int64_t nb = (n / 4 + 255) / 256, cap = 16 * (int64_t)sm_count();
+    k_form<<<(unsigned)(nb < cap ? nb : cap), 256, 0, st>>>(q, X, eps, d.qp, n / 4, n);
+    q = d.qp;
+    hx = false;
+    if constexpr (KT<KIND>::VISC)
+      launch_pdl_r(k_rgf<P, KIND, false>, ge, R::TH, GFL<P, false>::BYTES, st, d.C, m, q, (const double*)nullptr,
+                   eps, rd.wh, rd.frec, bad);
     else
-      launch_pdl_r(k_rgrad<P, false>, ge, R::TH, GL<P, false>::BYTES, st, d.C, m, q, X, eps,
-                   (const double*)rd.wh, rd.frec, bad);
+      launch_pdl_r(k_rface<P, KIND, false, FREC>, gf, 128, 0, st, d.C, m, q, (const double*)nullptr, eps, rd.frec,
+                   rd.wh, bad);
+    X = nullptr;
+  } else if (fold && KT<KIND>::VISC) {
+    if constexpr (KT<KIND>::VISC) {
+#if PMGB_RECT_PDL0   // the chain's first kernel may start while its stream predecessor drains
+      if (hx)
+        launch_pdl_r(k_rgf<P, KIND, true>, ge, R::TH, GFL<P, true>::BYTES, st, d.C, m, q, X, eps, rd.wh, rd.frec,
+                     bad);
+      else
+        launch_pdl_r(k_rgf<P, KIND, false>, ge, R::TH, GFL<P, false>::BYTES, st, d.C, m, q, X, eps, rd.wh,
+                     rd.frec, bad);
+#else
+      if (hx)
+        k_rgf<P, KIND, true><<<ge, R::TH, GFL<P, true>::BYTES, st>>>(d.C, m, q, X, eps, rd.wh, rd.frec, bad);
+      else
+        k_rgf<P, KIND, false><<<ge, R::TH, GFL<P, false>::BYTES, st>>>(d.C, m, q, X, eps, rd.wh, rd.frec, bad);
+#endif
+    }
+  } else if (fold) {   // Euler kinds: F itself is the record's G
+#if PMGB_RECT_PDL0
+    if (hx)
+      launch_pdl_r(k_rface<P, KIND, true, FREC>, gf, 128, 0, st, d.C, m, q, X, eps, rd.frec, rd.wh, bad);
+    else
+      launch_pdl_r(k_rface<P, KIND, false, FREC>, gf, 128, 0, st, d.C, m, q, X, eps, rd.frec, rd.wh, bad);
+#else
+    if (hx)
+      k_rface<P, KIND, true, FREC><<<gf, 128, 0, st>>>(d.C, m, q, X, eps, rd.frec, rd.wh, bad);
+    else
+      k_rface<P, KIND, false, FREC><<<gf, 128, 0, st>>>(d.C, m, q, X, eps, rd.frec, rd.wh, bad);
+#endif
+  } else {
+    if (hx)
+      k_rface<P, KIND, true><<<gf, 128, 0, st>>>(d.C, m, q, X, eps, rd.frec, rd.wh, bad);
+    else
+      k_rface<P, KIND, false><<<gf, 128, 0, st>>>(d.C, m, q, X, eps, rd.frec, rd.wh, bad);
+    if constexpr (KT<KIND>::VISC) {
+      if (hx)
+        launch_pdl_r(k_rgrad<P, true>, ge, R::TH, GL<P, true>::BYTES, st, d.C, m, q, X, eps,
+                     (const double*)rd.wh, rd.frec, bad);
+      else
+        launch_pdl_r(k_rgrad<P, false>, ge, R::TH, GL<P, false>::BYTES, st, d.C, m, q, X, eps,
+                     (const double*)rd.wh, rd.frec, bad);
+    }
+  }
+  if (d.has_rect == 4 || (d.has_rect == 1 && P <= PMGB_RECT_PERSIST_MAXP)) {
+    RasmPFn fn = hx ? rasm_p_for<P, KIND, true>(epi.mode) : rasm_p_for<P, KIND, false>(epi.mode);
+    const size_t smem = hx ? PL<P, KIND, true>::BYTES : PL<P, KIND, false>::BYTES;
+    const unsigned gp = ge < 2u * (unsigned)sm_count() ? ge : 2u * (unsigned)sm_count();
+    launch_pdl_r(fn, gp, R::TH, smem, st, d.C, m, q, X, eps, (const double*)rd.wh, (const double*)rd.frec, epi,
+                 out, bad, stp, (int)ge);
+    return (int)cudaGetLastError();
+  }
+  if (fold) {
+    RasmFn fn = hx ? rasm_for<P, KIND, true, true>(epi.mode) : rasm_for<P, KIND, false, true>(epi.mode);
+    const size_t smem = hx ? AL<P, KIND, true, true>::BYTES : AL<P, KIND, false, true>::BYTES;
+    launch_pdl_r(fn, ge, R::TH, smem, st, d.C, m, q, X, eps, (const double*)rd.wh, (const double*)rd.frec, epi,
+                 out, bad, stp);
+    return (int)cudaGetLastError();
   }
   launch_pdl_r(k_rfc<P, KIND>, gf, 128, 0, st, d.C, m, (const double*)rd.frec, rd.fc);
-  RasmFn fn = hx ? rasm_for<P, KIND, true>(epi.mode) : rasm_for<P, KIND, false>(epi.mode);
-  const size_t smem = hx ? AL<P, KIND, true>::BYTES : AL<P, KIND, false>::BYTES;
+  RasmFn fn = hx ? rasm_for<P, KIND, true, false>(epi.mode) : rasm_for<P, KIND, false, false>(epi.mode);
+  const size_t smem = hx ? AL<P, KIND, true, false>::BYTES : AL<P, KIND, false, false>::BYTES;
   launch_pdl_r(fn, ge, R::TH, smem, st, d.C, m, q, X, eps, (const double*)rd.wh, (const double*)rd.fc, epi, out,
                bad, stp);
   return (int)cudaGetLastError();
@@ -1030,6 +1934,13 @@ static int run_rect(const RectDev& rd, const DiscDev& d, const double* q, const 
 
 int launch_residual_rect(const RectDev& rd, const DiscDev& d, const double* q, const double* X, double eps,
                          const Epi& epi, double* out, int* bad, Status* stp, cudaStream_t st) {
+#ifdef PMGB_RECT_DEV   // experiment builds (tools/build_variant.sh): the config-2 / config-4 instances only
+  switch (d.kind * 8 + d.p) {
+    case K_NS * 8 + 3: return run_rect<3, K_NS>(rd, d, q, X, eps, epi, out, bad, stp, st);
+    case K_NS * 8 + 4: return run_rect<4, K_NS>(rd, d, q, X, eps, epi, out, bad, stp, st);
+  }
+  return -1000;
+#else
   switch (d.kind * 8 + d.p) {
     case K_EULER * 8 + 1: return run_rect<1, K_EULER>(rd, d, q, X, eps, epi, out, bad, stp, st);
     case K_EULER * 8 + 2: return run_rect<2, K_EULER>(rd, d, q, X, eps, epi, out, bad, stp, st);
@@ -1043,6 +1954,12 @@ int launch_residual_rect(const RectDev& rd, const DiscDev& d, const double* q, c
     case K_NS * 8 + 5: return run_rect<5, K_NS>(rd, d, q, X, eps, epi, out, bad, stp, st);
   }
   return -1000;
+#endif
+}
+
+int rect_launches(const DiscDev& d, bool has_x) {
+  if (d.has_rect == 2) return d.kind == K_NS ? 4 : 3;
+  return 2 + ((has_x && d.qp != nullptr && rect_preform()) ? 1 : 0);
 }
 
 bool rect_supported(int p, int kind) { return p >= 1 && p <= 5 && (kind == K_EULER || kind == K_NS); }

@@ -177,6 +177,7 @@ int launch_residual(const DiscDev& d, const double* q, const double* X, double e
 int launch_residual_rect(const RectDev& rd, const DiscDev& d, const double* q, const double* X, double eps,
                          const Epi& epi, double* out, int* bad, Status* stp, cudaStream_t st);
 bool rect_supported(int p, int kind);
+int rect_launches(const DiscDev& d, bool has_x);  // kernels one evaluation launches on the rectangle path
 size_t fr_grad_scratch_doubles(int p, int kind, int64_t M);
 int launch_rk_lambda(const DiscDev& d, const double* q, double adv, double* lam, cudaStream_t st);
 int launch_freeze(const DiscDev& d, const double* q, double* qtr, double* fvn, cudaStream_t st);

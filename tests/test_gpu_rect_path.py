@@ -149,3 +149,38 @@ def test_rect_config2_matches_general_full_size(cuda):
     r, g = _both(d, lambda: d.residual(q))
     assert _rel(r, g) <= 2e-9  # both within the reference's own floor of the truth (1.2e-9)
     assert torch.equal(r, d.residual(q)), "bitwise determinism"
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("kind", ["euler", "navier-stokes"])
+def test_chain_variants_agree(cuda, p, kind):
+    """The three rectangle chains -- k_rgf + persistent k_rasm_p ("rect2p"), k_rgf
+    + one-shot k_rasm ("rect2"), k_rface + k_rgrad + k_rfc + k_rasm ("rect4")
+    -- evaluate the same formulas: "rect2p" and "rect2" bit for bit (same
+    arithmetic, different scheduling), both within rounding of "rect4" (the
+    common flux is summed per side, (F - fl/2) + fr/2), on walled channels
+    (every boundary branch), Rusanov / LDG, for R and the fused Jv; more
+    blocks than resident CTAs so the persistent loop wraps."""
+    yn = np.array([0.0, 0.03, 0.1, 0.3, 0.6, 1.0])
+    nx = 210 if p == 4 else 23
+    for m, opts in ((mm.generate_channel(nx, 5, 2.0, yn, bottom="wall-isothermal", top="wall-adiabatic"), {}),
+                    (mm.generate_channel(7, 5, 2.0, yn, bottom="far-field", top="wall-slip"), {}),
+                    (mm.generate_box(9, 7, 2.0, 1.5, periodic=True),
+                     {"riemann": "rusanov", "viscous_scheme": "ldg"})):
+        eqn = EquationSpec(kind=kind, mach=0.3, reynolds=150.0, **opts)
+        d = Discretization(m, p, eqn)
+        n = d.n_dofs
+        o = OracleDisc(m, p, eqn)
+        q = torch.as_tensor(o.free_stream_field() * (1 + 0.03 * np.random.default_rng(p).standard_normal(n)),
+                            device="cuda")
+        X = torch.randn(n, dtype=torch.float64, device="cuda", generator=torch.Generator("cuda").manual_seed(p))
+        out = {}
+        for path in ("rect2p", "rect2", "rect4", "rect"):
+            assert d.residual_path(path) == path
+            out[path] = (d.residual(q), d.eval(q, _lib.EPI_JV, X=X, eps=1e-6, s=1.5, R0=X),
+                         d.eval(q, _lib.EPI_DEFECT, s=2.0, Sb=X, Se=0.25))
+        for a, b, c in zip(out["rect2p"], out["rect2"], out["rect"]):
+            assert torch.equal(a, b) and torch.equal(a, c)
+        assert _rel(out["rect2"][0], out["rect4"][0]) <= 1e-13
+        assert _rel(out["rect2"][1], out["rect4"][1]) <= 1e-8   # rounding / eps
+        assert _rel(out["rect2"][2], out["rect4"][2]) <= 1e-13

@@ -1,6 +1,6 @@
 # durations / DRAM bytes of one rect R chain + one Jv chain at a config (ncu, serialised)
 mkdir -p gpurun_out
-ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,smsp__inst_executed.sum,sm__warps_active.avg.pct_of_peak_sustained_active --clock-control none -k regex:"k_r(face|grad|asm|fc)" -c 24 --csv python tools/time_residual.py ${1:-2} 2 > gpurun_out/ncu_rect_dur.csv 2>/dev/null
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,smsp__inst_executed.sum,sm__warps_active.avg.pct_of_peak_sustained_active --clock-control none -k regex:"k_r(face|grad|asm|fc|gf)" -c 24 --csv python tools/time_residual.py ${1:-2} 2 > gpurun_out/ncu_rect_dur.csv 2>/dev/null
 python - <<'PY'
 import csv
 from collections import defaultdict

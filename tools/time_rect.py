@@ -4,7 +4,12 @@ kernels (csrc/fr_kernels.cu).  CUDA-event times over rotating buffers
 (>= 4x L2), R and fused Jv, plus the max relative difference of the two
 paths' R.
 
-    python tools/time_rect.py [configs...]      (default: 2 4)
+    python tools/time_rect.py [configs...]      (default: 2 4; "2:p2" = config 2's mesh at degree 2)
+
+"rect2" is the two-kernel chain with the one-shot second kernel (k_rgf +
+k_rasm), "rect2p" the same with the persistent k_rasm_p, "rect" the default
+(the faster of the two per degree), "rect4" the four-kernel chain they
+replaced (k_rface + k_rgrad + k_rfc + k_rasm).  RECT_PATHS selects.
 """
 
 import json
@@ -31,11 +36,21 @@ def ev(fn, reps):
     return e0.elapsed_time(e1) * 1e-3 / reps
 
 
+import os
+PATHS = tuple(os.environ.get("RECT_PATHS", "rect,rect2,rect2p,rect4,general").split(","))
+
+
 def main():
-    ks = [int(a) for a in sys.argv[1:]] or [2, 4]
-    for k in ks:
+    ks = sys.argv[1:] or ["2", "4"]
+    for arg in ks:
+        k, _, pov = arg.partition(":p")
+        k = int(k)
         c = cases.config(k)
-        d = Discretization(c.mesh, c.p, c.eqn)
+        p = int(pov) if pov else c.p
+        d = Discretization(c.mesh, p, c.eqn)
+        if p != c.p:   # the same mesh and physics at another degree (a pMG level): perturbed free stream
+            fs = d.free_stream_field().data.cpu().numpy().reshape(-1)
+            c.q0 = fs * (1.0 + 0.01 * np.random.default_rng(0).standard_normal(fs.size))
         n = d.n_dofs
         nb = max(2, int(np.ceil(4 * 126e6 / (32.0 * n))))
         q0 = torch.as_tensor(c.q0, device="cuda")
@@ -44,9 +59,9 @@ def main():
         X = torch.randn(n, dtype=torch.float64, device="cuda", generator=torch.Generator("cuda").manual_seed(7))
         R0 = d.residual(q0)
         reps = 10 if n > 1e8 else 100
-        rec = {"config": k, "n_dofs": n, "p": c.p}
+        rec = {"config": k, "n_dofs": n, "p": p}
         outs = {}
-        for path in ("rect", "general"):
+        for path in PATHS:
             d.residual_path(path)
             r = lambda i: d.eval(qs[i % nb], _lib.EPI_R, Rs[i % nb])  # noqa: E731
             j = lambda i: d.eval(qs[i % nb], _lib.EPI_JV, Rs[i % nb], X=X, eps=1e-6, s=3.7, R0=R0)  # noqa: E731
@@ -56,9 +71,15 @@ def main():
             tr, tj = ev(r, reps), ev(j, reps)
             outs[path] = d.residual(q0).cpu().numpy()
             rec[path] = {"r_us": tr * 1e6, "r_gdofs": n / tr / 1e9, "jv_us": tj * 1e6, "jv_gdofs": n / tj / 1e9}
-        a, b = outs["rect"], outs["general"]
-        rec["rect_vs_general"] = float(np.max(np.abs(a - b)) / np.max(np.abs(b)))
-        rec["speedup_r"] = rec["general"]["r_us"] / rec["rect"]["r_us"]
+        if "general" in outs:
+            a, b = outs["rect"], outs["general"]
+            rec["rect_vs_general"] = float(np.max(np.abs(a - b)) / np.max(np.abs(b)))
+            rec["speedup_r"] = rec["general"]["r_us"] / rec["rect"]["r_us"]
+        first = outs[PATHS[0]]
+        if "rect4" in outs:
+            rec[f"{PATHS[0]}_vs_rect4"] = float(np.max(np.abs(first - outs["rect4"])) / np.max(np.abs(outs["rect4"])))
+        if "rect2p" in outs and "rect2" in outs:
+            rec["rect2_bitwise_rect2p"] = bool(np.array_equal(outs["rect2"], outs["rect2p"]))
         print(json.dumps(rec), flush=True)
         del d, qs, Rs
         torch.cuda.empty_cache()
