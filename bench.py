@@ -406,7 +406,7 @@ def run_ours(args):
     achieved = flops / (t_r / K) / 1e12
     flops_jv = (FLOP_PER_DOF_R[case.p] + 4.0) * n
     achieved_jv = flops_jv / (t_jv / K) / 1e12
-    kern = ("R(u): k_rface + k_rgrad + k_rfc + k_rasm (csrc/fr_rect.cu)" if path == "rect"
+    kern = ("R(u): k_rgf + k_rasm (csrc/fr_rect.cu)" if path == "rect"
             else "R(u): k_trace_lines + k_fvn + k_assemble_async (csrc/fr_kernels.cu)")
     cfg = dict(workload(case, args.config), l2="4 rotating q/R buffer pairs (419 MB > 126 MB L2)",
                parallelism=parallelism, residual_path=path)

@@ -425,10 +425,9 @@ PMGB_API int pmgb_mdisc_element_residual(pmgb_mdisc* h, int32_t p, const int64_t
 
 PMGB_API int pmgb_disc_residual_path(pmgb_disc* h, int32_t want) {
   if (!h) return -1;
-  // 0 general, 1 rectangle kernels (the two-kernel chain, its second kernel chosen
-  // per degree), 2 the four-kernel chain, 3 the two-kernel chain with the one-shot
-  // k_rasm, 4 with the persistent k_rasm_p (2-4: A/B runs and cross-checks)
-  if (want >= 0) h->d.has_rect = (want != 0 && h->d.rect.frec != nullptr) ? (want >= 2 && want <= 4 ? want : 1) : 0;
+  // 0 general, 1 rectangle kernels (the two-kernel chain), 2 the four-kernel chain
+  // (A/B runs and cross-checks)
+  if (want >= 0) h->d.has_rect = (want != 0 && h->d.rect.frec != nullptr) ? (want == 2 ? 2 : 1) : 0;
   return h->d.has_rect;
 }
 

@@ -18,24 +18,30 @@
 // differ from it only in rounding).  The one-sided viscous normal flux on a
 // face is +-fx or +-fy, so only that row of the stress is formed.
 //
-// Four kernels chained with programmatic dependent launch.  Element
-// kernels read only contiguous per-element blocks, staged by TMA bulk
-// copies (UBLKCP) completed on an mbarrier; gathers happen only in the two
-// face kernels, scattered writes wherever a result belongs to other
-// elements:
-//   k_rface  one thread per point of each UNIQUE face: the two face traces
-//            from the elements' q lines, the interface flux F (Roe /
-//            Rusanov, once per face) into the face record, the BR1 common
-//            value What into both sides' per-element What blocks
-//   k_rgrad  one thread per (element, line): BR1 gradients by line passes
-//            (rows gx, columns gy, one shared-memory transpose each), their
-//            face traces, the one-sided viscous fluxes into the face record
-//   k_rfc    one thread per unique face point: the common total normal
-//            flux Fc = F - Fv (spatial.py:559-568) into both sides'
-//            per-element Fc blocks (R side negated: bitwise its own value)
-//   k_rasm   one thread per (element, line): gradients again (cheaper than a
-//            2 x 79 MB round trip at config 2), point fluxes, the FR
-//            divergence by line passes, the fused epilogue
+// Two kernels chained with programmatic dependent launch (navier-stokes;
+// for euler the first one is the per-face k_rface).  Both take one thread
+// per (element, line); a CTA's contiguous q / What blocks arrive by TMA bulk
+// copies (UBLKCP) completed on an mbarrier; the only gathers are the
+// neighbours' q lines (k_rgf) and the four face records of a thread
+// (k_rasm):
+//   k_rgf    traces on the four faces (own: from the staged q block;
+//            neighbours of the CTA's own element run: handed over through
+//            shared memory; other neighbours: gathered from q), the BR1
+//            common value What into the element's own What block, the
+//            interface flux F (Roe / Rusanov) once per face by its L side,
+//            BR1 gradients by line passes (rows gx, columns gy, one
+//            shared-memory transpose each), their face traces, and the
+//            element's share of the common total normal flux (spatial.py:
+//            559-568) into the face record: G = F - fl/2 from the L side,
+//            H = fr/2 from the R side (LDG: G = F, H = fr; boundary: F - fl)
+//   k_rasm   Fc = +-(G + H) from the gathered records, gradients again
+//            (cheaper than a 2 x 79 MB round trip at config 2), point
+//            fluxes, the FR divergence by line passes, the fused epilogue;
+//            element blocks in descending order (k_rgf's last blocks are
+//            still in L2), epilogue operands prefetched to L2 at the start
+// Kept for A/B and as a cross-check (Discretization.residual_path): the
+// four-kernel chain this replaced (k_rface + k_rgrad + k_rfc + k_rasm with
+// per-element Fc blocks).
 // Line threads keep each line in registers, so the operator contractions
 // read shared memory only for the transposes (blocks of one line, stride
 // an odd number of 16-byte units: conflict-free 128-bit accesses).
@@ -82,11 +88,22 @@ __host__ __device__ constexpr int tl(int el, int line, int pos) {
 // per-face-point record of the unique-face array: F on L's normal, then the
 // one-sided viscous fluxes of the L and R sides on their own normals
 constexpr int FREC4 = 12;
-// two-kernel chain: [0..3] G = F - (L's share of the common viscous flux),
-// written by the L side; [4..6] H = the R side's share (component 0 of a
-// viscous flux is identically zero), written by the R side; the common
-// total normal flux on L's normal is Fc = G + H (boundary faces: G)
-constexpr int FREC = 8;
+// Two-kernel chain.  PMGB_RECT_REC12 = 1 (default): the same 12-double
+// record [F | fl | fr], the L side writing F and fl, the R side fr, and
+// k_rasm forming Fc = F - 0.5 (fl - fr) as the reference rounds it
+// (spatial.py:559-568; k_rfc's arithmetic).
+// PMGB_RECT_REC12 = 0: 8 doubles, [0..3] G = F - (L's share of the common
+// viscous flux) from the L side, [4..6] H = the R side's share, Fc = G + H:
+// a third less record traffic (config-2 R 114.6 -> 105.0 us,
+// profiles/r2/ab_rec12_r2t.log), but (F - fl/2) + fr/2 rounds F's
+// magnitude once more than the reference does; through the FD products
+// that moved one restarted-GMRES count of the 48^2 config-2 step from
+// within 1 to within 2 of the reference's (tests/test_gpu_fullsize_oracle.py),
+// so it is not the default.
+#ifndef PMGB_RECT_REC12
+#define PMGB_RECT_REC12 1
+#endif
+constexpr int FREC = PMGB_RECT_REC12 ? 12 : 8;
 
 #ifndef PMGB_RECT_TH   // CTA width target of the element kernels (A/B)
 #define PMGB_RECT_TH 128
@@ -352,8 +369,8 @@ __global__ void __launch_bounds__(128) k_rface(const FrConst C, const RectMesh m
   const double g = C.gamma;
   const Phys ph = phys_of(C);
   const int kk = rev ? N - 1 - k : k;
-  // q is k_form's output when the chain evaluates at q + eps X; the
-  // successors (which read q ahead of their own wait) start after it
+  // the stream predecessor (launched ahead of with programmatic
+  // serialization) may still be writing q or reading the records
   pdl_wait();
   pdl_trigger();
   double qa[4], qc[4];
@@ -855,6 +872,78 @@ __device__ __forceinline__ void gh_combine(bool lft, const double* G, const doub
   Fc[3] = lft ? c3 : -c3;
 }
 
+// One face record as a thread of the two-kernel chain holds it
+struct FaceRec {
+  double a[4], b[4];   // REC12: F, fl;  else G, H
+#if PMGB_RECT_REC12
+  double c[4];         // fr
+#endif
+};
+__device__ __forceinline__ void rec_load(const double* rec, bool visc, bool interior, bool lv, FaceRec& r) {
+#pragma unroll
+  for (int v = 0; v < 4; ++v) {
+    r.a[v] = r.b[v] = 0.0;
+#if PMGB_RECT_REC12
+    r.c[v] = 0.0;
+#endif
+  }
+  if (!lv) return;
+  ldg4c(rec, r.a);
+#if PMGB_RECT_REC12
+  if (visc) {
+    ldg4c(rec + 4, r.b);
+    if (interior) ldg4c(rec + 8, r.c);
+  }
+#else
+  if (visc && interior) ldg4c(rec + 4, r.b);
+#endif
+}
+// Fc on the thread's own normal (k_rfc's arithmetic when REC12)
+__device__ __forceinline__ void rec_combine(const Phys& ph, bool visc, bool bnd, int tag, bool lft, const FaceRec& r,
+                                            double* Fc) {
+#if PMGB_RECT_REC12
+  double c[4] = {r.a[0], r.a[1], r.a[2], r.a[3]};
+  if (visc) {
+    double Fv[4];
+    if (bnd) {
+#pragma unroll
+      for (int v = 0; v < 4; ++v) Fv[v] = common_fv(ph, false, true, r.b[v], r.b[v]);
+      if (tag == T_WALL_ADIABATIC) Fv[3] = 0.0;
+    } else {
+#pragma unroll
+      for (int v = 0; v < 4; ++v) Fv[v] = common_fv(ph, true, true, r.b[v], r.c[v]);
+    }
+#pragma unroll
+    for (int v = 0; v < 4; ++v) c[v] = c[v] - Fv[v];
+  }
+#pragma unroll
+  for (int v = 0; v < 4; ++v) Fc[v] = lft ? c[v] : -c[v];
+#else
+  gh_combine(lft, r.a, r.b, Fc);
+#endif
+}
+// k_rgf's side of the record: F and the one-sided viscous flux o on the own normal
+__device__ __forceinline__ void rec_put(const Phys& ph, bool bnd, int tag, bool lft, const double* F, const double* o,
+                                        double* rec) {
+#if PMGB_RECT_REC12
+  if (lft) {
+    stg4_last(rec, F);
+    stg4_last(rec + 4, o);
+  } else {
+    stg4_last(rec + 8, o);
+  }
+#else
+  double r[4];
+  if (lft) {
+    gh_left(ph, bnd, tag, F, o, r);
+    stg4_last(rec, r);
+  } else {
+    gh_right(ph, o, r);
+    stg4_last(rec + 4, r);
+  }
+#endif
+}
+
 // ---------------------------------------------------------------------------
 // Static face data of line thread (el, a): its four face points sit at the
 // ends of row a (faces 1, 3) and of column a (faces 2, 0).
@@ -928,8 +1017,8 @@ k_rgf(const FrConst C, const RectMesh m, const double* __restrict__ q, const dou
   const double g = C.gamma;
   if (t == 0) mbar_init(bar);
   __syncthreads();
-  // q is k_form's output when the chain evaluates at q + eps X; k_rasm
-  // (which requests its q block ahead of its own wait) starts after it
+  // the stream predecessor (launched ahead of with programmatic
+  // serialization) may still be writing q or reading What / the records
   pdl_wait();
   pdl_trigger();
   const uint32_t qbytes = (uint32_t)ne * NP * 32;
@@ -1144,14 +1233,7 @@ k_rgf(const FrConst C, const RectMesh m, const double* __restrict__ q, const dou
   // -fx, face 2 +fy, face 0 -fy; each side's half of the face record
   auto put = [&](int f, double* o) {
     const bool bnd = fs.nb[f] < 0;
-    double r[4];
-    if (bnd || lk_left(fs.fl[f])) {
-      gh_left(ph, bnd, lk_tag(fs.fl[f]), Fk[f], o, r);
-      stg4_last(frec + (int64_t)fs.ri[f] * FREC, r);
-    } else {
-      gh_right(ph, o, r);
-      stg4_last(frec + (int64_t)fs.ri[f] * FREC + 4, r);
-    }
+    rec_put(ph, bnd, lk_tag(fs.fl[f]), bnd || lk_left(fs.fl[f]), Fk[f], o, frec + (int64_t)fs.ri[f] * FREC);
   };
   double o[4];
   {
@@ -1250,21 +1332,12 @@ k_rasm(const FrConst C, const RectMesh m, const double* __restrict__ q, const do
     if (blockIdx.x == 0) commit_status(bad, st);
   }
   double fcv[4][4];
-  double rG[4][4], rH[4][4];
+  FaceRec rc[4];
   if constexpr (FOLD) {
     // the four face records (fc here is the face-record array), gathered
     // while the q block is in flight
 #pragma unroll
-    for (int f = 0; f < 4; ++f) {
-      const double* rec = fc + (int64_t)fs.ri[f] * FREC;
-#pragma unroll
-      for (int v = 0; v < 4; ++v) rG[f][v] = rH[f][v] = 0.0;
-      if (live) {
-        ldg4c(rec, rG[f]);
-        if constexpr (VISC)
-          if (fs.nb[f] >= 0) ldg4c(rec + 4, rH[f]);
-      }
-    }
+    for (int f = 0; f < 4; ++f) rec_load(fc + (int64_t)fs.ri[f] * FREC, VISC, fs.nb[f] >= 0, live, rc[f]);
   }
 #if PMGB_RECT_PF > 0
   if (t == 0 && (int64_t)(blockIdx.x + PMGB_RECT_PF) * E + E <= m.M) {
@@ -1275,7 +1348,8 @@ k_rasm(const FrConst C, const RectMesh m, const double* __restrict__ q, const do
 #endif
   auto combine = [&]() {
 #pragma unroll
-    for (int f = 0; f < 4; ++f) gh_combine(fs.nb[f] < 0 || lk_left(fs.fl[f]), rG[f], rH[f], fcv[f]);
+    for (int f = 0; f < 4; ++f)
+      rec_combine(ph, VISC, fs.nb[f] < 0, lk_tag(fs.fl[f]), fs.nb[f] < 0 || lk_left(fs.fl[f]), rc[f], fcv[f]);
   };
   mbar_wait(bar, 0);
   if constexpr (HASX) {
@@ -1438,309 +1512,6 @@ k_rasm(const FrConst C, const RectMesh m, const double* __restrict__ q, const do
 }
 
 // ---------------------------------------------------------------------------
-// k_rasm_p: k_rasm as a persistent, software-pipelined kernel.  A CTA walks
-// the element blocks b = blockIdx.x, blockIdx.x + gridDim.x, ...; while block
-// i is computed the TMA copies of block i+1's q (+ X) and What blocks are in
-// flight into the other stage, its four face records per thread are in
-// flight into registers, and the static face data of block i+2 is being
-// fetched -- the load phase of every block but a CTA's first overlaps the
-// arithmetic of its predecessor (the one-shot kernels spend 40-50 % of their
-// warp time waiting at the start of each CTA: T_load + T_compute instead of
-// max(T_load, T_compute)).  Two CTAs of 128 threads per SM, so a thread may
-// hold the in-flight records in registers.
-
-// the arithmetic of one block after its operands are in registers / shared
-// memory: W^T, gy, gx, point fluxes, FR divergence, fused epilogue
-template <int P, int KIND, int EK>
-__device__ __forceinline__ void rasm_body(const FrConst& C, const Phys& ph, const Epi& ep, const double* sQ,
-                                          double* sX, double* sY, double (&w)[3][P + 1],
-                                          const double (&whv)[4][3], const double (&fcv)[4][4], const double2 rg,
-                                          const int el, const int a, const int64_t e, const bool live,
-                                          double* __restrict__ out) {
-  constexpr int N = P + 1, NP = N * N;
-  constexpr bool VISC = KT<KIND>::VISC;
-  const double g = C.gamma;
-  const double* row = sQ + (el * N + a) * N * 4;
-  double gy[3][N];
-  if constexpr (VISC) {
-#pragma unroll
-    for (int i = 0; i < N; ++i)
-#pragma unroll
-      for (int c = 0; c < 3; ++c) sX[tl<N, 3>(el, i, c * N + a)] = w[c][i];
-    __syncthreads();
-    // column a: gy -> row blocks
-    {
-      const double* blk = sX + tl<N, 3>(el, a, 0);
-#pragma unroll
-      for (int c = 0; c < 3; ++c)
-#pragma unroll
-        for (int i = 0; i < N; ++i) w[c][i] = blk[c * N + i];
-      double gc[3][N];
-      line_gradient<N>(C, w, whv[2], whv[0], rg.y, gc);
-#pragma unroll
-      for (int i = 0; i < N; ++i)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) sY[tl<N, 3>(el, i, c * N + a)] = gc[c][i];
-    }
-    __syncthreads();
-    const double* blk = sY + tl<N, 3>(el, a, 0);
-#pragma unroll
-    for (int c = 0; c < 3; ++c)
-#pragma unroll
-      for (int i = 0; i < N; ++i) gy[c][i] = blk[c * N + i];
-  }
-  // row a: primitives (again: cheaper than holding them through the column
-  // pass), gx, point fluxes -- fx stays in registers, fy -> column blocks
-  double qr[4][N];
-  Pr pr[N];
-#pragma unroll
-  for (int i = 0; i < N; ++i) {
-    double x[4];
-    lds4(row + 4 * i, x);
-#pragma unroll
-    for (int v = 0; v < 4; ++v) qr[v][i] = x[v];
-    pr[i] = prim_of(x, g);
-  }
-  double gx[3][N];
-  if constexpr (VISC) {
-#pragma unroll
-    for (int i = 0; i < N; ++i) {
-      w[0][i] = pr[i].u;
-      w[1][i] = pr[i].v;
-      w[2][i] = pr[i].p * pr[i].ir;
-    }
-    line_gradient<N>(C, w, whv[1], whv[3], rg.x, gx);
-  }
-  double fx[4][N];
-#pragma unroll
-  for (int i = 0; i < N; ++i) {
-    const Pr& s = pr[i];
-    double Fx[4], Fy[4];
-    Fx[0] = qr[1][i];
-    Fx[1] = qr[1][i] * s.u + s.p;
-    Fx[2] = qr[1][i] * s.v;
-    Fx[3] = s.u * (qr[3][i] + s.p);
-    Fy[0] = qr[2][i];
-    Fy[1] = qr[2][i] * s.u;
-    Fy[2] = qr[2][i] * s.v + s.p;
-    Fy[3] = s.v * (qr[3][i] + s.p);
-    if constexpr (VISC) {
-      const double gxx[3] = {gx[0][i], gx[1][i], gx[2][i]};
-      const double gyy[3] = {gy[0][i], gy[1][i], gy[2][i]};
-      const double d = gxx[0] + gyy[1];
-      const double txx = ph.mu * (2.0 * gxx[0] - (2.0 / 3.0) * d);
-      const double tyy = ph.mu * (2.0 * gyy[1] - (2.0 / 3.0) * d);
-      const double txy = ph.mu * (gyy[0] + gxx[1]);
-      Fx[1] = Fx[1] - txx;
-      Fx[2] = Fx[2] - txy;
-      Fx[3] = Fx[3] - (s.u * txx + s.v * txy + ph.kappa * gxx[2]);
-      Fy[1] = Fy[1] - txy;
-      Fy[2] = Fy[2] - tyy;
-      Fy[3] = Fy[3] - (s.u * txy + s.v * tyy + ph.kappa * gyy[2]);
-      Fx[0] = Fx[0] - 0.0;
-      Fy[0] = Fy[0] - 0.0;
-    }
-#pragma unroll
-    for (int v = 0; v < 4; ++v) {
-      fx[v][i] = Fx[v];
-      sX[tl<N, 4>(el, i, v * N + a)] = Fy[v];
-    }
-  }
-  // X_xi along row a
-  double xx[4][N];
-  line_div<N>(C, fx, fcv[1], fcv[3], xx);
-  if constexpr (VISC) __syncthreads();  // gy row reads of sY done
-#pragma unroll
-  for (int i = 0; i < N; ++i)
-#pragma unroll
-    for (int v = 0; v < 4; ++v) sY[tl<N, 4>(el, i, v * N + a)] = xx[v][i];
-  __syncthreads();
-  if (live) {
-  // column a: fy and X_xi of the column, faces 2 / 0, X_eta, R, epilogue
-  double fyc[4][N];
-  {
-    const double* blk = sX + tl<N, 4>(el, a, 0);
-#pragma unroll
-    for (int v = 0; v < 4; ++v)
-#pragma unroll
-      for (int i = 0; i < N; ++i) fyc[v][i] = blk[v * N + i];
-  }
-  double xe[4][N];
-  line_div<N>(C, fyc, fcv[2], fcv[0], xe);
-  const double* bx = sY + tl<N, 4>(el, a, 0);
-  constexpr bool NEEDQ = !(EK == EPI_R || EK == EPI_JV || EK == EPI_NEG_R);
-  const double ce = (EK == EPI_RK) ? epi_rk_coef(ep, e) : 0.0;
-#pragma unroll
-  for (int i = 0; i < N; ++i) {   // point (i, a)
-    const int64_t pt = e * NP + i * N + a;
-    double qv[4] = {0, 0, 0, 0};
-    if constexpr (NEEDQ) lds4(sQ + ((el * N + i) * N + a) * 4, qv);
-    double o[4], o1[4], o2[4], o3[4];
-    if constexpr (EK != EPI_R) epi_load4_k<EK>(ep, pt * 4, o1, o2, o3);   // operands as 256-bit loads
-#pragma unroll
-    for (int v = 0; v < 4; ++v) {
-      const double Rv = -(rg.x * bx[v * N + i] + rg.y * xe[v][i]);
-      if constexpr (EK == EPI_R)
-        o[v] = Rv;
-      else
-        o[v] = (EK == EPI_RK) ? epi_rk(ep, ce, Rv, qv[v], o1[v], o2[v], o3[v])
-                              : epi_pre_k<EK>(ep, Rv, qv[v], o1[v], o2[v], o3[v]);
-    }
-    stg4(out + pt * 4, o);
-  }
-  }
-}
-
-template <int P, int KIND, bool HASX> struct PL {
-  using R = RC<P>;
-  static constexpr bool VISC = KT<KIND>::VISC;
-  static constexpr int S_ = TL<R::N, 3>::S > TL<R::N, 4>::S ? TL<R::N, 3>::S : TL<R::N, 4>::S;
-  static constexpr int BUF = R::EPB * S_;
-  static constexpr int OFF_Q1 = R::QD, OFF_XQ = 2 * R::QD, OFF_W = OFF_XQ + (HASX ? R::QD : 0);
-  static constexpr int OFF_X = OFF_W + (VISC ? R::WD : 0), OFF_Y = OFF_X + BUF, OFF_BAR = OFF_Y + BUF;
-  static constexpr size_t BYTES = sizeof(double) * (OFF_BAR + 2);
-};
-
-template <int P, int KIND, int EK, bool HASX>
-__global__ void __launch_bounds__(RC<P>::TH, 2)
-k_rasm_p(const FrConst C, const RectMesh m, const double* __restrict__ q, const double* __restrict__ X, double eps,
-         const double* __restrict__ wh, const double* __restrict__ frec, const Epi ep, double* __restrict__ out,
-         int* bad, Status* st, int nblk) {
-  using R = RC<P>;
-  using L = PL<P, KIND, HASX>;
-  constexpr int N = R::N, NP = R::NP, E = R::EPB;
-  constexpr bool VISC = KT<KIND>::VISC;
-  extern __shared__ __align__(128) double sm[];
-  double* sXq = sm + L::OFF_XQ;
-  const double* sWb = sm + L::OFF_W;
-  double* sX = sm + L::OFF_X;
-  double* sY = sm + L::OFF_Y;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::OFF_BAR);
-  const int t = threadIdx.x;
-  const int el = t / N, a = t % N;
-  const bool inr = t < E * N;
-  const Phys ph = phys_of(C);
-  const double g = C.gamma;
-  if (t == 0) {
-    mbar_init(bar);
-    mbar_init(bar + 1);
-  }
-  __syncthreads();
-  // thread 0: the TMA copies of block blk into stage s
-  auto issue = [&](int blk, int s) {
-    const int64_t e0 = (int64_t)blk * E;
-    const int ne = (int)((m.M - e0) < E ? (m.M - e0) : E);
-    const uint32_t qb = (uint32_t)ne * NP * 32, wb = (uint32_t)ne * 4 * N * 24;
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    mbar_expect(bar + s, (HASX ? 2 * qb : qb) + (VISC ? wb : 0u));
-    bulk_g2s(sm + s * R::QD, q + e0 * NP * 4, qb, bar + s);
-    if (HASX) bulk_g2s(sXq, X + e0 * NP * 4, qb, bar + s);
-    if (VISC) bulk_g2s(sm + L::OFF_W, wh + e0 * 4 * N * 3, wb, bar + s);
-  };
-  auto live_of = [&](int blk) { return inr && blk < nblk && (int64_t)blk * E + el < m.M; };
-  // the thread's four face records of a block (static data fs)
-  auto fetch = [&](const FaceStat& fs, bool lv, double (&rG)[4][4], double (&rH)[4][4]) {
-#pragma unroll
-    for (int f = 0; f < 4; ++f) {
-      const double* rec = frec + (int64_t)fs.ri[f] * FREC;
-#pragma unroll
-      for (int v = 0; v < 4; ++v) rG[f][v] = rH[f][v] = 0.0;
-      if (lv) {
-        ldg4c(rec, rG[f]);
-        if constexpr (VISC)
-          if (fs.nb[f] >= 0) ldg4c(rec + 4, rH[f]);
-      }
-    }
-  };
-  int b = blockIdx.x;
-  const int G = gridDim.x;
-  // static data of the first two blocks (no dependence on the predecessor)
-  FaceStat fs0, fs1;
-  face_stat<N>(m, (int64_t)b * E + el, a, live_of(b), fs0);
-  face_stat<N>(m, (int64_t)(b + G) * E + el, a, live_of(b + G), fs1);
-  double2 rg0 = live_of(b) ? __ldg(m.rgeo + (int64_t)b * E + el) : make_double2(1.0, 1.0);
-  double2 rg1 = live_of(b + G) ? __ldg(m.rgeo + (int64_t)(b + G) * E + el) : make_double2(1.0, 1.0);
-  pdl_wait();  // What and the face records (k_rgf / k_rface), status flags
-  if (t == 0) {
-    if (b < nblk) issue(b, 0);
-    if (blockIdx.x == 0) commit_status(bad, st);
-  }
-  double rG[4][4], rH[4][4];
-  fetch(fs0, live_of(b), rG, rH);
-  for (int it = 0; b < nblk; b += G, ++it) {
-    const int s = it & 1;
-    const double* sQ = sm + s * R::QD;
-    const int64_t e = (int64_t)b * E + el;
-    const bool live = live_of(b);
-    const double2 rg = rg0;
-    // this block's common fluxes; then the next block's records and the
-    // static data of the block after it take their place in flight
-    double fcv[4][4];
-#pragma unroll
-    for (int f = 0; f < 4; ++f) gh_combine(fs0.nb[f] < 0 || lk_left(fs0.fl[f]), rG[f], rH[f], fcv[f]);
-    fs0 = fs1;
-    rg0 = rg1;
-    fetch(fs0, live_of(b + G), rG, rH);
-    face_stat<N>(m, (int64_t)(b + 2 * G) * E + el, a, live_of(b + 2 * G), fs1);
-    rg1 = live_of(b + 2 * G) ? __ldg(m.rgeo + (int64_t)(b + 2 * G) * E + el) : make_double2(1.0, 1.0);
-    mbar_wait(bar + s, (it >> 1) & 1);
-    if constexpr (HASX) {
-      const int64_t e0 = (int64_t)b * E;
-      const int ne = (int)((m.M - e0) < E ? (m.M - e0) : E);
-      form_qp<R::TH>(const_cast<double*>(sQ), sXq, eps, ne * NP * 4);
-      __syncthreads();
-    }
-    const double* row = sQ + (el * N + a) * N * 4;
-    double w[3][N];
-    if constexpr (VISC) {
-#pragma unroll
-      for (int i = 0; i < N; ++i) {
-        double x[4];
-        lds4(row + 4 * i, x);
-        const Pr sp = prim_of(x, g);
-        w[0][i] = sp.u;
-        w[1][i] = sp.v;
-        w[2][i] = sp.p * sp.ir;
-      }
-    }
-    double whv[4][3];
-    if constexpr (VISC) {
-#pragma unroll
-      for (int f = 0; f < 4; ++f)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) whv[f][c] = sWb[(el * 4 * N + fpt_of<N>(f, a)) * 3 + c];
-    }
-    __syncthreads();  // every thread is past the previous block; the What / X stages are consumed
-    if (t == 0 && b + G < nblk) issue(b + G, s ^ 1);
-    rasm_body<P, KIND, EK>(C, ph, ep, sQ, sX, sY, w, whv, fcv, rg, el, a, e, live, out);
-  }
-}
-
-// ---------------------------------------------------------------------------
-// k_form: qp = q + eps X once per evaluation (the reference's rounding,
-// newton_krylov.py:76 -- the same two roundings as form_qp / ld_q), so the
-// chain's kernels run their X-free instances on qp: the neighbour gathers
-// and the staged blocks read one array instead of two.
-
-__global__ void __launch_bounds__(256) k_form(const double* __restrict__ q, const double* __restrict__ X, double eps,
-                                              double* __restrict__ qp, int64_t n4, int64_t n) {
-  pdl_trigger();
-  const int64_t stride = (int64_t)gridDim.x * 256;
-  for (int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x; i < n4; i += stride) {
-    double a[4], x[4];
-    ldg4(q + 4 * i, a);
-    ldg4(X + 4 * i, x);
-#pragma unroll
-    for (int v = 0; v < 4; ++v) a[v] = __dadd_rn(a[v], __dmul_rn(eps, x[v]));
-    stg4(qp + 4 * i, a);
-  }
-  if (blockIdx.x == 0 && threadIdx.x < (n & 3)) {   // scalar kinds never come here; kept for safety
-    const int64_t i = 4 * n4 + threadIdx.x;
-    qp[i] = __dadd_rn(q[i], __dmul_rn(eps, X[i]));
-  }
-}
-
-// ---------------------------------------------------------------------------
 // host side
 
 template <typename... KArgs, typename... Args>
@@ -1775,46 +1546,8 @@ static RasmFn rasm_for(int mode) {
   return k_rasm<P, KIND, -1, HASX, FOLD>;
 }
 
-using RasmPFn = void (*)(const FrConst, const RectMesh, const double*, const double*, double, const double*,
-                         const double*, const Epi, double*, int*, Status*, int);
-template <int P, int KIND, bool HASX>
-static RasmPFn rasm_p_for(int mode) {
-  switch (mode) {
-    case EPI_R: return k_rasm_p<P, KIND, EPI_R, HASX>;
-    case EPI_JV: return k_rasm_p<P, KIND, EPI_JV, HASX>;
-    case EPI_STAGE_JV: return k_rasm_p<P, KIND, EPI_STAGE_JV, HASX>;
-    case EPI_DEFECT: return k_rasm_p<P, KIND, EPI_DEFECT, HASX>;
-    case EPI_F: return k_rasm_p<P, KIND, EPI_F, HASX>;
-    case EPI_RK: return k_rasm_p<P, KIND, EPI_RK, HASX>;
-  }
-  return k_rasm_p<P, KIND, -1, HASX>;
-}
-
-static int sm_count() {
-  static int n[64] = {0};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (n[dev & 63] == 0) cudaDeviceGetAttribute(&n[dev & 63], cudaDevAttrMultiProcessorCount, dev);
-  return n[dev & 63];
-}
-
-// PMGB_RECT_PREFORM=1: a k_form pass and the chain's X-free instances on qp
-// instead of forming q + eps X in every kernel.  Measured even at config 2
-// (Jv 168.9 vs 167.4 us) and slower at config 5 (4.00 vs 3.75 ms,
-// profiles/r2/negative/ab_preform_r2n.log): off unless asked for.
-static bool rect_preform() {
-  static const bool on = [] {
-    const char* env = std::getenv("PMGB_RECT_PREFORM");
-    return env != nullptr && env[0] == '1';
-  }();
-  return on;
-}
-
 template <int P, int KIND, bool HASX>
 static void set_rect_attrs() {
-  for (int md : {(int)EPI_R, (int)EPI_JV, (int)EPI_STAGE_JV, (int)EPI_DEFECT, (int)EPI_F, (int)EPI_RK, -1})
-    cudaFuncSetAttribute(rasm_p_for<P, KIND, HASX>(md), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)PL<P, KIND, HASX>::BYTES);
   for (int md : {(int)EPI_R, (int)EPI_JV, (int)EPI_STAGE_JV, (int)EPI_DEFECT, (int)EPI_F, (int)EPI_RK, -1}) {
     cudaFuncSetAttribute(rasm_for<P, KIND, HASX, false>(md), cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)AL<P, KIND, HASX, false>::BYTES);
@@ -1828,16 +1561,12 @@ static void set_rect_attrs() {
   }
 }
 
-// d.has_rect: 3 the two-kernel chain k_rgf / k_rface + the one-shot k_rasm
-// (common flux folded in), 4 the same with the persistent k_rasm_p, 1 the
-// faster of the two at this degree (PERSIST below: measured on the B200,
-// profiles/r2/ab_chain_r2m.jsonl), 2 the four-kernel chain they replaced
-// (kept for A/B and as a cross-check)
+// d.has_rect: 1 the two-kernel chain k_rgf / k_rface + k_rasm (common flux
+// folded in), 2 the four-kernel chain it replaced (kept for A/B and as a
+// cross-check).  A persistent, double-buffered k_rasm was measured slower at
+// every degree (profiles/r2/ab_chain_r2m.jsonl, "rect2p") and removed.
 #ifndef PMGB_RECT_PDL0   // measured: config-2 R 113.0 -> 110.7 us, config 3 34.1 -> 32.0 us
 #define PMGB_RECT_PDL0 1
-#endif
-#ifndef PMGB_RECT_PERSIST_MAXP
-#define PMGB_RECT_PERSIST_MAXP 0
 #endif
 template <int P, int KIND>
 static int run_rect(const RectDev& rd, const DiscDev& d, const double* q, const double* X, double eps,
@@ -1851,23 +1580,9 @@ static int run_rect(const RectDev& rd, const DiscDev& d, const double* q, const 
   const RectMesh m{d.M, rd.nface, rd.faces, rd.fslot, d.link, rd.rgeo, d.geom};
   const unsigned gf = (unsigned)((rd.nface * (P + 1) + 127) / 128);
   const unsigned ge = (unsigned)((d.M + R::EPB - 1) / R::EPB);
-  bool hx = X != nullptr;
+  const bool hx = X != nullptr;
   const bool fold = d.has_rect != 2;
-  if (fold && hx && d.qp != nullptr && rect_preform()) {
-    // evaluate at qp = q + eps X formed once; the epilogues still read X
-    const int64_t n = d.M * R::NP * 4;
-    const int64_t nb = (n / 4 + 255) / 256, cap = 16 * (int64_t)sm_count();
-    k_form<<<(unsigned)(nb < cap ? nb : cap), 256, 0, st>>>(q, X, eps, d.qp, n / 4, n);
-    q = d.qp;
-    hx = false;
-    if constexpr (KT<KIND>::VISC)
-      launch_pdl_r(k_rgf<P, KIND, false>, ge, R::TH, GFL<P, false>::BYTES, st, d.C, m, q, (const double*)nullptr,
-                   eps, rd.wh, rd.frec, bad);
-    else
-      launch_pdl_r(k_rface<P, KIND, false, FREC>, gf, 128, 0, st, d.C, m, q, (const double*)nullptr, eps, rd.frec,
-                   rd.wh, bad);
-    X = nullptr;
-  } else if (fold && KT<KIND>::VISC) {
+  if (fold && KT<KIND>::VISC) {
     if constexpr (KT<KIND>::VISC) {
 #if PMGB_RECT_PDL0   // the chain's first kernel may start while its stream predecessor drains
       if (hx)
@@ -1908,14 +1623,6 @@ static int run_rect(const RectDev& rd, const DiscDev& d, const double* q, const 
         launch_pdl_r(k_rgrad<P, false>, ge, R::TH, GL<P, false>::BYTES, st, d.C, m, q, X, eps,
                      (const double*)rd.wh, rd.frec, bad);
     }
-  }
-  if (d.has_rect == 4 || (d.has_rect == 1 && P <= PMGB_RECT_PERSIST_MAXP)) {
-    RasmPFn fn = hx ? rasm_p_for<P, KIND, true>(epi.mode) : rasm_p_for<P, KIND, false>(epi.mode);
-    const size_t smem = hx ? PL<P, KIND, true>::BYTES : PL<P, KIND, false>::BYTES;
-    const unsigned gp = ge < 2u * (unsigned)sm_count() ? ge : 2u * (unsigned)sm_count();
-    launch_pdl_r(fn, gp, R::TH, smem, st, d.C, m, q, X, eps, (const double*)rd.wh, (const double*)rd.frec, epi,
-                 out, bad, stp, (int)ge);
-    return (int)cudaGetLastError();
   }
   if (fold) {
     RasmFn fn = hx ? rasm_for<P, KIND, true, true>(epi.mode) : rasm_for<P, KIND, false, true>(epi.mode);
@@ -1959,7 +1666,8 @@ int launch_residual_rect(const RectDev& rd, const DiscDev& d, const double* q, c
 
 int rect_launches(const DiscDev& d, bool has_x) {
   if (d.has_rect == 2) return d.kind == K_NS ? 4 : 3;
-  return 2 + ((has_x && d.qp != nullptr && rect_preform()) ? 1 : 0);
+  (void)has_x;
+  return 2;
 }
 
 bool rect_supported(int p, int kind) { return p >= 1 && p <= 5 && (kind == K_EULER || kind == K_NS); }

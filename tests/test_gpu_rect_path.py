@@ -154,13 +154,15 @@ def test_rect_config2_matches_general_full_size(cuda):
 @pytest.mark.parametrize("p", [1, 2, 3, 4, 5])
 @pytest.mark.parametrize("kind", ["euler", "navier-stokes"])
 def test_chain_variants_agree(cuda, p, kind):
-    """The three rectangle chains -- k_rgf + persistent k_rasm_p ("rect2p"), k_rgf
-    + one-shot k_rasm ("rect2"), k_rface + k_rgrad + k_rfc + k_rasm ("rect4")
-    -- evaluate the same formulas: "rect2p" and "rect2" bit for bit (same
-    arithmetic, different scheduling), both within rounding of "rect4" (the
-    common flux is summed per side, (F - fl/2) + fr/2), on walled channels
-    (every boundary branch), Rusanov / LDG, for R and the fused Jv; more
-    blocks than resident CTAs so the persistent loop wraps."""
+    """The two rectangle chains -- k_rgf (k_rface for euler) + k_rasm with the
+    common flux folded in ("rect", the default) and k_rface + k_rgrad + k_rfc +
+    k_rasm ("rect4") -- evaluate the same formulas in the same order (the
+    compiler's FMA contraction differs between the kernels, so they agree to
+    rounding, not bit for bit): on walled channels (every boundary branch),
+    with Rusanov / LDG, for R, the fused Jv and the defect epilogue; more
+    element blocks than resident CTAs, element runs that end inside a CTA,
+    neighbours inside and outside a CTA's run (the shared-memory trace
+    hand-over)."""
     yn = np.array([0.0, 0.03, 0.1, 0.3, 0.6, 1.0])
     nx = 210 if p == 4 else 23
     for m, opts in ((mm.generate_channel(nx, 5, 2.0, yn, bottom="wall-isothermal", top="wall-adiabatic"), {}),
@@ -175,12 +177,12 @@ def test_chain_variants_agree(cuda, p, kind):
                             device="cuda")
         X = torch.randn(n, dtype=torch.float64, device="cuda", generator=torch.Generator("cuda").manual_seed(p))
         out = {}
-        for path in ("rect2p", "rect2", "rect4", "rect"):
+        for path in ("rect", "rect4"):
             assert d.residual_path(path) == path
             out[path] = (d.residual(q), d.eval(q, _lib.EPI_JV, X=X, eps=1e-6, s=1.5, R0=X),
                          d.eval(q, _lib.EPI_DEFECT, s=2.0, Sb=X, Se=0.25))
-        for a, b, c in zip(out["rect2p"], out["rect2"], out["rect"]):
-            assert torch.equal(a, b) and torch.equal(a, c)
-        assert _rel(out["rect2"][0], out["rect4"][0]) <= 1e-13
-        assert _rel(out["rect2"][1], out["rect4"][1]) <= 1e-8   # rounding / eps
-        assert _rel(out["rect2"][2], out["rect4"][2]) <= 1e-13
+        assert _rel(out["rect"][0], out["rect4"][0]) <= 1e-13
+        assert _rel(out["rect"][1], out["rect4"][1]) <= 1e-8   # rounding / eps
+        assert _rel(out["rect"][2], out["rect4"][2]) <= 1e-13
+        d.residual_path("rect")
+        assert torch.equal(out["rect"][0], d.residual(q)), "bitwise determinism"

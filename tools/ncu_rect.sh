@@ -7,5 +7,5 @@ ncu -i /tmp/prof_rect.ncu-rep --page details --csv > gpurun_out/ncu_rect_details
 for k in k_rface k_rgrad k_rasm k_rfc k_rgf; do
   ncu -i /tmp/prof_rect.ncu-rep -k regex:$k -c 1 --page source --csv --print-source sass > gpurun_out/ncu_rect_src_$k.csv 2>/dev/null
 done
-cp /tmp/prof_rect.ncu-rep gpurun_out/ 2>/dev/null
+# the .ncu-rep stays on the box (gpurun_out/ is capped at 64 MiB)
 ls -la gpurun_out

@@ -6,10 +6,8 @@ paths' R.
 
     python tools/time_rect.py [configs...]      (default: 2 4; "2:p2" = config 2's mesh at degree 2)
 
-"rect2" is the two-kernel chain with the one-shot second kernel (k_rgf +
-k_rasm), "rect2p" the same with the persistent k_rasm_p, "rect" the default
-(the faster of the two per degree), "rect4" the four-kernel chain they
-replaced (k_rface + k_rgrad + k_rfc + k_rasm).  RECT_PATHS selects.
+"rect" is the two-kernel chain (k_rgf + k_rasm), "rect4" the four-kernel
+chain it replaced (k_rface + k_rgrad + k_rfc + k_rasm).  RECT_PATHS selects.
 """
 
 import json
@@ -37,7 +35,7 @@ def ev(fn, reps):
 
 
 import os
-PATHS = tuple(os.environ.get("RECT_PATHS", "rect,rect2,rect2p,rect4,general").split(","))
+PATHS = tuple(os.environ.get("RECT_PATHS", "rect,rect4,general").split(","))
 
 
 def main():
@@ -75,11 +73,8 @@ def main():
             a, b = outs["rect"], outs["general"]
             rec["rect_vs_general"] = float(np.max(np.abs(a - b)) / np.max(np.abs(b)))
             rec["speedup_r"] = rec["general"]["r_us"] / rec["rect"]["r_us"]
-        first = outs[PATHS[0]]
-        if "rect4" in outs:
-            rec[f"{PATHS[0]}_vs_rect4"] = float(np.max(np.abs(first - outs["rect4"])) / np.max(np.abs(outs["rect4"])))
-        if "rect2p" in outs and "rect2" in outs:
-            rec["rect2_bitwise_rect2p"] = bool(np.array_equal(outs["rect2"], outs["rect2p"]))
+        if "rect4" in outs and "rect" in outs:
+            rec["rect_bitwise_rect4"] = bool(np.array_equal(outs["rect"], outs["rect4"]))
         print(json.dumps(rec), flush=True)
         del d, qs, Rs
         torch.cuda.empty_cache()
