@@ -68,8 +68,12 @@ PMGB_API int64_t pmgb_disc_n_dofs(const pmgb_disc* d);
 /* Residual kernel family of a context: 1 = the axis-aligned-rectangle
    path (fr_rect.cu; chosen at creation when every element qualifies),
    0 = the general bilinear path.  `want` < 0 only queries; 1 is honoured
-   only when the mesh qualifies.  Returns the path now in effect.  (No
-   reference counterpart: both paths implement spatial.py:501-570.) */
+   only when the mesh qualifies.  2 and 3 pin the rectangle path's
+   four-kernel / two-kernel launch chain (1 takes the faster one per
+   degree; for A/B runs and cross-checks).  Returns the path now in
+   effect.  (No reference counterpart: every path implements
+   spatial.py:501-570.)  On the rectangle path the state and operand
+   arrays of pmgb_eval must be 32-byte aligned (error -6 otherwise). */
 PMGB_API int pmgb_disc_residual_path(pmgb_disc* d, int32_t want);
 
 /* R(q) -- replaces Discretization.residual (spatial.py:501-570). */

@@ -425,9 +425,9 @@ PMGB_API int pmgb_mdisc_element_residual(pmgb_mdisc* h, int32_t p, const int64_t
 
 PMGB_API int pmgb_disc_residual_path(pmgb_disc* h, int32_t want) {
   if (!h) return -1;
-  // 0 general, 1 rectangle kernels (the two-kernel chain), 2 the four-kernel chain
-  // (A/B runs and cross-checks)
-  if (want >= 0) h->d.has_rect = (want != 0 && h->d.rect.frec != nullptr) ? (want == 2 ? 2 : 1) : 0;
+  // 0 general, 1 rectangle kernels (the faster chain per degree), 2 the four-kernel
+  // chain, 3 the two-kernel chain (2, 3: A/B runs and cross-checks)
+  if (want >= 0) h->d.has_rect = (want != 0 && h->d.rect.frec != nullptr) ? (want == 2 || want == 3 ? want : 1) : 0;
   return h->d.has_rect;
 }
 

@@ -105,10 +105,14 @@ constexpr int FREC4 = 12;
 #endif
 constexpr int FREC = PMGB_RECT_REC12 ? 12 : 8;
 
-#ifndef PMGB_RECT_TH   // CTA width target of the element kernels (A/B)
-#define PMGB_RECT_TH 128
+// CTA width target of the element kernels: 64 threads (12 elements at p = 4,
+// six CTAs per SM) interleave the CTAs' load and compute phases more finely than
+// 128 (config-2 R 114.5 -> 111.8 us; 96: 112.5, 48: 114.7, 32: 114.6;
+// profiles/r2/ab_cta_width_r2t.log)
+#ifndef PMGB_RECT_TH
+#define PMGB_RECT_TH 64
 #endif
-#ifndef PMGB_RECT_PF   // L2 prefetch distance in CTAs (0: off) (A/B)
+#ifndef PMGB_RECT_PF   // L2 prefetch distance in CTAs (0: off; 888 and 1776 measured slower, ab_cta_width_r2t.log)
 #define PMGB_RECT_PF 0
 #endif
 // k_rasm (two-kernel chain) walks the element blocks in descending order: what
@@ -329,6 +333,16 @@ __device__ __forceinline__ void stg4_last(double* p, const double* v) {
 #if PMGB_RECT_L2_HINTS
   asm volatile("st.global.L2::cache_hint.v4.f64 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "d"(v[0]), "d"(v[1]),
                "d"(v[2]), "d"(v[3]), "l"(pol_last())
+               : "memory");
+#else
+  stg4(p, v);
+#endif
+}
+// the chain's output: nothing in the chain reads it again
+__device__ __forceinline__ void stg4_first(double* p, const double* v) {
+#if PMGB_RECT_L2_HINTS
+  asm volatile("st.global.L2::cache_hint.v4.f64 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "d"(v[0]), "d"(v[1]),
+               "d"(v[2]), "d"(v[3]), "l"(pol_first())
                : "memory");
 #else
   stg4(p, v);
@@ -1027,6 +1041,10 @@ k_rgf(const FrConst C, const RectMesh m, const double* __restrict__ q, const dou
     bulk_g2s(sQ, q + e0 * NP * 4, qbytes, bar);
     if (HASX) bulk_g2s(sX, X + e0 * NP * 4, qbytes, bar);
   }
+#if PMGB_RECT_PF > 0
+  if (t == 32 && ((int64_t)blockIdx.x + PMGB_RECT_PF + 1) * E <= m.M)
+    l2_prefetch(q + ((int64_t)blockIdx.x + PMGB_RECT_PF) * E * NP * 4, (uint32_t)E * NP * 32);
+#endif
   FaceStat fs;
   face_stat<N>(m, e, a, live, fs);
   const double2 rg = live ? __ldg(m.rgeo + e) : make_double2(0.0, 0.0);
@@ -1339,11 +1357,13 @@ k_rasm(const FrConst C, const RectMesh m, const double* __restrict__ q, const do
 #pragma unroll
     for (int f = 0; f < 4; ++f) rec_load(fc + (int64_t)fs.ri[f] * FREC, VISC, fs.nb[f] >= 0, live, rc[f]);
   }
-#if PMGB_RECT_PF > 0
-  if (t == 0 && (int64_t)(blockIdx.x + PMGB_RECT_PF) * E + E <= m.M) {
-    const int64_t en = (int64_t)(blockIdx.x + PMGB_RECT_PF) * E;
-    l2_prefetch(q + en * NP * 4, (uint32_t)E * NP * 32);
-    if (VISC) l2_prefetch(wh + en * 4 * N * 3, (uint32_t)E * 4 * N * 24);
+#if PMGB_RECT_PF > 0   // the q / What blocks of the CTA PMGB_RECT_PF positions later in the walk
+  {
+    const int64_t bn = (FOLD && PMGB_RECT_REV) ? blk - PMGB_RECT_PF : blk + PMGB_RECT_PF;
+    if (t == 32 && bn >= 0 && (bn + 1) * E <= m.M) {
+      l2_prefetch(q + bn * E * NP * 4, (uint32_t)E * NP * 32);
+      if (VISC) l2_prefetch(wh + bn * E * 4 * N * 3, (uint32_t)E * 4 * N * 24);
+    }
   }
 #endif
   auto combine = [&]() {
@@ -1507,7 +1527,7 @@ k_rasm(const FrConst C, const RectMesh m, const double* __restrict__ q, const do
         o[v] = (EK == EPI_RK) ? epi_rk(ep, ce, Rv, qv[v], o1[v], o2[v], o3[v])
                               : epi_pre_k<EK>(ep, Rv, qv[v], o1[v], o2[v], o3[v]);
     }
-    stg4(out + pt * 4, o);
+    stg4_first(out + pt * 4, o);
   }
 }
 
@@ -1561,10 +1581,15 @@ static void set_rect_attrs() {
   }
 }
 
-// d.has_rect: 1 the two-kernel chain k_rgf / k_rface + k_rasm (common flux
-// folded in), 2 the four-kernel chain it replaced (kept for A/B and as a
-// cross-check).  A persistent, double-buffered k_rasm was measured slower at
-// every degree (profiles/r2/ab_chain_r2m.jsonl, "rect2p") and removed.
+// d.has_rect: 3 the two-kernel chain k_rgf / k_rface + k_rasm (common flux
+// folded in), 2 the four-kernel chain it replaced, 1 the faster of the two
+// at this degree: the four-kernel chain at p = 2 (config-2 coarse level R
+// 55.4 vs 69.1 us), the two-kernel chain elsewhere (p = 1: 34.7 vs 39.0,
+// p = 3: 85.5 vs 102.4, p = 4: 111.8 vs 114.4, p = 5: even;
+// profiles/r2/ab_chain_r2u.log).  A persistent, double-buffered k_rasm was
+// measured slower at every degree (profiles/r2/ab_chain_r2m.jsonl,
+// "rect2p") and removed.
+template <int P> constexpr bool rect_two_kernel_default() { return P != 2; }
 #ifndef PMGB_RECT_PDL0   // measured: config-2 R 113.0 -> 110.7 us, config 3 34.1 -> 32.0 us
 #define PMGB_RECT_PDL0 1
 #endif
@@ -1581,7 +1606,7 @@ static int run_rect(const RectDev& rd, const DiscDev& d, const double* q, const 
   const unsigned gf = (unsigned)((rd.nface * (P + 1) + 127) / 128);
   const unsigned ge = (unsigned)((d.M + R::EPB - 1) / R::EPB);
   const bool hx = X != nullptr;
-  const bool fold = d.has_rect != 2;
+  const bool fold = d.has_rect == 3 || (d.has_rect == 1 && rect_two_kernel_default<P>());
   if (fold && KT<KIND>::VISC) {
     if constexpr (KT<KIND>::VISC) {
 #if PMGB_RECT_PDL0   // the chain's first kernel may start while its stream predecessor drains
@@ -1665,8 +1690,8 @@ int launch_residual_rect(const RectDev& rd, const DiscDev& d, const double* q, c
 }
 
 int rect_launches(const DiscDev& d, bool has_x) {
-  if (d.has_rect == 2) return d.kind == K_NS ? 4 : 3;
   (void)has_x;
+  if (d.has_rect == 2 || (d.has_rect == 1 && d.p == 2)) return d.kind == K_NS ? 4 : 3;
   return 2;
 }
 

@@ -188,12 +188,13 @@ class Discretization:
         csrc/fr_rect.cu; chosen automatically when every element
         qualifies) or "general" (bilinear elements, csrc/fr_kernels.cu).
         ``want`` switches an eligible context (for A/B runs and tests);
-        "rect4" is the four-kernel rectangle chain "rect" replaced."""
-        code = {None: -1, "general": 0, "rect": 1, "rect4": 2}[want]
+        "rect2" / "rect4" pin the two- / four-kernel rectangle chain
+        ("rect" takes the faster one per degree)."""
+        code = {None: -1, "general": 0, "rect": 1, "rect4": 2, "rect2": 3}[want]
         r = load().pmgb_disc_residual_path(self._h, code)
         if r < 0:
             raise RuntimeError("residual_path: invalid context")
-        return {0: "general", 1: "rect", 2: "rect4"}[r]
+        return {0: "general", 1: "rect", 2: "rect4", 3: "rect2"}[r]
 
     # -- host-side conveniences ------------------------------------------------
 

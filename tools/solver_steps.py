@@ -5,7 +5,7 @@
               e.g. esdirk3:rk-ej:50:1.5:1-2:0.25/0.5/1  (stages '/'-separated)
     env: NX (mesh override), MAX_PTC, RESTARTS (caps for exploration runs),
          DT_SCALE (multiplies the case's dt), BLOCK_PRECISION (fp64 | fp32),
-         DTAU_SCALE (ptc.dtau_init = DTAU_SCALE x dt)
+         DTAU_SCALE (ptc.dtau_init = DTAU_SCALE x dt), PTC_RTOL (default 1e-4)
 
 Prints one JSON line per variant: per-step device wall time (synchronised),
 PTC / GMRES iteration counts, peak device memory.  Used for the DESIGN.md
@@ -46,7 +46,8 @@ def main():
         cfg = {"case.precond": "pmg", "pmg.levels": c.levels, "pmg.smooth": smooth, "pmg.smoother": smoothers,
                "pmg.rk.stages": stages,
                "pmg.smoother_shift": shift, "pmg.rk.cfl": cfl, "gmres.kdim": c.kdim, "gmres.rtol": 1e-3,
-               "ptc.dtau_init": c.dt * float(os.environ.get("DTAU_SCALE", 1.0)), "ptc.rtol": 1e-4,
+               "ptc.dtau_init": c.dt * float(os.environ.get("DTAU_SCALE", 1.0)),
+               "ptc.rtol": float(os.environ.get("PTC_RTOL", 1e-4)),
                "ptc.max_iters": int(os.environ.get("MAX_PTC", 100)),
                "gmres.max_restarts": int(os.environ.get("RESTARTS", 10)),
                "pmg.block_precision": os.environ.get("BLOCK_PRECISION", "fp64")}

@@ -6,8 +6,9 @@ paths' R.
 
     python tools/time_rect.py [configs...]      (default: 2 4; "2:p2" = config 2's mesh at degree 2)
 
-"rect" is the two-kernel chain (k_rgf + k_rasm), "rect4" the four-kernel
-chain it replaced (k_rface + k_rgrad + k_rfc + k_rasm).  RECT_PATHS selects.
+"rect2" is the two-kernel chain (k_rgf + k_rasm), "rect4" the four-kernel
+chain it replaced (k_rface + k_rgrad + k_rfc + k_rasm), "rect" the default
+(the faster of the two per degree).  RECT_PATHS selects.
 """
 
 import json
