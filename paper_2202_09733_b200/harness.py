@@ -35,7 +35,7 @@ DEFAULTS = {
     "pmg.levels": "3-1", "pmg.smooth": "2", "pmg.smoother": "ej", "pmg.switch_after": None,
     "pmg.mbnk.rtol": 0.1, "pmg.mbnk.maxiter": 5, "pmg.smoother_shift": 0.0,
     "pmg.rk.cfl": 1.5, "pmg.rk.stages": "0.25,0.3333333333333333,0.5,1.0", "pmg.block_precision": "fp64",
-    "case.precond": "ej",
+    "pmg.graph": "auto", "case.precond": "ej",
 }
 
 
@@ -50,7 +50,8 @@ def pmg_precond_config(cfg) -> "pmg_mod.PmgPrecondConfig":
                                     smoother_shift=cfg["pmg.smoother_shift"],
                                     rk_cfl=float(cfg["pmg.rk.cfl"]),
                                     rk_alphas=alphas,
-                                    block_precision=str(cfg["pmg.block_precision"]))
+                                    block_precision=str(cfg["pmg.block_precision"]),
+                                    graph=str(cfg["pmg.graph"]))
 
 
 @dataclass
@@ -234,7 +235,7 @@ SCHEMA = {
     "pmg.levels": (str, "3-1"), "pmg.smooth": (str, "2"), "pmg.smoother": (str, "ej"),
     "pmg.switch_after": (int, None), "pmg.mbnk.rtol": (float, 0.1), "pmg.mbnk.maxiter": (int, 5),
     "pmg.smoother_shift": (float, 0.0), "pmg.rk.cfl": (float, 1.5),
-    "pmg.rk.stages": (str, "0.25,0.3333333333333333,0.5,1.0"), "pmg.block_precision": (str, "fp64"),
+    "pmg.rk.stages": (str, "0.25,0.3333333333333333,0.5,1.0"), "pmg.block_precision": (str, "fp64"), "pmg.graph": (str, "auto"),
     "adapt.enable": (_as_bool, False), "adapt.variable": (str, "momentum-x"), "adapt.nu_max": (float, 0.2),
     "adapt.nu_min": (float, 0.001), "adapt.p_min": (int, 1), "adapt.p_max": (int, 4),
     "adapt.every_n_steps": (int, 10),
@@ -248,6 +249,7 @@ _VALID_CHOICES = {
     "case.solver": ("jfnk", "pmg-solver"),
     "case.precond": ("ej", "pmg", "none"),
     "pmg.block_precision": ("fp64", "fp32"),
+    "pmg.graph": ("auto", "on", "off"),
     "case.init": ("free-stream", "zero"),
     "ooa.mode": ("spatial", "temporal"),
     "ooa.case": ("advected-sine", "vortex"),

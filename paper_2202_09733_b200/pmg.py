@@ -86,10 +86,15 @@ class PmgPrecondConfig:
     # storage of the EJ block factors: fp64 (reference) or fp32 (option:
     # FP32 storage, FP64 arithmetic -- halves the EJ apply's HBM bytes)
     block_precision: str = "fp64"
+    # precondition() as a CUDA-graph replay of its V-cycles: "auto" (meshes up
+    # to PmgContext.GRAPH_AUTO_DOFS unknowns, where the cycle is launch-bound), "on", "off"
+    graph: str = "auto"
 
     def __post_init__(self):
         if self.block_precision not in ("fp64", "fp32"):
             raise ValueError(f"unknown block precision {self.block_precision!r}")
+        if self.graph not in ("auto", "on", "off"):
+            raise ValueError(f"unknown graph mode {self.graph!r}")
         if self.m_max < 1:
             raise ValueError("m_max must be >= 1")
         if self.rk_cfl <= 0.0 or not self.rk_alphas:
@@ -207,9 +212,18 @@ class PmgContext:
         self.R_outer = None
         self.S_outer = None
         self.shift = 0.0
+        # graph replay of precondition(): captured on the second call after a
+        # prepare() (the first runs eagerly: lazy one-time setup in the library
+        # must not happen under capture), dropped by the next prepare()
+        self._graph = None
+        self._graph_in = self._graph_out = None
+        self._warm = False
+        self.graph_replays = 0
 
     def prepare(self, q, shift: float):
         """Freeze the linearisation state and assemble the EJ blocks."""
+        self._graph = None   # the cycle's arguments (state, shift, factors) change
+        self._graph_in = self._graph_out = None
         q = to_device(q, self.disc.device)
         self.q_outer = q.clone()
         self.R_outer = self.levels[0].disc.eval(self.q_outer, _lib.EPI_R)
@@ -280,17 +294,56 @@ class PmgContext:
         lev.q = T.prolong_add(coarse.q, qb, lev.q.clone())
         self._smooth(k)
 
-    def precondition(self, X):
-        """Approximate (s I - dR/dq)^-1 X by pseudo-time V-cycles (pmg.py:280-298)."""
-        is_np = not isinstance(X, torch.Tensor)
-        X = to_device(X, self.disc.device)
+    # measured (tools/time_graph.py, profiles/r2/time_graph_r2v.jsonl): config 1 (16 K unknowns) 74.9 ->
+    # 65.6 ms per step; even at 0.1-0.4 M; slower from 1.6 M (a capture per prepare(), the output copy)
+    GRAPH_AUTO_DOFS = 65_536
+
+    def _graphable(self) -> bool:
+        """The V-cycles of precondition() are a fixed launch sequence between
+        two prepare() calls when every level smooths with EJ or RK (MBNK runs
+        a host-driven inner GMRES) on an unpartitioned mesh (the halo refresh
+        is a host-issued collective)."""
+        if self.cfg.graph == "off" or active_partition() is not None:
+            return False
+        h = self.cfg.hierarchy
+        if h.switch_after is not None or any(s not in ("ej", "rk") for s in h.smoothers):
+            return False
+        return self.cfg.graph == "on" or self.disc.n_dofs <= self.GRAPH_AUTO_DOFS
+
+    def _cycles(self, X) -> torch.Tensor:
+        """m_max V-cycles on (s I - dR/dq) e = X from e = 0; returns e."""
         fine = self.levels[0]
         fine.q = self.q_outer.clone()
         fine.S_base = self.S_outer
         fine.S_extra = X
+        for _ in range(self.cfg.m_max):
+            self.vcycle()
+        return lincomb((1.0, -1.0), (fine.q, self.q_outer))
+
+    def precondition(self, X):
+        """Approximate (s I - dR/dq)^-1 X by pseudo-time V-cycles (pmg.py:280-298).
+        On small meshes the cycle is launch-bound (≈ 30 kernels of a few µs),
+        so between two prepare() calls it is captured once into a CUDA graph
+        and replayed: the same kernels in the same order, bit for bit."""
+        is_np = not isinstance(X, torch.Tensor)
+        X = to_device(X, self.disc.device)
+        fine = self.levels[0]
+        replay = self._graphable() and self._warm
+        if replay:
+            if self._graph is None:
+                self._graph_in = torch.empty_like(X)
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):   # a private pool per capture; prepare() drops it with the graph
+                    self._graph_out = self._cycles(self._graph_in)
+                self._graph = g
+            self._graph_in.copy_(X)
+            self._graph.replay()
+            self.graph_replays += 1
+            Y = self._graph_out
+        else:
+            Y = self._cycles(X)
+            self._warm = True
         try:
-            for _ in range(self.cfg.m_max):
-                self.vcycle()
             raise_status()
         except NonPhysicalStateError:
             self.fallbacks += 1
@@ -299,7 +352,8 @@ class PmgContext:
             else:
                 Y = fine.blocks.apply(X)
         else:
-            Y = lincomb((1.0, -1.0), (fine.q, self.q_outer))
+            if replay:
+                Y = Y.clone()   # the graph's output buffer is rewritten by the next replay
         return Y.cpu().numpy() if is_np else Y
 
 
