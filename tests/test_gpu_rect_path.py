@@ -187,3 +187,59 @@ def test_chain_variants_agree(cuda, p, kind):
         # the default is one of the two, bit for bit (the four-kernel chain at p = 2)
         same = out["rect4"] if p == 2 else out["rect2"]
         assert all(torch.equal(a, b) for a, b in zip(out["rect"], same))
+
+
+def _renumber(mesh, perm):
+    """The same mesh with element e renamed perm[e] (face roles L / R kept)."""
+    M = mesh.n_elements
+    inv = np.empty(M, dtype=np.int64)
+    inv[perm] = np.arange(M)
+    elements = mesh.elements[inv]
+    itf = mesh.interior_faces.copy()
+    itf[:, 0], itf[:, 2] = perm[itf[:, 0]], perm[itf[:, 2]]
+    itf = itf[np.lexsort((itf[:, 1], itf[:, 0]))]
+    bf = mesh.boundary_faces.copy()
+    bf[:, 0] = perm[bf[:, 0]]
+    order = np.lexsort((bf[:, 1], bf[:, 0]))
+    tags = tuple(mesh.boundary_tags[i] for i in order)
+    return mm.Mesh(mesh.nodes, elements, itf, bf[order], tags)
+
+
+@pytest.mark.parametrize("p", [2, 3, 4, 5])
+def test_arbitrary_element_numbering(cuda, p):
+    """The rectangle kernels take the connectivity as a gathered list (the
+    reference's face batches, spatial.py:521-526), not a structured grid: a
+    random renumbering of the elements scatters every CTA's element run over
+    the mesh -- neighbours inside and outside a CTA's run in every pattern, the
+    shared-memory trace hand-over on arbitrary pairs, self-neighbours through
+    the periodic wrap -- and must give the same R (against the oracle on the
+    renumbered mesh, and the renumbered result of the ordered mesh bit for
+    bit: the per-element arithmetic does not depend on the numbering)."""
+    yn = np.array([0.0, 0.02, 0.07, 0.2, 0.45, 0.7, 1.0])
+    rng = np.random.default_rng(40 + p)
+    for m0 in (mm.generate_channel(29, 6, 3.0, yn, bottom="wall-isothermal", top="wall-adiabatic"),
+               mm.generate_box(13, 11, 2.0, 1.5, periodic=True),
+               mm.generate_box(1, 7, 1.0, 3.0, periodic=True)):
+        M = m0.n_elements
+        perm = rng.permutation(M)
+        m1 = _renumber(m0, perm)
+        eqn = EquationSpec(kind="navier-stokes", mach=0.3, reynolds=150.0)
+        d0, d1 = Discretization(m0, p, eqn), Discretization(m1, p, eqn)
+        assert d0.residual_path() == "rect" and d1.residual_path() == "rect"
+        o1 = OracleDisc(m1, p, eqn)
+        npe = d0.n_dofs // M
+        q0 = o1.free_stream_field() * (1 + 0.03 * rng.standard_normal(d0.n_dofs))
+        q1 = np.empty_like(q0)
+        q1.reshape(M, npe)[perm] = q0.reshape(M, npe)
+        X0 = rng.standard_normal(d0.n_dofs)
+        X1 = np.empty_like(X0)
+        X1.reshape(M, npe)[perm] = X0.reshape(M, npe)
+        t = lambda a: torch.as_tensor(a, device="cuda")  # noqa: E731
+        for path in ("rect2", "rect4", "rect"):
+            d0.residual_path(path), d1.residual_path(path)
+            R0, R1 = d0.residual(t(q0)), d1.residual(t(q1))
+            assert _rel(R1, o1.residual(q1)) <= 1e-12
+            assert torch.equal(R1.view(M, npe)[t(perm)], R0.view(M, npe))
+            J0 = d0.eval(t(q0), _lib.EPI_JV, X=t(X0), eps=1e-6, s=1.5, R0=R0)
+            J1 = d1.eval(t(q1), _lib.EPI_JV, X=t(X1), eps=1e-6, s=1.5, R0=R1)
+            assert torch.equal(J1.view(M, npe)[t(perm)], J0.view(M, npe))
