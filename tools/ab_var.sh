@@ -12,7 +12,7 @@ import sys, json
 for l in sys.stdin:
     try: d = json.loads(l)
     except Exception: print(l.rstrip()); continue
-    print(' '.join([f\"c{d['config']}\"] + [f\"{k}: R {v['r_us']:.1f} Jv {v['jv_us']:.1f}\" for k, v in d.items() if isinstance(v, dict)]))
+    print(' '.join([f\"c{d['config']}\"] + [f\"{k}: R {v['r_us']:.1f} Jv {v['jv_us']:.1f} stageJv {v.get('stage_jv_us', 0):.1f} defect {v.get('defect_us', 0):.1f}\" for k, v in d.items() if isinstance(v, dict)]))
 " | tee -a gpurun_out/ab_var.log
   done
 done

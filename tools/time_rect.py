@@ -64,12 +64,19 @@ def main():
             d.residual_path(path)
             r = lambda i: d.eval(qs[i % nb], _lib.EPI_R, Rs[i % nb])  # noqa: E731
             j = lambda i: d.eval(qs[i % nb], _lib.EPI_JV, Rs[i % nb], X=X, eps=1e-6, s=3.7, R0=R0)  # noqa: E731
+            # the PTC matvec of a stage (X/dtau + (F(q + eps X) - Fk)/eps, three divisions per value)
+            sj = lambda i: d.eval(qs[i % nb], _lib.EPI_STAGE_JV, Rs[i % nb], X=X, eps=1e-6, adt=0.0123, dtau=0.37,  # noqa: E731
+                                  R0=R0, E=q0)
+            df = lambda i: d.eval(qs[i % nb], _lib.EPI_DEFECT, Rs[i % nb], s=3.7, Sb=R0, Se=X)  # noqa: E731
             for i in range(3):
                 r(i)
                 j(i)
-            tr, tj = ev(r, reps), ev(j, reps)
+                sj(i)
+                df(i)
+            tr, tj, ts, td = ev(r, reps), ev(j, reps), ev(sj, reps), ev(df, reps)
             outs[path] = d.residual(q0).cpu().numpy()
-            rec[path] = {"r_us": tr * 1e6, "r_gdofs": n / tr / 1e9, "jv_us": tj * 1e6, "jv_gdofs": n / tj / 1e9}
+            rec[path] = {"r_us": tr * 1e6, "r_gdofs": n / tr / 1e9, "jv_us": tj * 1e6, "jv_gdofs": n / tj / 1e9,
+                         "stage_jv_us": ts * 1e6, "defect_us": td * 1e6}
         if "general" in outs:
             a, b = outs["rect"], outs["general"]
             rec["rect_vs_general"] = float(np.max(np.abs(a - b)) / np.max(np.abs(b)))
