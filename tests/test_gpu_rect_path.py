@@ -243,3 +243,19 @@ def test_arbitrary_element_numbering(cuda, p):
             J0 = d0.eval(t(q0), _lib.EPI_JV, X=t(X0), eps=1e-6, s=1.5, R0=R0)
             J1 = d1.eval(t(q1), _lib.EPI_JV, X=t(X1), eps=1e-6, s=1.5, R0=R1)
             assert torch.equal(J1.view(M, npe)[t(perm)], J0.view(M, npe))
+
+
+def test_misaligned_operands_are_rejected(cuda):
+    """The rectangle kernels move whole points (4 doubles, 256-bit accesses): an
+    array that does not start on a 32-byte boundary is refused with a clear
+    error instead of faulting."""
+    c = cases.config(1, nx=4)
+    d = Discretization(c.mesh, c.p, c.eqn)
+    n = d.n_dofs
+    buf = torch.zeros(n + 1, dtype=torch.float64, device="cuda")
+    q = torch.as_tensor(c.q0, device="cuda")
+    buf[1:].copy_(q)
+    with pytest.raises(_lib.PmgbError, match="32-byte aligned"):
+        d.residual(buf[1:])
+    with pytest.raises(_lib.PmgbError, match="32-byte aligned"):
+        d.eval(q, _lib.EPI_JV, X=buf[1:], eps=1e-6, s=1.0, R0=q)
