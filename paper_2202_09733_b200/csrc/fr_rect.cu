@@ -293,6 +293,11 @@ __device__ __forceinline__ void epi_load4_k(const Epi& ep, int64_t i, double* o1
 // L2 prefetch of the epilogue operands of a CTA's element block (issued at
 // kernel start: the operands are inputs of the whole chain), so that the
 // loads at the end of the kernel find them in L2
+// epilogue operand request distance in points (0: at the point itself); measured
+// (profiles/r2/ab_epd_r2x.log): 1 takes 1-2 % off the Jv / stage-Jv / defect forms
+#ifndef PMGB_RECT_EPD
+#define PMGB_RECT_EPD 1
+#endif
 #ifndef PMGB_RECT_EPF   // measured: config-2 Jv 166.4 -> 161.3 us (profiles/r2/ab_pdl0_epf_r2p.log)
 #define PMGB_RECT_EPF 1
 #endif
@@ -1497,7 +1502,15 @@ k_rasm(const FrConst C, const RectMesh m, const double* __restrict__ q, const do
     for (int v = 0; v < 4; ++v) sY[tl<N, 4>(el, i, v * N + a)] = xx[v][i];
   __syncthreads();
   if (!live) return;
-  // column a: fy and X_xi of the column, faces 2 / 0, X_eta, R, epilogue
+  // column a: fy and X_xi of the column, faces 2 / 0, X_eta, R, epilogue.
+  // The epilogue operands of point i + EPD are requested before point i is
+  // formed and stored (the first EPD points before the column pass), so
+  // their latency overlaps the arithmetic instead of heading every point.
+  constexpr int EPD = (EK == EPI_R) ? 0 : (PMGB_RECT_EPD < N ? PMGB_RECT_EPD : N);
+  double o1[N][4], o2[N][4], o3[N][4];
+  auto epi_req = [&](int i) { epi_load4_k<EK>(ep, (e * NP + i * N + a) * 4, o1[i], o2[i], o3[i]); };
+#pragma unroll
+  for (int i = 0; i < EPD; ++i) epi_req(i);
   double fyc[4][N];
   {
     const double* blk = sX + tl<N, 4>(el, a, 0);
@@ -1516,16 +1529,17 @@ k_rasm(const FrConst C, const RectMesh m, const double* __restrict__ q, const do
     const int64_t pt = e * NP + i * N + a;
     double qv[4] = {0, 0, 0, 0};
     if constexpr (NEEDQ) lds4(sQ + ((el * N + i) * N + a) * 4, qv);
-    double o[4], o1[4], o2[4], o3[4];
-    if constexpr (EK != EPI_R) epi_load4_k<EK>(ep, pt * 4, o1, o2, o3);   // operands as 256-bit loads
+    double o[4];
+    if constexpr (EK != EPI_R)
+      if (i + EPD < N) epi_req(i + EPD);   // operands as 256-bit loads
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
       const double Rv = -(rg.x * bx[v * N + i] + rg.y * xe[v][i]);
       if constexpr (EK == EPI_R)
         o[v] = Rv;
       else
-        o[v] = (EK == EPI_RK) ? epi_rk(ep, ce, Rv, qv[v], o1[v], o2[v], o3[v])
-                              : epi_pre_k<EK>(ep, Rv, qv[v], o1[v], o2[v], o3[v]);
+        o[v] = (EK == EPI_RK) ? epi_rk(ep, ce, Rv, qv[v], o1[i][v], o2[i][v], o3[i][v])
+                              : epi_pre_k<EK>(ep, Rv, qv[v], o1[i][v], o2[i][v], o3[i][v]);
     }
     stg4_first(out + pt * 4, o);
   }
