@@ -25,8 +25,7 @@
 // neighbours' q lines (k_rgf) and the four face records of a thread
 // (k_rasm):
 //   k_rgf    traces on the four faces (own: from the staged q block;
-//            neighbours of the CTA's own element run: handed over through
-//            shared memory; other neighbours: gathered from q), the BR1
+//            neighbours: gathered from q), the BR1
 //            common value What into the element's own What block, the
 //            interface flux F (Roe / Rusanov) once per face by its L side,
 //            BR1 gradients by line passes (rows gx, columns gy, one
@@ -107,8 +106,8 @@ constexpr int FREC = PMGB_RECT_REC12 ? 12 : 8;
 
 // CTA width target of the element kernels: 64 threads (12 elements at p = 4,
 // six CTAs per SM) interleave the CTAs' load and compute phases more finely than
-// 128 (config-2 R 114.5 -> 111.8 us; 96: 112.5, 48: 114.7, 32: 114.6;
-// profiles/r2/ab_cta_width_r2t.log)
+// 128 (config-2 R 105.9 -> 105.1 us, config 4 87.3 -> 85.9; 96: 108.6 / 86.0, 48: 117.2 / 91.5;
+// profiles/r2/ab_xch_r2n.log, ab_cta_width_r2t.log)
 #ifndef PMGB_RECT_TH
 #define PMGB_RECT_TH 64
 #endif
@@ -121,15 +120,8 @@ constexpr int FREC = PMGB_RECT_REC12 ? 12 : 8;
 #ifndef PMGB_RECT_REV
 #define PMGB_RECT_REV 1
 #endif
-#ifndef PMGB_RECT_XCH_MASK   // degrees whose k_rgf hands traces over inside the CTA (bit P)
-#define PMGB_RECT_XCH_MASK 0x14
-#endif
 template <int P> struct RC {
   static constexpr int N = P + 1, NP = N * N;
-  // k_rgf: neighbours inside the CTA's element run pass their traces
-  // through shared memory instead of being gathered again (measured per
-  // degree, profiles/r2/ab_xch_r2n.log: faster at p = 2 and 4)
-  static constexpr bool XCH = ((PMGB_RECT_XCH_MASK >> P) & 1) != 0;
   static constexpr int EPB = PMGB_RECT_TH / N;  // elements per CTA
   static constexpr int TH = EPB * N;   // one thread per (element, line)
   // line block strides in doubles: >= 3N (gradient passes) / 4N (flux
@@ -1008,8 +1000,7 @@ template <int P, bool HASX> struct GFL {
   static constexpr int BUF = R::EPB * TL<R::N, 3>::S;
   static constexpr int A = 2 * BUF, B = HASX ? R::QD : 0;
   static constexpr int STAGE = A > B ? A : B;
-  static constexpr int OFF_T = R::QD + STAGE;
-  static constexpr int OFF_BAR = OFF_T + (R::XCH ? R::FD : 0);
+  static constexpr int OFF_BAR = R::QD + STAGE;
   static constexpr size_t BYTES = sizeof(double) * (OFF_BAR + 2);
 };
 
@@ -1024,7 +1015,6 @@ k_rgf(const FrConst C, const RectMesh m, const double* __restrict__ q, const dou
   double* sQ = sm;
   double* sX = sm + R::QD;            // X block; then W, then gx (column blocks)
   double* sY = sm + R::QD + L::BUF;   // gy (row blocks)
-  double* sT = sm + L::OFF_T;         // own traces [el][f][k][4]
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::OFF_BAR);
   const int t = threadIdx.x;
   const int el = t / N, a = t % N;  // row a of element el; also column a
@@ -1053,21 +1043,17 @@ k_rgf(const FrConst C, const RectMesh m, const double* __restrict__ q, const dou
   FaceStat fs;
   face_stat<N>(m, e, a, live, fs);
   const double2 rg = live ? __ldg(m.rgeo + e) : make_double2(0.0, 0.0);
-  // the neighbours' traces at the thread's four face points: gathered
-  // from q when the neighbour belongs to another CTA; a neighbour of this
-  // CTA's own element run hands over the trace it forms itself (below) --
-  // the same sum in the same order
+  // the neighbours' traces at the thread's four face points, gathered
+  // from q (issued before the q block is awaited)
   double qn[4][4];
   double2 nrm[4];
-  bool inb[4];
 #pragma unroll
   for (int f = 0; f < 4; ++f) {
     qn[f][0] = qn[f][1] = qn[f][2] = qn[f][3] = 1.0;
     nrm[f] = make_double2(0.0, 0.0);
-    inb[f] = R::XCH && fs.nb[f] >= e0 && fs.nb[f] < e0 + ne;
     if (live) {
       nrm[f] = __ldg(reinterpret_cast<const double2*>(m.geom + e * 20 + 8 + 2 * f));
-      if (fs.nb[f] >= 0 && !inb[f]) {
+      if (fs.nb[f] >= 0) {
         const int k = (f >= 2) ? N - 1 - a : a;
         face_trace<P, HASX>(C, q, X, eps, fs.nb[f], lk_face(fs.fl[f]), lk_rev(fs.fl[f]) ? N - 1 - k : k, qn[f]);
       }
@@ -1102,23 +1088,6 @@ k_rgf(const FrConst C, const RectMesh m, const double* __restrict__ q, const dou
       qo[2][v] += C.eR[i] * x[v];
       qo[0][v] += C.eL[i] * x[v];
     }
-  }
-  // hand the own traces to the neighbours inside the CTA
-  if constexpr (R::XCH) {
-#pragma unroll
-    for (int f = 0; f < 4; ++f) {
-      double* d = sT + ((el * 4 + f) * N + ((f >= 2) ? N - 1 - a : a)) * 4;
-      reinterpret_cast<double2*>(d)[0] = make_double2(qo[f][0], qo[f][1]);
-      reinterpret_cast<double2*>(d)[1] = make_double2(qo[f][2], qo[f][3]);
-    }
-    __syncthreads();
-#pragma unroll
-    for (int f = 0; f < 4; ++f)
-      if (live && inb[f]) {
-        const int k = (f >= 2) ? N - 1 - a : a;
-        const int kk = lk_rev(fs.fl[f]) ? N - 1 - k : k;
-        lds4(sT + (((int)(fs.nb[f] - e0) * 4 + lk_face(fs.fl[f])) * N + kk) * 4, qn[f]);
-      }
   }
   // common values; the interface flux on the faces this element owns
   double whv[4][3], uv[4][2], Fk[4][4];
@@ -1598,11 +1567,12 @@ static void set_rect_attrs() {
 // d.has_rect: 3 the two-kernel chain k_rgf / k_rface + k_rasm (common flux
 // folded in), 2 the four-kernel chain it replaced, 1 the faster of the two
 // at this degree: the four-kernel chain at p = 2 (config-2 coarse level R
-// 55.4 vs 69.1 us), the two-kernel chain elsewhere (p = 1: 34.7 vs 39.0,
-// p = 3: 85.5 vs 102.4, p = 4: 111.8 vs 114.4, p = 5: even;
-// profiles/r2/ab_chain_r2u.log).  A persistent, double-buffered k_rasm was
-// measured slower at every degree (profiles/r2/ab_chain_r2m.jsonl,
-// "rect2p") and removed.
+// 55.4 vs 63.8 us), the two-kernel chain elsewhere (p = 1: 34.7 vs 39.0,
+// p = 3: 85.8 vs 102.7, p = 4: 105.1 vs 114.8, p = 5: even;
+// profiles/r2/ab_chain_r2u.log).  Measured slower and removed: a
+// persistent, double-buffered k_rasm (profiles/r2/ab_chain_r2m.jsonl,
+// "rect2p") and a shared-memory hand-over of the traces between
+// neighbours of one CTA in k_rgf (profiles/r2/ab_xch_r2n.log).
 template <int P> constexpr bool rect_two_kernel_default() { return P != 2; }
 #ifndef PMGB_RECT_PDL0   // measured: config-2 R 113.0 -> 110.7 us, config 3 34.1 -> 32.0 us
 #define PMGB_RECT_PDL0 1
