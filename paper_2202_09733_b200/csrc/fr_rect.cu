@@ -131,7 +131,11 @@ template <int P> struct RC {
   static constexpr int WD = EPB * 4 * N * 3;  // of a What block
   static constexpr int FD = EPB * 4 * N * 4;  // of an Fc block
   // CTAs per SM the register target is set for
+#ifdef PMGB_RECT_MINB   // experiment builds: resident CTAs per SM at every degree
+  static constexpr int MINB = PMGB_RECT_MINB;
+#else
   static constexpr int MINB = (P == 5 ? 2 : (P >= 3 ? 3 : 4)) * (128 / PMGB_RECT_TH);
+#endif
 };
 
 // q (+ eps X with the reference's rounding, newton_krylov.py:76) of point pt
