@@ -111,6 +111,21 @@ constexpr int FREC = PMGB_RECT_REC12 ? 12 : 8;
 #ifndef PMGB_RECT_TH
 #define PMGB_RECT_TH 64
 #endif
+// k_rgf: a neighbour that sits in the CTA's own staged q block is read from
+// shared memory instead of being gathered from global memory (same operands,
+// same order: bitwise the gathered trace)
+// -1: per degree (RC<P>::NBS); 0 off, 1 in the Jv forms only, 2 always
+#ifndef PMGB_RECT_NBS
+#define PMGB_RECT_NBS -1
+#endif
+// k_rgf / k_rasm: rows of the staged q (and X) block padded by this many
+// doubles (one bulk copy per row): at the raw row stride of N * 32 B the line
+// threads' 128-bit row reads collide in the banks (2-way at p = 4, 8-way at
+// p = 3, 4-way at p = 5); + 16 B makes every quarter-warp conflict-free
+// -1: per degree (RC<P>::QPAD)
+#ifndef PMGB_RECT_QPAD
+#define PMGB_RECT_QPAD -1
+#endif
 #ifndef PMGB_RECT_PF   // L2 prefetch distance in CTAs (0: off; 888 and 1776 measured slower, ab_cta_width_r2t.log)
 #define PMGB_RECT_PF 0
 #endif
@@ -127,7 +142,12 @@ template <int P> struct RC {
   // line block strides in doubles: >= 3N (gradient passes) / 4N (flux
   // passes), even, an odd number of 16-byte units
 
-  static constexpr int QD = EPB * NP * 4;   // doubles of a q block
+  // measured per degree (profiles/r2/ab_qpad_nbs_r2y.log): one bulk copy per
+  // row costs more than the 2-way conflicts it removes at p = 4
+  static constexpr int QPAD = PMGB_RECT_QPAD >= 0 ? PMGB_RECT_QPAD : (P == 3 ? 2 : 0);
+  static constexpr int NBS = PMGB_RECT_NBS >= 0 ? PMGB_RECT_NBS : (P == 3 ? 2 : (P >= 4 ? 1 : 0));
+  static constexpr int RS = N * 4 + QPAD;  // row stride of a staged q block (k_rgf / k_rasm)
+  static constexpr int QD = EPB * N * RS;   // doubles of a q block
   static constexpr int WD = EPB * 4 * N * 3;  // of a What block
   static constexpr int FD = EPB * 4 * N * 4;  // of an Fc block
   // CTAs per SM the register target is set for
@@ -529,6 +549,71 @@ __device__ __forceinline__ void lds4(const double* p, double* o) {
   o[1] = a.y;
   o[2] = b.x;
   o[3] = b.y;
+}
+
+// the CTA's q (+ X) rows into the (padded) staged block: one bulk copy for the
+// block, or one per row by its line thread when the rows are padded
+template <int P, bool HASX, bool FIRST>
+__device__ __forceinline__ void stage_q(double* sQ, double* sX, const double* __restrict__ q,
+                                        const double* __restrict__ X, int64_t e0, int ne, uint64_t* bar) {
+  using R = RC<P>;
+  constexpr int N = R::N, NP = R::NP;
+  const int t = threadIdx.x;
+  const uint32_t qbytes = (uint32_t)ne * NP * 32;
+  if (t == 0) mbar_expect(bar, HASX ? 2 * qbytes : qbytes);
+  if constexpr (R::QPAD > 0) {
+    if (t < ne * N) {
+      const double* src = q + (e0 * NP + (int64_t)t * N) * 4;
+      if (FIRST) bulk_g2s_first(sQ + t * R::RS, src, N * 32, bar);
+      else bulk_g2s(sQ + t * R::RS, src, N * 32, bar);
+      if (HASX) bulk_g2s(sX + t * R::RS, X + (e0 * NP + (int64_t)t * N) * 4, N * 32, bar);
+    }
+  } else if (t == 0) {
+    if (FIRST) bulk_g2s_first(sQ, q + e0 * NP * 4, qbytes, bar);
+    else bulk_g2s(sQ, q + e0 * NP * 4, qbytes, bar);
+    if (HASX) bulk_g2s(sX, X + e0 * NP * 4, qbytes, bar);
+  }
+}
+// q + eps X in place, row by row (the rows may be padded)
+template <int P>
+__device__ __forceinline__ void form_qp_rows(double* sQ, const double* sXb, double eps, int ne) {
+  using R = RC<P>;
+  if constexpr (R::QPAD > 0) {
+    const int t = threadIdx.x;
+    if (t < ne * R::N) {
+#pragma unroll
+      for (int i = 0; i < R::N * 4; i += 2) {
+        double2 a = *reinterpret_cast<const double2*>(sQ + t * R::RS + i);
+        const double2 x = *reinterpret_cast<const double2*>(sXb + t * R::RS + i);
+        a.x = __dadd_rn(a.x, __dmul_rn(eps, x.x));
+        a.y = __dadd_rn(a.y, __dmul_rn(eps, x.y));
+        *reinterpret_cast<double2*>(sQ + t * R::RS + i) = a;
+      }
+    }
+  } else {
+    form_qp<R::TH>(sQ, sXb, eps, ne * R::NP * 4);
+  }
+}
+
+// face_trace() on a staged q block (q + eps X already formed in place)
+template <int P>
+__device__ __forceinline__ void face_trace_s(const FrConst& C, const double* sQ, int el, int f, int k, double* tr) {
+  constexpr int N = P + 1, NP = N * N;
+  const bool col = (f == 0 || f == 2);
+  const int kk = (f >= 2) ? N - 1 - k : k;
+  const int start = col ? kk : kk * N;
+  const int step = col ? N : 1;
+  const double* w = (f == 1 || f == 2) ? C.eR : C.eL;
+  tr[0] = tr[1] = tr[2] = tr[3] = 0.0;
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    double x[4];
+    const int pt = start + i * step;
+    lds4(sQ + (el * N + pt / N) * RC<P>::RS + (pt % N) * 4, x);
+    const double wi = w[i];
+#pragma unroll
+    for (int v = 0; v < 4; ++v) tr[v] += wi * x[v];
+  }
 }
 
 // face points of line thread a: [0] face 0 point a, [1] face 1 point a,
@@ -1034,12 +1119,7 @@ k_rgf(const FrConst C, const RectMesh m, const double* __restrict__ q, const dou
   // serialization) may still be writing q or reading What / the records
   pdl_wait();
   pdl_trigger();
-  const uint32_t qbytes = (uint32_t)ne * NP * 32;
-  if (t == 0) {
-    mbar_expect(bar, HASX ? 2 * qbytes : qbytes);
-    bulk_g2s(sQ, q + e0 * NP * 4, qbytes, bar);
-    if (HASX) bulk_g2s(sX, X + e0 * NP * 4, qbytes, bar);
-  }
+  stage_q<P, HASX, false>(sQ, sX, q, X, e0, ne, bar);
 #if PMGB_RECT_PF > 0
   if (t == 32 && ((int64_t)blockIdx.x + PMGB_RECT_PF + 1) * E <= m.M)
     l2_prefetch(q + ((int64_t)blockIdx.x + PMGB_RECT_PF) * E * NP * 4, (uint32_t)E * NP * 32);
@@ -1057,7 +1137,9 @@ k_rgf(const FrConst C, const RectMesh m, const double* __restrict__ q, const dou
     nrm[f] = make_double2(0.0, 0.0);
     if (live) {
       nrm[f] = __ldg(reinterpret_cast<const double2*>(m.geom + e * 20 + 8 + 2 * f));
-      if (fs.nb[f] >= 0) {
+      constexpr bool NBS = R::NBS == 2 || (R::NBS == 1 && HASX);
+      const bool ins = NBS && fs.nb[f] >= e0 && fs.nb[f] < e0 + ne;
+      if (fs.nb[f] >= 0 && !ins) {
         const int k = (f >= 2) ? N - 1 - a : a;
         face_trace<P, HASX>(C, q, X, eps, fs.nb[f], lk_face(fs.fl[f]), lk_rev(fs.fl[f]) ? N - 1 - k : k, qn[f]);
       }
@@ -1065,14 +1147,22 @@ k_rgf(const FrConst C, const RectMesh m, const double* __restrict__ q, const dou
   }
   mbar_wait(bar, 0);
   if constexpr (HASX) {
-    form_qp<R::TH>(sQ, sX, eps, ne * NP * 4);
+    form_qp_rows<P>(sQ, sX, eps, ne);
     __syncthreads();
+  }
+  if constexpr (R::NBS == 2 || (R::NBS == 1 && HASX)) {
+#pragma unroll
+    for (int f = 0; f < 4; ++f)
+      if (live && fs.nb[f] >= e0 && fs.nb[f] < e0 + ne) {
+        const int k = (f >= 2) ? N - 1 - a : a;
+        face_trace_s<P>(C, sQ, (int)(fs.nb[f] - e0), lk_face(fs.fl[f]), lk_rev(fs.fl[f]) ? N - 1 - k : k, qn[f]);
+      }
   }
   // own traces: faces 1 / 3 from row a, faces 2 / 0 from column a
   double qo[4][4];
 #pragma unroll
   for (int f = 0; f < 4; ++f) qo[f][0] = qo[f][1] = qo[f][2] = qo[f][3] = 0.0;
-  const double* row = sQ + (el * N + a) * N * 4;
+  const double* row = sQ + (el * N + a) * R::RS;
 #pragma unroll
   for (int i = 0; i < N; ++i) {
     double x[4];
@@ -1086,7 +1176,7 @@ k_rgf(const FrConst C, const RectMesh m, const double* __restrict__ q, const dou
 #pragma unroll
   for (int i = 0; i < N; ++i) {
     double x[4];
-    lds4(sQ + ((el * N + i) * N + a) * 4, x);
+    lds4(sQ + (el * N + i) * R::RS + a * 4, x);
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
       qo[2][v] += C.eR[i] * x[v];
@@ -1308,11 +1398,7 @@ k_rasm(const FrConst C, const RectMesh m, const double* __restrict__ q, const do
   }
   __syncthreads();
   const uint32_t qbytes = (uint32_t)ne * NP * 32;
-  if (t == 0) {
-    mbar_expect(bar, HASX ? 2 * qbytes : qbytes);
-    bulk_g2s_first(sQ, q + e0 * NP * 4, qbytes, bar);
-    if (HASX) bulk_g2s(sX, X + e0 * NP * 4, qbytes, bar);
-  }
+  stage_q<P, HASX, true>(sQ, sX, q, X, e0, ne, bar);
 #if PMGB_RECT_EPF
   if (t == 32) epi_prefetch<EK>(ep, e0 * NP * 4, qbytes);
 #endif
@@ -1351,10 +1437,10 @@ k_rasm(const FrConst C, const RectMesh m, const double* __restrict__ q, const do
   };
   mbar_wait(bar, 0);
   if constexpr (HASX) {
-    form_qp<R::TH>(sQ, sX, eps, ne * NP * 4);
+    form_qp_rows<P>(sQ, sX, eps, ne);
     __syncthreads();
   }
-  const double* row = sQ + (el * N + a) * N * 4;
+  const double* row = sQ + (el * N + a) * R::RS;
   double w[3][N];
   if constexpr (VISC) {
 #pragma unroll
@@ -1501,7 +1587,7 @@ k_rasm(const FrConst C, const RectMesh m, const double* __restrict__ q, const do
   for (int i = 0; i < N; ++i) {   // point (i, a)
     const int64_t pt = e * NP + i * N + a;
     double qv[4] = {0, 0, 0, 0};
-    if constexpr (NEEDQ) lds4(sQ + ((el * N + i) * N + a) * 4, qv);
+    if constexpr (NEEDQ) lds4(sQ + (el * N + i) * R::RS + a * 4, qv);
     double o[4];
     if constexpr (EK != EPI_R)
       if (i + EPD < N) epi_req(i + EPD);   // operands as 256-bit loads
