@@ -126,6 +126,14 @@ constexpr int FREC = PMGB_RECT_REC12 ? 12 : 8;
 #ifndef PMGB_RECT_QPAD
 #define PMGB_RECT_QPAD -1
 #endif
+// NS two-kernel chain: the 12-double records of a face laid out part by part
+// ([F of the N points | fl | fr]) instead of point by point, so the line
+// threads of an element touch 2 cache lines per 256-bit record access, not 4
+// (config-2 R 105.0 -> 102.8 us, Jv 142.8 -> 139.1; config 4 R 74.1 -> 71.9;
+// bitwise the same results; profiles/r2/ab_rsoa_r2y.log)
+#ifndef PMGB_RECT_RSOA
+#define PMGB_RECT_RSOA 1
+#endif
 #ifndef PMGB_RECT_PF   // L2 prefetch distance in CTAs (0: off; 888 and 1776 measured slower, ab_cta_width_r2t.log)
 #define PMGB_RECT_PF 0
 #endif
@@ -972,6 +980,12 @@ __device__ __forceinline__ void gh_combine(bool lft, const double* G, const doub
   Fc[3] = lft ? c3 : -c3;
 }
 
+// offset (doubles) of face-point record ri = slot * N + k and the stride
+// between its parts: point by point, or (NS two-kernel chain, RSOA) part by part
+template <int N>
+__device__ __forceinline__ int64_t rec_off(int ri, bool soa) {
+  return soa ? (int64_t)(ri / N) * (N * FREC) + (ri % N) * 4 : (int64_t)ri * FREC;
+}
 // One face record as a thread of the two-kernel chain holds it
 struct FaceRec {
   double a[4], b[4];   // REC12: F, fl;  else G, H
@@ -979,7 +993,8 @@ struct FaceRec {
   double c[4];         // fr
 #endif
 };
-__device__ __forceinline__ void rec_load(const double* rec, bool visc, bool interior, bool lv, FaceRec& r) {
+__device__ __forceinline__ void rec_load(const double* rec, bool visc, bool interior, bool lv, FaceRec& r,
+                                         int ps = 4) {
 #pragma unroll
   for (int v = 0; v < 4; ++v) {
     r.a[v] = r.b[v] = 0.0;
@@ -991,8 +1006,8 @@ __device__ __forceinline__ void rec_load(const double* rec, bool visc, bool inte
   ldg4c(rec, r.a);
 #if PMGB_RECT_REC12
   if (visc) {
-    ldg4c(rec + 4, r.b);
-    if (interior) ldg4c(rec + 8, r.c);
+    ldg4c(rec + ps, r.b);
+    if (interior) ldg4c(rec + 2 * ps, r.c);
   }
 #else
   if (visc && interior) ldg4c(rec + 4, r.b);
@@ -1024,13 +1039,13 @@ __device__ __forceinline__ void rec_combine(const Phys& ph, bool visc, bool bnd,
 }
 // k_rgf's side of the record: F and the one-sided viscous flux o on the own normal
 __device__ __forceinline__ void rec_put(const Phys& ph, bool bnd, int tag, bool lft, const double* F, const double* o,
-                                        double* rec) {
+                                        double* rec, int ps = 4) {
 #if PMGB_RECT_REC12
   if (lft) {
     stg4_last(rec, F);
-    stg4_last(rec + 4, o);
+    stg4_last(rec + ps, o);
   } else {
-    stg4_last(rec + 8, o);
+    stg4_last(rec + 2 * ps, o);
   }
 #else
   double r[4];
@@ -1099,6 +1114,7 @@ k_rgf(const FrConst C, const RectMesh m, const double* __restrict__ q, const dou
       double* __restrict__ wh, double* __restrict__ frec, int* __restrict__ bad) {
   using R = RC<P>;
   using L = GFL<P, HASX>;
+  constexpr bool RSOA = PMGB_RECT_RSOA && PMGB_RECT_REC12;
   constexpr int N = R::N, NP = R::NP, E = R::EPB;
   extern __shared__ __align__(128) double sm[];
   double* sQ = sm;
@@ -1319,7 +1335,8 @@ k_rgf(const FrConst C, const RectMesh m, const double* __restrict__ q, const dou
   // -fx, face 2 +fy, face 0 -fy; each side's half of the face record
   auto put = [&](int f, double* o) {
     const bool bnd = fs.nb[f] < 0;
-    rec_put(ph, bnd, lk_tag(fs.fl[f]), bnd || lk_left(fs.fl[f]), Fk[f], o, frec + (int64_t)fs.ri[f] * FREC);
+    rec_put(ph, bnd, lk_tag(fs.fl[f]), bnd || lk_left(fs.fl[f]), Fk[f], o, frec + rec_off<N>(fs.ri[f], RSOA),
+            RSOA ? 4 * N : 4);
   };
   double o[4];
   {
@@ -1373,6 +1390,7 @@ k_rasm(const FrConst C, const RectMesh m, const double* __restrict__ q, const do
   using L = AL<P, KIND, HASX, FOLD>;
   constexpr int N = R::N, NP = R::NP, E = R::EPB;
   constexpr bool VISC = KT<KIND>::VISC;
+  constexpr bool RSOA = PMGB_RECT_RSOA && PMGB_RECT_REC12 && VISC && FOLD;
   extern __shared__ __align__(128) double sm[];
   double* sQ = sm;
   double* sX = sm + R::QD;            // X block; then W, then fy (column blocks)
@@ -1419,7 +1437,8 @@ k_rasm(const FrConst C, const RectMesh m, const double* __restrict__ q, const do
     // the four face records (fc here is the face-record array), gathered
     // while the q block is in flight
 #pragma unroll
-    for (int f = 0; f < 4; ++f) rec_load(fc + (int64_t)fs.ri[f] * FREC, VISC, fs.nb[f] >= 0, live, rc[f]);
+    for (int f = 0; f < 4; ++f)
+      rec_load(fc + rec_off<N>(fs.ri[f], RSOA), VISC, fs.nb[f] >= 0, live, rc[f], RSOA ? 4 * N : 4);
   }
 #if PMGB_RECT_PF > 0   // the q / What blocks of the CTA PMGB_RECT_PF positions later in the walk
   {
