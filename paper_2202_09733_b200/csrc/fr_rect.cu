@@ -134,6 +134,13 @@ constexpr int FREC = PMGB_RECT_REC12 ? 12 : 8;
 #ifndef PMGB_RECT_RSOA
 #define PMGB_RECT_RSOA 1
 #endif
+// k_rgf: the CTA's What block staged in shared memory and written by one bulk
+// store instead of 12 scattered 8-byte stores per thread.  -1: where it
+// measured faster (p = 4, R / defect forms: config-2 R 102.7 -> 101.3 us; the
+// Jv forms and p = 3 lose 0.5-1.5 %; profiles/r2/ab_wtma_r2y.log), 0 off, 1 on
+#ifndef PMGB_RECT_WTMA
+#define PMGB_RECT_WTMA -1
+#endif
 #ifndef PMGB_RECT_PF   // L2 prefetch distance in CTAs (0: off; 888 and 1776 measured slower, ab_cta_width_r2t.log)
 #define PMGB_RECT_PF 0
 #endif
@@ -1105,7 +1112,9 @@ template <int P, bool HASX> struct GFL {
   static constexpr int A = 2 * BUF, B = HASX ? R::QD : 0;
   static constexpr int STAGE = A > B ? A : B;
   static constexpr int OFF_BAR = R::QD + STAGE;
-  static constexpr size_t BYTES = sizeof(double) * (OFF_BAR + 2);
+  static constexpr bool WTMA = PMGB_RECT_WTMA >= 0 ? PMGB_RECT_WTMA != 0 : (P == 4 && !HASX);
+  static constexpr int OFF_WS = OFF_BAR + 2;   // What block staged for the bulk store (WTMA)
+  static constexpr size_t BYTES = sizeof(double) * (OFF_BAR + 2 + (WTMA ? R::WD : 0));
 };
 
 template <int P, int KIND, bool HASX>
@@ -1234,10 +1243,16 @@ k_rgf(const FrConst C, const RectMesh m, const double* __restrict__ q, const dou
       for (int c = 0; c < 3; ++c) whv[f][c] = common_w(ph, true, true, wq[c], wo[c]);
     }
     if (live) {
-      double* dw = wh + ((e * 4 + f) * N + ((f >= 2) ? N - 1 - a : a)) * 3;
-      stg1_last(dw, whv[f][0]), stg1_last(dw + 1, whv[f][1]), stg1_last(dw + 2, whv[f][2]);
+      if constexpr (L::WTMA) {
+        double* dw = sm + L::OFF_WS + ((el * 4 + f) * N + ((f >= 2) ? N - 1 - a : a)) * 3;
+        dw[0] = whv[f][0], dw[1] = whv[f][1], dw[2] = whv[f][2];
+      } else {
+        double* dw = wh + ((e * 4 + f) * N + ((f >= 2) ? N - 1 - a : a)) * 3;
+        stg1_last(dw, whv[f][0]), stg1_last(dw + 1, whv[f][1]), stg1_last(dw + 2, whv[f][2]);
+      }
     }
   }
+  if constexpr (L::WTMA) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   // rows: primitives, W
   double w[3][N];
   {
@@ -1263,6 +1278,14 @@ k_rgf(const FrConst C, const RectMesh m, const double* __restrict__ q, const dou
   double gx[3][N];
   line_gradient<N>(C, w, whv[1], whv[3], rg.x, gx);
   __syncthreads();
+  if constexpr (L::WTMA) {
+    if (t == 0) {   // the staged What block is complete: one bulk store
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(wh + e0 * 4 * N * 3),
+                   "r"(saddr(sm + L::OFF_WS)), "r"((uint32_t)ne * 4 * N * 24)
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+  }
   // column a: W of the column, gy (faces 2 and 0)
   double gy[3][N];
   {
@@ -1360,6 +1383,9 @@ k_rgf(const FrConst C, const RectMesh m, const double* __restrict__ q, const dou
     visc_fy_uv(uv[0][0], uv[0][1], gxv, tgy0, ph, o);
     o[1] = -o[1], o[2] = -o[2], o[3] = -o[3];
     put(0, o);
+  }
+  if constexpr (L::WTMA) {
+    if (t == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
 }
 
